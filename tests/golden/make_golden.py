@@ -1,0 +1,199 @@
+"""Generate golden vectors from the REFERENCE package itself.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+It imports the reference read-only, evaluates the hot-path functions on
+seeded inputs and writes ``tests/golden/golden.npz``.  The reference does
+not exist on the GPU box, so these committed fixtures are how the oracle
+(``oracle/serq_oracle.py``) is pinned there and here.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+from serq.compensate import (  # noqa: E402
+    Compensator,
+    build_serq_rtn,
+    build_serq_rtn_mx,
+    forward_reconstructed,
+)
+from serq.mxfmt import (  # noqa: E402
+    e2m1_nearest,
+    int_gemm_reference,
+    mx_encode,
+    mx_gemm_reference,
+    save_mx,
+)
+from serq.quantcore import (  # noqa: E402
+    IntQuantConfig,
+    dequantize,
+    gather_columns,
+    per_token_config,
+    quantize_asymmetric,
+    quantize_symmetric,
+)
+from serq.saliency import build_plan, score_rows  # noqa: E402
+from serq.tensorio import SyntheticSpec, gen_synthetic_activations  # noqa: E402
+from serq.flatten import compute_smoothing_scales  # noqa: E402
+from serq.tensorio import collect_calib_stats  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
+
+
+def bf16(x):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+def main():
+    g = {}
+    # -- quantizers: hand cases and random rows across bit widths ------------
+    rng = np.random.default_rng(100)
+    qx = [np.array([[7.0, -7.0, 3.5]]), np.zeros((1, 4)), np.array([[0.0, 15.0]]),
+          np.full((1, 5), 3.0), np.full((1, 5), -3.0)]
+    for i in range(8):
+        qx.append(rng.standard_normal((6, 64)) * 10.0 ** float(rng.integers(-3, 4)))
+    # bf16-valued outlier rows like the benchmark activations
+    spec = SyntheticSpec(rows=64, cols=256, n_outlier_channels=3, outlier_magnitude=50, seed=7)
+    qx.append(bf16(gen_synthetic_activations(spec)))
+    for i, x in enumerate(qx):
+        g[f"q_x_{i}"] = x
+        for bits in (2, 4, 8):
+            s = quantize_symmetric(x, IntQuantConfig(bits, True, "per-row"))
+            a = quantize_asymmetric(x, per_token_config(bits))
+            g[f"q_sym{bits}_codes_{i}"] = s.codes
+            g[f"q_sym{bits}_scales_{i}"] = s.scales
+            g[f"q_asym{bits}_codes_{i}"] = a.codes
+            g[f"q_asym{bits}_scales_{i}"] = a.scales
+            g[f"q_asym{bits}_zps_{i}"] = a.zero_points
+    g["q_count"] = np.array(len(qx))
+
+    # -- E2M1 grid (acceptance 04 grid) --------------------------------------
+    grid = np.linspace(-8.0, 8.0, 100_001)
+    c, v = e2m1_nearest(grid)
+    g["e2m1_grid"] = grid
+    g["e2m1_codes"] = c
+    g["e2m1_vals"] = v
+
+    # -- MX encode: random, zero blocks, tiny/huge magnitudes -----------------
+    mx_inputs = [rng.standard_normal((8, 128)) * 5, np.zeros((2, 64)),
+                 rng.standard_normal((4, 96)) * 1e-30, rng.standard_normal((4, 64)) * 1e30,
+                 bf16(gen_synthetic_activations(spec))]
+    tiny = np.zeros((1, 64))
+    tiny[0, :32] = np.ldexp(1.0, -140) * np.arange(1, 33)  # block amax < 2^-126
+    mx_inputs.append(tiny)
+    for i, x in enumerate(mx_inputs):
+        t = mx_encode(x, 32)
+        g[f"mx_x_{i}"] = x
+        g[f"mx_codes_{i}"] = t.element_codes
+        g[f"mx_exps_{i}"] = t.block_scale_exponents
+    g["mx_count"] = np.array(len(mx_inputs))
+
+    # on-disk MX bytes (mxfmt.py:228-251)
+    import tempfile
+
+    t = mx_encode(mx_inputs[0][:4, :64], 32)
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "t.mx")
+        save_mx(p, t)
+        g["mxfile_bytes"] = np.frombuffer(open(p, "rb").read(), dtype=np.uint8)
+    g["mxfile_src"] = mx_inputs[0][:4, :64]
+
+    # -- int GEMM partials (criterion-03 style) --------------------------------
+    for i in range(6):
+        r2 = np.random.default_rng(200 + i)
+        k = int(r2.choice([64, 128, 256]))
+        gs = int(r2.choice([16, 32, 64]))
+        x = r2.standard_normal((5, k)) * 3
+        w = r2.standard_normal((k, 24))
+        bits = int(r2.choice([4, 8]))
+        xq = quantize_asymmetric(x, per_token_config(bits))
+        wq = quantize_symmetric(w, IntQuantConfig(4, True, gs, "row"))
+        out, parts = int_gemm_reference(xq, wq, return_partials=True)
+        g[f"ig_x_{i}"] = x
+        g[f"ig_w_{i}"] = w
+        g[f"ig_meta_{i}"] = np.array([k, gs, bits])
+        g[f"ig_out_{i}"] = out
+        g[f"ig_parts_{i}"] = np.stack([p[1] for p in parts])
+    # per-output-channel weights (group_size=K): one integer group
+    x = rng.standard_normal((7, 128))
+    w = rng.standard_normal((128, 40)) * 0.02
+    xq = quantize_symmetric(x, IntQuantConfig(4, True, "per-row"))
+    wq = quantize_symmetric(w, IntQuantConfig(4, True, 128, "row"))
+    out, parts = int_gemm_reference(xq, wq, return_partials=True)
+    g["igpc_x"], g["igpc_w"], g["igpc_out"], g["igpc_acc"] = x, w, out, parts[0][1]
+    g["igpc_wcodes"], g["igpc_wscales"] = wq.codes, wq.scales
+
+    # -- MX GEMM ---------------------------------------------------------------
+    xa = mx_encode(rng.standard_normal((6, 128)) * 4, 32)
+    wa = mx_encode(rng.standard_normal((9, 128)), 32)
+    g["mg_xc"], g["mg_xe"] = xa.element_codes, xa.block_scale_exponents
+    g["mg_wc"], g["mg_we"] = wa.element_codes, wa.block_scale_exponents
+    g["mg_out"] = mx_gemm_reference(xa, wa)
+
+    # -- full decomposed forward, MX (reference builder + forward) -------------
+    spec2 = SyntheticSpec(rows=128 + 64, cols=512, n_outlier_channels=5, outlier_magnitude=50, seed=0)
+    pool = gen_synthetic_activations(spec2)
+    calib, x = pool[:128], pool[128:]
+    w = np.random.default_rng(1).standard_normal((512, 384)) * 0.02
+    s = compute_smoothing_scales(collect_calib_stats(calib), w, 0.5).s
+    wt, xt = s[:, None] * w, x / s
+    plan = build_plan(score_rows(wt), 64)
+    wp, xp = wt[plan.permutation], bf16(xt[:, plan.permutation])
+    plan_p = build_plan(score_rows(wp), 64)
+    main_t, comp = build_serq_rtn_mx(wp, plan_p, 32)
+    g["fmx_x"], g["fmx_w"] = xp, wp
+    g["fmx_idx"] = plan_p.salient_idx
+    g["fmx_main_codes"], g["fmx_main_exps"] = main_t.element_codes, main_t.block_scale_exponents
+    g["fmx_r_codes"], g["fmx_r_exps"] = comp.r_q.element_codes, comp.r_q.block_scale_exponents
+    g["fmx_y"] = forward_reconstructed(xp, main_t, comp, None)
+    # gather fallback: same artefacts, arbitrary salient index set
+    idx = np.random.default_rng(3).permutation(512)[:64]
+    comp_g = Compensator("rtn_residual", 64, idx, r_q=comp.r_q)
+    g["fmx_gidx"] = idx
+    g["fmx_y_gather"] = forward_reconstructed(xp, main_t, comp_g, None)
+
+    # -- full decomposed forward, INT (asym A8, per-output-channel W, int R) ---
+    k, n, r = 256, 96, 32
+    xi = bf16(np.random.default_rng(11).standard_normal((9, k)) * 2)
+    wi = np.random.default_rng(12).standard_normal((k, n)) * 0.02
+    main = quantize_symmetric(wi, IntQuantConfig(4, True, k, "row"))
+    resid = wi[:r] - dequantize(main)[:r]
+    rq = quantize_symmetric(resid, IntQuantConfig(4, True, r, "row"))
+    comp_i = Compensator("rtn_residual", r, np.arange(r), r_q=rq)
+    for bits in (4, 8):
+        yv = forward_reconstructed(xi, main, comp_i, per_token_config(bits))
+        xq = quantize_asymmetric(xi, per_token_config(bits))
+        _, mp = int_gemm_reference(xq, main, return_partials=True)
+        _, rp = int_gemm_reference(gather_columns(xq, np.arange(r)), rq, return_partials=True)
+        g[f"fint_y_a{bits}"] = yv
+        g[f"fint_acc_a{bits}"] = mp[0][1]
+        g[f"fint_accr_a{bits}"] = rp[0][1]
+    g["fint_x"], g["fint_w"] = xi, wi
+    # dense-R variant (r_dense, "L in bf16")
+    comp_d = Compensator("rtn_residual", r, np.arange(r), r_dense=bf16(resid))
+    g["fint_y_dense_a8"] = forward_reconstructed(xi, main, comp_d, per_token_config(8))
+    # the per-row default builder path (float branch) for the drop-in rejection test
+    plan_i = build_plan(score_rows(wi), r)
+    m2, c2 = build_serq_rtn(wi, plan_i, IntQuantConfig(4, True, 16, "row"),
+                            IntQuantConfig(4, True, r, "row"))
+    g["fint_g16_y"] = forward_reconstructed(xi, m2, c2, per_token_config(8))
+    g["fint_g16_idx"] = plan_i.salient_idx
+
+    np.savez_compressed(OUT, **g)
+    print(f"wrote {OUT} ({os.path.getsize(OUT)/1e6:.2f} MB, {len(g)} arrays)")
+
+
+if __name__ == "__main__":
+    main()
