@@ -1,0 +1,126 @@
+/* serq_b200.h -- C ABI of the B200-native SERQ quantized-linear hot path.
+ *
+ * Plain pointers, sizes and a CUDA stream; no torch types.  All device
+ * pointers are caller-owned unless stated.  Every entry point returns 0 on
+ * success, SERQ_EINVAL for a violated precondition (the Python mirror raises
+ * ValidationError, as the reference does in _validation.py:14-15) or
+ * SERQ_ECUDA for a CUDA failure; serq_last_error() gives a thread-local
+ * message.  Work is stream-ordered; nothing blocks the host except the
+ * *_host entry points, which synchronise `stream` before returning.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src/serq):
+ *   serq_act_quant_mx      mx_encode + _block_exponents + e2m1_nearest   mxfmt.py:52-108
+ *                          and the salient re-encode in _forward_mx      compensate.py:335
+ *   serq_act_quant_int     quantize_symmetric / quantize_asymmetric      quantcore.py:108-137
+ *                          + gather_columns (salient slice)              quantcore.py:158-175
+ *   serq_pack_mx           MxBlockTensor artefacts (main_t, comp.r_q)     mxfmt.py:34-49, compensate.py:343-357
+ *   serq_unpack_mx         inverse of the device layout (artefact export)
+ *   serq_pack_int          QuantizedTensor artefacts (main, comp.r_q / comp.r_dense)
+ *                                                                         quantcore.py:59-80, compensate.py:48-69
+ *   serq_linear_mx         _forward_mx: mx_gemm_reference(x,W)+mx_gemm_reference(xs,R)
+ *                                                                         compensate.py:319-340, mxfmt.py:198-225
+ *   serq_linear_int        forward_reconstructed int branch: int_gemm_reference(xq, main)
+ *                          + R term (int_gemm_reference(xs, r_q) or dequantize(xs) @ r_dense)
+ *                                                                         compensate.py:300-316, mxfmt.py:135-195
+ *   serq_forward_mx_host   forward_reconstructed(x, main_t, comp, None) end to end from host memory
+ *                                                                         compensate.py:272-295
+ */
+#ifndef SERQ_B200_H
+#define SERQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SERQ_OK 0
+#define SERQ_EINVAL 1
+#define SERQ_ECUDA 2
+
+/* input element types for the quantizers */
+#define SERQ_BF16 0
+#define SERQ_F32 1
+#define SERQ_F64 2
+
+/* compensation-matrix modes for the integer path */
+#define SERQ_R_NONE 0
+#define SERQ_R_DENSE 1 /* comp.r_dense: float64 [r, N], consumed as bf16 */
+#define SERQ_R_INT 2   /* comp.r_q: int codes [r, N] with one scale per output column */
+
+typedef struct serq_linear serq_linear_t; /* packed weight handle (opaque) */
+typedef void* serq_stream_t;              /* cudaStream_t */
+
+const char* serq_last_error(void);
+const char* serq_version(void);
+int serq_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* Bytes of the device MX activation buffers for an [rows, cols] matrix. */
+int serq_mx_sizes(int64_t rows, int64_t cols, int64_t* codes_bytes, int64_t* sf_bytes);
+
+/* K1-MX: X [M, K] (row stride ldx elements) -> packed E2M1 codes [M, K/2] and
+ * tiled E8M0 scale factors.  If gather_idx != NULL, also encodes the salient
+ * slice X[:, gather_idx[0..r)] into xs_codes [M, r/2] / xs_sf (the reference
+ * re-encodes the gathered columns, compensate.py:335).  K % 32 == 0, r % 32 == 0. */
+int serq_act_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, uint8_t* codes, uint8_t* sf,
+                      const int32_t* gather_idx, int r, uint8_t* xs_codes, uint8_t* xs_sf, serq_stream_t stream);
+
+/* K1-INT: per-token quantization (bits in [2, 8]).  codes int8 [M, K] (u8 bit
+ * patterns when asymmetric), scale64/scale32 [M], zp [M] (asymmetric only; may
+ * be NULL when symmetric).  xs_kind: 0 none; 1 write xs_out bf16 [M, r] =
+ * codes[:, idx] - zp (dense-R operand); 2 write xs_out int8 [M, r] = codes[:, idx].
+ * salient_idx == NULL means idx = arange(r). */
+int serq_act_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, int bits, int symmetric,
+                       int8_t* codes, double* scale64, float* scale32, int32_t* zp, const int32_t* salient_idx, int r,
+                       void* xs_out, int xs_kind, serq_stream_t stream);
+
+/* Pack MX artefacts held in DEVICE memory, reference layouts:
+ * codes uint8 [N, K] (values 0..15), exps int32 [N, K/32] (main_t of
+ * build_serq_rtn_mx, stored transposed), r_codes uint8 [N, r], r_exps int32
+ * [N, r/32] (comp.r_q) or NULL with r == 0.  salient_contiguous != 0 when
+ * salient_idx == arange(r) (permuted layout: the salient slice is read from
+ * the leading columns of X, no re-encode). */
+int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K, const uint8_t* r_codes,
+                 const int32_t* r_exps, int r, int salient_contiguous, serq_linear_t** out, serq_stream_t stream);
+
+/* Inverse of the device MX layout for an activation/weight buffer pair. */
+int serq_unpack_mx(const uint8_t* codes_packed, const uint8_t* sf, int64_t rows, int64_t cols, uint8_t* codes,
+                   int32_t* exps, serq_stream_t stream);
+
+/* Pack INT artefacts held in DEVICE memory, reference layouts: codes int32
+ * [K, N] (main.codes), scales float64 [N] (main.scales, one group: group_size
+ * == K, axis 'row').  r_mode SERQ_R_DENSE: r_data = float64 [r, N] (r_dense);
+ * SERQ_R_INT: r_data = int32 [r, N] codes with r_scales float64 [N].
+ * a_bits/a_symmetric describe the activation quantizer the handle expects. */
+int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t N, int w_bits, int r_mode,
+                  const void* r_data, const double* r_scales, int r, int salient_contiguous, serq_linear_t** out,
+                  serq_stream_t stream);
+
+int serq_linear_destroy(serq_linear_t* h);
+int serq_linear_info(const serq_linear_t* h, int64_t* N, int64_t* K, int* r, int* mode, int* r_mode);
+
+/* K2: Y[M, N] (bf16, row stride ldy) = Xq.Wq + Xs,q.R in one kernel.  a_codes /
+ * a_sf from serq_act_quant_mx; xs_codes / xs_sf only for a non-contiguous
+ * salient set (NULL otherwise). */
+int serq_linear_mx(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t* a_sf, int64_t M,
+                   const uint8_t* xs_codes, const uint8_t* xs_sf, void* y, int64_t ldy, serq_stream_t stream);
+
+/* K3: integer path.  a_codes int8 [M, K]; sx [M] f32; zp [M] or NULL (symmetric
+ * activations); xs = the quantizer's xs_out (dense R, or gathered codes for a
+ * non-contiguous int R) or NULL.  acc_dump / accr_dump (int32 [M, N], optional)
+ * receive the exact integer accumulators sum (c - zp) * w. */
+int serq_linear_int(const serq_linear_t* h, const int8_t* a_codes, const float* sx, const int32_t* zp, int64_t M,
+                    const void* xs, void* y, int64_t ldy, int32_t* acc_dump, int32_t* accr_dump, serq_stream_t stream);
+
+/* End to end from HOST memory (pinned for full PCIe rate): copy X (bf16 [M, K])
+ * in, quantize, GEMM, copy Y (bf16 [M, N]) out; synchronises `stream`.
+ * Device scratch lives in the handle and grows on demand. */
+int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* y_host, serq_stream_t stream);
+
+/* Number of kernels the last forward on this thread launched (evidence for bench). */
+int serq_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SERQ_B200_H */

@@ -1,0 +1,472 @@
+// serq_capi.cu -- the extern "C" boundary (include/serq_b200.h): validation,
+// weight handles, tensor maps, launches.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/serq_b200.h"
+#include "serq_gemm.cuh"
+#include "serq_quant.cuh"
+
+using namespace serq;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                           \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) return fail(SERQ_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define LAUNCH_CHECK(what)                                                                        \
+  do {                                                                                            \
+    cudaError_t e_ = cudaGetLastError();                                                          \
+    if (e_ != cudaSuccess) return fail(SERQ_ECUDA, "%s launch: %s", what, cudaGetErrorString(e_)); \
+    ++g_launches;                                                                                 \
+  } while (0)
+
+inline cudaStream_t S(serq_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+// SF chunks (4 x 32-blocks = 128 K) per 128-row block, padded to the 256-K pipeline step
+inline int kc_pad_of(int64_t cols) { return int(cdiv(cols, 256) * 2); }
+inline int64_t sf_bytes_of(int64_t rows, int64_t cols) { return cdiv(rows, 128) * kc_pad_of(cols) * 512; }
+
+// ---------------------------------------------------------------- tensor maps
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 2-D row-major map: `inner` elements per row (contiguous), `rows` rows, row pitch in bytes.
+int make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t rows,
+             uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return fail(SERQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (pitch_bytes & 15))
+    return fail(SERQ_EINVAL, "tensor base and row pitch must be 16-byte aligned (pitch %llu)",
+                (unsigned long long)pitch_bytes);
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {pitch_bytes};
+  cuuint32_t box[2] = {box_inner, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SERQ_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return SERQ_OK;
+}
+
+bool g_attr_set[2] = {false, false};
+template <int kMode>
+int ensure_attr() {
+  if (!g_attr_set[kMode]) {
+    CK(cudaFuncSetAttribute(serq_linear_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    g_attr_set[kMode] = true;
+  }
+  return SERQ_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ handle
+struct serq_linear {
+  int mode = 0;  // kModeMX / kModeI8
+  int64_t N = 0, K = 0;
+  int r = 0, r_mode = SERQ_R_NONE, w_bits = 4, contiguous = 1;
+  void* w = nullptr;        // MX packed [N, K/2] | INT s8 [N, K]
+  uint8_t* sfw = nullptr;   // MX scale factors
+  void* rbuf = nullptr;     // MX packed [N, r/2] | INT s8 [N, r] | bf16 [N, r]
+  uint8_t* sfr = nullptr;
+  float* sw = nullptr;
+  int32_t* colsum = nullptr;
+  float* sr = nullptr;
+  int32_t* colsum_r = nullptr;
+  CUtensorMap map_b, map_r;
+  // end-to-end scratch
+  int64_t ws_m = 0;
+  void* ws_x = nullptr;
+  uint8_t* ws_codes = nullptr;
+  uint8_t* ws_sf = nullptr;
+  void* ws_y = nullptr;
+};
+
+namespace {
+void free_handle(serq_linear* h) {
+  void* ptrs[] = {h->w, h->sfw, h->rbuf, h->sfr, h->sw, h->colsum, h->sr, h->colsum_r,
+                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete h;
+}
+}  // namespace
+
+extern "C" {
+
+const char* serq_last_error(void) { return g_err.c_str(); }
+const char* serq_version(void) { return "serq_b200 0.1 (sm_100a tcgen05)"; }
+int serq_last_launch_count(void) { return g_launches; }
+
+int serq_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  return SERQ_OK;
+}
+
+int serq_mx_sizes(int64_t rows, int64_t cols, int64_t* codes_bytes, int64_t* sf_bytes) {
+  if (rows < 0 || cols < 0 || cols % 32) return fail(SERQ_EINVAL, "MX layout needs cols %% 32 == 0 (got %lld)", (long long)cols);
+  if (codes_bytes) *codes_bytes = rows * cols / 2;
+  if (sf_bytes) *sf_bytes = sf_bytes_of(rows, cols);
+  return SERQ_OK;
+}
+
+int serq_act_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, uint8_t* codes, uint8_t* sf,
+                      const int32_t* gather_idx, int r, uint8_t* xs_codes, uint8_t* xs_sf, serq_stream_t stream) {
+  g_launches = 0;
+  if (M <= 0 || K <= 0) return fail(SERQ_EINVAL, "x must be non-empty (M=%lld, K=%lld)", (long long)M, (long long)K);
+  if (K % 32) return fail(SERQ_EINVAL, "row length %lld not divisible by block_size 32", (long long)K);
+  if (ldx < K) return fail(SERQ_EINVAL, "ldx < K");
+  if (dtype < 0 || dtype > 2) return fail(SERQ_EINVAL, "unknown dtype %d", dtype);
+  if (gather_idx && (r <= 0 || r % 32)) return fail(SERQ_EINVAL, "MX residual path needs rank divisible by block size");
+  if (gather_idx && (!xs_codes || !xs_sf)) return fail(SERQ_EINVAL, "gather needs xs_codes and xs_sf");
+  if (dtype == SERQ_BF16 && ((reinterpret_cast<uintptr_t>(x) & 15) || (ldx % 8)))
+    return fail(SERQ_EINVAL, "bf16 input must be 16-byte aligned with ldx %% 8 == 0");
+  if (dtype == SERQ_F32 && ((reinterpret_cast<uintptr_t>(x) & 15) || (ldx % 4)))
+    return fail(SERQ_EINVAL, "f32 input must be 16-byte aligned with ldx %% 4 == 0");
+  cudaStream_t st = S(stream);
+  const int kc = kc_pad_of(K);
+  // padded SF rows / chunks must read as zero codes' scale (any finite value); zero them
+  if (M % 128 || K % 256) CK(cudaMemsetAsync(sf, 0, sf_bytes_of(M, K), st));
+  const int krc = gather_idx ? kc_pad_of(r) : 0;
+  if (gather_idx && (M % 128 || r % 256)) CK(cudaMemsetAsync(xs_sf, 0, sf_bytes_of(M, r), st));
+  const int64_t nb_main = cdiv(M * (K / 8), 256);
+  const int64_t nb_g = gather_idx ? cdiv(M * (r / 8), 256) : 0;
+  dim3 grid(unsigned(nb_main + nb_g));
+  switch (dtype) {
+    case SERQ_BF16:
+      mx_encode_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), M, K, ldx, codes,
+                                                            sf, kc, gather_idx, r, xs_codes, xs_sf, krc, nb_main);
+      break;
+    case SERQ_F32:
+      mx_encode_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(x), M, K, ldx, codes, sf, kc, gather_idx,
+                                                    r, xs_codes, xs_sf, krc, nb_main);
+      break;
+    default:
+      mx_encode_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(x), M, K, ldx, codes, sf, kc,
+                                                     gather_idx, r, xs_codes, xs_sf, krc, nb_main);
+  }
+  LAUNCH_CHECK("mx_encode");
+  return SERQ_OK;
+}
+
+int serq_act_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, int bits, int symmetric,
+                       int8_t* codes, double* scale64, float* scale32, int32_t* zp, const int32_t* salient_idx, int r,
+                       void* xs_out, int xs_kind, serq_stream_t stream) {
+  g_launches = 0;
+  if (M <= 0 || K <= 0) return fail(SERQ_EINVAL, "x must be non-empty");
+  if (bits < 2 || bits > 8) return fail(SERQ_EINVAL, "bits must be in [2, 8], got %d", bits);
+  if (ldx < K) return fail(SERQ_EINVAL, "ldx < K");
+  if (!symmetric && !zp) return fail(SERQ_EINVAL, "asymmetric quantization needs a zero-point buffer");
+  if (xs_kind && (r <= 0 || r > K || !xs_out)) return fail(SERQ_EINVAL, "salient slice needs 0 < r <= K and xs_out");
+  cudaStream_t st = S(stream);
+  const dim3 grid(static_cast<unsigned>(M));
+  switch (dtype) {
+    case SERQ_BF16:
+      int_quant_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), M, K, ldx, bits,
+                                                            symmetric, codes, scale64, scale32, zp, salient_idx, r,
+                                                            xs_out, xs_kind);
+      break;
+    case SERQ_F32:
+      int_quant_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(x), M, K, ldx, bits, symmetric, codes,
+                                                    scale64, scale32, zp, salient_idx, r, xs_out, xs_kind);
+      break;
+    case SERQ_F64:
+      int_quant_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(x), M, K, ldx, bits, symmetric, codes,
+                                                     scale64, scale32, zp, salient_idx, r, xs_out, xs_kind);
+      break;
+    default:
+      return fail(SERQ_EINVAL, "unknown dtype %d", dtype);
+  }
+  LAUNCH_CHECK("int_quant");
+  return SERQ_OK;
+}
+
+int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K, const uint8_t* r_codes,
+                 const int32_t* r_exps, int r, int salient_contiguous, serq_linear_t** out, serq_stream_t stream) {
+  g_launches = 0;
+  if (!out) return fail(SERQ_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (N <= 0 || K <= 0 || K % 32) return fail(SERQ_EINVAL, "MX weight needs K %% 32 == 0 (N=%lld, K=%lld)", (long long)N, (long long)K);
+  if (N % 8) return fail(SERQ_EINVAL, "output dim N must be a multiple of 8 (bf16 row pitch), got %lld", (long long)N);
+  if (r < 0 || r % 32) return fail(SERQ_EINVAL, "MX residual path needs rank divisible by block size");
+  if (r > 0 && (!r_codes || !r_exps)) return fail(SERQ_EINVAL, "rank > 0 needs r_codes and r_exps");
+  if (r > K) return fail(SERQ_EINVAL, "rank %d exceeds K", r);
+  cudaStream_t st = S(stream);
+  serq_linear* h = new serq_linear();
+  h->mode = kModeMX;
+  h->N = N;
+  h->K = K;
+  h->r = r;
+  h->contiguous = salient_contiguous ? 1 : 0;
+  auto bail = [&](int code) {
+    free_handle(h);
+    return code;
+  };
+  if (cudaMalloc(&h->w, N * K / 2) != cudaSuccess || cudaMalloc(&h->sfw, sf_bytes_of(N, K)) != cudaSuccess)
+    return bail(fail(SERQ_ECUDA, "cudaMalloc failed for MX weights"));
+  if (cudaMemsetAsync(h->sfw, 0, sf_bytes_of(N, K), st) != cudaSuccess) return bail(fail(SERQ_ECUDA, "memset"));
+  pack_mx_kernel<<<unsigned(cdiv(N * K / 8, 256)), 256, 0, st>>>(codes, exps, N, K, static_cast<uint8_t*>(h->w), h->sfw,
+                                                                  kc_pad_of(K));
+  if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_mx launch failed"));
+  int rc = make_map(&h->map_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K / 2, N, K / 2, 128, kBN);
+  if (rc) return bail(rc);
+  if (r > 0) {
+    if (cudaMalloc(&h->rbuf, N * r / 2) != cudaSuccess || cudaMalloc(&h->sfr, sf_bytes_of(N, r)) != cudaSuccess)
+      return bail(fail(SERQ_ECUDA, "cudaMalloc failed for R"));
+    if (cudaMemsetAsync(h->sfr, 0, sf_bytes_of(N, r), st) != cudaSuccess) return bail(fail(SERQ_ECUDA, "memset"));
+    pack_mx_kernel<<<unsigned(cdiv(N * r / 8, 256)), 256, 0, st>>>(r_codes, r_exps, N, r,
+                                                                    static_cast<uint8_t*>(h->rbuf), h->sfr, kc_pad_of(r));
+    if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_mx launch failed"));
+    rc = make_map(&h->map_r, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r / 2, N, r / 2, 128, kBN);
+    if (rc) return bail(rc);
+  }
+  *out = h;
+  return SERQ_OK;
+}
+
+int serq_unpack_mx(const uint8_t* codes_packed, const uint8_t* sf, int64_t rows, int64_t cols, uint8_t* codes,
+                   int32_t* exps, serq_stream_t stream) {
+  g_launches = 0;
+  if (rows <= 0 || cols <= 0 || cols % 32) return fail(SERQ_EINVAL, "MX layout needs cols %% 32 == 0");
+  unpack_mx_kernel<<<unsigned(cdiv(rows * cols / 8, 256)), 256, 0, S(stream)>>>(codes_packed, sf, rows, cols,
+                                                                                kc_pad_of(cols), codes, exps);
+  LAUNCH_CHECK("unpack_mx");
+  return SERQ_OK;
+}
+
+int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t N, int w_bits, int r_mode,
+                  const void* r_data, const double* r_scales, int r, int salient_contiguous, serq_linear_t** out,
+                  serq_stream_t stream) {
+  g_launches = 0;
+  if (!out) return fail(SERQ_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (N <= 0 || K <= 0) return fail(SERQ_EINVAL, "empty weight");
+  if (K % 16) return fail(SERQ_EINVAL, "K must be a multiple of 16 (int8 row pitch), got %lld", (long long)K);
+  if (N % 8) return fail(SERQ_EINVAL, "output dim N must be a multiple of 8, got %lld", (long long)N);
+  if (w_bits < 2 || w_bits > 8) return fail(SERQ_EINVAL, "weight bits must be in [2, 8]");
+  if (r_mode < SERQ_R_NONE || r_mode > SERQ_R_INT) return fail(SERQ_EINVAL, "unknown r_mode %d", r_mode);
+  if (r_mode != SERQ_R_NONE && (r <= 0 || r > K || !r_data)) return fail(SERQ_EINVAL, "R needs 0 < r <= K and data");
+  if (r_mode == SERQ_R_INT && !r_scales) return fail(SERQ_EINVAL, "integer R needs r_scales");
+  if (r_mode == SERQ_R_DENSE && r % 8) return fail(SERQ_EINVAL, "dense R needs r %% 8 == 0 (bf16 row pitch)");
+  if (r_mode == SERQ_R_INT && r % 16) return fail(SERQ_EINVAL, "integer R needs r %% 16 == 0 (int8 row pitch)");
+  cudaStream_t st = S(stream);
+  serq_linear* h = new serq_linear();
+  h->mode = kModeI8;
+  h->N = N;
+  h->K = K;
+  h->w_bits = w_bits;
+  h->r = r_mode == SERQ_R_NONE ? 0 : r;
+  h->r_mode = r_mode;
+  h->contiguous = salient_contiguous ? 1 : 0;
+  auto bail = [&](int code) {
+    free_handle(h);
+    return code;
+  };
+  if (cudaMalloc(&h->w, N * K) != cudaSuccess || cudaMalloc(&h->sw, N * 4) != cudaSuccess ||
+      cudaMalloc(&h->colsum, N * 4) != cudaSuccess)
+    return bail(fail(SERQ_ECUDA, "cudaMalloc failed for INT weights"));
+  transpose_codes_kernel<<<dim3(unsigned(cdiv(N, 32)), unsigned(cdiv(K, 32))), dim3(32, 8), 0, st>>>(
+      codes, K, N, static_cast<int8_t*>(h->w));
+  colsum_kernel<<<unsigned(cdiv(N, 256)), 256, 0, st>>>(codes, K, N, scales, h->colsum, h->sw);
+  if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_int launch failed"));
+  int rc = make_map(&h->map_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, kBN);
+  if (rc) return bail(rc);
+  if (r_mode == SERQ_R_DENSE) {
+    if (cudaMalloc(&h->rbuf, N * r * 2) != cudaSuccess) return bail(fail(SERQ_ECUDA, "cudaMalloc R"));
+    dense_r_kernel<<<unsigned(cdiv(N * r, 256)), 256, 0, st>>>(static_cast<const double*>(r_data), r, N,
+                                                               static_cast<__nv_bfloat16*>(h->rbuf));
+    if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "dense_r launch failed"));
+    rc = make_map(&h->map_r, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h->rbuf, r, N, r * 2, 64, kBN);
+    if (rc) return bail(rc);
+  } else if (r_mode == SERQ_R_INT) {
+    if (cudaMalloc(&h->rbuf, N * r) != cudaSuccess || cudaMalloc(&h->sr, N * 4) != cudaSuccess ||
+        cudaMalloc(&h->colsum_r, N * 4) != cudaSuccess)
+      return bail(fail(SERQ_ECUDA, "cudaMalloc R"));
+    const int32_t* rc32 = static_cast<const int32_t*>(r_data);
+    transpose_codes_kernel<<<dim3(unsigned(cdiv(N, 32)), unsigned(cdiv(r, 32))), dim3(32, 8), 0, st>>>(
+        rc32, r, N, static_cast<int8_t*>(h->rbuf));
+    colsum_kernel<<<unsigned(cdiv(N, 256)), 256, 0, st>>>(rc32, r, N, r_scales, h->colsum_r, h->sr);
+    if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack R launch failed"));
+    rc = make_map(&h->map_r, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r, N, r, 128, kBN);
+    if (rc) return bail(rc);
+  }
+  *out = h;
+  return SERQ_OK;
+}
+
+int serq_linear_destroy(serq_linear_t* h) {
+  if (h) free_handle(h);
+  return SERQ_OK;
+}
+
+int serq_linear_info(const serq_linear_t* h, int64_t* N, int64_t* K, int* r, int* mode, int* r_mode) {
+  if (!h) return fail(SERQ_EINVAL, "NULL handle");
+  if (N) *N = h->N;
+  if (K) *K = h->K;
+  if (r) *r = h->r;
+  if (mode) *mode = h->mode;
+  if (r_mode) *r_mode = h->r_mode;
+  return SERQ_OK;
+}
+
+int serq_linear_mx(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t* a_sf, int64_t M,
+                   const uint8_t* xs_codes, const uint8_t* xs_sf, void* y, int64_t ldy, serq_stream_t stream) {
+  g_launches = 0;
+  if (!h || h->mode != kModeMX) return fail(SERQ_EINVAL, "handle is not an MX linear");
+  if (M <= 0) return fail(SERQ_EINVAL, "x must be non-empty");
+  if (ldy < h->N || ldy % 8) return fail(SERQ_EINVAL, "ldy must be >= N and a multiple of 8");
+  const bool need_xs = h->r > 0 && !h->contiguous;
+  if (need_xs && (!xs_codes || !xs_sf)) return fail(SERQ_EINVAL, "non-contiguous salient set needs the xs slice");
+  int rc = ensure_attr<kModeMX>();
+  if (rc) return rc;
+  CUtensorMap ma, mxs, my;
+  rc = make_map(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, kBM);
+  if (rc) return rc;
+  if (need_xs) {
+    rc = make_map(&mxs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_codes, h->r / 2, M, h->r / 2, 128, kBM);
+    if (rc) return rc;
+  } else {
+    mxs = ma;
+  }
+  rc = make_map(&my, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, h->N, M, ldy * 2, 64, 32);
+  if (rc) return rc;
+  GemmParams p{};
+  p.M = int(M);
+  p.N = int(h->N);
+  p.K = int(h->K);
+  p.r = h->r;
+  p.k_steps = int(cdiv(h->K / 2, kStepBytes));
+  p.r_steps = int(cdiv(h->r / 2, kStepBytes));
+  p.r_mode = h->r > 0 ? 1 : 0;
+  p.sfa = a_sf;
+  p.sfb = h->sfw;
+  p.xs_is_x = need_xs ? 0 : 1;
+  p.sfa_r = need_xs ? xs_sf : a_sf;
+  p.sfb_r = h->sfr;
+  p.kc_pad = kc_pad_of(h->K);
+  p.kc_pad_r = kc_pad_of(h->r > 0 ? h->r : 32);
+  dim3 grid(unsigned(cdiv(M, kBM)), unsigned(cdiv(h->N, kBN)));
+  serq_linear_kernel<kModeMX><<<grid, kThreads, kSmemBytes, S(stream)>>>(ma, h->map_b, mxs, h->r ? h->map_r : h->map_b,
+                                                                         my, p);
+  LAUNCH_CHECK("serq_linear_kernel<mx>");
+  return SERQ_OK;
+}
+
+int serq_linear_int(const serq_linear_t* h, const int8_t* a_codes, const float* sx, const int32_t* zp, int64_t M,
+                    const void* xs, void* y, int64_t ldy, int32_t* acc_dump, int32_t* accr_dump, serq_stream_t stream) {
+  g_launches = 0;
+  if (!h || h->mode != kModeI8) return fail(SERQ_EINVAL, "handle is not an INT linear");
+  if (M <= 0) return fail(SERQ_EINVAL, "x must be non-empty");
+  if (ldy < h->N || ldy % 8) return fail(SERQ_EINVAL, "ldy must be >= N and a multiple of 8");
+  const bool need_xs = h->r_mode == SERQ_R_DENSE || (h->r_mode == SERQ_R_INT && !h->contiguous);
+  if (need_xs && !xs) return fail(SERQ_EINVAL, "this R mode needs the quantizer's xs slice");
+  int rc = ensure_attr<kModeI8>();
+  if (rc) return rc;
+  CUtensorMap ma, mxs, my;
+  rc = make_map(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K, M, h->K, 128, kBM);
+  if (rc) return rc;
+  if (h->r_mode == SERQ_R_DENSE)
+    rc = make_map(&mxs, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xs, h->r, M, h->r * 2, 64, kBM);
+  else if (need_xs)
+    rc = make_map(&mxs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs, h->r, M, h->r, 128, kBM);
+  else
+    mxs = ma;
+  if (rc) return rc;
+  rc = make_map(&my, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, h->N, M, ldy * 2, 64, 32);
+  if (rc) return rc;
+  GemmParams p{};
+  p.M = int(M);
+  p.N = int(h->N);
+  p.K = int(h->K);
+  p.r = h->r;
+  p.k_steps = int(cdiv(h->K, kStepBytes));
+  p.r_mode = h->r_mode;
+  p.r_steps = int(cdiv(h->r_mode == SERQ_R_DENSE ? 2 * h->r : h->r, kStepBytes));
+  p.a_signed = zp ? 0 : 1;
+  p.xs_is_x = need_xs ? 0 : 1;
+  p.sx = sx;
+  p.zp = zp;
+  p.sw = h->sw;
+  p.colsum = h->colsum;
+  p.sr = h->sr;
+  p.colsum_r = h->colsum_r;
+  p.acc_dump = acc_dump;
+  p.accr_dump = accr_dump;
+  dim3 grid(unsigned(cdiv(M, kBM)), unsigned(cdiv(h->N, kBN)));
+  serq_linear_kernel<kModeI8><<<grid, kThreads, kSmemBytes, S(stream)>>>(ma, h->map_b, mxs, h->r ? h->map_r : h->map_b,
+                                                                         my, p);
+  LAUNCH_CHECK("serq_linear_kernel<i8>");
+  return SERQ_OK;
+}
+
+int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* y_host, serq_stream_t stream) {
+  if (!h || h->mode != kModeMX) return fail(SERQ_EINVAL, "handle is not an MX linear");
+  if (h->r > 0 && !h->contiguous)
+    return fail(SERQ_EINVAL, "serq_forward_mx_host supports the permuted (contiguous) salient layout only");
+  if (M <= 0) return fail(SERQ_EINVAL, "x must be non-empty");
+  cudaStream_t st = S(stream);
+  if (M > h->ws_m) {
+    for (void* p : {h->ws_x, (void*)h->ws_codes, (void*)h->ws_sf, h->ws_y})
+      if (p) cudaFree(p);
+    h->ws_x = h->ws_y = nullptr;
+    h->ws_codes = h->ws_sf = nullptr;
+    const int64_t mm = cdiv(M, 128) * 128;
+    CK(cudaMalloc(&h->ws_x, mm * h->K * 2));
+    CK(cudaMalloc(&h->ws_codes, mm * h->K / 2));
+    CK(cudaMalloc(&h->ws_sf, sf_bytes_of(mm, h->K)));
+    CK(cudaMalloc(&h->ws_y, mm * h->N * 2));
+    h->ws_m = mm;
+  }
+  CK(cudaMemcpyAsync(h->ws_x, x_host, M * h->K * 2, cudaMemcpyHostToDevice, st));
+  int rc = serq_act_quant_mx(h->ws_x, SERQ_BF16, M, h->K, h->K, h->ws_codes, h->ws_sf, nullptr, 0, nullptr, nullptr,
+                             stream);
+  if (rc) return rc;
+  const int n1 = g_launches;
+  rc = serq_linear_mx(h, h->ws_codes, h->ws_sf, M, nullptr, nullptr, h->ws_y, h->N, stream);
+  if (rc) return rc;
+  g_launches += n1;
+  CK(cudaMemcpyAsync(y_host, h->ws_y, M * h->N * 2, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return SERQ_OK;
+}
+
+}  // extern "C"

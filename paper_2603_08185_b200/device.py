@@ -1,0 +1,287 @@
+"""Device-resident SERQ operators on torch tensors (torch = memory + streams).
+
+Every operator here is a thin call through the C-ABI (``_lib``) on the
+current torch CUDA stream; there is no PyTorch or CPU compute fallback.
+
+Layouts:
+  MX activation  codes uint8 [M, K/2] + tiled E8M0 scale factors
+  INT activation codes int8 [M, K] + per-token scales f32/f64 + zero points
+  MX weight      packed [N, K/2] (+ R [N, r/2]) owned by an ``MxLinear`` handle
+  INT weight     int8 [N, K] + f32 scales + column sums (+ R) in an ``IntLinear``
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ValidationError
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dtype_id(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return _lib.SERQ_BF16
+    if t.dtype == torch.float32:
+        return _lib.SERQ_F32
+    if t.dtype == torch.float64:
+        return _lib.SERQ_F64
+    raise ValidationError(f"unsupported activation dtype {t.dtype}")
+
+
+def _require_cuda(t: torch.Tensor, name: str) -> None:
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise ValidationError(f"{name} must be a CUDA tensor")
+
+
+def mx_sizes(rows: int, cols: int) -> tuple[int, int]:
+    cb, sb = ctypes.c_int64(), ctypes.c_int64()
+    _lib.call("serq_mx_sizes", rows, cols, ctypes.byref(cb), ctypes.byref(sb))
+    return cb.value, sb.value
+
+
+# ---------------------------------------------------------------- activations
+
+
+@dataclass
+class MxActivation:
+    """Device MXFP4 activation: packed E2M1 codes + tiled E8M0 scales."""
+
+    codes: torch.Tensor
+    sf: torch.Tensor
+    M: int
+    K: int
+    xs_codes: torch.Tensor | None = None
+    xs_sf: torch.Tensor | None = None
+
+
+@dataclass
+class IntActivation:
+    """Device per-token integer activation (codes int8, u8 bit patterns if asymmetric)."""
+
+    codes: torch.Tensor
+    scale64: torch.Tensor
+    scale32: torch.Tensor
+    zp: torch.Tensor | None
+    bits: int
+    symmetric: bool
+    xs: torch.Tensor | None = None
+
+
+def quantize_mx(x: torch.Tensor, gather_idx: torch.Tensor | None = None, out: MxActivation | None = None) -> MxActivation:
+    """K1-MX.  x: [M, K] bf16/f32/f64 on the GPU.  ``gather_idx`` (int32, length
+    r) additionally encodes the salient slice x[:, idx] (compensate.py:335)."""
+    _require_cuda(x, "x")
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ValidationError("x must be a row-major 2-D tensor")
+    M, K = x.shape
+    if K % 32:
+        raise ValidationError(f"row length {K} not divisible by block_size 32")
+    r = 0 if gather_idx is None else int(gather_idx.numel())
+    if out is None:
+        cb, sb = mx_sizes(M, K)
+        out = MxActivation(torch.empty(cb, dtype=torch.uint8, device=x.device),
+                           torch.empty(sb, dtype=torch.uint8, device=x.device), M, K)
+        if r:
+            cbr, sbr = mx_sizes(M, r)
+            out.xs_codes = torch.empty(cbr, dtype=torch.uint8, device=x.device)
+            out.xs_sf = torch.empty(sbr, dtype=torch.uint8, device=x.device)
+    _lib.call("serq_act_quant_mx", x.data_ptr(), _dtype_id(x), M, K, x.stride(0), out.codes.data_ptr(),
+              out.sf.data_ptr(), _ptr(gather_idx), r, _ptr(out.xs_codes), _ptr(out.xs_sf), _stream())
+    return out
+
+
+def unpack_mx(codes: torch.Tensor, sf: torch.Tensor, rows: int, cols: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """Device layout -> reference artefact layout (uint8 codes [rows, cols], int32 exps [rows, cols/32])."""
+    c = torch.empty((rows, cols), dtype=torch.uint8, device=codes.device)
+    e = torch.empty((rows, cols // 32), dtype=torch.int32, device=codes.device)
+    _lib.call("serq_unpack_mx", codes.data_ptr(), sf.data_ptr(), rows, cols, c.data_ptr(), e.data_ptr(), _stream())
+    return c, e
+
+
+def quantize_int(x: torch.Tensor, bits: int, symmetric: bool, salient_idx: torch.Tensor | None = None, r: int = 0,
+                 xs_kind: int = 0) -> IntActivation:
+    """K1-INT per-token quantizer (quantcore.py:108-137), bit-exact codes/scales/zps.
+
+    xs_kind 1: also emit the bf16 (codes - zp) salient slice for a dense R;
+    xs_kind 2: emit the gathered int8 salient codes for a non-contiguous int R."""
+    _require_cuda(x, "x")
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ValidationError("x must be a row-major 2-D tensor")
+    M, K = x.shape
+    dev = x.device
+    codes = torch.empty((M, K), dtype=torch.int8, device=dev)
+    s64 = torch.empty(M, dtype=torch.float64, device=dev)
+    s32 = torch.empty(M, dtype=torch.float32, device=dev)
+    zp = None if symmetric else torch.empty(M, dtype=torch.int32, device=dev)
+    xs = None
+    if xs_kind == 1:
+        xs = torch.empty((M, r), dtype=torch.bfloat16, device=dev)
+    elif xs_kind == 2:
+        xs = torch.empty((M, r), dtype=torch.int8, device=dev)
+    _lib.call("serq_act_quant_int", x.data_ptr(), _dtype_id(x), M, K, x.stride(0), bits, int(symmetric),
+              codes.data_ptr(), s64.data_ptr(), s32.data_ptr(), _ptr(zp), _ptr(salient_idx), r, _ptr(xs),
+              xs_kind, _stream())
+    return IntActivation(codes, s64, s32, zp, bits, symmetric, xs)
+
+
+# ---------------------------------------------------------------- weights
+
+
+def _dev(a, dtype, device) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dtype).contiguous()
+
+
+class _Handle:
+    def __init__(self, h: ctypes.c_void_p):
+        self._h = h
+
+    @property
+    def ptr(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            _lib.load().serq_linear_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class MxLinear:
+    """Packed MXFP4 SERQ linear (main_t + comp.r_q of build_serq_rtn_mx,
+    compensate.py:343-357) resident on one GPU."""
+
+    def __init__(self, codes, exps, r_codes=None, r_exps=None, salient_idx=None, device="cuda"):
+        device = torch.device(device)
+        codes = _dev(codes, torch.uint8, device)
+        exps = _dev(exps, torch.int32, device)
+        self.N, self.K = codes.shape
+        self.r = 0 if r_codes is None else int(r_codes.shape[1])
+        if self.r:
+            rc = _dev(r_codes, torch.uint8, device)
+            re = _dev(r_exps, torch.int32, device)
+        else:
+            rc = re = None
+        idx = None if salient_idx is None else np.asarray(salient_idx, dtype=np.int64)
+        self.contiguous = idx is None or np.array_equal(idx, np.arange(self.r))
+        self.gather_idx = None if self.contiguous else torch.from_numpy(idx.astype(np.int32)).to(device)
+        h = ctypes.c_void_p()
+        _lib.call("serq_pack_mx", codes.data_ptr(), exps.data_ptr(), self.N, self.K, _ptr(rc), _ptr(re), self.r,
+                  int(self.contiguous), ctypes.byref(h), _stream())
+        torch.cuda.current_stream().synchronize()  # inputs may be temporaries
+        self._h = _Handle(h)
+        self.device = device
+
+    def quantize(self, x: torch.Tensor, out: MxActivation | None = None) -> MxActivation:
+        return quantize_mx(x, None if self.contiguous else self.gather_idx, out)
+
+    def gemm(self, act: MxActivation, y: torch.Tensor | None = None) -> torch.Tensor:
+        if act.K != self.K:
+            raise ValidationError("x columns must equal weight input dim")
+        if y is None:
+            y = torch.empty((act.M, self.N), dtype=torch.bfloat16, device=self.device)
+        _lib.call("serq_linear_mx", self._h.ptr, act.codes.data_ptr(), act.sf.data_ptr(), act.M, _ptr(act.xs_codes),
+                  _ptr(act.xs_sf), y.data_ptr(), y.stride(0), _stream())
+        return y
+
+    def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
+        return self.gemm(self.quantize(x), y)
+
+    def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor) -> None:
+        """End to end from (pinned) host bf16 memory through the C-ABI."""
+        if x_host.is_cuda or y_host.is_cuda:
+            raise ValidationError("forward_host takes host tensors")
+        _lib.call("serq_forward_mx_host", self._h.ptr, x_host.data_ptr(), x_host.shape[0], y_host.data_ptr(),
+                  _stream())
+
+
+class IntLinear:
+    """Packed integer SERQ linear: per-output-channel INT weights
+    (QuantizedTensor with group_size == K, quantcore.py:59-80) plus the
+    compensator R as bf16 (r_dense) or integer codes with one scale per
+    output column (r_q, row groups of size r)."""
+
+    def __init__(self, codes, scales, bits=4, r_dense=None, r_codes=None, r_scales=None, salient_idx=None,
+                 device="cuda"):
+        device = torch.device(device)
+        codes = _dev(codes, torch.int32, device)
+        self.K, self.N = codes.shape
+        scales = _dev(np.asarray(scales, dtype=np.float64).reshape(-1) if not isinstance(scales, torch.Tensor)
+                      else scales.reshape(-1), torch.float64, device)
+        if scales.numel() != self.N:
+            raise ValidationError("integer main path needs one scale per output column (group_size == K)")
+        if r_dense is not None:
+            self.r_mode = _lib.SERQ_R_DENSE
+            rd = _dev(r_dense, torch.float64, device)
+            self.r = rd.shape[0]
+            rdata, rs = rd, None
+        elif r_codes is not None:
+            self.r_mode = _lib.SERQ_R_INT
+            rdata = _dev(r_codes, torch.int32, device)
+            self.r = rdata.shape[0]
+            rs = _dev(np.asarray(r_scales, dtype=np.float64).reshape(-1) if not isinstance(r_scales, torch.Tensor)
+                      else r_scales.reshape(-1), torch.float64, device)
+            if rs.numel() != self.N:
+                raise ValidationError("integer R needs one scale per output column (row groups of size r)")
+        else:
+            self.r_mode, self.r, rdata, rs = _lib.SERQ_R_NONE, 0, None, None
+        idx = None if salient_idx is None else np.asarray(salient_idx, dtype=np.int64)
+        self.contiguous = idx is None or np.array_equal(idx, np.arange(self.r))
+        self.salient_idx = None if idx is None or self.contiguous else torch.from_numpy(idx.astype(np.int32)).to(device)
+        h = ctypes.c_void_p()
+        _lib.call("serq_pack_int", codes.data_ptr(), scales.data_ptr(), self.K, self.N, bits, self.r_mode,
+                  _ptr(rdata), _ptr(rs), self.r, int(self.contiguous), ctypes.byref(h), _stream())
+        torch.cuda.current_stream().synchronize()
+        self._h = _Handle(h)
+        self.device = device
+
+    def xs_kind(self) -> int:
+        if self.r_mode == _lib.SERQ_R_DENSE:
+            return 1
+        if self.r_mode == _lib.SERQ_R_INT and not self.contiguous:
+            return 2
+        return 0
+
+    def quantize(self, x: torch.Tensor, bits: int, symmetric: bool) -> IntActivation:
+        return quantize_int(x, bits, symmetric, self.salient_idx, self.r, self.xs_kind())
+
+    def gemm(self, act: IntActivation, y=None, acc_dump=None, accr_dump=None) -> torch.Tensor:
+        M, K = act.codes.shape
+        if K != self.K:
+            raise ValidationError("x columns must equal main rows")
+        if y is None:
+            y = torch.empty((M, self.N), dtype=torch.bfloat16, device=self.device)
+        _lib.call("serq_linear_int", self._h.ptr, act.codes.data_ptr(), act.scale32.data_ptr(), _ptr(act.zp), M,
+                  _ptr(act.xs), y.data_ptr(), y.stride(0), _ptr(acc_dump), _ptr(accr_dump), _stream())
+        return y
+
+    def __call__(self, x: torch.Tensor, bits: int, symmetric: bool, y=None) -> torch.Tensor:
+        return self.gemm(self.quantize(x, bits, symmetric), y)
+
+
+def device_info() -> dict:
+    sm, ma, mi = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _lib.call("serq_device_info", ctypes.byref(sm), ctypes.byref(ma), ctypes.byref(mi))
+    return {"sm_count": sm.value, "cc": (ma.value, mi.value)}
+
+
+def last_launch_count() -> int:
+    return int(_lib.load().serq_last_launch_count())

@@ -1,0 +1,225 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) vs the oracle.
+
+Integer outputs (codes, scales, zero points, E8M0 exponents, integer
+accumulators) must be bit-exact.  bf16 outputs are compared with
+bf16_rne(Y_oracle) at tolerance max 1e-2 / mean 1e-3
+(BASELINE.json north_star), written here as TOL_MAX / TOL_MEAN.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import serq_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL_MAX, TOL_MEAN = 1e-2, 1e-3
+
+
+@pytest.fixture(scope="module")
+def D():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2603_08185_b200 import device
+
+    return device
+
+
+def _bf16_outlier_x(M, K, seed=0, n_out=None, mag=50.0):
+    n_out = max(1, K // 100) if n_out is None else n_out
+    return O.bf16_round(O.synthetic_activations(M, K, n_out, mag, seed))
+
+
+def _cuda(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)
+
+
+def _check_mx_encode(D, x, dtype):
+    M, K = x.shape
+    act = D.quantize_mx(_cuda(x, dtype))
+    c, e = D.unpack_mx(act.codes, act.sf, M, K)
+    ref = O.mx_encode(x, 32)
+    assert np.array_equal(e.cpu().numpy(), ref.block_scale_exponents)
+    assert np.array_equal(c.cpu().numpy(), ref.element_codes)
+
+
+# ---------------------------------------------------------------- K1-MX
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32", "f64"])
+def test_mx_encode_bitexact_outliers(D, dtype):
+    x = _bf16_outlier_x(300, 1024, seed=1)
+    if dtype == "f64":
+        x = x + np.random.default_rng(2).standard_normal(x.shape) * 1e-9  # not bf16-representable
+    tdt = {"bf16": torch.bfloat16, "f32": torch.float32, "f64": torch.float64}[dtype]
+    _check_mx_encode(D, x, tdt)
+
+
+def test_mx_encode_golden(D, golden):
+    for i in range(int(golden["mx_count"])):
+        x = golden[f"mx_x_{i}"]
+        act = D.quantize_mx(_cuda(x, torch.float64))
+        c, e = D.unpack_mx(act.codes, act.sf, *x.shape)
+        assert np.array_equal(c.cpu().numpy(), golden[f"mx_codes_{i}"]), i
+        assert np.array_equal(e.cpu().numpy(), golden[f"mx_exps_{i}"]), i
+
+
+def test_mx_encode_every_bf16_value(D):
+    # all 65536 bf16 bit patterns (minus NaN/Inf), shuffled into 32-blocks
+    bits = np.arange(65536, dtype=np.uint32)
+    vals = (bits << 16).view(np.float32).astype(np.float64)
+    vals = vals[np.isfinite(vals)]
+    rng = np.random.default_rng(3)
+    for perm in range(3):
+        v = vals[rng.permutation(vals.size)] if perm else vals.copy()
+        v = v[: (v.size // 256) * 256].reshape(-1, 256)
+        _check_mx_encode(D, v, torch.bfloat16)
+
+
+def test_mx_encode_acceptance_grid(D):
+    # acceptance criterion 04 grid (test_acceptance.py:158-179) in blocks with max 6 -> e = 0
+    grid = np.linspace(-8.0, 8.0, 100_001)[:99_968].reshape(-1, 32).copy()
+    grid[:, 0] = 6.0  # pin the block exponent to 0 so codes are the plain E2M1 rounding
+    _check_mx_encode(D, grid, torch.float64)
+    _check_mx_encode(D, grid.astype(np.float32).astype(np.float64), torch.float32)
+
+
+# ---------------------------------------------------------------- K1-INT
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("symmetric", [True, False])
+@pytest.mark.parametrize("dtype", ["bf16", "f64"])
+def test_int_quant_bitexact(D, bits, symmetric, dtype):
+    x = _bf16_outlier_x(257, 1024, seed=bits)
+    if dtype == "f64":
+        x = x * 1.000000123
+    xt = _cuda(x, torch.bfloat16 if dtype == "bf16" else torch.float64)
+    act = D.quantize_int(xt, bits, symmetric)
+    cfg = O.IntCfg(bits, symmetric, "per-row")
+    ref = O.quantize_symmetric(x, cfg) if symmetric else O.quantize_asymmetric(x, cfg)
+    codes = act.codes.cpu().numpy()
+    codes = codes.astype(np.int32) if symmetric else codes.view(np.uint8).astype(np.int32)
+    assert np.array_equal(act.scale64.cpu().numpy(), ref.scales[:, 0])
+    if not symmetric:
+        assert np.array_equal(act.zp.cpu().numpy(), ref.zero_points[:, 0])
+    assert np.array_equal(codes, ref.codes)
+
+
+def test_int_quant_golden(D, golden):
+    for i in range(int(golden["q_count"])):
+        x = golden[f"q_x_{i}"]
+        if x.shape[1] % 16:
+            continue
+        for bits in (2, 4, 8):
+            s = D.quantize_int(_cuda(x, torch.float64), bits, True)
+            a = D.quantize_int(_cuda(x, torch.float64), bits, False)
+            assert np.array_equal(s.codes.cpu().numpy().astype(np.int32), golden[f"q_sym{bits}_codes_{i}"])
+            assert np.array_equal(s.scale64.cpu().numpy(), golden[f"q_sym{bits}_scales_{i}"][:, 0])
+            assert np.array_equal(a.codes.cpu().numpy().view(np.uint8).astype(np.int32),
+                                  golden[f"q_asym{bits}_codes_{i}"])
+            assert np.array_equal(a.zp.cpu().numpy(), golden[f"q_asym{bits}_zps_{i}"][:, 0])
+
+
+# ---------------------------------------------------------------- K2 MX linear
+
+
+def _mx_case(M, K, N, r, seed=0):
+    x = _bf16_outlier_x(M, K, seed=seed)
+    w = np.random.default_rng(seed + 1).standard_normal((K, N)) * 0.02
+    w[:r] *= 8  # salient rows carry more error
+    main_t, comp = O.build_serq_rtn_mx(w, np.arange(r), 32)
+    return x, main_t, comp
+
+
+@pytest.mark.parametrize("M,K,N,r", [(256, 1024, 512, 64), (100, 512, 384, 32), (128, 256, 256, 0),
+                                     (384, 2048, 768, 128), (17, 4096, 256, 256)])
+def test_mx_linear_parity(D, M, K, N, r):
+    x, main_t, comp = _mx_case(M, K, N, r, seed=M)
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents,
+                     comp.r_q.element_codes if r else None, comp.r_q.block_scale_exponents if r else None,
+                     np.arange(r) if r else None)
+    y = lin(_cuda(x, torch.bfloat16)).float().cpu().numpy()
+    mx, mean = O.parity_errors(y, O.forward_mx(x, main_t, comp))
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+def test_mx_linear_golden_and_gather(D, golden):
+    x = golden["fmx_x"]
+    lin = D.MxLinear(golden["fmx_main_codes"], golden["fmx_main_exps"], golden["fmx_r_codes"],
+                     golden["fmx_r_exps"], golden["fmx_idx"])
+    y = lin(_cuda(x, torch.bfloat16)).float().cpu().numpy()
+    mx, mean = O.parity_errors(y, golden["fmx_y"])
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+    lin_g = D.MxLinear(golden["fmx_main_codes"], golden["fmx_main_exps"], golden["fmx_r_codes"],
+                       golden["fmx_r_exps"], golden["fmx_gidx"])
+    assert not lin_g.contiguous
+    y = lin_g(_cuda(x, torch.bfloat16)).float().cpu().numpy()
+    mx, mean = O.parity_errors(y, golden["fmx_y_gather"])
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+# ---------------------------------------------------------------- K3 INT linear
+
+
+@pytest.mark.parametrize("bits,symmetric,r_mode", [(4, True, "dense"), (8, False, "int"), (4, False, "int"),
+                                                   (8, False, "dense"), (4, True, "none")])
+def test_int_linear_parity(D, bits, symmetric, r_mode):
+    M, K, N, r = 200, 1024, 512, 64
+    x = _bf16_outlier_x(M, K, seed=bits + 10)
+    w = np.random.default_rng(5).standard_normal((K, N)) * 0.02
+    main, comp = O.build_per_channel_int(w, np.arange(r), r_mode="dense" if r_mode == "none" else r_mode)
+    if r_mode == "none":
+        comp = None
+    kw = {}
+    if r_mode == "dense":
+        kw = dict(r_dense=comp.r_dense, salient_idx=np.arange(r))
+    elif r_mode == "int":
+        kw = dict(r_codes=comp.r_q.codes, r_scales=comp.r_q.scales, salient_idx=np.arange(r))
+    lin = D.IntLinear(main.codes, main.scales, 4, **kw)
+    xt = _cuda(x, torch.bfloat16)
+    act = lin.quantize(xt, bits, symmetric)
+    acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    accr = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    y = lin.gemm(act, acc_dump=acc, accr_dump=accr).float().cpu().numpy()
+    cfg = O.IntCfg(bits, symmetric, "per-row")
+    y_ref, xq = O.forward_int(x, main, comp, cfg, symmetric_act=symmetric)
+    _, parts = O.int_gemm(xq, main, return_partials=True)
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), parts[0][1])
+    if r_mode == "int":
+        _, rp = O.int_gemm(O.gather_columns(xq, np.arange(r)), comp.r_q, return_partials=True)
+        assert np.array_equal(accr.cpu().numpy().astype(np.int64), rp[0][1])
+    mx, mean = O.parity_errors(y, y_ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+def test_int_linear_golden(D, golden):
+    x, w = golden["fint_x"], golden["fint_w"]
+    main, comp = O.build_per_channel_int(w, np.arange(32), r_mode="int")
+    lin = D.IntLinear(main.codes, main.scales, 4, r_codes=comp.r_q.codes, r_scales=comp.r_q.scales,
+                      salient_idx=np.arange(32))
+    for bits in (4, 8):
+        act = lin.quantize(_cuda(x, torch.bfloat16), bits, False)
+        acc = torch.zeros((x.shape[0], w.shape[1]), dtype=torch.int32, device="cuda")
+        accr = torch.zeros_like(acc)
+        y = lin.gemm(act, acc_dump=acc, accr_dump=accr).float().cpu().numpy()
+        assert np.array_equal(acc.cpu().numpy(), golden[f"fint_acc_a{bits}"])
+        assert np.array_equal(accr.cpu().numpy(), golden[f"fint_accr_a{bits}"])
+        mx, mean = O.parity_errors(y, golden[f"fint_y_a{bits}"])
+        assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+def test_int_linear_gather_int_r(D):
+    M, K, N, r = 64, 512, 256, 32
+    x = _bf16_outlier_x(M, K, seed=21)
+    w = np.random.default_rng(22).standard_normal((K, N)) * 0.02
+    idx = np.random.default_rng(23).permutation(K)[:r]
+    main, comp = O.build_per_channel_int(w, idx, r_mode="int")
+    lin = D.IntLinear(main.codes, main.scales, 4, r_codes=comp.r_q.codes, r_scales=comp.r_q.scales, salient_idx=idx)
+    assert not lin.contiguous
+    act = lin.quantize(_cuda(x, torch.bfloat16), 8, False)
+    y = lin.gemm(act).float().cpu().numpy()
+    y_ref, _ = O.forward_int(x, main, comp, O.IntCfg(8, False, "per-row"))
+    mx, mean = O.parity_errors(y, y_ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
