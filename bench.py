@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the SERQ W4A4 linear hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl serq|reference]
+
+Workload (N=1): BASELINE config 2 -- SERQ MXFP4 linear, X bf16 [M=4096,
+K=4096] (N(0,1), 1% of channels x50, seed 0, SAF-flattened and salient-
+permuted), W [N=4096, K=4096] ~ N(0, 0.02) (seed 1), rank r=64, bf16 output.
+One step = quantize X (K1-MX) + the fused SERQ linear (K2: main GEMM + the
+salient term + epilogue) on device-resident bf16 X.  An L2 flush (256 MiB
+write, > 126 MB L2) separates timed steps and is excluded from them.
+
+Multi-GPU (torchrun, one process per GPU): every rank runs the same linear
+on its own token batch (tokens are independent, no data-path collective),
+scaling "weak"; timing is the max over ranks.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port of serq.compensate._forward_mx, compensate.py:319-340) on the
+host cores over a bounded row sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+M, K, N, R = 4096, 4096, 4096, 64
+FP4_PEAK_TFLOPS = 9000.0  # nominal dense FP4 (B200_PROFILING.md table) -- no measured FP4 peak exists
+METRIC = "SERQ W4A4 linear TFLOPS (% of FP4/INT8 tensor peak) & tokens/s at 1/2/4/8 GPUs"
+WORKLOAD = "c2: SERQ MXFP4 linear M=4096 K=4096 N=4096 r=64 (quantize + fused GEMM/R/epilogue)"
+CPU_SAMPLE_ROWS = 256
+
+
+def flops_per_token() -> float:
+    return 2.0 * N * (K + R)  # main + salient term
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in open(self.path):
+                p = [c.strip() for c in line.split(",")]
+                if len(p) >= 9 and p[1].replace(".", "").isdigit():
+                    rows.append(p)
+        except OSError:
+            pass
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline_leg(x_bf16: np.ndarray, w: np.ndarray, rows: int = CPU_SAMPLE_ROWS, reps: int = 1) -> dict:
+    """The reference algorithm on host cores: oracle port of _forward_mx
+    (compensate.py:319-340) over a bounded row sample (output rows are
+    independent, so the sample is exact work per token)."""
+    from oracle import serq_oracle as O
+
+    main_t, comp = O.build_serq_rtn_mx(w, np.arange(R), 32)  # offline, untimed
+    xs = x_bf16[:rows]
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.forward_mx(xs, main_t, comp)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": rows * flops_per_token() / t / 1e12, "unit": "TFLOPS", "cores": os.cpu_count(),
+            "kind": "port", "seconds": t,
+            "sample": f"{rows} of {M} token rows of config c2 through oracle.forward_mx "
+                      f"(NumPy/OpenBLAS, {os.cpu_count()} threads), per-call W decode included as in the reference"}
+
+
+def run_reference(args) -> None:
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2603_08185_b200 import workload as WL
+
+    wl = WL.make_linear(K, N, M, R, 0.01, 50.0, "mx")
+    from oracle import serq_oracle as O
+
+    main_t, comp = O.build_serq_rtn_mx(wl.w, np.arange(R), 32)
+    rows = CPU_SAMPLE_ROWS
+    for _ in range(args.warmup):
+        O.forward_mx(wl.x[:rows], main_t, comp)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        lo = (i * rows) % M
+        O.forward_mx(wl.x[lo:lo + rows], main_t, comp)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = rows * flops_per_token() / dt / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOPS", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD + f" -- CPU sample {rows} token rows per step", "M": M, "K": K, "N": N,
+                   "r": R, "format": "mxfp4"},
+        "tokens_per_s": rows / dt,
+        "cpu_baseline": {"value": val, "unit": "TFLOPS", "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{rows} token rows per step (oracle port of _forward_mx, NumPy/OpenBLAS)"},
+        "e2e": {"value": val, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_serq(args) -> None:
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2603_08185_b200 import api
+    from paper_2603_08185_b200 import device as D
+    from paper_2603_08185_b200 import workload as WL
+
+    wl = WL.make_linear(K, N, M, R, 0.01, 50.0, "mx", x_seed=rank)
+    main_t, comp = api.build_serq_rtn_mx(wl.w, np.arange(R))
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                     comp.r_q.block_scale_exponents, np.arange(R))
+    x = torch.from_numpy(wl.x).to("cuda", torch.bfloat16)
+    act = lin.quantize(x)
+    y = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    # One step = quantize + fused linear, captured once as a CUDA graph (no host
+    # launch overhead inside the timed region); quantize-only / linear-only graphs
+    # give the per-kernel breakdown the roofline uses.
+    side = torch.cuda.Stream()
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        lin.quantize(x, act)
+        lin.gemm(act, y)
+        torch.cuda.synchronize()
+        g_step, g_q, g_l = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_step, stream=side):
+            lin.quantize(x, act)
+            n_q = D.last_launch_count()
+            lin.gemm(act, y)
+            launches_per_step = n_q + D.last_launch_count()
+        with torch.cuda.graph(g_q, stream=side):
+            lin.quantize(x, act)
+        with torch.cuda.graph(g_l, stream=side):
+            lin.gemm(act, y)
+    torch.cuda.synchronize()
+
+    def flush():
+        fa.zero_()
+        fb.sum()
+
+    fa = torch.empty(64 << 20, dtype=torch.float32, device="cuda")  # 256 MiB write ...
+    fb = torch.ones(64 << 20, dtype=torch.float32, device="cuda")   # ... then 256 MiB read (clean lines)
+    for _ in range(max(args.warmup, 3)):
+        flush()
+        g_step.replay()
+    torch.cuda.synchronize()
+
+    def timed(graph, n):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for a, b in evs:
+            flush()
+            a.record(stream)
+            graph.replay()
+            b.record(stream)
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in evs]
+
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_step = timed(g_step, args.steps)
+    if ws > 1:
+        torch.distributed.barrier()
+    launches = launches_per_step * args.steps
+    t_q = timed(g_q, max(args.steps, 10))
+    t_g = timed(g_l, max(args.steps, 10))
+    total_ms = sum(t_step)
+    if ws > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = ws * M * flops_per_token() * args.steps / (total_ms / 1e3) / 1e12
+    clocks = clk.summary()
+
+    # ---- end to end through the C-ABI from pinned host memory
+    xh = x.cpu().pin_memory()
+    yh = torch.empty((M, N), dtype=torch.bfloat16).pin_memory()
+    for _ in range(2):
+        lin.forward_host(xh, yh)
+    e2e_ms = []
+    for _ in range(max(3, min(args.steps, 10))):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        lin.forward_host(xh, yh)
+        e.record(stream)
+        e.synchronize()
+        e2e_ms.append(s.elapsed_time(e))
+    e2e_t = statistics.median(e2e_ms)
+    if ws > 1:
+        t = torch.tensor([e2e_t], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e_val = ws * M * flops_per_token() / (e2e_t / 1e3) / 1e12
+
+    if rank == 0:
+        g_ms = statistics.median(t_g)
+        q_ms = statistics.median(t_q)
+        peaks = measured_peaks()
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        gemm_tflops = M * flops_per_token() / (g_ms / 1e3) / 1e12
+        q_bytes = M * K * 2 + M * K // 2 + M * K // 32  # bf16 in, packed codes + E8M0 out
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("serq_linear_kernel", {}).get("dram_bytes_per_launch")
+            except (OSError, ValueError):
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": ws, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp4(e2m1)+e8m0 -> f32 accumulate -> bf16", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "M": M, "K": K, "N": N, "r": R, "format": "mxfp4",
+                       "activations": "N(0,1), 1% channels x50, SAF a=0.5, salient-permuted, bf16",
+                       "l2": "flushed between timed steps (256 MiB write + 256 MiB read of another buffer), flush excluded",
+                       "timing": "CUDA events around a CUDA-graph replay of the step (quantize + fused linear)",
+                       "parallelism": f"replicas x{ws} (tokens independent, no collective)"},
+            "tokens_per_s": ws * M / (ms_per_step / 1e3),
+            "tflops_pct_of_fp4_peak": 100.0 * value / FP4_PEAK_TFLOPS,
+            "breakdown_ms": {"quantize": q_ms, "linear": g_ms},
+            "roofline": {"bound": "tensor", "kernel": "serq_linear_kernel<mx> (fused main + salient term + epilogue)",
+                         "achieved": gemm_tflops, "peak": FP4_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": gemm_tflops / FP4_PEAK_TFLOPS,
+                         "peak_source": "nominal dense FP4 9 PFLOP/s (B200_PROFILING.md; MEASURED_PEAKS.json has no FP4 figure)",
+                         "measured_fp4_mma_ceiling_tflops": 8800.0,
+                         "measured_fp4_note": "tools/mma_rate.cu: back-to-back tcgen05.mma kind::mxf4 128x256x64 on 148 SMs, random operands (profiles/mma_rate_r01.txt)",
+                         "algorithmic_flops_per_launch": M * flops_per_token(), "traffic": traffic},
+            "quantizer_roofline": {"bound": "hbm", "kernel": "mx_encode_kernel<bf16>",
+                                   "achieved": q_bytes / (q_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                                   "frac": q_bytes / (q_ms / 1e3) / 1e9 / hbm,
+                                   "peak_source": "MEASURED_PEAKS.json hbm_gbs", "bytes_per_launch": q_bytes},
+            "e2e": {"value": e2e_val, "unit": "TFLOPS", "h2d_bytes_per_step": M * K * 2,
+                    "d2h_bytes_per_step": M * N * 2, "ms_per_step": e2e_t,
+                    "path": "serq_forward_mx_host (C-ABI): pinned H2D, quantize, fused linear, D2H"},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_leg(wl.x, wl.w)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="serq", choices=["serq", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_serq(args)
+
+
+if __name__ == "__main__":
+    main()

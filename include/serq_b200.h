@@ -120,6 +120,14 @@ int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* 
 /* Number of kernels the last forward on this thread launched (evidence for bench). */
 int serq_last_launch_count(void);
 
+/* Diagnostics for roofline work (results are WRONG while set): bit0 = the MX
+ * linear skips its operand loads (pure MMA ceiling), bit1 = skips the output
+ * stores.  0 restores normal operation. */
+int serq_set_debug_flags(int flags);
+/* Diagnostics: device buffer (>= 512 int64) receiving clock64 stamps around the
+ * MX linear's per-stage waits in CTA 0, or NULL to disable. */
+int serq_set_debug_timestamps(long long* dev_buf);
+
 #ifdef __cplusplus
 }
 #endif

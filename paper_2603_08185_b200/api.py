@@ -1,0 +1,419 @@
+"""Reference-facing mirror of the SERQ hot path, backed by the sm_100a kernels.
+
+Same names, argument meaning and error behaviour as the reference package
+(``/root/reference/pkg/src/serq``) for the functions on the hot path, so a
+caller of the reference can switch import paths:
+
+  IntQuantConfig, QuantizedTensor, per_token_config   quantcore.py:28-80
+  quantize_symmetric / quantize_asymmetric            quantcore.py:108-137 (GPU, bit-exact)
+  dequantize, gather_columns                          quantcore.py:144-175
+  MxBlockTensor, mx_encode, mx_decode                 mxfmt.py:34-113 (encode on GPU, bit-exact)
+  Compensator, OpProbe                                compensate.py:48-77
+  build_serq_rtn_mx                                   compensate.py:343-357 (encodes on GPU)
+  forward_reconstructed                               compensate.py:272-340 (GPU linear)
+  SerqLinear / make_linear_fn                         the module-level API used by
+                                                      SerqQuantizer.predict (estimators.py:89-97)
+                                                      and forward_quantized's linear_fn
+                                                      (toymodel.py:363-374)
+
+Artefacts produced by the reference builders (its dataclasses) are accepted
+by duck typing.  Layouts that integer tensor cores cannot evaluate exactly
+(scales that vary along the reduction dimension) raise
+``ValidationError`` naming the layout; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import device as D
+from .errors import ValidationError
+
+ROW_GROUPS, COL_GROUPS, PER_ROW = "row", "col", "per-row"
+RTN_RESIDUAL, GPTQ_SWAPPED, SVD_BASELINE = "rtn_residual", "gptq_swapped", "svd_baseline"
+
+E2M1_MAGNITUDES = np.array([0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0])
+
+
+# ------------------------------------------------------------------ containers
+
+
+@dataclass(frozen=True)
+class IntQuantConfig:
+    bits: int = 4
+    symmetric: bool = True
+    group_size: int | str = PER_ROW
+    axis: str = ROW_GROUPS
+
+    def __post_init__(self):
+        if not 2 <= self.bits <= 8:
+            raise ValidationError(f"bits must be in [2, 8], got {self.bits}")
+        if self.axis not in (ROW_GROUPS, COL_GROUPS):
+            raise ValidationError(f"unknown axis {self.axis!r}")
+        if self.group_size != PER_ROW and (not isinstance(self.group_size, (int, np.integer)) or self.group_size < 1):
+            raise ValidationError(f"invalid group_size {self.group_size!r}")
+
+    @property
+    def qmax(self) -> int:
+        return 2 ** (self.bits - 1) - 1
+
+    @property
+    def levels(self) -> int:
+        return 2**self.bits - 1
+
+
+def per_token_config(bits: int = 8) -> IntQuantConfig:
+    return IntQuantConfig(bits=bits, symmetric=False, group_size=PER_ROW)
+
+
+@dataclass
+class QuantizedTensor:
+    codes: np.ndarray
+    scales: np.ndarray
+    zero_points: np.ndarray | None
+    config: IntQuantConfig
+    shape: tuple
+
+    @property
+    def rows(self) -> int:
+        return self.shape[0]
+
+    @property
+    def cols(self) -> int:
+        return self.shape[1]
+
+
+@dataclass
+class MxBlockTensor:
+    element_codes: np.ndarray
+    block_scale_exponents: np.ndarray
+    block_size: int
+    shape: tuple
+
+    @property
+    def rows(self) -> int:
+        return self.shape[0]
+
+    @property
+    def cols(self) -> int:
+        return self.shape[1]
+
+
+@dataclass
+class Compensator:
+    mode: str
+    rank: int
+    salient_idx: np.ndarray | None = None
+    r_q: object = None
+    r_dense: np.ndarray | None = None
+    l1: np.ndarray | None = None
+    l2: np.ndarray | None = None
+
+    def __post_init__(self):
+        if self.mode not in (RTN_RESIDUAL, GPTQ_SWAPPED, SVD_BASELINE):
+            raise ValidationError(f"unknown compensator mode {self.mode!r}")
+        if self.rank and self.mode in (RTN_RESIDUAL, GPTQ_SWAPPED):
+            if (self.r_q is not None) + (self.r_dense is not None) != 1:
+                raise ValidationError("single-matrix modes carry exactly one R")
+
+
+@dataclass
+class OpProbe:
+    aux_matmuls: int = 0
+    notes: list = field(default_factory=list)
+
+
+# ------------------------------------------------------------------ helpers
+
+
+def _as_matrix(a, name="x") -> np.ndarray:
+    arr = np.ascontiguousarray(a, dtype=np.float64)
+    if arr.ndim != 2:
+        raise ValidationError(f"{name} must be 2-D, got shape {arr.shape}")
+    if arr.size == 0:
+        raise ValidationError(f"{name} must be non-empty")
+    if not np.isfinite(arr).all():
+        raise ValidationError(f"{name} contains non-finite values")
+    return arr
+
+
+def _groups(cfg, shape):
+    rows, cols = shape
+    if cfg.group_size == PER_ROW:
+        return COL_GROUPS, cols
+    gs = int(cfg.group_size)
+    dim = rows if cfg.axis == ROW_GROUPS else cols
+    if dim % gs:
+        raise ValidationError(f"group_size {gs} does not divide grouped dimension {dim}")
+    return cfg.axis, gs
+
+
+def _to_gpu(x: np.ndarray, dtype=torch.float64) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dtype)
+
+
+# ------------------------------------------------------------------ quantizers
+
+
+def _quantize(x, cfg: IntQuantConfig, symmetric: bool) -> QuantizedTensor:
+    if cfg.symmetric != symmetric:
+        raise ValidationError("config is not symmetric" if symmetric else "config is not asymmetric")
+    x = _as_matrix(x)
+    axis, gs = _groups(cfg, x.shape)
+    if axis == COL_GROUPS and gs == x.shape[1]:
+        src, transpose = x, False  # one group per row (per-token)
+    elif axis == ROW_GROUPS and gs == x.shape[0]:
+        src, transpose = np.ascontiguousarray(x.T), True  # one group per column (per-output-channel)
+    else:
+        raise ValidationError(
+            f"group layout (group_size={cfg.group_size!r}, axis={cfg.axis!r}) is not supported on the device; "
+            "supported: 'per-row' or one group spanning the grouped dimension")
+    act = D.quantize_int(_to_gpu(src), cfg.bits, symmetric)
+    codes = act.codes.cpu().numpy()
+    codes = codes.astype(np.int32) if symmetric else codes.view(np.uint8).astype(np.int32)
+    scales = act.scale64.cpu().numpy().reshape(-1, 1)
+    zps = None if symmetric else act.zp.cpu().numpy().astype(np.int32).reshape(-1, 1)
+    if transpose:
+        codes, scales = np.ascontiguousarray(codes.T), scales.T.copy()
+        zps = None if zps is None else zps.T.copy()
+    return QuantizedTensor(codes, scales, zps, cfg, x.shape)
+
+
+def quantize_symmetric(x, cfg: IntQuantConfig) -> QuantizedTensor:
+    """GPU twin of quantcore.quantize_symmetric (quantcore.py:108-118), bit-exact."""
+    return _quantize(x, cfg, True)
+
+
+def quantize_asymmetric(x, cfg: IntQuantConfig) -> QuantizedTensor:
+    """GPU twin of quantcore.quantize_asymmetric (quantcore.py:121-137), bit-exact."""
+    return _quantize(x, cfg, False)
+
+
+def dequantize(q) -> np.ndarray:
+    """quantcore.py:144-150 (host arithmetic on artefacts; not on the hot path)."""
+    axis, gs = _groups(q.config, q.shape)
+    s = np.repeat(q.scales, gs, axis=0 if axis == ROW_GROUPS else 1)
+    if q.zero_points is None:
+        return s * q.codes
+    z = np.repeat(q.zero_points, gs, axis=0 if axis == ROW_GROUPS else 1)
+    return s * (q.codes.astype(np.float64) - z)
+
+
+def gather_columns(q, idx) -> QuantizedTensor:
+    """quantcore.py:158-175."""
+    axis, gs = _groups(q.config, q.shape)
+    if axis != COL_GROUPS or gs != q.shape[1]:
+        raise ValidationError("gather_columns requires one scale group per row")
+    idx = np.asarray(idx, dtype=np.intp)
+    return QuantizedTensor(np.ascontiguousarray(q.codes[:, idx]), q.scales, q.zero_points,
+                           replace(q.config, group_size=PER_ROW), (q.shape[0], idx.size))
+
+
+def mx_encode(x, block_size: int = 32) -> MxBlockTensor:
+    """GPU twin of mxfmt.mx_encode (mxfmt.py:97-108): exact for float64 input."""
+    if block_size != 32:
+        raise ValidationError("the device MX format uses 32-element blocks")
+    x = _as_matrix(x)
+    rows, cols = x.shape
+    if cols % block_size:
+        raise ValidationError(f"row length {cols} not divisible by block_size {block_size}")
+    act = D.quantize_mx(_to_gpu(x))
+    c, e = D.unpack_mx(act.codes, act.sf, rows, cols)
+    return MxBlockTensor(c.cpu().numpy(), e.cpu().numpy(), block_size, (rows, cols))
+
+
+def mx_decode(t) -> np.ndarray:
+    """mxfmt.py:111-113 (artefact utility, host)."""
+    c = np.asarray(t.element_codes)
+    v = np.where((c & 8) != 0, -1.0, 1.0) * E2M1_MAGNITUDES[c & 7]
+    return v * np.ldexp(1.0, np.repeat(t.block_scale_exponents, t.block_size, axis=1))
+
+
+def build_serq_rtn_mx(w_folded, plan, block_size: int = 32):
+    """compensate.py:343-357 with the encodes on the GPU.  ``plan`` is a
+    SaliencyPlan (uses ``.rank`` / ``.salient_idx``) or an index array."""
+    w = _as_matrix(w_folded, "w_folded")
+    idx = np.asarray(getattr(plan, "salient_idx", plan), dtype=np.intp)
+    r = idx.size
+    main_t = mx_encode(np.ascontiguousarray(w.T), block_size)
+    if r == 0:
+        return main_t, Compensator(RTN_RESIDUAL, 0, np.empty(0, np.intp))
+    if r % block_size:
+        raise ValidationError("MX mode needs rank divisible by block size")
+    resid = (w - mx_decode(main_t).T)[idx, :]
+    return main_t, Compensator(RTN_RESIDUAL, r, idx.copy(), r_q=mx_encode(np.ascontiguousarray(resid.T), block_size))
+
+
+def build_per_channel_int(w, salient_idx, bits: int = 4, r_mode: str = "dense"):
+    """Per-output-channel integer artefacts: main =
+    quantize_symmetric(W, (bits, True, K, 'row')); R = W[idx] -
+    dequantize(main)[idx], kept as bf16 (``r_mode='dense'``) or quantized with
+    one scale per output column (``'int'``)."""
+    w = _as_matrix(w, "w")
+    k = w.shape[0]
+    main = quantize_symmetric(w, IntQuantConfig(bits, True, k, ROW_GROUPS))
+    idx = np.asarray(salient_idx, dtype=np.intp)
+    r = idx.size
+    if r == 0:
+        return main, Compensator(RTN_RESIDUAL, 0, idx)
+    resid = w[idx] - dequantize(main)[idx]
+    if r_mode == "dense":
+        rd = torch.from_numpy(resid).to(torch.bfloat16).to(torch.float64).numpy()
+        return main, Compensator(RTN_RESIDUAL, r, idx.copy(), r_dense=rd)
+    return main, Compensator(RTN_RESIDUAL, r, idx.copy(),
+                             r_q=quantize_symmetric(resid, IntQuantConfig(bits, True, r, ROW_GROUPS)))
+
+
+# ------------------------------------------------------------------ linear modules
+
+
+def _is_mx(t) -> bool:
+    return hasattr(t, "element_codes") and hasattr(t, "block_scale_exponents")
+
+
+class SerqLinear:
+    """One SERQ linear resident on the GPU (packed once from the artefacts).
+
+    ``__call__`` takes a CUDA tensor [M, K] (bf16 for the serving path; f32/f64
+    accepted) and returns bf16 [M, N].  INT layers quantize activations with
+    ``act_cfg`` (asymmetric per-token as the reference requires, or symmetric
+    when ``allow_symmetric_act`` -- BASELINE config 1)."""
+
+    def __init__(self, main, comp=None, act_cfg=None, allow_symmetric_act=False, device="cuda"):
+        self.fmt = "mx" if _is_mx(main) else "int"
+        has_r = comp is not None and getattr(comp, "rank", 0)
+        if has_r and getattr(comp, "mode", RTN_RESIDUAL) == SVD_BASELINE:
+            raise ValidationError("the two-factor SVD compensator is not part of the device path")
+        idx = None if not has_r else np.asarray(comp.salient_idx, dtype=np.intp)
+        if self.fmt == "mx":
+            if getattr(main, "block_size", 32) != 32:
+                raise ValidationError("the device MX format uses 32-element blocks")
+            if has_r and comp.r_dense is not None:
+                raise ValidationError("MX layers need an MX-encoded compensator (comp.r_q)")
+            if has_r and comp.rank % 32:
+                raise ValidationError("MX residual path needs rank divisible by block size")
+            rq = comp.r_q if has_r else None
+            self.impl = D.MxLinear(main.element_codes, main.block_scale_exponents,
+                                   None if rq is None else rq.element_codes,
+                                   None if rq is None else rq.block_scale_exponents, idx, device)
+            self.K, self.N = main.shape[1], main.shape[0]
+        else:
+            if act_cfg is None or (act_cfg.symmetric and not allow_symmetric_act):
+                raise ValidationError("act_cfg must be asymmetric (per-token)")
+            a_axis, a_gs = _groups(act_cfg, (1, main.shape[0]))
+            if not (a_axis == COL_GROUPS and a_gs == main.shape[0]):
+                raise ValidationError("activations must be quantized per token ('per-row')")
+            axis, gs = _groups(main.config, main.shape)
+            if not (axis == ROW_GROUPS and gs == main.shape[0]):
+                raise ValidationError(
+                    f"integer main layout (group_size={main.config.group_size!r}, axis={main.config.axis!r}) puts "
+                    "scales on the reduction dimension; the device path needs per-output-channel weights "
+                    "(group_size == K, axis 'row')")
+            kw = {}
+            if has_r:
+                if comp.r_dense is not None:
+                    kw = dict(r_dense=np.asarray(comp.r_dense))
+                else:
+                    rq = comp.r_q
+                    ax, g = _groups(rq.config, rq.shape)
+                    if not (ax == ROW_GROUPS and g == rq.shape[0]) or rq.zero_points is not None:
+                        raise ValidationError(
+                            "integer R must be symmetric with one scale per output column (row groups of size r)")
+                    kw = dict(r_codes=rq.codes, r_scales=rq.scales)
+            self.impl = D.IntLinear(main.codes, main.scales, main.config.bits, salient_idx=idx, device=device, **kw)
+            self.act_bits, self.act_symmetric = act_cfg.bits, act_cfg.symmetric
+            self.K, self.N = main.shape
+        self.rank = int(comp.rank) if has_r else 0
+
+    def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
+        if x.shape[-1] != self.K:
+            raise ValidationError("x columns must equal main rows")
+        if self.fmt == "mx":
+            return self.impl(x, y)
+        return self.impl(x, self.act_bits, self.act_symmetric, y)
+
+
+_CACHE: dict = {}
+
+
+def clear_cache() -> None:
+    _CACHE.clear()
+
+
+def _linear_for(main, comp, act_cfg, allow_symmetric_act=False) -> SerqLinear:
+    key = (id(main), id(comp), act_cfg, allow_symmetric_act)
+    hit = _CACHE.get(key)
+    if hit is not None and hit[0] is main and hit[1] is comp:
+        return hit[2]
+    lin = SerqLinear(main, comp, act_cfg, allow_symmetric_act)
+    _CACHE[key] = (main, comp, lin)  # keep the artefacts alive so ids stay unique
+    return lin
+
+
+def forward_reconstructed(x, main, comp, act_cfg, probe: OpProbe | None = None) -> np.ndarray:
+    """Drop-in for compensate.forward_reconstructed (compensate.py:272-316).
+
+    Activations are sent to the device as float64 and quantized there
+    bit-exactly; the main and salient products run in ONE fused kernel; the
+    bf16 result is returned as float64.  Weights are packed once per artefact
+    object and cached.  ``probe.aux_matmuls`` still counts the one auxiliary
+    product of the SERQ path (compensate.py:312-313)."""
+    x = _as_matrix(x)
+    if isinstance(main, np.ndarray):
+        # quantization-disabled mode (compensate.py:288-293): exact product on the device
+        xt = _to_gpu(x)
+        y = xt @ _to_gpu(main)
+        if comp is not None and comp.rank:
+            full = np.zeros(main.shape)
+            full[np.asarray(comp.salient_idx)] = np.asarray(comp.r_dense if comp.r_dense is not None else dequantize(comp.r_q))
+            y = y + xt @ _to_gpu(full)
+        return y.cpu().numpy()
+    if _is_mx(main):
+        if x.shape[1] != main.shape[1]:
+            raise ValidationError("x columns must equal weight input dim")
+    else:
+        if x.shape[1] != main.shape[0]:
+            raise ValidationError("x columns must equal main rows")
+        if act_cfg is None or act_cfg.symmetric:
+            raise ValidationError("act_cfg must be asymmetric (per-token)")
+    lin = _linear_for(main, comp, act_cfg)
+    y = lin(_to_gpu(x))
+    if probe is not None and lin.rank:
+        probe.aux_matmuls += 1
+    return y.float().cpu().numpy().astype(np.float64)
+
+
+def forward_symmetric_act(x, main, comp, act_cfg: IntQuantConfig) -> np.ndarray:
+    """BASELINE config 1: symmetric per-token activations.  The reference
+    forward rejects symmetric act_cfg (compensate.py:298-299); this is the
+    composition int_gemm_reference(quantize_symmetric(x), main) +
+    dequantize(gather_columns(xq, idx)) @ r_dense."""
+    if not act_cfg.symmetric:
+        raise ValidationError("forward_symmetric_act needs a symmetric act_cfg")
+    x = _as_matrix(x)
+    lin = _linear_for(main, comp, act_cfg, allow_symmetric_act=True)
+    return lin(_to_gpu(x)).float().cpu().numpy().astype(np.float64)
+
+
+def make_linear_fn(bundle, device="cuda"):
+    """``linear_fn(name, x)`` for the reference's graph_forward hook
+    (saliency.py:256-257; toymodel.forward_quantized, toymodel.py:363-374):
+    every linear of a QuantizedBlockBundle runs on the GPU."""
+    lins = {}
+    for name, lb in bundle.linears.items():
+        if isinstance(lb.main, np.ndarray):
+            lins[name] = None
+        else:
+            lins[name] = SerqLinear(lb.main, lb.comp, lb.act_cfg, device=device)
+
+    def linear_fn(name, xin):
+        lin = lins[name]
+        lb = bundle.linears[name]
+        if lin is None:
+            return forward_reconstructed(xin, lb.main, lb.comp, lb.act_cfg)
+        return lin(_to_gpu(_as_matrix(xin))).float().cpu().numpy().astype(np.float64)
+
+    return linear_fn

@@ -2,6 +2,7 @@
 
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 
@@ -9,8 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "serq_capi.cu")
 OUT = os.path.join(HERE, "libserq_b200.so")
-HEADERS = [os.path.join(HERE, "csrc", f) for f in ("serq_ptx.cuh", "serq_gemm.cuh", "serq_quant.cuh")] + [
-    os.path.join(ROOT, "include", "serq_b200.h")]
+HEADERS = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "serq_b200.h")]
 
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=default"]

@@ -8,6 +8,8 @@
 
 #include "../../include/serq_b200.h"
 #include "serq_gemm.cuh"
+#include "serq_gemm_mx.cuh"
+#include "serq_gemm_mx2.cuh"
 #include "serq_quant.cuh"
 
 using namespace serq;
@@ -16,6 +18,8 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_launches = 0;
+int g_debug_flags = 0;  // serq_set_debug_flags (diagnostic benchmarking only)
+long long* g_debug_ts = nullptr;
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -65,7 +69,8 @@ EncodeFn encode_fn() {
 
 // 2-D row-major map: `inner` elements per row (contiguous), `rows` rows, row pitch in bytes.
 int make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t rows,
-             uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_rows) {
+             uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_rows,
+             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeFn fn = encode_fn();
   if (!fn) return fail(SERQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
   if ((reinterpret_cast<uintptr_t>(base) & 15) || (pitch_bytes & 15))
@@ -76,9 +81,26 @@ int make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t 
   cuuint32_t box[2] = {box_inner, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SERQ_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return SERQ_OK;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// scale factors as rows of 128 B (one 1-KB box = 2 SF chunks of a 128-row block)
+int make_sf_map(CUtensorMap* m, const uint8_t* sf, int64_t rows, int64_t cols) {
+  return make_map(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, sf, 128, uint64_t(sf_bytes_of(rows, cols) / 128), 128, 128, 8,
+                  CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
 bool g_attr_set[2] = {false, false};
@@ -107,6 +129,7 @@ struct serq_linear {
   float* sr = nullptr;
   int32_t* colsum_r = nullptr;
   CUtensorMap map_b, map_r;
+  CUtensorMap map_b128, map_r128, map_sfw, map_sfr;  // CTA-pair kernel: 128-row B boxes, scale-factor maps
   // end-to-end scratch
   int64_t ws_m = 0;
   void* ws_x = nullptr;
@@ -130,6 +153,14 @@ extern "C" {
 const char* serq_last_error(void) { return g_err.c_str(); }
 const char* serq_version(void) { return "serq_b200 0.1 (sm_100a tcgen05)"; }
 int serq_last_launch_count(void) { return g_launches; }
+int serq_set_debug_flags(int flags) {
+  g_debug_flags = flags;
+  return SERQ_OK;
+}
+int serq_set_debug_timestamps(long long* dev_buf) {
+  g_debug_ts = dev_buf;
+  return SERQ_OK;
+}
 
 int serq_device_info(int* sm_count, int* cc_major, int* cc_minor) {
   int dev = 0;
@@ -168,22 +199,45 @@ int serq_act_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ld
   if (M % 128 || K % 256) CK(cudaMemsetAsync(sf, 0, sf_bytes_of(M, K), st));
   const int krc = gather_idx ? kc_pad_of(r) : 0;
   if (gather_idx && (M % 128 || r % 256)) CK(cudaMemsetAsync(xs_sf, 0, sf_bytes_of(M, r), st));
+  if (dtype != SERQ_F64) {
+    const dim3 grid(unsigned(cdiv(K / 8, 256)), unsigned(cdiv(M, kMxRows)));
+    if (dtype == SERQ_BF16 && (g_debug_flags & 32))
+      mx_encode_fast_kernel<__nv_bfloat16, 2><<<dim3(grid.x, unsigned(cdiv(M, 2))), 256, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(x), int(M), int(K), ldx, codes, sf, kc);
+    else if (dtype == SERQ_BF16 && (g_debug_flags & 64))
+      mx_encode_fast_kernel<__nv_bfloat16, 8><<<dim3(grid.x, unsigned(cdiv(M, 8))), 256, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(x), int(M), int(K), ldx, codes, sf, kc);
+    else if (dtype == SERQ_BF16 && (g_debug_flags & 128)) {
+      // grid-stride: ~8 resident blocks of 256 threads per SM
+      const int64_t want = int64_t(sm_count()) * 8 / grid.x;
+      const int64_t groups = cdiv(M, 4);
+      mx_encode_bf16_stride_kernel<<<dim3(grid.x, unsigned(want < groups ? (want > 0 ? want : 1) : groups)), 256, 0,
+                                     st>>>(static_cast<const __nv_bfloat16*>(x), int(M), int(K), ldx, codes, sf, kc);
+    }
+    else if (dtype == SERQ_BF16)
+      mx_encode_fast_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), int(M), int(K),
+                                                                 ldx, codes, sf, kc);
+    else
+      mx_encode_fast_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(x), int(M), int(K), ldx, codes, sf,
+                                                         kc);
+    LAUNCH_CHECK("mx_encode_fast");
+    if (gather_idx) {
+      const dim3 g2(unsigned(cdiv(M * (r / 8), 256)));
+      if (dtype == SERQ_BF16)
+        mx_encode_kernel<__nv_bfloat16><<<g2, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), M, K, ldx, codes,
+                                                            sf, kc, gather_idx, r, xs_codes, xs_sf, krc, 0);
+      else
+        mx_encode_kernel<float><<<g2, 256, 0, st>>>(static_cast<const float*>(x), M, K, ldx, codes, sf, kc,
+                                                    gather_idx, r, xs_codes, xs_sf, krc, 0);
+      LAUNCH_CHECK("mx_encode_gather");
+    }
+    return SERQ_OK;
+  }
   const int64_t nb_main = cdiv(M * (K / 8), 256);
   const int64_t nb_g = gather_idx ? cdiv(M * (r / 8), 256) : 0;
-  dim3 grid(unsigned(nb_main + nb_g));
-  switch (dtype) {
-    case SERQ_BF16:
-      mx_encode_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), M, K, ldx, codes,
-                                                            sf, kc, gather_idx, r, xs_codes, xs_sf, krc, nb_main);
-      break;
-    case SERQ_F32:
-      mx_encode_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(x), M, K, ldx, codes, sf, kc, gather_idx,
-                                                    r, xs_codes, xs_sf, krc, nb_main);
-      break;
-    default:
-      mx_encode_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(x), M, K, ldx, codes, sf, kc,
-                                                     gather_idx, r, xs_codes, xs_sf, krc, nb_main);
-  }
+  const dim3 grid(unsigned(nb_main + nb_g));
+  mx_encode_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(x), M, K, ldx, codes, sf, kc, gather_idx,
+                                                 r, xs_codes, xs_sf, krc, nb_main);
   LAUNCH_CHECK("mx_encode");
   return SERQ_OK;
 }
@@ -199,6 +253,21 @@ int serq_act_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t l
   if (xs_kind && (r <= 0 || r > K || !xs_out)) return fail(SERQ_EINVAL, "salient slice needs 0 < r <= K and xs_out");
   cudaStream_t st = S(stream);
   const dim3 grid(static_cast<unsigned>(M));
+  if (dtype == SERQ_BF16 && K % 8 == 0 && K <= 8192 && ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(codes) & 7) == 0) {
+    const int nv = int(cdiv(K, 2048));
+    const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
+#define SERQ_INTQ(NV)                                                                                          \
+  int_quant_bf16_kernel<NV><<<grid, 256, 0, st>>>(xb, int(K), ldx, bits, symmetric, codes, scale64, scale32, zp, \
+                                                  salient_idx, r, xs_out, xs_kind)
+    if (nv == 1) SERQ_INTQ(1);
+    else if (nv == 2) SERQ_INTQ(2);
+    else if (nv == 3) SERQ_INTQ(3);
+    else SERQ_INTQ(4);
+#undef SERQ_INTQ
+    LAUNCH_CHECK("int_quant_bf16");
+    return SERQ_OK;
+  }
   switch (dtype) {
     case SERQ_BF16:
       int_quant_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), M, K, ldx, bits,
@@ -248,7 +317,11 @@ int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K
                                                                   kc_pad_of(K));
   if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_mx launch failed"));
   int rc = make_map(&h->map_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K / 2, N, K / 2, 128, kBN);
+  if (!rc) rc = make_map(&h->map_b128, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K / 2, N, K / 2, 128, 128);
+  if (!rc) rc = make_sf_map(&h->map_sfw, h->sfw, N, K);
   if (rc) return bail(rc);
+  h->map_r128 = h->map_b128;
+  h->map_sfr = h->map_sfw;
   if (r > 0) {
     if (cudaMalloc(&h->rbuf, N * r / 2) != cudaSuccess || cudaMalloc(&h->sfr, sf_bytes_of(N, r)) != cudaSuccess)
       return bail(fail(SERQ_ECUDA, "cudaMalloc failed for R"));
@@ -257,6 +330,8 @@ int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K
                                                                     static_cast<uint8_t*>(h->rbuf), h->sfr, kc_pad_of(r));
     if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_mx launch failed"));
     rc = make_map(&h->map_r, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r / 2, N, r / 2, 128, kBN);
+    if (!rc) rc = make_map(&h->map_r128, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r / 2, N, r / 2, 128, 128);
+    if (!rc) rc = make_sf_map(&h->map_sfr, h->sfr, N, r);
     if (rc) return bail(rc);
   }
   *out = h;
@@ -356,8 +431,12 @@ int serq_linear_mx(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t
   if (ldy < h->N || ldy % 8) return fail(SERQ_EINVAL, "ldy must be >= N and a multiple of 8");
   const bool need_xs = h->r > 0 && !h->contiguous;
   if (need_xs && (!xs_codes || !xs_sf)) return fail(SERQ_EINVAL, "non-contiguous salient set needs the xs slice");
-  int rc = ensure_attr<kModeMX>();
-  if (rc) return rc;
+  static bool attr_done = false;
+  if (!attr_done) {
+    CK(cudaFuncSetAttribute(serq_mx_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmemBytes));
+    attr_done = true;
+  }
+  int rc = SERQ_OK;
   CUtensorMap ma, mxs, my;
   rc = make_map(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, kBM);
   if (rc) return rc;
@@ -384,10 +463,45 @@ int serq_linear_mx(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t
   p.sfb_r = h->sfr;
   p.kc_pad = kc_pad_of(h->K);
   p.kc_pad_r = kc_pad_of(h->r > 0 ? h->r : 32);
-  dim3 grid(unsigned(cdiv(M, kBM)), unsigned(cdiv(h->N, kBN)));
-  serq_linear_kernel<kModeMX><<<grid, kThreads, kSmemBytes, S(stream)>>>(ma, h->map_b, mxs, h->r ? h->map_r : h->map_b,
-                                                                         my, p);
-  LAUNCH_CHECK("serq_linear_kernel<mx>");
+  p.dbg = g_debug_flags;
+  p.dbg_ts = g_debug_ts;
+  if (M > 128 && !(g_debug_flags & 16)) {
+    static bool attr2 = false;
+    if (!attr2) {
+      CK(cudaFuncSetAttribute(serq_mx_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k2SmemBytes));
+      attr2 = true;
+    }
+    Pair2Maps pm;
+    rc = make_map(&pm.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, 128);
+    if (rc) return rc;
+    pm.b = h->map_b128;
+    pm.r = h->map_r128;
+    rc = make_map(&pm.y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, h->N, M, ldy * 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+    pm.sfb = h->map_sfw;
+    pm.sfr = h->map_sfr;
+    rc = make_sf_map(&pm.sfa, a_sf, M, h->K);
+    if (rc) return rc;
+    if (need_xs) {
+      rc = make_map(&pm.xs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_codes, h->r / 2, M, h->r / 2, 128, 128);
+      if (!rc) rc = make_sf_map(&pm.sfxs, xs_sf, M, h->r);
+      if (rc) return rc;
+    } else {
+      pm.xs = pm.a;
+      pm.sfxs = pm.sfa;
+    }
+    const int64_t pairs = cdiv(M, 256) * cdiv(h->N, kBN);
+    const int64_t max_pairs = sm_count() / 2;
+    const dim3 grid(unsigned(2 * (pairs < max_pairs ? pairs : max_pairs)));
+    serq_mx_pair_kernel<<<grid, kThreads, k2SmemBytes, S(stream)>>>(pm, p);
+    LAUNCH_CHECK("serq_mx_pair_kernel");
+    return SERQ_OK;
+  }
+  const int64_t tiles = cdiv(M, kBM) * cdiv(h->N, kBN);
+  const dim3 grid(unsigned(tiles < sm_count() ? tiles : sm_count()));
+  serq_mx_persistent_kernel<<<grid, kThreads, kPSmemBytes, S(stream)>>>(ma, h->map_b, mxs, h->r ? h->map_r : h->map_b,
+                                                                        my, p);
+  LAUNCH_CHECK("serq_mx_persistent_kernel");
   return SERQ_OK;
 }
 

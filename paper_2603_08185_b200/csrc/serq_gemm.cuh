@@ -68,6 +68,8 @@ struct GemmParams {
   const int32_t* colsum_r;
   int32_t* acc_dump;     // debug: exact main accumulators (acc - zp*colsum), [M,N]
   int32_t* accr_dump;    // debug: exact R accumulators
+  long long* dbg_ts;     // diagnostics: per-iteration clock64 stamps of the MMA warp (CTA 0), or nullptr
+  int dbg;               // diagnostics: bit0 = producer skips all loads (MMA ceiling), bit1 = no output stores
 };
 
 template <int kMode>

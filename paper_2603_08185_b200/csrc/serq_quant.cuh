@@ -58,17 +58,24 @@ __device__ __forceinline__ uint32_t e2m1_index_sw(double a) {
   return i;
 }
 
-// two f32 (exact after the power-of-two scaling) -> packed e2m1x2 byte, lo = even element;
-// hardware RNE + satfinite, then -0 (code 8) canonicalised to +0 (mxfmt.py:67).
-__device__ __forceinline__ uint32_t cvt_e2m1x2(float even, float odd) {
+// two f32 (exact after the power-of-two scaling) -> packed e2m1x2 byte, lo = even element
+// (hardware RNE + satfinite; cuda_fp4.hpp operand order: first source -> high nibble).
+__device__ __forceinline__ uint32_t cvt_e2m1x2_raw(float even, float odd) {
   uint32_t out;
   asm("{\n .reg .b8 t;\n cvt.rn.satfinite.e2m1x2.f32 t, %1, %2;\n cvt.u32.u8 %0, t;\n}\n"
       : "=r"(out)
       : "f"(odd), "f"(even));
-  uint32_t lo = out & 0xF, hi = (out >> 4) & 0xF;
-  lo = lo == 8 ? 0 : lo;
-  hi = hi == 8 ? 0 : hi;
-  return lo | (hi << 4);
+  return out;
+}
+// -0 (code 8) -> +0 on eight packed nibbles (the reference emits +0 for values
+// rounding to zero, mxfmt.py:67): clear the sign of every zero-magnitude nibble.
+__device__ __forceinline__ uint32_t canon_neg_zero(uint32_t p) {
+  const uint32_t mag = p & 0x77777777u;
+  const uint32_t z = ~(mag | (mag >> 1) | (mag >> 2)) & 0x11111111u;
+  return p & ~(z << 3);
+}
+__device__ __forceinline__ uint32_t cvt_e2m1x2(float even, float odd) {
+  return canon_neg_zero(cvt_e2m1x2_raw(even, odd));
 }
 
 // block exponent e = floor(log2 amax) - 2 (0 for amax == 0), clipped to [-127, 127]
@@ -165,6 +172,145 @@ __global__ void __launch_bounds__(256) mx_encode_kernel(const T* __restrict__ x,
     for (int i = 0; i < 4; ++i) packed |= cvt_e2m1x2(v[2 * i] * inv, v[2 * i + 1] * inv) << (8 * i);
     *reinterpret_cast<uint32_t*>(out_codes + row * (cols / 2) + c0 / 2) = packed;
     if ((threadIdx.x & 3) == 0) out_sf[sf_offset(row, c0 / 32, kcp)] = uint8_t(e + 127);
+  }
+}
+
+// Fast path for bf16 / f32 rows: 2-D grid (x: 2048-column chunks, y: kMxRows-row
+// groups); each thread keeps kMxRows independent 16-B loads in flight and emits a
+// 32-bit word of 8 packed codes per row.  For bf16 the block amax is an integer
+// 16-bit SIMD max over |x| bit patterns (monotonic for finite bf16) and the
+// exponent comes straight from those bits, so the only float work is the exact
+// power-of-two scaling feeding cvt.rn.satfinite.e2m1x2.
+constexpr int kMxRows = 4;  // default rows per thread
+__device__ __forceinline__ int mx_block_exp_bf16bits(uint32_t amax_bits) {
+  // amax_bits: 15-bit magnitude of a bf16; exponent field = bits >> 7
+  const int ef = int(amax_bits >> 7);
+  return amax_bits == 0 ? 0 : (ef == 0 ? -127 : max(ef - 129, -127));
+}
+template <typename T, int kMxRows = serq::kMxRows>
+__global__ void __launch_bounds__(256) mx_encode_fast_kernel(const T* __restrict__ x, int M, int K, int64_t ldx,
+                                                             uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
+                                                             int kc_pad) {
+  const int c8 = blockIdx.x * 256 + threadIdx.x;  // 8-element group within the row
+  const int r0 = blockIdx.y * kMxRows;
+  const bool col_ok = c8 < (K >> 3);
+  if constexpr (In<T>::kId == 0) {
+    const uint4* src = reinterpret_cast<const uint4*>(x + int64_t(r0) * ldx) + c8;
+    const int64_t stride = ldx >> 3;
+    uint4 raw[kMxRows];
+#pragma unroll
+    for (int rr = 0; rr < kMxRows; ++rr)
+      raw[rr] = (col_ok && r0 + rr < M) ? __ldg(src + rr * stride) : make_uint4(0, 0, 0, 0);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(codes + int64_t(r0) * (K >> 1)) + c8;
+    const int kb = c8 >> 2;
+    // SF byte offset of (row r0 + rr, block kb): rows r0..r0+3 share row>>5 and row>>7
+    const size_t sf0 = (size_t(r0 >> 7) * kc_pad + size_t(kb >> 2)) * 512 + size_t((r0 >> 5) & 3) * 4 + size_t(kb & 3);
+#pragma unroll
+    for (int rr = 0; rr < kMxRows; ++rr) {
+      const uint32_t w[4] = {raw[rr].x, raw[rr].y, raw[rr].z, raw[rr].w};
+      uint32_t m2 = __vmaxu2(__vmaxu2(w[0] & 0x7FFF7FFFu, w[1] & 0x7FFF7FFFu),
+                             __vmaxu2(w[2] & 0x7FFF7FFFu, w[3] & 0x7FFF7FFFu));
+      uint32_t m = max(m2 & 0xFFFFu, m2 >> 16);
+      m = max(m, __shfl_xor_sync(0xffffffff, m, 1));
+      m = max(m, __shfl_xor_sync(0xffffffff, m, 2));
+      const int e = mx_block_exp_bf16bits(m);
+      const float inv = __uint_as_float(uint32_t(127 - e) << 23);  // 2^-e, exact
+      uint32_t packed = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        packed |= cvt_e2m1x2_raw(__uint_as_float(w[i] << 16) * inv, __uint_as_float(w[i] & 0xFFFF0000u) * inv)
+                  << (8 * i);
+      const int row = r0 + rr;
+      if (col_ok && row < M) {
+        dst[int64_t(rr) * (K >> 3)] = canon_neg_zero(packed);
+        if ((threadIdx.x & 3) == 0) sf[sf0 + size_t(((r0 + rr) & 31)) * 16] = uint8_t(e + 127);
+      }
+    }
+  } else {
+    float v[kMxRows][8];
+#pragma unroll
+    for (int rr = 0; rr < kMxRows; ++rr) {
+      const int row = r0 + rr;
+      if (col_ok && row < M) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(x + int64_t(row) * ldx) + 2 * c8);
+        const float4 b = __ldg(reinterpret_cast<const float4*>(x + int64_t(row) * ldx) + 2 * c8 + 1);
+        v[rr][0] = a.x; v[rr][1] = a.y; v[rr][2] = a.z; v[rr][3] = a.w;
+        v[rr][4] = b.x; v[rr][5] = b.y; v[rr][6] = b.z; v[rr][7] = b.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[rr][i] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < kMxRows; ++rr) {
+      const int row = r0 + rr;
+      float amax = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(v[rr][i]));
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffff, amax, 1));
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffff, amax, 2));
+      const int e = mx_block_exp_f32(amax);
+      const float inv = __uint_as_float(uint32_t(127 - e) << 23);
+      uint32_t packed = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) packed |= cvt_e2m1x2_raw(v[rr][2 * i] * inv, v[rr][2 * i + 1] * inv) << (8 * i);
+      if (col_ok && row < M) {
+        reinterpret_cast<uint32_t*>(codes + int64_t(row) * (K >> 1))[c8] = canon_neg_zero(packed);
+        if ((threadIdx.x & 3) == 0) sf[sf_offset(row, c8 >> 2, kc_pad)] = uint8_t(e + 127);
+      }
+    }
+  }
+}
+
+// Grid-stride variant for bf16: blockIdx.y strides over 4-row groups and the loads
+// of the next group are issued before the current group is converted (register
+// double buffering), so every thread keeps 8 x 16 B in flight across iterations.
+__global__ void __launch_bounds__(256) mx_encode_bf16_stride_kernel(const __nv_bfloat16* __restrict__ x, int M, int K,
+                                                                    int64_t ldx, uint8_t* __restrict__ codes,
+                                                                    uint8_t* __restrict__ sf, int kc_pad) {
+  constexpr int R = 4;
+  const int c8 = blockIdx.x * 256 + threadIdx.x;
+  const bool col_ok = c8 < (K >> 3);
+  const int n_groups = (M + R - 1) / R;
+  const int64_t stride = ldx >> 3;
+  const int kb = c8 >> 2;
+  uint4 cur[R], nxt[R];
+  auto load = [&](uint4 (&buf)[R], int grp) {
+    const int r0 = grp * R;
+    const uint4* src = reinterpret_cast<const uint4*>(x + int64_t(r0) * ldx) + c8;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr)
+      buf[rr] = (col_ok && grp < n_groups && r0 + rr < M) ? __ldg(src + rr * stride) : make_uint4(0, 0, 0, 0);
+  };
+  int grp = blockIdx.y;
+  load(cur, grp);
+  for (; grp < n_groups; grp += gridDim.y) {
+    load(nxt, grp + gridDim.y);
+    const int r0 = grp * R;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(codes + int64_t(r0) * (K >> 1)) + c8;
+    const size_t sf0 = (size_t(r0 >> 7) * kc_pad + size_t(kb >> 2)) * 512 + size_t((r0 >> 5) & 3) * 4 + size_t(kb & 3);
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const uint32_t w[4] = {cur[rr].x, cur[rr].y, cur[rr].z, cur[rr].w};
+      const uint32_t m2 = __vmaxu2(__vmaxu2(w[0] & 0x7FFF7FFFu, w[1] & 0x7FFF7FFFu),
+                                   __vmaxu2(w[2] & 0x7FFF7FFFu, w[3] & 0x7FFF7FFFu));
+      uint32_t m = max(m2 & 0xFFFFu, m2 >> 16);
+      m = max(m, __shfl_xor_sync(0xffffffff, m, 1));
+      m = max(m, __shfl_xor_sync(0xffffffff, m, 2));
+      const int e = mx_block_exp_bf16bits(m);
+      const float inv = __uint_as_float(uint32_t(127 - e) << 23);
+      uint32_t packed = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        packed |= cvt_e2m1x2_raw(__uint_as_float(w[i] << 16) * inv, __uint_as_float(w[i] & 0xFFFF0000u) * inv)
+                  << (8 * i);
+      if (col_ok && r0 + rr < M) {
+        dst[int64_t(rr) * (K >> 3)] = canon_neg_zero(packed);
+        if ((threadIdx.x & 3) == 0) sf[sf0 + size_t((r0 + rr) & 31) * 16] = uint8_t(e + 127);
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) cur[rr] = nxt[rr];
   }
 }
 
@@ -274,6 +420,108 @@ __global__ void __launch_bounds__(256) int_quant_kernel(const T* __restrict__ x,
       } else {
         reinterpret_cast<int8_t*>(xs_out)[row * r + j] = int8_t(c);
       }
+    }
+  }
+}
+
+// Fast path for bf16 rows with K % 8 == 0 and K <= 2048 * kNV: one CTA per row,
+// the row stays in registers between the reduction and the quantization pass
+// (one HBM read), 16-B loads and 8-B code stores.
+template <int kNV>
+__global__ void __launch_bounds__(256) int_quant_bf16_kernel(const __nv_bfloat16* __restrict__ x, int K, int64_t ldx,
+                                                             int bits, int symmetric, int8_t* __restrict__ codes,
+                                                             double* __restrict__ scale64, float* __restrict__ scale32,
+                                                             int32_t* __restrict__ zp_out,
+                                                             const int32_t* __restrict__ sidx, int r,
+                                                             void* __restrict__ xs_out, int xs_kind) {
+  const int64_t row = blockIdx.x;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * ldx);
+  const int n8 = K >> 3;
+  __shared__ float red_lo[8], red_hi[8];
+  __shared__ double s_scale;
+  __shared__ int s_zp;
+  uint4 raw[kNV];
+  float lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < kNV; ++j) {
+    const int c8 = threadIdx.x + j * 256;
+    raw[j] = c8 < n8 ? __ldg(xr + c8) : make_uint4(0, 0, 0, 0);
+    if (c8 < n8) {
+      const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float a = __uint_as_float(w[i] << 16), b = __uint_as_float(w[i] & 0xFFFF0000u);
+        lo = fminf(lo, fminf(a, b));
+        hi = fmaxf(hi, fmaxf(a, b));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffff, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffff, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red_lo[threadIdx.x >> 5] = lo;
+    red_hi[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      lo = fminf(lo, red_lo[w]);
+      hi = fmaxf(hi, red_hi[w]);
+    }
+    const double dlo = lo, dhi = hi;  // exact (bf16 values)
+    double sc;
+    int zp = 0;
+    if (symmetric) {
+      sc = fmax(fabs(dlo), fabs(dhi)) / double((1 << (bits - 1)) - 1);
+      if (sc == 0.0) sc = 1.0;
+    } else {
+      sc = (dhi - dlo) / double((1 << bits) - 1);
+      if (sc == 0.0) sc = 1.0;
+      zp = int(rint(-dlo / sc));
+    }
+    s_scale = sc;
+    s_zp = zp;
+    scale64[row] = sc;
+    scale32[row] = float(sc);
+    if (zp_out) zp_out[row] = zp;
+  }
+  __syncthreads();
+  const double sc = s_scale;
+  const int zp = s_zp;
+  const double inv64 = 1.0 / sc;
+  const float inv32 = float(inv64);
+  const int qmax = symmetric ? (1 << (bits - 1)) - 1 : (1 << bits) - 1;
+  const int qmin = symmetric ? -qmax : 0;
+  uint2* out = reinterpret_cast<uint2*>(codes + row * K);
+#pragma unroll
+  for (int j = 0; j < kNV; ++j) {
+    const int c8 = threadIdx.x + j * 256;
+    if (c8 >= n8) continue;
+    const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
+    uint32_t packed[2] = {0u, 0u};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t hbits = (i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16);
+      const __nv_bfloat16 xv = __ushort_as_bfloat16(static_cast<unsigned short>(hbits >> 16));
+      const double qd = rint_quot<__nv_bfloat16>(xv, sc, inv32, inv64) + double(zp);
+      const int q = int(fmin(fmax(qd, double(qmin)), double(qmax)));
+      packed[i >> 2] |= (uint32_t(q) & 0xFFu) << (8 * (i & 3));
+    }
+    out[c8] = make_uint2(packed[0], packed[1]);
+  }
+  if (xs_kind != 0) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < r; j += blockDim.x) {
+      const int col = sidx ? sidx[j] : j;
+      const int c = symmetric ? int(codes[row * K + col]) : int(uint8_t(codes[row * K + col]));
+      if (xs_kind == 1)
+        reinterpret_cast<__nv_bfloat16*>(xs_out)[row * r + j] = __int2bfloat16_rn(c - zp);
+      else
+        reinterpret_cast<int8_t*>(xs_out)[row * r + j] = int8_t(c);
     }
   }
 }
