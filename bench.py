@@ -282,7 +282,7 @@ def run_serq(args) -> None:
         prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof)).get("serq_linear_kernel", {}).get("dram_bytes_per_launch")
+                traffic = json.load(open(prof)).get("serq_mx_pair_kernel", {}).get("dram_bytes_per_launch")
             except (OSError, ValueError):
                 traffic = None
         line = {

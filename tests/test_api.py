@@ -1,0 +1,180 @@
+"""The reference-facing mirror (paper_2603_08185_b200.api): same names,
+dataclasses, argument meaning and error behaviour as serq.compensate /
+serq.quantcore / serq.mxfmt for the hot path."""
+
+import types
+
+import numpy as np
+import pytest
+
+from oracle import serq_oracle as O
+from paper_2603_08185_b200 import api
+from paper_2603_08185_b200.errors import ValidationError
+
+torch = pytest.importorskip("torch")
+
+TOL_MAX, TOL_MEAN = 1e-2, 1e-3
+
+
+# ---------------------------------------------------------------- CPU: preconditions fail loudly, before the GPU
+
+
+def test_validation_error_is_value_error():
+    assert issubclass(ValidationError, ValueError)
+
+
+def test_config_validation_mirrors_reference():
+    # quantcore.py:35-43
+    with pytest.raises(ValidationError):
+        api.IntQuantConfig(bits=9)
+    with pytest.raises(ValidationError):
+        api.IntQuantConfig(axis="diag")
+    with pytest.raises(ValidationError):
+        api.IntQuantConfig(group_size=0)
+    assert api.per_token_config(8) == api.IntQuantConfig(8, False, "per-row")
+
+
+def test_forward_requires_asymmetric_act_cfg():
+    # compensate.py:298-299
+    main = api.QuantizedTensor(np.zeros((8, 4), np.int32), np.ones((1, 4)), None,
+                               api.IntQuantConfig(4, True, 8, "row"), (8, 4))
+    with pytest.raises(ValidationError, match="asymmetric"):
+        api.forward_reconstructed(np.ones((2, 8)), main, None, api.IntQuantConfig(4, True))
+    with pytest.raises(ValidationError, match="main rows"):
+        api.forward_reconstructed(np.ones((2, 7)), main, None, api.per_token_config(8))
+
+
+def test_layouts_integer_cores_cannot_evaluate_are_rejected():
+    # per-row (per input channel) main scales vary along K
+    main = api.QuantizedTensor(np.zeros((8, 4), np.int32), np.ones((8, 1)), None,
+                               api.IntQuantConfig(4, True, "per-row"), (8, 4))
+    with pytest.raises(ValidationError, match="reduction dimension"):
+        api.SerqLinear(main, None, api.per_token_config(8))
+    with pytest.raises(ValidationError):
+        api.forward_reconstructed(np.ones((2, 8)), main, None, api.per_token_config(8))
+
+
+def test_svd_compensator_rejected():
+    comp = api.Compensator(api.SVD_BASELINE, 2, l1=np.ones((8, 2)), l2=np.ones((2, 4)))
+    main = api.MxBlockTensor(np.zeros((4, 32), np.uint8), np.zeros((4, 1), np.int32), 32, (4, 32))
+    with pytest.raises(ValidationError, match="SVD"):
+        api.SerqLinear(main, comp)
+
+
+def test_nonfinite_input_rejected():
+    main = api.MxBlockTensor(np.zeros((4, 32), np.uint8), np.zeros((4, 1), np.int32), 32, (4, 32))
+    with pytest.raises(ValidationError, match="non-finite"):
+        api.forward_reconstructed(np.full((2, 32), np.nan), main, None, None)
+
+
+def test_single_matrix_compensator_invariant():
+    with pytest.raises(ValidationError, match="exactly one R"):
+        api.Compensator(api.RTN_RESIDUAL, 4, np.arange(4))
+
+
+# ---------------------------------------------------------------- GPU: drop-in parity
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    api.clear_cache()
+    return True
+
+
+def _mx_artifacts(golden, idx_key="fmx_idx"):
+    main = api.MxBlockTensor(golden["fmx_main_codes"], golden["fmx_main_exps"], 32, golden["fmx_main_codes"].shape)
+    rq = api.MxBlockTensor(golden["fmx_r_codes"], golden["fmx_r_exps"], 32, golden["fmx_r_codes"].shape)
+    comp = api.Compensator(api.RTN_RESIDUAL, 64, np.asarray(golden[idx_key]), r_q=rq)
+    return main, comp
+
+
+@pytest.mark.gpu
+def test_forward_reconstructed_mx_golden(gpu, golden):
+    main, comp = _mx_artifacts(golden)
+    probe = api.OpProbe()
+    y = api.forward_reconstructed(golden["fmx_x"], main, comp, None, probe)
+    assert probe.aux_matmuls == 1  # one auxiliary product (compensate.py:336-337)
+    mx, mean = O.parity_errors(y, golden["fmx_y"])
+    assert y.dtype == np.float64 and mx <= TOL_MAX and mean <= TOL_MEAN
+    # gather fallback
+    main_g, comp_g = _mx_artifacts(golden, "fmx_gidx")
+    y = api.forward_reconstructed(golden["fmx_x"], main_g, comp_g, None)
+    mx, mean = O.parity_errors(y, golden["fmx_y_gather"])
+    assert mx <= TOL_MAX and mean <= TOL_MEAN
+
+
+@pytest.mark.gpu
+def test_forward_reconstructed_int_golden(gpu, golden):
+    x, w = golden["fint_x"], golden["fint_w"]
+    main, comp = api.build_per_channel_int(w, np.arange(32), r_mode="int")
+    for bits in (4, 8):
+        y = api.forward_reconstructed(x, main, comp, api.per_token_config(bits))
+        mx, mean = O.parity_errors(y, golden[f"fint_y_a{bits}"])
+        assert mx <= TOL_MAX and mean <= TOL_MEAN, (bits, mx, mean)
+    main_d, comp_d = api.build_per_channel_int(w, np.arange(32), r_mode="dense")
+    y = api.forward_reconstructed(x, main_d, comp_d, api.per_token_config(8))
+    mx, mean = O.parity_errors(y, golden["fint_y_dense_a8"])
+    assert mx <= TOL_MAX and mean <= TOL_MEAN
+
+
+@pytest.mark.gpu
+def test_gpu_quantizers_and_builders_match_oracle(gpu, golden):
+    x = golden["q_x_13"]
+    for bits in (2, 4, 8):
+        s = api.quantize_symmetric(x, api.IntQuantConfig(bits, True, "per-row"))
+        a = api.quantize_asymmetric(x, api.per_token_config(bits))
+        assert np.array_equal(s.codes, golden[f"q_sym{bits}_codes_13"])
+        assert np.array_equal(a.codes, golden[f"q_asym{bits}_codes_13"])
+        assert np.array_equal(a.zero_points, golden[f"q_asym{bits}_zps_13"])
+    # per-output-channel weights: group_size == rows, axis 'row' (one scale per column)
+    wq = api.quantize_symmetric(golden["igpc_w"], api.IntQuantConfig(4, True, 128, "row"))
+    assert np.array_equal(wq.codes, golden["igpc_wcodes"]) and np.array_equal(wq.scales, golden["igpc_wscales"])
+    # mx_encode (f64 exact) and the MX builder
+    for i in range(int(golden["mx_count"])):
+        t = api.mx_encode(golden[f"mx_x_{i}"], 32)
+        assert np.array_equal(t.element_codes, golden[f"mx_codes_{i}"])
+        assert np.array_equal(t.block_scale_exponents, golden[f"mx_exps_{i}"])
+    main_t, comp = api.build_serq_rtn_mx(golden["fmx_w"], golden["fmx_idx"])
+    assert np.array_equal(main_t.element_codes, golden["fmx_main_codes"])
+    assert np.array_equal(comp.r_q.element_codes, golden["fmx_r_codes"])
+    assert np.array_equal(comp.r_q.block_scale_exponents, golden["fmx_r_exps"])
+
+
+@pytest.mark.gpu
+def test_passthrough_mode(gpu):
+    # quantization-disabled mode (compensate.py:288-293)
+    rng = np.random.default_rng(0)
+    x, w = rng.standard_normal((5, 16)), rng.standard_normal((16, 8))
+    np.testing.assert_allclose(api.forward_reconstructed(x, w, None, None), x @ w, rtol=1e-12)
+
+
+@pytest.mark.gpu
+def test_serq_linear_module_and_linear_fn(gpu, golden):
+    main, comp = _mx_artifacts(golden)
+    lin = api.SerqLinear(main, comp)
+    xt = torch.from_numpy(golden["fmx_x"]).to("cuda", torch.bfloat16)
+    y = lin(xt)
+    assert y.dtype == torch.bfloat16 and y.shape == (golden["fmx_x"].shape[0], main.shape[0])
+    mx, mean = O.parity_errors(y.float().cpu().numpy(), golden["fmx_y"])
+    assert mx <= TOL_MAX and mean <= TOL_MEAN
+    # graph_forward(linear_fn=...) hook with a bundle-shaped object
+    bundle = types.SimpleNamespace(linears={"down_proj": types.SimpleNamespace(main=main, comp=comp, act_cfg=None)})
+    fn = api.make_linear_fn(bundle)
+    mx, mean = O.parity_errors(fn("down_proj", golden["fmx_x"]), golden["fmx_y"])
+    assert mx <= TOL_MAX and mean <= TOL_MEAN
+
+
+@pytest.mark.gpu
+def test_symmetric_activation_composition_c1_style(gpu):
+    # BASELINE C1 composition: symmetric per-token INT4 activations, bf16 L
+    rng = np.random.default_rng(7)
+    x = O.bf16_round(O.synthetic_activations(96, 512, 5, 50.0, 7))
+    w = rng.standard_normal((512, 256)) * 0.02
+    main, comp = api.build_per_channel_int(w, np.arange(64), r_mode="dense")
+    y = api.forward_symmetric_act(x, main, comp, api.IntQuantConfig(4, True, "per-row"))
+    main_o, comp_o = O.build_per_channel_int(w, np.arange(64), r_mode="dense")
+    y_ref, _ = O.forward_int(x, main_o, comp_o, O.IntCfg(4, True, "per-row"), symmetric_act=True)
+    mx, mean = O.parity_errors(y, y_ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN
