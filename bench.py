@@ -282,7 +282,7 @@ def run_serq(args) -> None:
         prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof)).get("serq_mx_pair_kernel", {}).get("dram_bytes_per_launch")
+                traffic = json.load(open(prof)).get("serq_mx_pair3_kernel", {}).get("dram_bytes_per_launch")
             except (OSError, ValueError):
                 traffic = None
         line = {
@@ -297,7 +297,7 @@ def run_serq(args) -> None:
             "tokens_per_s": ws * M / (ms_per_step / 1e3),
             "tflops_pct_of_fp4_peak": 100.0 * value / FP4_PEAK_TFLOPS,
             "breakdown_ms": {"quantize": q_ms, "linear": g_ms},
-            "roofline": {"bound": "tensor", "kernel": "serq_linear_kernel<mx> (fused main + salient term + epilogue)",
+            "roofline": {"bound": "tensor", "kernel": "serq_mx_pair3_kernel (CTA-pair tcgen05 kind::mxf4, fused main + salient term + epilogue)",
                          "achieved": gemm_tflops, "peak": FP4_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": gemm_tflops / FP4_PEAK_TFLOPS,
                          "peak_source": "nominal dense FP4 9 PFLOP/s (B200_PROFILING.md; MEASURED_PEAKS.json has no FP4 figure)",

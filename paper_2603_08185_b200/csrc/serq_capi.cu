@@ -10,6 +10,7 @@
 #include "serq_gemm.cuh"
 #include "serq_gemm_mx.cuh"
 #include "serq_gemm_mx2.cuh"
+#include "serq_gemm_mx3.cuh"
 #include "serq_quant.cuh"
 
 using namespace serq;
@@ -130,6 +131,8 @@ struct serq_linear {
   int32_t* colsum_r = nullptr;
   CUtensorMap map_b, map_r;
   CUtensorMap map_b128, map_r128, map_sfw, map_sfr;  // CTA-pair kernel: 128-row B boxes, scale-factor maps
+  CUtensorMap map_r32, map_sfr4;                     // pair3 kernel: R as 32-B swizzled rows, 512-B SF boxes
+  bool has_r32 = false;
   // end-to-end scratch
   int64_t ws_m = 0;
   void* ws_x = nullptr;
@@ -333,6 +336,15 @@ int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K
     if (!rc) rc = make_map(&h->map_r128, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r / 2, N, r / 2, 128, 128);
     if (!rc) rc = make_sf_map(&h->map_sfr, h->sfr, N, r);
     if (rc) return bail(rc);
+    if (r == 64 && salient_contiguous) {
+      rc = make_map(&h->map_r32, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r / 2, N, r / 2, 32, 128,
+                    CU_TENSOR_MAP_SWIZZLE_32B);
+      if (!rc)
+        rc = make_map(&h->map_sfr4, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->sfr, 128, uint64_t(sf_bytes_of(N, r) / 128),
+                      128, 128, 4, CU_TENSOR_MAP_SWIZZLE_NONE);
+      if (rc) return bail(rc);
+      h->has_r32 = true;
+    }
   }
   *out = h;
   return SERQ_OK;
@@ -465,6 +477,29 @@ int serq_linear_mx(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t
   p.kc_pad_r = kc_pad_of(h->r > 0 ? h->r : 32);
   p.dbg = g_debug_flags;
   p.dbg_ts = g_debug_ts;
+  if (M > 128 && (h->r == 0 || h->has_r32) && !(g_debug_flags & (16 | 512))) {
+    static bool attr3 = false;
+    if (!attr3) {
+      CK(cudaFuncSetAttribute(serq_mx_pair3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k3SmemBytes));
+      attr3 = true;
+    }
+    Pair3Maps pm;
+    rc = make_map(&pm.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, 128);
+    if (!rc) rc = make_sf_map(&pm.sfa, a_sf, M, h->K);
+    if (!rc)
+      rc = make_map(&pm.y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, h->N, M, ldy * 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+    pm.b = h->map_b128;
+    pm.sfb = h->map_sfw;
+    pm.r = h->has_r32 ? h->map_r32 : h->map_b128;
+    pm.sfr = h->has_r32 ? h->map_sfr4 : h->map_sfw;
+    const int64_t pairs = cdiv(M, 256) * cdiv(h->N, kBN);
+    const int64_t max_pairs = sm_count() / 2;
+    const dim3 grid(unsigned(2 * (pairs < max_pairs ? pairs : max_pairs)));
+    serq_mx_pair3_kernel<<<grid, kThreads, k3SmemBytes, S(stream)>>>(pm, p);
+    LAUNCH_CHECK("serq_mx_pair3_kernel");
+    return SERQ_OK;
+  }
   if (M > 128 && !(g_debug_flags & 16)) {
     static bool attr2 = false;
     if (!attr2) {

@@ -72,6 +72,12 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
+// Relaxed arrive: orders nothing but the preceding tcgen05.fence::before_thread_sync,
+// which is all the TMEM hand-off needs (a release at cluster scope would wait for
+// the warp's in-flight TMA-store traffic: ~1000+ cycles measured).
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
 
 struct Pair2Maps {
   CUtensorMap a, b, xs, r, y, sfa, sfb, sfxs, sfr;
@@ -117,7 +123,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     mbar_init(&tmem_full[0], 1);
     mbar_init(&tmem_full[1], 1);
-    mbar_init(tmem_empty, 8);
+    mbar_init(tmem_empty, (p.dbg & 256) ? 4 : 8);  // dbg 256: timing only, leader epilogue alone
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -218,6 +224,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(tmem_empty, (i - 1) & 1);  // both epilogues drained the overlapping columns
           tc_fence_after();
         }
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && blockIdx.x == 0 && i < 8 && lane_id() == 0) p.dbg_ts[460 + i] = clock64();
+#endif
         for (int uu = 0; uu < units; ++uu) {
           const bool pair = uu < kpairs;
           const int len = unit_stages(uu);
@@ -339,8 +348,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int m_own = mt * 256 + int(rank) * 128;
       const int n0 = nt * kBN;
       const uint32_t b = i & 1;
+#ifdef SERQ_DIAG_TS
+      const bool est = p.dbg_ts && blockIdx.x == 0 && i < 8 && lane_id() == 0 && q == 0;
+      if (est) p.dbg_ts[420 + 4 * i] = clock64();
+#endif
       mbar_wait(&tmem_full[b], (i >> 1) & 1);
       tc_fence_after();
+#ifdef SERQ_DIAG_TS
+      if (est) p.dbg_ts[421 + 4 * i] = clock64();
+#endif
       const uint32_t acc = (b ? kAccB1 : 0u) + lane_base;
 #pragma unroll 1
       for (int cc = 0; cc < 4; ++cc) {
@@ -350,9 +366,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tmem_ld_32x32b_x32(acc + c * 64 + 32, w);
         tmem_ld_wait();
         if (cc == 0) {
+#ifdef SERQ_DIAG_TS
+          if (est) p.dbg_ts[422 + 4 * i] = clock64();
+#endif
           tc_fence_before();
           __syncwarp();
-          if (lane_id() == 0) mbar_arrive_cluster(tmem_empty_leader);
+          if (lane_id() == 0 && (leader || !(p.dbg & 256))) mbar_arrive_cluster_relaxed(tmem_empty_leader);
+#ifdef SERQ_DIAG_TS
+          if (est) p.dbg_ts[423 + 4 * i] = clock64();
+#endif
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {

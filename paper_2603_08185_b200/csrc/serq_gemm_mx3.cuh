@@ -1,0 +1,301 @@
+// serq_gemm_mx3.cuh -- MXFP4 SERQ linear, CTA pairs, two-K-step pipeline slots
+// and the salient term riding on K-step 0 (the production kernel for M > 128).
+//
+// Differences to serq_gemm_mx2.cuh (kept for the gather / large-r cases):
+//  * a pipeline SLOT holds two 256-K steps (8 MMAs of 256x256x64) behind ONE
+//    full and ONE empty barrier: the issuing thread pays one mbarrier wait and
+//    one commit per 8 MMAs (each try_wait costs ~145 cycles even when complete);
+//  * with the permuted salient layout the salient activation slice IS K-tile 0
+//    of X, so only R's B tile (128 rows x r/2 bytes per CTA, 32- or
+//    64-byte swizzle) and its scale factors are staged -- in a side buffer that
+//    completes on the same barrier as K-step 0 -- and r/64 MMAs follow K-step
+//    0's MMAs into the same accumulator.  No extra pipeline step, no second GEMM.
+#pragma once
+#include "serq_gemm_mx2.cuh"
+
+namespace serq {
+
+constexpr int k3Slots = 3;                    // 3 slots x 2 steps = 6 x 35 KB
+constexpr int k3StepBytes = k2StageBytes;     // one 256-K step per CTA: A 16K, B 16K, SFA 1K, SFB 2K
+constexpr int k3SlotBytes = 2 * k3StepBytes;  // 70 KB
+constexpr int k3RB = 128 * 32;                // R B tile (r <= 64: 32 B per row) per CTA
+constexpr int k3RSF = 1024;                   // R SFB: one chunk, both 128-row blocks
+constexpr int k3SmemBytes = 1024 + k3Slots * k3SlotBytes + k3RB + k3RSF + 4 * k2EpiStage + 256;
+static_assert(k3SmemBytes <= 232448, "exceeds the 227 KB dynamic shared memory limit");
+
+struct Pair3Maps {
+  CUtensorMap a, b, r, y, sfa, sfb, sfr;
+};
+
+__device__ __forceinline__ void tma_load_2d_pair_nohint(uint32_t dst, const CUtensorMap* m, uint32_t bar, int32_t c0,
+                                                        int32_t c1) {
+  tma_load_2d_pair(dst, m, bar, c0, c1, kEvictNormal);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    serq_mx_pair3_kernel(const __grid_constant__ Pair3Maps maps, const GemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* rbuf = smem + k3Slots * k3SlotBytes;  // R B tile (1 KB aligned) then R SFB
+  uint8_t* epi_smem = rbuf + k3RB + k3RSF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + 4 * k2EpiStage);
+  uint64_t* full = bars;                        // [k3Slots] leader's used
+  uint64_t* empty = bars + k3Slots;             // [k3Slots] both
+  uint64_t* tmem_full = bars + 2 * k3Slots;     // [2] both
+  uint64_t* tmem_empty = bars + 2 * k3Slots + 2;
+  uint64_t* r_empty = bars + 2 * k3Slots + 3;   // R side buffer consumed (both)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * k3Slots + 4);
+
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x >> 1;
+  const int n_clusters = gridDim.x >> 1;
+  const int tiles_m = (p.M + 255) / 256;
+  const int tiles_n = (p.N + kBN - 1) / kBN;
+  const int n_tiles = tiles_m * tiles_n;
+  const bool has_r = p.r > 0;
+  const int units = (p.k_steps + 1) >> 1;       // slots per tile (last one may hold a single step)
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&maps.a);
+    tma_prefetch(&maps.b);
+    tma_prefetch(&maps.y);
+    tma_prefetch(&maps.sfa);
+    tma_prefetch(&maps.sfb);
+    if (has_r) {
+      tma_prefetch(&maps.r);
+      tma_prefetch(&maps.sfr);
+    }
+    for (int s = 0; s < k3Slots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tmem_full[0], 1);
+    mbar_init(&tmem_full[1], 1);
+    mbar_init(tmem_empty, 8);
+    mbar_init(r_empty, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (threadIdx.x == 0 && *tmem_slot != 0) __trap();
+
+  const int my_tiles = cluster_id < n_tiles ? (n_tiles - 1 - cluster_id) / n_clusters + 1 : 0;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer (both CTAs)
+    if (elect_one()) {
+      const uint32_t smem_base = smem_u32(smem);
+      const uint32_t rb = smem_u32(rbuf);
+      uint32_t u = 0;  // global unit (slot use) counter
+      for (int i = 0; i < my_tiles; ++i) {
+        const int tile = cluster_id + i * n_clusters;
+        const int mt = tile % tiles_m, nt = tile / tiles_m;
+        const int m_own = mt * 256 + int(rank) * 128;
+        const int n0 = nt * kBN;
+        const int n_half = n0 + int(rank) * 128;
+        const int mblk = m_own / 128;
+        for (int uu = 0; uu < units; ++uu, ++u) {
+          const int slot = u % k3Slots;
+          mbar_wait(&empty[slot], ((u / k3Slots) & 1) ^ 1);
+          const int k0 = 2 * uu;
+          const int len = (k0 + 1 < p.k_steps) ? 2 : 1;
+          const bool with_r = has_r && uu == 0;
+          if (with_r && i > 0) mbar_wait(r_empty, (i - 1) & 1);  // previous tile's R MMAs are done
+          const uint32_t fbar = map_rank(smem_u32(&full[slot]), 0);
+          if (leader) mbar_expect_tx(&full[slot], 2u * (len * k3StepBytes + (with_r ? k3RB + k3RSF : 0)));
+          const uint32_t st = smem_base + slot * k3SlotBytes;
+          for (int h = 0; h < len; ++h) {
+            const uint32_t ss = st + h * k3StepBytes;
+            const int kk = k0 + h;
+            tma_load_2d_pair_nohint(ss, &maps.a, fbar, kk * kStepBytes, m_own);
+            tma_load_2d_pair_nohint(ss + k2SmemA, &maps.b, fbar, kk * kStepBytes, n_half);
+            tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB, &maps.sfa, fbar, 0, (mblk * p.kc_pad + 2 * kk) * 4);
+            tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB + k2SmemSFA, &maps.sfb, fbar, 0,
+                                    ((n0 / 128) * p.kc_pad + 2 * kk) * 4);
+            tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB + k2SmemSFA + 1024, &maps.sfb, fbar, 0,
+                                    ((n0 / 128 + 1) * p.kc_pad + 2 * kk) * 4);
+          }
+          if (with_r) {
+            tma_load_2d_pair_nohint(rb, &maps.r, fbar, 0, n_half);  // [128 rows x 32 B], 32B swizzle
+            // R SFB chunk 0 for both 128-row blocks: 512 B each = 4 rows of 128 B of the SF map
+            tma_load_2d_pair_nohint(rb + k3RB, &maps.sfr, fbar, 0, ((n0 / 128) * p.kc_pad_r) * 4);
+            tma_load_2d_pair_nohint(rb + k3RB + 512, &maps.sfr, fbar, 0, ((n0 / 128 + 1) * p.kc_pad_r) * 4);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
+    if (leader) {
+      const uint32_t smem_base = smem_u32(smem);
+      const uint32_t rb = smem_u32(rbuf);
+      constexpr uint32_t id0 = idesc_mxf4(256, kBN), id1 = id0 | (2u << 4) | (2u << 29);
+      constexpr uint32_t kSfR = kSfBase + 2 * kSfCols;  // R's SFB slot: 8 columns at 496
+      const uint32_t total = uint32_t(my_tiles) * units;
+      auto cps = [&](uint32_t st, uint32_t fa, uint32_t fb) {
+        const uint32_t sa = st + k2SmemA + k2SmemB, sb = sa + k2SmemSFA;
+        tmem_cp_pair(fa, make_sdesc(sa, 128, 128, 0));
+        tmem_cp_pair(fa + 4, make_sdesc(sa + 512, 128, 128, 0));
+        tmem_cp_pair(fb, make_sdesc(sb, 128, 128, 0));
+        tmem_cp_pair(fb + 4, make_sdesc(sb + 1024, 128, 128, 0));
+        tmem_cp_pair(fb + 8, make_sdesc(sb + 512, 128, 128, 0));
+        tmem_cp_pair(fb + 12, make_sdesc(sb + 1536, 128, 128, 0));
+      };
+      // 4 MMAs (K = 256) of one step
+      auto step4 = [&](uint32_t acc, uint64_t a, uint64_t b, uint32_t fa, uint32_t fb, uint32_t first, int n) {
+        mma_mxf4_pair(acc, a, b, id0, fa, fb, first);
+        mma_mxf4_pair(acc, a + 2, b + 2, id1, fa | (2u << 30), fb | (2u << 30), 1u);
+        mma_mxf4_pair(acc, a + 4, b + 4, id0, fa + 4, fb + 8, 1u);
+        if (n == 4) mma_mxf4_pair(acc, a + 6, b + 6, id1, (fa + 4) | (2u << 30), (fb + 8) | (2u << 30), 1u);
+      };
+      uint32_t u = 0;
+#ifdef SERQ_DIAG_TS
+      uint64_t gt0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+      const long long ck0 = clock64();
+#endif
+      if (total > 0) {
+        mbar_wait(&full[0], 0);
+        tc_fence_after();
+      }
+      for (int i = 0; i < my_tiles; ++i) {
+        const uint32_t acc = (i & 1) ? kAccB1 : 0u;
+        if (i > 0) {
+          mbar_wait(tmem_empty, (i - 1) & 1);  // both epilogues drained the overlapping columns
+          tc_fence_after();
+        }
+        for (int uu = 0; uu < units; ++uu, ++u) {
+          const int slot = u % k3Slots;
+          const int len = (2 * uu + 1 < p.k_steps) ? 2 : 1;
+          const bool with_r = has_r && uu == 0;
+          const uint32_t st0 = smem_base + slot * k3SlotBytes, st1 = st0 + k3StepBytes;
+          const uint64_t a0 = make_sdesc(st0, 16, 1024, 2), b0 = make_sdesc(st0 + k2SmemA, 16, 1024, 2);
+          const uint64_t a1 = make_sdesc(st1, 16, 1024, 2), b1 = make_sdesc(st1 + k2SmemA, 16, 1024, 2);
+          const uint32_t fa0 = kSfBase, fb0 = fa0 + 8, fa1 = kSfBase + kSfCols, fb1 = fa1 + 8;
+          const uint32_t first = uu > 0 ? 1u : 0u;
+#ifdef SERQ_DIAG_TS
+          const bool stamp = p.dbg_ts && blockIdx.x == 0 && u < 100 && lane_id() == 0;
+          if (stamp) p.dbg_ts[4 * u] = clock64();
+#endif
+          const bool no_mma = p.dbg & 1024;  // diagnostics: feed rate alone
+          if (elect_one() && !no_mma) {
+            cps(st0, fa0, fb0);
+            step4(acc, a0, b0, fa0, fb0, first, 4);
+            if (with_r) {
+              // salient term: A = K-tile 0 of X (same smem, same SFA slot), B = R (32-B rows, 32B swizzle)
+              tmem_cp_pair(kSfR, make_sdesc(rb + k3RB, 128, 128, 0));
+              tmem_cp_pair(kSfR + 4, make_sdesc(rb + k3RB + 512, 128, 128, 0));
+              mma_mxf4_pair(acc, a0, make_sdesc(rb, 16, 256, 6), id0, fa0, kSfR, 1u);  // r == 64: one K=64 slice
+              tc_commit_pair(r_empty);
+            }
+            if (len == 2) {
+              cps(st1, fa1, fb1);
+              step4(acc, a1, b1, fa1, fb1, 1u, 3);
+            }
+          }
+          __syncwarp();
+#ifdef SERQ_DIAG_TS
+          if (stamp) p.dbg_ts[4 * u + 1] = clock64();
+#endif
+          if (u + 1 < total) {  // look ahead while the pipe still holds this slot's MMAs
+            const uint32_t un = u + 1;
+            mbar_wait(&full[un % k3Slots], (un / k3Slots) & 1);
+            tc_fence_after();
+          }
+#ifdef SERQ_DIAG_TS
+          if (stamp) p.dbg_ts[4 * u + 2] = clock64();
+#endif
+          if (elect_one()) {
+            if (no_mma && with_r) tc_commit_pair(r_empty);
+            if (len == 2 && !no_mma)
+              mma_mxf4_pair(acc, a1 + 6, b1 + 6, id1, (fa1 + 4) | (2u << 30), (fb1 + 8) | (2u << 30), 1u);
+            tc_commit_pair(&empty[slot]);
+            if (uu == units - 1) tc_commit_pair(&tmem_full[i & 1]);
+          }
+          __syncwarp();
+#ifdef SERQ_DIAG_TS
+          if (stamp) p.dbg_ts[4 * u + 3] = clock64();
+#endif
+        }
+      }
+#ifdef SERQ_DIAG_TS
+      if (p.dbg_ts && blockIdx.x == 0 && lane_id() == 0) {
+        uint64_t gt1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
+        p.dbg_ts[508] = ck0;
+        p.dbg_ts[509] = clock64();
+        p.dbg_ts[510] = (long long)gt0;
+        p.dbg_ts[511] = (long long)gt1;
+      }
+#endif
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const uint32_t q = warp & 3;
+    const uint32_t lane_base = (q * 32u) << 16;
+    uint8_t* stage_out = epi_smem + q * k2EpiStage;
+    const uint32_t rbase = smem_u32(stage_out) + lane_id() * 64;
+    const uint32_t sw = (lane_id() >> 1) & 3;
+    const uint32_t tmem_empty_leader = map_rank(smem_u32(tmem_empty), 0);
+    for (int i = 0; i < my_tiles; ++i) {
+      const int tile = cluster_id + i * n_clusters;
+      const int mt = tile % tiles_m, nt = tile / tiles_m;
+      const int m_own = mt * 256 + int(rank) * 128;
+      const int n0 = nt * kBN;
+      const uint32_t b = i & 1;
+      mbar_wait(&tmem_full[b], (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t acc = (b ? kAccB1 : 0u) + lane_base;
+#pragma unroll 1
+      for (int cc = 0; cc < 4; ++cc) {
+        const int c = b ? cc : (cc + 3) & 3;
+        uint32_t v[32], w[32];
+        tmem_ld_32x32b_x32(acc + c * 64, v);
+        tmem_ld_32x32b_x32(acc + c * 64 + 32, w);
+        tmem_ld_wait();
+        if (cc == 0) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive_cluster_relaxed(tmem_empty_leader);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t* src = h ? w : v;
+          if (lane_id() == 0) bulk_wait_read_all();
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            st_shared_v4(rbase + ((uint32_t(j) ^ sw) * 16),
+                         pack_bf16x2(__uint_as_float(src[8 * j]), __uint_as_float(src[8 * j + 1])),
+                         pack_bf16x2(__uint_as_float(src[8 * j + 2]), __uint_as_float(src[8 * j + 3])),
+                         pack_bf16x2(__uint_as_float(src[8 * j + 4]), __uint_as_float(src[8 * j + 5])),
+                         pack_bf16x2(__uint_as_float(src[8 * j + 6]), __uint_as_float(src[8 * j + 7])));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane_id() == 0 && m_own < p.M) {
+            tma_store_2d(&maps.y, stage_out, n0 + c * 64 + h * 32, m_own + q * 32);
+            bulk_commit();
+          }
+        }
+      }
+    }
+    if (lane_id() == 0) bulk_wait_all();
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(0u));
+  }
+}
+
+}  // namespace serq

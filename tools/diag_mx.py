@@ -27,7 +27,12 @@ fl = 2.0 * M * N * (K + R)
 out = {}
 for flags in [int(f) for f in os.environ.get('FLAGS', '0,1,2,3').split(',')]:
     _lib.load().serq_set_debug_flags(flags)
-    t = timeit(lambda: lin.gemm(act, y))
+    gg = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(torch.cuda.Stream()):
+        lin.gemm(act, y); torch.cuda.synchronize()
+        with torch.cuda.graph(gg):
+            lin.gemm(act, y)
+    t = timeit(lambda: gg.replay())
     out[f"linear_dbg{flags}_us"] = t; out[f"linear_dbg{flags}_tflops"] = fl / t / 1e6
 qb = M * K * 2 + M * K // 2 + M * K // 32
 for qf in (0, 128):

@@ -29,5 +29,5 @@ for flags in [int(f) for f in os.environ.get("FLAGS", "0,15").split(",")]:
     t = full[:400].reshape(100, 4)
     d = np.diff(t, axis=1)
     print("unit: [issue part1, wait next, last mma+commit], gap to next unit")
-    for u in list(range(0, 12)) + list(range(16, 22)):
+    for u in range(0, 20):
         print(u, d[u].tolist(), int(t[u + 1, 0] - t[u, 3]))
