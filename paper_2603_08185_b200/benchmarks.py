@@ -1,0 +1,143 @@
+"""Secondary measurements reported beside the headline bench line (BASELINE
+configs other than C2): decode (C4), integer linears (C1, C3) and the
+Llama-70B-shaped block linears (C5, tp=1 on one GPU).
+
+Every measurement replays a CUDA graph of the hot path (quantize + fused
+linear) with the L2 flushed before each replay, timed with CUDA events on the
+launching stream.  Weights are synthetic N(0, 0.02) encoded on the device;
+activations follow the reference's outlier recipe (tensorio.py:157-168).
+"""
+
+from __future__ import annotations
+
+import statistics
+
+import numpy as np
+import torch
+
+from . import device as D
+
+
+class Flusher:
+    def __init__(self):
+        self.a = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+        self.b = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+
+    def __call__(self):
+        self.a.zero_()
+        self.b.sum()
+
+
+def graph_of(fn):
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            fn()
+    torch.cuda.synchronize()
+    return g
+
+
+def time_graph(g, flush: Flusher | None, n=20, warm=3):
+    ts = []
+    for i in range(n + warm):
+        if flush is not None:
+            flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        if i >= warm:
+            ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def device_mx_linear(K: int, N: int, r: int, seed: int = 1):
+    """Synthetic SERQ MX linear built on the device: W ~ N(0, 0.02) [K, N],
+    main_t = mx_encode(W^T), R = exact residual of the first r rows (the
+    salient rows after the offline permutation), encoded [N, r]."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    wt = torch.randn((N, K), generator=g, device="cuda", dtype=torch.float32) * 0.02
+    act = D.quantize_mx(wt)
+    codes, exps = D.unpack_mx(act.codes, act.sf, N, K)
+    if r:
+        mags = torch.tensor([0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0], device="cuda")
+        c = codes[:, :r].long()
+        dec = torch.where((c & 8) != 0, -1.0, 1.0) * mags[c & 7]
+        dec = dec * torch.exp2(exps[:, : r // 32].float()).repeat_interleave(32, dim=1)
+        resid = (wt[:, :r] - dec).contiguous()
+        ra = D.quantize_mx(resid)
+        rc, re_ = D.unpack_mx(ra.codes, ra.sf, N, r)
+    else:
+        rc = re_ = None
+    lin = D.MxLinear(codes, exps, rc, re_, np.arange(r) if r else None)
+    del wt
+    return lin
+
+
+def outlier_x(M: int, K: int, seed: int = 0, frac=0.01, mag=50.0) -> torch.Tensor:
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randn((M, K), generator=g, device="cuda")
+    n = max(1, int(round(frac * K)))
+    cols = torch.randperm(K, generator=g, device="cuda")[:n]
+    x[:, cols] *= mag
+    return x.to(torch.bfloat16)
+
+
+def mx_linear_point(lin, M: int, flush: Flusher) -> dict:
+    x = outlier_x(M, lin.K)
+    act = lin.quantize(x)
+    y = torch.empty((M, lin.N), dtype=torch.bfloat16, device="cuda")
+    g_step = graph_of(lambda: (lin.quantize(x, act), lin.gemm(act, y)))
+    g_lin = graph_of(lambda: lin.gemm(act, y))
+    t_step = time_graph(g_step, flush)
+    t_lin = time_graph(g_lin, flush)
+    K, N, r = lin.K, lin.N, lin.r
+    flops = 2.0 * M * N * (K + r)
+    w_bytes = N * K / 2 + N * K / 32 + N * r / 2 + N * r / 32
+    io_bytes = M * K / 2 + M * K / 32 + 2 * M * N
+    return {"M": M, "K": K, "N": N, "r": r, "step_us": t_step * 1e3, "linear_us": t_lin * 1e3,
+            "linear_tflops": flops / (t_lin * 1e-3) / 1e12, "step_tflops": flops / (t_step * 1e-3) / 1e12,
+            "linear_hbm_gbs": (w_bytes + io_bytes) / (t_lin * 1e-3) / 1e9, "tokens_per_s": M / (t_step * 1e-3)}
+
+
+def decode_points(hbm_peak_gbs: float, layers: int = 16) -> list:
+    """BASELINE C4 decode: Llama-2-7B up_proj (4096 x 11008) and down_proj
+    (11008 x 4096), M in {1, 4, 16}, r = 64.  Steady state: ONE graph runs the
+    step (quantize + linear) over ``layers`` distinct weight sets whose total
+    size (~390 MB) exceeds the 126 MB L2, so every layer streams its weights
+    from HBM; per-step time = graph time / layers."""
+    out = []
+    for K, N in ((4096, 11008), (11008, 4096)):
+        lins = [device_mx_linear(K, N, 64, seed=1 + i) for i in range(layers)]
+        for M in (1, 4, 16):
+            x = outlier_x(M, K)
+            acts = [lin.quantize(x) for lin in lins]
+            ys = [torch.empty((M, N), dtype=torch.bfloat16, device="cuda") for _ in lins]
+
+            def run_all():
+                for lin, a, y in zip(lins, acts, ys):
+                    lin.quantize(x, a)
+                    lin.gemm(a, y)
+
+            def lin_all():
+                for lin, a, y in zip(lins, acts, ys):
+                    lin.gemm(a, y)
+
+            t_step = time_graph(graph_of(run_all), None, n=10) / layers
+            t_lin = time_graph(graph_of(lin_all), None, n=10) / layers
+            r = 64
+            flops = 2.0 * M * N * (K + r)
+            w_bytes = N * K / 2 + N * K / 32 + N * r / 2 + N * r / 32
+            io_bytes = M * K / 2 + M * K / 32 + 2 * M * N
+            out.append({"M": M, "K": K, "N": N, "r": r, "layers_in_graph": layers, "step_us": t_step * 1e3,
+                        "linear_us": t_lin * 1e3, "linear_hbm_gbs": (w_bytes + io_bytes) / (t_lin * 1e-3) / 1e9,
+                        "linear_hbm_frac": (w_bytes + io_bytes) / (t_lin * 1e-3) / 1e9 / hbm_peak_gbs,
+                        "step_tflops": flops / (t_step * 1e-3) / 1e12, "tokens_per_s": M / (t_step * 1e-3)})
+        del lins
+        torch.cuda.empty_cache()
+    return out

@@ -11,6 +11,7 @@
 #include "serq_gemm_mx.cuh"
 #include "serq_gemm_mx2.cuh"
 #include "serq_gemm_mx3.cuh"
+#include "serq_gemm_decode.cuh"
 #include "serq_quant.cuh"
 
 using namespace serq;
@@ -120,7 +121,7 @@ int ensure_attr() {
 struct serq_linear {
   int mode = 0;  // kModeMX / kModeI8
   int64_t N = 0, K = 0;
-  int r = 0, r_mode = SERQ_R_NONE, w_bits = 4, contiguous = 1;
+  int r = 0, r_mode = SERQ_R_NONE, w_bits = 4, contiguous = 1, w_ksteps = 0;
   void* w = nullptr;        // MX packed [N, K/2] | INT s8 [N, K]
   uint8_t* sfw = nullptr;   // MX scale factors
   void* rbuf = nullptr;     // MX packed [N, r/2] | INT s8 [N, r] | bf16 [N, r]
@@ -133,6 +134,10 @@ struct serq_linear {
   CUtensorMap map_b128, map_r128, map_sfw, map_sfr;  // CTA-pair kernel: 128-row B boxes, scale-factor maps
   CUtensorMap map_r32, map_sfr4;                     // pair3 kernel: R as 32-B swizzled rows, 512-B SF boxes
   bool has_r32 = false;
+  // decode split-K workspace: fp32 partials + per-tile arrival counters
+  float* dec_ws = nullptr;
+  int64_t dec_ws_floats = 0;
+  int* dec_cnt = nullptr;
   // end-to-end scratch
   int64_t ws_m = 0;
   void* ws_x = nullptr;
@@ -144,7 +149,7 @@ struct serq_linear {
 namespace {
 void free_handle(serq_linear* h) {
   void* ptrs[] = {h->w, h->sfw, h->rbuf, h->sfr, h->sw, h->colsum, h->sr, h->colsum_r,
-                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y};
+                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y, h->dec_ws, h->dec_cnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete h;
@@ -313,14 +318,19 @@ int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K
     free_handle(h);
     return code;
   };
-  if (cudaMalloc(&h->w, N * K / 2) != cudaSuccess || cudaMalloc(&h->sfw, sf_bytes_of(N, K)) != cudaSuccess)
+  // weights pre-tiled [N/128][ksteps][128 rows x 128 B] (zero padded): each TMA box is one contiguous 16 KB
+  h->w_ksteps = int(cdiv(K / 2, kStepBytes));
+  const int64_t w_bytes = cdiv(N, 128) * h->w_ksteps * 128 * 128;
+  if (cudaMalloc(&h->w, w_bytes) != cudaSuccess || cudaMalloc(&h->sfw, sf_bytes_of(N, K)) != cudaSuccess)
     return bail(fail(SERQ_ECUDA, "cudaMalloc failed for MX weights"));
   if (cudaMemsetAsync(h->sfw, 0, sf_bytes_of(N, K), st) != cudaSuccess) return bail(fail(SERQ_ECUDA, "memset"));
+  if ((N % 128 || (K / 2) % kStepBytes) && cudaMemsetAsync(h->w, 0, w_bytes, st) != cudaSuccess)
+    return bail(fail(SERQ_ECUDA, "memset"));
   pack_mx_kernel<<<unsigned(cdiv(N * K / 8, 256)), 256, 0, st>>>(codes, exps, N, K, static_cast<uint8_t*>(h->w), h->sfw,
-                                                                  kc_pad_of(K));
+                                                                  kc_pad_of(K), h->w_ksteps);
   if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_mx launch failed"));
-  int rc = make_map(&h->map_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K / 2, N, K / 2, 128, kBN);
-  if (!rc) rc = make_map(&h->map_b128, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K / 2, N, K / 2, 128, 128);
+  int rc = make_map(&h->map_b128, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, 128, uint64_t(w_bytes / 128), 128, 128, 128);
+  h->map_b = h->map_b128;
   if (!rc) rc = make_sf_map(&h->map_sfw, h->sfw, N, K);
   if (rc) return bail(rc);
   h->map_r128 = h->map_b128;
@@ -330,7 +340,7 @@ int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K
       return bail(fail(SERQ_ECUDA, "cudaMalloc failed for R"));
     if (cudaMemsetAsync(h->sfr, 0, sf_bytes_of(N, r), st) != cudaSuccess) return bail(fail(SERQ_ECUDA, "memset"));
     pack_mx_kernel<<<unsigned(cdiv(N * r / 8, 256)), 256, 0, st>>>(r_codes, r_exps, N, r,
-                                                                    static_cast<uint8_t*>(h->rbuf), h->sfr, kc_pad_of(r));
+                                                                    static_cast<uint8_t*>(h->rbuf), h->sfr, kc_pad_of(r), 0);
     if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_mx launch failed"));
     rc = make_map(&h->map_r, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r / 2, N, r / 2, 128, kBN);
     if (!rc) rc = make_map(&h->map_r128, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r / 2, N, r / 2, 128, 128);
@@ -475,8 +485,79 @@ int serq_linear_mx(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t
   p.sfb_r = h->sfr;
   p.kc_pad = kc_pad_of(h->K);
   p.kc_pad_r = kc_pad_of(h->r > 0 ? h->r : 32);
+  p.w_ksteps = h->w_ksteps;
   p.dbg = g_debug_flags;
   p.dbg_ts = g_debug_ts;
+  if (M <= kDecN && (h->r == 0 || h->has_r32) && !(g_debug_flags & 2048)) {
+    static bool attrd = false;
+    if (!attrd) {
+      CK(cudaFuncSetAttribute(serq_mx_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem));
+      attrd = true;
+    }
+    serq_linear* hm = const_cast<serq_linear*>(h);
+    const int tiles = int(cdiv(h->N, 128));
+    const int ksteps = p.k_steps;
+    // one wave: at most two resident CTAs per SM (100 KB smem each)
+    int want = int((2 * sm_count()) / tiles);
+    want = want < 1 ? 1 : (want > ksteps ? ksteps : want);
+    int per = int(cdiv(ksteps, want));
+    int splits = int(cdiv(ksteps, per));
+    while (splits > 1 && int64_t(splits) * tiles > 2 * sm_count()) {
+      ++per;
+      splits = int(cdiv(ksteps, per));
+    }
+    if (splits > 1) {
+      const int64_t need = int64_t(splits) * tiles * 128 * kDecN;
+      if (need > hm->dec_ws_floats) {
+        if (hm->dec_ws) cudaFree(hm->dec_ws);
+        hm->dec_ws = nullptr;
+        CK(cudaMalloc(&hm->dec_ws, need * 4));
+        hm->dec_ws_floats = need;
+      }
+      if (!hm->dec_cnt) {
+        CK(cudaMalloc(&hm->dec_cnt, 4 * cdiv(h->N, 128) + 4096));
+        CK(cudaMemsetAsync(hm->dec_cnt, 0, 4 * cdiv(h->N, 128) + 4096, S(stream)));
+      }
+    }
+    DecodeMaps dm;
+    dm.w = h->map_b128;
+    rc = make_map(&dm.x, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, kDecN);
+    if (!rc) rc = make_sf_map(&dm.sfx, a_sf, M, h->K);
+    if (rc) return rc;
+    dm.sfw = h->map_sfw;
+    dm.r = h->has_r32 ? h->map_r32 : h->map_b128;
+    dm.sfr = h->has_r32 ? h->map_sfr4 : h->map_sfw;
+    DecodeParams dp{};
+    dp.M = int(M);
+    dp.N = int(h->N);
+    dp.K = int(h->K);
+    dp.r = h->r;
+    dp.k_steps = ksteps;
+    dp.splits = splits;
+    dp.kc_pad = p.kc_pad;
+    dp.kc_pad_r = p.kc_pad_r;
+    dp.w_ksteps = h->w_ksteps;
+    dp.dbg_ts = g_debug_ts;
+    dp.ws = hm->dec_ws;
+    dp.counters = hm->dec_cnt;
+    dp.y = static_cast<__nv_bfloat16*>(y);
+    dp.ldy = ldy;
+    // programmatic dependent launch: overlap this kernel's prologue and weight
+    // stream with the tail of the quantizer that produced a_codes / a_sf
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(tiles), unsigned(splits));
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = kDecSmem;
+    cfg.stream = S(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_kernel, dm, dp));
+    LAUNCH_CHECK("serq_mx_decode_kernel");
+    return SERQ_OK;
+  }
   if (M > 128 && (h->r == 0 || h->has_r32) && !(g_debug_flags & (16 | 512))) {
     static bool attr3 = false;
     if (!attr3) {

@@ -57,6 +57,7 @@ struct GemmParams {
   const uint8_t* sfa_r;  // SF of the salient activation slice (== sfa when contiguous)
   const uint8_t* sfb_r;  // SF of R
   int kc_pad;            // SF chunks per row block (A and B), even
+  int w_ksteps;          // MX weights are pre-tiled [N/128][w_ksteps][128 rows x 128 B]
   int kc_pad_r;          // SF chunks per row block for R and the salient slice
   int xs_is_x;           // salient slice = leading columns of X (no side buffer)
   // INT epilogue operands

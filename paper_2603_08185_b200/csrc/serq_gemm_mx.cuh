@@ -87,7 +87,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(&full[s], kStageBytes);
           if (!rstep) {
             tma_load_2d(st, &map_a, &full[s], kk * kStepBytes, m0, kEvictNormal);
-            tma_load_2d(st + kSmemA, &map_b, &full[s], kk * kStepBytes, n0, kEvictNormal);
+            tma_load_2d(st + kSmemA, &map_b, &full[s], 0, ((n0 >> 7) * p.w_ksteps + kk) * 128, kEvictNormal);
+            tma_load_2d(st + kSmemA + 128 * kStepBytes, &map_b, &full[s], 0, ((n0 >> 7) * p.w_ksteps + p.w_ksteps + kk) * 128,
+                        kEvictNormal);
           } else {
             tma_load_2d(st, p.xs_is_x ? &map_a : &map_xs, &full[s], kk * kStepBytes, m0, kEvictNormal);
             tma_load_2d(st + kSmemA, &map_r, &full[s], kk * kStepBytes, n0, kEvictNormal);

@@ -172,7 +172,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int kca = rstep && !p.xs_is_x ? p.kc_pad_r : p.kc_pad;
           const int kcb = rstep ? p.kc_pad_r : p.kc_pad;
           tma_load_2d_pair(st, ma, fbar, kk * kStepBytes, m_own, kEvictNormal);
-          tma_load_2d_pair(st + k2SmemA, mb, fbar, kk * kStepBytes, n_half, kEvictNormal);
+          if (rstep)
+            tma_load_2d_pair(st + k2SmemA, mb, fbar, kk * kStepBytes, n_half, kEvictNormal);
+          else
+            tma_load_2d_pair(st + k2SmemA, mb, fbar, 0, ((n_half >> 7) * p.w_ksteps + kk) * 128, kEvictNormal);
           // scale factors: 1 KB (8 rows of 128 B) per 128-row block and 256-K step
           tma_load_2d_pair(st + k2SmemA + k2SmemB, msa, fbar, 0, (mblk * kca + 2 * kk) * 4, kEvictNormal);
           tma_load_2d_pair(st + k2SmemA + k2SmemB + k2SmemSFA, msb, fbar, 0, ((n0 / 128) * kcb + 2 * kk) * 4,

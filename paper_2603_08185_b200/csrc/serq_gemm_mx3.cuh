@@ -115,7 +115,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t ss = st + h * k3StepBytes;
             const int kk = k0 + h;
             tma_load_2d_pair_nohint(ss, &maps.a, fbar, kk * kStepBytes, m_own);
-            tma_load_2d_pair_nohint(ss + k2SmemA, &maps.b, fbar, kk * kStepBytes, n_half);
+            tma_load_2d_pair_nohint(ss + k2SmemA, &maps.b, fbar, 0, ((n_half >> 7) * p.w_ksteps + kk) * 128);
             tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB, &maps.sfa, fbar, 0, (mblk * p.kc_pad + 2 * kk) * 4);
             tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB + k2SmemSFA, &maps.sfb, fbar, 0,
                                     ((n0 / 128) * p.kc_pad + 2 * kk) * 4);

@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(256) mx_encode_fast_kernel(const T* __restrict
   const int c8 = blockIdx.x * 256 + threadIdx.x;  // 8-element group within the row
   const int r0 = blockIdx.y * kMxRows;
   const bool col_ok = c8 < (K >> 3);
+  pdl_launch_dependents();  // the linear may start streaming its weights now
   if constexpr (In<T>::kId == 0) {
     const uint4* src = reinterpret_cast<const uint4*>(x + int64_t(r0) * ldx) + c8;
     const int64_t stride = ldx >> 3;
@@ -530,7 +531,8 @@ __global__ void __launch_bounds__(256) int_quant_bf16_kernel(const __nv_bfloat16
 // Reference MX artefacts (unpacked codes uint8 [rows, cols], exps int32 [rows, cols/32])
 // -> device packed codes + tiled E8M0.
 __global__ void pack_mx_kernel(const uint8_t* __restrict__ codes, const int32_t* __restrict__ exps, int64_t rows,
-                               int64_t cols, uint8_t* __restrict__ packed, uint8_t* __restrict__ sf, int kc_pad) {
+                               int64_t cols, uint8_t* __restrict__ packed, uint8_t* __restrict__ sf, int kc_pad,
+                               int tiled_ksteps) {
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t per_row = cols / 8;
   if (t >= rows * per_row) return;
@@ -538,7 +540,15 @@ __global__ void pack_mx_kernel(const uint8_t* __restrict__ codes, const int32_t*
   uint32_t p = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) p |= uint32_t(codes[row * cols + c0 + i] & 0xF) << (4 * i);
-  *reinterpret_cast<uint32_t*>(packed + row * (cols / 2) + c0 / 2) = p;
+  size_t off;
+  if (tiled_ksteps > 0) {
+    // pre-tiled weights: [row/128][byte/128][row%128][byte%128] -> every 16-KB TMA box is contiguous
+    const int64_t cb = c0 / 2;
+    off = ((size_t(row >> 7) * tiled_ksteps + size_t(cb >> 7)) * 128 + size_t(row & 127)) * 128 + size_t(cb & 127);
+  } else {
+    off = size_t(row) * (cols / 2) + c0 / 2;
+  }
+  *reinterpret_cast<uint32_t*>(packed + off) = p;
   if ((c0 & 31) == 0) sf[sf_offset(row, c0 / 32, kc_pad)] = uint8_t(exps[row * (cols / 32) + c0 / 32] + 127);
 }
 

@@ -223,3 +223,20 @@ def test_int_linear_gather_int_r(D):
     y_ref, _ = O.forward_int(x, main, comp, O.IntCfg(8, False, "per-row"))
     mx, mean = O.parity_errors(y, y_ref)
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+# ---------------------------------------------------------------- decode (M <= 16): swap-AB split-K kernel
+
+
+@pytest.mark.parametrize("M,K,N,r", [(1, 2048, 1536, 64), (4, 4096, 1024, 64), (16, 2048, 1000, 64),
+                                     (3, 1024, 512, 0), (16, 11008 // 32 * 32, 768, 64)])
+def test_mx_decode_parity(D, M, K, N, r):
+    x, main_t, comp = _mx_case(M, K, N, r, seed=K + M)
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents,
+                     comp.r_q.element_codes if r else None, comp.r_q.block_scale_exponents if r else None,
+                     np.arange(r) if r else None)
+    xt = _cuda(x, torch.bfloat16)
+    for _ in range(2):  # the second call reuses the self-resetting split-K counters
+        y = lin(xt).float().cpu().numpy()
+    mx, mean = O.parity_errors(y, O.forward_mx(x, main_t, comp))
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
