@@ -316,7 +316,63 @@ def run_serq(args) -> None:
         }
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_leg(wl.x, wl.w)
+        if ws == 1 and not args.no_extra:
+            line["other_configs"] = other_configs(hbm)
         print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def _round(d):
+    if isinstance(d, dict):
+        return {k: _round(v) for k, v in d.items()}
+    if isinstance(d, list):
+        return [_round(v) for v in d]
+    return round(d, 4) if isinstance(d, float) else d
+
+
+def other_configs(hbm_gbs: float) -> dict:
+    """The other BASELINE configs, measured the same way (CUDA-graph replays,
+    CUDA events); not the headline metric."""
+    from paper_2603_08185_b200 import benchmarks as B
+
+    fl = B.Flusher()
+    out = {}
+    try:
+        out["c1_int4_sym_dense_L"] = B.int_linear_point(512, 4096, 4096, 64, "dense", 4, True, fl)
+        out["c3_w4a8_asym_int_R"] = B.int_linear_point(2048, 4096, 11008, 128, "int", 8, False, fl)
+        out["c4_decode"] = B.decode_points(hbm_gbs)
+        out["c5_block_tp1"] = B.c5_block_point(1, 0, flush=fl)
+    except Exception as e:  # secondary numbers must not hide the headline line
+        out["error"] = f"{type(e).__name__}: {e}"
+    return _round(out)
+
+
+def run_c5(args) -> None:
+    """--workload c5: Llama-3-70B-shaped block linears, tensor parallel over
+    the launched ranks (NCCL all-reduce after o_proj and down_proj)."""
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    group = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2603_08185_b200 import benchmarks as B
+
+    p = B.c5_block_point(ws, rank, M=8192, steps=max(args.steps, 3), group=group)
+    t = torch.tensor([p["block_ms"]], device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({"metric": "SERQ W4A4 Llama-3-70B-shaped block linears tokens/s", "value": 8192 / (ms * 1e-3),
+                          "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": 2, "ms_per_step": ms,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                          "dtype": "fp4(e2m1)+e8m0 -> f32 -> bf16", "data": "synthetic",
+                          "config": {"workload": "c5 block linears tp", "parallelism": f"tp{ws}", **_round(p)}}))
     if ws > 1:
         torch.distributed.destroy_process_group()
 
@@ -328,9 +384,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="serq", choices=["serq", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other-config measurements")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5"])
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c5":
+        run_c5(args)
     else:
         run_serq(args)
 

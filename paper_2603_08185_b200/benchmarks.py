@@ -141,3 +141,104 @@ def decode_points(hbm_peak_gbs: float, layers: int = 16) -> list:
         del lins
         torch.cuda.empty_cache()
     return out
+
+
+def device_int_linear(K: int, N: int, r: int, r_mode: str, seed: int = 1):
+    """Synthetic per-output-channel INT4 SERQ linear (SURVEY F4 composition):
+    W ~ N(0, 0.02) [K, N]; main = per-column symmetric INT4; R = residual of
+    the first r rows, dense bf16 (``r_mode='dense'``) or INT4 with one scale
+    per output column (``'int'``)."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    w = torch.randn((K, N), generator=g, device="cuda", dtype=torch.float64) * 0.02
+    s = w.abs().amax(dim=0) / 7.0
+    s = torch.where(s == 0, torch.ones_like(s), s)
+    codes = torch.clamp(torch.round(w / s), -7, 7).to(torch.int32)
+    kw = {}
+    if r:
+        resid = w[:r] - codes[:r].double() * s
+        if r_mode == "dense":
+            kw = dict(r_dense=resid.to(torch.bfloat16).double(), salient_idx=np.arange(r))
+        else:
+            sr = resid.abs().amax(dim=0) / 7.0
+            sr = torch.where(sr == 0, torch.ones_like(sr), sr)
+            kw = dict(r_codes=torch.clamp(torch.round(resid / sr), -7, 7).to(torch.int32), r_scales=sr,
+                      salient_idx=np.arange(r))
+    return D.IntLinear(codes, s, 4, **kw)
+
+
+def int_linear_point(M, K, N, r, r_mode, bits, symmetric, flush: Flusher) -> dict:
+    lin = device_int_linear(K, N, r, r_mode)
+    x = outlier_x(M, K)
+    act = lin.quantize(x, bits, symmetric)
+    y = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    g_step = graph_of(lambda: lin.gemm(lin.quantize(x, bits, symmetric), y))
+    g_lin = graph_of(lambda: lin.gemm(act, y))
+    t_step = time_graph(g_step, flush)
+    t_lin = time_graph(g_lin, flush)
+    flops = 2.0 * M * N * (K + r)
+    return {"M": M, "K": K, "N": N, "r": r, "r_mode": r_mode, "act_bits": bits, "act_symmetric": symmetric,
+            "step_us": t_step * 1e3, "linear_us": t_lin * 1e3, "linear_tops": flops / (t_lin * 1e-3) / 1e12,
+            "step_tops": flops / (t_step * 1e-3) / 1e12, "tokens_per_s": M / (t_step * 1e-3)}
+
+
+def c5_block_point(world: int = 1, rank: int = 0, M: int = 8192, r: int = 128, group=None, steps: int = 5,
+                   flush: Flusher | None = None) -> dict:
+    """BASELINE C5: Llama-3-70B-shaped decoder-block linears (hidden 8192,
+    FFN 28672, GQA kv 1024), SERQ W4A4 MXFP4, M tokens, tensor parallel over
+    ``world`` ranks with one all-reduce after o_proj and after down_proj
+    (tp.TPBlockLinears).  q/k/v and gate/up are fused (one salient plan each);
+    row-parallel layers hold salient_per_rank(r) channels per rank.  The
+    attention output and SiLU(gate)*up feeding o/down are synthetic tensors of
+    the right shape (non-linear ops are out of scope for this path)."""
+    from . import tp
+
+    specs = tp.block_specs(8192, 28672, 1024)
+    lins, feeds, acts = {}, {}, {}
+    for spec in specs:
+        if spec.kind == "column":
+            n0, n1 = tp.column_shard(spec.n, world, rank)
+            lins[spec.name] = device_mx_linear(spec.k, n1 - n0, r, seed=hash(spec.name) % 1000)
+        else:
+            k0, k1 = tp.row_shard(spec.k, world, rank)
+            lins[spec.name] = device_mx_linear(k1 - k0, spec.n, tp.salient_per_rank(r, world),
+                                               seed=hash(spec.name) % 1000)
+            feeds[spec.name] = outlier_x(M, k1 - k0, seed=7)
+    x = outlier_x(M, 8192, seed=3)
+    outs = {s.name: torch.empty((M, lins[s.name].N), dtype=torch.bfloat16, device="cuda") for s in specs}
+
+    def run_linear(name):
+        def f(xin):
+            lin = lins[name]
+            a = acts.get(name)
+            acts[name] = lin.quantize(xin, a)
+            return lin.gemm(acts[name], outs[name])
+        return f
+
+    drv = tp.TPBlockLinears(specs, {s.name: run_linear(s.name) for s in specs}, world, rank, group)
+
+    def step():
+        drv.forward(x, feeds)
+
+    step()
+    torch.cuda.synchronize()
+    use_graph = world == 1  # NCCL collectives are kept outside graphs here
+    g = graph_of(step) if use_graph else None
+    ts = []
+    for i in range(steps + 2):
+        if flush is not None:
+            flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay() if use_graph else step()
+        b.record()
+        b.synchronize()
+        if i >= 2:
+            ts.append(a.elapsed_time(b))
+    t = statistics.median(ts)
+    flops = 0.0
+    for s in specs:
+        lin = lins[s.name]
+        flops += 2.0 * M * lin.N * (lin.K + lin.r)
+    return {"M": M, "tp": world, "r": r, "block_ms": t, "tokens_per_s": M / (t * 1e-3),
+            "rank_tflops": flops / (t * 1e-3) / 1e12, "graph": use_graph,
+            "linears": {s.name: [lins[s.name].K, lins[s.name].N, lins[s.name].r] for s in specs}}
