@@ -134,6 +134,11 @@ struct serq_linear {
   CUtensorMap map_b128, map_r128, map_sfw, map_sfr;  // CTA-pair kernel: 128-row B boxes, scale-factor maps
   CUtensorMap map_r32, map_sfr4;                     // pair3 kernel: R as 32-B swizzled rows, 512-B SF boxes
   bool has_r32 = false;
+  // CTA-pair split last wave: fp32 partials + per-(tile, rank) counters
+  float* sk_ws = nullptr;
+  int64_t sk_ws_floats = 0;
+  int* sk_cnt = nullptr;
+  int64_t sk_cnt_n = 0;
   // decode split-K workspace: fp32 partials + per-tile arrival counters
   float* dec_ws = nullptr;
   int64_t dec_ws_floats = 0;
@@ -149,7 +154,7 @@ struct serq_linear {
 namespace {
 void free_handle(serq_linear* h) {
   void* ptrs[] = {h->w, h->sfw, h->rbuf, h->sfr, h->sw, h->colsum, h->sr, h->colsum_r,
-                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y, h->dec_ws, h->dec_cnt};
+                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y, h->dec_ws, h->dec_cnt, h->sk_ws, h->sk_cnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete h;
@@ -209,20 +214,7 @@ int serq_act_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ld
   if (gather_idx && (M % 128 || r % 256)) CK(cudaMemsetAsync(xs_sf, 0, sf_bytes_of(M, r), st));
   if (dtype != SERQ_F64) {
     const dim3 grid(unsigned(cdiv(K / 8, 256)), unsigned(cdiv(M, kMxRows)));
-    if (dtype == SERQ_BF16 && (g_debug_flags & 32))
-      mx_encode_fast_kernel<__nv_bfloat16, 2><<<dim3(grid.x, unsigned(cdiv(M, 2))), 256, 0, st>>>(
-          static_cast<const __nv_bfloat16*>(x), int(M), int(K), ldx, codes, sf, kc);
-    else if (dtype == SERQ_BF16 && (g_debug_flags & 64))
-      mx_encode_fast_kernel<__nv_bfloat16, 8><<<dim3(grid.x, unsigned(cdiv(M, 8))), 256, 0, st>>>(
-          static_cast<const __nv_bfloat16*>(x), int(M), int(K), ldx, codes, sf, kc);
-    else if (dtype == SERQ_BF16 && (g_debug_flags & 128)) {
-      // grid-stride: ~8 resident blocks of 256 threads per SM
-      const int64_t want = int64_t(sm_count()) * 8 / grid.x;
-      const int64_t groups = cdiv(M, 4);
-      mx_encode_bf16_stride_kernel<<<dim3(grid.x, unsigned(want < groups ? (want > 0 ? want : 1) : groups)), 256, 0,
-                                     st>>>(static_cast<const __nv_bfloat16*>(x), int(M), int(K), ldx, codes, sf, kc);
-    }
-    else if (dtype == SERQ_BF16)
+    if (dtype == SERQ_BF16)
       mx_encode_fast_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), int(M), int(K),
                                                                  ldx, codes, sf, kc);
     else
@@ -576,8 +568,48 @@ int serq_linear_mx(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t
     pm.sfr = h->has_r32 ? h->map_sfr4 : h->map_sfw;
     const int64_t pairs = cdiv(M, 256) * cdiv(h->N, kBN);
     const int64_t max_pairs = sm_count() / 2;
-    const dim3 grid(unsigned(2 * (pairs < max_pairs ? pairs : max_pairs)));
-    serq_mx_pair3_kernel<<<grid, kThreads, k3SmemBytes, S(stream)>>>(pm, p);
+    const int64_t clusters = pairs < max_pairs ? pairs : max_pairs;
+    // split the last partial wave into K-halves when they fit in one round
+    const int64_t rounds = pairs / clusters, left = pairs - rounds * clusters;
+    p.split_from = int(pairs);
+    p.y = static_cast<__nv_bfloat16*>(y);
+    p.ldy = ldy;
+    // opt-in (debug flag 8192): measured slower than 4 full rounds for 4096^3 (partner flag + partial traffic)
+    if (left > 0 && 2 * left <= clusters && p.k_steps >= 4 && (g_debug_flags & 8192)) {
+      serq_linear* hm = const_cast<serq_linear*>(h);
+      const int64_t need = left * 2 * 2 * 128 * kBN;
+      if (need > hm->sk_ws_floats) {
+        if (hm->sk_ws) cudaFree(hm->sk_ws);
+        hm->sk_ws = nullptr;
+        CK(cudaMalloc(&hm->sk_ws, need * 4));
+        hm->sk_ws_floats = need;
+      }
+      if (left * 4 > hm->sk_cnt_n) {  // counters [left][2] then ready flags [left][2]
+        if (hm->sk_cnt) cudaFree(hm->sk_cnt);
+        hm->sk_cnt = nullptr;
+        CK(cudaMalloc(&hm->sk_cnt, left * 4 * 4));
+        CK(cudaMemsetAsync(hm->sk_cnt, 0, left * 4 * 4, S(stream)));
+        hm->sk_cnt_n = left * 4;
+      }
+      rc = make_map(&pm.ws, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, hm->sk_ws, kBN, uint64_t(left * 4 * 128), kBN * 4, 32, 32,
+                    CU_TENSOR_MAP_SWIZZLE_128B);
+      if (rc) return rc;
+      p.split_from = int(rounds * clusters);
+      p.sk_ws = hm->sk_ws;
+      p.sk_cnt = hm->sk_cnt;
+    }
+    if (p.split_from >= int(pairs)) pm.ws = pm.y;  // unused
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(2 * clusters));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = k3SmemBytes;
+    cfg.stream = S(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap with the quantizer's tail
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, serq_mx_pair3_kernel, pm, p));
     LAUNCH_CHECK("serq_mx_pair3_kernel");
     return SERQ_OK;
   }

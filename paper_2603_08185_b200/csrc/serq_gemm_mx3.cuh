@@ -20,11 +20,12 @@ constexpr int k3StepBytes = k2StageBytes;     // one 256-K step per CTA: A 16K, 
 constexpr int k3SlotBytes = 2 * k3StepBytes;  // 70 KB
 constexpr int k3RB = 128 * 32;                // R B tile (r <= 64: 32 B per row) per CTA
 constexpr int k3RSF = 1024;                   // R SFB: one chunk, both 128-row blocks
-constexpr int k3SmemBytes = 1024 + k3Slots * k3SlotBytes + k3RB + k3RSF + 4 * k2EpiStage + 256;
+constexpr int k3SmemBytes = 1024 + k3Slots * k3SlotBytes + k3RB + k3RSF + 4 * k2EpiStage + 512;
 static_assert(k3SmemBytes <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 
 struct Pair3Maps {
   CUtensorMap a, b, r, y, sfa, sfb, sfr;
+  CUtensorMap ws;  // split-wave fp32 partials [slabs x 128 rows][256], box 32 x 32, 128B swizzle
 };
 
 __device__ __forceinline__ void tma_load_2d_pair_nohint(uint32_t dst, const CUtensorMap* m, uint32_t bar, int32_t c0,
@@ -44,7 +45,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tmem_full = bars + 2 * k3Slots;     // [2] both
   uint64_t* tmem_empty = bars + 2 * k3Slots + 2;
   uint64_t* r_empty = bars + 2 * k3Slots + 3;   // R side buffer consumed (both)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * k3Slots + 4);
+  uint64_t* ws_bar = bars + 2 * k3Slots + 4;    // [4] per epilogue warp: partner partial landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * k3Slots + 8);
 
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t rank = cluster_rank();
@@ -56,6 +58,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int n_tiles = tiles_m * tiles_n;
   const bool has_r = p.r > 0;
   const int units = (p.k_steps + 1) >> 1;       // slots per tile (last one may hold a single step)
+  // work items: tiles [0, split_from) whole, then every remaining tile as two K-halves
+  const int split_from = min(p.split_from, n_tiles);
+  const int n_items = split_from + 2 * (n_tiles - split_from);
+  const int half_units = units >> 1;
+  struct Item {
+    int tile, half, lo, hi;  // half: -1 = whole tile; [lo, hi) = k-unit range
+  };
+  auto item_of = [&](int w) {
+    Item it;
+    if (w < split_from) {
+      it.tile = w;
+      it.half = -1;
+      it.lo = 0;
+      it.hi = units;
+    } else {
+      const int j = w - split_from;
+      it.tile = split_from + (j >> 1);
+      it.half = j & 1;
+      it.lo = it.half ? half_units : 0;
+      it.hi = it.half ? units : half_units;
+    }
+    return it;
+  };
 
   if (warp == 0 && elect_one()) {
     tma_prefetch(&maps.a);
@@ -75,6 +100,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     mbar_init(&tmem_full[1], 1);
     mbar_init(tmem_empty, 8);
     mbar_init(r_empty, 1);
+    for (int w = 0; w < 4; ++w) mbar_init(&ws_bar[w], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -86,7 +112,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   if (threadIdx.x == 0 && *tmem_slot != 0) __trap();
 
-  const int my_tiles = cluster_id < n_tiles ? (n_tiles - 1 - cluster_id) / n_clusters + 1 : 0;
+  const int my_tiles = cluster_id < n_items ? (n_items - 1 - cluster_id) / n_clusters + 1 : 0;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer (both CTAs)
@@ -94,33 +120,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t smem_base = smem_u32(smem);
       const uint32_t rb = smem_u32(rbuf);
       uint32_t u = 0;  // global unit (slot use) counter
+      int r_uses = 0;
       for (int i = 0; i < my_tiles; ++i) {
-        const int tile = cluster_id + i * n_clusters;
+        const Item itm = item_of(cluster_id + i * n_clusters);
+        const int tile = (p.dbg & 16384) ? 0 : itm.tile;  // diagnostics: every cluster streams tile 0
         const int mt = tile % tiles_m, nt = tile / tiles_m;
         const int m_own = mt * 256 + int(rank) * 128;
         const int n0 = nt * kBN;
         const int n_half = n0 + int(rank) * 128;
         const int mblk = m_own / 128;
-        for (int uu = 0; uu < units; ++uu, ++u) {
+        for (int uu = itm.lo; uu < itm.hi; ++uu, ++u) {
           const int slot = u % k3Slots;
           mbar_wait(&empty[slot], ((u / k3Slots) & 1) ^ 1);
           const int k0 = 2 * uu;
           const int len = (k0 + 1 < p.k_steps) ? 2 : 1;
           const bool with_r = has_r && uu == 0;
-          if (with_r && i > 0) mbar_wait(r_empty, (i - 1) & 1);  // previous tile's R MMAs are done
+          if (with_r && r_uses > 0) mbar_wait(r_empty, (r_uses - 1) & 1);  // previous R MMAs are done
+          if (with_r) ++r_uses;
           const uint32_t fbar = map_rank(smem_u32(&full[slot]), 0);
           if (leader) mbar_expect_tx(&full[slot], 2u * (len * k3StepBytes + (with_r ? k3RB + k3RSF : 0)));
           const uint32_t st = smem_base + slot * k3SlotBytes;
+          // weights (B, SFB) never depend on the previous kernel: load them first
           for (int h = 0; h < len; ++h) {
             const uint32_t ss = st + h * k3StepBytes;
             const int kk = k0 + h;
-            tma_load_2d_pair_nohint(ss, &maps.a, fbar, kk * kStepBytes, m_own);
             tma_load_2d_pair_nohint(ss + k2SmemA, &maps.b, fbar, 0, ((n_half >> 7) * p.w_ksteps + kk) * 128);
-            tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB, &maps.sfa, fbar, 0, (mblk * p.kc_pad + 2 * kk) * 4);
             tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB + k2SmemSFA, &maps.sfb, fbar, 0,
                                     ((n0 / 128) * p.kc_pad + 2 * kk) * 4);
             tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB + k2SmemSFA + 1024, &maps.sfb, fbar, 0,
                                     ((n0 / 128 + 1) * p.kc_pad + 2 * kk) * 4);
+          }
+          if (u == 0) pdl_wait();  // activations come from the quantizer launched just before
+          for (int h = 0; h < len; ++h) {
+            const uint32_t ss = st + h * k3StepBytes;
+            const int kk = k0 + h;
+            tma_load_2d_pair_nohint(ss, &maps.a, fbar, kk * kStepBytes, m_own);
+            tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB, &maps.sfa, fbar, 0, (mblk * p.kc_pad + 2 * kk) * 4);
           }
           if (with_r) {
             tma_load_2d_pair_nohint(rb, &maps.r, fbar, 0, n_half);  // [128 rows x 32 B], 32B swizzle
@@ -138,7 +173,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t rb = smem_u32(rbuf);
       constexpr uint32_t id0 = idesc_mxf4(256, kBN), id1 = id0 | (2u << 4) | (2u << 29);
       constexpr uint32_t kSfR = kSfBase + 2 * kSfCols;  // R's SFB slot: 8 columns at 496
-      const uint32_t total = uint32_t(my_tiles) * units;
+      uint32_t total = 0;
+      for (int i = 0; i < my_tiles; ++i) {
+        const Item itm = item_of(cluster_id + i * n_clusters);
+        total += uint32_t(itm.hi - itm.lo);
+      }
       auto cps = [&](uint32_t st, uint32_t fa, uint32_t fb) {
         const uint32_t sa = st + k2SmemA + k2SmemB, sb = sa + k2SmemSFA;
         tmem_cp_pair(fa, make_sdesc(sa, 128, 128, 0));
@@ -171,7 +210,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(tmem_empty, (i - 1) & 1);  // both epilogues drained the overlapping columns
           tc_fence_after();
         }
-        for (int uu = 0; uu < units; ++uu, ++u) {
+        const Item itm = item_of(cluster_id + i * n_clusters);
+        for (int uu = itm.lo; uu < itm.hi; ++uu, ++u) {
           const int slot = u % k3Slots;
           const int len = (2 * uu + 1 < p.k_steps) ? 2 : 1;
           const bool with_r = has_r && uu == 0;
@@ -179,7 +219,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint64_t a0 = make_sdesc(st0, 16, 1024, 2), b0 = make_sdesc(st0 + k2SmemA, 16, 1024, 2);
           const uint64_t a1 = make_sdesc(st1, 16, 1024, 2), b1 = make_sdesc(st1 + k2SmemA, 16, 1024, 2);
           const uint32_t fa0 = kSfBase, fb0 = fa0 + 8, fa1 = kSfBase + kSfCols, fb1 = fa1 + 8;
-          const uint32_t first = uu > 0 ? 1u : 0u;
+          const uint32_t first = uu > itm.lo ? 1u : 0u;
 #ifdef SERQ_DIAG_TS
           const bool stamp = p.dbg_ts && blockIdx.x == 0 && u < 100 && lane_id() == 0;
           if (stamp) p.dbg_ts[4 * u] = clock64();
@@ -217,7 +257,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (len == 2 && !no_mma)
               mma_mxf4_pair(acc, a1 + 6, b1 + 6, id1, (fa1 + 4) | (2u << 30), (fb1 + 8) | (2u << 30), 1u);
             tc_commit_pair(&empty[slot]);
-            if (uu == units - 1) tc_commit_pair(&tmem_full[i & 1]);
+            if (uu == itm.hi - 1) tc_commit_pair(&tmem_full[i & 1]);
           }
           __syncwarp();
 #ifdef SERQ_DIAG_TS
@@ -244,15 +284,139 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t rbase = smem_u32(stage_out) + lane_id() * 64;
     const uint32_t sw = (lane_id() >> 1) & 3;
     const uint32_t tmem_empty_leader = map_rank(smem_u32(tmem_empty), 0);
+    pdl_wait();
+    pdl_launch_dependents();
+    __shared__ int s_second;
     for (int i = 0; i < my_tiles; ++i) {
-      const int tile = cluster_id + i * n_clusters;
+      const Item itm = item_of(cluster_id + i * n_clusters);
+      const int tile = itm.tile;
       const int mt = tile % tiles_m, nt = tile / tiles_m;
       const int m_own = mt * 256 + int(rank) * 128;
       const int n0 = nt * kBN;
       const uint32_t b = i & 1;
+#ifdef SERQ_DIAG_TS
+      const bool est = p.dbg_ts && q == 0 && lane_id() == 0 && i < 4;
+      long long* ep = p.dbg_ts + 256 + (blockIdx.x * 4 + i) * 6 % 240;
+      if (est) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); ep[0] = (long long)g; }
+#endif
       mbar_wait(&tmem_full[b], (i >> 1) & 1);
       tc_fence_after();
+#ifdef SERQ_DIAG_TS
+      if (est) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); ep[1] = (long long)g; ep[5] = itm.half; }
+#endif
       const uint32_t acc = (b ? kAccB1 : 0u) + lane_base;
+      if (itm.half >= 0) {
+        // ---- split tile (always in the last round: the pipeline smem is free).
+        // The first finisher TMA-stores its fp32 partial and raises a flag; the
+        // second waits for the flag, TMA-loads the partner's partial chunk by
+        // chunk, adds its own accumulator and stores bf16.  a + b == b + a in
+        // fp32, so the result does not depend on which half finishes first.
+        const int st_idx = tile - split_from;
+        uint8_t* wbuf = smem + q * 16384;  // 4 x 4-KB 128B-swizzled fp32 boxes (32 rows x 32 cols)
+        const uint32_t wb = smem_u32(wbuf);
+        const uint32_t rowb = wb + lane_id() * 128;
+        const uint32_t swz = lane_id() & 7;
+        const int slab_row = ((st_idx * 2) * 2 + int(rank)) * 128 + q * 32;  // + half * 256 rows
+        if (q == 0 && lane_id() == 0) s_second = atomicAdd(&p.sk_cnt[st_idx * 2 + rank], 1);
+        named_bar_sync(1, 128);
+        const bool second = s_second == 1;
+        named_bar_sync(1, 128);
+        int* flag = p.sk_cnt + (n_tiles - split_from) * 2 + st_idx * 2 + rank;  // flags follow the counters
+        if (second && lane_id() == 0) {
+          while (ld_acquire_gpu(flag) == 0) {
+          }
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int cc = 0; cc < 4; ++cc) {
+          const int c = b ? cc : (cc + 3) & 3;
+          uint32_t v[32], w[32];
+          tmem_ld_32x32b_x32(acc + c * 64, v);
+          tmem_ld_32x32b_x32(acc + c * 64 + 32, w);
+          tmem_ld_wait();
+          if (cc == 0) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive_cluster_relaxed(tmem_empty_leader);
+          }
+          if (!second) {
+            if (lane_id() == 0) bulk_wait_read_all();
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t* src = h ? w : v;
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                st_shared_v4(rowb + h * 4096 + ((uint32_t(j) ^ swz) * 16), src[4 * j], src[4 * j + 1], src[4 * j + 2],
+                             src[4 * j + 3]);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane_id() == 0) {
+              tma_store_2d(&maps.ws, wbuf, c * 64, slab_row + itm.half * 256);
+              tma_store_2d(&maps.ws, wbuf + 4096, c * 64 + 32, slab_row + itm.half * 256);
+              bulk_commit();
+            }
+          } else {
+            // partner's partial for this chunk -> smem, add, bf16, TMA store
+            if (lane_id() == 0) {
+              bulk_wait_read_all();
+              mbar_expect_tx(&ws_bar[q], 8192);
+              tma_load_2d(wbuf, &maps.ws, &ws_bar[q], c * 64, slab_row + (itm.half ^ 1) * 256, kEvictFirst);
+              tma_load_2d(wbuf + 4096, &maps.ws, &ws_bar[q], c * 64 + 32, slab_row + (itm.half ^ 1) * 256, kEvictFirst);
+            }
+            mbar_wait(&ws_bar[q], cc & 1);
+            float f[64];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 o = *reinterpret_cast<const float4*>(wbuf + h * 4096 + lane_id() * 128 + ((j ^ swz) * 16));
+                const uint32_t* src = h ? w : v;
+                f[h * 32 + 4 * j] = __uint_as_float(src[4 * j]) + o.x;
+                f[h * 32 + 4 * j + 1] = __uint_as_float(src[4 * j + 1]) + o.y;
+                f[h * 32 + 4 * j + 2] = __uint_as_float(src[4 * j + 2]) + o.z;
+                f[h * 32 + 4 * j + 3] = __uint_as_float(src[4 * j + 3]) + o.w;
+              }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (lane_id() == 0) bulk_wait_read_all();
+              __syncwarp();
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                st_shared_v4(rbase + ((uint32_t(j) ^ sw) * 16), pack_bf16x2(f[h * 32 + 8 * j], f[h * 32 + 8 * j + 1]),
+                             pack_bf16x2(f[h * 32 + 8 * j + 2], f[h * 32 + 8 * j + 3]),
+                             pack_bf16x2(f[h * 32 + 8 * j + 4], f[h * 32 + 8 * j + 5]),
+                             pack_bf16x2(f[h * 32 + 8 * j + 6], f[h * 32 + 8 * j + 7]));
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane_id() == 0 && m_own < p.M) {
+                tma_store_2d(&maps.y, stage_out, n0 + c * 64 + h * 32, m_own + q * 32);
+                bulk_commit();
+              }
+            }
+            __syncwarp();
+          }
+        }
+        if (!second) {
+          // partial globally visible -> raise the flag for the partner CTA
+          if (lane_id() == 0) bulk_wait_all();
+          fence_proxy_async_global();
+          named_bar_sync(1, 128);
+          if (q == 0 && lane_id() == 0) {
+            __threadfence();
+            st_release_gpu(flag, 1);
+          }
+        } else {
+          named_bar_sync(1, 128);
+          if (q == 0 && lane_id() == 0) {
+            p.sk_cnt[st_idx * 2 + rank] = 0;  // ready for the next launch
+            *flag = 0;
+          }
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int cc = 0; cc < 4; ++cc) {
         const int c = b ? cc : (cc + 3) & 3;

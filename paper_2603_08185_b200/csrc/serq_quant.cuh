@@ -263,58 +263,6 @@ __global__ void __launch_bounds__(256) mx_encode_fast_kernel(const T* __restrict
   }
 }
 
-// Grid-stride variant for bf16: blockIdx.y strides over 4-row groups and the loads
-// of the next group are issued before the current group is converted (register
-// double buffering), so every thread keeps 8 x 16 B in flight across iterations.
-__global__ void __launch_bounds__(256) mx_encode_bf16_stride_kernel(const __nv_bfloat16* __restrict__ x, int M, int K,
-                                                                    int64_t ldx, uint8_t* __restrict__ codes,
-                                                                    uint8_t* __restrict__ sf, int kc_pad) {
-  constexpr int R = 4;
-  const int c8 = blockIdx.x * 256 + threadIdx.x;
-  const bool col_ok = c8 < (K >> 3);
-  const int n_groups = (M + R - 1) / R;
-  const int64_t stride = ldx >> 3;
-  const int kb = c8 >> 2;
-  uint4 cur[R], nxt[R];
-  auto load = [&](uint4 (&buf)[R], int grp) {
-    const int r0 = grp * R;
-    const uint4* src = reinterpret_cast<const uint4*>(x + int64_t(r0) * ldx) + c8;
-#pragma unroll
-    for (int rr = 0; rr < R; ++rr)
-      buf[rr] = (col_ok && grp < n_groups && r0 + rr < M) ? __ldg(src + rr * stride) : make_uint4(0, 0, 0, 0);
-  };
-  int grp = blockIdx.y;
-  load(cur, grp);
-  for (; grp < n_groups; grp += gridDim.y) {
-    load(nxt, grp + gridDim.y);
-    const int r0 = grp * R;
-    uint32_t* dst = reinterpret_cast<uint32_t*>(codes + int64_t(r0) * (K >> 1)) + c8;
-    const size_t sf0 = (size_t(r0 >> 7) * kc_pad + size_t(kb >> 2)) * 512 + size_t((r0 >> 5) & 3) * 4 + size_t(kb & 3);
-#pragma unroll
-    for (int rr = 0; rr < R; ++rr) {
-      const uint32_t w[4] = {cur[rr].x, cur[rr].y, cur[rr].z, cur[rr].w};
-      const uint32_t m2 = __vmaxu2(__vmaxu2(w[0] & 0x7FFF7FFFu, w[1] & 0x7FFF7FFFu),
-                                   __vmaxu2(w[2] & 0x7FFF7FFFu, w[3] & 0x7FFF7FFFu));
-      uint32_t m = max(m2 & 0xFFFFu, m2 >> 16);
-      m = max(m, __shfl_xor_sync(0xffffffff, m, 1));
-      m = max(m, __shfl_xor_sync(0xffffffff, m, 2));
-      const int e = mx_block_exp_bf16bits(m);
-      const float inv = __uint_as_float(uint32_t(127 - e) << 23);
-      uint32_t packed = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        packed |= cvt_e2m1x2_raw(__uint_as_float(w[i] << 16) * inv, __uint_as_float(w[i] & 0xFFFF0000u) * inv)
-                  << (8 * i);
-      if (col_ok && r0 + rr < M) {
-        dst[int64_t(rr) * (K >> 3)] = canon_neg_zero(packed);
-        if ((threadIdx.x & 3) == 0) sf[sf0 + size_t((r0 + rr) & 31) * 16] = uint8_t(e + 127);
-      }
-    }
-#pragma unroll
-    for (int rr = 0; rr < R; ++rr) cur[rr] = nxt[rr];
-  }
-}
-
 // ------------------------------------------------------------------ INT quantize
 // One CTA per token row.  Scales / zero points in f64 exactly as the reference;
 // codes rint(x / s) bit-exact: a fast product against 1/s decides the rounding

@@ -240,3 +240,23 @@ def test_mx_decode_parity(D, M, K, N, r):
         y = lin(xt).float().cpu().numpy()
     mx, mean = O.parity_errors(y, O.forward_mx(x, main_t, comp))
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+def test_mx_linear_split_last_wave(D):
+    # 10 x 8 = 80 CTA-pair tiles on 74 pairs: the 6 leftover tiles run as K-halves
+    M, K, N, r = 2560, 1024, 2048, 64
+    x, main_t, comp = _mx_case(M, K, N, r, seed=99)
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                     comp.r_q.block_scale_exponents, np.arange(r))
+    ref = O.forward_mx(x, main_t, comp)
+    xt = _cuda(x, torch.bfloat16)
+    from paper_2603_08185_b200 import _lib
+
+    _lib.load().serq_set_debug_flags(8192)  # the split last wave is opt-in
+    try:
+        for _ in range(2):
+            y = lin(xt).float().cpu().numpy()
+            mx, mean = O.parity_errors(y, ref)
+            assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+    finally:
+        _lib.load().serq_set_debug_flags(0)

@@ -35,7 +35,7 @@ for flags in [int(f) for f in os.environ.get('FLAGS', '0,1,2,3').split(',')]:
     t = timeit(lambda: gg.replay())
     out[f"linear_dbg{flags}_us"] = t; out[f"linear_dbg{flags}_tflops"] = fl / t / 1e6
 qb = M * K * 2 + M * K // 2 + M * K // 32
-for qf in (0, 128):
+for qf in (0,):
     _lib.load().serq_set_debug_flags(qf)
     for f in (True, False):
         t = timeit(lambda: lin.quantize(x, act), fl=f)
