@@ -12,6 +12,7 @@
 #include "serq_gemm_mx2.cuh"
 #include "serq_gemm_mx3.cuh"
 #include "serq_gemm_decode.cuh"
+#include "serq_gemm_i8.cuh"
 #include "serq_quant.cuh"
 
 using namespace serq;
@@ -134,6 +135,9 @@ struct serq_linear {
   CUtensorMap map_b128, map_r128, map_sfw, map_sfr;  // CTA-pair kernel: 128-row B boxes, scale-factor maps
   CUtensorMap map_r32, map_sfr4;                     // pair3 kernel: R as 32-B swizzled rows, 512-B SF boxes
   bool has_r32 = false;
+  void* w4 = nullptr;                                // INT: packed int4 weights, tiled [N/128][K/128][128][64 B]
+  CUtensorMap map_w4, map_r_pair;                    // INT pair kernel maps (R with 128-row boxes)
+  bool has_w4 = false;
   // CTA-pair split last wave: fp32 partials + per-(tile, rank) counters
   float* sk_ws = nullptr;
   int64_t sk_ws_floats = 0;
@@ -154,7 +158,7 @@ struct serq_linear {
 namespace {
 void free_handle(serq_linear* h) {
   void* ptrs[] = {h->w, h->sfw, h->rbuf, h->sfr, h->sw, h->colsum, h->sr, h->colsum_r,
-                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y, h->dec_ws, h->dec_cnt, h->sk_ws, h->sk_cnt};
+                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y, h->dec_ws, h->dec_cnt, h->sk_ws, h->sk_cnt, h->w4};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete h;
@@ -399,12 +403,27 @@ int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t
   if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_int launch failed"));
   int rc = make_map(&h->map_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, kBN);
   if (rc) return bail(rc);
+  if (w_bits <= 4) {
+    // packed INT4 copy for the CTA-pair kernel (widened to INT8 in shared memory)
+    const int ksteps = int(cdiv(K, 128));
+    const int64_t bytes = cdiv(N, 128) * ksteps * 128 * 64;
+    if (cudaMalloc(&h->w4, bytes) != cudaSuccess) return bail(fail(SERQ_ECUDA, "cudaMalloc failed for INT4 weights"));
+    if (cudaMemsetAsync(h->w4, 0, bytes, st) != cudaSuccess) return bail(fail(SERQ_ECUDA, "memset"));
+    pack_int4_tiled_kernel<<<dim3(unsigned(cdiv(N, 256)), unsigned(cdiv(K, 2))), 256, 0, st>>>(
+        codes, K, N, ksteps, static_cast<uint8_t*>(h->w4));
+    if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_int4 launch failed"));
+    rc = make_map(&h->map_w4, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w4, 64, uint64_t(bytes / 64), 64, 64, 128,
+                  CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc) return bail(rc);
+    h->has_w4 = true;
+  }
   if (r_mode == SERQ_R_DENSE) {
     if (cudaMalloc(&h->rbuf, N * r * 2) != cudaSuccess) return bail(fail(SERQ_ECUDA, "cudaMalloc R"));
     dense_r_kernel<<<unsigned(cdiv(N * r, 256)), 256, 0, st>>>(static_cast<const double*>(r_data), r, N,
                                                                static_cast<__nv_bfloat16*>(h->rbuf));
     if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "dense_r launch failed"));
     rc = make_map(&h->map_r, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h->rbuf, r, N, r * 2, 64, kBN);
+    if (!rc) rc = make_map(&h->map_r_pair, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h->rbuf, r, N, r * 2, 64, 128);
     if (rc) return bail(rc);
   } else if (r_mode == SERQ_R_INT) {
     if (cudaMalloc(&h->rbuf, N * r) != cudaSuccess || cudaMalloc(&h->sr, N * 4) != cudaSuccess ||
@@ -416,6 +435,7 @@ int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t
     colsum_kernel<<<unsigned(cdiv(N, 256)), 256, 0, st>>>(rc32, r, N, r_scales, h->colsum_r, h->sr);
     if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack R launch failed"));
     rc = make_map(&h->map_r, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r, N, r, 128, kBN);
+    if (!rc) rc = make_map(&h->map_r_pair, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r, N, r, 128, 128);
     if (rc) return bail(rc);
   }
   *out = h;
@@ -661,6 +681,49 @@ int serq_linear_int(const serq_linear_t* h, const int8_t* a_codes, const float* 
   if (ldy < h->N || ldy % 8) return fail(SERQ_EINVAL, "ldy must be >= N and a multiple of 8");
   const bool need_xs = h->r_mode == SERQ_R_DENSE || (h->r_mode == SERQ_R_INT && !h->contiguous);
   if (need_xs && !xs) return fail(SERQ_EINVAL, "this R mode needs the quantizer's xs slice");
+  const bool pair_ok = h->has_w4 && M > 128 && (h->r_mode != SERQ_R_INT || h->contiguous) && h->r <= 128 &&
+                       (h->r_mode != SERQ_R_DENSE || h->r <= 64) && !(g_debug_flags & 65536);
+  if (pair_ok) {
+    static bool attri = false;
+    if (!attri) {
+      CK(cudaFuncSetAttribute(serq_i8_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kI8Smem));
+      attri = true;
+    }
+    I8Maps im;
+    int rc = make_map(&im.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K, M, h->K, 128, 128);
+    if (!rc)
+      rc = make_map(&im.y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, h->N, M, ldy * 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (!rc && h->r_mode == SERQ_R_DENSE)
+      rc = make_map(&im.xs, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xs, h->r, M, h->r * 2, 64, 128);
+    if (rc) return rc;
+    if (h->r_mode != SERQ_R_DENSE) im.xs = im.a;
+    im.bp = h->map_w4;
+    im.r = h->r_mode != SERQ_R_NONE ? h->map_r_pair : h->map_w4;
+    GemmParams p{};
+    p.dbg = g_debug_flags;
+    p.M = int(M);
+    p.N = int(h->N);
+    p.K = int(h->K);
+    p.r = h->r;
+    p.k_steps = int(cdiv(h->K, 128));
+    p.r_mode = h->r_mode;
+    p.a_signed = zp ? 0 : 1;
+    p.sx = sx;
+    p.zp = zp;
+    p.sw = h->sw;
+    p.colsum = h->colsum;
+    p.sr = h->sr;
+    p.colsum_r = h->colsum_r;
+    p.acc_dump = acc_dump;
+    p.accr_dump = accr_dump;
+    p.dbg_ts = g_debug_ts;
+    const int64_t tiles = cdiv(M, 256) * cdiv(h->N, kBN);
+    const int64_t max_pairs = sm_count() / 2;
+    const dim3 grid(unsigned(2 * (tiles < max_pairs ? tiles : max_pairs)));
+    serq_i8_pair_kernel<<<grid, kI8Threads, kI8Smem, S(stream)>>>(im, p);
+    LAUNCH_CHECK("serq_i8_pair_kernel");
+    return SERQ_OK;
+  }
   int rc = ensure_attr<kModeI8>();
   if (rc) return rc;
   CUtensorMap ma, mxs, my;

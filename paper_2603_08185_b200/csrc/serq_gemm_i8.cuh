@@ -1,0 +1,459 @@
+// serq_gemm_i8.cuh -- integer SERQ linear on CTA pairs with INT4 weights
+// widened to INT8 in shared memory (BASELINE configs 1 and 3).
+//
+// Y = sx[m] * ( sw[n] * (acc - zp[m]*colsum[n]) + R-term ),  acc = sum_k c[m,k] w[k,n]
+// (int_gemm_reference, mxfmt.py:177-195; forward_reconstructed, compensate.py:300-316).
+//
+// * tcgen05.mma.cta_group::2.kind::i8, 256 x 256 x 32 per instruction: u8
+//   (asymmetric) or s8 (symmetric) activation codes x s8 weights, s32 in TMEM.
+// * Weights stay PACKED INT4 in HBM, tiled [N/128][K/128][128 rows x 64 B];
+//   TMA brings 8 KB per 128-K step per CTA into a staging buffer and four
+//   transform warps widen nibbles to int8 straight into the 128B-swizzled
+//   K-major operand layout (PRMT/VSUB4, 8 codes per word).  Blackwell has no
+//   INT4 MMA; widening in SMEM halves the per-SM operand ingress for B.
+// * The salient term accumulates into a second TMEM accumulator (columns
+//   [256,512)): integer R (kind::i8, A = K-tile 0 of X, B = R codes) or dense
+//   bf16 R (kind::f16, A = bf16 (codes - zp) slice, B = L^T), both staged with
+//   K-step 0 of the tile.
+// * Two accumulators fill TMEM, so the epilogue of a tile is not overlapped
+//   with the next tile's MMAs; it reads both accumulators, applies the
+//   zero-point correction exactly (int64) and the scales, and stores bf16.
+#pragma once
+#include "serq_gemm_mx2.cuh"
+
+namespace serq {
+
+constexpr int kI8Stages = 4;
+constexpr int kI8A = 128 * 128;    // own 128 activation rows x 128 int8
+constexpr int kI8Bp = 128 * 64;    // packed int4 staging, own 128 weight rows
+constexpr int kI8B = 128 * 128;    // widened int8 operand
+constexpr int kI8Stage = kI8A + kI8Bp + kI8B;  // 40 KB
+constexpr int kI8Side = 2 * 16384;             // R operands: [A' (dense only)] + B_R
+constexpr int kI8Const = 4 * 256 * 4;
+constexpr int kI8Threads = 512;
+constexpr int kI8TrWarps = 8;  // warps 8..15
+constexpr int kI8Smem = 1024 + kI8Stages * kI8Stage + kI8Side + kI8Const + 4 * 2048 + 512;
+static_assert(kI8Smem <= 232448, "smem budget");
+
+struct I8Maps {
+  CUtensorMap a, bp, r, xs, y;
+};
+
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred P;\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n"
+      " selp.b32 %0, 1, 0, P;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_cluster(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_i8_or_bf16(bool bf16, uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                               uint32_t acc) {
+  if (bf16)
+    mma_bf16_pair(d, a, b, idesc, acc);
+  else
+    mma_i8_pair(d, a, b, idesc, acc);
+}
+__device__ __forceinline__ uint2 ld_shared_v2(const void* p) {
+  uint2 v;
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
+__device__ __forceinline__ void ld_shared_v4u(uint32_t addr, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr));
+}
+__device__ __forceinline__ void mbar_wait_bo(uint64_t* bar, uint32_t parity, bool backoff) {
+  while (!mbar_try_wait(bar, parity)) {
+    if (backoff) __nanosleep(200);
+  }
+}
+// Remote arrive with the default (.release.cta) semantics: orders this
+// thread's prior shared-memory writes (already fenced to the async proxy)
+// without the cluster-scope drain a .release.cluster arrive pays.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+// 8 packed two's-complement nibbles -> 8 int8 (element 2i in the low nibble)
+__device__ __forceinline__ uint2 widen_int4x8(uint32_t w) {
+  const uint32_t lo = __vsub4((w & 0x0F0F0F0Fu) ^ 0x08080808u, 0x08080808u);
+  const uint32_t hi = __vsub4(((w >> 4) & 0x0F0F0F0Fu) ^ 0x08080808u, 0x08080808u);
+  return make_uint2(__byte_perm(lo, hi, 0x5140), __byte_perm(lo, hi, 0x7362));
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
+    serq_i8_pair_kernel(const __grid_constant__ I8Maps maps, const GemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* side = smem + kI8Stages * kI8Stage;       // [A' 16K][B_R 16K]
+  float* cst_f = reinterpret_cast<float*>(side + kI8Side);  // sw[256] | sr[256]
+  int32_t* cst_i = reinterpret_cast<int32_t*>(cst_f + 512); // colsum[256] | colsum_r[256]
+  uint8_t* epi = reinterpret_cast<uint8_t*>(cst_i + 512);   // 4 x 2 KB staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + 4 * 2048);
+  uint64_t* full = bars;                       // [S] leader: A (+ side) landed, both CTAs
+  uint64_t* bpk = bars + kI8Stages;            // [S] local: packed B landed
+  uint64_t* bready = bars + 2 * kI8Stages;     // [S] leader: both CTAs widened B (+ A landed), 16 warps
+  uint64_t* empty = bars + 3 * kI8Stages;      // [S] both: MMAs of the stage done
+  uint64_t* side_empty = bars + 4 * kI8Stages; // both: R MMAs done
+  uint64_t* tmem_full = side_empty + 1;        // both
+  uint64_t* tmem_empty = side_empty + 2;       // leader: 8 epilogue warps drained TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(side_empty + 3);
+
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x >> 1;
+  const int n_clusters = gridDim.x >> 1;
+  const int tiles_m = (p.M + 255) / 256;
+  const int tiles_n = (p.N + kBN - 1) / kBN;
+  const int n_tiles = tiles_m * tiles_n;
+  const int my_tiles = cluster_id < n_tiles ? (n_tiles - 1 - cluster_id) / n_clusters + 1 : 0;
+  const bool has_r = p.r_mode != kRNone;
+  const bool dense = p.r_mode == kRDense;
+  const int ks = p.k_steps;  // 128-K steps
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&maps.a);
+    tma_prefetch(&maps.bp);
+    tma_prefetch(&maps.y);
+    if (has_r) {
+      tma_prefetch(&maps.r);
+      tma_prefetch(&maps.xs);
+    }
+    for (int s = 0; s < kI8Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&bpk[s], 1);
+      mbar_init(&bready[s], 2 * kI8TrWarps);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(side_empty, 1);
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 8);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (threadIdx.x == 0 && *tmem_slot != 0) __trap();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer (both CTAs)
+    if (elect_one()) {
+      const uint32_t sb = smem_u32(smem), sside = smem_u32(side);
+      uint32_t g = 0;
+      for (int i = 0; i < my_tiles; ++i) {
+        const int tile = cluster_id + i * n_clusters;
+        const int mt = tile % tiles_m, nt = tile / tiles_m;
+        const int m_own = mt * 256 + int(rank) * 128;
+        const int n_half = nt * kBN + int(rank) * 128;
+        for (int kk = 0; kk < ks; ++kk, ++g) {
+          const int s = g % kI8Stages;
+          mbar_wait_bo(&empty[s], ((g / kI8Stages) & 1) ^ 1, p.dbg & (1 << 20));
+          const bool with_side = has_r && kk == 0;
+          if (with_side && i > 0) mbar_wait(side_empty, (i - 1) & 1);
+          const uint32_t fbar = map_rank(smem_u32(&full[s]), 0);
+          const uint32_t st = sb + s * kI8Stage;
+          if (leader) mbar_expect_tx(&full[s], 2u * (kI8A + (with_side ? (dense ? 2 * 16384 : 16384) : 0)));
+          mbar_expect_tx(&bpk[s], kI8Bp);
+          tma_load_2d(smem + s * kI8Stage + kI8A, &maps.bp, &bpk[s], 0, ((n_half >> 7) * ks + kk) * 128,
+                      kEvictNormal);
+          tma_load_2d_pair(st, &maps.a, fbar, kk * 128, m_own, kEvictNormal);
+          if (with_side) {
+            tma_load_2d_pair(sside + 16384, &maps.r, fbar, 0, n_half, kEvictNormal);
+            if (dense) tma_load_2d_pair(sside, &maps.xs, fbar, 0, m_own, kEvictNormal);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader)
+    if (leader) {
+      const uint32_t sb = smem_u32(smem), sside = smem_u32(side);
+      const uint32_t id_main = idesc_i8(256, kBN, p.a_signed != 0, true);
+      const uint32_t id_r = dense ? idesc_bf16(256, kBN) : id_main;
+      const uint32_t total = uint32_t(my_tiles) * ks;
+      if (total > 0) {
+        mbar_wait_cluster(&bready[0], 0);
+        tc_fence_after();
+      }
+      uint32_t g = 0;
+      for (int i = 0; i < my_tiles; ++i) {
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && lane_id() == 0 && i < 8) p.dbg_ts[512 + (blockIdx.x >> 1) * 64 + i * 8] = globaltimer();
+#endif
+        if (i > 0) {
+          mbar_wait_bo(tmem_empty, (i - 1) & 1, p.dbg & (1 << 20));
+          tc_fence_after();
+        }
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && lane_id() == 0 && i < 8) p.dbg_ts[512 + (blockIdx.x >> 1) * 64 + i * 8 + 1] = globaltimer();
+#endif
+        for (int kk = 0; kk < ks; ++kk, ++g) {
+          const int s = g % kI8Stages;
+          const uint32_t st = sb + s * kI8Stage;
+          const uint64_t a = make_sdesc(st, 16, 1024, 2), b = make_sdesc(st + kI8A + kI8Bp, 16, 1024, 2);
+          const uint32_t first = kk > 0 ? 1u : 0u;
+          const bool no_mma = p.dbg & (1 << 18);
+          if (elect_one() && !no_mma) {
+            mma_i8_pair(0, a, b, id_main, first);
+            mma_i8_pair(0, a + 2, b + 2, id_main, 1u);
+            mma_i8_pair(0, a + 4, b + 4, id_main, 1u);
+            if (has_r && kk == 0) {
+              // salient term into the second accumulator (columns [256, 512))
+              const uint64_t ar = dense ? make_sdesc(sside, 16, 1024, 2) : a;
+              const uint64_t br = make_sdesc(sside + 16384, 16, 1024, 2);
+              const int nk = dense ? (2 * p.r + 31) / 32 : (p.r + 31) / 32;
+              for (int j = 0; j < nk; ++j) mma_i8_or_bf16(dense, 256, ar + 2 * j, br + 2 * j, id_r, j > 0 ? 1u : 0u);
+              tc_commit_pair(side_empty);
+            }
+          }
+          __syncwarp();
+#ifdef SERQ_DIAG_TS
+          if (p.dbg_ts && blockIdx.x == 0 && lane_id() == 0 && g < 32) p.dbg_ts[8 * g + 5] = clock64();
+#endif
+          if (g + 1 < total) {
+            const uint32_t gn = g + 1;
+            mbar_wait_cluster(&bready[gn % kI8Stages], (gn / kI8Stages) & 1);
+            tc_fence_after();
+          }
+#ifdef SERQ_DIAG_TS
+          if (p.dbg_ts && blockIdx.x == 0 && lane_id() == 0 && g < 32) p.dbg_ts[8 * g + 6] = clock64();
+#endif
+          if (elect_one()) {
+            if (!no_mma) mma_i8_pair(0, a + 6, b + 6, id_main, 1u);
+            tc_commit_pair(&empty[s]);
+            if (kk == ks - 1) tc_commit_pair(tmem_full);
+          }
+          __syncwarp();
+        }
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && lane_id() == 0 && i < 8) p.dbg_ts[512 + (blockIdx.x >> 1) * 64 + i * 8 + 2] = globaltimer();
+#endif
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ INT4 -> INT8 transform (both CTAs)
+    const int tw = int(warp) - 8;  // 0..7
+    const uint32_t bready_leader = map_rank(smem_u32(&bready[0]), 0);
+    uint32_t g = 0;
+    for (int i = 0; i < my_tiles; ++i) {
+      for (int kk = 0; kk < ks; ++kk, ++g) {
+        const int s = g % kI8Stages;
+        const uint32_t ph = (g / kI8Stages) & 1;
+#ifdef SERQ_DIAG_TS
+        const bool stamp = p.dbg_ts && blockIdx.x == 0 && tw == 0 && lane_id() == 0 && g < 32;
+        if (stamp) p.dbg_ts[8 * g] = clock64();
+#endif
+        mbar_wait_bo(&bpk[s], ph, p.dbg & (1 << 20));
+#ifdef SERQ_DIAG_TS
+        if (stamp) p.dbg_ts[8 * g + 1] = clock64();
+#endif
+        const uint8_t* pk = smem + s * kI8Stage + kI8A;
+        const uint32_t bdst = smem_u32(smem + s * kI8Stage + kI8A + kI8Bp);
+        // 1024 tasks (128 rows x 8 output chunks of 16 B); a warp covers 4 rows per pass.
+        // All loads first: the st.shared asm below is a compiler barrier.
+        constexpr int kIt = 1024 / (32 * kI8TrWarps);
+        uint2 wv[kIt];
+        if (!(p.dbg & (1 << 17)))
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+          const int task = (it * kI8TrWarps + tw) * 32 + int(lane_id());
+          wv[it] = ld_shared_v2(pk + (task >> 3) * 64 + (task & 7) * 8);
+        }
+        if (!(p.dbg & (1 << 17)))
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+          const int task = (it * kI8TrWarps + tw) * 32 + int(lane_id());
+          const int row = task >> 3, chunk = task & 7;
+          const uint2 lo = widen_int4x8(wv[it].x), hi = widen_int4x8(wv[it].y);
+          st_shared_v4(bdst + row * 128 + ((uint32_t(chunk) ^ uint32_t(row & 7)) * 16), lo.x, lo.y, hi.x, hi.y);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+#ifdef SERQ_DIAG_TS
+        if (stamp) p.dbg_ts[8 * g + 2] = clock64();
+#endif
+        if (leader) {
+          // the MMA waits on this barrier only: also make it imply "A landed"
+          mbar_wait(&full[s], ph);
+        }
+        __syncwarp();
+#ifdef SERQ_DIAG_TS
+        if (stamp) p.dbg_ts[8 * g + 3] = clock64();
+#endif
+        if (lane_id() == 0) {
+          if (p.dbg & 4096)
+            mbar_arrive_cluster(bready_leader + uint32_t(s) * 8u);
+          else
+            mbar_arrive_remote(bready_leader + uint32_t(s) * 8u);
+        }
+#ifdef SERQ_DIAG_TS
+        if (stamp) p.dbg_ts[8 * g + 4] = clock64();
+#endif
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const uint32_t q = warp & 3;
+    const uint32_t lane_base = (q * 32u) << 16;
+    uint8_t* stage_out = epi + q * 2048;
+    const uint32_t rbase = smem_u32(stage_out) + lane_id() * 64;
+    const uint32_t swz = (lane_id() >> 1) & 3;
+    const uint32_t tmem_empty_leader = map_rank(smem_u32(tmem_empty), 0);
+    for (int i = 0; i < my_tiles; ++i) {
+      const int tile = cluster_id + i * n_clusters;
+      const int mt = tile % tiles_m, nt = tile / tiles_m;
+      const int m_own = mt * 256 + int(rank) * 128;
+      const int n0 = nt * kBN;
+      // per-column constants of this tile
+      named_bar_sync(1, 128);  // previous tile's readers are done with the constants
+      for (int c = threadIdx.x - 128; c < kBN; c += 128) {
+        const int n = n0 + c;
+        const bool ok = n < p.N;
+        cst_f[c] = ok ? p.sw[n] : 0.f;
+        cst_i[c] = (ok && p.zp) ? -p.colsum[n] : 0;  // negated: acc + zp*(-colsum) is one IMAD
+        cst_f[256 + c] = (ok && p.r_mode == kRInt) ? p.sr[n] : 0.f;
+        cst_i[256 + c] = (ok && p.zp && p.r_mode == kRInt) ? -p.colsum_r[n] : 0;
+      }
+      named_bar_sync(1, 128);
+      const int row = m_own + int(q) * 32 + int(lane_id());
+      float sx = 0.f;
+      uint32_t zp = 0;
+      if (row < p.M) {
+        sx = p.sx[row];
+        zp = p.zp ? uint32_t(p.zp[row]) : 0u;
+      }
+#ifdef SERQ_DIAG_TS
+      if (p.dbg_ts && leader && q == 0 && lane_id() == 0 && i < 8) p.dbg_ts[512 + cluster_id * 64 + i * 8 + 3] = globaltimer();
+#endif
+      mbar_wait(tmem_full, i & 1);
+      tc_fence_after();
+#ifdef SERQ_DIAG_TS
+      if (p.dbg_ts && leader && q == 0 && lane_id() == 0 && i < 8) p.dbg_ts[512 + cluster_id * 64 + i * 8 + 4] = globaltimer();
+#endif
+#pragma unroll 1
+      for (int c = 0; c < kBN / 32; ++c) {
+        // exact in wrapping int32: |acc - zp*colsum| <= 255 * 8 * K < 2^31 for K < 2^20
+        uint32_t packed[16];
+#pragma unroll
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == 1) p.dbg_ts[5300 + c * 8 + 0] = globaltimer();
+#endif
+        for (int h = 0; h < 2; ++h) {
+          uint32_t v[16], w[16];
+          const uint32_t col0 = uint32_t(c * 32 + h * 16);
+          tmem_ld_32x32b_x16(lane_base + col0, v);
+          if (has_r) tmem_ld_32x32b_x16(lane_base + 256 + col0, w);
+          tmem_ld_wait();
+#ifdef SERQ_DIAG_TS
+          if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == 1) p.dbg_ts[5300 + c * 8 + 4 + h] = globaltimer();
+#endif
+          if (c == kBN / 32 - 1 && h == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive_cluster_relaxed(tmem_empty_leader);
+          }
+          // this half-chunk's column constants: broadcast vector loads, once
+          const uint32_t cf = smem_u32(cst_f) + col0 * 4, ci = smem_u32(cst_i) + col0 * 4;
+          float f[16];
+#pragma unroll
+          for (int j4 = 0; j4 < 4; ++j4) {
+            // 4 columns' constants per broadcast vector load
+            uint32_t cs[4], fs[4], cr[4] = {0, 0, 0, 0}, fr[4] = {0, 0, 0, 0};
+            ld_shared_v4u(ci + 16 * j4, cs[0], cs[1], cs[2], cs[3]);
+            ld_shared_v4u(cf + 16 * j4, fs[0], fs[1], fs[2], fs[3]);
+            if (has_r && !dense) {
+              ld_shared_v4u(ci + 1024 + 16 * j4, cr[0], cr[1], cr[2], cr[3]);
+              ld_shared_v4u(cf + 1024 + 16 * j4, fr[0], fr[1], fr[2], fr[3]);
+            }
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const int j = 4 * j4 + jj;
+              const int32_t a = int32_t(v[j] + zp * cs[jj]);
+              float yv = float(a) * __uint_as_float(fs[jj]);
+              if (has_r) {
+                if (dense) {
+                  yv += __uint_as_float(w[j]);
+                } else {
+                  const int32_t ar = int32_t(w[j] + zp * cr[jj]);
+                  yv += float(ar) * __uint_as_float(fr[jj]);
+                }
+              }
+              f[j] = yv * sx;
+            }
+          }
+          if (p.acc_dump && row < p.M) {
+            // debug: exact accumulators (tests)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int col = int(col0) + j;
+              if (n0 + col >= p.N) continue;
+              p.acc_dump[size_t(row) * p.N + n0 + col] = int32_t(v[j] + zp * uint32_t(cst_i[col]));
+              if (p.accr_dump && has_r && !dense)
+                p.accr_dump[size_t(row) * p.N + n0 + col] = int32_t(w[j] + zp * uint32_t(cst_i[256 + col]));
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) packed[h * 8 + j] = pack_bf16x2(f[2 * j], f[2 * j + 1]);
+        }
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == 1) p.dbg_ts[5300 + c * 8 + 1] = globaltimer();
+#endif
+        if (lane_id() == 0) bulk_wait_read_all();
+        __syncwarp();
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == 1) p.dbg_ts[5300 + c * 8 + 2] = globaltimer();
+#endif
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          st_shared_v4(rbase + ((uint32_t(j) ^ swz) * 16), packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
+                       packed[4 * j + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane_id() == 0 && m_own < p.M) {
+          tma_store_2d(&maps.y, stage_out, n0 + c * 32, m_own + int(q) * 32);
+          bulk_commit();
+        }
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == 1) p.dbg_ts[5300 + c * 8 + 3] = globaltimer();
+#endif
+      }
+#ifdef SERQ_DIAG_TS
+      if (p.dbg_ts && leader && q == 0 && lane_id() == 0 && i < 8) p.dbg_ts[512 + cluster_id * 64 + i * 8 + 5] = globaltimer();
+#endif
+    }
+    if (lane_id() == 0) bulk_wait_all();
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(0u));
+  }
+}
+
+}  // namespace serq

@@ -138,13 +138,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (with_r && r_uses > 0) mbar_wait(r_empty, (r_uses - 1) & 1);  // previous R MMAs are done
           if (with_r) ++r_uses;
           const uint32_t fbar = map_rank(smem_u32(&full[slot]), 0);
-          if (leader) mbar_expect_tx(&full[slot], 2u * (len * k3StepBytes + (with_r ? k3RB + k3RSF : 0)));
+          const bool no_sf = p.dbg & 32768;  // diagnostics: skip scale-factor loads (request-count test)
+          if (leader)
+            mbar_expect_tx(&full[slot], 2u * (len * (k3StepBytes - (no_sf ? 3072 : 0)) + (with_r ? k3RB + k3RSF : 0)));
           const uint32_t st = smem_base + slot * k3SlotBytes;
           // weights (B, SFB) never depend on the previous kernel: load them first
           for (int h = 0; h < len; ++h) {
             const uint32_t ss = st + h * k3StepBytes;
             const int kk = k0 + h;
             tma_load_2d_pair_nohint(ss + k2SmemA, &maps.b, fbar, 0, ((n_half >> 7) * p.w_ksteps + kk) * 128);
+            if (no_sf) continue;
             tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB + k2SmemSFA, &maps.sfb, fbar, 0,
                                     ((n0 / 128) * p.kc_pad + 2 * kk) * 4);
             tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB + k2SmemSFA + 1024, &maps.sfb, fbar, 0,
@@ -155,7 +158,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t ss = st + h * k3StepBytes;
             const int kk = k0 + h;
             tma_load_2d_pair_nohint(ss, &maps.a, fbar, kk * kStepBytes, m_own);
-            tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB, &maps.sfa, fbar, 0, (mblk * p.kc_pad + 2 * kk) * 4);
+            if (!no_sf)
+              tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB, &maps.sfa, fbar, 0, (mblk * p.kc_pad + 2 * kk) * 4);
           }
           if (with_r) {
             tma_load_2d_pair_nohint(rb, &maps.r, fbar, 0, n_half);  // [128 rows x 32 B], 32B swizzle
