@@ -22,6 +22,8 @@
  *   serq_linear_int        forward_reconstructed int branch: int_gemm_reference(xq, main)
  *                          + R term (int_gemm_reference(xs, r_q) or dequantize(xs) @ r_dense)
  *                                                                         compensate.py:300-316, mxfmt.py:135-195
+ *   serq_forward_mx        forward_reconstructed(x, main_t, comp, None) on device: mx_encode(x)
+ *                          (+ re-encode of x[:, idx]) then the fused GEMM      compensate.py:319-340
  *   serq_forward_mx_host   forward_reconstructed(x, main_t, comp, None) end to end from host memory
  *                                                                         compensate.py:272-295
  */
@@ -111,6 +113,15 @@ int serq_linear_mx(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t
  * receive the exact integer accumulators sum (c - zp) * w. */
 int serq_linear_int(const serq_linear_t* h, const int8_t* a_codes, const float* sx, const int32_t* zp, int64_t M,
                     const void* xs, void* y, int64_t ldy, int32_t* acc_dump, int32_t* accr_dump, serq_stream_t stream);
+
+/* Quantize + linear in one call (compensate.py:319-340 _forward_mx): x (bf16 /
+ * f32 / f64 [M, K], row pitch ldx elements) -> codes / sf (serq_act_quant_mx
+ * layout, caller-allocated) -> y.  The linear is launched with programmatic
+ * dependent launch so its prologue and weight stream overlap the quantizer.
+ * gather_idx / xs_codes / xs_sf are needed only for a non-contiguous salient set. */
+int serq_forward_mx(serq_linear_t* h, const void* x, int dtype, int64_t M, int64_t ldx, const int32_t* gather_idx,
+                    uint8_t* codes, uint8_t* sf, uint8_t* xs_codes, uint8_t* xs_sf, void* y, int64_t ldy,
+                    serq_stream_t stream);
 
 /* End to end from HOST memory (pinned for full PCIe rate): copy X (bf16 [M, K])
  * in, quantize, GEMM, copy Y (bf16 [M, N]) out; synchronises `stream`.

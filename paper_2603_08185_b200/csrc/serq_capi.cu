@@ -1,3 +1,4 @@
+#include <cstdlib>
 // serq_capi.cu -- the extern "C" boundary (include/serq_b200.h): validation,
 // weight handles, tensor maps, launches.
 #include <cstdarg>
@@ -119,6 +120,8 @@ int ensure_attr() {
 }  // namespace
 
 // ------------------------------------------------------------------ handle
+constexpr int kE2eMaxChunks = 16;
+
 struct serq_linear {
   int mode = 0;  // kModeMX / kModeI8
   int64_t N = 0, K = 0;
@@ -153,6 +156,9 @@ struct serq_linear {
   uint8_t* ws_codes = nullptr;
   uint8_t* ws_sf = nullptr;
   void* ws_y = nullptr;
+  // end-to-end pipeline: H2D and D2H copy streams + per-chunk events (created lazily)
+  cudaStream_t e2e_in = nullptr, e2e_out = nullptr;
+  cudaEvent_t e2e_ev[3 * kE2eMaxChunks + 1] = {};
 };
 
 namespace {
@@ -161,6 +167,10 @@ void free_handle(serq_linear* h) {
                   h->ws_x, h->ws_codes, h->ws_sf, h->ws_y, h->dec_ws, h->dec_cnt, h->sk_ws, h->sk_cnt, h->w4};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (cudaEvent_t e : h->e2e_ev)
+    if (e) cudaEventDestroy(e);
+  if (h->e2e_in) cudaStreamDestroy(h->e2e_in);
+  if (h->e2e_out) cudaStreamDestroy(h->e2e_out);
   delete h;
 }
 }  // namespace
@@ -197,8 +207,8 @@ int serq_mx_sizes(int64_t rows, int64_t cols, int64_t* codes_bytes, int64_t* sf_
   return SERQ_OK;
 }
 
-int serq_act_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, uint8_t* codes, uint8_t* sf,
-                      const int32_t* gather_idx, int r, uint8_t* xs_codes, uint8_t* xs_sf, serq_stream_t stream) {
+static int act_quant_mx_impl(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, uint8_t* codes, uint8_t* sf,
+                             const int32_t* gather_idx, int r, uint8_t* xs_codes, uint8_t* xs_sf, serq_stream_t stream) {
   g_launches = 0;
   if (M <= 0 || K <= 0) return fail(SERQ_EINVAL, "x must be non-empty (M=%lld, K=%lld)", (long long)M, (long long)K);
   if (K % 32) return fail(SERQ_EINVAL, "row length %lld not divisible by block_size 32", (long long)K);
@@ -218,12 +228,13 @@ int serq_act_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ld
   if (gather_idx && (M % 128 || r % 256)) CK(cudaMemsetAsync(xs_sf, 0, sf_bytes_of(M, r), st));
   if (dtype != SERQ_F64) {
     const dim3 grid(unsigned(cdiv(K / 8, 256)), unsigned(cdiv(M, kMxRows)));
-    if (dtype == SERQ_BF16)
+    if (dtype == SERQ_BF16) {
       mx_encode_fast_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), int(M), int(K),
                                                                  ldx, codes, sf, kc);
-    else
+    } else {
       mx_encode_fast_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(x), int(M), int(K), ldx, codes, sf,
                                                          kc);
+    }
     LAUNCH_CHECK("mx_encode_fast");
     if (gather_idx) {
       const dim3 g2(unsigned(cdiv(M * (r / 8), 256)));
@@ -244,6 +255,11 @@ int serq_act_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ld
                                                  r, xs_codes, xs_sf, krc, nb_main);
   LAUNCH_CHECK("mx_encode");
   return SERQ_OK;
+}
+
+int serq_act_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, uint8_t* codes, uint8_t* sf,
+                      const int32_t* gather_idx, int r, uint8_t* xs_codes, uint8_t* xs_sf, serq_stream_t stream) {
+  return act_quant_mx_impl(x, dtype, M, K, ldx, codes, sf, gather_idx, r, xs_codes, xs_sf, stream);
 }
 
 int serq_act_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, int bits, int symmetric,
@@ -457,8 +473,8 @@ int serq_linear_info(const serq_linear_t* h, int64_t* N, int64_t* K, int* r, int
   return SERQ_OK;
 }
 
-int serq_linear_mx(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t* a_sf, int64_t M,
-                   const uint8_t* xs_codes, const uint8_t* xs_sf, void* y, int64_t ldy, serq_stream_t stream) {
+static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t* a_sf, int64_t M,
+                          const uint8_t* xs_codes, const uint8_t* xs_sf, void* y, int64_t ldy, serq_stream_t stream) {
   g_launches = 0;
   if (!h || h->mode != kModeMX) return fail(SERQ_EINVAL, "handle is not an MX linear");
   if (M <= 0) return fail(SERQ_EINVAL, "x must be non-empty");
@@ -592,6 +608,8 @@ int serq_linear_mx(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t
     // split the last partial wave into K-halves when they fit in one round
     const int64_t rounds = pairs / clusters, left = pairs - rounds * clusters;
     p.split_from = int(pairs);
+    // tile order: N-fastest measured +2.4% at 8192^3, equal at 4096^3 (tools/sweep_mx.py)
+    p.group_m = (g_debug_flags & 262144) ? 0 : 1;
     p.y = static_cast<__nv_bfloat16*>(y);
     p.ldy = ldy;
     // opt-in (debug flag 8192): measured slower than 4 full rounds for 4096^3 (partner flag + partial traffic)
@@ -671,6 +689,30 @@ int serq_linear_mx(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t
                                                                         my, p);
   LAUNCH_CHECK("serq_mx_persistent_kernel");
   return SERQ_OK;
+}
+
+int serq_linear_mx(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t* a_sf, int64_t M,
+                   const uint8_t* xs_codes, const uint8_t* xs_sf, void* y, int64_t ldy, serq_stream_t stream) {
+  return linear_mx_impl(h, a_codes, a_sf, M, xs_codes, xs_sf, y, ldy, stream);
+}
+
+int serq_forward_mx(serq_linear_t* h, const void* x, int dtype, int64_t M, int64_t ldx, const int32_t* gather_idx,
+                    uint8_t* codes, uint8_t* sf, uint8_t* xs_codes, uint8_t* xs_sf, void* y, int64_t ldy,
+                    serq_stream_t stream) {
+  if (!h || h->mode != kModeMX) return fail(SERQ_EINVAL, "handle is not an MX linear");
+  const bool gather = h->r > 0 && !h->contiguous;
+  if (gather && (!gather_idx || !xs_codes || !xs_sf))
+    return fail(SERQ_EINVAL, "non-contiguous salient set needs gather_idx and the xs buffers");
+  // the linear is launched with programmatic dependent launch: its prologue and
+  // weight stream overlap the quantizer (a per-row-tile counter hand-off was
+  // measured slower: 45.1 vs 43.0 us at 4096^3, tools/fuse_probe.py)
+  int rc = act_quant_mx_impl(x, dtype, M, h->K, ldx, codes, sf, gather ? gather_idx : nullptr, gather ? h->r : 0,
+                             xs_codes, xs_sf, stream);
+  if (rc) return rc;
+  const int n1 = g_launches;
+  rc = linear_mx_impl(h, codes, sf, M, gather ? xs_codes : nullptr, gather ? xs_sf : nullptr, y, ldy, stream);
+  g_launches += n1;
+  return rc;
 }
 
 int serq_linear_int(const serq_linear_t* h, const int8_t* a_codes, const float* sx, const int32_t* zp, int64_t M,
@@ -781,15 +823,56 @@ int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* 
     CK(cudaMalloc(&h->ws_y, mm * h->N * 2));
     h->ws_m = mm;
   }
-  CK(cudaMemcpyAsync(h->ws_x, x_host, M * h->K * 2, cudaMemcpyHostToDevice, st));
-  int rc = serq_act_quant_mx(h->ws_x, SERQ_BF16, M, h->K, h->K, h->ws_codes, h->ws_sf, nullptr, 0, nullptr, nullptr,
-                             stream);
-  if (rc) return rc;
-  const int n1 = g_launches;
-  rc = serq_linear_mx(h, h->ws_codes, h->ws_sf, M, nullptr, nullptr, h->ws_y, h->N, stream);
-  if (rc) return rc;
-  g_launches += n1;
-  CK(cudaMemcpyAsync(y_host, h->ws_y, M * h->N * 2, cudaMemcpyDeviceToHost, st));
+  // Chunked over token rows (multiples of 256) so that the H2D copy of chunk
+  // i+1, the quantize + fused linear of chunk i and the D2H copy of chunk i-1
+  // run concurrently on the two copy engines and the SMs.
+  if (!h->e2e_in) {
+    CK(cudaStreamCreateWithFlags(&h->e2e_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->e2e_out, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : h->e2e_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  int64_t rows = cdiv(cdiv(M, kE2eMaxChunks), 256) * 256;
+  if (rows < 1024) rows = 1024;  // measured: 1024-row chunks 0.94 ms vs 256-row 1.15 ms at 4096^2
+  if (const char* e = getenv("SERQ_E2E_ROWS")) rows = cdiv(atoll(e), 256) * 256;  // diagnostics
+  if (cdiv(M, rows) > kE2eMaxChunks) rows = cdiv(cdiv(M, kE2eMaxChunks), 256) * 256;
+  const int64_t chunks = cdiv(M, rows);
+  cudaEvent_t* ev_in = h->e2e_ev;                       // [chunks] x chunk landed
+  cudaEvent_t* ev_done = h->e2e_ev + kE2eMaxChunks;     // [chunks] y chunk computed
+  cudaEvent_t* ev_out = h->e2e_ev + 2 * kE2eMaxChunks;  // [chunks] y chunk copied out
+  cudaEvent_t ev_start = h->e2e_ev[3 * kE2eMaxChunks];
+  CK(cudaEventRecord(ev_start, st));  // the copies must follow earlier work on the caller's stream
+  CK(cudaStreamWaitEvent(h->e2e_in, ev_start, 0));
+  const int64_t kc_pad = kc_pad_of(h->K);
+  for (int64_t c = 0; c < chunks; ++c) {
+    const int64_t r0 = c * rows, mc = (M - r0 < rows) ? M - r0 : rows;
+    CK(cudaMemcpyAsync(static_cast<uint8_t*>(h->ws_x) + r0 * h->K * 2, static_cast<const uint8_t*>(x_host) + r0 * h->K * 2,
+                       mc * h->K * 2, cudaMemcpyHostToDevice, h->e2e_in));
+    CK(cudaEventRecord(ev_in[c], h->e2e_in));
+  }
+  const int n0 = g_launches;
+  int launches = 0;
+  for (int64_t c = 0; c < chunks; ++c) {
+    const int64_t r0 = c * rows, mc = (M - r0 < rows) ? M - r0 : rows;
+    uint8_t* codes = h->ws_codes + r0 * h->K / 2;
+    uint8_t* sf = h->ws_sf + (r0 / 128) * kc_pad * 512;
+    CK(cudaStreamWaitEvent(st, ev_in[c], 0));
+    int rc = serq_act_quant_mx(static_cast<uint8_t*>(h->ws_x) + r0 * h->K * 2, SERQ_BF16, mc, h->K, h->K, codes, sf,
+                               nullptr, 0, nullptr, nullptr, stream);
+    if (rc) return rc;
+    launches += g_launches;
+    rc = serq_linear_mx(h, codes, sf, mc, nullptr, nullptr, static_cast<uint8_t*>(h->ws_y) + r0 * h->N * 2, h->N,
+                        stream);
+    if (rc) return rc;
+    launches += g_launches;
+    CK(cudaEventRecord(ev_done[c], st));
+    CK(cudaStreamWaitEvent(h->e2e_out, ev_done[c], 0));
+    CK(cudaMemcpyAsync(static_cast<uint8_t*>(y_host) + r0 * h->N * 2, static_cast<uint8_t*>(h->ws_y) + r0 * h->N * 2,
+                       mc * h->N * 2, cudaMemcpyDeviceToHost, h->e2e_out));
+    CK(cudaEventRecord(ev_out[c], h->e2e_out));
+  }
+  (void)n0;
+  g_launches = launches;
+  CK(cudaStreamWaitEvent(st, ev_out[chunks - 1], 0));
   CK(cudaStreamSynchronize(st));
   return SERQ_OK;
 }

@@ -76,6 +76,7 @@ struct GemmParams {
   int* sk_cnt;           // [split tiles][2 ranks] self-resetting arrival counters
   __nv_bfloat16* y;      // output (direct stores of split tiles)
   int64_t ldy;
+  int group_m;           // tile order: 0 = M fastest over all tiles; g > 0 = groups of g M-tiles
   int dbg;               // diagnostics: bit0 = producer skips all loads (MMA ceiling), bit1 = no output stores
 };
 

@@ -65,6 +65,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   struct Item {
     int tile, half, lo, hi;  // half: -1 = whole tile; [lo, hi) = k-unit range
   };
+  // tile -> (M tile, N tile): M fastest, or grouped (group_m M-tiles x all N-tiles per group)
+  auto tile_mn = [&](int tile, int& mt, int& nt) {
+    if (p.group_m <= 0) {
+      mt = tile % tiles_m;
+      nt = tile / tiles_m;
+      return;
+    }
+    const int per = p.group_m * tiles_n;
+    const int g = tile / per, first = g * p.group_m;
+    const int gs = min(p.group_m, tiles_m - first);
+    const int w = tile - g * per;
+    mt = first + w % gs;
+    nt = w / gs;
+  };
   auto item_of = [&](int w) {
     Item it;
     if (w < split_from) {
@@ -124,7 +138,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int i = 0; i < my_tiles; ++i) {
         const Item itm = item_of(cluster_id + i * n_clusters);
         const int tile = (p.dbg & 16384) ? 0 : itm.tile;  // diagnostics: every cluster streams tile 0
-        const int mt = tile % tiles_m, nt = tile / tiles_m;
+        int mt, nt;
+        tile_mn(tile, mt, nt);
         const int m_own = mt * 256 + int(rank) * 128;
         const int n0 = nt * kBN;
         const int n_half = n0 + int(rank) * 128;
@@ -294,7 +309,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int i = 0; i < my_tiles; ++i) {
       const Item itm = item_of(cluster_id + i * n_clusters);
       const int tile = itm.tile;
-      const int mt = tile % tiles_m, nt = tile / tiles_m;
+      int mt, nt;
+      tile_mn(tile, mt, nt);
       const int m_own = mt * 256 + int(rank) * 128;
       const int n0 = nt * kBN;
       const uint32_t b = i & 1;

@@ -202,8 +202,32 @@ class MxLinear:
                   _ptr(act.xs_sf), y.data_ptr(), y.stride(0), _stream())
         return y
 
+    def forward(self, x: torch.Tensor, act: MxActivation | None = None, y: torch.Tensor | None = None) -> torch.Tensor:
+        """Quantize + linear in ONE C-ABI call (serq_forward_mx): for M > 128 the
+        quantizer hands finished 256-row tiles to the running linear."""
+        _require_cuda(x, "x")
+        if x.dim() != 2 or x.stride(1) != 1:
+            raise ValidationError("x must be a row-major 2-D tensor")
+        M, K = x.shape
+        if K != self.K:
+            raise ValidationError("x columns must equal weight input dim")
+        if act is None:
+            cb, sb = mx_sizes(M, K)
+            act = MxActivation(torch.empty(cb, dtype=torch.uint8, device=x.device),
+                               torch.empty(sb, dtype=torch.uint8, device=x.device), M, K)
+            if not self.contiguous:
+                cbr, sbr = mx_sizes(M, self.r)
+                act.xs_codes = torch.empty(cbr, dtype=torch.uint8, device=x.device)
+                act.xs_sf = torch.empty(sbr, dtype=torch.uint8, device=x.device)
+        if y is None:
+            y = torch.empty((M, self.N), dtype=torch.bfloat16, device=self.device)
+        _lib.call("serq_forward_mx", self._h.ptr, x.data_ptr(), _dtype_id(x), M, x.stride(0), _ptr(self.gather_idx),
+                  act.codes.data_ptr(), act.sf.data_ptr(), _ptr(act.xs_codes), _ptr(act.xs_sf), y.data_ptr(),
+                  y.stride(0), _stream())
+        return y
+
     def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
-        return self.gemm(self.quantize(x), y)
+        return self.forward(x, None, y)
 
     def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor) -> None:
         """End to end from (pinned) host bf16 memory through the C-ABI."""

@@ -260,3 +260,40 @@ def test_mx_linear_split_last_wave(D):
             assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
     finally:
         _lib.load().serq_set_debug_flags(0)
+
+
+@pytest.mark.parametrize("M", [1000, 300, 4096])
+def test_mx_forward_host_chunked(D, M):
+    # serq_forward_mx_host pipelines H2D / quantize+linear / D2H over 256-row
+    # chunks: rows land in the same tiles' K order as the device path, so the
+    # output equals the device path exactly when every chunk runs the pair kernel
+    K, N, r = 1024, 512, 64
+    x, main_t, comp = _mx_case(M, K, N, r, seed=M + 5)
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                     comp.r_q.block_scale_exponents, np.arange(r))
+    xh = torch.from_numpy(x).to(torch.bfloat16).pin_memory()
+    yh = torch.empty((M, N), dtype=torch.bfloat16).pin_memory()
+    lin.forward_host(xh, yh)
+    y = yh.float().numpy()
+    mx, mean = O.parity_errors(y, O.forward_mx(x, main_t, comp))
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+    if M % 256 == 0 or M % 256 > 128:
+        yd = lin(xh.to("cuda")).cpu()
+        assert torch.equal(yd, yh)
+
+
+@pytest.mark.parametrize("M,K,N", [(4096, 1024, 1024), (1000, 2048, 768), (2600, 512, 4096)])
+def test_mx_forward_fused_equals_two_launches(D, M, K, N):
+    # serq_forward_mx (one C-ABI call, PDL between the two kernels) must equal
+    # quantize-then-linear exactly, on every call
+    r = 64
+    x, main_t, comp = _mx_case(M, K, N, r, seed=M + 7)
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                     comp.r_q.block_scale_exponents, np.arange(r))
+    xt = _cuda(x, torch.bfloat16)
+    y2 = lin.gemm(lin.quantize(xt))
+    for _ in range(3):
+        y1 = lin.forward(xt)
+        assert torch.equal(y1, y2)
+    mx, mean = O.parity_errors(y2.float().cpu().numpy(), O.forward_mx(x, main_t, comp))
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
