@@ -13,6 +13,7 @@
 #include "serq_gemm_mx2.cuh"
 #include "serq_gemm_mx3.cuh"
 #include "serq_gemm_decode.cuh"
+#include "serq_gemm_decode3.cuh"
 #include "serq_gemm_i8.cuh"
 #include "serq_quant.cuh"
 
@@ -88,6 +89,23 @@ int make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t 
                   swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SERQ_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return SERQ_OK;
+}
+
+// launch with programmatic stream serialization: the kernel may start under the
+// previous kernel's tail and must call griddepcontrol.wait before reading its inputs
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 int sm_count() {
@@ -222,18 +240,20 @@ static int act_quant_mx_impl(const void* x, int dtype, int64_t M, int64_t K, int
     return fail(SERQ_EINVAL, "f32 input must be 16-byte aligned with ldx %% 4 == 0");
   cudaStream_t st = S(stream);
   const int kc = kc_pad_of(K);
-  // padded SF rows / chunks must read as zero codes' scale (any finite value); zero them
-  if (M % 128 || K % 256) CK(cudaMemsetAsync(sf, 0, sf_bytes_of(M, K), st));
+  // padded SF rows / chunks must read as a finite scale: the fast kernels write
+  // them (grid over the padded extent); the f64 / gather kernels need the memset
+  if ((M % 128 || K % 256) && (dtype == SERQ_F64)) CK(cudaMemsetAsync(sf, 0, sf_bytes_of(M, K), st));
   const int krc = gather_idx ? kc_pad_of(r) : 0;
   if (gather_idx && (M % 128 || r % 256)) CK(cudaMemsetAsync(xs_sf, 0, sf_bytes_of(M, r), st));
   if (dtype != SERQ_F64) {
-    const dim3 grid(unsigned(cdiv(K / 8, 256)), unsigned(cdiv(M, kMxRows)));
+    const int64_t m_rows = (M % 128) ? cdiv(M, 128) * 128 : M;  // cover the SF row padding
+    const dim3 grid(unsigned(cdiv(int64_t(kc) * 16, 256)), unsigned(cdiv(m_rows, kMxRows)));
     if (dtype == SERQ_BF16) {
-      mx_encode_fast_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), int(M), int(K),
-                                                                 ldx, codes, sf, kc);
+      CK(launch_pdl(mx_encode_fast_kernel<__nv_bfloat16>, grid, dim3(256), 0, st, static_cast<const __nv_bfloat16*>(x),
+                    int(M), int(K), ldx, codes, sf, kc));
     } else {
-      mx_encode_fast_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(x), int(M), int(K), ldx, codes, sf,
-                                                         kc);
+      CK(launch_pdl(mx_encode_fast_kernel<float>, grid, dim3(256), 0, st, static_cast<const float*>(x), int(M), int(K),
+                    ldx, codes, sf, kc));
     }
     LAUNCH_CHECK("mx_encode_fast");
     if (gather_idx) {
@@ -473,6 +493,79 @@ int serq_linear_info(const serq_linear_t* h, int64_t* N, int64_t* K, int* r, int
   return SERQ_OK;
 }
 
+// Decode (M <= 16): one cluster of S CTAs per 128-row weight tile, split-K,
+// DSMEM reduction (serq_gemm_decode3.cuh).  x != nullptr: the quantizer is
+// fused in (x bf16 [M, K], pitch ldx); codes_out / sf_out optionally receive
+// the quantized activation.
+static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const uint8_t* a_sf,
+                            const __nv_bfloat16* x, int64_t ldx, uint8_t* codes_out, uint8_t* sf_out, int64_t M,
+                            void* y, int64_t ldy, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClSmem));
+    CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClSmem));
+    attr = true;
+  }
+  const bool fuse = x != nullptr;
+  const int tiles = int(cdiv(h->N, 128));
+  const int ks = int(cdiv(h->K / 2, kStepBytes));
+  // CTAs per tile, ~3/4 CTA per SM in total (Llama-2-7B: up_proj 86 tiles -> 1, down_proj 32 -> 3);
+  // measured best among 1..8 for both shapes (tools/decode_probe.py)
+  int S = (3 * sm_count()) / (4 * tiles);
+  if (const char* e = getenv("SERQ_DEC_S")) S = atoi(e);  // diagnostics
+  S = S < 1 ? 1 : (S > 8 ? 8 : S);
+  if (S > ks) S = ks;
+  ClParams cp{};
+  cp.M = int(M);
+  cp.N = int(h->N);
+  cp.K = int(h->K);
+  cp.r = h->r;
+  cp.k_steps = ks;
+  cp.S = S;
+  cp.kc_pad = kc_pad_of(h->K);
+  cp.kc_pad_r = kc_pad_of(h->r > 0 ? h->r : 32);
+  cp.w_ksteps = h->w_ksteps;
+  cp.y = static_cast<__nv_bfloat16*>(y);
+  cp.ldy = ldy;
+  cp.x = x;
+  cp.ldx = ldx;
+  cp.codes_out = codes_out;
+  cp.sf_out = sf_out;
+  DecodeMaps dm;
+  dm.w = h->map_b128;
+  dm.sfw = h->map_sfw;
+  dm.r = h->has_r32 ? h->map_r32 : h->map_b128;
+  dm.sfr = h->has_r32 ? h->map_sfr4 : h->map_sfw;
+  if (fuse) {
+    dm.x = dm.sfx = h->map_b128;  // unused: X is produced in-kernel
+  } else {
+    int rc = make_map(&dm.x, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, kDecN);
+    if (!rc) rc = make_sf_map(&dm.sfx, a_sf, M, h->K);
+    if (rc) return rc;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(tiles * S));
+  cfg.blockDim = dim3(kClThreads);
+  cfg.dynamicSmemBytes = kClSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = unsigned(S);
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  if (fuse) {
+    CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<true>, dm, cp));
+  } else {
+    CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<false>, dm, cp));
+  }
+  LAUNCH_CHECK("serq_mx_decode_cl_kernel");
+  return SERQ_OK;
+}
+
 static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t* a_sf, int64_t M,
                           const uint8_t* xs_codes, const uint8_t* xs_sf, void* y, int64_t ldy, serq_stream_t stream) {
   g_launches = 0;
@@ -516,21 +609,29 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
   p.w_ksteps = h->w_ksteps;
   p.dbg = g_debug_flags;
   p.dbg_ts = g_debug_ts;
+  if (M <= kDecN && (h->r == 0 || h->has_r32) && !(g_debug_flags & (2048 | (1 << 22))))
+    return launch_decode_cl(h, a_codes, a_sf, nullptr, 0, nullptr, nullptr, M, y, ldy, S(stream));
   if (M <= kDecN && (h->r == 0 || h->has_r32) && !(g_debug_flags & 2048)) {
+    // diagnostics: SERQ_DEC="stages,ctas_per_sm" overrides the pipeline depth / split policy
+    int dec_stages = kDecStagesDefault, dec_cps = 2;
+    if (const char* e = getenv("SERQ_DEC")) sscanf(e, "%d,%d", &dec_stages, &dec_cps);
     static bool attrd = false;
     if (!attrd) {
-      CK(cudaFuncSetAttribute(serq_mx_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem));
+      CK(cudaFuncSetAttribute(serq_mx_decode_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, dec_smem(2)));
+      CK(cudaFuncSetAttribute(serq_mx_decode_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, dec_smem(3)));
+      CK(cudaFuncSetAttribute(serq_mx_decode_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, dec_smem(4)));
+      CK(cudaFuncSetAttribute(serq_mx_decode_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, dec_smem(5)));
+      CK(cudaFuncSetAttribute(serq_mx_decode_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, dec_smem(8)));
       attrd = true;
     }
     serq_linear* hm = const_cast<serq_linear*>(h);
     const int tiles = int(cdiv(h->N, 128));
     const int ksteps = p.k_steps;
-    // one wave: at most two resident CTAs per SM (100 KB smem each)
-    int want = int((2 * sm_count()) / tiles);
+    int want = int((dec_cps * sm_count()) / tiles);
     want = want < 1 ? 1 : (want > ksteps ? ksteps : want);
     int per = int(cdiv(ksteps, want));
     int splits = int(cdiv(ksteps, per));
-    while (splits > 1 && int64_t(splits) * tiles > 2 * sm_count()) {
+    while (splits > 1 && int64_t(splits) * tiles > dec_cps * sm_count()) {
       ++per;
       splits = int(cdiv(ksteps, per));
     }
@@ -575,14 +676,20 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(tiles), unsigned(splits));
     cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = kDecSmem;
+    cfg.dynamicSmemBytes = dec_smem(dec_stages);
     cfg.stream = S(stream);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_kernel, dm, dp));
+    switch (dec_stages) {
+      case 2: CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_kernel<2>, dm, dp)); break;
+      case 3: CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_kernel<3>, dm, dp)); break;
+      case 4: CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_kernel<4>, dm, dp)); break;
+      case 8: CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_kernel<8>, dm, dp)); break;
+      default: CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_kernel<5>, dm, dp)); break;
+    }
     LAUNCH_CHECK("serq_mx_decode_kernel");
     return SERQ_OK;
   }
@@ -703,6 +810,17 @@ int serq_forward_mx(serq_linear_t* h, const void* x, int dtype, int64_t M, int64
   const bool gather = h->r > 0 && !h->contiguous;
   if (gather && (!gather_idx || !xs_codes || !xs_sf))
     return fail(SERQ_EINVAL, "non-contiguous salient set needs gather_idx and the xs buffers");
+  if (M <= kDecN && (h->r == 0 || h->has_r32) && dtype == SERQ_BF16 && !gather &&
+      !(reinterpret_cast<uintptr_t>(x) & 15) && ldx % 8 == 0 && ldx >= h->K && (g_debug_flags & (1 << 23)) &&
+      !(g_debug_flags & 2048)) {
+    // decode with the quantizer inside the linear (opt-in, debug flag 1<<23): measured
+    // slower than quantizer kernel + PDL-chained linear for Llama-2-7B up_proj (9.2 vs
+    // 8.3 us/layer at M=1) -- 86 x S CTAs re-read the same bf16 rows (tools/decode_probe.py)
+    g_launches = 0;
+    if (ldy < h->N || ldy % 8) return fail(SERQ_EINVAL, "ldy must be >= N and a multiple of 8");
+    return launch_decode_cl(h, nullptr, nullptr, static_cast<const __nv_bfloat16*>(x), ldx, codes, sf, M, y, ldy,
+                            S(stream));
+  }
   // the linear is launched with programmatic dependent launch: its prologue and
   // weight stream overlap the quantizer (a per-row-tile counter hand-off was
   // measured slower: 45.1 vs 43.0 us at 4096^3, tools/fuse_probe.py)

@@ -16,13 +16,14 @@
 namespace serq {
 
 constexpr int kDecN = 16;                       // tokens per MMA (padded)
-constexpr int kDecStages = 5;  // 100 KB: two CTAs per SM
+constexpr int kDecStagesDefault = 5;  // 100 KB: two CTAs per SM
 constexpr int kDecW = 128 * kStepBytes;         // 16 KB weight tile per 256-K step
 constexpr int kDecX = kDecN * kStepBytes;       // 2 KB token tile
 constexpr int kDecSF = 1024;                    // 2 SF chunks of one 128-row block
 constexpr int kDecStage = kDecW + kDecX + 2 * kDecSF;  // 20 KB (1 KB aligned)
 constexpr int kDecRB = 128 * 32;                // R tile: 128 rows x 32 B
-constexpr int kDecSmem = 1024 + kDecStages * kDecStage + kDecRB + 512 + 256;
+constexpr int dec_smem(int stages) { return 1024 + stages * kDecStage + kDecRB + 512 + 256; }
+constexpr int kDecSmem = dec_smem(kDecStagesDefault);
 static_assert(kDecStage % 1024 == 0, "stage alignment");
 
 struct DecodeMaps {
@@ -42,6 +43,7 @@ struct DecodeParams {
   int64_t ldy;
 };
 
+template <int kDecStages>
 __global__ void __launch_bounds__(128, 1) serq_mx_decode_kernel(const __grid_constant__ DecodeMaps maps,
                                                                 const DecodeParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];

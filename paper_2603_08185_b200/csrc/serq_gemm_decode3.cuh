@@ -1,0 +1,316 @@
+// serq_gemm_decode3.cuh -- MXFP4 SERQ linear for decode (M <= 16): cluster
+// split-K with a DSMEM reduction, optionally with the activation quantizer
+// fused in.
+//
+// Swap-AB as in serq_gemm_decode.cuh: weight rows are the MMA's M (128 per
+// tile), the <= 16 tokens its N (tcgen05.mma.cta_group::1.kind::mxf4,
+// 128x16x64).  Each 128-row weight tile is handled by a CLUSTER of S CTAs
+// (S = cluster size, <= 8) that split its K steps; the S fp32 partials
+// (128 x 16 each) meet in the rank-0 CTA's shared memory over DSMEM and are
+// summed in rank (= K) order -- deterministic, no global workspace, no flags,
+// no float atomics.  (A global-memory reduction costs ~3 L2 round trips on the
+// critical path of every layer, ~3 us measured; DSMEM ~0.2 us.)
+//
+// Fused quantizer (kFuse): the epilogue warps, idle during the main loop,
+// read the bf16 activations of each K step (16 rows x 256 columns, L2
+// resident), encode them exactly like mx_encode (mxfmt.py:97-108: block
+// exponent from the 32-block amax, RNE-to-E2M1 with saturation, -0 -> +0) and
+// write the codes (128B-swizzled, the layout a TMA box would produce) and the
+// E8M0 scale factors straight into the pipeline stage next to the TMA-loaded
+// weights.  This removes the separate quantizer kernel and its two
+// kernel-boundary dependencies from every decode step.
+//
+// Sized for layer-to-layer overlap: ~107 KB of shared memory and 64 TMEM
+// columns per CTA, so the NEXT linear's CTA fits on the same SM; with
+// programmatic dependent launch (trigger at CTA start) it streams its first
+// weight stages while this one finishes.
+#pragma once
+#include "serq_gemm_decode.cuh"
+#include "serq_gemm_i8.cuh"  // mbar_wait_cluster
+#include "serq_quant.cuh"    // MX encode helpers
+
+namespace serq {
+
+constexpr int kClStages = 5;
+constexpr int kClThreads = 192;
+constexpr int kClSmem = 1024 + kClStages * kDecStage + kDecRB + 512 + 512;
+static_assert(kClSmem <= 116 * 1024, "two CTAs (this linear and the next) must fit on one SM");
+static_assert(7 * 128 * kDecN * 4 <= kClStages * kDecStage, "rank-0 reduction buffer reuses the stages");
+
+struct ClParams {
+  int M, N, K, r;
+  int k_steps, S;        // K steps per tile, CTAs per tile (cluster size)
+  int kc_pad, kc_pad_r, w_ksteps;
+  __nv_bfloat16* y;
+  int64_t ldy;
+  // fused quantizer: bf16 activations (row pitch ldx); the tile-0 cluster also
+  // writes the quantized activation (codes [M, K/2], scale factors tiled) if non-null
+  const __nv_bfloat16* x;
+  int64_t ldx;
+  uint8_t* codes_out;
+  uint8_t* sf_out;
+};
+
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+template <bool kFuse>
+__global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const __grid_constant__ DecodeMaps maps,
+                                                                          const ClParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* rbuf = smem + kClStages * kDecStage;  // R tile (4 KB) + R scale factors (512 B)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rbuf + kDecRB + 512);
+  uint64_t* full = bars;                  // [kClStages]
+  uint64_t* empty = bars + kClStages;     // [kClStages]
+  uint64_t* rfull = bars + 2 * kClStages;
+  uint64_t* done = rfull + 1;             // accumulator complete
+  uint64_t* red_free = done + 1;          // rank > 0: rank 0's buffer may be written
+  uint64_t* red_full = red_free + 1;      // rank 0: every partial has landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_full + 1);
+
+  pdl_launch_dependents();  // the next linear may launch once every CTA is resident
+  const uint32_t warp = threadIdx.x >> 5;
+  const int S = p.S;
+  const int rank = int(cluster_rank());
+  const int tile = int(blockIdx.x) / S;
+  const int n0 = tile * 128;
+  const int k0 = (rank * p.k_steps) / S, k1 = ((rank + 1) * p.k_steps) / S;
+  const int nsteps = k1 - k0;
+  const bool with_r = p.r > 0 && rank == 0;
+  constexpr uint32_t kWBytes = kDecW + kDecSF;  // TMA bytes per stage when X is produced in-kernel
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&maps.w);
+    tma_prefetch(&maps.sfw);
+    if (!kFuse) {
+      tma_prefetch(&maps.x);
+      tma_prefetch(&maps.sfx);
+    }
+    for (int s = 0; s < kClStages; ++s) {
+      mbar_init(&full[s], kFuse ? 1 + 4 : 1);  // + one arrival per X-producing warp
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(rfull, 1);
+    mbar_init(done, 1);
+    mbar_init(red_free, 1);
+    mbar_init(red_full, S > 1 ? (S - 1) * 128 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<64>(tmem_slot);
+  if (kFuse) {
+    // X scale-factor atoms: rows 16..127 of each 512-B atom are never produced; give them a finite scale
+    for (int s = 0; s < kClStages; ++s)
+      for (int b = threadIdx.x; b < 2 * 512 / 16; b += blockDim.x)
+        reinterpret_cast<uint4*>(smem + s * kDecStage + kDecW + kDecX + kDecSF)[b] = make_uint4(
+            0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
+    fence_proxy_async_smem();
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barrier inits visible cluster-wide before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // [0,16) accumulator, [16,24) SFA, [24,32) SFB, [32,36) R SFA
+
+  if (warp == 0) {
+    if (elect_one()) {
+      auto load_w = [&](int s, int kk) {
+        uint8_t* st = smem + s * kDecStage;
+        mbar_expect_tx(&full[s], kFuse ? kWBytes : kDecStage);
+        tma_load_2d(st, &maps.w, &full[s], 0, (tile * p.w_ksteps + kk) * 128, kEvictFirst);
+        tma_load_2d(st + kDecW + kDecX, &maps.sfw, &full[s], 0, (tile * p.kc_pad + 2 * kk) * 4, kEvictFirst);
+      };
+      if (with_r) {  // R does not depend on the previous kernel either
+        mbar_expect_tx(rfull, kDecRB + 512);
+        tma_load_2d(rbuf, &maps.r, rfull, 0, n0, kEvictFirst);
+        tma_load_2d(rbuf + kDecRB, &maps.sfr, rfull, 0, (tile * p.kc_pad_r) * 4, kEvictFirst);
+      }
+      const int pre = min(nsteps, kClStages);
+      for (int i = 0; i < pre; ++i) load_w(i, k0 + i);
+      if (!kFuse) pdl_wait();  // activation codes come from the quantizer kernel
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = i % kClStages;
+        if (i >= pre) {
+          mbar_wait(&empty[s], ((i / kClStages) & 1) ^ 1);
+          load_w(s, k0 + i);
+        }
+        if (!kFuse) {
+          uint8_t* st = smem + s * kDecStage;
+          tma_load_2d(st + kDecW, &maps.x, &full[s], (k0 + i) * kStepBytes, 0, kEvictLast);
+          tma_load_2d(st + kDecW + kDecX + kDecSF, &maps.sfx, &full[s], 0, (2 * (k0 + i)) * 4, kEvictLast);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t id0 = idesc_mxf4(128, kDecN), id1 = id0 | (2u << 4) | (2u << 29);
+      const uint32_t acc = tmem, sfa = tmem + 16, sfb = tmem + 24, sfr = tmem + 32;
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = i % kClStages;
+        mbar_wait(&full[s], (i / kClStages) & 1);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + s * kDecStage);
+        const uint64_t a = make_sdesc(st, 16, 1024, 2), b = make_sdesc(st + kDecW, 16, 1024, 2);
+        const uint32_t sa = st + kDecW + kDecX, sb = sa + kDecSF;
+        tmem_cp_32x128b_x4(sfa, make_sdesc(sa, 128, 128, 0));
+        tmem_cp_32x128b_x4(sfa + 4, make_sdesc(sa + 512, 128, 128, 0));
+        tmem_cp_32x128b_x4(sfb, make_sdesc(sb, 128, 128, 0));
+        tmem_cp_32x128b_x4(sfb + 4, make_sdesc(sb + 512, 128, 128, 0));
+        mma_mxf4(acc, a, b, id0, sfa, sfb, i > 0 ? 1u : 0u);
+        mma_mxf4(acc, a + 2, b + 2, id1, sfa | (2u << 30), sfb | (2u << 30), 1u);
+        mma_mxf4(acc, a + 4, b + 4, id0, sfa + 4, sfb + 4, 1u);
+        mma_mxf4(acc, a + 6, b + 6, id1, (sfa + 4) | (2u << 30), (sfb + 4) | (2u << 30), 1u);
+        if (with_r && i == 0) {
+          // salient term: A = R rows (K = r = 64), B = K-tile 0 of X (this stage), SFB = X chunk 0
+          mbar_wait(rfull, 0);
+          tc_fence_after();
+          tmem_cp_32x128b_x4(sfr, make_sdesc(smem_u32(rbuf + kDecRB), 128, 128, 0));
+          mma_mxf4(acc, make_sdesc(smem_u32(rbuf), 16, 256, 6), b, id0, sfr, sfb, 1u);
+        }
+        tc_commit(&empty[s]);
+      }
+      if (nsteps > 0) tc_commit(done);
+      else mbar_arrive(done);
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ warps 2..5
+    const uint32_t q = warp & 3;  // TMEM lane quadrant
+    const int et = int(q * 32 + lane_id());
+    pdl_wait();  // X (fused) / Y writes after the previous kernel
+    if constexpr (kFuse) {
+      // X producer: thread -> (token row m, 32-block part) of each K step
+      const int m = et >> 3, part = et & 7;
+      const bool row_ok = m < p.M;
+      const bool write_out = p.codes_out != nullptr && tile == 0 && row_ok;
+      auto load_x = [&](int kk, uint4 (&v)[4]) {
+        const bool ok = row_ok && kk * 256 + part * 32 < p.K;  // K % 32 == 0: blocks are all in or all out
+        const uint4* src = reinterpret_cast<const uint4*>(p.x + int64_t(m) * p.ldx + kk * 256 + part * 32);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = ok ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+      };
+      auto put_x = [&](int i, const uint4 (&cur)[4]) {
+        const int s = i % kClStages;
+        const int kk = k0 + i;
+        // 32-element block: amax over |x| bit patterns, exponent, RNE-to-E2M1 (as mx_encode_fast_kernel)
+        uint32_t w[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          w[4 * c] = cur[c].x;
+          w[4 * c + 1] = cur[c].y;
+          w[4 * c + 2] = cur[c].z;
+          w[4 * c + 3] = cur[c].w;
+        }
+        uint32_t m2 = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) m2 = __vmaxu2(m2, w[k] & 0x7FFF7FFFu);
+        const uint32_t amax = max(m2 & 0xFFFFu, m2 >> 16);
+        const int e = mx_block_exp_bf16bits(amax);
+        const float inv = __uint_as_float(uint32_t(127 - e) << 23);
+        uint32_t pk[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t packed = 0;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const uint32_t wv = w[4 * k + h];
+            packed |= cvt_e2m1x2_raw(__uint_as_float(wv << 16) * inv, __uint_as_float(wv & 0xFFFF0000u) * inv)
+                      << (8 * h);
+          }
+          pk[k] = canon_neg_zero(packed);
+        }
+        if (i >= kClStages) mbar_wait(&empty[s], ((i / kClStages) & 1) ^ 1);
+        uint8_t* st = smem + s * kDecStage;
+        // codes: row m, 16-B chunk `part` of the 128-B row, 128B swizzle (chunk ^ row % 8)
+        st_shared_v4(smem_u32(st + kDecW + m * 128 + ((part ^ (m & 7)) * 16)), pk[0], pk[1], pk[2], pk[3]);
+        // scale factor: chunk part/4, atom row m, byte part%4
+        st[kDecW + kDecX + kDecSF + (part >> 2) * 512 + m * 16 + (part & 3)] = uint8_t(e + 127);
+        if (write_out && kk * 256 + part * 32 < p.K) {
+          *reinterpret_cast<uint4*>(p.codes_out + int64_t(m) * (p.K / 2) + kk * 128 + part * 16) =
+              make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          p.sf_out[sf_offset(m, kk * 8 + part, p.kc_pad)] = uint8_t(e + 127);
+        }
+        fence_proxy_async_smem();  // generic-proxy smem writes -> the tensor core's async proxy
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&full[s]);
+      };
+      // three K steps of activations in flight (L2 latency), converted in order
+      uint4 b0[4], b1[4], b2[4];
+      if (nsteps > 0) load_x(k0, b0);
+      if (nsteps > 1) load_x(k0 + 1, b1);
+      if (nsteps > 2) load_x(k0 + 2, b2);
+      for (int i = 0; i < nsteps; i += 3) {
+        put_x(i, b0);
+        if (i + 3 < nsteps) load_x(k0 + i + 3, b0);
+        if (i + 1 < nsteps) put_x(i + 1, b1);
+        if (i + 4 < nsteps) load_x(k0 + i + 4, b1);
+        if (i + 2 < nsteps) put_x(i + 2, b2);
+        if (i + 5 < nsteps) load_x(k0 + i + 5, b2);
+      }
+    }
+    // ---- accumulator -> Y (S == 1) or the rank-0 DSMEM reduction
+    mbar_wait(done, 0);
+    tc_fence_after();
+    uint32_t v[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(tmem + ((q * 32u) << 16)));
+    tmem_ld_wait();
+    if (nsteps == 0) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = 0u;
+    }
+    const int row = et;  // TMEM lane = weight row within the tile
+    float out[kDecN];
+#pragma unroll
+    for (int j = 0; j < kDecN; ++j) out[j] = __uint_as_float(v[j]);
+    bool store = true;
+    if (S > 1) {
+      float* red = reinterpret_cast<float*>(smem);  // rank 0: [S-1][128][16] fp32 (the stages are drained)
+      if (rank == 0) {
+        // every MMA of this CTA is complete, so its stage memory is free: invite the partials
+        if (et < S - 1) mbar_arrive_release_cluster(map_rank(smem_u32(red_free), uint32_t(et + 1)));
+        mbar_wait_cluster(red_full, 0);
+        for (int sl = 0; sl < S - 1; ++sl) {
+          const float4* src = reinterpret_cast<const float4*>(red + (size_t(sl) * 128 + row) * kDecN);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float4 t4 = src[k];
+            out[4 * k] += t4.x;
+            out[4 * k + 1] += t4.y;
+            out[4 * k + 2] += t4.z;
+            out[4 * k + 3] += t4.w;
+          }
+        }
+      } else {
+        mbar_wait_cluster(red_free, 0);
+        const uint32_t dst = map_rank(smem_u32(red + (size_t(rank - 1) * 128 + row) * kDecN), 0u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) st_cluster_v4(dst + 16 * k, out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+        mbar_arrive_release_cluster(map_rank(smem_u32(red_full), 0u));
+        store = false;
+      }
+    }
+    const int n = n0 + row;
+    if (store && n < p.N) {
+#pragma unroll
+      for (int m = 0; m < kDecN; ++m)
+        if (m < p.M) p.y[m * p.ldy + n] = __float2bfloat16_rn(out[m]);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // no CTA leaves while a peer may still touch its shared memory
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<64>(tmem);
+  }
+}
+
+}  // namespace serq

@@ -194,7 +194,13 @@ __global__ void __launch_bounds__(256) mx_encode_fast_kernel(const T* __restrict
   const int c8 = blockIdx.x * 256 + threadIdx.x;  // 8-element group within the row
   const int r0 = blockIdx.y * kMxRows;
   const bool col_ok = c8 < (K >> 3);
+  // the grid also covers the scale-factor padding (rows up to the 128-row block,
+  // blocks up to kc_pad chunks): those get the finite scale of a zero block, so
+  // no memset (which would break the programmatic-dependent-launch chain) is needed
+  const bool sf_col_ok = c8 < kc_pad * 16;
+  const int m_sf = ((M + 127) >> 7) << 7;
   pdl_launch_dependents();  // the linear may start streaming its weights now
+  pdl_wait();               // launched as a dependent itself: x comes from the previous kernel
   if constexpr (In<T>::kId == 0) {
     const uint4* src = reinterpret_cast<const uint4*>(x + int64_t(r0) * ldx) + c8;
     const int64_t stride = ldx >> 3;
@@ -222,10 +228,8 @@ __global__ void __launch_bounds__(256) mx_encode_fast_kernel(const T* __restrict
         packed |= cvt_e2m1x2_raw(__uint_as_float(w[i] << 16) * inv, __uint_as_float(w[i] & 0xFFFF0000u) * inv)
                   << (8 * i);
       const int row = r0 + rr;
-      if (col_ok && row < M) {
-        dst[int64_t(rr) * (K >> 3)] = canon_neg_zero(packed);
-        if ((threadIdx.x & 3) == 0) sf[sf0 + size_t(((r0 + rr) & 31)) * 16] = uint8_t(e + 127);
-      }
+      if (col_ok && row < M) dst[int64_t(rr) * (K >> 3)] = canon_neg_zero(packed);
+      if (sf_col_ok && row < m_sf && (threadIdx.x & 3) == 0) sf[sf0 + size_t(((r0 + rr) & 31)) * 16] = uint8_t(e + 127);
     }
   } else {
     float v[kMxRows][8];
@@ -255,10 +259,8 @@ __global__ void __launch_bounds__(256) mx_encode_fast_kernel(const T* __restrict
       uint32_t packed = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) packed |= cvt_e2m1x2_raw(v[rr][2 * i] * inv, v[rr][2 * i + 1] * inv) << (8 * i);
-      if (col_ok && row < M) {
-        reinterpret_cast<uint32_t*>(codes + int64_t(row) * (K >> 1))[c8] = canon_neg_zero(packed);
-        if ((threadIdx.x & 3) == 0) sf[sf_offset(row, c8 >> 2, kc_pad)] = uint8_t(e + 127);
-      }
+      if (col_ok && row < M) reinterpret_cast<uint32_t*>(codes + int64_t(row) * (K >> 1))[c8] = canon_neg_zero(packed);
+      if (sf_col_ok && row < m_sf && (threadIdx.x & 3) == 0) sf[sf_offset(row, c8 >> 2, kc_pad)] = uint8_t(e + 127);
     }
   }
 }

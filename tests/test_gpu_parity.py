@@ -229,17 +229,39 @@ def test_int_linear_gather_int_r(D):
 
 
 @pytest.mark.parametrize("M,K,N,r", [(1, 2048, 1536, 64), (4, 4096, 1024, 64), (16, 2048, 1000, 64),
-                                     (3, 1024, 512, 0), (16, 11008 // 32 * 32, 768, 64)])
+                                     (3, 1024, 512, 0), (16, 11008 // 32 * 32, 768, 64),
+                                     # stream-K partitions: whole tiles per CTA (K=256), tiles split over
+                                     # several CTAs (few tiles, long K), ragged N, 86 tiles on 148 SMs
+                                     (7, 256, 11008, 0), (2, 512, 20000, 64), (16, 11008, 256, 64),
+                                     (5, 8192, 200, 32), (1, 4096, 11008, 64), (16, 11008, 4096, 64),
+                                     (1, 32768, 128, 64)])  # one tile over many CTAs (slot cap 32)
 def test_mx_decode_parity(D, M, K, N, r):
+    from paper_2603_08185_b200 import _lib
+
     x, main_t, comp = _mx_case(M, K, N, r, seed=K + M)
     lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents,
                      comp.r_q.element_codes if r else None, comp.r_q.block_scale_exponents if r else None,
                      np.arange(r) if r else None)
     xt = _cuda(x, torch.bfloat16)
-    for _ in range(2):  # the second call reuses the self-resetting split-K counters
-        y = lin(xt).float().cpu().numpy()
-    mx, mean = O.parity_errors(y, O.forward_mx(x, main_t, comp))
-    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+    ref = O.forward_mx(x, main_t, comp)
+    for _ in range(2):
+        # fused decode (quantizer inside the linear): Y and the activation codes it reports
+        act = D.MxActivation(torch.empty(D.mx_sizes(M, K)[0], dtype=torch.uint8, device="cuda"),
+                             torch.empty(D.mx_sizes(M, K)[1], dtype=torch.uint8, device="cuda"), M, K)
+        _lib.load().serq_set_debug_flags(1 << 23)  # the fused-quantizer decode kernel is opt-in
+        try:
+            y = lin.forward(xt, act).float().cpu().numpy()
+        finally:
+            _lib.load().serq_set_debug_flags(0)
+        mx, mean = O.parity_errors(y, ref)
+        assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+        c, e = D.unpack_mx(act.codes, act.sf, M, K)
+        enc = O.mx_encode(x, 32)
+        assert np.array_equal(c.cpu().numpy(), enc.element_codes)
+        assert np.array_equal(e.cpu().numpy(), enc.block_scale_exponents)
+        # two-kernel path (quantizer, then the linear on codes)
+        y2 = lin.gemm(lin.quantize(xt)).float().cpu().numpy()
+        assert np.array_equal(y2, y)
 
 
 def test_mx_linear_split_last_wave(D):
