@@ -12,7 +12,6 @@
 #include "serq_gemm_mx.cuh"
 #include "serq_gemm_mx2.cuh"
 #include "serq_gemm_mx3.cuh"
-#include "serq_gemm_decode.cuh"
 #include "serq_gemm_decode3.cuh"
 #include "serq_gemm_i8.cuh"
 #include "serq_quant.cuh"
@@ -164,10 +163,6 @@ struct serq_linear {
   int64_t sk_ws_floats = 0;
   int* sk_cnt = nullptr;
   int64_t sk_cnt_n = 0;
-  // decode split-K workspace: fp32 partials + per-tile arrival counters
-  float* dec_ws = nullptr;
-  int64_t dec_ws_floats = 0;
-  int* dec_cnt = nullptr;
   // end-to-end scratch
   int64_t ws_m = 0;
   void* ws_x = nullptr;
@@ -182,7 +177,7 @@ struct serq_linear {
 namespace {
 void free_handle(serq_linear* h) {
   void* ptrs[] = {h->w, h->sfw, h->rbuf, h->sfr, h->sw, h->colsum, h->sr, h->colsum_r,
-                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y, h->dec_ws, h->dec_cnt, h->sk_ws, h->sk_cnt, h->w4};
+                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y, h->sk_ws, h->sk_cnt, h->w4};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : h->e2e_ev)
@@ -609,90 +604,8 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
   p.w_ksteps = h->w_ksteps;
   p.dbg = g_debug_flags;
   p.dbg_ts = g_debug_ts;
-  if (M <= kDecN && (h->r == 0 || h->has_r32) && !(g_debug_flags & (2048 | (1 << 22))))
+  if (M <= kDecN && (h->r == 0 || h->has_r32) && !(g_debug_flags & 2048))
     return launch_decode_cl(h, a_codes, a_sf, nullptr, 0, nullptr, nullptr, M, y, ldy, S(stream));
-  if (M <= kDecN && (h->r == 0 || h->has_r32) && !(g_debug_flags & 2048)) {
-    // diagnostics: SERQ_DEC="stages,ctas_per_sm" overrides the pipeline depth / split policy
-    int dec_stages = kDecStagesDefault, dec_cps = 2;
-    if (const char* e = getenv("SERQ_DEC")) sscanf(e, "%d,%d", &dec_stages, &dec_cps);
-    static bool attrd = false;
-    if (!attrd) {
-      CK(cudaFuncSetAttribute(serq_mx_decode_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, dec_smem(2)));
-      CK(cudaFuncSetAttribute(serq_mx_decode_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, dec_smem(3)));
-      CK(cudaFuncSetAttribute(serq_mx_decode_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, dec_smem(4)));
-      CK(cudaFuncSetAttribute(serq_mx_decode_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, dec_smem(5)));
-      CK(cudaFuncSetAttribute(serq_mx_decode_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, dec_smem(8)));
-      attrd = true;
-    }
-    serq_linear* hm = const_cast<serq_linear*>(h);
-    const int tiles = int(cdiv(h->N, 128));
-    const int ksteps = p.k_steps;
-    int want = int((dec_cps * sm_count()) / tiles);
-    want = want < 1 ? 1 : (want > ksteps ? ksteps : want);
-    int per = int(cdiv(ksteps, want));
-    int splits = int(cdiv(ksteps, per));
-    while (splits > 1 && int64_t(splits) * tiles > dec_cps * sm_count()) {
-      ++per;
-      splits = int(cdiv(ksteps, per));
-    }
-    if (splits > 1) {
-      const int64_t need = int64_t(splits) * tiles * 128 * kDecN;
-      if (need > hm->dec_ws_floats) {
-        if (hm->dec_ws) cudaFree(hm->dec_ws);
-        hm->dec_ws = nullptr;
-        CK(cudaMalloc(&hm->dec_ws, need * 4));
-        hm->dec_ws_floats = need;
-      }
-      if (!hm->dec_cnt) {
-        CK(cudaMalloc(&hm->dec_cnt, 4 * cdiv(h->N, 128) + 4096));
-        CK(cudaMemsetAsync(hm->dec_cnt, 0, 4 * cdiv(h->N, 128) + 4096, S(stream)));
-      }
-    }
-    DecodeMaps dm;
-    dm.w = h->map_b128;
-    rc = make_map(&dm.x, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, kDecN);
-    if (!rc) rc = make_sf_map(&dm.sfx, a_sf, M, h->K);
-    if (rc) return rc;
-    dm.sfw = h->map_sfw;
-    dm.r = h->has_r32 ? h->map_r32 : h->map_b128;
-    dm.sfr = h->has_r32 ? h->map_sfr4 : h->map_sfw;
-    DecodeParams dp{};
-    dp.M = int(M);
-    dp.N = int(h->N);
-    dp.K = int(h->K);
-    dp.r = h->r;
-    dp.k_steps = ksteps;
-    dp.splits = splits;
-    dp.kc_pad = p.kc_pad;
-    dp.kc_pad_r = p.kc_pad_r;
-    dp.w_ksteps = h->w_ksteps;
-    dp.dbg_ts = g_debug_ts;
-    dp.ws = hm->dec_ws;
-    dp.counters = hm->dec_cnt;
-    dp.y = static_cast<__nv_bfloat16*>(y);
-    dp.ldy = ldy;
-    // programmatic dependent launch: overlap this kernel's prologue and weight
-    // stream with the tail of the quantizer that produced a_codes / a_sf
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(tiles), unsigned(splits));
-    cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = dec_smem(dec_stages);
-    cfg.stream = S(stream);
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    switch (dec_stages) {
-      case 2: CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_kernel<2>, dm, dp)); break;
-      case 3: CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_kernel<3>, dm, dp)); break;
-      case 4: CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_kernel<4>, dm, dp)); break;
-      case 8: CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_kernel<8>, dm, dp)); break;
-      default: CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_kernel<5>, dm, dp)); break;
-    }
-    LAUNCH_CHECK("serq_mx_decode_kernel");
-    return SERQ_OK;
-  }
   if (M > 128 && (h->r == 0 || h->has_r32) && !(g_debug_flags & (16 | 512))) {
     static bool attr3 = false;
     if (!attr3) {

@@ -2,9 +2,11 @@
 // split-K with a DSMEM reduction, optionally with the activation quantizer
 // fused in.
 //
-// Swap-AB as in serq_gemm_decode.cuh: weight rows are the MMA's M (128 per
-// tile), the <= 16 tokens its N (tcgen05.mma.cta_group::1.kind::mxf4,
-// 128x16x64).  Each 128-row weight tile is handled by a CLUSTER of S CTAs
+// Swap-AB: D^T[128 weight rows, 16 tokens] = W_tile[128, K] . X^T -- weight
+// rows are the MMA's M (128 per tile), the zero-padded <= 16 tokens its N
+// (tcgen05.mma.cta_group::1.kind::mxf4, 128x16x64).  The tensor work is tiny;
+// the kernel is bound by HBM bytes
+//     N*K/2 (codes) + N*K/32 (E8M0) + N*r/2 + N*r/32 (R) + M*K*(1/2 + 1/32) (X) + 2*M*N (Y).  Each 128-row weight tile is handled by a CLUSTER of S CTAs
 // (S = cluster size, <= 8) that split its K steps; the S fp32 partials
 // (128 x 16 each) meet in the rank-0 CTA's shared memory over DSMEM and are
 // summed in rank (= K) order -- deterministic, no global workspace, no flags,
@@ -25,11 +27,23 @@
 // programmatic dependent launch (trigger at CTA start) it streams its first
 // weight stages while this one finishes.
 #pragma once
-#include "serq_gemm_decode.cuh"
+#include "serq_gemm.cuh"
 #include "serq_gemm_i8.cuh"  // mbar_wait_cluster
 #include "serq_quant.cuh"    // MX encode helpers
 
 namespace serq {
+
+constexpr int kDecN = 16;                              // tokens per MMA (padded)
+constexpr int kDecW = 128 * kStepBytes;                // 16 KB weight tile per 256-K step
+constexpr int kDecX = kDecN * kStepBytes;              // 2 KB token tile
+constexpr int kDecSF = 1024;                           // 2 SF chunks of one 128-row block
+constexpr int kDecStage = kDecW + kDecX + 2 * kDecSF;  // 20 KB (1 KB aligned)
+constexpr int kDecRB = 128 * 32;                       // R tile: 128 rows x 32 B (r <= 64)
+static_assert(kDecStage % 1024 == 0, "stage alignment");
+
+struct DecodeMaps {
+  CUtensorMap w, x, sfw, sfx, r, sfr;
+};
 
 constexpr int kClStages = 5;
 constexpr int kClThreads = 192;
