@@ -41,6 +41,55 @@ def graph_of(fn):
     return g
 
 
+def time_in_graph(fn, flush: Flusher | None = None, n=20, warm=3) -> float:
+    """Median device time (ms) of fn() measured by CUDA event-record nodes INSIDE
+    one captured graph [flush, event, fn, event]: excludes the graph launch
+    latency (~6 us for a one-kernel graph on this box) and the L2 flush."""
+    a = torch.cuda.Event(enable_timing=True, external=True)
+    b = torch.cuda.Event(enable_timing=True, external=True)
+
+    def body():
+        if flush is not None:
+            flush()
+        a.record()
+        fn()
+        b.record()
+
+    g = graph_of(body)
+    ts = []
+    for i in range(n + warm):
+        g.replay()
+        torch.cuda.synchronize()
+        if i >= warm:
+            ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def time_steps(step, n_steps: int, warm: int = 2) -> float:
+    """Device time per step (ms): ONE captured graph [event, step(0), ...,
+    step(n_steps - 1), event], replayed once after `warm` untimed replays.  The
+    caller's step(i) cycles over input / weight sets whose total size exceeds
+    the 126 MB L2, so every step reads cold operands (the alternative to an L2
+    flush between steps); the two event nodes add ~3 us once per graph, not per
+    step (a one-kernel graph timed alone reads ~6 us above the kernel)."""
+    a = torch.cuda.Event(enable_timing=True, external=True)
+    b = torch.cuda.Event(enable_timing=True, external=True)
+
+    def body():
+        a.record()
+        for i in range(n_steps):
+            step(i)
+        b.record()
+
+    g = graph_of(body)
+    for _ in range(warm):
+        g.replay()
+    torch.cuda.synchronize()
+    g.replay()
+    b.synchronize()
+    return a.elapsed_time(b) / n_steps
+
+
 def time_graph(g, flush: Flusher | None, n=20, warm=3):
     ts = []
     for i in range(n + warm):
@@ -92,10 +141,8 @@ def mx_linear_point(lin, M: int, flush: Flusher) -> dict:
     x = outlier_x(M, lin.K)
     act = lin.quantize(x)
     y = torch.empty((M, lin.N), dtype=torch.bfloat16, device="cuda")
-    g_step = graph_of(lambda: (lin.quantize(x, act), lin.gemm(act, y)))
-    g_lin = graph_of(lambda: lin.gemm(act, y))
-    t_step = time_graph(g_step, flush)
-    t_lin = time_graph(g_lin, flush)
+    t_step = time_in_graph(lambda: lin.forward(x, act, y), flush)
+    t_lin = time_in_graph(lambda: lin.gemm(act, y), flush)
     K, N, r = lin.K, lin.N, lin.r
     flops = 2.0 * M * N * (K + r)
     w_bytes = N * K / 2 + N * K / 32 + N * r / 2 + N * r / 32
@@ -128,8 +175,8 @@ def decode_points(hbm_peak_gbs: float, layers: int = 16) -> list:
                 for lin, a, y in zip(lins, acts, ys):
                     lin.gemm(a, y)
 
-            t_step = time_graph(graph_of(run_all), None, n=10) / layers
-            t_lin = time_graph(graph_of(lin_all), None, n=10) / layers
+            t_step = time_in_graph(run_all, None, n=10) / layers
+            t_lin = time_in_graph(lin_all, None, n=10) / layers
             r = 64
             flops = 2.0 * M * N * (K + r)
             w_bytes = N * K / 2 + N * K / 32 + N * r / 2 + N * r / 32
@@ -166,15 +213,22 @@ def device_int_linear(K: int, N: int, r: int, r_mode: str, seed: int = 1):
     return D.IntLinear(codes, s, 4, **kw)
 
 
-def int_linear_point(M, K, N, r, r_mode, bits, symmetric, flush: Flusher) -> dict:
-    lin = device_int_linear(K, N, r, r_mode)
-    x = outlier_x(M, K)
-    act = lin.quantize(x, bits, symmetric)
-    y = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
-    g_step = graph_of(lambda: lin.gemm(lin.quantize(x, bits, symmetric), y))
-    g_lin = graph_of(lambda: lin.gemm(act, y))
-    t_step = time_graph(g_step, flush)
-    t_lin = time_graph(g_lin, flush)
+def int_linear_point(M, K, N, r, r_mode, bits, symmetric, flush: Flusher | None = None, n_steps: int = 16) -> dict:
+    """Steady state over n_steps steps cycling 8 weight sets x 8 activation sets
+    (> L2 at these shapes: cold operands every step, no flush)."""
+    lins = [device_int_linear(K, N, r, r_mode, seed=1 + i) for i in range(8)]
+    xs = [outlier_x(M, K, seed=i) for i in range(8)]
+    acts = [lins[0].quantize(x, bits, symmetric) for x in xs]
+    ys = [torch.empty((M, N), dtype=torch.bfloat16, device="cuda") for _ in xs]
+
+    def step(i):
+        lins[i % 8].gemm(lins[i % 8].quantize(xs[i % 8], bits, symmetric), ys[i % 8])
+
+    def lin_only(i):
+        lins[i % 8].gemm(acts[i % 8], ys[i % 8])
+
+    t_step = time_steps(step, n_steps)
+    t_lin = time_steps(lin_only, n_steps)
     flops = 2.0 * M * N * (K + r)
     return {"M": M, "K": K, "N": N, "r": r, "r_mode": r_mode, "act_bits": bits, "act_symmetric": symmetric,
             "step_us": t_step * 1e3, "linear_us": t_lin * 1e3, "linear_tops": flops / (t_lin * 1e-3) / 1e12,
