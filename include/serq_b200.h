@@ -22,6 +22,8 @@
  *   serq_linear_int        forward_reconstructed int branch: int_gemm_reference(xq, main)
  *                          + R term (int_gemm_reference(xs, r_q) or dequantize(xs) @ r_dense)
  *                                                                         compensate.py:300-316, mxfmt.py:135-195
+ *   serq_linear_int_addend forward_reconstructed int branch, SVD baseline: int_gemm + (x_hat L1) L2
+ *                                                                         compensate.py:300-310
  *   serq_forward_mx        forward_reconstructed(x, main_t, comp, None) on device: mx_encode(x)
  *                          (+ re-encode of x[:, idx]) then the fused GEMM      compensate.py:319-340
  *   serq_forward_mx_host   forward_reconstructed(x, main_t, comp, None) end to end from host memory
@@ -122,6 +124,14 @@ int serq_linear_int(const serq_linear_t* h, const int8_t* a_codes, const float* 
 int serq_forward_mx(serq_linear_t* h, const void* x, int dtype, int64_t M, int64_t ldx, const int32_t* gather_idx,
                     uint8_t* codes, uint8_t* sf, uint8_t* xs_codes, uint8_t* xs_sf, void* y, int64_t ldy,
                     serq_stream_t stream);
+
+/* K3 with an fp32 addend C [M, N] (row pitch N) summed into the output before the
+ * bf16 store: y = bf16(sx * (sw * acc (+ R term)) + C).  Serves the SVD baseline
+ * (compensate.py:304-310), whose two-factor correction (x_hat @ L1) @ L2 spans all
+ * K columns and so cannot ride in the fused salient term. */
+int serq_linear_int_addend(const serq_linear_t* h, const int8_t* a_codes, const float* sx, const int32_t* zp,
+                           int64_t M, const void* xs, const float* addend, void* y, int64_t ldy,
+                           serq_stream_t stream);
 
 /* End to end from HOST memory (pinned for full PCIe rate): copy X (bf16 [M, K])
  * in, quantize, GEMM, copy Y (bf16 [M, N]) out; synchronises `stream`.

@@ -304,12 +304,15 @@ def pack_mx_file_bytes(t: MxT) -> bytes:
 
 @dataclass
 class Comp:
-    """``Compensator`` (compensate.py:48-69), single-matrix modes only."""
+    """``Compensator`` (compensate.py:48-69): one matrix R (rtn_residual /
+    gptq_swapped) or the SVD baseline's two factors L1 [K, r], L2 [r, N]."""
 
     rank: int
-    salient_idx: np.ndarray
+    salient_idx: np.ndarray | None = None
     r_q: object = None
     r_dense: np.ndarray | None = None
+    l1: np.ndarray | None = None
+    l2: np.ndarray | None = None
 
 
 def forward_int(x, main: IntQ, comp: Comp | None, act_cfg: IntCfg, symmetric_act=False):
@@ -328,6 +331,10 @@ def forward_int(x, main: IntQ, comp: Comp | None, act_cfg: IntCfg, symmetric_act
     y = int_gemm(xq, main)
     if comp is None or comp.rank == 0:
         return y, xq
+    if comp.l1 is not None:
+        # SVD baseline (compensate.py:304-310): sequential two-factor product over the
+        # full dequantized activation
+        return y + (dequantize(xq) @ comp.l1) @ comp.l2, xq
     xs = gather_columns(xq, comp.salient_idx)
     if comp.r_dense is not None:
         return y + dequantize(xs) @ comp.r_dense, xq

@@ -115,6 +115,11 @@ class Compensator:
     def __post_init__(self):
         if self.mode not in (RTN_RESIDUAL, GPTQ_SWAPPED, SVD_BASELINE):
             raise ValidationError(f"unknown compensator mode {self.mode!r}")
+        if self.rank and self.mode == SVD_BASELINE:  # compensate.py:59-63
+            if self.l1 is None or self.l2 is None:
+                raise ValidationError("SVD mode carries two factors")
+            if self.r_q is not None or self.r_dense is not None:
+                raise ValidationError("SVD mode must not carry a residual matrix")
         if self.rank and self.mode in (RTN_RESIDUAL, GPTQ_SWAPPED):
             if (self.r_q is not None) + (self.r_dense is not None) != 1:
                 raise ValidationError("single-matrix modes carry exactly one R")
@@ -285,8 +290,19 @@ class SerqLinear:
     def __init__(self, main, comp=None, act_cfg=None, allow_symmetric_act=False, device="cuda"):
         self.fmt = "mx" if _is_mx(main) else "int"
         has_r = comp is not None and getattr(comp, "rank", 0)
+        self.svd = None
         if has_r and getattr(comp, "mode", RTN_RESIDUAL) == SVD_BASELINE:
-            raise ValidationError("the two-factor SVD compensator is not part of the device path")
+            # SVD baseline (compensate.py:209-224, 304-310): INT main through the fused kernel with no
+            # salient term; the two-factor correction (x_hat @ L1) @ L2 spans all K columns, so it runs as
+            # two plain fp32 cuBLAS GEMMs whose result is added in the kernel epilogue before the bf16 store
+            if _is_mx(main):
+                raise ValidationError("the SVD baseline compensates integer mains only")
+            l1 = np.asarray(comp.l1, dtype=np.float64)
+            l2 = np.asarray(comp.l2, dtype=np.float64)
+            if l1.shape != (main.shape[0], comp.rank) or l2.shape != (comp.rank, main.shape[1]):
+                raise ValidationError("SVD factors must be L1 [K, r] and L2 [r, N]")
+            self.svd = (torch.from_numpy(l1).to(device, torch.float32), torch.from_numpy(l2).to(device, torch.float32))
+            comp, has_r = None, 0
         idx = None if not has_r else np.asarray(comp.salient_idx, dtype=np.intp)
         if self.fmt == "mx":
             if getattr(main, "block_size", 32) != 32:
@@ -327,12 +343,23 @@ class SerqLinear:
             self.act_bits, self.act_symmetric = act_cfg.bits, act_cfg.symmetric
             self.K, self.N = main.shape
         self.rank = int(comp.rank) if has_r else 0
+        self.aux_matmuls = 2 if self.svd is not None else (1 if self.rank else 0)
 
     def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
         if x.shape[-1] != self.K:
             raise ValidationError("x columns must equal main rows")
         if self.fmt == "mx":
             return self.impl(x, y)
+        if self.svd is not None:
+            act = self.impl.quantize(x, self.act_bits, self.act_symmetric)
+            l1, l2 = self.svd
+            prev = torch.backends.cuda.matmul.allow_tf32
+            torch.backends.cuda.matmul.allow_tf32 = False  # fp32 products, like the reference's f64 within tolerance
+            try:
+                corr = (D.IntLinear.dequantize(act) @ l1) @ l2
+            finally:
+                torch.backends.cuda.matmul.allow_tf32 = prev
+            return self.impl.gemm(act, y, addend=corr.contiguous())
         return self.impl(x, self.act_bits, self.act_symmetric, y)
 
 
@@ -381,8 +408,10 @@ def forward_reconstructed(x, main, comp, act_cfg, probe: OpProbe | None = None) 
             raise ValidationError("act_cfg must be asymmetric (per-token)")
     lin = _linear_for(main, comp, act_cfg)
     y = lin(_to_gpu(x))
-    if probe is not None and lin.rank:
-        probe.aux_matmuls += 1
+    if probe is not None and lin.aux_matmuls:
+        probe.aux_matmuls += lin.aux_matmuls
+        if lin.svd is not None:
+            probe.notes.append("sequential two-factor path")
     return y.float().cpu().numpy().astype(np.float64)
 
 

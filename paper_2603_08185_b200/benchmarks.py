@@ -235,6 +235,35 @@ def int_linear_point(M, K, N, r, r_mode, bits, symmetric, flush: Flusher | None 
             "step_tops": flops / (t_step * 1e-3) / 1e12, "tokens_per_s": M / (t_step * 1e-3)}
 
 
+def svd_baseline_point(M, K, N, r, bits=8, n_steps: int = 16) -> dict:
+    """The paper's L2QER-style comparison (SVD baseline, compensate.py:209-224,
+    304-310) at an INT shape: the same fused INT kernel without a salient term,
+    plus the two-factor correction (x_hat @ L1) @ L2 as two fp32 cuBLAS GEMMs
+    added in the epilogue.  Factors are random with the right shapes (only the
+    cost is measured here; parity is a test)."""
+    lins = [device_int_linear(K, N, 0, "dense", seed=1 + i) for i in range(8)]
+    g = torch.Generator(device="cuda").manual_seed(5)
+    l1 = torch.randn((K, r), generator=g, device="cuda") * 0.01
+    l2 = torch.randn((r, N), generator=g, device="cuda") * 0.01
+    xs = [outlier_x(M, K, seed=i, frac=0.005, mag=100.0) for i in range(8)]
+    ys = [torch.empty((M, N), dtype=torch.bfloat16, device="cuda") for _ in xs]
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+
+    def step(i):
+        lin = lins[i % 8]
+        act = lin.quantize(xs[i % 8], bits, False)
+        corr = (D.IntLinear.dequantize(act) @ l1) @ l2
+        lin.gemm(act, ys[i % 8], addend=corr)
+
+    try:
+        t = time_steps(step, n_steps)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return {"M": M, "K": K, "N": N, "r": r, "act_bits": bits, "step_us": t * 1e3, "aux_matmuls": 2,
+            "tokens_per_s": M / (t * 1e-3)}
+
+
 def c5_block_point(world: int = 1, rank: int = 0, M: int = 8192, r: int = 128, group=None, steps: int = 5,
                    flush: Flusher | None = None) -> dict:
     """BASELINE C5: Llama-3-70B-shaped decoder-block linears (hidden 8192,

@@ -746,8 +746,9 @@ int serq_forward_mx(serq_linear_t* h, const void* x, int dtype, int64_t M, int64
   return rc;
 }
 
-int serq_linear_int(const serq_linear_t* h, const int8_t* a_codes, const float* sx, const int32_t* zp, int64_t M,
-                    const void* xs, void* y, int64_t ldy, int32_t* acc_dump, int32_t* accr_dump, serq_stream_t stream) {
+static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const float* sx, const int32_t* zp,
+                           int64_t M, const void* xs, void* y, int64_t ldy, const float* addend, int32_t* acc_dump,
+                           int32_t* accr_dump, serq_stream_t stream) {
   g_launches = 0;
   if (!h || h->mode != kModeI8) return fail(SERQ_EINVAL, "handle is not an INT linear");
   if (M <= 0) return fail(SERQ_EINVAL, "x must be non-empty");
@@ -788,6 +789,8 @@ int serq_linear_int(const serq_linear_t* h, const int8_t* a_codes, const float* 
     p.sr = h->sr;
     p.colsum_r = h->colsum_r;
     p.acc_dump = acc_dump;
+  p.addend = addend;
+    p.addend = addend;
     p.accr_dump = accr_dump;
     p.dbg_ts = g_debug_ts;
     const int64_t tiles = cdiv(M, 256) * cdiv(h->N, kBN);
@@ -828,12 +831,26 @@ int serq_linear_int(const serq_linear_t* h, const int8_t* a_codes, const float* 
   p.sr = h->sr;
   p.colsum_r = h->colsum_r;
   p.acc_dump = acc_dump;
+  p.addend = addend;
   p.accr_dump = accr_dump;
   dim3 grid(unsigned(cdiv(M, kBM)), unsigned(cdiv(h->N, kBN)));
   serq_linear_kernel<kModeI8><<<grid, kThreads, kSmemBytes, S(stream)>>>(ma, h->map_b, mxs, h->r ? h->map_r : h->map_b,
                                                                          my, p);
   LAUNCH_CHECK("serq_linear_kernel<i8>");
   return SERQ_OK;
+}
+
+int serq_linear_int(const serq_linear_t* h, const int8_t* a_codes, const float* sx, const int32_t* zp, int64_t M,
+                    const void* xs, void* y, int64_t ldy, int32_t* acc_dump, int32_t* accr_dump, serq_stream_t stream) {
+  return linear_int_impl(h, a_codes, sx, zp, M, xs, y, ldy, nullptr, acc_dump, accr_dump, stream);
+}
+
+int serq_linear_int_addend(const serq_linear_t* h, const int8_t* a_codes, const float* sx, const int32_t* zp,
+                           int64_t M, const void* xs, const float* addend, void* y, int64_t ldy,
+                           serq_stream_t stream) {
+  if (!addend) return fail(SERQ_EINVAL, "addend is NULL");
+  if (reinterpret_cast<uintptr_t>(addend) & 3) return fail(SERQ_EINVAL, "addend must be 4-byte aligned");
+  return linear_int_impl(h, a_codes, sx, zp, M, xs, y, ldy, addend, nullptr, nullptr, stream);
 }
 
 int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* y_host, serq_stream_t stream) {

@@ -67,6 +67,7 @@ struct GemmParams {
   const int32_t* colsum; // [N] sum_k W[k,n] (for the zero-point correction)
   const float* sr;       // [N] R scale (int R)
   const int32_t* colsum_r;
+  const float* addend;   // INT: optional fp32 [M, N] (pitch N) added after scaling (SVD-baseline correction)
   int32_t* acc_dump;     // debug: exact main accumulators (acc - zp*colsum), [M,N]
   int32_t* accr_dump;    // debug: exact R accumulators
   long long* dbg_ts;     // diagnostics: per-iteration clock64 stamps of the MMA warp (CTA 0), or nullptr
@@ -280,6 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           f[i] = y * sx;
+          if (p.addend && row < p.M && n0 + col < p.N) f[i] += p.addend[size_t(row) * p.N + n0 + col];
         }
       }
       // 32 fp32 -> 64 B of bf16 = four 16-B chunks of a 128-B swizzled row

@@ -404,6 +404,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
               f[j] = yv * sx;
             }
           }
+          if (p.addend && row < p.M) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (n0 + int(col0) + j < p.N) f[j] += p.addend[size_t(row) * p.N + n0 + col0 + j];
+          }
           if (p.acc_dump && row < p.M) {
             // debug: exact accumulators (tests)
 #pragma unroll

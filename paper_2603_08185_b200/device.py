@@ -287,15 +287,30 @@ class IntLinear:
     def quantize(self, x: torch.Tensor, bits: int, symmetric: bool) -> IntActivation:
         return quantize_int(x, bits, symmetric, self.salient_idx, self.r, self.xs_kind())
 
-    def gemm(self, act: IntActivation, y=None, acc_dump=None, accr_dump=None) -> torch.Tensor:
+    def gemm(self, act: IntActivation, y=None, acc_dump=None, accr_dump=None,
+             addend: torch.Tensor | None = None) -> torch.Tensor:
         M, K = act.codes.shape
         if K != self.K:
             raise ValidationError("x columns must equal main rows")
         if y is None:
             y = torch.empty((M, self.N), dtype=torch.bfloat16, device=self.device)
+        if addend is not None:
+            if addend.dtype != torch.float32 or tuple(addend.shape) != (M, self.N) or not addend.is_contiguous():
+                raise ValidationError("addend must be a contiguous float32 [M, N] tensor")
+            _lib.call("serq_linear_int_addend", self._h.ptr, act.codes.data_ptr(), act.scale32.data_ptr(),
+                      _ptr(act.zp), M, _ptr(act.xs), addend.data_ptr(), y.data_ptr(), y.stride(0), _stream())
+            return y
         _lib.call("serq_linear_int", self._h.ptr, act.codes.data_ptr(), act.scale32.data_ptr(), _ptr(act.zp), M,
                   _ptr(act.xs), y.data_ptr(), y.stride(0), _ptr(acc_dump), _ptr(accr_dump), _stream())
         return y
+
+    @staticmethod
+    def dequantize(act: IntActivation) -> torch.Tensor:
+        """x_hat = s * (codes - zp) in float32 (quantcore.py:144-150) on the device."""
+        c = act.codes.view(torch.uint8).float() if not act.symmetric else act.codes.float()
+        if act.zp is not None:
+            c = c - act.zp.float()[:, None]
+        return c * act.scale32[:, None]
 
     def __call__(self, x: torch.Tensor, bits: int, symmetric: bool, y=None) -> torch.Tensor:
         return self.gemm(self.quantize(x, bits, symmetric), y)

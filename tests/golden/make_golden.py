@@ -23,7 +23,9 @@ if REF not in sys.path:
 
 from serq.compensate import (  # noqa: E402
     Compensator,
+    OpProbe,
     build_serq_rtn,
+    build_svd_baseline,
     build_serq_rtn_mx,
     forward_reconstructed,
 )
@@ -190,6 +192,14 @@ def main():
                             IntQuantConfig(4, True, r, "row"))
     g["fint_g16_y"] = forward_reconstructed(xi, m2, c2, per_token_config(8))
     g["fint_g16_idx"] = plan_i.salient_idx
+
+    # -- SVD baseline (two-factor L1 L2 over the full quantization error, compensate.py:209-224, 304-310)
+    main_s, comp_s = build_svd_baseline(wi, IntQuantConfig(4, True, k, "row"), 8)
+    probe = OpProbe()
+    g["fsvd_y_a8"] = forward_reconstructed(xi, main_s, comp_s, per_token_config(8), probe)
+    g["fsvd_aux"] = np.array(probe.aux_matmuls)
+    g["fsvd_l1"], g["fsvd_l2"] = comp_s.l1, comp_s.l2
+    g["fsvd_codes"], g["fsvd_scales"] = main_s.codes, main_s.scales
 
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)/1e6:.2f} MB, {len(g)} arrays)")

@@ -54,7 +54,11 @@ def test_layouts_integer_cores_cannot_evaluate_are_rejected():
         api.forward_reconstructed(np.ones((2, 8)), main, None, api.per_token_config(8))
 
 
-def test_svd_compensator_rejected():
+def test_svd_compensator_validation():
+    with pytest.raises(ValidationError, match="two factors"):
+        api.Compensator(api.SVD_BASELINE, 2, l1=np.ones((8, 2)))
+    with pytest.raises(ValidationError, match="residual"):
+        api.Compensator(api.SVD_BASELINE, 2, l1=np.ones((8, 2)), l2=np.ones((2, 4)), r_dense=np.ones((2, 4)))
     comp = api.Compensator(api.SVD_BASELINE, 2, l1=np.ones((8, 2)), l2=np.ones((2, 4)))
     main = api.MxBlockTensor(np.zeros((4, 32), np.uint8), np.zeros((4, 1), np.int32), 32, (4, 32))
     with pytest.raises(ValidationError, match="SVD"):
@@ -178,3 +182,26 @@ def test_symmetric_activation_composition_c1_style(gpu):
     y_ref, _ = O.forward_int(x, main_o, comp_o, O.IntCfg(4, True, "per-row"), symmetric_act=True)
     mx, mean = O.parity_errors(y, y_ref)
     assert mx <= TOL_MAX and mean <= TOL_MEAN
+
+
+@pytest.mark.gpu
+def test_forward_reconstructed_svd_baseline_golden(gpu, golden):
+    # build_svd_baseline artefacts (reference-built golden): INT main through the fused kernel,
+    # (x_hat @ L1) @ L2 as two fp32 GEMMs added in the epilogue; two aux products (compensate.py:307-309)
+    x = golden["fint_x"]
+    k, n = golden["fsvd_codes"].shape
+    main = api.QuantizedTensor(golden["fsvd_codes"], golden["fsvd_scales"], None,
+                               api.IntQuantConfig(4, True, k, "row"), (k, n))
+    comp = api.Compensator(api.SVD_BASELINE, 8, l1=golden["fsvd_l1"], l2=golden["fsvd_l2"])
+    probe = api.OpProbe()
+    y = api.forward_reconstructed(x, main, comp, api.per_token_config(8), probe)
+    assert probe.aux_matmuls == int(golden["fsvd_aux"]) == 2
+    mx, mean = O.parity_errors(y, golden["fsvd_y_a8"])
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+    # the large-M CTA-pair kernel takes the same addend
+    xb = np.tile(x, (40, 1))[:300]
+    yb = api.forward_reconstructed(xb, main, comp, api.per_token_config(8))
+    ref, _ = O.forward_int(xb, O.IntQ(main.codes, main.scales, None, O.IntCfg(4, True, k, "row"), (k, n)),
+                           O.Comp(8, l1=comp.l1, l2=comp.l2), O.IntCfg(8, False, "per-row"))
+    mx, mean = O.parity_errors(yb, ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)

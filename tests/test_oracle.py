@@ -93,6 +93,18 @@ def test_int_forward_matches_reference_golden(golden):
     np.testing.assert_array_equal(y, golden["fint_y_dense_a8"])
 
 
+def test_svd_baseline_forward_matches_reference_golden(golden):
+    # build_svd_baseline main is per-output-channel INT4 (compensate.py:209-224); the
+    # forward adds (dequantize(xq) @ L1) @ L2 (compensate.py:304-310), two aux products
+    xi = golden["fint_x"]
+    k, n = golden["fsvd_codes"].shape
+    main = O.IntQ(golden["fsvd_codes"], golden["fsvd_scales"], None, O.IntCfg(4, True, k, "row"), (k, n))
+    comp = O.Comp(8, l1=golden["fsvd_l1"], l2=golden["fsvd_l2"])
+    y, _ = O.forward_int(xi, main, comp, O.IntCfg(8, False, "per-row"))
+    np.testing.assert_array_equal(y, golden["fsvd_y_a8"])
+    assert int(golden["fsvd_aux"]) == 2
+
+
 # ------------------------------------------- the reference's known-answer tests
 
 

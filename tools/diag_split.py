@@ -1,3 +1,7 @@
+"""Per-CTA timeline of the CTA-pair MX linear at 4096^3 (SERQ_DIAG_TS build),
+whole tiles only (flags 0) vs the split last wave (flags 8192): per work item,
+when its accumulator was complete and when its epilogue ended (us from the
+first CTA entry), and the kernel's first entry / last exit."""
 import os, sys, subprocess
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -8,15 +12,24 @@ lib = _lib.load(diag); _lib._lib = lib
 from paper_2603_08185_b200 import benchmarks as B
 lin = B.device_mx_linear(4096, 4096, 64)
 x = B.outlier_x(4096, 4096); act = lin.quantize(x); y = torch.empty((4096, 4096), dtype=torch.bfloat16, device="cuda")
-ts = torch.zeros(512, dtype=torch.int64, device="cuda")
-for _ in range(3): lin.gemm(act, y)
-torch.cuda.synchronize()
-lib.serq_set_debug_timestamps(ts.data_ptr()); lin.gemm(act, y); torch.cuda.synchronize(); lib.serq_set_debug_timestamps(None)
-t = ts.cpu().numpy()
-t0 = t[510]
-print("kernel span (MMA warp CTA0):", (t[511] - t[510]) / 1e3, "us")
-e = t[256:496].reshape(40, 6)
-for row in e:
-    if row[0] == 0: continue
-    r = (row[:5] - t0) / 1e3
-    print(f"half={row[5]:2d} wait_start={r[0]:7.2f} full={r[1]:7.2f} partial_done={r[2]:7.2f} atomic={r[3]:7.2f} end={r[4]:7.2f}")
+for flags in [int(f) for f in os.environ.get('FLAGS', '0,8192').split(',')]:
+    lib.serq_set_debug_flags(flags)
+    ts = torch.zeros(8192, dtype=torch.int64, device="cuda")
+    for _ in range(3): lin.gemm(act, y)
+    torch.cuda.synchronize()
+    lib.serq_set_debug_timestamps(ts.data_ptr()); lin.gemm(act, y); torch.cuda.synchronize()
+    lib.serq_set_debug_timestamps(None)
+    t = ts.cpu().numpy().astype(np.float64)
+    ent = t[1024 + 148 * 24::2][:148]; ex = t[1024 + 148 * 24 + 1::2][:148]
+    t0 = ent[ent > 0].min()
+    print(f"flags={flags}: entry spread {(ent.max()-t0)/1e3:.2f} us, exit first/median/last "
+          f"{(ex.min()-t0)/1e3:.2f}/{(np.median(ex)-t0)/1e3:.2f}/{(ex.max()-t0)/1e3:.2f} us")
+    items = t[1024:1024 + 148 * 24].reshape(148, 6, 4)
+    for i in range(6):
+        v = items[:, i, :]
+        ok = v[:, 1] > 0
+        if not ok.any(): continue
+        full = (v[ok, 1] - t0) / 1e3; end = (v[ok, 2] - t0) / 1e3; half = v[ok, 3]
+        print(f"  item {i}: ctas={ok.sum():3d} halves={int((half >= 0).sum()):3d} acc done min/med/max "
+              f"{full.min():6.2f}/{np.median(full):6.2f}/{full.max():6.2f}  epi end {end.min():6.2f}/{np.median(end):6.2f}/{end.max():6.2f}")
+lib.serq_set_debug_flags(0)
