@@ -15,6 +15,7 @@
  *                          + gather_columns (salient slice)              quantcore.py:158-175
  *   serq_pack_mx           MxBlockTensor artefacts (main_t, comp.r_q)     mxfmt.py:34-49, compensate.py:343-357
  *   serq_unpack_mx         inverse of the device layout (artefact export)
+ *   serq_mx_container_decode  load_mx body -> codes / exponents on the device  mxfmt.py:254-280
  *   serq_pack_int          QuantizedTensor artefacts (main, comp.r_q / comp.r_dense)
  *                                                                         quantcore.py:59-80, compensate.py:48-69
  *   serq_linear_mx         _forward_mx: mx_gemm_reference(x,W)+mx_gemm_reference(xs,R)
@@ -88,6 +89,14 @@ int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K
                  const int32_t* r_exps, int r, int salient_contiguous, serq_linear_t** out, serq_stream_t stream);
 
 /* Inverse of the device MX layout for an activation/weight buffer pair. */
+/* The reference's packed MX file body (mxfmt.py:228-251, after the 28-byte
+ * header; bundleio.py load path): rows x cols/32 records of 17 bytes (exponent
+ * byte e+127, 16 nibble bytes, element 2i low) already in device memory ->
+ * element codes uint8 [rows, cols] (16-B aligned) and exponents int32
+ * [rows, cols/32], the serq_pack_mx inputs.  Replaces load_mx's per-block loop. */
+int serq_mx_container_decode(const uint8_t* body, int64_t rows, int64_t cols, uint8_t* codes, int32_t* exps,
+                             serq_stream_t stream);
+
 int serq_unpack_mx(const uint8_t* codes_packed, const uint8_t* sf, int64_t rows, int64_t cols, uint8_t* codes,
                    int32_t* exps, serq_stream_t stream);
 

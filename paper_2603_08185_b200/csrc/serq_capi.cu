@@ -397,6 +397,19 @@ int serq_unpack_mx(const uint8_t* codes_packed, const uint8_t* sf, int64_t rows,
   return SERQ_OK;
 }
 
+int serq_mx_container_decode(const uint8_t* body, int64_t rows, int64_t cols, uint8_t* codes, int32_t* exps,
+                             serq_stream_t stream) {
+  g_launches = 0;
+  if (rows <= 0 || cols <= 0 || cols % 32)
+    return fail(SERQ_EINVAL, "MX container for the device needs 32-element blocks and cols %% 32 == 0");
+  if (!body || !codes || !exps) return fail(SERQ_EINVAL, "null pointer");
+  if (reinterpret_cast<uintptr_t>(codes) & 15) return fail(SERQ_EINVAL, "codes must be 16-byte aligned");
+  const int64_t records = rows * (cols / 32);
+  mx_container_decode_kernel<<<unsigned(cdiv(records, 256)), 256, 0, S(stream)>>>(body, records, codes, exps);
+  LAUNCH_CHECK("mx_container_decode");
+  return SERQ_OK;
+}
+
 int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t N, int w_bits, int r_mode,
                   const void* r_data, const double* r_scales, int r, int salient_contiguous, serq_linear_t** out,
                   serq_stream_t stream) {

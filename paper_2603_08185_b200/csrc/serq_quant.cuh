@@ -265,6 +265,29 @@ __global__ void __launch_bounds__(256) mx_encode_fast_kernel(const T* __restrict
   }
 }
 
+// ------------------------------------------------------------------ MX container
+// The reference's packed MX file body (mxfmt.py:228-251): per 32-block one
+// biased exponent byte (e + 127) then 16 bytes of nibbles, element 2i in the
+// low nibble -- 17-byte records, row-major over (row, block).  One thread per
+// record: the element codes [rows, cols] and exponents [rows, cols / 32] that
+// serq_pack_mx consumes.
+__global__ void mx_container_decode_kernel(const uint8_t* __restrict__ body, int64_t records,
+                                           uint8_t* __restrict__ codes, int32_t* __restrict__ exps) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= records) return;
+  const uint8_t* rec = body + i * 17;
+  exps[i] = int32_t(rec[0]) - 127;
+  uint32_t out[8];
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const uint32_t b0 = rec[1 + 2 * w], b1 = rec[2 + 2 * w];
+    out[w] = (b0 & 0xFu) | ((b0 >> 4) << 8) | ((b1 & 0xFu) << 16) | ((b1 >> 4) << 24);
+  }
+  uint4* dst = reinterpret_cast<uint4*>(codes + i * 32);  // block i covers codes [32 i, 32 i + 32)
+  dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
+  dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
+}
+
 // ------------------------------------------------------------------ INT quantize
 // One CTA per token row.  Scales / zero points in f64 exactly as the reference;
 // codes rint(x / s) bit-exact: a fast product against 1/s decides the rounding

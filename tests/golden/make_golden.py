@@ -201,6 +201,30 @@ def main():
     g["fsvd_l1"], g["fsvd_l2"] = comp_s.l1, comp_s.l2
     g["fsvd_codes"], g["fsvd_scales"] = main_s.codes, main_s.scales
 
+    # -- a small bundle written by the reference's own save_bundle (bundleio.py:73-126), for the
+    #    device bundle loader: MX main + MX R, INT main + INT R, INT main + SVD factors
+    from serq.bundleio import save_bundle
+    from serq.toymodel import LinearBundle, QuantizedBlockBundle
+
+    bdir = os.path.join(os.path.dirname(OUT), "bundle")
+    wb = np.random.default_rng(21).standard_normal((256, 128)) * 0.02
+    mx_main, mx_comp = build_serq_rtn_mx(wb, build_plan(score_rows(wb), 32), 32)
+    int_main = quantize_symmetric(wb, IntQuantConfig(4, True, 256, "row"))
+    rb = wb[:32] - dequantize(int_main)[:32]
+    int_comp = Compensator("rtn_residual", 32, np.arange(32), r_q=quantize_symmetric(rb, IntQuantConfig(4, True, 32, "row")))
+    svd_main, svd_comp = build_svd_baseline(wb, IntQuantConfig(4, True, 256, "row"), 4)
+    linears = {"up_proj": LinearBundle(mx_main, mx_comp, None),
+               "down_proj": LinearBundle(int_main, int_comp, per_token_config(8)),
+               "o_proj": LinearBundle(svd_main, svd_comp, per_token_config(8))}
+    gains = {"ln1": np.abs(np.random.default_rng(22).standard_normal(256)) + 0.5}
+    save_bundle(bdir, QuantizedBlockBundle(linears=linears, nl_weights=gains, plans={}, rank=32, fmt="mixed"))
+    xb = bf16(np.random.default_rng(23).standard_normal((40, 256)))
+    g["bundle_x"] = xb
+    for name, lb in linears.items():
+        g[f"bundle_y_{name}"] = forward_reconstructed(xb, lb.main, lb.comp, lb.act_cfg)
+    g["bundle_up_codes"], g["bundle_up_exps"] = mx_main.element_codes, mx_main.block_scale_exponents
+    g["bundle_up_rcodes"], g["bundle_up_rexps"] = mx_comp.r_q.element_codes, mx_comp.r_q.block_scale_exponents
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)/1e6:.2f} MB, {len(g)} arrays)")
 
