@@ -339,6 +339,7 @@ def other_configs(hbm_gbs: float) -> dict:
         # the paper's comparison at C3's shape: SVD baseline (two-factor L1 L2, r = 128) vs SERQ's fused R
         out["c3_svd_baseline_r128"] = B.svd_baseline_point(2048, 4096, 11008, 128)
         out["c4_decode"] = B.decode_points(hbm_gbs)
+        out["producer_rmsnorm_quant_c2"] = B.rmsnorm_quant_point(4096, 4096, hbm_gbs)
         out["c5_block_tp1"] = B.c5_block_point(1, 0, flush=fl)
     except Exception as e:  # secondary numbers must not hide the headline line
         out["error"] = f"{type(e).__name__}: {e}"

@@ -15,6 +15,7 @@
  *                          + gather_columns (salient slice)              quantcore.py:158-175
  *   serq_pack_mx           MxBlockTensor artefacts (main_t, comp.r_q)     mxfmt.py:34-49, compensate.py:343-357
  *   serq_unpack_mx         inverse of the device layout (artefact export)
+ *   serq_rmsnorm_quant_mx  rmsnorm(x, gain) -> mx_encode, fused        saliency.py:194-196, mxfmt.py:97-108
  *   serq_mx_container_decode  load_mx body -> codes / exponents on the device  mxfmt.py:254-280
  *   serq_pack_int          QuantizedTensor artefacts (main, comp.r_q / comp.r_dense)
  *                                                                         quantcore.py:59-80, compensate.py:48-69
@@ -89,6 +90,14 @@ int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K
                  const int32_t* r_exps, int r, int salient_contiguous, serq_linear_t** out, serq_stream_t stream);
 
 /* Inverse of the device MX layout for an activation/weight buffer pair. */
+/* Producer fusion: y = x / sqrt(mean(x^2) + eps) * gain
+ * (saliency.py:194-196; gain = the RMSNorm weight with the SAF scales folded in,
+ * toymodel.py:203-217) encoded straight to MX codes / scale factors in the
+ * serq_act_quant_mx layout.  x bf16/f32 [M, K] (16-B aligned rows), gain f64 [K].
+ * f64 arithmetic in the reference's order; the normalised x never reaches HBM. */
+int serq_rmsnorm_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, const double* gain, double eps,
+                          uint8_t* codes, uint8_t* sf, serq_stream_t stream);
+
 /* The reference's packed MX file body (mxfmt.py:228-251, after the 28-byte
  * header; bundleio.py load path): rows x cols/32 records of 17 bytes (exponent
  * byte e+127, 16 nibble bytes, element 2i low) already in device memory ->

@@ -431,6 +431,13 @@ def plan_permutation(scores, r):
     return sal, np.concatenate([sal, rest])
 
 
+def rmsnorm(x, gain, eps: float = 1e-6) -> np.ndarray:
+    """saliency.py:194-196: x / sqrt(mean(x^2) + eps) * gain, in float64."""
+    x = np.asarray(x, dtype=np.float64)
+    rms = np.sqrt(np.mean(x * x, axis=1, keepdims=True) + eps)
+    return x / rms * np.asarray(gain, dtype=np.float64)[None, :]
+
+
 def bf16_round(x) -> np.ndarray:
     """Round float64 to the nearest bfloat16 (ties to even), returned as f64.
 

@@ -264,6 +264,21 @@ def svd_baseline_point(M, K, N, r, bits=8, n_steps: int = 16) -> dict:
             "tokens_per_s": M / (t * 1e-3)}
 
 
+def rmsnorm_quant_point(M: int, K: int, hbm_peak_gbs: float, n_steps: int = 16) -> dict:
+    """Producer fusion: rmsnorm(x, gain) -> MX codes in one
+    kernel vs the plain MX quantizer on an already-normalised bf16 X, same shape,
+    8 activation sets (cold).  Bytes per launch: 2MK in, MK/2 + MK/32 out."""
+    xs = [outlier_x(M, K, seed=i) for i in range(8)]
+    gain = (torch.rand(K, device="cuda", dtype=torch.float64) + 0.5)
+    acts = [D.quantize_mx(x) for x in xs]
+    t_f = time_steps(lambda i: D.rmsnorm_quantize_mx(xs[i % 8], gain, 1e-6, acts[i % 8]), n_steps)
+    t_q = time_steps(lambda i: D.quantize_mx(xs[i % 8], None, acts[i % 8]), n_steps)
+    byts = 2 * M * K + M * K / 2 + M * K / 32
+    return {"M": M, "K": K, "rmsnorm_quant_us": t_f * 1e3, "quant_only_us": t_q * 1e3,
+            "rmsnorm_quant_hbm_frac": byts / (t_f * 1e-3) / 1e9 / hbm_peak_gbs,
+            "unfused_extra_bytes": 4 * M * K}
+
+
 def c5_block_point(world: int = 1, rank: int = 0, M: int = 8192, r: int = 128, group=None, steps: int = 5,
                    flush: Flusher | None = None) -> dict:
     """BASELINE C5: Llama-3-70B-shaped decoder-block linears (hidden 8192,

@@ -397,6 +397,31 @@ int serq_unpack_mx(const uint8_t* codes_packed, const uint8_t* sf, int64_t rows,
   return SERQ_OK;
 }
 
+int serq_rmsnorm_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, const double* gain, double eps,
+                          uint8_t* codes, uint8_t* sf, serq_stream_t stream) {
+  g_launches = 0;
+  if (M <= 0 || K <= 0) return fail(SERQ_EINVAL, "x must be non-empty (M=%lld, K=%lld)", (long long)M, (long long)K);
+  if (K % 32) return fail(SERQ_EINVAL, "row length %lld not divisible by block_size 32", (long long)K);
+  if (ldx < K) return fail(SERQ_EINVAL, "ldx < K");
+  if (!gain) return fail(SERQ_EINVAL, "gain is NULL");
+  if (!(eps >= 0.0)) return fail(SERQ_EINVAL, "eps must be >= 0");
+  if (dtype != SERQ_BF16 && dtype != SERQ_F32) return fail(SERQ_EINVAL, "rmsnorm input must be bf16 or f32");
+  const int align = dtype == SERQ_BF16 ? 8 : 4;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || ldx % align) return fail(SERQ_EINVAL, "x must be 16-byte aligned rows");
+  cudaStream_t st = S(stream);
+  const int kc = kc_pad_of(K);
+  // rows / chunks beyond the matrix must read as a finite scale
+  if (M % 128 || K % 256) CK(cudaMemsetAsync(sf, 0, sf_bytes_of(M, K), st));
+  if (dtype == SERQ_BF16)
+    CK(launch_pdl(rmsnorm_mx_encode_kernel<__nv_bfloat16>, dim3(unsigned(M)), dim3(256), 0, st,
+                  static_cast<const __nv_bfloat16*>(x), int(K), ldx, gain, eps, codes, sf, kc));
+  else
+    CK(launch_pdl(rmsnorm_mx_encode_kernel<float>, dim3(unsigned(M)), dim3(256), 0, st, static_cast<const float*>(x),
+                  int(K), ldx, gain, eps, codes, sf, kc));
+  LAUNCH_CHECK("rmsnorm_mx_encode");
+  return SERQ_OK;
+}
+
 int serq_mx_container_decode(const uint8_t* body, int64_t rows, int64_t cols, uint8_t* codes, int32_t* exps,
                              serq_stream_t stream) {
   g_launches = 0;

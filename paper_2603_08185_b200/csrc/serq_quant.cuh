@@ -265,6 +265,92 @@ __global__ void __launch_bounds__(256) mx_encode_fast_kernel(const T* __restrict
   }
 }
 
+// ------------------------------------------------------------------ RMSNorm -> MX (producer fusion)
+// One CTA per token row: y = x / sqrt(mean(x^2) + eps) * gain (saliency.py:194-196,
+// the gain carrying the folded SAF scales, toymodel.py:203-217), then mx_encode(y)
+// -- the normalised activation never goes to HBM.  Arithmetic is the
+// reference's, in f64 and in the same order (square, mean = sum / K, + eps,
+// sqrt, divide, multiply), every step IEEE-rounded; only the summation order of
+// the squares differs (exact whenever the squares' exponents span < 2^37), and
+// the f64 E2M1 rounding is the exact software path.  The row is read twice: the
+// second pass hits L1 / L2, so HBM sees it once.
+template <typename T>
+__device__ __forceinline__ void load8_f64(const T* __restrict__ p, bool ok, double (&v)[8]) {
+  if (!ok) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = 0.0;
+    return;
+  }
+  if constexpr (In<T>::kId == 0) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = double(__uint_as_float(w[i] << 16));
+      v[2 * i + 1] = double(__uint_as_float(w[i] & 0xFFFF0000u));
+    }
+  } else {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) rmsnorm_mx_encode_kernel(const T* __restrict__ x, int K, int64_t ldx,
+                                                                const double* __restrict__ gain, double eps,
+                                                                uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
+                                                                int kc_pad) {
+  __shared__ double red[8];
+  pdl_launch_dependents();
+  pdl_wait();
+  const int64_t row = blockIdx.x;
+  const T* xr = x + row * ldx;
+  double ss = 0.0;
+  for (int c = threadIdx.x * 8; c < K; c += 256 * 8) {
+    double v[8];
+    load8_f64(xr + c, true, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss = fma(v[i], v[i], ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  double total = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) total += red[w];
+  const double rms = sqrt(total / double(K) + eps);
+  const int iters = (K + 2047) / 2048;
+  for (int it = 0; it < iters; ++it) {
+    const int c = it * 2048 + threadIdx.x * 8;
+    const bool ok = c < K;
+    double v[8];
+    load8_f64(xr + c, ok, v);
+    double amax = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[i] = ok ? (v[i] / rms) * gain[c + i] : 0.0;
+      amax = fmax(amax, fabs(v[i]));
+    }
+    amax = fmax(amax, __shfl_xor_sync(0xffffffff, amax, 1));
+    amax = fmax(amax, __shfl_xor_sync(0xffffffff, amax, 2));
+    const int e = mx_block_exp_f64(amax);
+    const double inv = ldexp(1.0, -e);
+    uint32_t packed = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double s = v[i] * inv;  // exact: power-of-two scaling
+      const uint32_t idx = e2m1_index_sw(fabs(s));
+      packed |= ((s < 0.0 && idx > 0) ? idx + 8 : idx) << (4 * i);
+    }
+    if (ok) {
+      *reinterpret_cast<uint32_t*>(codes + row * (K / 2) + c / 2) = packed;
+      if ((threadIdx.x & 3) == 0) sf[sf_offset(row, c / 32, kc_pad)] = uint8_t(e + 127);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ MX container
 // The reference's packed MX file body (mxfmt.py:228-251): per 32-block one
 // biased exponent byte (e + 127) then 16 bytes of nibbles, element 2i in the

@@ -102,6 +102,27 @@ def quantize_mx(x: torch.Tensor, gather_idx: torch.Tensor | None = None, out: Mx
     return out
 
 
+def rmsnorm_quantize_mx(x: torch.Tensor, gain: torch.Tensor, eps: float = 1e-6,
+                        out: MxActivation | None = None) -> MxActivation:
+    """Producer fusion: mx_encode(rmsnorm(x, gain, eps)) in ONE kernel
+    (saliency.py:194-196 then mxfmt.py:97-108).  x: bf16/f32 [M, K] residual
+    stream on the GPU; gain: float64 [K] (the RMSNorm weight with the smoothing
+    scales folded in and the salient permutation applied)."""
+    _require_cuda(x, "x")
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ValidationError("x must be a row-major 2-D tensor")
+    M, K = x.shape
+    if gain.dtype != torch.float64 or gain.numel() != K or not gain.is_cuda:
+        raise ValidationError("gain must be a float64 CUDA vector of length K")
+    if out is None:
+        cb, sb = mx_sizes(M, K)
+        out = MxActivation(torch.empty(cb, dtype=torch.uint8, device=x.device),
+                           torch.empty(sb, dtype=torch.uint8, device=x.device), M, K)
+    _lib.call("serq_rmsnorm_quant_mx", x.data_ptr(), _dtype_id(x), M, K, x.stride(0), gain.contiguous().data_ptr(),
+              float(eps), out.codes.data_ptr(), out.sf.data_ptr(), _stream())
+    return out
+
+
 def unpack_mx(codes: torch.Tensor, sf: torch.Tensor, rows: int, cols: int) -> tuple[torch.Tensor, torch.Tensor]:
     """Device layout -> reference artefact layout (uint8 codes [rows, cols], int32 exps [rows, cols/32])."""
     c = torch.empty((rows, cols), dtype=torch.uint8, device=codes.device)
@@ -228,6 +249,15 @@ class MxLinear:
 
     def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
         return self.forward(x, None, y)
+
+    def forward_rmsnorm(self, x: torch.Tensor, gain: torch.Tensor, eps: float = 1e-6,
+                        act: MxActivation | None = None, y: torch.Tensor | None = None) -> torch.Tensor:
+        """linear(rmsnorm(x, gain)) with the normalisation fused into the quantizer
+        (the permuted / contiguous salient layout: the salient slice is K-tile 0)."""
+        if not self.contiguous:
+            raise ValidationError("the fused RMSNorm quantizer needs the permuted (contiguous) salient layout")
+        act = rmsnorm_quantize_mx(x, gain, eps, act)
+        return self.gemm(act, y)
 
     def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor) -> None:
         """End to end from (pinned) host bf16 memory through the C-ABI."""

@@ -225,6 +225,14 @@ def main():
     g["bundle_up_codes"], g["bundle_up_exps"] = mx_main.element_codes, mx_main.block_scale_exponents
     g["bundle_up_rcodes"], g["bundle_up_rexps"] = mx_comp.r_q.element_codes, mx_comp.r_q.block_scale_exponents
 
+    # -- producer RMSNorm (saliency.py:194-196) feeding the fused quantizer
+    from serq.saliency import rmsnorm
+
+    xr = bf16(np.random.default_rng(31).standard_normal((16, 512)) * 3)
+    gr = np.abs(np.random.default_rng(32).standard_normal(512)) + 0.5
+    g["rms_x"], g["rms_gain"], g["rms_y"] = xr, gr, rmsnorm(xr, gr)
+    g["rms_codes"] = mx_encode(g["rms_y"], 32).element_codes
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)/1e6:.2f} MB, {len(g)} arrays)")
 

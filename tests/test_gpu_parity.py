@@ -319,3 +319,50 @@ def test_mx_forward_fused_equals_two_launches(D, M, K, N):
         assert torch.equal(y1, y2)
     mx, mean = O.parity_errors(y2.float().cpu().numpy(), O.forward_mx(x, main_t, comp))
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+def _near_midpoint(y, bs=32, rel=1e-12):
+    """Elements whose scaled magnitude lies within `rel` of an E2M1 rounding
+    midpoint, or whose block amax is within `rel` of a power of two: the only
+    places a last-ulp difference in the f64 normalisation can change a code."""
+    M, K = y.shape
+    blk = np.abs(y).reshape(M, K // bs, bs)
+    amax = blk.max(axis=2, keepdims=True)
+    with np.errstate(divide="ignore"):
+        lg = np.log2(np.where(amax > 0, amax, 1.0))
+    e_edge = np.abs(lg - np.round(lg)) < rel * 4
+    e = np.where(amax > 0, np.floor(lg) - 2, 0)
+    s = blk / np.exp2(e)
+    mids = np.array([0.25, 0.75, 1.25, 1.75, 2.5, 3.5, 5.0])
+    near = (np.abs(s[..., None] - mids) <= rel * np.maximum(s[..., None], 1e-300)).any(axis=-1)
+    return (near | e_edge).reshape(M, K)
+
+
+@pytest.mark.parametrize("dtype,M,K", [("bf16", 300, 4096), ("f32", 64, 1024), ("bf16", 5, 8192)])
+def test_rmsnorm_quant_mx_matches_reference_order(D, dtype, M, K):
+    rng = np.random.default_rng(M + K)
+    x = O.bf16_round(_bf16_outlier_x(M, K, seed=K) * 3.0)
+    if dtype == "f32":
+        x = x + rng.standard_normal(x.shape) * 1e-3
+        x = x.astype(np.float32).astype(np.float64)
+    gain = (np.abs(rng.standard_normal(K)) + 0.5) / np.exp2(rng.uniform(-2, 2, K))  # ln weight / SAF scales
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    act = D.rmsnorm_quantize_mx(_cuda(x, tdt), torch.from_numpy(gain).to("cuda"), 1e-6)
+    c, e = D.unpack_mx(act.codes, act.sf, M, K)
+    yref = O.rmsnorm(x, gain, 1e-6)
+    ref = O.mx_encode(yref, 32)
+    eb = np.repeat(e.cpu().numpy() != ref.block_scale_exponents, 32, axis=1)
+    diff = (c.cpu().numpy() != ref.element_codes) | eb
+    allowed = _near_midpoint(yref)
+    assert not (diff & ~allowed).any(), int((diff & ~allowed).sum())
+
+
+def test_rmsnorm_fused_linear_parity(D):
+    M, K, N, r = 512, 2048, 768, 64
+    x, main_t, comp = _mx_case(M, K, N, r, seed=31)
+    gain = np.abs(np.random.default_rng(32).standard_normal(K)) + 0.5
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                     comp.r_q.block_scale_exponents, np.arange(r))
+    y = lin.forward_rmsnorm(_cuda(x, torch.bfloat16), torch.from_numpy(gain).to("cuda")).float().cpu().numpy()
+    mx, mean = O.parity_errors(y, O.forward_mx(O.rmsnorm(x, gain), main_t, comp))
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)

@@ -181,3 +181,10 @@ def test_bf16_round_matches_torch():
     x32 = x.astype(np.float32).astype(np.float64)
     t = torch.from_numpy(x32.astype(np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
     assert np.array_equal(O.bf16_round(x32), t)
+
+
+def test_rmsnorm_matches_reference_golden(golden):
+    # saliency.py:194-196, the producer of q/k/v and gate/up inputs (fused into the quantizer on the GPU)
+    y = O.rmsnorm(golden["rms_x"], golden["rms_gain"])
+    assert np.array_equal(y, golden["rms_y"])
+    assert np.array_equal(O.mx_encode(y, 32).element_codes, golden["rms_codes"])
