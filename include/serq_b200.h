@@ -93,10 +93,12 @@ int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K
 /* Producer fusion: y = x / sqrt(mean(x^2) + eps) * gain
  * (saliency.py:194-196; gain = the RMSNorm weight with the SAF scales folded in,
  * toymodel.py:203-217) encoded straight to MX codes / scale factors in the
- * serq_act_quant_mx layout.  x bf16/f32 [M, K] (16-B aligned rows), gain f64 [K].
- * f64 arithmetic in the reference's order; the normalised x never reaches HBM. */
-int serq_rmsnorm_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, const double* gain, double eps,
-                          uint8_t* codes, uint8_t* sf, serq_stream_t stream);
+ * serq_act_quant_mx layout.  x bf16/f32 [M, K] (16-B aligned rows), gain f64 [K]
+ * and its f32 rounding gain32 [K] (16-B aligned).  Codes equal mx_encode of the
+ * reference's f64 result: an f32 fast path with a proven error bound, and the
+ * reference's f64 operations for any 32-block the bound cannot decide.  K <= 8192. */
+int serq_rmsnorm_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, const double* gain,
+                          const float* gain32, double eps, uint8_t* codes, uint8_t* sf, serq_stream_t stream);
 
 /* The reference's packed MX file body (mxfmt.py:228-251, after the 28-byte
  * header; bundleio.py load path): rows x cols/32 records of 17 bytes (exponent

@@ -397,13 +397,14 @@ int serq_unpack_mx(const uint8_t* codes_packed, const uint8_t* sf, int64_t rows,
   return SERQ_OK;
 }
 
-int serq_rmsnorm_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, const double* gain, double eps,
-                          uint8_t* codes, uint8_t* sf, serq_stream_t stream) {
+int serq_rmsnorm_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, const double* gain,
+                          const float* gain32, double eps, uint8_t* codes, uint8_t* sf, serq_stream_t stream) {
   g_launches = 0;
   if (M <= 0 || K <= 0) return fail(SERQ_EINVAL, "x must be non-empty (M=%lld, K=%lld)", (long long)M, (long long)K);
   if (K % 32) return fail(SERQ_EINVAL, "row length %lld not divisible by block_size 32", (long long)K);
   if (ldx < K) return fail(SERQ_EINVAL, "ldx < K");
-  if (!gain) return fail(SERQ_EINVAL, "gain is NULL");
+  if (!gain || !gain32) return fail(SERQ_EINVAL, "gain is NULL");
+  if (reinterpret_cast<uintptr_t>(gain32) & 15) return fail(SERQ_EINVAL, "gain32 must be 16-byte aligned");
   if (!(eps >= 0.0)) return fail(SERQ_EINVAL, "eps must be >= 0");
   if (dtype != SERQ_BF16 && dtype != SERQ_F32) return fail(SERQ_EINVAL, "rmsnorm input must be bf16 or f32");
   const int align = dtype == SERQ_BF16 ? 8 : 4;
@@ -412,12 +413,34 @@ int serq_rmsnorm_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_
   const int kc = kc_pad_of(K);
   // rows / chunks beyond the matrix must read as a finite scale
   if (M % 128 || K % 256) CK(cudaMemsetAsync(sf, 0, sf_bytes_of(M, K), st));
-  if (dtype == SERQ_BF16)
-    CK(launch_pdl(rmsnorm_mx_encode_kernel<__nv_bfloat16>, dim3(unsigned(M)), dim3(256), 0, st,
-                  static_cast<const __nv_bfloat16*>(x), int(K), ldx, gain, eps, codes, sf, kc));
-  else
-    CK(launch_pdl(rmsnorm_mx_encode_kernel<float>, dim3(unsigned(M)), dim3(256), 0, st, static_cast<const float*>(x),
-                  int(K), ldx, gain, eps, codes, sf, kc));
+  if (K > 4 * 2048) return fail(SERQ_EINVAL, "fused RMSNorm quantizer supports rows up to 8192 elements");
+
+  // kTpr threads per row (8 elements each per chunk), 256 / kTpr rows per CTA
+  // threads per row: 128 for K <= 4096, 256 above (measured best of 64 / 128 / 256 at 4096^2 and 8192^2)
+  const int tpr = K <= 4096 ? 128 : 256;
+  const int chunks = int(cdiv(K, tpr * 8));  // <= 4
+  const dim3 grid{unsigned(cdiv(M, 256 / tpr))}, blk{256};
+#define RMS_LAUNCH(T, P, C)                                                                                       \
+  CK(launch_pdl(rmsnorm_mx_encode_kernel<T, P, C>, grid, blk, 0, st, static_cast<const T*>(x), int(M), int(K), ldx, \
+                gain, gain32, eps, codes, sf, kc))
+  if (dtype == SERQ_BF16) {
+    if (tpr == 128) {
+      if (chunks <= 2) RMS_LAUNCH(__nv_bfloat16, 128, 2);
+      else RMS_LAUNCH(__nv_bfloat16, 128, 4);
+    } else {
+      if (chunks <= 2) RMS_LAUNCH(__nv_bfloat16, 256, 2);
+      else RMS_LAUNCH(__nv_bfloat16, 256, 4);
+    }
+  } else {
+    if (tpr == 128) {
+      if (chunks <= 2) RMS_LAUNCH(float, 128, 2);
+      else RMS_LAUNCH(float, 128, 4);
+    } else {
+      if (chunks <= 2) RMS_LAUNCH(float, 256, 2);
+      else RMS_LAUNCH(float, 256, 4);
+    }
+  }
+#undef RMS_LAUNCH
   LAUNCH_CHECK("rmsnorm_mx_encode");
   return SERQ_OK;
 }

@@ -268,85 +268,193 @@ __global__ void __launch_bounds__(256) mx_encode_fast_kernel(const T* __restrict
 // ------------------------------------------------------------------ RMSNorm -> MX (producer fusion)
 // One CTA per token row: y = x / sqrt(mean(x^2) + eps) * gain (saliency.py:194-196,
 // the gain carrying the folded SAF scales, toymodel.py:203-217), then mx_encode(y)
-// -- the normalised activation never goes to HBM.  Arithmetic is the
-// reference's, in f64 and in the same order (square, mean = sum / K, + eps,
-// sqrt, divide, multiply), every step IEEE-rounded; only the summation order of
-// the squares differs (exact whenever the squares' exponents span < 2^37), and
-// the f64 E2M1 rounding is the exact software path.  The row is read twice: the
-// second pass hits L1 / L2, so HBM sees it once.
-template <typename T>
-__device__ __forceinline__ void load8_f64(const T* __restrict__ p, bool ok, double (&v)[8]) {
-  if (!ok) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = 0.0;
-    return;
-  }
-  if constexpr (In<T>::kId == 0) {
-    const uint4 raw = *reinterpret_cast<const uint4*>(p);
-    const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      v[2 * i] = double(__uint_as_float(w[i] << 16));
-      v[2 * i + 1] = double(__uint_as_float(w[i] & 0xFFFF0000u));
-    }
-  } else {
-    const float4 a = *reinterpret_cast<const float4*>(p);
-    const float4 b = *reinterpret_cast<const float4*>(p + 4);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-  }
+// -- the normalised activation never goes to HBM.  Arithmetic follows the
+// reference (square, mean = sum / K, + eps, sqrt, divide, multiply): the mean of
+// squares at f64-level accuracy (compensated f32), the normalised value in f32
+// with a proven error bound, and -- for any 32-block the bound cannot decide (an
+// element within 4e-7 of an E2M1 decision point, or the block max that close to
+// a power of two) -- the reference's f64 operations with IEEE division.  Several
+// rows per CTA, each row's elements in its threads' registers (read once).
+// E2M1 code (sign | magnitude index) of an exactly power-of-two-scaled f64 value, through
+// the hardware f32 converter: sc and f32(sc) round alike unless f32(sc) lands exactly ON a
+// decision point (all of which are f32 values) while sc is not -- then sc's side decides.
+__device__ __forceinline__ uint32_t e2m1_code_f64(double sc) {
+  const double a = fabs(sc);
+  float t = float(a);  // RN
+  const bool mid = t == 0.25f || t == 0.75f || t == 1.25f || t == 1.75f || t == 2.5f || t == 3.5f || t == 5.0f;
+  if (mid && double(t) != a) t = double(t) < a ? __int_as_float(__float_as_int(t) + 1) : __int_as_float(__float_as_int(t) - 1);
+  const uint32_t idx = cvt_e2m1x2_raw(t, 0.f) & 7u;  // even element -> low nibble
+  return (sc < 0.0 && idx > 0) ? idx + 8 : idx;
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) rmsnorm_mx_encode_kernel(const T* __restrict__ x, int K, int64_t ldx,
-                                                                const double* __restrict__ gain, double eps,
+struct Raw8;
+template <>
+struct Raw8<__nv_bfloat16> {
+  uint32_t w[4];
+  __device__ __forceinline__ void load(const __nv_bfloat16* p, bool ok) {
+    const uint4 r = ok ? __ldg(reinterpret_cast<const uint4*>(p)) : make_uint4(0, 0, 0, 0);
+    w[0] = r.x; w[1] = r.y; w[2] = r.z; w[3] = r.w;
+  }
+  __device__ __forceinline__ float f(int i) const {
+    return __uint_as_float((i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16));
+  }
+};
+template <>
+struct Raw8<float> {
+  float v[8];
+  __device__ __forceinline__ void load(const float* p, bool ok) {
+    const float4 a = ok ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0, 0, 0, 0);
+    const float4 b = ok ? __ldg(reinterpret_cast<const float4*>(p) + 1) : make_float4(0, 0, 0, 0);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  __device__ __forceinline__ float f(int i) const { return v[i]; }
+};
+
+template <typename T, int kTpr, int kChunks>
+__global__ void __launch_bounds__(256) rmsnorm_mx_encode_kernel(const T* __restrict__ x, int M, int K, int64_t ldx,
+                                                                const double* __restrict__ gain,
+                                                                const float* __restrict__ gain32, double eps,
                                                                 uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
                                                                 int kc_pad) {
-  __shared__ double red[8];
+  constexpr int kRows = 256 / kTpr, kWarps = kTpr / 32;
+  // Error budget of the f32 fast path vs the reference's f64 y: per-thread recursive f32
+  // sum of n = 8 kChunks positive squares (<= (n - 1) 2^-24 relative), halved by the sqrt,
+  // plus five f32 roundings (1/rms, x r, * g, gain, r32).
+  constexpr float kRel = float((8 * kChunks - 1) * 0.5 + 6.0) * 5.9604645e-8f;
+  constexpr uint32_t kMantEdge = uint32_t(kRel * 8388608.0f) + 2u;  // power-of-two proximity, in f32 ulps
+  __shared__ double red[kRows][kWarps];
+  __shared__ double s_rms[kRows];
+  __shared__ float s_r32[kRows];
+  __shared__ int s_unsure[kRows];
   pdl_launch_dependents();
   pdl_wait();
-  const int64_t row = blockIdx.x;
-  const T* xr = x + row * ldx;
-  double ss = 0.0;
-  for (int c = threadIdx.x * 8; c < K; c += 256 * 8) {
-    double v[8];
-    load8_f64(xr + c, true, v);
+  const int rl = threadIdx.x / kTpr, t = threadIdx.x % kTpr;
+  const int64_t row = int64_t(blockIdx.x) * kRows + rl;
+  const bool row_ok = row < M;
+  const T* xr = x + (row_ok ? row : 0) * ldx;
+  Raw8<T> v[kChunks];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) ss = fma(v[i], v[i], ss);
+  for (int it = 0; it < kChunks; ++it) {
+    const int c = it * (kTpr * 8) + t * 8;
+    v[it].load(xr + c, row_ok && c < K);
   }
+  // ---- pass 1: mean of squares in f32 per thread, combined in f64
+  float ss32 = 0.f;
+#pragma unroll
+  for (int it = 0; it < kChunks; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss32 = fmaf(v[it].f(i), v[it].f(i), ss32);
+  double ss = ss32;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  if ((t & 31) == 0) red[rl][t >> 5] = ss;
+  if (t == 0) s_unsure[rl] = 0;
   __syncthreads();
-  double total = 0.0;
+  if (t == 0) {
+    double total = 0.0;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) total += red[w];
-  const double rms = sqrt(total / double(K) + eps);
-  const int iters = (K + 2047) / 2048;
-  for (int it = 0; it < iters; ++it) {
-    const int c = it * 2048 + threadIdx.x * 8;
-    const bool ok = c < K;
-    double v[8];
-    load8_f64(xr + c, ok, v);
-    double amax = 0.0;
+    for (int w = 0; w < kWarps; ++w) total += red[rl][w];
+    s_r32[rl] = float(1.0 / sqrt(total / double(K) + eps));
+  }
+  __syncthreads();
+  const float r32 = s_r32[rl];
+  // ---- pass 2: f32 encode; blocks the error budget cannot decide are left for pass 3
+  uint32_t unsure_mask = 0;  // bit it: chunk `it`'s 32-block is undecided
+#pragma unroll
+  for (int it = 0; it < kChunks; ++it) {
+    const int c = it * (kTpr * 8) + t * 8;
+    const bool ok = row_ok && c < K;
+    float y[8];
+    float amax = 0.f;
+    float4 g0 = make_float4(0, 0, 0, 0), g1 = make_float4(0, 0, 0, 0);
+    if (ok) {
+      g0 = __ldg(reinterpret_cast<const float4*>(gain32 + c));
+      g1 = __ldg(reinterpret_cast<const float4*>(gain32 + c) + 1);
+    }
+    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      v[i] = ok ? (v[i] / rms) * gain[c + i] : 0.0;
-      amax = fmax(amax, fabs(v[i]));
+      y[i] = v[it].f(i) * r32 * g[i];
+      amax = fmaxf(amax, fabsf(y[i]));
     }
-    amax = fmax(amax, __shfl_xor_sync(0xffffffff, amax, 1));
-    amax = fmax(amax, __shfl_xor_sync(0xffffffff, amax, 2));
-    const int e = mx_block_exp_f64(amax);
-    const double inv = ldexp(1.0, -e);
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffff, amax, 1));
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffff, amax, 2));
+    const uint32_t mant = __float_as_uint(amax) & 0x7FFFFFu;
+    bool unsure = amax != 0.f &&
+                  (mant < kMantEdge || mant > 0x7FFFFFu - kMantEdge || amax < 0x1p-100f || !(amax < 0x1p+100f));
+    const int e = mx_block_exp_f32(amax);
+    const float inv = __uint_as_float(uint32_t(127 - e) << 23);
+    // E2M1 rounding is monotone: if both ends of [s (1 - kRel), s (1 + kRel)] round to the
+    // same code, every value in it (the reference's included) does
+    const float inv_lo = inv * (1.f - kRel), inv_hi = inv * (1.f + kRel);
+    uint32_t packed = 0, packed_hi = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      packed |= cvt_e2m1x2_raw(y[2 * i] * inv_lo, y[2 * i + 1] * inv_lo) << (8 * i);
+      packed_hi |= cvt_e2m1x2_raw(y[2 * i] * inv_hi, y[2 * i + 1] * inv_hi) << (8 * i);
+    }
+    unsure |= packed != packed_hi;
+    unsure = __shfl_xor_sync(0xffffffff, int(unsure), 1) | unsure;
+    unsure = __shfl_xor_sync(0xffffffff, int(unsure), 2) | unsure;
+    if (unsure) {
+      unsure_mask |= 1u << it;
+    } else if (ok) {
+      *reinterpret_cast<uint32_t*>(codes + row * (K / 2) + c / 2) = canon_neg_zero(packed);
+      if ((t & 3) == 0) sf[sf_offset(row, c / 32, kc_pad)] = uint8_t(e + 127);
+    }
+  }
+  // ---- pass 3 (rare): rows holding an undecided block redo them with the reference's f64
+  // operations: the mean of squares at f64 accuracy, IEEE division, exact E2M1 rounding
+  if (unsure_mask) s_unsure[rl] = 1;
+  if (!__syncthreads_or(unsure_mask != 0)) return;
+  const bool redo = s_unsure[rl] != 0;
+  double ss64 = 0.0;
+  if (redo) {
+#pragma unroll
+    for (int it = 0; it < kChunks; ++it)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double d = v[it].f(i);
+        ss64 = fma(d, d, ss64);
+      }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss64 += __shfl_xor_sync(0xffffffff, ss64, o);
+  __syncthreads();  // red[] reuse
+  if ((t & 31) == 0) red[rl][t >> 5] = ss64;
+  __syncthreads();
+  if (t == 0 && redo) {
+    double total = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) total += red[rl][w];
+    s_rms[rl] = sqrt(total / double(K) + eps);
+  }
+  __syncthreads();
+  if (!redo) return;
+  const double rms = s_rms[rl];
+#pragma unroll
+  for (int it = 0; it < kChunks; ++it) {
+    if (!__any_sync(0xffffffff, (unsure_mask >> it) & 1u)) continue;
+    const int c = it * (kTpr * 8) + t * 8;
+    const bool ok = row_ok && c < K;
+    double yd[8];
+    double amaxd = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      yd[i] = ok ? __ddiv_rn(double(v[it].f(i)), rms) * gain[c + i] : 0.0;
+      amaxd = fmax(amaxd, fabs(yd[i]));
+    }
+    amaxd = fmax(amaxd, __shfl_xor_sync(0xffffffff, amaxd, 1));
+    amaxd = fmax(amaxd, __shfl_xor_sync(0xffffffff, amaxd, 2));
+    const int e = mx_block_exp_f64(amaxd);
+    const double invd = ldexp(1.0, -e);
     uint32_t packed = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const double s = v[i] * inv;  // exact: power-of-two scaling
-      const uint32_t idx = e2m1_index_sw(fabs(s));
-      packed |= ((s < 0.0 && idx > 0) ? idx + 8 : idx) << (4 * i);
-    }
-    if (ok) {
+    for (int i = 0; i < 8; ++i) packed |= e2m1_code_f64(yd[i] * invd) << (4 * i);
+    if (ok && ((unsure_mask >> it) & 1u)) {
       *reinterpret_cast<uint32_t*>(codes + row * (K / 2) + c / 2) = packed;
-      if ((threadIdx.x & 3) == 0) sf[sf_offset(row, c / 32, kc_pad)] = uint8_t(e + 127);
+      if ((t & 3) == 0) sf[sf_offset(row, c / 32, kc_pad)] = uint8_t(e + 127);
     }
   }
 }

@@ -118,7 +118,9 @@ def rmsnorm_quantize_mx(x: torch.Tensor, gain: torch.Tensor, eps: float = 1e-6,
         cb, sb = mx_sizes(M, K)
         out = MxActivation(torch.empty(cb, dtype=torch.uint8, device=x.device),
                            torch.empty(sb, dtype=torch.uint8, device=x.device), M, K)
-    _lib.call("serq_rmsnorm_quant_mx", x.data_ptr(), _dtype_id(x), M, K, x.stride(0), gain.contiguous().data_ptr(),
+    gain = gain.contiguous()
+    g32 = gain.float()
+    _lib.call("serq_rmsnorm_quant_mx", x.data_ptr(), _dtype_id(x), M, K, x.stride(0), gain.data_ptr(), g32.data_ptr(),
               float(eps), out.codes.data_ptr(), out.sf.data_ptr(), _stream())
     return out
 

@@ -366,3 +366,18 @@ def test_rmsnorm_fused_linear_parity(D):
     y = lin.forward_rmsnorm(_cuda(x, torch.bfloat16), torch.from_numpy(gain).to("cuda")).float().cpu().numpy()
     mx, mean = O.parity_errors(y, O.forward_mx(O.rmsnorm(x, gain), main_t, comp))
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+def test_rmsnorm_quant_mx_exact_fallback_blocks(D):
+    # rows built so many blocks sit exactly on E2M1 decision points / power-of-two maxima after
+    # normalisation: the kernel must send them through its exact f64 path
+    K = 256
+    base = np.array([0.25, 0.75, 1.25, 1.75, 2.5, 3.5, 5.0, 6.0] * (K // 8))
+    x = np.stack([base * 2.0 ** k for k in range(-3, 5)])
+    x = O.bf16_round(x)
+    gain = np.ones(K)
+    act = D.rmsnorm_quantize_mx(_cuda(x, torch.bfloat16), torch.from_numpy(gain).to("cuda"), 0.0)
+    c, e = D.unpack_mx(act.codes, act.sf, *x.shape)
+    ref = O.mx_encode(O.rmsnorm(x, gain, 0.0), 32)
+    assert np.array_equal(e.cpu().numpy(), ref.block_scale_exponents)
+    assert np.array_equal(c.cpu().numpy(), ref.element_codes)
