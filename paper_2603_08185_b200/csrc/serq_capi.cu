@@ -703,7 +703,7 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
         CK(cudaMalloc(&hm->sk_ws, need * 4));
         hm->sk_ws_floats = need;
       }
-      if (left * 4 > hm->sk_cnt_n) {  // counters [left][2] then ready flags [left][2]
+      if (left * 4 > hm->sk_cnt_n) {  // ready flags [left][2 halves][2 ranks] (self-resetting)
         if (hm->sk_cnt) cudaFree(hm->sk_cnt);
         hm->sk_cnt = nullptr;
         CK(cudaMalloc(&hm->sk_cnt, left * 4 * 4));

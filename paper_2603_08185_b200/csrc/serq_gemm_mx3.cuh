@@ -22,6 +22,7 @@ constexpr int k3RB = 128 * 32;                // R B tile (r <= 64: 32 B per row
 constexpr int k3RSF = 1024;                   // R SFB: one chunk, both 128-row blocks
 constexpr int k3SmemBytes = 1024 + k3Slots * k3SlotBytes + k3RB + k3RSF + 4 * k2EpiStage + 512;
 static_assert(k3SmemBytes <= 232448, "exceeds the 227 KB dynamic shared memory limit");
+static_assert(131072 + 32768 <= k3Slots * k3SlotBytes, "split-tile exchange regions must fit in the drained pipeline");
 
 struct Pair3Maps {
   CUtensorMap a, b, r, y, sfa, sfb, sfr;
@@ -52,6 +53,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int cluster_id = blockIdx.x >> 1;
+#ifdef SERQ_DIAG_TS
+  if (p.dbg_ts && threadIdx.x == 0) {
+    uint64_t g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    p.dbg_ts[1024 + 148 * 24 + blockIdx.x * 2] = (long long)g;
+  }
+#endif
   const int n_clusters = gridDim.x >> 1;
   const int tiles_m = (p.M + 255) / 256;
   const int tiles_n = (p.N + kBN - 1) / kBN;
@@ -305,7 +313,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tmem_empty_leader = map_rank(smem_u32(tmem_empty), 0);
     pdl_wait();
     pdl_launch_dependents();
-    __shared__ int s_second;
     for (int i = 0; i < my_tiles; ++i) {
       const Item itm = item_of(cluster_id + i * n_clusters);
       const int tile = itm.tile;
@@ -315,126 +322,153 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int n0 = nt * kBN;
       const uint32_t b = i & 1;
 #ifdef SERQ_DIAG_TS
-      const bool est = p.dbg_ts && q == 0 && lane_id() == 0 && i < 4;
-      long long* ep = p.dbg_ts + 256 + (blockIdx.x * 4 + i) * 6 % 240;
+      // per CTA, per work item (< 6): [before tmem_full, after tmem_full, item epilogue done, half]
+      const bool est = p.dbg_ts && q == 0 && lane_id() == 0 && i < 6;
+      long long* ep = p.dbg_ts + 1024 + blockIdx.x * 24 + i * 4;
       if (est) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); ep[0] = (long long)g; }
 #endif
       mbar_wait(&tmem_full[b], (i >> 1) & 1);
       tc_fence_after();
 #ifdef SERQ_DIAG_TS
-      if (est) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); ep[1] = (long long)g; ep[5] = itm.half; }
+      if (est) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); ep[1] = (long long)g; ep[3] = itm.half; }
 #endif
       const uint32_t acc = (b ? kAccB1 : 0u) + lane_base;
       if (itm.half >= 0) {
-        // ---- split tile (always in the last round: the pipeline smem is free).
-        // The first finisher TMA-stores its fp32 partial and raises a flag; the
-        // second waits for the flag, TMA-loads the partner's partial chunk by
-        // chunk, adds its own accumulator and stores bf16.  a + b == b + a in
-        // fp32, so the result does not depend on which half finishes first.
+        // ---- split tile (always in the last round: the pipeline smem is drained).
+        // Symmetric exchange: half h finalises output chunks {2h, 2h+1} (64 columns
+        // each) and publishes its fp32 partial of the OTHER two chunks to its slab,
+        // then raises its flag; it waits for the partner's flag, TMA-loads the
+        // partner's partial of its own chunks, adds its accumulator (main K-half +
+        // partner K-half, a + b == b + a in fp32: order-independent) and stores bf16.
+        // Every box has its own slot of drained pipeline memory:
+        //   [0, 64 KB): 4 warps x 2 published chunks x 2 fp32 boxes (32 x 32, 128B swizzle)
+        //   [64, 128 KB): 4 warps x 2 partner chunks x 2 fp32 boxes
+        //   [128, 160 KB): 4 warps x 2 own chunks x 2 bf16 output boxes
         const int st_idx = tile - split_from;
-        uint8_t* wbuf = smem + q * 16384;  // 4 x 4-KB 128B-swizzled fp32 boxes (32 rows x 32 cols)
-        const uint32_t wb = smem_u32(wbuf);
-        const uint32_t rowb = wb + lane_id() * 128;
+        const int hf = itm.half;
         const uint32_t swz = lane_id() & 7;
         const int slab_row = ((st_idx * 2) * 2 + int(rank)) * 128 + q * 32;  // + half * 256 rows
-        if (q == 0 && lane_id() == 0) s_second = atomicAdd(&p.sk_cnt[st_idx * 2 + rank], 1);
-        named_bar_sync(1, 128);
-        const bool second = s_second == 1;
-        named_bar_sync(1, 128);
-        int* flag = p.sk_cnt + (n_tiles - split_from) * 2 + st_idx * 2 + rank;  // flags follow the counters
-        if (second && lane_id() == 0) {
-          while (ld_acquire_gpu(flag) == 0) {
-          }
-        }
-        __syncwarp();
+        int* flags = p.sk_cnt + st_idx * 4;                                    // [half][rank]
+        // 1) publish the partner's chunks
 #pragma unroll 1
-        for (int cc = 0; cc < 4; ++cc) {
-          const int c = b ? cc : (cc + 3) & 3;
+        for (int k = 0; k < 2; ++k) {
+          const int c = 2 * (hf ^ 1) + k;
           uint32_t v[32], w[32];
           tmem_ld_32x32b_x32(acc + c * 64, v);
           tmem_ld_32x32b_x32(acc + c * 64 + 32, w);
           tmem_ld_wait();
-          if (cc == 0) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane_id() == 0) mbar_arrive_cluster_relaxed(tmem_empty_leader);
+          uint8_t* wb8 = smem + q * 16384 + k * 8192;
+          const uint32_t rowb = smem_u32(wb8) + lane_id() * 128;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t* src = h ? w : v;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              st_shared_v4(rowb + h * 4096 + ((uint32_t(j) ^ swz) * 16), src[4 * j], src[4 * j + 1], src[4 * j + 2],
+                           src[4 * j + 3]);
           }
-          if (!second) {
-            if (lane_id() == 0) bulk_wait_read_all();
-            __syncwarp();
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane_id() == 0) {
+            tma_store_2d(&maps.ws, wb8, c * 64, slab_row + hf * 256);
+            tma_store_2d(&maps.ws, wb8 + 4096, c * 64 + 32, slab_row + hf * 256);
+            bulk_commit();
+          }
+        }
+
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && q == 0 && lane_id() == 0) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p.dbg_ts[1024 + 148 * 24 + 296 + blockIdx.x * 8 + 0] = (long long)g; }
+#endif
+        if (lane_id() == 0) bulk_wait_all();
+        fence_proxy_async_global();
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && q == 0 && lane_id() == 0) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p.dbg_ts[1024 + 148 * 24 + 296 + blockIdx.x * 8 + 1] = (long long)g; }
+#endif
+        named_bar_sync(1, 128);
+        if (q == 0 && lane_id() == 0) {
+          __threadfence();
+          st_release_gpu(flags + hf * 2 + int(rank), 1);
+        }
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && q == 0 && lane_id() == 0) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p.dbg_ts[1024 + 148 * 24 + 296 + blockIdx.x * 8 + 2] = (long long)g; }
+#endif
+
+        // 2) the partner's partial of our chunks
+        if (lane_id() == 0) {
+          int* pf = flags + (hf ^ 1) * 2 + int(rank);
+          while (ld_acquire_gpu(pf) == 0) {
+          }
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && q == 0) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p.dbg_ts[1024 + 148 * 24 + 296 + blockIdx.x * 8 + 3] = (long long)g; }
+#endif
+          fence_proxy_async_global();
+          mbar_expect_tx(&ws_bar[q], 16384);
+          for (int k = 0; k < 2; ++k) {
+            const int c = 2 * hf + k;
+            uint8_t* pb = smem + 65536 + q * 16384 + k * 8192;
+            tma_load_2d(pb, &maps.ws, &ws_bar[q], c * 64, slab_row + (hf ^ 1) * 256, kEvictFirst);
+            tma_load_2d(pb + 4096, &maps.ws, &ws_bar[q], c * 64 + 32, slab_row + (hf ^ 1) * 256, kEvictFirst);
+          }
+        }
+        __syncwarp();
+        mbar_wait(&ws_bar[q], 0);
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && q == 0 && lane_id() == 0) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p.dbg_ts[1024 + 148 * 24 + 296 + blockIdx.x * 8 + 4] = (long long)g; }
+#endif
+
+        // 3) own chunks: accumulator + partner partial -> bf16 -> TMA store
+#pragma unroll 1
+        for (int k = 0; k < 2; ++k) {
+          const int c = 2 * hf + k;
+          uint32_t v[32], w[32];
+          tmem_ld_32x32b_x32(acc + c * 64, v);
+          tmem_ld_32x32b_x32(acc + c * 64 + 32, w);
+          tmem_ld_wait();
+          const uint8_t* pb = smem + 65536 + q * 16384 + k * 8192;
+          float f[64];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 o = *reinterpret_cast<const float4*>(pb + h * 4096 + lane_id() * 128 + ((j ^ swz) * 16));
               const uint32_t* src = h ? w : v;
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                st_shared_v4(rowb + h * 4096 + ((uint32_t(j) ^ swz) * 16), src[4 * j], src[4 * j + 1], src[4 * j + 2],
-                             src[4 * j + 3]);
+              f[h * 32 + 4 * j] = __uint_as_float(src[4 * j]) + o.x;
+              f[h * 32 + 4 * j + 1] = __uint_as_float(src[4 * j + 1]) + o.y;
+              f[h * 32 + 4 * j + 2] = __uint_as_float(src[4 * j + 2]) + o.z;
+              f[h * 32 + 4 * j + 3] = __uint_as_float(src[4 * j + 3]) + o.w;
             }
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint8_t* ybox = smem + 131072 + q * 8192 + (k * 2 + h) * 2048;
+            const uint32_t ybase = smem_u32(ybox) + lane_id() * 64;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              st_shared_v4(ybase + ((uint32_t(j) ^ sw) * 16), pack_bf16x2(f[h * 32 + 8 * j], f[h * 32 + 8 * j + 1]),
+                           pack_bf16x2(f[h * 32 + 8 * j + 2], f[h * 32 + 8 * j + 3]),
+                           pack_bf16x2(f[h * 32 + 8 * j + 4], f[h * 32 + 8 * j + 5]),
+                           pack_bf16x2(f[h * 32 + 8 * j + 6], f[h * 32 + 8 * j + 7]));
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane_id() == 0) {
-              tma_store_2d(&maps.ws, wbuf, c * 64, slab_row + itm.half * 256);
-              tma_store_2d(&maps.ws, wbuf + 4096, c * 64 + 32, slab_row + itm.half * 256);
+            if (lane_id() == 0 && m_own < p.M) {
+              tma_store_2d(&maps.y, ybox, n0 + c * 64 + h * 32, m_own + q * 32);
               bulk_commit();
             }
-          } else {
-            // partner's partial for this chunk -> smem, add, bf16, TMA store
-            if (lane_id() == 0) {
-              bulk_wait_read_all();
-              mbar_expect_tx(&ws_bar[q], 8192);
-              tma_load_2d(wbuf, &maps.ws, &ws_bar[q], c * 64, slab_row + (itm.half ^ 1) * 256, kEvictFirst);
-              tma_load_2d(wbuf + 4096, &maps.ws, &ws_bar[q], c * 64 + 32, slab_row + (itm.half ^ 1) * 256, kEvictFirst);
-            }
-            mbar_wait(&ws_bar[q], cc & 1);
-            float f[64];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float4 o = *reinterpret_cast<const float4*>(wbuf + h * 4096 + lane_id() * 128 + ((j ^ swz) * 16));
-                const uint32_t* src = h ? w : v;
-                f[h * 32 + 4 * j] = __uint_as_float(src[4 * j]) + o.x;
-                f[h * 32 + 4 * j + 1] = __uint_as_float(src[4 * j + 1]) + o.y;
-                f[h * 32 + 4 * j + 2] = __uint_as_float(src[4 * j + 2]) + o.z;
-                f[h * 32 + 4 * j + 3] = __uint_as_float(src[4 * j + 3]) + o.w;
-              }
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              if (lane_id() == 0) bulk_wait_read_all();
-              __syncwarp();
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                st_shared_v4(rbase + ((uint32_t(j) ^ sw) * 16), pack_bf16x2(f[h * 32 + 8 * j], f[h * 32 + 8 * j + 1]),
-                             pack_bf16x2(f[h * 32 + 8 * j + 2], f[h * 32 + 8 * j + 3]),
-                             pack_bf16x2(f[h * 32 + 8 * j + 4], f[h * 32 + 8 * j + 5]),
-                             pack_bf16x2(f[h * 32 + 8 * j + 6], f[h * 32 + 8 * j + 7]));
-              fence_proxy_async_smem();
-              __syncwarp();
-              if (lane_id() == 0 && m_own < p.M) {
-                tma_store_2d(&maps.y, stage_out, n0 + c * 64 + h * 32, m_own + q * 32);
-                bulk_commit();
-              }
-            }
-            __syncwarp();
           }
         }
-        if (!second) {
-          // partial globally visible -> raise the flag for the partner CTA
-          if (lane_id() == 0) bulk_wait_all();
-          fence_proxy_async_global();
-          named_bar_sync(1, 128);
-          if (q == 0 && lane_id() == 0) {
-            __threadfence();
-            st_release_gpu(flag, 1);
-          }
-        } else {
-          named_bar_sync(1, 128);
-          if (q == 0 && lane_id() == 0) {
-            p.sk_cnt[st_idx * 2 + rank] = 0;  // ready for the next launch
-            *flag = 0;
-          }
-        }
+        // every accumulator column has been read (no later tile reuses it: last round)
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive_cluster_relaxed(tmem_empty_leader);
+        named_bar_sync(1, 128);
+        if (q == 0 && lane_id() == 0) flags[(hf ^ 1) * 2 + int(rank)] = 0;  // consumed: ready for the next launch
+#ifdef SERQ_DIAG_TS
+        if (p.dbg_ts && q == 0 && lane_id() == 0) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p.dbg_ts[1024 + 148 * 24 + 296 + blockIdx.x * 8 + 5] = (long long)g; }
+#endif
+
+#ifdef SERQ_DIAG_TS
+        if (est) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); ep[2] = (long long)g; }
+#endif
         continue;
       }
 #pragma unroll 1
@@ -449,14 +483,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane_id() == 0) mbar_arrive_cluster_relaxed(tmem_empty_leader);
         }
+        // the CTA's final tile: the pipeline is drained, so each (chunk, half) box gets its
+        // own 2 KB of slot memory and the TMA stores go out without waiting on each other
+        const bool final_tile = i == my_tiles - 1 && !(p.dbg & (1 << 26));
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t* src = h ? w : v;
-          if (lane_id() == 0) bulk_wait_read_all();
+          uint8_t* box = final_tile ? smem + q * 16384 + (cc * 2 + h) * 2048 : stage_out;
+          const uint32_t bbase = final_tile ? smem_u32(box) + lane_id() * 64 : rbase;
+          if (!final_tile && lane_id() == 0) bulk_wait_read_all();
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            st_shared_v4(rbase + ((uint32_t(j) ^ sw) * 16),
+            st_shared_v4(bbase + ((uint32_t(j) ^ sw) * 16),
                          pack_bf16x2(__uint_as_float(src[8 * j]), __uint_as_float(src[8 * j + 1])),
                          pack_bf16x2(__uint_as_float(src[8 * j + 2]), __uint_as_float(src[8 * j + 3])),
                          pack_bf16x2(__uint_as_float(src[8 * j + 4]), __uint_as_float(src[8 * j + 5])),
@@ -464,11 +503,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane_id() == 0 && m_own < p.M) {
-            tma_store_2d(&maps.y, stage_out, n0 + c * 64 + h * 32, m_own + q * 32);
+            tma_store_2d(&maps.y, box, n0 + c * 64 + h * 32, m_own + q * 32);
             bulk_commit();
           }
         }
       }
+#ifdef SERQ_DIAG_TS
+      if (est) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); ep[2] = (long long)g; }
+#endif
     }
     if (lane_id() == 0) bulk_wait_all();
     __syncwarp();
@@ -480,6 +522,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(0u));
   }
+#ifdef SERQ_DIAG_TS
+  if (p.dbg_ts && threadIdx.x == 0) {
+    uint64_t g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    p.dbg_ts[1024 + 148 * 24 + blockIdx.x * 2 + 1] = (long long)g;
+  }
+#endif
 }
 
 }  // namespace serq

@@ -1,0 +1,27 @@
+// How many clusters of size 2 / 4 / 8 fit at once with ~224 KB of shared memory per CTA
+// (one CTA per SM)?  Answers whether a 4-CTA cluster layout would strand SMs.
+#include <cstdio>
+#include <cuda_runtime.h>
+__global__ void k(int* p) { if (p) p[0] = 1; }
+int main() {
+  int smem = 224 * 1024;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  for (int cs : {1, 2, 4, 8, 16}) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(148 * 4);
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = cs;
+    a[0].val.clusterDim.y = 1;
+    a[0].val.clusterDim.z = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = 1;
+    int n = -1;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&n, k, &cfg);
+    printf("cluster %2d: max active clusters %d -> %d CTAs (%s)\n", cs, n, n * cs, cudaGetErrorString(e));
+  }
+  return 0;
+}

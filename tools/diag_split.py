@@ -32,4 +32,11 @@ for flags in [int(f) for f in os.environ.get('FLAGS', '0,8192').split(',')]:
         full = (v[ok, 1] - t0) / 1e3; end = (v[ok, 2] - t0) / 1e3; half = v[ok, 3]
         print(f"  item {i}: ctas={ok.sum():3d} halves={int((half >= 0).sum()):3d} acc done min/med/max "
               f"{full.min():6.2f}/{np.median(full):6.2f}/{full.max():6.2f}  epi end {end.min():6.2f}/{np.median(end):6.2f}/{end.max():6.2f}")
+    sk = t[1024 + 148 * 24 + 296:1024 + 148 * 24 + 296 + 148 * 8].reshape(148, 8)[:, :6]
+    ok = sk[:, 0] > 0
+    if ok.any():
+        names = ["publish issued", "publish landed", "flag raised", "partner flag seen", "partner partial in", "done"]
+        for k, nm in enumerate(names):
+            col = (sk[ok, k] - t0) / 1e3
+            print(f"    split {nm:18s} min/med/max {col.min():6.2f}/{np.median(col):6.2f}/{col.max():6.2f}")
 lib.serq_set_debug_flags(0)
