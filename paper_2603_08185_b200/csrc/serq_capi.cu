@@ -171,6 +171,7 @@ struct serq_linear {
   void* ws_y = nullptr;
   // end-to-end pipeline: H2D and D2H copy streams + per-chunk events (created lazily)
   cudaStream_t e2e_in = nullptr, e2e_out = nullptr;
+  std::mutex e2e_mu;  // the end-to-end scratch and streams are per handle: one host call at a time
   cudaEvent_t e2e_ev[3 * kE2eMaxChunks + 1] = {};
 };
 
@@ -916,6 +917,7 @@ int serq_linear_int_addend(const serq_linear_t* h, const int8_t* a_codes, const 
 
 int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* y_host, serq_stream_t stream) {
   if (!h || h->mode != kModeMX) return fail(SERQ_EINVAL, "handle is not an MX linear");
+  std::lock_guard<std::mutex> lock(h->e2e_mu);
   if (h->r > 0 && !h->contiguous)
     return fail(SERQ_EINVAL, "serq_forward_mx_host supports the permuted (contiguous) salient layout only");
   if (M <= 0) return fail(SERQ_EINVAL, "x must be non-empty");
