@@ -105,25 +105,28 @@ def time_graph(g, flush: Flusher | None, n=20, warm=3):
     return statistics.median(ts)
 
 
-def device_mx_linear(K: int, N: int, r: int, seed: int = 1):
+def device_mx_linear(K: int, N: int, r: int, seed: int = 1, salient_idx=None):
     """Synthetic SERQ MX linear built on the device: W ~ N(0, 0.02) [K, N],
     main_t = mx_encode(W^T), R = exact residual of the first r rows (the
-    salient rows after the offline permutation), encoded [N, r]."""
+    salient rows after the offline permutation), encoded [N, r].  With
+    ``salient_idx`` (length r) R covers those rows instead (gather fallback)."""
     g = torch.Generator(device="cuda").manual_seed(seed)
     wt = torch.randn((N, K), generator=g, device="cuda", dtype=torch.float32) * 0.02
     act = D.quantize_mx(wt)
     codes, exps = D.unpack_mx(act.codes, act.sf, N, K)
     if r:
         mags = torch.tensor([0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0], device="cuda")
-        c = codes[:, :r].long()
+        cols = torch.arange(r, device="cuda") if salient_idx is None else torch.as_tensor(
+            np.asarray(salient_idx), device="cuda", dtype=torch.long)
+        c = codes[:, cols].long()
         dec = torch.where((c & 8) != 0, -1.0, 1.0) * mags[c & 7]
-        dec = dec * torch.exp2(exps[:, : r // 32].float()).repeat_interleave(32, dim=1)
-        resid = (wt[:, :r] - dec).contiguous()
+        dec = dec * torch.exp2(exps[:, cols // 32].float())
+        resid = (wt[:, cols] - dec).contiguous()
         ra = D.quantize_mx(resid)
         rc, re_ = D.unpack_mx(ra.codes, ra.sf, N, r)
     else:
         rc = re_ = None
-    lin = D.MxLinear(codes, exps, rc, re_, np.arange(r) if r else None)
+    lin = D.MxLinear(codes, exps, rc, re_, (np.arange(r) if salient_idx is None else np.asarray(salient_idx)) if r else None)
     del wt
     return lin
 

@@ -240,28 +240,24 @@ static int act_quant_mx_impl(const void* x, int dtype, int64_t M, int64_t K, int
   // them (grid over the padded extent); the f64 / gather kernels need the memset
   if ((M % 128 || K % 256) && (dtype == SERQ_F64)) CK(cudaMemsetAsync(sf, 0, sf_bytes_of(M, K), st));
   const int krc = gather_idx ? kc_pad_of(r) : 0;
-  if (gather_idx && (M % 128 || r % 256)) CK(cudaMemsetAsync(xs_sf, 0, sf_bytes_of(M, r), st));
+  // the gathered slice's SF padding must read as a finite scale: the fast kernel's z = 1 plane
+  // writes it; the f64 kernel needs the memset
+  if (gather_idx && dtype == SERQ_F64 && (M % 128 || r % 256)) CK(cudaMemsetAsync(xs_sf, 0, sf_bytes_of(M, r), st));
   if (dtype != SERQ_F64) {
     const int64_t m_rows = (M % 128) ? cdiv(M, 128) * 128 : M;  // cover the SF row padding
-    const dim3 grid(unsigned(cdiv(int64_t(kc) * 16, 256)), unsigned(cdiv(m_rows, kMxRows)));
+    // z = 1 plane: the gathered salient slice (its SF tile padding included), same launch
+    const int64_t g_threads = gather_idx ? cdiv(M, 128) * 128 * int64_t(krc) * 16 : 0;
+    dim3 grid(unsigned(cdiv(int64_t(kc) * 16, 256)), unsigned(cdiv(m_rows, kMxRows)), gather_idx ? 2u : 1u);
+    while (gather_idx && int64_t(grid.x) * grid.y * 256 < g_threads) ++grid.y;  // the z = 1 plane must cover it
+    const MxGather mg{gather_idx, r, xs_codes, xs_sf, krc};
     if (dtype == SERQ_BF16) {
       CK(launch_pdl(mx_encode_fast_kernel<__nv_bfloat16>, grid, dim3(256), 0, st, static_cast<const __nv_bfloat16*>(x),
-                    int(M), int(K), ldx, codes, sf, kc));
+                    int(M), int(K), ldx, codes, sf, kc, mg));
     } else {
       CK(launch_pdl(mx_encode_fast_kernel<float>, grid, dim3(256), 0, st, static_cast<const float*>(x), int(M), int(K),
-                    ldx, codes, sf, kc));
+                    ldx, codes, sf, kc, mg));
     }
     LAUNCH_CHECK("mx_encode_fast");
-    if (gather_idx) {
-      const dim3 g2(unsigned(cdiv(M * (r / 8), 256)));
-      if (dtype == SERQ_BF16)
-        mx_encode_kernel<__nv_bfloat16><<<g2, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), M, K, ldx, codes,
-                                                            sf, kc, gather_idx, r, xs_codes, xs_sf, krc, 0);
-      else
-        mx_encode_kernel<float><<<g2, 256, 0, st>>>(static_cast<const float*>(x), M, K, ldx, codes, sf, kc,
-                                                    gather_idx, r, xs_codes, xs_sf, krc, 0);
-      LAUNCH_CHECK("mx_encode_gather");
-    }
     return SERQ_OK;
   }
   const int64_t nb_main = cdiv(M * (K / 8), 256);

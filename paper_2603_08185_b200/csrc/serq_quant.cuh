@@ -187,10 +187,55 @@ __device__ __forceinline__ int mx_block_exp_bf16bits(uint32_t amax_bits) {
   const int ef = int(amax_bits >> 7);
   return amax_bits == 0 ? 0 : (ef == 0 ? -127 : max(ef - 129, -127));
 }
+// The salient slice x[:, idx] of a non-permuted layer (compensate.py:335 re-encodes it;
+// the common case for q/k/v and gate/up) -- encoded by the z = 1 plane of the
+// fast quantizer's grid, concurrently with the main encode instead of in a second launch.
+struct MxGather {
+  const int32_t* idx;
+  int r;
+  uint8_t* xs_codes;
+  uint8_t* xs_sf;
+  int kc_pad_r;
+};
+
+template <typename T>
+__device__ __forceinline__ void mx_encode_gather_part(const T* __restrict__ x, int M, int64_t ldx, const MxGather& g) {
+  const int64_t t = (int64_t(blockIdx.y) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+  const int per_row = g.kc_pad_r * 16;  // 8-element groups incl. the SF chunk padding beyond r
+  const int64_t total = int64_t(((M + 127) >> 7) << 7) * per_row;  // rows padded to the SF tile
+  if ((int64_t(blockIdx.y) * gridDim.x + blockIdx.x) * blockDim.x >= total) return;  // whole CTA idle
+  const bool active = t < total;
+  const int64_t row = active ? t / per_row : 0;
+  const int c0 = active ? int(t - row * per_row) * 8 : 0;
+  const bool row_ok = active && row < M && c0 < g.r;
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = row_ok ? In<T>::f(x[row * ldx + g.idx[c0 + i]]) : 0.f;
+  float amax = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(v[i]));
+  amax = fmaxf(amax, __shfl_xor_sync(0xffffffff, amax, 1));
+  amax = fmaxf(amax, __shfl_xor_sync(0xffffffff, amax, 2));
+  const int e = mx_block_exp_f32(amax);
+  if (!active) return;
+  const float inv = __uint_as_float(uint32_t(127 - e) << 23);
+  uint32_t packed = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) packed |= cvt_e2m1x2(v[2 * i] * inv, v[2 * i + 1] * inv) << (8 * i);
+  if (row_ok) *reinterpret_cast<uint32_t*>(g.xs_codes + row * (g.r / 2) + c0 / 2) = packed;
+  if ((threadIdx.x & 3) == 0) g.xs_sf[sf_offset(row, c0 / 32, g.kc_pad_r)] = uint8_t(e + 127);
+}
+
 template <typename T, int kMxRows = serq::kMxRows>
 __global__ void __launch_bounds__(256) mx_encode_fast_kernel(const T* __restrict__ x, int M, int K, int64_t ldx,
                                                              uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
-                                                             int kc_pad) {
+                                                             int kc_pad, MxGather gather = MxGather{}) {
+  if (blockIdx.z == 1) {
+    pdl_launch_dependents();
+    pdl_wait();
+    mx_encode_gather_part<T>(x, M, ldx, gather);
+    return;
+  }
   const int c8 = blockIdx.x * 256 + threadIdx.x;  // 8-element group within the row
   const int r0 = blockIdx.y * kMxRows;
   const bool col_ok = c8 < (K >> 3);
