@@ -157,6 +157,7 @@ struct serq_linear {
   bool has_r32 = false;
   void* w4 = nullptr;                                // INT: packed int4 weights, tiled [N/128][K/128][128][64 B]
   CUtensorMap map_w4, map_r_pair;                    // INT pair kernel maps (R with 128-row boxes)
+  CUtensorMap map_w8;                                // INT pair kernel, direct int8 weights: 128 B x 128-row boxes
   bool has_w4 = false;
   // CTA-pair split last wave: fp32 partials + per-(tile, rank) counters
   float* sk_ws = nullptr;
@@ -491,6 +492,7 @@ int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t
   colsum_kernel<<<unsigned(cdiv(N, 256)), 256, 0, st>>>(codes, K, N, scales, h->colsum, h->sw);
   if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_int launch failed"));
   int rc = make_map(&h->map_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, kBN);
+  if (!rc) rc = make_map(&h->map_w8, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, 128);
   if (rc) return bail(rc);
   if (w_bits <= 4) {
     // packed INT4 copy for the CTA-pair kernel (widened to INT8 in shared memory)
@@ -813,12 +815,18 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   if (ldy < h->N || ldy % 8) return fail(SERQ_EINVAL, "ldy must be >= N and a multiple of 8");
   const bool need_xs = h->r_mode == SERQ_R_DENSE || (h->r_mode == SERQ_R_INT && !h->contiguous);
   if (need_xs && !xs) return fail(SERQ_EINVAL, "this R mode needs the quantizer's xs slice");
-  const bool pair_ok = h->has_w4 && M > 128 && (h->r_mode != SERQ_R_INT || h->contiguous) && h->r <= 128 &&
+  // CTA-pair kernel: int8 weights TMA'd directly (default; measured faster than widening packed
+  // INT4 in shared memory, which remains under debug flag 1<<28)
+  const bool widen = (g_debug_flags & (1 << 28)) && h->has_w4;
+  const bool pair_ok = M > 128 && (h->r_mode != SERQ_R_INT || h->contiguous) && h->r <= 128 &&
                        (h->r_mode != SERQ_R_DENSE || h->r <= 64) && !(g_debug_flags & 65536);
   if (pair_ok) {
     static bool attri = false;
     if (!attri) {
-      CK(cudaFuncSetAttribute(serq_i8_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kI8Smem));
+      CK(cudaFuncSetAttribute(serq_i8_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              I8Cfg<false>::kSmem));
+      CK(cudaFuncSetAttribute(serq_i8_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              I8Cfg<true>::kSmem));
       attri = true;
     }
     I8Maps im;
@@ -829,8 +837,8 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
       rc = make_map(&im.xs, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xs, h->r, M, h->r * 2, 64, 128);
     if (rc) return rc;
     if (h->r_mode != SERQ_R_DENSE) im.xs = im.a;
-    im.bp = h->map_w4;
-    im.r = h->r_mode != SERQ_R_NONE ? h->map_r_pair : h->map_w4;
+    im.bp = widen ? h->map_w4 : h->map_w8;
+    im.r = h->r_mode != SERQ_R_NONE ? h->map_r_pair : im.bp;
     GemmParams p{};
     p.dbg = g_debug_flags;
     p.M = int(M);
@@ -847,14 +855,16 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     p.sr = h->sr;
     p.colsum_r = h->colsum_r;
     p.acc_dump = acc_dump;
-  p.addend = addend;
     p.addend = addend;
     p.accr_dump = accr_dump;
     p.dbg_ts = g_debug_ts;
     const int64_t tiles = cdiv(M, 256) * cdiv(h->N, kBN);
     const int64_t max_pairs = sm_count() / 2;
     const dim3 grid(unsigned(2 * (tiles < max_pairs ? tiles : max_pairs)));
-    serq_i8_pair_kernel<<<grid, kI8Threads, kI8Smem, S(stream)>>>(im, p);
+    if (widen)
+      serq_i8_pair_kernel<false><<<grid, I8Cfg<false>::kThreads, I8Cfg<false>::kSmem, S(stream)>>>(im, p);
+    else
+      serq_i8_pair_kernel<true><<<grid, I8Cfg<true>::kThreads, I8Cfg<true>::kSmem, S(stream)>>>(im, p);
     LAUNCH_CHECK("serq_i8_pair_kernel");
     return SERQ_OK;
   }

@@ -23,17 +23,27 @@
 
 namespace serq {
 
-constexpr int kI8Stages = 4;
 constexpr int kI8A = 128 * 128;    // own 128 activation rows x 128 int8
 constexpr int kI8Bp = 128 * 64;    // packed int4 staging, own 128 weight rows
 constexpr int kI8B = 128 * 128;    // widened int8 operand
-constexpr int kI8Stage = kI8A + kI8Bp + kI8B;  // 40 KB
 constexpr int kI8Side = 2 * 16384;             // R operands: [A' (dense only)] + B_R
 constexpr int kI8Const = 4 * 256 * 4;
 constexpr int kI8Threads = 512;
 constexpr int kI8TrWarps = 8;  // warps 8..15
-constexpr int kI8Smem = 1024 + kI8Stages * kI8Stage + kI8Side + kI8Const + 4 * 2048 + 512;
-static_assert(kI8Smem <= 232448, "smem budget");
+// Two weight feeds:
+//  kDirect = false: packed INT4 in HBM, widened in SMEM by the transform warps (4 x 40 KB stages)
+//  kDirect = true : int8 in HBM, TMA'd straight into the 128B-swizzled operand (5 x 32 KB stages,
+//                   no transform warps): twice the weight bytes, but no SMEM widening traffic
+template <bool kDirect>
+struct I8Cfg {
+  static constexpr int kStages = kDirect ? 5 : 4;
+  static constexpr int kBp = kDirect ? 0 : kI8Bp;
+  static constexpr int kStage = kI8A + kBp + kI8B;
+  static constexpr int kSmem = 1024 + kStages * kStage + kI8Side + kI8Const + 4 * 2048 + 512;
+  static constexpr int kThreads = kDirect ? 256 : kI8Threads;
+  static_assert(kSmem <= 232448, "smem budget");
+};
+constexpr int kI8Smem = I8Cfg<false>::kSmem;
 
 struct I8Maps {
   CUtensorMap a, bp, r, xs, y;
@@ -99,8 +109,12 @@ __device__ __forceinline__ uint2 widen_int4x8(uint32_t w) {
   return make_uint2(__byte_perm(lo, hi, 0x5140), __byte_perm(lo, hi, 0x7362));
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
+template <bool kDirect>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThreads, 1)
     serq_i8_pair_kernel(const __grid_constant__ I8Maps maps, const GemmParams p) {
+  constexpr int kI8Stages = I8Cfg<kDirect>::kStages;
+  constexpr int kI8Stage = I8Cfg<kDirect>::kStage;
+  constexpr int kBp = I8Cfg<kDirect>::kBp;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* side = smem + kI8Stages * kI8Stage;       // [A' 16K][B_R 16K]
@@ -175,10 +189,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
           if (with_side && i > 0) mbar_wait(side_empty, (i - 1) & 1);
           const uint32_t fbar = map_rank(smem_u32(&full[s]), 0);
           const uint32_t st = sb + s * kI8Stage;
-          if (leader) mbar_expect_tx(&full[s], 2u * (kI8A + (with_side ? (dense ? 2 * 16384 : 16384) : 0)));
-          mbar_expect_tx(&bpk[s], kI8Bp);
-          tma_load_2d(smem + s * kI8Stage + kI8A, &maps.bp, &bpk[s], 0, ((n_half >> 7) * ks + kk) * 128,
-                      kEvictNormal);
+          if (leader)
+            mbar_expect_tx(&full[s], 2u * (kI8A + (kDirect ? kI8B : 0) + (with_side ? (dense ? 2 * 16384 : 16384) : 0)));
+          if constexpr (kDirect) {
+            tma_load_2d_pair(st + kI8A, &maps.bp, fbar, kk * 128, n_half, kEvictNormal);  // int8 [N, K] rows
+          } else {
+            mbar_expect_tx(&bpk[s], kI8Bp);
+            tma_load_2d(smem + s * kI8Stage + kI8A, &maps.bp, &bpk[s], 0, ((n_half >> 7) * ks + kk) * 128,
+                        kEvictNormal);
+          }
           tma_load_2d_pair(st, &maps.a, fbar, kk * 128, m_own, kEvictNormal);
           if (with_side) {
             tma_load_2d_pair(sside + 16384, &maps.r, fbar, 0, n_half, kEvictNormal);
@@ -195,7 +214,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
       const uint32_t id_r = dense ? idesc_bf16(256, kBN) : id_main;
       const uint32_t total = uint32_t(my_tiles) * ks;
       if (total > 0) {
-        mbar_wait_cluster(&bready[0], 0);
+        mbar_wait_cluster(kDirect ? &full[0] : &bready[0], 0);
         tc_fence_after();
       }
       uint32_t g = 0;
@@ -213,7 +232,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
         for (int kk = 0; kk < ks; ++kk, ++g) {
           const int s = g % kI8Stages;
           const uint32_t st = sb + s * kI8Stage;
-          const uint64_t a = make_sdesc(st, 16, 1024, 2), b = make_sdesc(st + kI8A + kI8Bp, 16, 1024, 2);
+          const uint64_t a = make_sdesc(st, 16, 1024, 2), b = make_sdesc(st + kI8A + kBp, 16, 1024, 2);
           const uint32_t first = kk > 0 ? 1u : 0u;
           const bool no_mma = p.dbg & (1 << 18);
           if (elect_one() && !no_mma) {
@@ -235,7 +254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
 #endif
           if (g + 1 < total) {
             const uint32_t gn = g + 1;
-            mbar_wait_cluster(&bready[gn % kI8Stages], (gn / kI8Stages) & 1);
+            mbar_wait_cluster(kDirect ? &full[gn % kI8Stages] : &bready[gn % kI8Stages], (gn / kI8Stages) & 1);
             tc_fence_after();
           }
 #ifdef SERQ_DIAG_TS
@@ -255,6 +274,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
     }
   } else if (warp >= 8) {
     // ------------------------------------------------------------ INT4 -> INT8 transform (both CTAs)
+    if constexpr (kDirect) return;  // (no such warps are launched in direct mode)
     const int tw = int(warp) - 8;  // 0..7
     const uint32_t bready_leader = map_rank(smem_u32(&bready[0]), 0);
     uint32_t g = 0;
@@ -271,7 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
         if (stamp) p.dbg_ts[8 * g + 1] = clock64();
 #endif
         const uint8_t* pk = smem + s * kI8Stage + kI8A;
-        const uint32_t bdst = smem_u32(smem + s * kI8Stage + kI8A + kI8Bp);
+        const uint32_t bdst = smem_u32(smem + s * kI8Stage + kI8A + kBp);
         // 1024 tasks (128 rows x 8 output chunks of 16 B); a warp covers 4 rows per pass.
         // All loads first: the st.shared asm below is a compiler barrier.
         constexpr int kIt = 1024 / (32 * kI8TrWarps);
