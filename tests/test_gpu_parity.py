@@ -381,3 +381,46 @@ def test_rmsnorm_quant_mx_exact_fallback_blocks(D):
     ref = O.mx_encode(O.rmsnorm(x, gain, 0.0), 32)
     assert np.array_equal(e.cpu().numpy(), ref.block_scale_exponents)
     assert np.array_equal(c.cpu().numpy(), ref.element_codes)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_tp_shards_on_device_match_single_device(D, world):
+    # SURVEY 8(e) with the real kernels: the per-rank shards of a column-parallel and a
+    # row-parallel MX linear, run one after another on this GPU, reproduce the unsharded
+    # layer -- column shards concatenate bit-exactly, row shards sum (the all-reduce, in
+    # bf16 as NCCL would) to the single-device oracle within tolerance
+    from paper_2603_08185_b200 import tp
+
+    rng = np.random.default_rng(40 + world)
+    M, K, N, r_rank = 300, 1024, 512, 32
+    w = rng.standard_normal((K, N)) * 0.02
+    x = O.bf16_round(O.synthetic_activations(M, K, 8, 50.0, 41))
+    xt = _cuda(x, torch.bfloat16)
+    # column parallel: shard N, X replicated
+    main_t, comp = O.build_serq_rtn_mx(w, np.arange(64), 32)
+    full = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                      comp.r_q.block_scale_exponents, np.arange(64))(xt)
+    parts = []
+    for rank in range(world):
+        n0, n1 = tp.column_shard(N, world, rank)
+        c, e, rc, re_ = tp.shard_columns_mx(main_t.element_codes, main_t.block_scale_exponents,
+                                            comp.r_q.element_codes, comp.r_q.block_scale_exponents, n0, n1)
+        parts.append(D.MxLinear(c, e, rc, re_, np.arange(64))(xt))
+    assert torch.equal(torch.cat(parts, dim=1), full)
+    # row parallel: each rank's K-slice leads with its own salient channels; one all-reduce
+    perm, _ = tp.row_parallel_salient_layout(np.abs(w).max(axis=1), world, r_rank)
+    wp, xp = w[perm], x[:, perm]
+    acc = None
+    for rank in range(world):
+        k0, k1 = tp.row_shard(K, world, rank)
+        mt, cp = O.build_serq_rtn_mx(wp[k0:k1], np.arange(r_rank), 32)
+        lin = D.MxLinear(mt.element_codes, mt.block_scale_exponents, cp.r_q.element_codes,
+                         cp.r_q.block_scale_exponents, np.arange(r_rank))
+        y = lin(_cuda(np.ascontiguousarray(xp[:, k0:k1]), torch.bfloat16)).float()
+        acc = y if acc is None else acc + y  # the all-reduce, accumulated in fp32
+    union = np.concatenate([tp.row_shard(K, world, rk)[0] + np.arange(r_rank) for rk in range(world)])
+    mg, cg = O.build_serq_rtn_mx(wp, union, 32)
+    mx, mean = O.parity_errors(acc.bfloat16().float().cpu().numpy(), O.forward_mx(xp, mg, cg))
+    # each rank's partial is rounded to bf16 before the reduction (world extra roundings of
+    # magnitude ~|Y| / sqrt(world)): the mean tolerance scales with the number of partials
+    assert mx <= TOL_MAX and mean <= TOL_MEAN * world, (mx, mean)
