@@ -288,15 +288,16 @@ int serq_act_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t l
   const dim3 grid(static_cast<unsigned>(M));
   if (dtype == SERQ_BF16 && K % 8 == 0 && K <= 8192 && ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(codes) & 7) == 0) {
-    const int nv = int(cdiv(K, 2048));
+    // one token row per 256-thread CTA (measured faster than 2 rows per CTA for K = 4096)
     const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
-#define SERQ_INTQ(NV)                                                                                          \
-  int_quant_bf16_kernel<NV><<<grid, 256, 0, st>>>(xb, int(K), ldx, bits, symmetric, codes, scale64, scale32, zp, \
-                                                  salient_idx, r, xs_out, xs_kind)
-    if (nv == 1) SERQ_INTQ(1);
-    else if (nv == 2) SERQ_INTQ(2);
-    else if (nv == 3) SERQ_INTQ(3);
-    else SERQ_INTQ(4);
+    const int cpt = int(cdiv(K / 8, 256));
+    const dim3 gq{unsigned(M)};
+#define SERQ_INTQ(P, C)                                                                                          \
+  CK(launch_pdl(int_quant_bf16_kernel<P, C>, gq, dim3(256), 0, st, xb, int(M), int(K), ldx, bits, symmetric, codes, \
+                scale64, scale32, zp, salient_idx, r, xs_out, xs_kind))
+    if (cpt <= 1) SERQ_INTQ(256, 1);
+    else if (cpt <= 2) SERQ_INTQ(256, 2);
+    else SERQ_INTQ(256, 4);
 #undef SERQ_INTQ
     LAUNCH_CHECK("int_quant_bf16");
     return SERQ_OK;

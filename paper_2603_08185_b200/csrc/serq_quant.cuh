@@ -560,6 +560,27 @@ __device__ __forceinline__ double rint_quot(T xv, double s, float inv32, double 
   }
 }
 
+// rint(x / s) as an int for 16-bit / 32-bit inputs: the f32 fast path decides with the proven
+// margin and everything stays on the FP32 / integer pipes (this GPU's FP64 pipe runs ~64x
+// slower); only values within the margin of a .5 tie take the correctly rounded f64 division.
+// Returns clip(rint(x / s) + zp, qmin, qmax).  |x/s| < 2^21 implies |zp| < 2^21 + 2^bits
+// (x lies in [lo, hi], zp = rint(-lo/s)), so the int sum is exact; larger quotients take
+// the reference's f64 expression.
+template <typename T>
+__device__ __forceinline__ int int_code(T xv, double s, float inv32, int zp, int qmin, int qmax) {
+  const float xf = In<T>::f(xv);
+  const float q = xf * inv32;  // |q - x/s| <= |q| * 2^-22.9
+  if (fabsf(q) < 0x1p21f) {
+    const float fl = floorf(q);
+    const float fr = q - fl;  // exact
+    const float margin = fabsf(q) * 0x1p-21f + 0x1p-40f;
+    const int r = fabsf(fr - 0.5f) > margin ? int(fl) + (fr > 0.5f ? 1 : 0) : int(rint(double(xf) / s));
+    return min(max(r + zp, qmin), qmax);
+  }
+  const double qd = rint(double(xf) / s) + double(zp);
+  return int(fmin(fmax(qd, double(qmin)), double(qmax)));
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) int_quant_kernel(const T* __restrict__ x, int64_t M, int64_t K, int64_t ldx,
                                                         int bits, int symmetric, int8_t* __restrict__ codes,
@@ -640,26 +661,37 @@ __global__ void __launch_bounds__(256) int_quant_kernel(const T* __restrict__ x,
 // Fast path for bf16 rows with K % 8 == 0 and K <= 2048 * kNV: one CTA per row,
 // the row stays in registers between the reduction and the quantization pass
 // (one HBM read), 16-B loads and 8-B code stores.
-template <int kNV>
-__global__ void __launch_bounds__(256) int_quant_bf16_kernel(const __nv_bfloat16* __restrict__ x, int K, int64_t ldx,
-                                                             int bits, int symmetric, int8_t* __restrict__ codes,
-                                                             double* __restrict__ scale64, float* __restrict__ scale32,
-                                                             int32_t* __restrict__ zp_out,
+// bf16 rows, K <= 8192: kTpr threads per token row, 256 / kTpr rows per CTA, each
+// thread keeps its kCpt 16-B chunks in registers (one HBM read); row min / max by
+// shuffles + a per-row shared-memory step; scale / zero point in f64 by one thread
+// per row exactly as the reference (quantcore.py:108-137); codes through int_code.
+template <int kTpr, int kCpt>
+__global__ void __launch_bounds__(256) int_quant_bf16_kernel(const __nv_bfloat16* __restrict__ x, int M, int K,
+                                                             int64_t ldx, int bits, int symmetric,
+                                                             int8_t* __restrict__ codes, double* __restrict__ scale64,
+                                                             float* __restrict__ scale32, int32_t* __restrict__ zp_out,
                                                              const int32_t* __restrict__ sidx, int r,
                                                              void* __restrict__ xs_out, int xs_kind) {
-  const int64_t row = blockIdx.x;
-  const uint4* xr = reinterpret_cast<const uint4*>(x + row * ldx);
+  constexpr int kRows = 256 / kTpr, kWarps = kTpr / 32;
+  __shared__ float red_lo[kRows][kWarps], red_hi[kRows][kWarps];
+  __shared__ double s_scale[kRows];
+  __shared__ float s_inv32[kRows];
+  __shared__ int s_zp[kRows];
+  pdl_launch_dependents();
+  pdl_wait();
+  const int rl = threadIdx.x / kTpr, t = threadIdx.x % kTpr;
+  const int64_t row = int64_t(blockIdx.x) * kRows + rl;
+  const bool row_ok = row < M;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (row_ok ? row : 0) * ldx);
   const int n8 = K >> 3;
-  __shared__ float red_lo[8], red_hi[8];
-  __shared__ double s_scale;
-  __shared__ int s_zp;
-  uint4 raw[kNV];
+  uint4 raw[kCpt];
   float lo = INFINITY, hi = -INFINITY;
 #pragma unroll
-  for (int j = 0; j < kNV; ++j) {
-    const int c8 = threadIdx.x + j * 256;
-    raw[j] = c8 < n8 ? __ldg(xr + c8) : make_uint4(0, 0, 0, 0);
-    if (c8 < n8) {
+  for (int j = 0; j < kCpt; ++j) {
+    const int c8 = t + j * kTpr;
+    const bool ok = row_ok && c8 < n8;
+    raw[j] = ok ? __ldg(xr + c8) : make_uint4(0, 0, 0, 0);
+    if (ok) {
       const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -674,16 +706,16 @@ __global__ void __launch_bounds__(256) int_quant_bf16_kernel(const __nv_bfloat16
     lo = fminf(lo, __shfl_xor_sync(0xffffffff, lo, o));
     hi = fmaxf(hi, __shfl_xor_sync(0xffffffff, hi, o));
   }
-  if ((threadIdx.x & 31) == 0) {
-    red_lo[threadIdx.x >> 5] = lo;
-    red_hi[threadIdx.x >> 5] = hi;
+  if ((t & 31) == 0) {
+    red_lo[rl][t >> 5] = lo;
+    red_hi[rl][t >> 5] = hi;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (t == 0 && row_ok) {
 #pragma unroll
-    for (int w = 1; w < 8; ++w) {
-      lo = fminf(lo, red_lo[w]);
-      hi = fmaxf(hi, red_hi[w]);
+    for (int w = 1; w < kWarps; ++w) {
+      lo = fminf(lo, red_lo[rl][w]);
+      hi = fmaxf(hi, red_hi[rl][w]);
     }
     const double dlo = lo, dhi = hi;  // exact (bf16 values)
     double sc;
@@ -696,23 +728,24 @@ __global__ void __launch_bounds__(256) int_quant_bf16_kernel(const __nv_bfloat16
       if (sc == 0.0) sc = 1.0;
       zp = int(rint(-dlo / sc));
     }
-    s_scale = sc;
-    s_zp = zp;
+    s_scale[rl] = sc;
+    s_inv32[rl] = float(1.0 / sc);
+    s_zp[rl] = zp;
     scale64[row] = sc;
     scale32[row] = float(sc);
     if (zp_out) zp_out[row] = zp;
   }
   __syncthreads();
-  const double sc = s_scale;
-  const int zp = s_zp;
-  const double inv64 = 1.0 / sc;
-  const float inv32 = float(inv64);
+  if (!row_ok) return;
+  const double sc = s_scale[rl];
+  const int zp = s_zp[rl];
+  const float inv32 = s_inv32[rl];
   const int qmax = symmetric ? (1 << (bits - 1)) - 1 : (1 << bits) - 1;
   const int qmin = symmetric ? -qmax : 0;
   uint2* out = reinterpret_cast<uint2*>(codes + row * K);
 #pragma unroll
-  for (int j = 0; j < kNV; ++j) {
-    const int c8 = threadIdx.x + j * 256;
+  for (int j = 0; j < kCpt; ++j) {
+    const int c8 = t + j * kTpr;
     if (c8 >= n8) continue;
     const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
     uint32_t packed[2] = {0u, 0u};
@@ -720,15 +753,15 @@ __global__ void __launch_bounds__(256) int_quant_bf16_kernel(const __nv_bfloat16
     for (int i = 0; i < 8; ++i) {
       const uint32_t hbits = (i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16);
       const __nv_bfloat16 xv = __ushort_as_bfloat16(static_cast<unsigned short>(hbits >> 16));
-      const double qd = rint_quot<__nv_bfloat16>(xv, sc, inv32, inv64) + double(zp);
-      const int q = int(fmin(fmax(qd, double(qmin)), double(qmax)));
+      const int q = int_code<__nv_bfloat16>(xv, sc, inv32, zp, qmin, qmax);
       packed[i >> 2] |= (uint32_t(q) & 0xFFu) << (8 * (i & 3));
     }
     out[c8] = make_uint2(packed[0], packed[1]);
   }
   if (xs_kind != 0) {
-    __syncthreads();
-    for (int j = threadIdx.x; j < r; j += blockDim.x) {
+    // salient slice from this row's codes (written above by this row's threads)
+    named_bar_sync(1 + rl, kTpr);
+    for (int j = t; j < r; j += kTpr) {
       const int col = sidx ? sidx[j] : j;
       const int c = symmetric ? int(codes[row * K + col]) : int(uint8_t(codes[row * K + col]));
       if (xs_kind == 1)
