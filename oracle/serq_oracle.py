@@ -438,6 +438,44 @@ def rmsnorm(x, gain, eps: float = 1e-6) -> np.ndarray:
     return x / rms * np.asarray(gain, dtype=np.float64)[None, :]
 
 
+def silu(x) -> np.ndarray:
+    """saliency.py:199-200."""
+    return x / (1.0 + np.exp(-x))
+
+
+def attention_mix(q, k, v, head_dim: int) -> np.ndarray:
+    """saliency.py:203-216: per-head softmax(Q K^T / sqrt(d)) V over the token batch."""
+    out = np.empty_like(v)
+    for h in range(q.shape[1] // head_dim):
+        sl = slice(h * head_dim, (h + 1) * head_dim)
+        logits = q[:, sl] @ k[:, sl].T / np.sqrt(head_dim)
+        logits -= logits.max(axis=1, keepdims=True)
+        a = np.exp(logits)
+        a /= a.sum(axis=1, keepdims=True)
+        out[:, sl] = a @ v[:, sl]
+    return out
+
+
+def forward_block_mx(x, linears: dict, gains: dict, head_dim: int, bf16_linear_out: bool = False) -> np.ndarray:
+    """toymodel.forward_quantized (toymodel.py:363-374) on toy_block_graph (toymodel.py:88-124):
+    graph_forward's node order with every linear through forward_mx.  ``linears``:
+    name -> (main_t, comp).  ``bf16_linear_out`` rounds every linear's output to bf16 --
+    the device linears' output contract -- before it feeds the next node."""
+    x = np.asarray(x, dtype=np.float64)
+
+    def lin(name, xin):
+        main_t, comp = linears[name]
+        y = forward_mx(xin, main_t, comp)
+        return bf16_round(y) if bf16_linear_out else y
+
+    h1 = rmsnorm(x, gains["ln1"])
+    attn = attention_mix(lin("q_proj", h1), lin("k_proj", h1), lin("v_proj", h1), head_dim)
+    res1 = x + lin("o_proj", attn)
+    h2 = rmsnorm(res1, gains["ln2"])
+    mid = silu(lin("gate_proj", h2)) * lin("up_proj", h2)
+    return res1 + lin("down_proj", mid)
+
+
 def bf16_round(x) -> np.ndarray:
     """Round float64 to the nearest bfloat16 (ties to even), returned as f64.
 

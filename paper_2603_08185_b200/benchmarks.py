@@ -282,6 +282,41 @@ def rmsnorm_quant_point(M: int, K: int, hbm_peak_gbs: float, n_steps: int = 16) 
             "unfused_extra_bytes": 4 * M * K}
 
 
+def llama7b_block_point(M: int, n_blocks: int = 4, r: int = 64) -> dict:
+    """Whole Llama-2-7B-shaped decoder block on the device (block.DeviceBlock: SERQ MXFP4
+    linears + f32 RMSNorm / attention / SiLU), ``n_blocks`` distinct blocks chained in ONE
+    CUDA graph (~400 MB of weights > L2, so every block streams its weights).  q/k/v and
+    gate/up use the gather fallback (their inputs come from the residual
+    stream), o/down the permuted layout; the (non-SERQ) token-batch attention runs as bf16
+    flash attention.  Tokens/s = M / per-block time."""
+    from .block import DeviceBlock
+
+    H, F, hd = 4096, 11008, 128
+    rng = np.random.default_rng(9)
+    blocks = []
+    for b in range(n_blocks):
+        def lin(k, n, gather, s):
+            idx = np.sort(rng.permutation(k)[:r]) if gather else None
+            return device_mx_linear(k, n, r, seed=100 * b + s, salient_idx=idx)
+        lins = {"q_proj": lin(H, H, True, 1), "k_proj": lin(H, H, True, 2), "v_proj": lin(H, H, True, 3),
+                "o_proj": lin(H, H, False, 4), "up_proj": lin(H, F, True, 5), "gate_proj": lin(H, F, True, 6),
+                "down_proj": lin(F, H, False, 7)}
+        gains = {"ln1": np.abs(rng.standard_normal(H)) + 0.5, "ln2": np.abs(rng.standard_normal(H)) + 0.5}
+        blocks.append(DeviceBlock(lins, gains, hd, fast_attention=True))
+    x = outlier_x(M, H).float()
+
+    def step():
+        h = x
+        for blk in blocks:
+            h = blk(h)
+        return h
+
+    t = time_in_graph(step, None, n=10) / n_blocks
+    flops = 2.0 * M * (4 * H * (H + r) + 2 * H * (F + r) + F * (H + r))
+    return {"M": M, "hidden": H, "ffn": F, "r": r, "blocks_in_graph": n_blocks, "block_us": t * 1e3,
+            "tokens_per_s": M / (t * 1e-3), "linear_tflops_equiv": flops / (t * 1e-3) / 1e12}
+
+
 def c5_block_point(world: int = 1, rank: int = 0, M: int = 8192, r: int = 128, group=None, steps: int = 5,
                    flush: Flusher | None = None) -> dict:
     """BASELINE C5: Llama-3-70B-shaped decoder-block linears (hidden 8192,

@@ -372,7 +372,7 @@ int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K
     if (!rc) rc = make_map(&h->map_r128, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r / 2, N, r / 2, 128, 128);
     if (!rc) rc = make_sf_map(&h->map_sfr, h->sfr, N, r);
     if (rc) return bail(rc);
-    if (r == 64 && salient_contiguous) {
+    if (r == 64) {  // 32-B R rows: the pair3 kernel (contiguous) and the decode kernel (both layouts)
       rc = make_map(&h->map_r32, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r / 2, N, r / 2, 32, 128,
                     CU_TENSOR_MAP_SWIZZLE_32B);
       if (!rc)
@@ -555,7 +555,8 @@ int serq_linear_info(const serq_linear_t* h, int64_t* N, int64_t* K, int* r, int
 // the quantized activation.
 static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const uint8_t* a_sf,
                             const __nv_bfloat16* x, int64_t ldx, uint8_t* codes_out, uint8_t* sf_out, int64_t M,
-                            void* y, int64_t ldy, cudaStream_t st) {
+                            void* y, int64_t ldy, cudaStream_t st, const uint8_t* xs_codes = nullptr,
+                            const uint8_t* xs_sf = nullptr) {
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClSmem));
@@ -592,6 +593,18 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
   dm.sfw = h->map_sfw;
   dm.r = h->has_r32 ? h->map_r32 : h->map_b128;
   dm.sfr = h->has_r32 ? h->map_sfr4 : h->map_sfw;
+  const bool gather = h->r > 0 && !h->contiguous;
+  if (gather && (fuse || !xs_codes || !xs_sf)) return fail(SERQ_EINVAL, "gather decode needs the xs slice");
+  cp.gather = gather ? 1 : 0;
+  dm.xs = dm.sfxs = h->map_b128;  // unused unless gather
+  if (gather) {
+    int rc = make_map(&dm.xs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_codes, h->r / 2, M, h->r / 2, 32, kDecN,
+                      CU_TENSOR_MAP_SWIZZLE_32B);
+    if (!rc)
+      rc = make_map(&dm.sfxs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_sf, 128, uint64_t(sf_bytes_of(M, h->r) / 128), 128, 128,
+                    4, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc) return rc;
+  }
   if (fuse) {
     dm.x = dm.sfx = h->map_b128;  // unused: X is produced in-kernel
   } else {
@@ -666,8 +679,8 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
   p.dbg = g_debug_flags;
   p.dbg_ts = g_debug_ts;
   if (M <= kDecN && (h->r == 0 || h->has_r32) && !(g_debug_flags & 2048))
-    return launch_decode_cl(h, a_codes, a_sf, nullptr, 0, nullptr, nullptr, M, y, ldy, S(stream));
-  if (M > 128 && (h->r == 0 || h->has_r32) && !(g_debug_flags & (16 | 512))) {
+    return launch_decode_cl(h, a_codes, a_sf, nullptr, 0, nullptr, nullptr, M, y, ldy, S(stream), xs_codes, xs_sf);
+  if (M > 128 && (h->r == 0 || (h->has_r32 && h->contiguous)) && !(g_debug_flags & (16 | 512))) {
     static bool attr3 = false;
     if (!attr3) {
       CK(cudaFuncSetAttribute(serq_mx_pair3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k3SmemBytes));

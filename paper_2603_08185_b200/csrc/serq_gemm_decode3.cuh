@@ -43,11 +43,13 @@ static_assert(kDecStage % 1024 == 0, "stage alignment");
 
 struct DecodeMaps {
   CUtensorMap w, x, sfw, sfx, r, sfr;
+  CUtensorMap xs, sfxs;  // gather fallback: the quantizer's x[:, idx] codes (32-B rows) and scale factors
 };
 
 constexpr int kClStages = 5;
 constexpr int kClThreads = 192;
-constexpr int kClSmem = 1024 + kClStages * kDecStage + kDecRB + 512 + 512;
+constexpr int kClXs = 512 + 512;  // gather fallback: 16 rows x 32 B of x[:, idx] codes + one SF atom
+constexpr int kClSmem = 1024 + kClStages * kDecStage + kDecRB + 512 + kClXs + 512;
 static_assert(kClSmem <= 116 * 1024, "two CTAs (this linear and the next) must fit on one SM");
 static_assert(7 * 128 * kDecN * 4 <= kClStages * kDecStage, "rank-0 reduction buffer reuses the stages");
 
@@ -55,6 +57,7 @@ struct ClParams {
   int M, N, K, r;
   int k_steps, S;        // K steps per tile, CTAs per tile (cluster size)
   int kc_pad, kc_pad_r, w_ksteps;
+  int gather;            // the salient term's B operand is the quantizer's x[:, idx] slice, not K-tile 0 of X
   __nv_bfloat16* y;
   int64_t ldy;
   // fused quantizer: bf16 activations (row pitch ldx); the tile-0 cluster also
@@ -79,14 +82,16 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* rbuf = smem + kClStages * kDecStage;  // R tile (4 KB) + R scale factors (512 B)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rbuf + kDecRB + 512);
+  uint8_t* xsbuf = rbuf + kDecRB + 512;           // gather: x[:, idx] codes (512 B) + SF atom (512 B)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xsbuf + kClXs);
   uint64_t* full = bars;                  // [kClStages]
   uint64_t* empty = bars + kClStages;     // [kClStages]
   uint64_t* rfull = bars + 2 * kClStages;
   uint64_t* done = rfull + 1;             // accumulator complete
   uint64_t* red_free = done + 1;          // rank > 0: rank 0's buffer may be written
   uint64_t* red_full = red_free + 1;      // rank 0: every partial has landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_full + 1);
+  uint64_t* xsfull = red_full + 1;        // gather: the salient slice landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xsfull + 1);
 
   pdl_launch_dependents();  // the next linear may launch once every CTA is resident
   const uint32_t warp = threadIdx.x >> 5;
@@ -114,6 +119,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
     mbar_init(done, 1);
     mbar_init(red_free, 1);
     mbar_init(red_full, S > 1 ? (S - 1) * 128 : 1);
+    mbar_init(xsfull, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<64>(tmem_slot);
@@ -128,7 +134,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
   tc_fence_before();
   cluster_sync_all();  // barrier inits visible cluster-wide before any remote arrive
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // [0,16) accumulator, [16,24) SFA, [24,32) SFB, [32,36) R SFA
+  const uint32_t tmem = *tmem_slot;  // [0,16) accumulator, [16,24) SFA, [24,32) SFB, [32,36) R SFA, [36,40) xs SFB
 
   if (warp == 0) {
     if (elect_one()) {
@@ -146,6 +152,11 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
       const int pre = min(nsteps, kClStages);
       for (int i = 0; i < pre; ++i) load_w(i, k0 + i);
       if (!kFuse) pdl_wait();  // activation codes come from the quantizer kernel
+      if (!kFuse && with_r && p.gather) {
+        mbar_expect_tx(xsfull, kClXs);
+        tma_load_2d(xsbuf, &maps.xs, xsfull, 0, 0, kEvictLast);
+        tma_load_2d(xsbuf + 512, &maps.sfxs, xsfull, 0, 0, kEvictLast);
+      }
       for (int i = 0; i < nsteps; ++i) {
         const int s = i % kClStages;
         if (i >= pre) {
@@ -163,7 +174,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
   } else if (warp == 1) {
     if (elect_one()) {
       constexpr uint32_t id0 = idesc_mxf4(128, kDecN), id1 = id0 | (2u << 4) | (2u << 29);
-      const uint32_t acc = tmem, sfa = tmem + 16, sfb = tmem + 24, sfr = tmem + 32;
+      const uint32_t acc = tmem, sfa = tmem + 16, sfb = tmem + 24, sfr = tmem + 32, sfxs = tmem + 36;
       for (int i = 0; i < nsteps; ++i) {
         const int s = i % kClStages;
         mbar_wait(&full[s], (i / kClStages) & 1);
@@ -184,7 +195,16 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
           mbar_wait(rfull, 0);
           tc_fence_after();
           tmem_cp_32x128b_x4(sfr, make_sdesc(smem_u32(rbuf + kDecRB), 128, 128, 0));
-          mma_mxf4(acc, make_sdesc(smem_u32(rbuf), 16, 256, 6), b, id0, sfr, sfb, 1u);
+          if (!kFuse && p.gather) {
+            // gather fallback: B = the quantizer's x[:, idx] slice (16 rows x 32 B, 32B swizzle)
+            mbar_wait(xsfull, 0);
+            tc_fence_after();
+            tmem_cp_32x128b_x4(sfxs, make_sdesc(smem_u32(xsbuf + 512), 128, 128, 0));
+            mma_mxf4(acc, make_sdesc(smem_u32(rbuf), 16, 256, 6), make_sdesc(smem_u32(xsbuf), 16, 256, 6), id0, sfr,
+                     sfxs, 1u);
+          } else {
+            mma_mxf4(acc, make_sdesc(smem_u32(rbuf), 16, 256, 6), b, id0, sfr, sfb, 1u);
+          }
         }
         tc_commit(&empty[s]);
       }

@@ -233,6 +233,23 @@ def main():
     g["rms_x"], g["rms_gain"], g["rms_y"] = xr, gr, rmsnorm(xr, gr)
     g["rms_codes"] = mx_encode(g["rms_y"], 32).element_codes
 
+    # -- a whole toy decoder block (toymodel.py:88-124), MXFP4 SERQ via the reference's own
+    #    quantize_block + save_bundle; forward_quantized (graph_forward + forward_reconstructed)
+    #    is the golden block output for the device block forward
+    from serq.toymodel import forward_fp, forward_quantized, quantize_block, random_block
+
+    blk = random_block(256, 512, head_dim=64, seed=51)
+    calib = gen_synthetic_activations(SyntheticSpec(rows=64, cols=256, n_outlier_channels=3,
+                                                    outlier_magnitude=20, seed=52))
+    qb = quantize_block(blk, calib, rank=32, fmt="mxfp4")
+    save_bundle(os.path.join(os.path.dirname(OUT), "block_mx"), qb)
+    xbk = bf16(gen_synthetic_activations(SyntheticSpec(rows=48, cols=256, n_outlier_channels=3,
+                                                       outlier_magnitude=20, seed=53)))
+    g["block_x"] = xbk
+    g["block_y_quant"] = forward_quantized(blk, xbk, qb)
+    g["block_y_fp"] = forward_fp(blk, xbk)
+    g["block_head_dim"] = np.array(64)
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)/1e6:.2f} MB, {len(g)} arrays)")
 

@@ -424,3 +424,23 @@ def test_tp_shards_on_device_match_single_device(D, world):
     # each rank's partial is rounded to bf16 before the reduction (world extra roundings of
     # magnitude ~|Y| / sqrt(world)): the mean tolerance scales with the number of partials
     assert mx <= TOL_MAX and mean <= TOL_MEAN * world, (mx, mean)
+
+
+@pytest.mark.parametrize("M,K,N", [(1, 1024, 768), (5, 4096, 1024), (16, 2048, 11008 // 128 * 128)])
+def test_mx_decode_gather_parity(D, M, K, N):
+    # decode (M <= 16) with an arbitrary salient set (SURVEY F8's common case): the salient
+    # term's B operand is the quantizer's x[:, idx] slice loaded next to R
+    r = 64
+    rng = np.random.default_rng(M + K)
+    x = _bf16_outlier_x(M, K, seed=M + 3)
+    w = rng.standard_normal((K, N)) * 0.02
+    idx = np.sort(rng.permutation(K)[:r])
+    w[idx] *= 8
+    main_t, comp = O.build_serq_rtn_mx(w, idx, 32)
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                     comp.r_q.block_scale_exponents, idx)
+    assert not lin.contiguous
+    for _ in range(2):
+        y = lin(_cuda(x, torch.bfloat16)).float().cpu().numpy()
+        mx, mean = O.parity_errors(y, O.forward_mx(x, main_t, comp))
+        assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
