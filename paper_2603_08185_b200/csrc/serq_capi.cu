@@ -584,6 +584,7 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
   cp.w_ksteps = h->w_ksteps;
   cp.y = static_cast<__nv_bfloat16*>(y);
   cp.ldy = ldy;
+  cp.dbg_ts = g_debug_ts;
   cp.x = x;
   cp.ldx = ldx;
   cp.codes_out = codes_out;

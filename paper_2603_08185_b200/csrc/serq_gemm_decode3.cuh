@@ -60,6 +60,7 @@ struct ClParams {
   int gather;            // the salient term's B operand is the quantizer's x[:, idx] slice, not K-tile 0 of X
   __nv_bfloat16* y;
   int64_t ldy;
+  long long* dbg_ts;     // diagnostics (SERQ_DIAG_TS builds): [cta][8] globaltimer stamps
   // fused quantizer: bf16 activations (row pitch ldx); the tile-0 cluster also
   // writes the quantized activation (codes [M, K/2], scale factors tiled) if non-null
   const __nv_bfloat16* x;
@@ -67,6 +68,17 @@ struct ClParams {
   uint8_t* codes_out;
   uint8_t* sf_out;
 };
+
+#ifdef SERQ_DIAG_TS
+#define CL_STAMP(i)                                                                      \
+  if (p.dbg_ts) {                                                                        \
+    uint64_t g_;                                                                         \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                              \
+    p.dbg_ts[blockIdx.x * 8 + (i)] = (long long)g_;                                      \
+  }
+#else
+#define CL_STAMP(i)
+#endif
 
 __device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
@@ -95,6 +107,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
 
   pdl_launch_dependents();  // the next linear may launch once every CTA is resident
   const uint32_t warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) CL_STAMP(0);
   const int S = p.S;
   const int rank = int(cluster_rank());
   const int tile = int(blockIdx.x) / S;
@@ -152,6 +165,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
       const int pre = min(nsteps, kClStages);
       for (int i = 0; i < pre; ++i) load_w(i, k0 + i);
       if (!kFuse) pdl_wait();  // activation codes come from the quantizer kernel
+      CL_STAMP(1);
       if (!kFuse && with_r && p.gather) {
         mbar_expect_tx(xsfull, kClXs);
         tma_load_2d(xsbuf, &maps.xs, xsfull, 0, 0, kEvictLast);
@@ -179,6 +193,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
         const int s = i % kClStages;
         mbar_wait(&full[s], (i / kClStages) & 1);
         tc_fence_after();
+        if (i == 0) CL_STAMP(2);
         const uint32_t st = smem_u32(smem + s * kDecStage);
         const uint64_t a = make_sdesc(st, 16, 1024, 2), b = make_sdesc(st + kDecW, 16, 1024, 2);
         const uint32_t sa = st + kDecW + kDecX, sb = sa + kDecSF;
@@ -208,6 +223,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
         }
         tc_commit(&empty[s]);
       }
+      CL_STAMP(3);
       if (nsteps > 0) tc_commit(done);
       else mbar_arrive(done);
     }
@@ -217,6 +233,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
     const uint32_t q = warp & 3;  // TMEM lane quadrant
     const int et = int(q * 32 + lane_id());
     pdl_wait();  // X (fused) / Y writes after the previous kernel
+    if (kFuse && q == 0 && lane_id() == 0) CL_STAMP(1);
     if constexpr (kFuse) {
       // X producer: thread -> (token row m, 32-block part) of each K step
       const int m = et >> 3, part = et & 7;
@@ -290,6 +307,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
     // ---- accumulator -> Y (S == 1) or the rank-0 DSMEM reduction
     mbar_wait(done, 0);
     tc_fence_after();
+    if (q == 0 && lane_id() == 0) CL_STAMP(4);
     uint32_t v[16];
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -339,12 +357,14 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
         if (m < p.M) p.y[m * p.ldy + n] = __float2bfloat16_rn(out[m]);
     }
   }
+  if (warp == 4 && lane_id() == 0) CL_STAMP(5);
   tc_fence_before();
   cluster_sync_all();  // no CTA leaves while a peer may still touch its shared memory
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<64>(tmem);
   }
+  if (threadIdx.x == 0) CL_STAMP(6);
 }
 
 }  // namespace serq
