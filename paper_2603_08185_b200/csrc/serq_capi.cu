@@ -559,8 +559,10 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
                             const uint8_t* xs_sf = nullptr) {
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClSmem));
-    CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClSmem));
+    CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            ClCfg<false>::kSmem));
+    CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            ClCfg<true>::kSmem));
     attr = true;
   }
   const bool fuse = x != nullptr;
@@ -597,6 +599,7 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
   const bool gather = h->r > 0 && !h->contiguous;
   if (gather && (fuse || !xs_codes || !xs_sf)) return fail(SERQ_EINVAL, "gather decode needs the xs slice");
   cp.gather = gather ? 1 : 0;
+  cp.red_narrow = (S - 1) * ((M + 3) / 4) * 128 * 16 <= kClRed && !(g_debug_flags & (1 << 29)) ? 1 : 0;
   dm.xs = dm.sfxs = h->map_b128;  // unused unless gather
   if (gather) {
     int rc = make_map(&dm.xs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_codes, h->r / 2, M, h->r / 2, 32, kDecN,
@@ -607,7 +610,8 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
     if (rc) return rc;
   }
   if (fuse) {
-    dm.x = dm.sfx = h->map_b128;  // unused: X is produced in-kernel
+    dm.x = h->map_b128;  // unused: X is converted in-kernel
+    dm.sfx = h->map_b128;  // unused
   } else {
     int rc = make_map(&dm.x, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, kDecN);
     if (!rc) rc = make_sf_map(&dm.sfx, a_sf, M, h->K);
@@ -616,7 +620,7 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(tiles * S));
   cfg.blockDim = dim3(kClThreads);
-  cfg.dynamicSmemBytes = kClSmem;
+  cfg.dynamicSmemBytes = fuse ? ClCfg<true>::kSmem : ClCfg<false>::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -798,12 +802,12 @@ int serq_forward_mx(serq_linear_t* h, const void* x, int dtype, int64_t M, int64
   const bool gather = h->r > 0 && !h->contiguous;
   if (gather && (!gather_idx || !xs_codes || !xs_sf))
     return fail(SERQ_EINVAL, "non-contiguous salient set needs gather_idx and the xs buffers");
-  if (M <= kDecN && (h->r == 0 || h->has_r32) && dtype == SERQ_BF16 && !gather &&
-      !(reinterpret_cast<uintptr_t>(x) & 15) && ldx % 8 == 0 && ldx >= h->K && (g_debug_flags & (1 << 23)) &&
+  if (M <= kClFuseM && (h->r == 0 || h->has_r32) && dtype == SERQ_BF16 && !gather &&
+      !(reinterpret_cast<uintptr_t>(x) & 15) && ldx % 8 == 0 && ldx >= h->K && !(g_debug_flags & (1 << 23)) &&
       !(g_debug_flags & 2048)) {
-    // decode with the quantizer inside the linear (opt-in, debug flag 1<<23): measured
-    // slower than quantizer kernel + PDL-chained linear for Llama-2-7B up_proj (9.2 vs
-    // 8.3 us/layer at M=1) -- 86 x S CTAs re-read the same bf16 rows (tools/decode_probe.py)
+    // decode (M <= 4) with the quantizer inside the linear: one kernel per layer instead of
+    // quantizer + PDL-chained linear (Llama-2-7B M=1: up_proj 7.8 vs 8.2 us/layer, down_proj
+    // 8.1 vs 9.1; tools/decode_probe.py); debug flag 1<<23 selects the two-kernel path
     g_launches = 0;
     if (ldy < h->N || ldy % 8) return fail(SERQ_EINVAL, "ldy must be >= N and a multiple of 8");
     return launch_decode_cl(h, nullptr, nullptr, static_cast<const __nv_bfloat16*>(x), ldx, codes, sf, M, y, ldy,

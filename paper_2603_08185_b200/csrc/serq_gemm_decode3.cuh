@@ -13,16 +13,17 @@
 // no float atomics.  (A global-memory reduction costs ~3 L2 round trips on the
 // critical path of every layer, ~3 us measured; DSMEM ~0.2 us.)
 //
-// Fused quantizer (kFuse): the epilogue warps, idle during the main loop,
-// read the bf16 activations of each K step (16 rows x 256 columns, L2
-// resident), encode them exactly like mx_encode (mxfmt.py:97-108: block
+// Fused quantizer (kFuse, M <= 4): the epilogue warps, idle during the main
+// loop, take the K steps round-robin (warp c: steps c, c+4, ...; three of its
+// steps' bf16 activations in flight in registers, L2 resident), encode them
+// exactly like mx_encode (mxfmt.py:97-108: block
 // exponent from the 32-block amax, RNE-to-E2M1 with saturation, -0 -> +0) and
 // write the codes (128B-swizzled, the layout a TMA box would produce) and the
 // E8M0 scale factors straight into the pipeline stage next to the TMA-loaded
 // weights.  This removes the separate quantizer kernel and its two
 // kernel-boundary dependencies from every decode step.
 //
-// Sized for layer-to-layer overlap: ~107 KB of shared memory and 64 TMEM
+// Sized for layer-to-layer overlap: <= 116 KB of shared memory and 64 TMEM
 // columns per CTA, so the NEXT linear's CTA fits on the same SM; with
 // programmatic dependent launch (trigger at CTA start) it streams its first
 // weight stages while this one finishes.
@@ -46,18 +47,25 @@ struct DecodeMaps {
   CUtensorMap xs, sfxs;  // gather fallback: the quantizer's x[:, idx] codes (32-B rows) and scale factors
 };
 
-constexpr int kClStages = 5;
 constexpr int kClThreads = 192;
-constexpr int kClXs = 512 + 512;  // gather fallback: 16 rows x 32 B of x[:, idx] codes + one SF atom
-constexpr int kClSmem = 1024 + kClStages * kDecStage + kDecRB + 512 + kClXs + 512;
-static_assert(kClSmem <= 116 * 1024, "two CTAs (this linear and the next) must fit on one SM");
-static_assert(7 * 128 * kDecN * 4 <= kClStages * kDecStage, "rank-0 reduction buffer reuses the stages");
+constexpr int kClXs = 512 + 512;     // gather fallback: 16 rows x 32 B of x[:, idx] codes + one SF atom
+constexpr int kClRed = 6 * 1024;     // rank-0 landing buffer for narrow partials ((S-1) x ceil(M/4) x 2 KB)
+constexpr int kClFuseM = 4;          // fused quantizer: one (token row, 32-block) per lane of a converter warp
+template <bool kFuse>
+struct ClCfg {
+  static constexpr int kStages = 5;
+  static constexpr int kSmem = 1024 + kStages * kDecStage + kDecRB + 512 + kClXs + kClRed + 512;
+  // 228 KB per SM, 1 KB reserved per CTA
+  static_assert(2 * (kSmem + 1024) <= 228 * 1024, "two CTAs (this linear and the next) must fit on one SM");
+  static_assert(7 * 128 * kDecN * 4 <= kStages * kDecStage, "rank-0 reduction buffer reuses the stages");
+};
 
 struct ClParams {
   int M, N, K, r;
   int k_steps, S;        // K steps per tile, CTAs per tile (cluster size)
   int kc_pad, kc_pad_r, w_ksteps;
   int gather;            // the salient term's B operand is the quantizer's x[:, idx] slice, not K-tile 0 of X
+  int red_narrow;        // partials carry only the M token columns and land in a dedicated buffer
   __nv_bfloat16* y;
   int64_t ldy;
   long long* dbg_ts;     // diagnostics (SERQ_DIAG_TS builds): [cta][8] globaltimer stamps
@@ -76,8 +84,12 @@ struct ClParams {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                              \
     p.dbg_ts[blockIdx.x * 8 + (i)] = (long long)g_;                                      \
   }
+// per-step SM-clock stamps of CTA 0: [8192 + 64 * kind + step]
+#define CL_STEP(kind, i)                                                                 \
+  if (p.dbg_ts && blockIdx.x == 0 && (i) < 64) p.dbg_ts[8192 + 64 * (kind) + (i)] = clock64();
 #else
 #define CL_STAMP(i)
+#define CL_STEP(kind, i)
 #endif
 
 __device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
@@ -91,11 +103,13 @@ __device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t bar_cluster
 template <bool kFuse>
 __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const __grid_constant__ DecodeMaps maps,
                                                                           const ClParams p) {
+  constexpr int kClStages = ClCfg<kFuse>::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* rbuf = smem + kClStages * kDecStage;  // R tile (4 KB) + R scale factors (512 B)
   uint8_t* xsbuf = rbuf + kDecRB + 512;           // gather: x[:, idx] codes (512 B) + SF atom (512 B)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xsbuf + kClXs);
+  float* redbuf = reinterpret_cast<float*>(xsbuf + kClXs);  // narrow reduction: [S-1][ceil(M/4)][128][4]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xsbuf + kClXs + kClRed);
   uint64_t* full = bars;                  // [kClStages]
   uint64_t* empty = bars + kClStages;     // [kClStages]
   uint64_t* rfull = bars + 2 * kClStages;
@@ -125,7 +139,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
       tma_prefetch(&maps.sfx);
     }
     for (int s = 0; s < kClStages; ++s) {
-      mbar_init(&full[s], kFuse ? 1 + 4 : 1);  // + one arrival per X-producing warp
+      mbar_init(&full[s], kFuse ? 2 : 1);  // + the converter warp of the step
       mbar_init(&empty[s], 1);
     }
     mbar_init(rfull, 1);
@@ -137,15 +151,20 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
   }
   if (warp == 1) tmem_alloc<64>(tmem_slot);
   if (kFuse) {
-    // X scale-factor atoms: rows 16..127 of each 512-B atom are never produced; give them a finite scale
-    for (int s = 0; s < kClStages; ++s)
+    // X rows >= kClFuseM of every stage stay zero, and scale-factor atom rows >= kClFuseM (never
+    // produced) get a finite scale; the converters rewrite rows < kClFuseM every step
+    for (int s = 0; s < kClStages; ++s) {
+      for (int b = threadIdx.x; b < (kDecX - kClFuseM * 128) / 16; b += blockDim.x)
+        reinterpret_cast<uint4*>(smem + s * kDecStage + kDecW + kClFuseM * 128)[b] = make_uint4(0, 0, 0, 0);
       for (int b = threadIdx.x; b < 2 * 512 / 16; b += blockDim.x)
         reinterpret_cast<uint4*>(smem + s * kDecStage + kDecW + kDecX + kDecSF)[b] = make_uint4(
             0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
+    }
     fence_proxy_async_smem();
   }
   tc_fence_before();
-  cluster_sync_all();  // barrier inits visible cluster-wide before any remote arrive
+  if (S > 1) cluster_sync_all();  // barrier inits visible cluster-wide before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;  // [0,16) accumulator, [16,24) SFA, [24,32) SFB, [32,36) R SFA, [36,40) xs SFB
 
@@ -164,7 +183,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
       }
       const int pre = min(nsteps, kClStages);
       for (int i = 0; i < pre; ++i) load_w(i, k0 + i);
-      if (!kFuse) pdl_wait();  // activation codes come from the quantizer kernel
+      pdl_wait();  // activations (bf16 or codes) come from the previous kernel
       CL_STAMP(1);
       if (!kFuse && with_r && p.gather) {
         mbar_expect_tx(xsfull, kClXs);
@@ -177,6 +196,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
           mbar_wait(&empty[s], ((i / kClStages) & 1) ^ 1);
           load_w(s, k0 + i);
         }
+        CL_STEP(0, i);
         if (!kFuse) {
           uint8_t* st = smem + s * kDecStage;
           tma_load_2d(st + kDecW, &maps.x, &full[s], (k0 + i) * kStepBytes, 0, kEvictLast);
@@ -193,6 +213,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
         const int s = i % kClStages;
         mbar_wait(&full[s], (i / kClStages) & 1);
         tc_fence_after();
+        CL_STEP(2, i);
         if (i == 0) CL_STAMP(2);
         const uint32_t st = smem_u32(smem + s * kDecStage);
         const uint64_t a = make_sdesc(st, 16, 1024, 2), b = make_sdesc(st + kDecW, 16, 1024, 2);
@@ -232,15 +253,18 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
     // ------------------------------------------------ warps 2..5
     const uint32_t q = warp & 3;  // TMEM lane quadrant
     const int et = int(q * 32 + lane_id());
-    pdl_wait();  // X (fused) / Y writes after the previous kernel
-    if (kFuse && q == 0 && lane_id() == 0) CL_STAMP(1);
+    pdl_wait();  // codes_out / Y writes after the previous kernel
     if constexpr (kFuse) {
-      // X producer: thread -> (token row m, 32-block part) of each K step
-      const int m = et >> 3, part = et & 7;
+      // X converter: warp c converts K steps c, c + 4, ... (four steps in flight, so the
+      // per-step latency -- L2 load, encode, shared store, proxy fence -- is hidden);
+      // lane -> (token row m = lane / 8, 32-block part = lane % 8) of the 16 x 256 tile
+      const int cw = int(warp) - 2;
+      const int m = int(lane_id()) >> 3, part = int(lane_id()) & 7;
       const bool row_ok = m < p.M;
       const bool write_out = p.codes_out != nullptr && tile == 0 && row_ok;
-      auto load_x = [&](int kk, uint4 (&v)[4]) {
-        const bool ok = row_ok && kk * 256 + part * 32 < p.K;  // K % 32 == 0: blocks are all in or all out
+      auto load_x = [&](int i, uint4 (&v)[4]) {
+        const int kk = k0 + i;
+        const bool ok = i < nsteps && row_ok && kk * 256 + part * 32 < p.K;  // K % 32 == 0
         const uint4* src = reinterpret_cast<const uint4*>(p.x + int64_t(m) * p.ldx + kk * 256 + part * 32);
 #pragma unroll
         for (int c = 0; c < 4; ++c) v[c] = ok ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
@@ -276,6 +300,7 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
           pk[k] = canon_neg_zero(packed);
         }
         if (i >= kClStages) mbar_wait(&empty[s], ((i / kClStages) & 1) ^ 1);
+        if (i == 0 && lane_id() == 0) CL_STEP(4, 0);
         uint8_t* st = smem + s * kDecStage;
         // codes: row m, 16-B chunk `part` of the 128-B row, 128B swizzle (chunk ^ row % 8)
         st_shared_v4(smem_u32(st + kDecW + m * 128 + ((part ^ (m & 7)) * 16)), pk[0], pk[1], pk[2], pk[3]);
@@ -289,19 +314,20 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
         fence_proxy_async_smem();  // generic-proxy smem writes -> the tensor core's async proxy
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(&full[s]);
+        if (lane_id() == 0) CL_STEP(5, i);
       };
-      // three K steps of activations in flight (L2 latency), converted in order
+      // this warp's next three steps in registers
       uint4 b0[4], b1[4], b2[4];
-      if (nsteps > 0) load_x(k0, b0);
-      if (nsteps > 1) load_x(k0 + 1, b1);
-      if (nsteps > 2) load_x(k0 + 2, b2);
-      for (int i = 0; i < nsteps; i += 3) {
+      load_x(cw, b0);
+      load_x(cw + 4, b1);
+      load_x(cw + 8, b2);
+      for (int i = cw; i < nsteps; i += 12) {
         put_x(i, b0);
-        if (i + 3 < nsteps) load_x(k0 + i + 3, b0);
-        if (i + 1 < nsteps) put_x(i + 1, b1);
-        if (i + 4 < nsteps) load_x(k0 + i + 4, b1);
-        if (i + 2 < nsteps) put_x(i + 2, b2);
-        if (i + 5 < nsteps) load_x(k0 + i + 5, b2);
+        load_x(i + 12, b0);
+        if (i + 4 < nsteps) put_x(i + 4, b1);
+        load_x(i + 16, b1);
+        if (i + 8 < nsteps) put_x(i + 8, b2);
+        load_x(i + 20, b2);
       }
     }
     // ---- accumulator -> Y (S == 1) or the rank-0 DSMEM reduction
@@ -324,7 +350,30 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
 #pragma unroll
     for (int j = 0; j < kDecN; ++j) out[j] = __uint_as_float(v[j]);
     bool store = true;
-    if (S > 1) {
+    if (S > 1 && p.red_narrow) {
+      // narrow: ceil(M/4) float4 per row straight into rank 0's dedicated buffer, no invitation
+      const int mq = (p.M + 3) >> 2;
+      if (rank == 0) {
+        mbar_wait_cluster(red_full, 0);
+        for (int sl = 0; sl < S - 1; ++sl)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k < mq) {
+              const float4 t4 = reinterpret_cast<const float4*>(redbuf)[(sl * mq + k) * 128 + row];
+              out[4 * k] += t4.x;
+              out[4 * k + 1] += t4.y;
+              out[4 * k + 2] += t4.z;
+              out[4 * k + 3] += t4.w;
+            }
+      } else {
+        const uint32_t dst = map_rank(smem_u32(redbuf + ((rank - 1) * mq * 128 + row) * 4), 0u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < mq) st_cluster_v4(dst + k * 128 * 16, out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+        mbar_arrive_release_cluster(map_rank(smem_u32(red_full), 0u));
+        store = false;
+      }
+    } else if (S > 1) {
       float* red = reinterpret_cast<float*>(smem);  // rank 0: [S-1][128][16] fp32 (the stages are drained)
       if (rank == 0) {
         // every MMA of this CTA is complete, so its stage memory is free: invite the partials
@@ -359,7 +408,8 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
   }
   if (warp == 4 && lane_id() == 0) CL_STAMP(5);
   tc_fence_before();
-  cluster_sync_all();  // no CTA leaves while a peer may still touch its shared memory
+  if (S > 1) cluster_sync_all();  // no CTA leaves while a peer may still touch its shared memory
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<64>(tmem);

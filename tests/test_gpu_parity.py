@@ -244,13 +244,17 @@ def test_mx_decode_parity(D, M, K, N, r):
                      np.arange(r) if r else None)
     xt = _cuda(x, torch.bfloat16)
     ref = O.forward_mx(x, main_t, comp)
-    for _ in range(2):
-        # fused decode (quantizer inside the linear): Y and the activation codes it reports
+    # debug flag 1<<29: partials of the split-K reduction in full width through the drained stages
+    for flags in (0, 1 << 29, 0):
+        # serq_forward_mx: for M <= 4 the quantizer runs inside the decode kernel; Y and
+        # the activation codes it reports
         act = D.MxActivation(torch.empty(D.mx_sizes(M, K)[0], dtype=torch.uint8, device="cuda"),
                              torch.empty(D.mx_sizes(M, K)[1], dtype=torch.uint8, device="cuda"), M, K)
-        _lib.load().serq_set_debug_flags(1 << 23)  # the fused-quantizer decode kernel is opt-in
+        _lib.load().serq_set_debug_flags(flags)
         try:
             y = lin.forward(xt, act).float().cpu().numpy()
+            # two-kernel path (quantizer, then the linear on codes)
+            y2 = lin.gemm(lin.quantize(xt)).float().cpu().numpy()
         finally:
             _lib.load().serq_set_debug_flags(0)
         mx, mean = O.parity_errors(y, ref)
@@ -259,8 +263,6 @@ def test_mx_decode_parity(D, M, K, N, r):
         enc = O.mx_encode(x, 32)
         assert np.array_equal(c.cpu().numpy(), enc.element_codes)
         assert np.array_equal(e.cpu().numpy(), enc.block_scale_exponents)
-        # two-kernel path (quantizer, then the linear on codes)
-        y2 = lin.gemm(lin.quantize(xt)).float().cpu().numpy()
         assert np.array_equal(y2, y)
 
 

@@ -6,13 +6,13 @@ for SERQ_DEC_S (CTAs per weight tile) variants."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-from paper_2603_08185_b200 import benchmarks as B
+from paper_2603_08185_b200 import benchmarks as B, _lib
 
 layers = 16
 variants = os.environ.get("VARIANTS", "auto,1,2,3,4,6,8").split(",")
 for K, N in ((4096, 11008), (11008, 4096)):
     lins = [B.device_mx_linear(K, N, 64, seed=1 + i) for i in range(layers)]
-    for M in (1, 16):
+    for M in [int(v) for v in os.environ.get("MS", "1,16").split(",")]:
         x = B.outlier_x(M, K)
         acts = [lin.quantize(x) for lin in lins]
         ys = [torch.empty((M, N), dtype=torch.bfloat16, device="cuda") for _ in lins]
@@ -34,6 +34,7 @@ for K, N in ((4096, 11008), (11008, 4096)):
                     lin.forward(x, a, y)
             r = {"K": K, "N": N, "M": M, "S": v}
             for name, fn in (("lin", lin_all), ("two", two_all), ("fused", fused_all)):
+                _lib.call("serq_set_debug_flags", 0 if name == "fused" else (1 << 23))
                 t = B.time_graph(B.graph_of(fn), None, n=10) / layers * 1e-3
                 r[name + "_us"] = round(t * 1e6, 2)
                 r[name + "_gbs"] = round(byts / t / 1e9)

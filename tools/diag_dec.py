@@ -16,9 +16,9 @@ for K, N in ((4096, 11008), (11008, 4096)):
     x = B.outlier_x(M, K)
     acts = [l.quantize(x) for l in lins]
     ys = [torch.empty((M, N), dtype=torch.bfloat16, device="cuda") for _ in lins]
-    ts = torch.zeros((L, 1024 * 8), dtype=torch.int64, device="cuda")
+    ts = torch.zeros((L, 1024 * 8 + 384), dtype=torch.int64, device="cuda")
     fused = bool(os.environ.get("FUSED"))
-    lib.serq_set_debug_flags((1 << 23) if fused else 0)
+    lib.serq_set_debug_flags(0 if fused else (1 << 23))
     def chain():
         for i in range(L):
             lib.serq_set_debug_timestamps(ts[i].data_ptr())
@@ -31,11 +31,19 @@ for K, N in ((4096, 11008), (11008, 4096)):
     g = B.graph_of(chain)
     for _ in range(3):
         ts.zero_(); torch.cuda.synchronize(); g.replay(); torch.cuda.synchronize()
-    t = ts.cpu().numpy().reshape(L, 1024, 8).astype(np.float64)
+    tt = ts.cpu().numpy()
+    t = tt[:, :8192].reshape(L, 1024, 8).astype(np.float64)
     ok = t[:, :, 0] > 0
     t0 = t[0][ok[0]][:, 0].min()
     print(f"fused={fused} K={K} N={N} M={M}: ctas/layer={ok[0].sum()} (us from layer 0's first entry)")
     for i in range(L):
         v = (t[i][ok[i]] - t0) / 1e3
         print(f"  layer {i}: " + "  ".join(f"{n}={np.median(v[:, c]):.2f}[{v[:, c].max():.2f}]" for c, n in enumerate(names)))
+    st = tt[1, 8192:].reshape(6, 64).astype(np.float64)
+    base = st[2, 0]
+    kinds = ["w issued", "x issued", "mma start", "cv xfull", "cv empty", "cv arrived"]
+    print("  layer 1 CTA 0 per-step SM-clock (kcycles from first MMA):")
+    for c, n in enumerate(kinds):
+        v = st[c]; v = v[v > 0]
+        print(f"    {n:10s} " + " ".join(f"{(a - base) / 1e3:6.2f}" for a in v[:24]))
     del lins
