@@ -158,7 +158,7 @@ def mx_linear_point(lin, M: int, flush: Flusher) -> dict:
 def decode_points(hbm_peak_gbs: float, layers: int = 16) -> list:
     """BASELINE C4 decode: Llama-2-7B up_proj (4096 x 11008) and down_proj
     (11008 x 4096), M in {1, 4, 16}, r = 64.  Steady state: ONE graph runs the
-    step (quantize + linear) over ``layers`` distinct weight sets whose total
+    step (serq_forward_mx: quantize + linear) over ``layers`` distinct weight sets whose total
     size (~390 MB) exceeds the 126 MB L2, so every layer streams its weights
     from HBM; per-step time = graph time / layers."""
     out = []
@@ -170,9 +170,9 @@ def decode_points(hbm_peak_gbs: float, layers: int = 16) -> list:
             ys = [torch.empty((M, N), dtype=torch.bfloat16, device="cuda") for _ in lins]
 
             def run_all():
+                # the public call (serq_forward_mx): quantizer fused into the decode kernel for M <= 4
                 for lin, a, y in zip(lins, acts, ys):
-                    lin.quantize(x, a)
-                    lin.gemm(a, y)
+                    lin.forward(x, a, y)
 
             def lin_all():
                 for lin, a, y in zip(lins, acts, ys):
