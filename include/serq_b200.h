@@ -21,6 +21,7 @@
  *                                                                         quantcore.py:59-80, compensate.py:48-69
  *   serq_linear_mx         _forward_mx: mx_gemm_reference(x,W)+mx_gemm_reference(xs,R)
  *                                                                         compensate.py:319-340, mxfmt.py:198-225
+ *   serq_pack_int_grouped  row-grouped (group_size g) QuantizedTensor main     mxfmt.py:177-195, gptq.py:98-146
  *   serq_linear_int        forward_reconstructed int branch: int_gemm_reference(xq, main)
  *                          + R term (int_gemm_reference(xs, r_q) or dequantize(xs) @ r_dense)
  *                                                                         compensate.py:300-316, mxfmt.py:135-195
@@ -119,6 +120,16 @@ int serq_unpack_mx(const uint8_t* codes_packed, const uint8_t* sf, int64_t rows,
 int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t N, int w_bits, int r_mode,
                   const void* r_data, const double* r_scales, int r, int salient_contiguous, serq_linear_t** out,
                   serq_stream_t stream);
+
+/* Group-wise integer weights (int_gemm_reference row-grouped
+ * branch, mxfmt.py:177-195; GPTQ group_size, gptq.py:98-146; _weight_config,
+ * pipeline.py:134-137): scales float64 [K/group_size, N] (main.scales of a
+ * row-grouped QuantizedTensor), group_size a multiple of 128 and <= 1024 that
+ * divides K; group_size == K is serq_pack_int.  R as in serq_pack_int.
+ * serq_linear_int on such a handle promotes one integer partial per group. */
+int serq_pack_int_grouped(const int32_t* codes, const double* scales, int64_t group_size, int64_t K, int64_t N,
+                          int w_bits, int r_mode, const void* r_data, const double* r_scales, int r,
+                          int salient_contiguous, serq_linear_t** out, serq_stream_t stream);
 
 int serq_linear_destroy(serq_linear_t* h);
 int serq_linear_info(const serq_linear_t* h, int64_t* N, int64_t* K, int* r, int* mode, int* r_mode);

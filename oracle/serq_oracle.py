@@ -395,6 +395,36 @@ def build_per_channel_int(w, salient_idx, bits=4, r_mode="dense"):
     return main, Comp(r, idx, r_q=quantize_symmetric(resid, IntCfg(bits, True, r, "row")))
 
 
+def default_r_config(cols, bits=4, main_group="per-row") -> IntCfg:
+    """compensate.py:80-86: R scales per (salient row x column group)."""
+    gs = cols if main_group == "per-row" else min(cols, int(main_group))
+    if cols % gs != 0:
+        gs = cols
+    return IntCfg(bits, True, gs, "col")
+
+
+def build_grouped_int(w, salient_idx, group, bits=4, r_mode="int"):
+    """Group-wise INT artefacts: main = quantize_symmetric(W,
+    (bits, True, g, 'row')) -- scales [K/g, N], _weight_config with an integer
+    group (pipeline.py:134-137) -- and R = W[idx] - dequantize(main)[idx]
+    (build_serq_rtn's R when the salient rows fill the leading group,
+    compensate.py:102-113).  ``r_mode``: 'int' (row groups of size r, one
+    scale per output column), 'dense' (bf16 residual) or 'col' (the
+    reference's default_r_config, compensate.py:80-86)."""
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    main = quantize_symmetric(w, IntCfg(bits, True, int(group), "row"))
+    idx = np.asarray(salient_idx, np.intp)
+    r = idx.size
+    if r == 0:
+        return main, Comp(0, idx)
+    resid = w[idx] - dequantize(main)[idx]
+    if r_mode == "dense":
+        return main, Comp(r, idx, r_dense=bf16_round(resid))
+    if r_mode == "col":
+        return main, Comp(r, idx, r_q=quantize_symmetric(resid, default_r_config(w.shape[1], bits, group)))
+    return main, Comp(r, idx, r_q=quantize_symmetric(resid, IntCfg(bits, True, r, "row")))
+
+
 # ---------------------------------------------------------------------------
 # workload recipe helpers (reference tensorio.py / flatten.py / saliency.py)
 # ---------------------------------------------------------------------------

@@ -323,11 +323,12 @@ class SerqLinear:
             if not (a_axis == COL_GROUPS and a_gs == main.shape[0]):
                 raise ValidationError("activations must be quantized per token ('per-row')")
             axis, gs = _groups(main.config, main.shape)
-            if not (axis == ROW_GROUPS and gs == main.shape[0]):
+            k = main.shape[0]
+            if not (axis == ROW_GROUPS and (gs == k or (gs % 128 == 0 and gs <= 1024))) or main.zero_points is not None:
                 raise ValidationError(
-                    f"integer main layout (group_size={main.config.group_size!r}, axis={main.config.axis!r}) puts "
-                    "scales on the reduction dimension; the device path needs per-output-channel weights "
-                    "(group_size == K, axis 'row')")
+                    f"integer main layout (group_size={main.config.group_size!r}, axis={main.config.axis!r}) is not "
+                    "GPU-native: scales must be symmetric per output column (group_size == K, axis 'row') or per "
+                    "(row group, output column) with group_size a multiple of 128 up to 1024 (SURVEY F12)")
             kw = {}
             if has_r:
                 if comp.r_dense is not None:
@@ -335,11 +336,19 @@ class SerqLinear:
                 else:
                     rq = comp.r_q
                     ax, g = _groups(rq.config, rq.shape)
-                    if not (ax == ROW_GROUPS and g == rq.shape[0]) or rq.zero_points is not None:
+                    if ax == ROW_GROUPS and g == rq.shape[0] and rq.zero_points is None:
+                        kw = dict(r_codes=rq.codes, r_scales=rq.scales)
+                    elif ax == COL_GROUPS:
+                        # default_r_config (compensate.py:80-86): scales vary along the salient rows, so the
+                        # reference runs this term in its float branch (mxfmt.py:165-175) on dequantize(r_q);
+                        # the device runs it as the dense bf16 R term
+                        kw = dict(r_dense=dequantize(rq))
+                    else:
                         raise ValidationError(
-                            "integer R must be symmetric with one scale per output column (row groups of size r)")
-                    kw = dict(r_codes=rq.codes, r_scales=rq.scales)
-            self.impl = D.IntLinear(main.codes, main.scales, main.config.bits, salient_idx=idx, device=device, **kw)
+                            "integer R must be symmetric with one scale per output column (row groups of size r) or "
+                            "column-grouped (default_r_config)")
+            self.impl = D.IntLinear(main.codes, main.scales, main.config.bits, salient_idx=idx, device=device,
+                                    group_size=gs, **kw)
             self.act_bits, self.act_symmetric = act_cfg.bits, act_cfg.symmetric
             self.K, self.N = main.shape
         self.rank = int(comp.rank) if has_r else 0

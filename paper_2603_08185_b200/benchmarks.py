@@ -193,19 +193,22 @@ def decode_points(hbm_peak_gbs: float, layers: int = 16) -> list:
     return out
 
 
-def device_int_linear(K: int, N: int, r: int, r_mode: str, seed: int = 1):
-    """Synthetic per-output-channel INT4 SERQ linear (SURVEY F4 composition):
-    W ~ N(0, 0.02) [K, N]; main = per-column symmetric INT4; R = residual of
-    the first r rows, dense bf16 (``r_mode='dense'``) or INT4 with one scale
+def device_int_linear(K: int, N: int, r: int, r_mode: str, seed: int = 1, group: int | None = None):
+    """Synthetic SERQ INT4 linear (SURVEY F4 composition): W ~ N(0, 0.02) [K, N];
+    main = symmetric INT4 with one scale per output column (``group`` None) or
+    per (row group of ``group`` input rows, column); R = residual
+    of the first r rows, dense bf16 (``r_mode='dense'``) or INT4 with one scale
     per output column (``'int'``)."""
     g = torch.Generator(device="cuda").manual_seed(seed)
     w = torch.randn((K, N), generator=g, device="cuda", dtype=torch.float64) * 0.02
-    s = w.abs().amax(dim=0) / 7.0
+    gs = K if group is None else group
+    wg = w.view(K // gs, gs, N)
+    s = wg.abs().amax(dim=1) / 7.0  # [G, N]
     s = torch.where(s == 0, torch.ones_like(s), s)
-    codes = torch.clamp(torch.round(w / s), -7, 7).to(torch.int32)
+    codes = torch.clamp(torch.round(wg / s[:, None, :]), -7, 7).to(torch.int32).view(K, N)
     kw = {}
     if r:
-        resid = w[:r] - codes[:r].double() * s
+        resid = w[:r] - (codes.view(K // gs, gs, N).double() * s[:, None, :]).view(K, N)[:r]
         if r_mode == "dense":
             kw = dict(r_dense=resid.to(torch.bfloat16).double(), salient_idx=np.arange(r))
         else:
@@ -213,13 +216,14 @@ def device_int_linear(K: int, N: int, r: int, r_mode: str, seed: int = 1):
             sr = torch.where(sr == 0, torch.ones_like(sr), sr)
             kw = dict(r_codes=torch.clamp(torch.round(resid / sr), -7, 7).to(torch.int32), r_scales=sr,
                       salient_idx=np.arange(r))
-    return D.IntLinear(codes, s, 4, **kw)
+    return D.IntLinear(codes, s if group is not None else s.reshape(-1), 4, group_size=gs, **kw)
 
 
-def int_linear_point(M, K, N, r, r_mode, bits, symmetric, flush: Flusher | None = None, n_steps: int = 16) -> dict:
+def int_linear_point(M, K, N, r, r_mode, bits, symmetric, flush: Flusher | None = None, n_steps: int = 16,
+                     group: int | None = None) -> dict:
     """Steady state over n_steps steps cycling 8 weight sets x 8 activation sets
     (> L2 at these shapes: cold operands every step, no flush)."""
-    lins = [device_int_linear(K, N, r, r_mode, seed=1 + i) for i in range(8)]
+    lins = [device_int_linear(K, N, r, r_mode, seed=1 + i, group=group) for i in range(8)]
     xs = [outlier_x(M, K, seed=i) for i in range(8)]
     acts = [lins[0].quantize(x, bits, symmetric) for x in xs]
     ys = [torch.empty((M, N), dtype=torch.bfloat16, device="cuda") for _ in xs]
@@ -234,7 +238,7 @@ def int_linear_point(M, K, N, r, r_mode, bits, symmetric, flush: Flusher | None 
     t_lin = time_steps(lin_only, n_steps)
     flops = 2.0 * M * N * (K + r)
     return {"M": M, "K": K, "N": N, "r": r, "r_mode": r_mode, "act_bits": bits, "act_symmetric": symmetric,
-            "step_us": t_step * 1e3, "linear_us": t_lin * 1e3, "linear_tops": flops / (t_lin * 1e-3) / 1e12,
+            "weight_group": group or K, "step_us": t_step * 1e3, "linear_us": t_lin * 1e3, "linear_tops": flops / (t_lin * 1e-3) / 1e12,
             "step_tops": flops / (t_step * 1e-3) / 1e12, "tokens_per_s": M / (t_step * 1e-3)}
 
 

@@ -14,6 +14,7 @@
 #include "serq_gemm_mx3.cuh"
 #include "serq_gemm_decode3.cuh"
 #include "serq_gemm_i8.cuh"
+#include "serq_gemm_i8g.cuh"
 #include "serq_quant.cuh"
 
 using namespace serq;
@@ -159,6 +160,11 @@ struct serq_linear {
   CUtensorMap map_w4, map_r_pair;                    // INT pair kernel maps (R with 128-row boxes)
   CUtensorMap map_w8;                                // INT pair kernel, direct int8 weights: 128 B x 128-row boxes
   bool has_w4 = false;
+  // INT, group-wise weight scales along K (serq_pack_int_grouped)
+  int groups = 1, gsteps = 0;
+  float* sw_g = nullptr;       // [G][N]
+  int32_t* colsum_g = nullptr; // [G][N]
+  float* cterm = nullptr;      // [N]
   // CTA-pair split last wave: fp32 partials + per-(tile, rank) counters
   float* sk_ws = nullptr;
   int64_t sk_ws_floats = 0;
@@ -179,7 +185,8 @@ struct serq_linear {
 namespace {
 void free_handle(serq_linear* h) {
   void* ptrs[] = {h->w, h->sfw, h->rbuf, h->sfr, h->sw, h->colsum, h->sr, h->colsum_r,
-                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y, h->sk_ws, h->sk_cnt, h->w4};
+                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y, h->sk_ws, h->sk_cnt, h->w4,
+                  h->sw_g, h->colsum_g, h->cterm};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : h->e2e_ev)
@@ -534,6 +541,44 @@ int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t
   return SERQ_OK;
 }
 
+int serq_pack_int_grouped(const int32_t* codes, const double* scales, int64_t group_size, int64_t K, int64_t N,
+                          int w_bits, int r_mode, const void* r_data, const double* r_scales, int r,
+                          int salient_contiguous, serq_linear_t** out, serq_stream_t stream) {
+  if (group_size == K)
+    return serq_pack_int(codes, scales, K, N, w_bits, r_mode, r_data, r_scales, r, salient_contiguous, out, stream);
+  if (!out) return fail(SERQ_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (group_size <= 0 || group_size % 128 || group_size > 1024 || K % group_size)
+    return fail(SERQ_EINVAL,
+                "group_size %lld: the device needs a multiple of 128, at most 1024, dividing K = %lld "
+                "(one integer partial per 128-K steps, |partial| < 2^22)",
+                (long long)group_size, (long long)K);
+  if (r_mode == SERQ_R_INT && (!salient_contiguous || r > 128))
+    return fail(SERQ_EINVAL, "group-wise weights with integer R need the permuted layout and r <= 128");
+  if (r_mode == SERQ_R_DENSE && r > 128) return fail(SERQ_EINVAL, "group-wise weights with dense R need r <= 128");
+  // the per-channel pack builds the int8 weights, R and their maps (its group-0 scales go unused)
+  serq_linear_t* h = nullptr;
+  int rc = serq_pack_int(codes, scales, K, N, w_bits, r_mode, r_data, r_scales, r, salient_contiguous, &h, stream);
+  if (rc) return rc;
+  const int64_t G = K / group_size;
+  h->groups = int(G);
+  h->gsteps = int(group_size / 128);
+  if (cudaMalloc(&h->sw_g, G * N * 4) != cudaSuccess || cudaMalloc(&h->colsum_g, G * N * 4) != cudaSuccess ||
+      cudaMalloc(&h->cterm, N * 4) != cudaSuccess) {
+    free_handle(h);
+    return fail(SERQ_ECUDA, "cudaMalloc failed for group scales");
+  }
+  group_pack_kernel<<<unsigned(cdiv(N, 256)), 256, 0, S(stream)>>>(
+      codes, K, N, group_size, scales, r_mode == SERQ_R_INT ? r_scales : nullptr, h->colsum_r, h->colsum_g, h->sw_g,
+      h->cterm);
+  if (cudaGetLastError() != cudaSuccess) {
+    free_handle(h);
+    return fail(SERQ_ECUDA, "group_pack launch failed");
+  }
+  *out = h;
+  return SERQ_OK;
+}
+
 int serq_linear_destroy(serq_linear_t* h) {
   if (h) free_handle(h);
   return SERQ_OK;
@@ -834,6 +879,54 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   if (ldy < h->N || ldy % 8) return fail(SERQ_EINVAL, "ldy must be >= N and a multiple of 8");
   const bool need_xs = h->r_mode == SERQ_R_DENSE || (h->r_mode == SERQ_R_INT && !h->contiguous);
   if (need_xs && !xs) return fail(SERQ_EINVAL, "this R mode needs the quantizer's xs slice");
+  if (h->groups > 1) {
+    // group-wise weight scales: one promoted integer partial per group (serq_gemm_i8g.cuh), any M
+    static bool attrg = false;
+    if (!attrg) {
+      CK(cudaFuncSetAttribute(serq_i8g_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kI8gSmem));
+      CK(cudaFuncSetAttribute(serq_i8g_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kI8gSmem));
+      attrg = true;
+    }
+    I8Maps im;
+    int rc = make_map(&im.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K, M, h->K, 128, 128);
+    if (!rc)  // 32 rows x 16 columns per epilogue-warp store, no swizzle
+      rc = make_map(&im.y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, h->N, M, ldy * 2, 16, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (!rc && h->r_mode == SERQ_R_DENSE)
+      rc = make_map(&im.xs, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xs, h->r, M, h->r * 2, 64, 128);
+    if (rc) return rc;
+    if (h->r_mode != SERQ_R_DENSE) im.xs = im.a;
+    im.bp = h->map_w8;
+    im.r = h->r_mode != SERQ_R_NONE ? h->map_r_pair : im.bp;
+    I8gParams p{};
+    p.M = int(M);
+    p.N = int(h->N);
+    p.K = int(h->K);
+    p.r = h->r;
+    p.r_mode = h->r_mode;
+    p.a_signed = zp ? 0 : 1;
+    p.k_steps = int(h->K / 128);
+    p.gsteps = h->gsteps;
+    p.sx = sx;
+    p.zp = zp;
+    p.sw_g = h->sw_g;
+    p.cterm = h->cterm;
+    p.sr = h->sr;
+    p.colsum_g = h->colsum_g;
+    p.colsum_r = h->colsum_r;
+    p.addend = addend;
+    p.acc_dump = acc_dump;
+    p.accr_dump = accr_dump;
+    p.dbg_ts = g_debug_ts;
+    const int64_t tiles = cdiv(M, 256) * cdiv(h->N, 256);
+    const int64_t max_pairs = sm_count() / 2;
+    const dim3 grid(unsigned(2 * (tiles < max_pairs ? tiles : max_pairs)));
+    if (acc_dump || accr_dump)
+      serq_i8g_pair_kernel<true><<<grid, kI8gThreads, kI8gSmem, S(stream)>>>(im, p);
+    else
+      serq_i8g_pair_kernel<false><<<grid, kI8gThreads, kI8gSmem, S(stream)>>>(im, p);
+    LAUNCH_CHECK("serq_i8g_pair_kernel");
+    return SERQ_OK;
+  }
   // CTA-pair kernel: int8 weights TMA'd directly (default; measured faster than widening packed
   // INT4 in shared memory, which remains under debug flag 1<<28)
   const bool widen = (g_debug_flags & (1 << 28)) && h->has_w4;

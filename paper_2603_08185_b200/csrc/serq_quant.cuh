@@ -851,6 +851,27 @@ __global__ void colsum_kernel(const int32_t* __restrict__ src, int64_t K, int64_
 }
 
 // dense R (f64 [r, N]) -> L^T bf16 [N, r], one rounding f64 -> bf16
+// Group-wise weights (row groups of gs input rows): per column n, the group
+// colsums, the fp32 group scales and the folded zero-point term
+// C[n] = sum_g s[g,n] * colsum_g[n] (+ sr[n] * colsum_r[n]), accumulated in f64.
+__global__ void group_pack_kernel(const int32_t* __restrict__ src, int64_t K, int64_t N, int64_t gs,
+                                  const double* __restrict__ s64, const double* __restrict__ sr64,
+                                  const int32_t* __restrict__ colsum_r, int32_t* __restrict__ colsum_g,
+                                  float* __restrict__ sw_g, float* __restrict__ cterm) {
+  const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  double c = 0.0;
+  for (int64_t g = 0; g < K / gs; ++g) {
+    int32_t acc = 0;
+    for (int64_t k = g * gs; k < (g + 1) * gs; ++k) acc += src[k * N + n];
+    colsum_g[g * N + n] = acc;
+    sw_g[g * N + n] = float(s64[g * N + n]);
+    c += s64[g * N + n] * double(acc);
+  }
+  if (sr64) c += sr64[n] * double(colsum_r[n]);
+  cterm[n] = float(c);
+}
+
 __global__ void dense_r_kernel(const double* __restrict__ src, int64_t r, int64_t N, __nv_bfloat16* __restrict__ dst) {
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= r * N) return;

@@ -270,20 +270,26 @@ class MxLinear:
 
 
 class IntLinear:
-    """Packed integer SERQ linear: per-output-channel INT weights
-    (QuantizedTensor with group_size == K, quantcore.py:59-80) plus the
+    """Packed integer SERQ linear: INT weights with per-output-channel scales
+    (QuantizedTensor with group_size == K, quantcore.py:59-80; ``scales`` [N])
+    or group-wise along K (row groups of ``group_size`` a multiple of 128,
+    gptq.py:98-146 / pipeline.py:134-137; ``scales`` [K/group_size, N]) plus the
     compensator R as bf16 (r_dense) or integer codes with one scale per
     output column (r_q, row groups of size r)."""
 
     def __init__(self, codes, scales, bits=4, r_dense=None, r_codes=None, r_scales=None, salient_idx=None,
-                 device="cuda"):
+                 device="cuda", group_size=None):
         device = torch.device(device)
         codes = _dev(codes, torch.int32, device)
         self.K, self.N = codes.shape
-        scales = _dev(np.asarray(scales, dtype=np.float64).reshape(-1) if not isinstance(scales, torch.Tensor)
-                      else scales.reshape(-1), torch.float64, device)
-        if scales.numel() != self.N:
-            raise ValidationError("integer main path needs one scale per output column (group_size == K)")
+        scales = _dev(np.asarray(scales, dtype=np.float64) if not isinstance(scales, torch.Tensor) else scales,
+                      torch.float64, device)
+        self.group_size = self.K if group_size is None else int(group_size)
+        if self.group_size <= 0 or self.K % self.group_size:
+            raise ValidationError(f"group_size {self.group_size} does not divide K = {self.K}")
+        if scales.numel() != (self.K // self.group_size) * self.N:
+            raise ValidationError("integer main path needs scales [K/group_size, N] (one per output column and group)")
+        scales = scales.reshape(-1).contiguous()
         if r_dense is not None:
             self.r_mode = _lib.SERQ_R_DENSE
             rd = _dev(r_dense, torch.float64, device)
@@ -303,8 +309,8 @@ class IntLinear:
         self.contiguous = idx is None or np.array_equal(idx, np.arange(self.r))
         self.salient_idx = None if idx is None or self.contiguous else torch.from_numpy(idx.astype(np.int32)).to(device)
         h = ctypes.c_void_p()
-        _lib.call("serq_pack_int", codes.data_ptr(), scales.data_ptr(), self.K, self.N, bits, self.r_mode,
-                  _ptr(rdata), _ptr(rs), self.r, int(self.contiguous), ctypes.byref(h), _stream())
+        _lib.call("serq_pack_int_grouped", codes.data_ptr(), scales.data_ptr(), self.group_size, self.K, self.N, bits,
+                  self.r_mode, _ptr(rdata), _ptr(rs), self.r, int(self.contiguous), ctypes.byref(h), _stream())
         torch.cuda.current_stream().synchronize()
         self._h = _Handle(h)
         self.device = device

@@ -225,6 +225,65 @@ def test_int_linear_gather_int_r(D):
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
 
 
+# ---------------------------------------------------------------- K3 with group-wise weight scales
+
+
+@pytest.mark.parametrize("M,K,N,g,r,bits,symmetric,r_mode", [
+    (300, 1024, 512, 128, 64, 8, False, "int"),
+    (200, 2048, 768, 128, 128, 4, False, "int"),
+    (100, 1024, 1000, 256, 64, 8, False, "dense"),
+    (512, 1024, 512, 128, 64, 4, True, "col"),
+    (70, 512, 264, 128, 0, 8, False, "none"),
+    (600, 3072, 512, 1024, 32, 8, False, "int"),
+    (256, 2048, 512, 128, 128, 8, False, "col"),    # the paper's g = r = 128 with default_r_config R
+    (130, 1024, 776, 256, 96, 4, False, "dense"),
+])
+def test_int_grouped_linear_parity(D, M, K, N, g, r, bits, symmetric, r_mode):
+    # int_gemm_reference row-grouped branch: one exact integer partial per group
+    # (acc_dump [G, M, N]), promoted with the group's scales in fp32
+    x = _bf16_outlier_x(M, K, seed=M + g)
+    w = np.random.default_rng(K + g).standard_normal((K, N)) * 0.02
+    main, comp = O.build_grouped_int(w, np.arange(r), g, 4, "int" if r_mode == "none" else r_mode)
+    if r_mode == "none":
+        comp = None
+    kw = {}
+    if r_mode == "dense":
+        kw = dict(r_dense=comp.r_dense, salient_idx=np.arange(r))
+    elif r_mode == "col":
+        kw = dict(r_dense=O.dequantize(comp.r_q), salient_idx=np.arange(r))
+    elif r_mode == "int":
+        kw = dict(r_codes=comp.r_q.codes, r_scales=comp.r_q.scales, salient_idx=np.arange(r))
+    lin = D.IntLinear(main.codes, main.scales, 4, group_size=g, **kw)
+    act = lin.quantize(_cuda(x, torch.bfloat16), bits, symmetric)
+    G = K // g
+    acc = torch.zeros((G, M, N), dtype=torch.int32, device="cuda")
+    accr = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    for _ in range(2):
+        y = lin.gemm(act, acc_dump=acc, accr_dump=accr).float().cpu().numpy()
+        cfg = O.IntCfg(bits, symmetric, "per-row")
+        y_ref, xq = O.forward_int(x, main, comp, cfg, symmetric_act=symmetric)
+        _, parts = O.int_gemm(xq, main, return_partials=True)
+        assert len(parts) == G
+        for gi in range(G):
+            assert np.array_equal(acc[gi].cpu().numpy().astype(np.int64), parts[gi][1]), gi
+        if r_mode == "int":
+            _, rp = O.int_gemm(O.gather_columns(xq, np.arange(r)), comp.r_q, return_partials=True)
+            assert np.array_equal(accr.cpu().numpy().astype(np.int64), rp[0][1])
+        mx, mean = O.parity_errors(y, y_ref)
+        assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+def test_int_grouped_rejects_unsupported_groups(D):
+    from paper_2603_08185_b200.errors import ValidationError
+
+    K, N = 512, 256
+    w = np.random.default_rng(3).standard_normal((K, N)) * 0.02
+    for g in (64, 32):
+        main = O.quantize_symmetric(w, O.IntCfg(4, True, g, "row"))
+        with pytest.raises(ValidationError):
+            D.IntLinear(main.codes, main.scales, 4, group_size=g)
+
+
 # ---------------------------------------------------------------- decode (M <= 16): swap-AB split-K kernel
 
 
