@@ -54,6 +54,9 @@ extern "C" {
 #define SERQ_R_NONE 0
 #define SERQ_R_DENSE 1 /* comp.r_dense: float64 [r, N], consumed as bf16 */
 #define SERQ_R_INT 2   /* comp.r_q: int codes [r, N] with one scale per output column */
+#define SERQ_R_DENSE_SPLIT 3 /* float64 [r, N] consumed as bf16 hi + bf16 lo (relative error 2^-17):
+                              * dequantize(r_q) of a column-grouped R (default_r_config), a GPTQ-swapped
+                              * R, or an f64 r_dense; serq_pack_int_grouped only */
 
 typedef struct serq_linear serq_linear_t; /* packed weight handle (opaque) */
 typedef void* serq_stream_t;              /* cudaStream_t */

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 SERQ_OK, SERQ_EINVAL, SERQ_ECUDA = 0, 1, 2
 SERQ_BF16, SERQ_F32, SERQ_F64 = 0, 1, 2
-SERQ_R_NONE, SERQ_R_DENSE, SERQ_R_INT = 0, 1, 2
+SERQ_R_NONE, SERQ_R_DENSE, SERQ_R_INT, SERQ_R_DENSE_SPLIT = 0, 1, 2, 3
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

@@ -167,23 +167,27 @@ def _quantize(x, cfg: IntQuantConfig, symmetric: bool) -> QuantizedTensor:
     if cfg.symmetric != symmetric:
         raise ValidationError("config is not symmetric" if symmetric else "config is not asymmetric")
     x = _as_matrix(x)
+    rows, cols = x.shape
     axis, gs = _groups(cfg, x.shape)
-    if axis == COL_GROUPS and gs == x.shape[1]:
-        src, transpose = x, False  # one group per row (per-token)
-    elif axis == ROW_GROUPS and gs == x.shape[0]:
-        src, transpose = np.ascontiguousarray(x.T), True  # one group per column (per-output-channel)
+    # every group is a 1-D run of gs elements: lay the groups out as the rows of a
+    # [n_groups, gs] matrix and quantize per row on the device (quantcore.py:83-94 layouts)
+    if axis == COL_GROUPS:
+        src = x.reshape(rows * (cols // gs), gs)  # scale per (row, column group)
     else:
-        raise ValidationError(
-            f"group layout (group_size={cfg.group_size!r}, axis={cfg.axis!r}) is not supported on the device; "
-            "supported: 'per-row' or one group spanning the grouped dimension")
-    act = D.quantize_int(_to_gpu(src), cfg.bits, symmetric)
+        src = np.ascontiguousarray(x.reshape(rows // gs, gs, cols).transpose(0, 2, 1)).reshape(-1, gs)
+    act = D.quantize_int(_to_gpu(np.ascontiguousarray(src)), cfg.bits, symmetric)
     codes = act.codes.cpu().numpy()
     codes = codes.astype(np.int32) if symmetric else codes.view(np.uint8).astype(np.int32)
-    scales = act.scale64.cpu().numpy().reshape(-1, 1)
-    zps = None if symmetric else act.zp.cpu().numpy().astype(np.int32).reshape(-1, 1)
-    if transpose:
-        codes, scales = np.ascontiguousarray(codes.T), scales.T.copy()
-        zps = None if zps is None else zps.T.copy()
+    scales = act.scale64.cpu().numpy()
+    zps = None if symmetric else act.zp.cpu().numpy().astype(np.int32)
+    if axis == COL_GROUPS:
+        codes = codes.reshape(rows, cols)
+        scales = scales.reshape(rows, cols // gs)
+        zps = None if zps is None else zps.reshape(rows, cols // gs)
+    else:
+        codes = np.ascontiguousarray(codes.reshape(rows // gs, cols, gs).transpose(0, 2, 1)).reshape(rows, cols)
+        scales = scales.reshape(rows // gs, cols)
+        zps = None if zps is None else zps.reshape(rows // gs, cols)
     return QuantizedTensor(codes, scales, zps, cfg, x.shape)
 
 
@@ -275,6 +279,28 @@ def build_per_channel_int(w, salient_idx, bits: int = 4, r_mode: str = "dense"):
 # ------------------------------------------------------------------ linear modules
 
 
+def build_serq_rtn(w_folded, plan, wcfg: IntQuantConfig, rcfg: IntQuantConfig | None):
+    """compensate.build_serq_rtn (compensate.py:89-114) with the device quantizers:
+    main = quantize_symmetric(W, wcfg); R = Ws - fake_quant(Ws, wcfg) over the
+    salient rows, quantized with ``rcfg`` or kept dense (``rcfg=None``).  With
+    wcfg row groups of g and r a multiple of g this is the
+    group-wise artefact the device consumes."""
+    w = _as_matrix(w_folded, "w_folded")
+    scores = np.asarray(plan.scores)
+    if scores.shape[0] != w.shape[0]:
+        raise ValidationError("plan was not built for this weight")
+    main = quantize_symmetric(w, wcfg)
+    r = int(plan.rank)
+    if r == 0:
+        return main, Compensator(RTN_RESIDUAL, 0, np.empty(0, np.intp))
+    idx = np.asarray(plan.salient_idx, dtype=np.intp)
+    ws = w[idx]
+    resid = ws - dequantize(quantize_symmetric(ws, wcfg))
+    if rcfg is None:
+        return main, Compensator(RTN_RESIDUAL, r, idx.copy(), r_dense=resid)
+    return main, Compensator(RTN_RESIDUAL, r, idx.copy(), r_q=quantize_symmetric(resid, rcfg))
+
+
 def _is_mx(t) -> bool:
     return hasattr(t, "element_codes") and hasattr(t, "block_scale_exponents")
 
@@ -332,7 +358,8 @@ class SerqLinear:
             kw = {}
             if has_r:
                 if comp.r_dense is not None:
-                    kw = dict(r_dense=np.asarray(comp.r_dense))
+                    # a GPTQ-swapped R holds the salient rows themselves (compensate.py:136-143): hi + lo planes
+                    kw = dict(r_dense=np.asarray(comp.r_dense), r_split=comp.mode == GPTQ_SWAPPED)
                 else:
                     rq = comp.r_q
                     ax, g = _groups(rq.config, rq.shape)
@@ -341,8 +368,9 @@ class SerqLinear:
                     elif ax == COL_GROUPS:
                         # default_r_config (compensate.py:80-86): scales vary along the salient rows, so the
                         # reference runs this term in its float branch (mxfmt.py:165-175) on dequantize(r_q);
-                        # the device runs it as the dense bf16 R term
-                        kw = dict(r_dense=dequantize(rq))
+                        # the device runs it as a dense R split into bf16 hi + lo planes (a GPTQ-swapped R
+                        # is the salient rows themselves, too large a share of Y for one bf16 rounding)
+                        kw = dict(r_dense=dequantize(rq), r_split=True)
                     else:
                         raise ValidationError(
                             "integer R must be symmetric with one scale per output column (row groups of size r) or "

@@ -162,6 +162,7 @@ struct serq_linear {
   bool has_w4 = false;
   // INT, group-wise weight scales along K (serq_pack_int_grouped)
   int groups = 1, gsteps = 0;
+  bool use_i8g = false;        // served by serq_i8g_pair_kernel
   float* sw_g = nullptr;       // [G][N]
   int32_t* colsum_g = nullptr; // [G][N]
   float* cterm = nullptr;      // [N]
@@ -544,22 +545,45 @@ int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t
 int serq_pack_int_grouped(const int32_t* codes, const double* scales, int64_t group_size, int64_t K, int64_t N,
                           int w_bits, int r_mode, const void* r_data, const double* r_scales, int r,
                           int salient_contiguous, serq_linear_t** out, serq_stream_t stream) {
-  if (group_size == K)
+  if (group_size == K && r_mode != SERQ_R_DENSE_SPLIT)
     return serq_pack_int(codes, scales, K, N, w_bits, r_mode, r_data, r_scales, r, salient_contiguous, out, stream);
   if (!out) return fail(SERQ_EINVAL, "out is NULL");
   *out = nullptr;
-  if (group_size <= 0 || group_size % 128 || group_size > 1024 || K % group_size)
+  if (group_size <= 0 || group_size % 128 || group_size > 8192 || K % group_size)
     return fail(SERQ_EINVAL,
-                "group_size %lld: the device needs a multiple of 128, at most 1024, dividing K = %lld "
-                "(one integer partial per 128-K steps, |partial| < 2^22)",
+                "group_size %lld: the device needs a multiple of 128, at most 8192, dividing K = %lld "
+                "(one integer partial per group, exact in fp32)",
                 (long long)group_size, (long long)K);
   if (r_mode == SERQ_R_INT && (!salient_contiguous || r > 128))
     return fail(SERQ_EINVAL, "group-wise weights with integer R need the permuted layout and r <= 128");
-  if (r_mode == SERQ_R_DENSE && r > 128) return fail(SERQ_EINVAL, "group-wise weights with dense R need r <= 128");
-  // the per-channel pack builds the int8 weights, R and their maps (its group-0 scales go unused)
+  if ((r_mode == SERQ_R_DENSE || r_mode == SERQ_R_DENSE_SPLIT) && (r > 128 || r % 8 || r <= 0 || !r_data))
+    return fail(SERQ_EINVAL, "group-wise weights with dense R need 0 < r <= 128, r %% 8 == 0");
+  // the per-channel pack builds the int8 weights (and R unless split) and their maps; its group-0
+  // scales go unused
   serq_linear_t* h = nullptr;
-  int rc = serq_pack_int(codes, scales, K, N, w_bits, r_mode, r_data, r_scales, r, salient_contiguous, &h, stream);
+  const bool split = r_mode == SERQ_R_DENSE_SPLIT;
+  int rc = serq_pack_int(codes, scales, K, N, w_bits, split ? SERQ_R_NONE : r_mode, split ? nullptr : r_data,
+                         r_scales, split ? 0 : r, salient_contiguous, &h, stream);
   if (rc) return rc;
+  h->use_i8g = true;
+  if (split) {
+    // bf16 hi plane rows [0, N), lo plane rows [N, 2N), each [N, r]
+    h->r = r;
+    h->r_mode = SERQ_R_DENSE_SPLIT;
+    h->contiguous = salient_contiguous ? 1 : 0;
+    if (cudaMalloc(&h->rbuf, 2 * N * r * 2) != cudaSuccess) {
+      free_handle(h);
+      return fail(SERQ_ECUDA, "cudaMalloc R");
+    }
+    __nv_bfloat16* hi = static_cast<__nv_bfloat16*>(h->rbuf);
+    dense_r_split_kernel<<<unsigned(cdiv(N * r, 256)), 256, 0, S(stream)>>>(static_cast<const double*>(r_data), r, N,
+                                                                            hi, hi + N * r);
+    rc = make_map(&h->map_r_pair, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h->rbuf, r, 2 * N, r * 2, 64, 128);
+    if (rc || cudaGetLastError() != cudaSuccess) {
+      free_handle(h);
+      return rc ? rc : fail(SERQ_ECUDA, "dense_r_split launch failed");
+    }
+  }
   const int64_t G = K / group_size;
   h->groups = int(G);
   h->gsteps = int(group_size / 128);
@@ -877,24 +901,27 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   if (!h || h->mode != kModeI8) return fail(SERQ_EINVAL, "handle is not an INT linear");
   if (M <= 0) return fail(SERQ_EINVAL, "x must be non-empty");
   if (ldy < h->N || ldy % 8) return fail(SERQ_EINVAL, "ldy must be >= N and a multiple of 8");
-  const bool need_xs = h->r_mode == SERQ_R_DENSE || (h->r_mode == SERQ_R_INT && !h->contiguous);
+  const bool need_xs = h->r_mode == SERQ_R_DENSE || h->r_mode == SERQ_R_DENSE_SPLIT ||
+                       (h->r_mode == SERQ_R_INT && !h->contiguous);
   if (need_xs && !xs) return fail(SERQ_EINVAL, "this R mode needs the quantizer's xs slice");
-  if (h->groups > 1) {
+  if (h->use_i8g) {
     // group-wise weight scales: one promoted integer partial per group (serq_gemm_i8g.cuh), any M
     static bool attrg = false;
     if (!attrg) {
-      CK(cudaFuncSetAttribute(serq_i8g_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kI8gSmem));
-      CK(cudaFuncSetAttribute(serq_i8g_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kI8gSmem));
+      int mx = 0;
+      for (int m = 0; m <= kRDenseSplit; ++m) mx = i8g_smem(m) > mx ? i8g_smem(m) : mx;
+      CK(cudaFuncSetAttribute(serq_i8g_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      CK(cudaFuncSetAttribute(serq_i8g_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
       attrg = true;
     }
     I8Maps im;
     int rc = make_map(&im.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K, M, h->K, 128, 128);
     if (!rc)  // 32 rows x 16 columns per epilogue-warp store, no swizzle
       rc = make_map(&im.y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, h->N, M, ldy * 2, 16, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
-    if (!rc && h->r_mode == SERQ_R_DENSE)
+    if (!rc && (h->r_mode == SERQ_R_DENSE || h->r_mode == SERQ_R_DENSE_SPLIT))
       rc = make_map(&im.xs, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xs, h->r, M, h->r * 2, 64, 128);
     if (rc) return rc;
-    if (h->r_mode != SERQ_R_DENSE) im.xs = im.a;
+    if (h->r_mode != SERQ_R_DENSE && h->r_mode != SERQ_R_DENSE_SPLIT) im.xs = im.a;
     im.bp = h->map_w8;
     im.r = h->r_mode != SERQ_R_NONE ? h->map_r_pair : im.bp;
     I8gParams p{};
@@ -921,9 +948,9 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     const int64_t max_pairs = sm_count() / 2;
     const dim3 grid(unsigned(2 * (tiles < max_pairs ? tiles : max_pairs)));
     if (acc_dump || accr_dump)
-      serq_i8g_pair_kernel<true><<<grid, kI8gThreads, kI8gSmem, S(stream)>>>(im, p);
+      serq_i8g_pair_kernel<true><<<grid, kI8gThreads, i8g_smem(h->r_mode), S(stream)>>>(im, p);
     else
-      serq_i8g_pair_kernel<false><<<grid, kI8gThreads, kI8gSmem, S(stream)>>>(im, p);
+      serq_i8g_pair_kernel<false><<<grid, kI8gThreads, i8g_smem(h->r_mode), S(stream)>>>(im, p);
     LAUNCH_CHECK("serq_i8g_pair_kernel");
     return SERQ_OK;
   }

@@ -23,7 +23,7 @@
 namespace serq {
 
 enum GemmMode : int { kModeMX = 0, kModeI8 = 1 };
-enum RMode : int { kRNone = 0, kRDense = 1, kRInt = 2 };
+enum RMode : int { kRNone = 0, kRDense = 1, kRInt = 2, kRDenseSplit = 3 };
 
 constexpr int kBM = 128;
 constexpr int kBN = 256;

@@ -22,21 +22,36 @@
 //   scales (staged in shared memory one unit ahead), and hand the accumulator back.
 // * The salient term is one more unit per tile: integer R (kind::i8, A = K-tile 0 of X,
 //   B = R codes, scale sr[n]; r <= 128) or dense bf16 R (kind::f16, A = bf16 (c - zp) slice,
-//   B = L^T, r <= 128 in two 64-column atoms; fp32 accumulator added as is).
+//   B = L^T, r <= 128 in two 64-column atoms; fp32 accumulator added as is) -- optionally
+//   split as L = hi + lo (two bf16 planes, both MMAs into the same accumulator: relative
+//   error 2^-17 instead of 2^-9), for R matrices that are not small residuals (GPTQ-swapped).
+// * Pipeline depth follows the side buffer: 5 stages (no / integer R), 4 (dense), 3 (split).
 #pragma once
 #include "serq_gemm_i8.cuh"
 
 namespace serq {
 
-constexpr int kI8gStages = 4;
+constexpr int kI8gMaxStages = 5;
 constexpr int kI8gStage = kI8A + kI8B;  // 16 KB activation + 16 KB weight rows
 // 18 warps: 5 on two of the SM's sub-partitions, so <= 96 registers per thread (64 KB / 4 SMSPs)
 constexpr int kI8gEpiWarps = 16;        // four per TMEM lane quadrant
 constexpr int kI8gCols = 256 / (kI8gEpiWarps / 4);  // accumulator columns per epilogue thread
 constexpr int kI8gThreads = 32 * (2 + kI8gEpiWarps);  // producer, MMA, epilogue
-constexpr int kI8gSide = 4 * 16384;     // R operands, r <= 128: [A' bf16 2 x 16K][B_R 2 x 16K (bf16) | 16K (int8)]
-constexpr int kI8gSmem = 1024 + kI8gStages * kI8gStage + kI8gSide + 2 * 1024 + 1024 + kI8gEpiWarps * 1024 + 512;
-static_assert(kI8gSmem <= 232448, "smem budget");
+// R operands (r <= 128) in the side buffer: integer R: B_R [0, 16K); dense / split bf16 R:
+// A' [0, 32K), B (hi) [32K, 64K), B lo [64K, 96K) (split only).  The pipeline gets what is left.
+constexpr int kI8gFixed = 1024 + 2 * 1024 + 1024 + kI8gEpiWarps * 1024 + 512;
+__host__ __device__ constexpr int i8g_side_bytes(int r_mode) {
+  return r_mode == kRInt ? 16384 : r_mode == kRDense ? 65536 : r_mode == kRDenseSplit ? 98304 : 0;
+}
+__host__ __device__ constexpr int i8g_stages(int r_mode) {
+  return (232448 - kI8gFixed - i8g_side_bytes(r_mode)) / kI8gStage < kI8gMaxStages
+             ? (232448 - kI8gFixed - i8g_side_bytes(r_mode)) / kI8gStage
+             : kI8gMaxStages;
+}
+__host__ __device__ constexpr int i8g_smem(int r_mode) {
+  return kI8gFixed + i8g_stages(r_mode) * kI8gStage + i8g_side_bytes(r_mode);
+}
+static_assert(i8g_stages(kRDenseSplit) >= 3, "smem budget");
 
 struct I8gParams {
   int M, N, K;
@@ -85,14 +100,15 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
     serq_i8g_pair_kernel(const __grid_constant__ I8Maps maps, const I8gParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* side = smem + kI8gStages * kI8gStage;              // [A' 32K][B_R 32K]
-  float* sc = reinterpret_cast<float*>(side + kI8gSide);      // [2][256] unit scales
+  const int S = i8g_stages(p.r_mode);
+  uint8_t* side = smem + S * kI8gStage;                       // R operands
+  float* sc = reinterpret_cast<float*>(side + i8g_side_bytes(p.r_mode));  // [2][256] unit scales
   float* cst = sc + 512;                                      // [256] C[n] of the current tile
   uint8_t* epi = reinterpret_cast<uint8_t*>(cst + 256);       // 8 x 2 KB store staging
   uint64_t* bars = reinterpret_cast<uint64_t*>(epi + kI8gEpiWarps * 1024);
   uint64_t* full = bars;                        // [S] leader: A + B (+ side) of both CTAs landed
-  uint64_t* empty = bars + kI8gStages;          // [S] both: the stage's MMAs are done
-  uint64_t* side_empty = bars + 2 * kI8gStages; // both: the R MMAs are done
+  uint64_t* empty = bars + kI8gMaxStages;       // [S] both: the stage's MMAs are done
+  uint64_t* side_empty = bars + 2 * kI8gMaxStages; // both: the R MMAs are done
   uint64_t* acc_full = side_empty + 1;          // [2] both: unit accumulator complete
   uint64_t* acc_empty = acc_full + 2;           // [2] leader: 16 epilogue warps drained it
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
@@ -107,7 +123,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
   const int n_tiles = tiles_m * tiles_n;
   const int my_tiles = cluster_id < n_tiles ? (n_tiles - 1 - cluster_id) / n_clusters + 1 : 0;
   const bool has_r = p.r_mode != kRNone;
-  const bool dense = p.r_mode == kRDense;
+  const bool split = p.r_mode == kRDenseSplit;
+  const bool dense = p.r_mode == kRDense || split;
   const int rch = (p.r + 63) / 64;  // dense R: 64-column bf16 atoms
   const int ks = p.k_steps;
   const int units = ks / p.gsteps + (has_r ? 1 : 0);  // per tile
@@ -120,7 +137,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
       tma_prefetch(&maps.r);
       tma_prefetch(&maps.xs);
     }
-    for (int s = 0; s < kI8gStages; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -151,13 +168,14 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
         const int m_own = mt * 256 + int(rank) * 128;
         const int n_half = nt * 256 + int(rank) * 128;
         for (int kk = 0; kk < ks; ++kk, ++g) {
-          const int s = g % kI8gStages;
-          mbar_wait(&empty[s], ((g / kI8gStages) & 1) ^ 1);
+          const int s = g % S;
+          mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
           const bool with_side = has_r && kk == 0;
           if (with_side && i > 0) mbar_wait(side_empty, (i - 1) & 1);
           const uint32_t fbar = map_rank(smem_u32(&full[s]), 0);
           const uint32_t st = sb + s * kI8gStage;
-          if (leader) mbar_expect_tx(&full[s], 2u * (kI8A + kI8B + (with_side ? (dense ? 2 * rch * 16384 : 16384) : 0)));
+          if (leader)
+            mbar_expect_tx(&full[s], 2u * (kI8A + kI8B + (with_side ? (dense ? (split ? 3 : 2) * rch * 16384 : 16384) : 0)));
           tma_load_2d_pair(st + kI8A, &maps.bp, fbar, kk * 128, n_half, kEvictNormal);
           tma_load_2d_pair(st, &maps.a, fbar, kk * 128, m_own, kEvictNormal);
           if (with_side) {
@@ -166,9 +184,11 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
               for (int h = 0; h < rch; ++h) {
                 tma_load_2d_pair(sside + h * 16384, &maps.xs, fbar, h * 64, m_own, kEvictNormal);
                 tma_load_2d_pair(sside + 32768 + h * 16384, &maps.r, fbar, h * 64, n_half, kEvictNormal);
+                if (split)  // lo plane: rows [N, 2N) of the same map
+                  tma_load_2d_pair(sside + 65536 + h * 16384, &maps.r, fbar, h * 64, p.N + n_half, kEvictNormal);
               }
             } else {
-              tma_load_2d_pair(sside + 32768, &maps.r, fbar, 0, n_half, kEvictNormal);
+              tma_load_2d_pair(sside, &maps.r, fbar, 0, n_half, kEvictNormal);
             }
           }
         }
@@ -190,8 +210,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
       };
       for (int i = 0; i < my_tiles; ++i) {
         for (int kk = 0; kk < ks; ++kk, ++g) {
-          const int s = g % kI8gStages;
-          mbar_wait_cluster(&full[s], (g / kI8gStages) & 1);
+          const int s = g % S;
+          mbar_wait_cluster(&full[s], (g / S) & 1);
           tc_fence_after();
           const uint32_t st = sb + s * kI8gStage;
           const uint64_t a = make_sdesc(st, 16, 1024, 2), b = make_sdesc(st + kI8A, 16, 1024, 2);
@@ -202,11 +222,12 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
               // K = 16 bf16 per MMA, four per 64-column atom
               for (int j = 0; j < (p.r + 15) / 16; ++j) {
                 const uint32_t off = uint32_t(j >> 2) * 16384u;
-                mma_bf16_pair(d, make_sdesc(sside + off, 16, 1024, 2) + 2 * (j & 3),
-                              make_sdesc(sside + 32768 + off, 16, 1024, 2) + 2 * (j & 3), id_r, j > 0 ? 1u : 0u);
+                const uint64_t ad = make_sdesc(sside + off, 16, 1024, 2) + 2 * (j & 3);
+                mma_bf16_pair(d, ad, make_sdesc(sside + 32768 + off, 16, 1024, 2) + 2 * (j & 3), id_r, j > 0 ? 1u : 0u);
+                if (split) mma_bf16_pair(d, ad, make_sdesc(sside + 65536 + off, 16, 1024, 2) + 2 * (j & 3), id_r, 1u);
               }
             } else {
-              const uint64_t br = make_sdesc(sside + 32768, 16, 1024, 2);
+              const uint64_t br = make_sdesc(sside, 16, 1024, 2);
               for (int j = 0; j < (p.r + 31) / 32; ++j) mma_i8_pair(d, a + 2 * j, br + 2 * j, id_main, j > 0 ? 1u : 0u);
             }
             tc_commit_pair(side_empty);

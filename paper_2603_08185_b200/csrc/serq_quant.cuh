@@ -872,6 +872,17 @@ __global__ void group_pack_kernel(const int32_t* __restrict__ src, int64_t K, in
   cterm[n] = float(c);
 }
 
+// f64 R [r, N] -> two bf16 planes [N, r]: hi = bf16(R), lo = bf16(R - hi)
+__global__ void dense_r_split_kernel(const double* __restrict__ src, int64_t r, int64_t N,
+                                     __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= r * N) return;
+  const int64_t n = t / r, j = t - n * r;
+  const double v = src[j * N + n];
+  const __nv_bfloat16 h = __double2bfloat16(v);
+  hi[n * r + j] = h;
+  lo[n * r + j] = __double2bfloat16(v - double(__bfloat162float(h)));
+}
 __global__ void dense_r_kernel(const double* __restrict__ src, int64_t r, int64_t N, __nv_bfloat16* __restrict__ dst) {
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= r * N) return;

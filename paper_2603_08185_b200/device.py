@@ -278,7 +278,10 @@ class IntLinear:
     output column (r_q, row groups of size r)."""
 
     def __init__(self, codes, scales, bits=4, r_dense=None, r_codes=None, r_scales=None, salient_idx=None,
-                 device="cuda", group_size=None):
+                 device="cuda", group_size=None, r_split=False):
+        """``r_split``: consume the dense R as bf16 hi + lo planes (relative error 2^-17) instead
+        of one bf16 plane -- for R matrices that carry a large share of the output (a GPTQ-swapped
+        R holds the salient rows themselves); served by the group-wise kernel (K <= 8192)."""
         device = torch.device(device)
         codes = _dev(codes, torch.int32, device)
         self.K, self.N = codes.shape
@@ -291,7 +294,7 @@ class IntLinear:
             raise ValidationError("integer main path needs scales [K/group_size, N] (one per output column and group)")
         scales = scales.reshape(-1).contiguous()
         if r_dense is not None:
-            self.r_mode = _lib.SERQ_R_DENSE
+            self.r_mode = _lib.SERQ_R_DENSE_SPLIT if r_split else _lib.SERQ_R_DENSE
             rd = _dev(r_dense, torch.float64, device)
             self.r = rd.shape[0]
             rdata, rs = rd, None
@@ -316,7 +319,7 @@ class IntLinear:
         self.device = device
 
     def xs_kind(self) -> int:
-        if self.r_mode == _lib.SERQ_R_DENSE:
+        if self.r_mode in (_lib.SERQ_R_DENSE, _lib.SERQ_R_DENSE_SPLIT):
             return 1
         if self.r_mode == _lib.SERQ_R_INT and not self.contiguous:
             return 2

@@ -24,7 +24,9 @@ if REF not in sys.path:
 from serq.compensate import (  # noqa: E402
     Compensator,
     OpProbe,
+    build_serq_gptq_swapped,
     build_serq_rtn,
+    default_r_config,
     build_svd_baseline,
     build_serq_rtn_mx,
     forward_reconstructed,
@@ -45,6 +47,7 @@ from serq.quantcore import (  # noqa: E402
     quantize_symmetric,
 )
 from serq.saliency import build_plan, score_rows  # noqa: E402
+from serq.gptq import GptqConfig, HessianState, accumulate_hessian  # noqa: E402
 from serq.tensorio import SyntheticSpec, gen_synthetic_activations  # noqa: E402
 from serq.flatten import compute_smoothing_scales  # noqa: E402
 from serq.tensorio import collect_calib_stats  # noqa: E402
@@ -200,6 +203,32 @@ def main():
     g["fsvd_aux"] = np.array(probe.aux_matmuls)
     g["fsvd_l1"], g["fsvd_l2"] = comp_s.l1, comp_s.l2
     g["fsvd_codes"], g["fsvd_scales"] = main_s.codes, main_s.scales
+
+    # -- group-wise INT weights (the paper's g = r = 128): reference builders
+    #    build_serq_rtn with row groups of 128 and build_serq_gptq_swapped (GPTQ group 128), R from
+    #    default_r_config (column groups: the float branch) or row groups of r (integer)
+    kg, ng, rg = 256, 96, 128
+    xg = bf16(np.random.default_rng(31).standard_normal((9, kg)) * 2)
+    wg = np.random.default_rng(32).standard_normal((kg, ng)) * 0.02
+    plan_g = build_plan(np.arange(kg, 0, -1.0), rg)  # salient rows = arange(r) (permuted layout)
+    wcfg_g = IntQuantConfig(4, True, 128, "row")
+    for tag, rcfg in (("col", default_r_config(ng, 4, 128)), ("int", IntQuantConfig(4, True, rg, "row"))):
+        mg, cg = build_serq_rtn(wg, plan_g, wcfg_g, rcfg)
+        g[f"fgrp_{tag}_codes"], g[f"fgrp_{tag}_scales"] = mg.codes, mg.scales
+        g[f"fgrp_{tag}_r_codes"], g[f"fgrp_{tag}_r_scales"] = cg.r_q.codes, cg.r_q.scales
+        probe = OpProbe()
+        g[f"fgrp_{tag}_y_a8"] = forward_reconstructed(xg, mg, cg, per_token_config(8), probe)
+        g[f"fgrp_{tag}_aux"] = np.array(probe.aux_matmuls)
+        _, parts = int_gemm_reference(quantize_asymmetric(xg, per_token_config(8)), mg, return_partials=True)
+        g[f"fgrp_{tag}_acc_a8"] = np.stack([acc for _, acc in parts])
+    calib_g = np.random.default_rng(33).standard_normal((64, kg))
+    hess = accumulate_hessian(HessianState.zeros(kg), calib_g)
+    mq, cq = build_serq_gptq_swapped(wg, plan_g, GptqConfig(4, 128), default_r_config(ng, 4, 128), hess)
+    g["fgptq_codes"], g["fgptq_scales"] = mq.codes, mq.scales
+    g["fgptq_r_codes"], g["fgptq_r_scales"] = cq.r_q.codes, cq.r_q.scales
+    for bits in (4, 8):
+        g[f"fgptq_y_a{bits}"] = forward_reconstructed(xg, mq, cq, per_token_config(bits))
+    g["fgrp_x"], g["fgrp_w"] = xg, wg
 
     # -- a small bundle written by the reference's own save_bundle (bundleio.py:73-126), for the
     #    device bundle loader: MX main + MX R, INT main + INT R, INT main + SVD factors

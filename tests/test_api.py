@@ -48,8 +48,13 @@ def test_layouts_integer_cores_cannot_evaluate_are_rejected():
     # per-row (per input channel) main scales vary along K
     main = api.QuantizedTensor(np.zeros((8, 4), np.int32), np.ones((8, 1)), None,
                                api.IntQuantConfig(4, True, "per-row"), (8, 4))
-    with pytest.raises(ValidationError, match="reduction dimension"):
+    with pytest.raises(ValidationError, match="GPU-native"):
         api.SerqLinear(main, None, api.per_token_config(8))
+    # row groups that are not a multiple of 128 (or above 1024) are rejected too
+    main_g = api.QuantizedTensor(np.zeros((256, 8), np.int32), np.ones((4, 8)), None,
+                                 api.IntQuantConfig(4, True, 64, "row"), (256, 8))
+    with pytest.raises(ValidationError, match="GPU-native"):
+        api.SerqLinear(main_g, None, api.per_token_config(8))
     with pytest.raises(ValidationError):
         api.forward_reconstructed(np.ones((2, 8)), main, None, api.per_token_config(8))
 
@@ -239,3 +244,34 @@ def test_serq_beats_rtn_and_rank_monotone(gpu):
         y = api.forward_reconstructed(x, main_t, comp if r else None, None)
         errs.append(np.linalg.norm(y - exact) / np.linalg.norm(exact))
     assert errs[0] > errs[1] > errs[2], errs
+
+
+@pytest.mark.gpu
+def test_forward_reconstructed_grouped_and_gptq_golden(gpu, golden):
+    # group-wise INT weights through the drop-in: RTN with row groups of 128 (default_r_config
+    # R and integer R) and the GPTQ-swapped artefacts, all built by the reference
+    xg, wg = golden["fgrp_x"], golden["fgrp_w"]
+    k, n = wg.shape
+    r = 128
+    plan = type("Plan", (), {"scores": np.arange(k, 0, -1.0), "rank": r, "salient_idx": np.arange(r)})()
+    for tag, rcfg in (("col", api.IntQuantConfig(4, True, 96, "col")), ("int", api.IntQuantConfig(4, True, r, "row"))):
+        main, comp = api.build_serq_rtn(wg, plan, api.IntQuantConfig(4, True, 128, "row"), rcfg)
+        # the device quantizers reproduce the reference artefacts bit for bit
+        assert np.array_equal(main.codes, golden[f"fgrp_{tag}_codes"])
+        assert np.array_equal(main.scales, golden[f"fgrp_{tag}_scales"])
+        assert np.array_equal(comp.r_q.codes, golden[f"fgrp_{tag}_r_codes"])
+        assert np.array_equal(comp.r_q.scales, golden[f"fgrp_{tag}_r_scales"])
+        probe = api.OpProbe()
+        y = api.forward_reconstructed(xg, main, comp, api.per_token_config(8), probe)
+        assert probe.aux_matmuls == int(golden[f"fgrp_{tag}_aux"])
+        mx, mean = O.parity_errors(y, golden[f"fgrp_{tag}_y_a8"])
+        assert mx <= TOL_MAX and mean <= TOL_MEAN, (tag, mx, mean)
+    main = api.QuantizedTensor(golden["fgptq_codes"], golden["fgptq_scales"], None,
+                               api.IntQuantConfig(4, True, 128, "row"), (k, n))
+    rq = api.QuantizedTensor(golden["fgptq_r_codes"], golden["fgptq_r_scales"], None,
+                             api.IntQuantConfig(4, True, 96, "col"), (r, n))
+    comp = api.Compensator(api.GPTQ_SWAPPED, r, np.arange(r), r_q=rq)
+    for bits in (4, 8):
+        y = api.forward_reconstructed(xg, main, comp, api.per_token_config(bits))
+        mx, mean = O.parity_errors(y, golden[f"fgptq_y_a{bits}"])
+        assert mx <= TOL_MAX and mean <= TOL_MEAN, (bits, mx, mean)

@@ -237,13 +237,15 @@ def test_int_linear_gather_int_r(D):
     (600, 3072, 512, 1024, 32, 8, False, "int"),
     (256, 2048, 512, 128, 128, 8, False, "col"),    # the paper's g = r = 128 with default_r_config R
     (130, 1024, 776, 256, 96, 4, False, "dense"),
+    (300, 1024, 512, 128, 128, 8, False, "split"),  # dequantize(col-grouped R) as bf16 hi + lo
+    (64, 2048, 256, 2048, 64, 8, False, "split"),   # one group spanning K: the split R on a per-channel main
 ])
 def test_int_grouped_linear_parity(D, M, K, N, g, r, bits, symmetric, r_mode):
     # int_gemm_reference row-grouped branch: one exact integer partial per group
     # (acc_dump [G, M, N]), promoted with the group's scales in fp32
     x = _bf16_outlier_x(M, K, seed=M + g)
     w = np.random.default_rng(K + g).standard_normal((K, N)) * 0.02
-    main, comp = O.build_grouped_int(w, np.arange(r), g, 4, "int" if r_mode == "none" else r_mode)
+    main, comp = O.build_grouped_int(w, np.arange(r), g, 4, {"none": "int", "split": "col"}.get(r_mode, r_mode))
     if r_mode == "none":
         comp = None
     kw = {}
@@ -251,6 +253,8 @@ def test_int_grouped_linear_parity(D, M, K, N, g, r, bits, symmetric, r_mode):
         kw = dict(r_dense=comp.r_dense, salient_idx=np.arange(r))
     elif r_mode == "col":
         kw = dict(r_dense=O.dequantize(comp.r_q), salient_idx=np.arange(r))
+    elif r_mode == "split":
+        kw = dict(r_dense=O.dequantize(comp.r_q), salient_idx=np.arange(r), r_split=True)
     elif r_mode == "int":
         kw = dict(r_codes=comp.r_q.codes, r_scales=comp.r_q.scales, salient_idx=np.arange(r))
     lin = D.IntLinear(main.codes, main.scales, 4, group_size=g, **kw)

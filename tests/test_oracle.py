@@ -93,6 +93,28 @@ def test_int_forward_matches_reference_golden(golden):
     np.testing.assert_array_equal(y, golden["fint_y_dense_a8"])
 
 
+def test_grouped_int_builder_and_forward_match_reference_golden(golden):
+    # build_serq_rtn with row groups of 128 and the GPTQ-swapped forward
+    xg, wg = golden["fgrp_x"], golden["fgrp_w"]
+    k, n = wg.shape
+    for tag in ("col", "int"):
+        main, comp = O.build_grouped_int(wg, np.arange(128), 128, 4, tag)
+        assert np.array_equal(main.codes, golden[f"fgrp_{tag}_codes"])
+        assert np.array_equal(main.scales, golden[f"fgrp_{tag}_scales"])
+        assert np.array_equal(comp.r_q.codes, golden[f"fgrp_{tag}_r_codes"])
+        assert np.array_equal(comp.r_q.scales, golden[f"fgrp_{tag}_r_scales"])
+        y, xq = O.forward_int(xg, main, comp, O.IntCfg(8, False, "per-row"))
+        np.testing.assert_allclose(y, golden[f"fgrp_{tag}_y_a8"], rtol=1e-12, atol=1e-12)
+        _, parts = O.int_gemm(xq, main, return_partials=True)
+        assert np.array_equal(np.stack([a for _, a in parts]), golden[f"fgrp_{tag}_acc_a8"])
+    main = O.IntQ(golden["fgptq_codes"], golden["fgptq_scales"], None, O.IntCfg(4, True, 128, "row"), (k, n))
+    rq = O.IntQ(golden["fgptq_r_codes"], golden["fgptq_r_scales"], None, O.default_r_config(n, 4, 128), (128, n))
+    comp = O.Comp(128, np.arange(128), r_q=rq)
+    for bits in (4, 8):
+        y, _ = O.forward_int(xg, main, comp, O.IntCfg(bits, False, "per-row"))
+        np.testing.assert_allclose(y, golden[f"fgptq_y_a{bits}"], rtol=1e-12, atol=1e-12)
+
+
 def test_svd_baseline_forward_matches_reference_golden(golden):
     # build_svd_baseline main is per-output-channel INT4 (compensate.py:209-224); the
     # forward adds (dequantize(xq) @ L1) @ L2 (compensate.py:304-310), two aux products
