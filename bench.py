@@ -336,6 +336,8 @@ def other_configs(hbm_gbs: float) -> dict:
     try:
         out["c1_int4_sym_dense_L"] = B.int_linear_point(512, 4096, 4096, 64, "dense", 4, True, fl)
         out["c3_w4a8_asym_int_R"] = B.int_linear_point(2048, 4096, 11008, 128, "int", 8, False, fl)
+        # the paper's group-wise weights (row groups of 128 along K) at C3's shape
+        out["c3_w4a8_group128_int_R"] = B.int_linear_point(2048, 4096, 11008, 128, "int", 8, False, fl, group=128)
         # the paper's comparison at C3's shape: SVD baseline (two-factor L1 L2, r = 128) vs SERQ's fused R
         out["c3_svd_baseline_r128"] = B.svd_baseline_point(2048, 4096, 11008, 128)
         out["c4_decode"] = B.decode_points(hbm_gbs)

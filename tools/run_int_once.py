@@ -3,7 +3,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2603_08185_b200 import benchmarks as B
-lin = B.device_int_linear(4096, 11008, 128, "int")
+g = int(os.environ.get("GROUP", "0")) or None  # GROUP=128: group-wise weights
+lin = B.device_int_linear(4096, 11008, 128, "int", group=g)
 x = B.outlier_x(2048, 4096, frac=0.005, mag=100.0)
 act = lin.quantize(x, 8, False)
 y = torch.empty((2048, 11008), dtype=torch.bfloat16, device="cuda")
