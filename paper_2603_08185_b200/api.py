@@ -350,11 +350,11 @@ class SerqLinear:
                 raise ValidationError("activations must be quantized per token ('per-row')")
             axis, gs = _groups(main.config, main.shape)
             k = main.shape[0]
-            if not (axis == ROW_GROUPS and (gs == k or (gs % 128 == 0 and gs <= 1024))) or main.zero_points is not None:
+            if not (axis == ROW_GROUPS and (gs == k or (gs % 128 == 0 and gs <= 8192))) or main.zero_points is not None:
                 raise ValidationError(
                     f"integer main layout (group_size={main.config.group_size!r}, axis={main.config.axis!r}) is not "
                     "GPU-native: scales must be symmetric per output column (group_size == K, axis 'row') or per "
-                    "(row group, output column) with group_size a multiple of 128 up to 1024 (SURVEY F12)")
+                    "(row group, output column) with group_size a multiple of 128 up to 8192 (SURVEY F12)")
             kw = {}
             if has_r:
                 if comp.r_dense is not None:

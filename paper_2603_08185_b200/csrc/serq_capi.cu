@@ -259,7 +259,21 @@ static int act_quant_mx_impl(const void* x, int dtype, int64_t M, int64_t K, int
     dim3 grid(unsigned(cdiv(int64_t(kc) * 16, 256)), unsigned(cdiv(m_rows, kMxRows)), gather_idx ? 2u : 1u);
     while (gather_idx && int64_t(grid.x) * grid.y * 256 < g_threads) ++grid.y;  // the z = 1 plane must cover it
     const MxGather mg{gather_idx, r, xs_codes, xs_sf, krc};
-    if (dtype == SERQ_BF16) {
+    if (dtype == SERQ_BF16 && !(g_debug_flags & (1 << 30))) {
+      // one thread per 32-block (measured best against 2 and 4 rows per thread, tools/quant_probe.py:
+      // 4096^2 8.1 / 8.8 / 10.8 us); debug flag 1<<30: the 8-elements-per-thread kernel (9.9 us)
+      const int kR = (g_debug_flags & (1 << 21)) ? 4 : (g_debug_flags & (1 << 22)) ? 2 : 1;  // diagnostics
+      const int64_t main_blocks = cdiv(cdiv(m_rows, kR) * int64_t(kc) * 4, 256);
+      const dim3 gb(unsigned(main_blocks > cdiv(g_threads, 256) ? main_blocks : cdiv(g_threads, 256)), 1u,
+                    gather_idx ? 2u : 1u);
+      const auto* xb = static_cast<const __nv_bfloat16*>(x);
+      if (kR == 4)
+        CK(launch_pdl(mx_encode_blk_kernel<4>, gb, dim3(256), 0, st, xb, int(M), int(K), ldx, codes, sf, kc, mg));
+      else if (kR == 1)
+        CK(launch_pdl(mx_encode_blk_kernel<1>, gb, dim3(256), 0, st, xb, int(M), int(K), ldx, codes, sf, kc, mg));
+      else
+        CK(launch_pdl(mx_encode_blk_kernel<2>, gb, dim3(256), 0, st, xb, int(M), int(K), ldx, codes, sf, kc, mg));
+    } else if (dtype == SERQ_BF16) {
       CK(launch_pdl(mx_encode_fast_kernel<__nv_bfloat16>, grid, dim3(256), 0, st, static_cast<const __nv_bfloat16*>(x),
                     int(M), int(K), ldx, codes, sf, kc, mg));
     } else {

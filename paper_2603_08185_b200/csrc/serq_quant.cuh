@@ -74,6 +74,11 @@ __device__ __forceinline__ uint32_t canon_neg_zero(uint32_t p) {
   const uint32_t z = ~(mag | (mag >> 1) | (mag >> 2)) & 0x11111111u;
   return p & ~(z << 3);
 }
+// the same in three ops: bit 3 of (mag + 7) per nibble is (mag != 0), no carry between nibbles
+__device__ __forceinline__ uint32_t canon_neg_zero3(uint32_t p) {
+  const uint32_t b = (p & 0x77777777u) + 0x77777777u;
+  return p & (b | 0x77777777u);
+}
 __device__ __forceinline__ uint32_t cvt_e2m1x2(float even, float odd) {
   return canon_neg_zero(cvt_e2m1x2_raw(even, odd));
 }
@@ -224,6 +229,88 @@ __device__ __forceinline__ void mx_encode_gather_part(const T* __restrict__ x, i
   for (int i = 0; i < 4; ++i) packed |= cvt_e2m1x2(v[2 * i] * inv, v[2 * i + 1] * inv) << (8 * i);
   if (row_ok) *reinterpret_cast<uint32_t*>(g.xs_codes + row * (g.r / 2) + c0 / 2) = packed;
   if ((threadIdx.x & 3) == 0) g.xs_sf[sf_offset(row, c0 / 32, g.kc_pad_r)] = uint8_t(e + 127);
+}
+
+// max(|a|, |b|) per bf16 lane (sign = xor of the signs; only the magnitude is used)
+__device__ __forceinline__ uint32_t bf16x2_absmax(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.xorsign.abs.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+// K1-MX for bf16 input, one thread per (32-block, kR rows): the block amax needs no
+// shuffles, the exponent is computed once per block, codes leave as one 16-B store and
+// the scale factor as one byte.  Bit-identical to mx_encode_fast_kernel (same exponent,
+// scaling and RNE conversion); ~half the ALU work per element, which bounds that kernel.
+// The grid covers the scale-factor padding (rows up to the 128-row block, blocks up to
+// kc_pad chunks) with the finite scale of a zero block, as mx_encode_fast_kernel does.
+template <int kR>
+__global__ void __launch_bounds__(256) mx_encode_blk_kernel(const __nv_bfloat16* __restrict__ x, int M, int K,
+                                                            int64_t ldx, uint8_t* __restrict__ codes,
+                                                            uint8_t* __restrict__ sf, int kc_pad,
+                                                            MxGather gather = MxGather{}) {
+  if (blockIdx.z == 1) {
+    pdl_launch_dependents();
+    pdl_wait();
+    mx_encode_gather_part<__nv_bfloat16>(x, M, ldx, gather);
+    return;
+  }
+  const int nbp = kc_pad * 4;  // 32-blocks per row including the SF chunk padding
+  const int64_t id = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  const int kb = int(id % nbp);
+  const int r0 = int(id / nbp) * kR;
+  const int m_sf = ((M + 127) >> 7) << 7;
+  pdl_launch_dependents();  // the linear may start streaming its weights now
+  pdl_wait();               // x comes from the previous kernel
+  if (r0 >= m_sf) return;
+  const bool col_ok = kb * 32 < K;  // K % 32 == 0: blocks are all in or all out
+  uint4 raw[kR][4];
+#pragma unroll
+  for (int rr = 0; rr < kR; ++rr) {
+    const bool ok = col_ok && r0 + rr < M;
+    const uint4* src = reinterpret_cast<const uint4*>(x + int64_t(r0 + rr) * ldx + kb * 32);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) raw[rr][c] = ok ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int rr = 0; rr < kR; ++rr) {
+    const int row = r0 + rr;
+    uint32_t w[16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      w[4 * c] = raw[rr][c].x;
+      w[4 * c + 1] = raw[rr][c].y;
+      w[4 * c + 2] = raw[rr][c].z;
+      w[4 * c + 3] = raw[rr][c].w;
+    }
+    uint32_t m8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m8[i] = bf16x2_absmax(w[2 * i], w[2 * i + 1]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) m8[i] = bf16x2_absmax(m8[2 * i], m8[2 * i + 1]);
+    m8[0] = bf16x2_absmax(bf16x2_absmax(m8[0], m8[1]), bf16x2_absmax(m8[2], m8[3]));
+    m8[0] = bf16x2_absmax(m8[0], __byte_perm(m8[0], 0, 0x1032));  // both halves
+    const uint32_t amax = m8[0] & 0x7FFFu;
+    // mx_block_exp_bf16bits without branches: 0 for a zero block, else max(ef, 2) - 129
+    const int ef = int(amax >> 7);
+    const int e = amax ? max(ef, 2) - 129 : 0;
+    const float inv = __uint_as_float(uint32_t(127 - e) << 23);
+    uint32_t pk[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t packed = 0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const uint32_t wv = w[4 * k + h];
+        packed |= cvt_e2m1x2_raw(__uint_as_float(wv << 16) * inv, __uint_as_float(wv & 0xFFFF0000u) * inv)
+                  << (8 * h);
+      }
+      pk[k] = canon_neg_zero3(packed);
+    }
+    if (col_ok && row < M)
+      *reinterpret_cast<uint4*>(codes + int64_t(row) * (K >> 1) + kb * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    if (row < m_sf) sf[sf_offset(row, kb, kc_pad)] = uint8_t(e + 127);
+  }
 }
 
 template <typename T, int kMxRows = serq::kMxRows>

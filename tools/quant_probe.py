@@ -11,7 +11,7 @@ for (M, K) in [(4096, 4096), (2048, 4096), (8192, 8192), (8192, 28672), (16, 409
     xs = [B.outlier_x(M, K, seed=i) for i in range(nx)]
     acts = [D.quantize_mx(x) for x in xs]
     out = {"M": M, "K": K}
-    for f in (0,):
+    for f in (0, 1 << 22, 1 << 30):
         _lib.load().serq_set_debug_flags(f)
         t = B.time_steps(lambda i: D.quantize_mx(xs[i % nx], None, acts[i % nx]), 16) * 1e-3
         byts = 2 * M * K + M * K / 2 + M * K / 32
