@@ -310,16 +310,28 @@ int serq_act_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t l
   const dim3 grid(static_cast<unsigned>(M));
   if (dtype == SERQ_BF16 && K % 8 == 0 && K <= 8192 && ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(codes) & 7) == 0) {
-    // one token row per 256-thread CTA (measured faster than 2 rows per CTA for K = 4096)
+    // one token row per SMALL CTA: the per-row chain (load, min/max reduction, f64 scale,
+    // codes) is latency-bound, so many resident rows per SM matter more than wide rows
+    // (tools/int_quant_probe.py, C3 2048 x 4096: 12.3 us with 256 threads per row, 5.2 with 64)
     const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
-    const int cpt = int(cdiv(K / 8, 256));
     const dim3 gq{unsigned(M)};
-#define SERQ_INTQ(P, C)                                                                                          \
-  CK(launch_pdl(int_quant_bf16_kernel<P, C>, gq, dim3(256), 0, st, xb, int(M), int(K), ldx, bits, symmetric, codes, \
+    const bool warp_rows = (g_debug_flags & (1 << 21)) != 0;  // diagnostics: one warp per row
+    const int tpr = warp_rows ? 32 : 64;
+    const int cpt = int(cdiv(K / 8, tpr));
+#define SERQ_INTQ(P, C)                                                                                         \
+  CK(launch_pdl(int_quant_bf16_kernel<P, C, P>, gq, dim3(P), 0, st, xb, int(M), int(K), ldx, bits, symmetric, codes, \
                 scale64, scale32, zp, salient_idx, r, xs_out, xs_kind))
-    if (cpt <= 1) SERQ_INTQ(256, 1);
-    else if (cpt <= 2) SERQ_INTQ(256, 2);
-    else SERQ_INTQ(256, 4);
+    if (warp_rows) {
+      if (cpt <= 4) SERQ_INTQ(32, 4);
+      else if (cpt <= 8) SERQ_INTQ(32, 8);
+      else if (cpt <= 16) SERQ_INTQ(32, 16);
+      else SERQ_INTQ(32, 32);
+    } else {
+      if (cpt <= 2) SERQ_INTQ(64, 2);
+      else if (cpt <= 4) SERQ_INTQ(64, 4);
+      else if (cpt <= 8) SERQ_INTQ(64, 8);
+      else SERQ_INTQ(64, 16);
+    }
 #undef SERQ_INTQ
     LAUNCH_CHECK("int_quant_bf16");
     return SERQ_OK;

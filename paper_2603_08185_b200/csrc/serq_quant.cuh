@@ -752,14 +752,45 @@ __global__ void __launch_bounds__(256) int_quant_kernel(const T* __restrict__ x,
 // thread keeps its kCpt 16-B chunks in registers (one HBM read); row min / max by
 // shuffles + a per-row shared-memory step; scale / zero point in f64 by one thread
 // per row exactly as the reference (quantcore.py:108-137); codes through int_code.
-template <int kTpr, int kCpt>
-__global__ void __launch_bounds__(256) int_quant_bf16_kernel(const __nv_bfloat16* __restrict__ x, int M, int K,
+// the exact path of int_code for the flagged elements (out of line: one copy of the f64
+// division instead of one per unrolled element)
+// clip(rint(x / s) + zp) exactly as the reference's f64 expression, for an element the
+// fp32 fast path flagged.  Near a .5 tie h = k + 1/2 the answer follows from the sign of
+// the exact residual r = RN(x - h*s) (one DFMA; x, h exact): r == 0 means x / s == h and
+// rint picks the even neighbour; |r| > 2 * (ulp(h)/2) * s means the f64 quotient cannot
+// round onto h, so the sign decides.  Only the razor-thin rest (and |x/s| >= 2^21) pays
+// the correctly rounded f64 division.  This GPU's FP64 pipe is slow: one DFMA instead
+// of a DDIV keeps a flagged row off the kernel's critical path.
+__device__ __forceinline__ int int_code_tie(float xf, double s, float inv32, int zp, int qmin, int qmax) {
+  const float q = xf * inv32;  // only steers toward the nearby half-integer
+  double k;
+  const float n = rintf(q);
+  if (fabsf(q) < 0x1p21f) {
+    const double h = double(n) + (q - n >= 0.f ? 0.5 : -0.5);
+    const double r = fma(-h, s, double(xf));
+    if (r == 0.0) {
+      const double lo = h - 0.5;
+      k = (int(lo) & 1) == 0 ? lo : lo + 1.0;  // |lo| < 2^21
+    } else {
+      int eh;
+      frexp(h, &eh);  // |h| in [2^(eh-1), 2^eh): ulp(h) = 2^(eh - 53)
+      const double half_ulp_s = ldexp(s, eh - 54);
+      k = fabs(r) > 2.0 * half_ulp_s ? (r > 0.0 ? h + 0.5 : h - 0.5) : rint(double(xf) / s);
+    }
+  } else {
+    k = rint(double(xf) / s);
+  }
+  return int(fmin(fmax(k + double(zp), double(qmin)), double(qmax)));
+}
+
+template <int kTpr, int kCpt, int kBlock = 256>
+__global__ void __launch_bounds__(kBlock) int_quant_bf16_kernel(const __nv_bfloat16* __restrict__ x, int M, int K,
                                                              int64_t ldx, int bits, int symmetric,
                                                              int8_t* __restrict__ codes, double* __restrict__ scale64,
                                                              float* __restrict__ scale32, int32_t* __restrict__ zp_out,
                                                              const int32_t* __restrict__ sidx, int r,
                                                              void* __restrict__ xs_out, int xs_kind) {
-  constexpr int kRows = 256 / kTpr, kWarps = kTpr / 32;
+  constexpr int kRows = kBlock / kTpr, kWarps = kTpr / 32;
   __shared__ float red_lo[kRows][kWarps], red_hi[kRows][kWarps];
   __shared__ double s_scale[kRows];
   __shared__ float s_inv32[kRows];
@@ -830,20 +861,55 @@ __global__ void __launch_bounds__(256) int_quant_bf16_kernel(const __nv_bfloat16
   const int qmax = symmetric ? (1 << (bits - 1)) - 1 : (1 << bits) - 1;
   const int qmin = symmetric ? -qmax : 0;
   uint2* out = reinterpret_cast<uint2*>(codes + row * K);
+  // fast path for every element (FP32 / integer pipes); the rare elements within the
+  // margin of a .5 tie (or with |x/s| >= 2^21) are fixed afterwards by ONE rolled loop
+  // that re-reads them and overwrites their code byte with the correctly rounded f64
+  // result (inlining the f64 division per unrolled element made this kernel
+  // instruction-bound; an out-of-line call forced the register arrays to the stack)
+  // Everything on the FP32 / ALU pipes, no F2I / FRND (conversion-pipe) instructions:
+  // n = rint(q) by the 1.5*2^23 magic add (|q| < 2^21), the code byte from the low
+  // mantissa bits of (clamp(n + zp) + 1.5*2^23).
+  constexpr float kMagic = 12582912.f;
+  const float zpf = float(zp), qminf = float(qmin), qmaxf = float(qmax);
+  constexpr int kBadWords = (8 * kCpt + 63) / 64;
+  uint64_t bad[kBadWords];  // bit 8j+i: element i of group j takes the exact path
+#pragma unroll
+  for (int b = 0; b < kBadWords; ++b) bad[b] = 0;
 #pragma unroll
   for (int j = 0; j < kCpt; ++j) {
-    const int c8 = t + j * kTpr;
-    if (c8 >= n8) continue;
     const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
-    uint32_t packed[2] = {0u, 0u};
+    uint32_t cb[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const uint32_t hbits = (i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16);
-      const __nv_bfloat16 xv = __ushort_as_bfloat16(static_cast<unsigned short>(hbits >> 16));
-      const int q = int_code<__nv_bfloat16>(xv, sc, inv32, zp, qmin, qmax);
-      packed[i >> 2] |= (uint32_t(q) & 0xFFu) << (8 * (i & 3));
+      const float xf = __uint_as_float((i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16));
+      const float q = xf * inv32;             // |q - x/s| <= |q| * 2^-22.9
+      const float n = (q + kMagic) - kMagic;  // rint(q), exact for |q| < 2^22
+      const float d = q - n;                  // exact, |d| <= 1/2
+      // not within the margin of a .5 tie: |d| + |q| 2^-21 < 1/2 (also excludes |q| >= 2^21,
+      // where the bound analysis stops)
+      const bool ok = fmaf(fabsf(q), 0x1p-21f, fabsf(d)) < 0.5f;
+      bad[(8 * j + i) >> 6] |= uint64_t(!ok) << ((8 * j + i) & 63);
+      const float c = fminf(fmaxf(n + zpf, qminf), qmaxf);
+      cb[i] = __float_as_uint(c + kMagic);  // low byte = two's-complement code
     }
-    out[c8] = make_uint2(packed[0], packed[1]);
+    const uint2 v = make_uint2(__byte_perm(__byte_perm(cb[0], cb[1], 0x0040), __byte_perm(cb[2], cb[3], 0x0040), 0x5410),
+                               __byte_perm(__byte_perm(cb[4], cb[5], 0x0040), __byte_perm(cb[6], cb[7], 0x0040), 0x5410));
+    const int c8 = t + j * kTpr;
+    if (c8 < n8) out[c8] = v;
+  }
+  // the flagged elements only (typically none: a row's slowest thread bounds the kernel, so
+  // no pass over all elements): re-read, exact code, overwrite the byte
+#pragma unroll
+  for (int b = 0; b < kBadWords; ++b) {
+    uint64_t m = bad[b];
+#pragma unroll 1
+    while (m) {
+      const int bit = __ffsll(static_cast<long long>(m)) - 1;
+      m &= m - 1;
+      const int e = 64 * b + bit;  // 8j + i; out-of-range groups hold zeros, which never flag
+      const int col = (t + (e >> 3) * kTpr) * 8 + (e & 7);
+      codes[row * K + col] = int8_t(int_code_tie(__bfloat162float(x[row * ldx + col]), sc, inv32, zp, qmin, qmax));
+    }
   }
   if (xs_kind != 0) {
     // salient slice from this row's codes (written above by this row's threads)

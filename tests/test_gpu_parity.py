@@ -107,6 +107,40 @@ def test_int_quant_bitexact(D, bits, symmetric, dtype):
     assert np.array_equal(codes, ref.codes)
 
 
+@pytest.mark.parametrize("K", [1024, 4096, 8192])
+def test_int_quant_exact_ties(D, K):
+    # rows built so that x / s lands EXACTLY on k + 1/2 for many elements (s a power of two),
+    # plus values a few ulps off the ties: the fast path must hand every one of them to the
+    # exact path and reproduce rint's half-to-even (quantcore.py:116, 131-132)
+    rng = np.random.default_rng(K)
+    M = 96
+    x = np.zeros((M, K))
+    for m in range(M):
+        e = -int(rng.integers(2, 9))
+        if m % 2 == 0:  # asymmetric A8: lo = 0, hi = 255 * 2^e -> s = 2^e
+            ties = (rng.integers(0, 127, K) + 0.5) * 2.0**e
+            x[m] = ties
+            x[m, 0], x[m, 1] = 0.0, 255 * 2.0**e
+        else:  # symmetric A4: amax = 7 * 2^e -> s = 2^e
+            ties = (rng.integers(-6, 6, K) + 0.5) * 2.0**e
+            x[m] = ties
+            x[m, 0] = 7 * 2.0**e
+        near = rng.random(K) < 0.1  # neighbours of the ties (next bf16 up / down)
+        x[m, near] = np.nextafter(x[m, near].astype(np.float32), np.float32(np.inf)).astype(np.float64)
+    x = O.bf16_round(x)
+    xt = _cuda(x, torch.bfloat16)
+    for sym, bits, rows in ((False, 8, slice(0, None, 2)), (True, 4, slice(1, None, 2))):
+        xr = np.ascontiguousarray(x[rows])
+        act = D.quantize_int(_cuda(xr, torch.bfloat16), bits, sym)
+        cfg = O.IntCfg(bits, sym, "per-row")
+        ref = O.quantize_symmetric(xr, cfg) if sym else O.quantize_asymmetric(xr, cfg)
+        codes = act.codes.cpu().numpy()
+        codes = codes.astype(np.int32) if sym else codes.view(np.uint8).astype(np.int32)
+        assert np.array_equal(act.scale64.cpu().numpy(), ref.scales[:, 0])
+        assert np.array_equal(codes, ref.codes), int((codes != ref.codes).sum())
+    del xt
+
+
 def test_int_quant_golden(D, golden):
     for i in range(int(golden["q_count"])):
         x = golden[f"q_x_{i}"]

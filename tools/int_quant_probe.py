@@ -3,7 +3,7 @@ import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_08185_b200 import _lib, benchmarks as B, device as D
 
-for f in (0,):
+for f in (0, 1 << 21):
   _lib.load().serq_set_debug_flags(f)
   for (M, K, bits, sym) in [(512, 4096, 4, True), (2048, 4096, 8, False), (8192, 8192, 8, False), (4096, 4096, 4, False)]:
     xs = [B.outlier_x(M, K, seed=i) for i in range(8)]
