@@ -974,9 +974,9 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     const int64_t max_pairs = sm_count() / 2;
     const dim3 grid(unsigned(2 * (tiles < max_pairs ? tiles : max_pairs)));
     if (acc_dump || accr_dump)
-      serq_i8g_pair_kernel<true><<<grid, kI8gThreads, i8g_smem(h->r_mode), S(stream)>>>(im, p);
+      CK(launch_pdl(serq_i8g_pair_kernel<true>, grid, dim3(kI8gThreads), i8g_smem(h->r_mode), S(stream), im, p));
     else
-      serq_i8g_pair_kernel<false><<<grid, kI8gThreads, i8g_smem(h->r_mode), S(stream)>>>(im, p);
+      CK(launch_pdl(serq_i8g_pair_kernel<false>, grid, dim3(kI8gThreads), i8g_smem(h->r_mode), S(stream), im, p));
     LAUNCH_CHECK("serq_i8g_pair_kernel");
     return SERQ_OK;
   }
@@ -1026,10 +1026,13 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     const int64_t tiles = cdiv(M, 256) * cdiv(h->N, kBN);
     const int64_t max_pairs = sm_count() / 2;
     const dim3 grid(unsigned(2 * (tiles < max_pairs ? tiles : max_pairs)));
+    // launched with programmatic dependent launch: the prologue and the first weight stages
+    // overlap the activation quantizer's tail
     if (widen)
-      serq_i8_pair_kernel<false><<<grid, I8Cfg<false>::kThreads, I8Cfg<false>::kSmem, S(stream)>>>(im, p);
+      CK(launch_pdl(serq_i8_pair_kernel<false>, grid, dim3(I8Cfg<false>::kThreads), I8Cfg<false>::kSmem, S(stream), im,
+                    p));
     else
-      serq_i8_pair_kernel<true><<<grid, I8Cfg<true>::kThreads, I8Cfg<true>::kSmem, S(stream)>>>(im, p);
+      CK(launch_pdl(serq_i8_pair_kernel<true>, grid, dim3(I8Cfg<true>::kThreads), I8Cfg<true>::kSmem, S(stream), im, p));
     LAUNCH_CHECK("serq_i8_pair_kernel");
     return SERQ_OK;
   }

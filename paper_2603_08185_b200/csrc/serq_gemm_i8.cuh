@@ -176,6 +176,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
     // ------------------------------------------------------------ producer (both CTAs)
     if (elect_one()) {
       const uint32_t sb = smem_u32(smem), sside = smem_u32(side);
+      // programmatic dependent launch: the first tile's weight stages do not depend on the
+      // previous kernel (the activation quantizer) -- stream them before griddepcontrol.wait
+      const int pre = kDirect && my_tiles > 0 ? (ks < kI8Stages ? ks : kI8Stages) : 0;
+      if (my_tiles > 0) {
+        const int n_half0 = (cluster_id / tiles_m) * kBN + int(rank) * 128;
+        for (int kk = 0; kk < pre; ++kk) {
+          const bool with_side = has_r && kk == 0;
+          if (leader)
+            mbar_expect_tx(&full[kk], 2u * (kI8A + kI8B + (with_side ? (dense ? 2 * 16384 : 16384) : 0)));
+          tma_load_2d_pair(sb + kk * kI8Stage + kI8A, &maps.bp, map_rank(smem_u32(&full[kk]), 0), kk * 128, n_half0,
+                           kEvictNormal);
+        }
+      }
+      pdl_wait();
       uint32_t g = 0;
       for (int i = 0; i < my_tiles; ++i) {
         const int tile = cluster_id + i * n_clusters;
@@ -184,15 +198,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
         const int n_half = nt * kBN + int(rank) * 128;
         for (int kk = 0; kk < ks; ++kk, ++g) {
           const int s = g % kI8Stages;
-          mbar_wait_bo(&empty[s], ((g / kI8Stages) & 1) ^ 1, p.dbg & (1 << 20));
+          const bool preloaded = i == 0 && kk < pre;
+          if (!preloaded) mbar_wait_bo(&empty[s], ((g / kI8Stages) & 1) ^ 1, p.dbg & (1 << 20));
           const bool with_side = has_r && kk == 0;
           if (with_side && i > 0) mbar_wait(side_empty, (i - 1) & 1);
           const uint32_t fbar = map_rank(smem_u32(&full[s]), 0);
           const uint32_t st = sb + s * kI8Stage;
-          if (leader)
+          if (leader && !preloaded)
             mbar_expect_tx(&full[s], 2u * (kI8A + (kDirect ? kI8B : 0) + (with_side ? (dense ? 2 * 16384 : 16384) : 0)));
           if constexpr (kDirect) {
-            tma_load_2d_pair(st + kI8A, &maps.bp, fbar, kk * 128, n_half, kEvictNormal);  // int8 [N, K] rows
+            if (!preloaded)
+              tma_load_2d_pair(st + kI8A, &maps.bp, fbar, kk * 128, n_half, kEvictNormal);  // int8 [N, K] rows
           } else {
             mbar_expect_tx(&bpk[s], kI8Bp);
             tma_load_2d(smem + s * kI8Stage + kI8A, &maps.bp, &bpk[s], 0, ((n_half >> 7) * ks + kk) * 128,
@@ -336,6 +352,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (both CTAs)
+    pdl_wait();  // sx / zp / xs come from the quantizer; y may still be read by a predecessor
+    pdl_launch_dependents();
     const uint32_t q = warp & 3;
     const uint32_t lane_base = (q * 32u) << 16;
     uint8_t* stage_out = epi + q * 2048;

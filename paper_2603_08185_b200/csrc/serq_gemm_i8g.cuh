@@ -161,6 +161,16 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
     // ------------------------------------------------------------ producer (both CTAs)
     if (elect_one()) {
       const uint32_t sb = smem_u32(smem), sside = smem_u32(side);
+      const uint32_t side_bytes = dense ? (split ? 3 : 2) * rch * 16384 : 16384;
+      // programmatic dependent launch: the first tile's weight stages stream before
+      // griddepcontrol.wait (they do not depend on the activation quantizer)
+      const int pre = my_tiles > 0 ? (ks < S ? ks : S) : 0;
+      for (int kk = 0; kk < pre; ++kk) {
+        if (leader) mbar_expect_tx(&full[kk], 2u * (kI8A + kI8B + (has_r && kk == 0 ? side_bytes : 0)));
+        tma_load_2d_pair(sb + kk * kI8gStage + kI8A, &maps.bp, map_rank(smem_u32(&full[kk]), 0), kk * 128,
+                         (cluster_id / tiles_m) * 256 + int(rank) * 128, kEvictNormal);
+      }
+      pdl_wait();
       uint32_t g = 0;
       for (int i = 0; i < my_tiles; ++i) {
         const int tile = cluster_id + i * n_clusters;
@@ -169,14 +179,14 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
         const int n_half = nt * 256 + int(rank) * 128;
         for (int kk = 0; kk < ks; ++kk, ++g) {
           const int s = g % S;
-          mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
+          const bool preloaded = i == 0 && kk < pre;
+          if (!preloaded) mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
           const bool with_side = has_r && kk == 0;
           if (with_side && i > 0) mbar_wait(side_empty, (i - 1) & 1);
           const uint32_t fbar = map_rank(smem_u32(&full[s]), 0);
           const uint32_t st = sb + s * kI8gStage;
-          if (leader)
-            mbar_expect_tx(&full[s], 2u * (kI8A + kI8B + (with_side ? (dense ? (split ? 3 : 2) * rch * 16384 : 16384) : 0)));
-          tma_load_2d_pair(st + kI8A, &maps.bp, fbar, kk * 128, n_half, kEvictNormal);
+          if (leader && !preloaded) mbar_expect_tx(&full[s], 2u * (kI8A + kI8B + (with_side ? side_bytes : 0)));
+          if (!preloaded) tma_load_2d_pair(st + kI8A, &maps.bp, fbar, kk * 128, n_half, kEvictNormal);
           tma_load_2d_pair(st, &maps.a, fbar, kk * 128, m_own, kEvictNormal);
           if (with_side) {
             if (dense) {
@@ -247,6 +257,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
     }
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
+    pdl_wait();  // sx / zp / xs come from the quantizer; y may still be read by a predecessor
+    pdl_launch_dependents();
     const uint32_t q = warp & 3;
     const int half = int(warp - 2) >> 2;        // column slice of the tile (kI8gCols wide)
     const int et = int(threadIdx.x) - 64;       // 0..32*kI8gEpiWarps-1
