@@ -280,8 +280,19 @@ def rmsnorm_quant_point(M: int, K: int, hbm_peak_gbs: float, n_steps: int = 16) 
     acts = [D.quantize_mx(x) for x in xs]
     t_f = time_steps(lambda i: D.rmsnorm_quantize_mx(xs[i % 8], gain, 1e-6, acts[i % 8]), n_steps)
     t_q = time_steps(lambda i: D.quantize_mx(xs[i % 8], None, acts[i % 8]), n_steps)
+    # the unfused alternative: torch RMSNorm to a bf16 tensor, then the quantizer (its codes are
+    # not the reference's: the normalised row is rounded to bf16 before encoding)
+    g16 = gain.to(torch.bfloat16)
+    hs = [torch.empty_like(x) for x in xs]
+
+    def unfused(i):
+        hs[i % 8].copy_(torch.nn.functional.rms_norm(xs[i % 8], (K,), g16, 1e-6))
+        D.quantize_mx(hs[i % 8], None, acts[i % 8])
+
+    t_u = time_steps(unfused, n_steps)
     byts = 2 * M * K + M * K / 2 + M * K / 32
     return {"M": M, "K": K, "rmsnorm_quant_us": t_f * 1e3, "quant_only_us": t_q * 1e3,
+            "unfused_torch_rmsnorm_then_quant_us": t_u * 1e3,
             "rmsnorm_quant_hbm_frac": byts / (t_f * 1e-3) / 1e9 / hbm_peak_gbs,
             "unfused_extra_bytes": 4 * M * K}
 
