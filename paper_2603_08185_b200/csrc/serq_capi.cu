@@ -1146,7 +1146,25 @@ int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* 
     }
     if (chunks == 0) plan[chunks++] = 0;
     plan[chunks - 1] += rem;
+    if (const char* e = getenv("SERQ_E2E_PLAN")) {  // diagnostics: explicit chunk rows, last absorbs the rest
+      int64_t n = 0, used = 0;
+      for (const char* q = e; *q && n < kE2eMaxChunks - 1;) {
+        const int64_t v = atoll(q);
+        if (v <= 0 || used + v >= M) break;
+        plan[n++] = v;
+        used += v;
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+      plan[n++] = M - used;
+      chunks = n;
+    }
   }
+  // diagnostics (SERQ_E2E_TIMING set): per-chunk timeline of the copies and kernels on stderr
+  static const bool timing = getenv("SERQ_E2E_TIMING") != nullptr;
+  cudaEvent_t tev[4 * kE2eMaxChunks + 1];
+  if (timing)
+    for (cudaEvent_t& e : tev) CK(cudaEventCreate(&e));
   cudaEvent_t* ev_in = h->e2e_ev;                       // [chunks] x chunk landed
   cudaEvent_t* ev_done = h->e2e_ev + kE2eMaxChunks;     // [chunks] y chunk computed
   cudaEvent_t* ev_out = h->e2e_ev + 2 * kE2eMaxChunks;  // [chunks] y chunk copied out
@@ -1156,11 +1174,13 @@ int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* 
   const int64_t kc_pad = kc_pad_of(h->K);
   int64_t start[kE2eMaxChunks];
   for (int64_t c = 0, r0 = 0; c < chunks; r0 += plan[c], ++c) start[c] = r0;
+  if (timing) CK(cudaEventRecord(tev[4 * kE2eMaxChunks], h->e2e_in));
   for (int64_t c = 0; c < chunks; ++c) {
     const int64_t r0 = start[c], mc = plan[c];
     CK(cudaMemcpyAsync(static_cast<uint8_t*>(h->ws_x) + r0 * h->K * 2, static_cast<const uint8_t*>(x_host) + r0 * h->K * 2,
                        mc * h->K * 2, cudaMemcpyHostToDevice, h->e2e_in));
     CK(cudaEventRecord(ev_in[c], h->e2e_in));
+    if (timing) CK(cudaEventRecord(tev[c], h->e2e_in));
   }
   const int n0 = g_launches;
   int launches = 0;
@@ -1169,6 +1189,7 @@ int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* 
     uint8_t* codes = h->ws_codes + r0 * h->K / 2;
     uint8_t* sf = h->ws_sf + (r0 / 128) * kc_pad * 512;
     CK(cudaStreamWaitEvent(st, ev_in[c], 0));
+    if (timing) CK(cudaEventRecord(tev[kE2eMaxChunks + c], st));
     int rc = serq_act_quant_mx(static_cast<uint8_t*>(h->ws_x) + r0 * h->K * 2, SERQ_BF16, mc, h->K, h->K, codes, sf,
                                nullptr, 0, nullptr, nullptr, stream);
     if (rc) return rc;
@@ -1178,15 +1199,26 @@ int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* 
     if (rc) return rc;
     launches += g_launches;
     CK(cudaEventRecord(ev_done[c], st));
+    if (timing) CK(cudaEventRecord(tev[2 * kE2eMaxChunks + c], st));
     CK(cudaStreamWaitEvent(h->e2e_out, ev_done[c], 0));
     CK(cudaMemcpyAsync(static_cast<uint8_t*>(y_host) + r0 * h->N * 2, static_cast<uint8_t*>(h->ws_y) + r0 * h->N * 2,
                        mc * h->N * 2, cudaMemcpyDeviceToHost, h->e2e_out));
     CK(cudaEventRecord(ev_out[c], h->e2e_out));
+    if (timing) CK(cudaEventRecord(tev[3 * kE2eMaxChunks + c], h->e2e_out));
   }
   (void)n0;
   g_launches = launches;
   CK(cudaStreamWaitEvent(st, ev_out[chunks - 1], 0));
   CK(cudaStreamSynchronize(st));
+  if (timing) {
+    for (int64_t c = 0; c < chunks; ++c) {
+      float t[4];
+      for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&t[k], tev[4 * kE2eMaxChunks], tev[k * kE2eMaxChunks + c]);
+      fprintf(stderr, "e2e chunk %lld rows %lld: h2d_end %.1f compute %.1f..%.1f d2h_end %.1f us\n", (long long)c,
+              (long long)plan[c], t[0] * 1e3, t[1] * 1e3, t[2] * 1e3, t[3] * 1e3);
+    }
+    for (cudaEvent_t& e : tev) cudaEventDestroy(e);
+  }
   return SERQ_OK;
 }
 

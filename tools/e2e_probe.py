@@ -9,8 +9,11 @@ lin = B.device_mx_linear(K, N, 64)
 x = B.outlier_x(M, K)
 xh = x.cpu().pin_memory()
 yh = torch.empty((M, N), dtype=torch.bfloat16).pin_memory()
-for rows in [int(v) for v in os.environ.get("ROWS_LIST", "0,512,1024,2048").split(",")]:
-    if rows:
+plans = os.environ.get("PLANS")
+for rows in ([p for p in plans.split(";")] if plans else [int(v) for v in os.environ.get("ROWS_LIST", "0,512,1024,2048").split(",")]):
+    if isinstance(rows, str):
+        os.environ["SERQ_E2E_PLAN"] = rows
+    elif rows:
         os.environ["SERQ_E2E_ROWS"] = str(rows)
     else:
         os.environ.pop("SERQ_E2E_ROWS", None)  # default plan
