@@ -656,7 +656,9 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
   if (!attr) {
     CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             ClCfg<false>::kSmem));
-    CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            ClCfg<true>::kSmem));
+    CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             ClCfg<true>::kSmem));
     attr = true;
   }
@@ -727,7 +729,11 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
   cfg.attrs = attrs;
   cfg.numAttrs = 2;
   if (fuse) {
-    CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<true>, dm, cp));
+    // converter lanes carry 1 or 2 token rows
+    if (M <= 4)
+      CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<true, 1>, dm, cp));
+    else
+      CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<true, 2>, dm, cp));
   } else {
     CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<false>, dm, cp));
   }
@@ -900,7 +906,7 @@ int serq_forward_mx(serq_linear_t* h, const void* x, int dtype, int64_t M, int64
   if (M <= kClFuseM && (h->r == 0 || h->has_r32) && dtype == SERQ_BF16 && !gather &&
       !(reinterpret_cast<uintptr_t>(x) & 15) && ldx % 8 == 0 && ldx >= h->K && !(g_debug_flags & (1 << 23)) &&
       !(g_debug_flags & 2048)) {
-    // decode (M <= 4) with the quantizer inside the linear: one kernel per layer instead of
+    // decode (M <= 8) with the quantizer inside the linear: one kernel per layer instead of
     // quantizer + PDL-chained linear (Llama-2-7B M=1: up_proj 7.8 vs 8.2 us/layer, down_proj
     // 8.1 vs 9.1; tools/decode_probe.py); debug flag 1<<23 selects the two-kernel path
     g_launches = 0;

@@ -13,7 +13,7 @@
 // no float atomics.  (A global-memory reduction costs ~3 L2 round trips on the
 // critical path of every layer, ~3 us measured; DSMEM ~0.2 us.)
 //
-// Fused quantizer (kFuse, M <= 4): the epilogue warps, idle during the main
+// Fused quantizer (kFuse, M <= 8): the epilogue warps, idle during the main
 // loop, take the K steps round-robin (warp c: steps c, c+4, ...; three of its
 // steps' bf16 activations in flight in registers, L2 resident), encode them
 // exactly like mx_encode (mxfmt.py:97-108: block
@@ -50,7 +50,9 @@ struct DecodeMaps {
 constexpr int kClThreads = 192;
 constexpr int kClXs = 512 + 512;     // gather fallback: 16 rows x 32 B of x[:, idx] codes + one SF atom
 constexpr int kClRed = 6 * 1024;     // rank-0 landing buffer for narrow partials ((S-1) x ceil(M/4) x 2 KB)
-constexpr int kClFuseM = 4;          // fused quantizer: one (token row, 32-block) per lane of a converter warp
+// fused quantizer: kP (token row, 32-block) pairs per lane, M <= 4 kP; used for M <= 8 (at
+// M = 16 the 4-pair converter was slower than the quantizer kernel + PDL: 10.5 vs 8.6 us)
+constexpr int kClFuseM = 8;
 template <bool kFuse>
 struct ClCfg {
   static constexpr int kStages = 5;
@@ -100,8 +102,8 @@ __device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t bar_cluster
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
-template <bool kFuse>
-__global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const __grid_constant__ DecodeMaps maps,
+template <bool kFuse, int kP = 1>
+__global__ void __launch_bounds__(kClThreads, 2) serq_mx_decode_cl_kernel(const __grid_constant__ DecodeMaps maps,
                                                                           const ClParams p) {
   constexpr int kClStages = ClCfg<kFuse>::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -151,11 +153,11 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
   }
   if (warp == 1) tmem_alloc<64>(tmem_slot);
   if (kFuse) {
-    // X rows >= kClFuseM of every stage stay zero, and scale-factor atom rows >= kClFuseM (never
-    // produced) get a finite scale; the converters rewrite rows < kClFuseM every step
+    // X rows >= 4 kP of every stage stay zero, and scale-factor atom rows >= 4 kP (never
+    // produced) get a finite scale; the converters rewrite rows < 4 kP every step
     for (int s = 0; s < kClStages; ++s) {
-      for (int b = threadIdx.x; b < (kDecX - kClFuseM * 128) / 16; b += blockDim.x)
-        reinterpret_cast<uint4*>(smem + s * kDecStage + kDecW + kClFuseM * 128)[b] = make_uint4(0, 0, 0, 0);
+      for (int b = threadIdx.x; b < (kDecX - 4 * kP * 128) / 16; b += blockDim.x)
+        reinterpret_cast<uint4*>(smem + s * kDecStage + kDecW + 4 * kP * 128)[b] = make_uint4(0, 0, 0, 0);
       for (int b = threadIdx.x; b < 2 * 512 / 16; b += blockDim.x)
         reinterpret_cast<uint4*>(smem + s * kDecStage + kDecW + kDecX + kDecSF)[b] = make_uint4(
             0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
@@ -257,77 +259,91 @@ __global__ void __launch_bounds__(kClThreads, 1) serq_mx_decode_cl_kernel(const 
     if constexpr (kFuse) {
       // X converter: warp c converts K steps c, c + 4, ... (four steps in flight, so the
       // per-step latency -- L2 load, encode, shared store, proxy fence -- is hidden);
-      // lane -> (token row m = lane / 8, 32-block part = lane % 8) of the 16 x 256 tile
+      // lane -> 32-block part = lane % 8 of token rows lane / 8 + 4 p (p < kP) of the 16 x 256 tile
+      constexpr int kDepth = kP == 1 ? 3 : 2;  // steps of this warp in flight in registers (<= 168 regs)
       const int cw = int(warp) - 2;
-      const int m = int(lane_id()) >> 3, part = int(lane_id()) & 7;
-      const bool row_ok = m < p.M;
-      const bool write_out = p.codes_out != nullptr && tile == 0 && row_ok;
-      auto load_x = [&](int i, uint4 (&v)[4]) {
+      const int m0 = int(lane_id()) >> 3, part = int(lane_id()) & 7;
+      auto load_x = [&](int i, uint4 (&v)[kP][4]) {
         const int kk = k0 + i;
-        const bool ok = i < nsteps && row_ok && kk * 256 + part * 32 < p.K;  // K % 32 == 0
-        const uint4* src = reinterpret_cast<const uint4*>(p.x + int64_t(m) * p.ldx + kk * 256 + part * 32);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) v[c] = ok ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+        for (int pp = 0; pp < kP; ++pp) {
+          const int m = m0 + 4 * pp;
+          const bool ok = i < nsteps && m < p.M && kk * 256 + part * 32 < p.K;  // K % 32 == 0
+          const uint4* src = reinterpret_cast<const uint4*>(p.x + int64_t(m) * p.ldx + kk * 256 + part * 32);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) v[pp][c] = ok ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+        }
       };
-      auto put_x = [&](int i, const uint4 (&cur)[4]) {
+      auto put_x = [&](int i, const uint4 (&cur)[kP][4]) {
         const int s = i % kClStages;
         const int kk = k0 + i;
-        // 32-element block: amax over |x| bit patterns, exponent, RNE-to-E2M1 (as mx_encode_fast_kernel)
-        uint32_t w[16];
+        uint32_t pk[kP][4];
+        int ex[kP];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          w[4 * c] = cur[c].x;
-          w[4 * c + 1] = cur[c].y;
-          w[4 * c + 2] = cur[c].z;
-          w[4 * c + 3] = cur[c].w;
-        }
-        uint32_t m2 = 0;
+        for (int pp = 0; pp < kP; ++pp) {
+          // 32-element block exactly as mx_encode_blk_kernel: abs-max tree, exponent, RNE to E2M1
+          uint32_t w[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) m2 = __vmaxu2(m2, w[k] & 0x7FFF7FFFu);
-        const uint32_t amax = max(m2 & 0xFFFFu, m2 >> 16);
-        const int e = mx_block_exp_bf16bits(amax);
-        const float inv = __uint_as_float(uint32_t(127 - e) << 23);
-        uint32_t pk[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint32_t packed = 0;
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const uint32_t wv = w[4 * k + h];
-            packed |= cvt_e2m1x2_raw(__uint_as_float(wv << 16) * inv, __uint_as_float(wv & 0xFFFF0000u) * inv)
-                      << (8 * h);
+          for (int c = 0; c < 4; ++c) {
+            w[4 * c] = cur[pp][c].x;
+            w[4 * c + 1] = cur[pp][c].y;
+            w[4 * c + 2] = cur[pp][c].z;
+            w[4 * c + 3] = cur[pp][c].w;
           }
-          pk[k] = canon_neg_zero(packed);
+          uint32_t m8[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = bf16x2_absmax(w[2 * k], w[2 * k + 1]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) m8[k] = bf16x2_absmax(m8[2 * k], m8[2 * k + 1]);
+          m8[0] = bf16x2_absmax(bf16x2_absmax(m8[0], m8[1]), bf16x2_absmax(m8[2], m8[3]));
+          m8[0] = bf16x2_absmax(m8[0], __byte_perm(m8[0], 0, 0x1032));
+          const uint32_t amax = m8[0] & 0x7FFFu;
+          const int e = amax ? max(int(amax >> 7), 2) - 129 : 0;
+          const float inv = __uint_as_float(uint32_t(127 - e) << 23);
+          ex[pp] = e;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint32_t packed = 0;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const uint32_t wv = w[4 * k + h];
+              packed |= cvt_e2m1x2_raw(__uint_as_float(wv << 16) * inv, __uint_as_float(wv & 0xFFFF0000u) * inv)
+                        << (8 * h);
+            }
+            pk[pp][k] = canon_neg_zero3(packed);
+          }
         }
         if (i >= kClStages) mbar_wait(&empty[s], ((i / kClStages) & 1) ^ 1);
         if (i == 0 && lane_id() == 0) CL_STEP(4, 0);
         uint8_t* st = smem + s * kDecStage;
-        // codes: row m, 16-B chunk `part` of the 128-B row, 128B swizzle (chunk ^ row % 8)
-        st_shared_v4(smem_u32(st + kDecW + m * 128 + ((part ^ (m & 7)) * 16)), pk[0], pk[1], pk[2], pk[3]);
-        // scale factor: chunk part/4, atom row m, byte part%4
-        st[kDecW + kDecX + kDecSF + (part >> 2) * 512 + m * 16 + (part & 3)] = uint8_t(e + 127);
-        if (write_out && kk * 256 + part * 32 < p.K) {
-          *reinterpret_cast<uint4*>(p.codes_out + int64_t(m) * (p.K / 2) + kk * 128 + part * 16) =
-              make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          p.sf_out[sf_offset(m, kk * 8 + part, p.kc_pad)] = uint8_t(e + 127);
+#pragma unroll
+        for (int pp = 0; pp < kP; ++pp) {
+          const int m = m0 + 4 * pp;
+          // codes: row m, 16-B chunk `part` of the 128-B row, 128B swizzle (chunk ^ row % 8)
+          st_shared_v4(smem_u32(st + kDecW + m * 128 + ((part ^ (m & 7)) * 16)), pk[pp][0], pk[pp][1], pk[pp][2],
+                       pk[pp][3]);
+          // scale factor: chunk part/4, atom row m, byte part%4
+          st[kDecW + kDecX + kDecSF + (part >> 2) * 512 + m * 16 + (part & 3)] = uint8_t(ex[pp] + 127);
+          if (p.codes_out != nullptr && tile == 0 && m < p.M && kk * 256 + part * 32 < p.K) {
+            *reinterpret_cast<uint4*>(p.codes_out + int64_t(m) * (p.K / 2) + kk * 128 + part * 16) =
+                make_uint4(pk[pp][0], pk[pp][1], pk[pp][2], pk[pp][3]);
+            p.sf_out[sf_offset(m, kk * 8 + part, p.kc_pad)] = uint8_t(ex[pp] + 127);
+          }
         }
         fence_proxy_async_smem();  // generic-proxy smem writes -> the tensor core's async proxy
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(&full[s]);
         if (lane_id() == 0) CL_STEP(5, i);
       };
-      // this warp's next three steps in registers
-      uint4 b0[4], b1[4], b2[4];
-      load_x(cw, b0);
-      load_x(cw + 4, b1);
-      load_x(cw + 8, b2);
-      for (int i = cw; i < nsteps; i += 12) {
-        put_x(i, b0);
-        load_x(i + 12, b0);
-        if (i + 4 < nsteps) put_x(i + 4, b1);
-        load_x(i + 16, b1);
-        if (i + 8 < nsteps) put_x(i + 8, b2);
-        load_x(i + 20, b2);
+      uint4 buf[kDepth][kP][4];
+#pragma unroll
+      for (int d = 0; d < kDepth; ++d) load_x(cw + 4 * d, buf[d]);
+      for (int i = cw; i < nsteps; i += 4 * kDepth) {
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) {
+          if (i + 4 * d < nsteps) put_x(i + 4 * d, buf[d]);
+          load_x(i + 4 * (d + kDepth), buf[d]);
+        }
       }
     }
     // ---- accumulator -> Y (S == 1) or the rank-0 DSMEM reduction

@@ -343,7 +343,7 @@ def test_mx_decode_parity(D, M, K, N, r):
     ref = O.forward_mx(x, main_t, comp)
     # debug flag 1<<29: partials of the split-K reduction in full width through the drained stages
     for flags in (0, 1 << 29, 0):
-        # serq_forward_mx: for M <= 4 the quantizer runs inside the decode kernel; Y and
+        # serq_forward_mx: for M <= 8 the quantizer runs inside the decode kernel; Y and
         # the activation codes it reports
         act = D.MxActivation(torch.empty(D.mx_sizes(M, K)[0], dtype=torch.uint8, device="cuda"),
                              torch.empty(D.mx_sizes(M, K)[1], dtype=torch.uint8, device="cuda"), M, K)
