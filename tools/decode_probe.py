@@ -33,8 +33,9 @@ for K, N in ((4096, 11008), (11008, 4096)):
                 for lin, a, y in zip(lins, acts, ys):
                     lin.forward(x, a, y)
             r = {"K": K, "N": N, "M": M, "S": v}
+            extra = int(os.environ.get("EXTRA_FLAGS", "0"))
             for name, fn in (("lin", lin_all), ("two", two_all), ("fused", fused_all)):
-                _lib.call("serq_set_debug_flags", 0 if name == "fused" else (1 << 23))
+                _lib.call("serq_set_debug_flags", extra | (0 if name == "fused" else (1 << 23)))
                 t = B.time_graph(B.graph_of(fn), None, n=10) / layers * 1e-3
                 r[name + "_us"] = round(t * 1e6, 2)
                 r[name + "_gbs"] = round(byts / t / 1e9)
