@@ -298,7 +298,7 @@ def run_serq(args) -> None:
                          "measured_fp4_mma_ceiling_tflops": 8800.0,
                          "measured_fp4_note": "tools/mma_rate.cu: back-to-back tcgen05.mma kind::mxf4 128x256x64 on 148 SMs, random operands (profiles/mma_rate_r01.txt)",
                          "algorithmic_flops_per_launch": M * flops_per_token(), "traffic": traffic},
-            "quantizer_roofline": {"bound": "hbm", "kernel": "mx_encode_kernel<bf16>",
+            "quantizer_roofline": {"bound": "hbm", "kernel": "mx_encode_blk_kernel<1> (one thread per 32-block)",
                                    "achieved": q_bytes / (q_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                                    "frac": q_bytes / (q_ms / 1e3) / 1e9 / hbm,
                                    "peak_source": "MEASURED_PEAKS.json hbm_gbs", "bytes_per_launch": q_bytes},
