@@ -16,6 +16,7 @@
  *   serq_pack_mx           MxBlockTensor artefacts (main_t, comp.r_q)     mxfmt.py:34-49, compensate.py:343-357
  *   serq_unpack_mx         inverse of the device layout (artefact export)
  *   serq_rmsnorm_quant_mx  rmsnorm(x, gain) -> mx_encode, fused        saliency.py:194-196, mxfmt.py:97-108
+ *   serq_rmsnorm_quant_mx_gather  ... + the salient gather x[:, idx]   compensate.py:335
  *   serq_mx_container_decode  load_mx body -> codes / exponents on the device  mxfmt.py:254-280
  *   serq_pack_int          QuantizedTensor artefacts (main, comp.r_q / comp.r_dense)
  *                                                                         quantcore.py:59-80, compensate.py:48-69
@@ -103,6 +104,14 @@ int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K
  * reference's f64 operations for any 32-block the bound cannot decide.  K <= 8192. */
 int serq_rmsnorm_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, const double* gain,
                           const float* gain32, double eps, uint8_t* codes, uint8_t* sf, serq_stream_t stream);
+
+/* serq_rmsnorm_quant_mx plus the gather fallback (compensate.py:335): the
+ * normalised salient slice rmsnorm(x)[:, gather_idx] (int32 [r], r % 32 == 0, r <= 1024)
+ * is encoded in the same kernel into xs_codes [M, r/2] / xs_sf (serq_act_quant_mx's xs
+ * layout); gather_idx NULL = serq_rmsnorm_quant_mx. */
+int serq_rmsnorm_quant_mx_gather(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, const double* gain,
+                                 const float* gain32, double eps, const int32_t* gather_idx, int r, uint8_t* codes,
+                                 uint8_t* sf, uint8_t* xs_codes, uint8_t* xs_sf, serq_stream_t stream);
 
 /* The reference's packed MX file body (mxfmt.py:228-251, after the 28-byte
  * header; bundleio.py load path): rows x cols/32 records of 17 bytes (exponent

@@ -432,6 +432,13 @@ int serq_unpack_mx(const uint8_t* codes_packed, const uint8_t* sf, int64_t rows,
 
 int serq_rmsnorm_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, const double* gain,
                           const float* gain32, double eps, uint8_t* codes, uint8_t* sf, serq_stream_t stream) {
+  return serq_rmsnorm_quant_mx_gather(x, dtype, M, K, ldx, gain, gain32, eps, nullptr, 0, codes, sf, nullptr, nullptr,
+                                      stream);
+}
+
+int serq_rmsnorm_quant_mx_gather(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, const double* gain,
+                                 const float* gain32, double eps, const int32_t* gather_idx, int r, uint8_t* codes,
+                                 uint8_t* sf, uint8_t* xs_codes, uint8_t* xs_sf, serq_stream_t stream) {
   g_launches = 0;
   if (M <= 0 || K <= 0) return fail(SERQ_EINVAL, "x must be non-empty (M=%lld, K=%lld)", (long long)M, (long long)K);
   if (K % 32) return fail(SERQ_EINVAL, "row length %lld not divisible by block_size 32", (long long)K);
@@ -447,6 +454,12 @@ int serq_rmsnorm_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_
   // rows / chunks beyond the matrix must read as a finite scale
   if (M % 128 || K % 256) CK(cudaMemsetAsync(sf, 0, sf_bytes_of(M, K), st));
   if (K > 4 * 2048) return fail(SERQ_EINVAL, "fused RMSNorm quantizer supports rows up to 8192 elements");
+  if (gather_idx && (r <= 0 || r % 32 || r > 1024 || r > K || !xs_codes || !xs_sf))
+    return fail(SERQ_EINVAL, "gather needs 0 < r <= min(K, 1024), r %% 32 == 0 and the xs buffers");
+  const int kcr = gather_idx ? kc_pad_of(r) : 0;
+  // the gathered slice's scale-factor padding (rows to the 128-row block, chunks to kc_pad_r)
+  if (gather_idx && (M % 128 || r % 256)) CK(cudaMemsetAsync(xs_sf, 0, sf_bytes_of(M, r), st));
+  const MxGather mg{gather_idx, r, xs_codes, xs_sf, kcr};
 
   // kTpr threads per row (8 elements each per chunk), 256 / kTpr rows per CTA
   // threads per row: 128 for K <= 4096, 256 above (measured best of 64 / 128 / 256 at 4096^2 and 8192^2)
@@ -455,7 +468,7 @@ int serq_rmsnorm_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_
   const dim3 grid{unsigned(cdiv(M, 256 / tpr))}, blk{256};
 #define RMS_LAUNCH(T, P, C)                                                                                       \
   CK(launch_pdl(rmsnorm_mx_encode_kernel<T, P, C>, grid, blk, 0, st, static_cast<const T*>(x), int(M), int(K), ldx, \
-                gain, gain32, eps, codes, sf, kc))
+                gain, gain32, eps, codes, sf, kc, mg))
   if (dtype == SERQ_BF16) {
     if (tpr == 128) {
       if (chunks <= 2) RMS_LAUNCH(__nv_bfloat16, 128, 2);

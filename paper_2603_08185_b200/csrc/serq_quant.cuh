@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(256) rmsnorm_mx_encode_kernel(const T* __restr
                                                                 const double* __restrict__ gain,
                                                                 const float* __restrict__ gain32, double eps,
                                                                 uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
-                                                                int kc_pad) {
+                                                                int kc_pad, MxGather gather = MxGather{}) {
   constexpr int kRows = 256 / kTpr, kWarps = kTpr / 32;
   // Error budget of the f32 fast path vs the reference's f64 y: per-thread recursive f32
   // sum of n = 8 kChunks positive squares (<= (n - 1) 2^-24 relative), halved by the sqrt,
@@ -536,10 +536,48 @@ __global__ void __launch_bounds__(256) rmsnorm_mx_encode_kernel(const T* __restr
       if ((t & 3) == 0) sf[sf_offset(row, c / 32, kc_pad)] = uint8_t(e + 127);
     }
   }
+  // ---- the salient slice x[:, idx] of a non-permuted layer (compensate.py:335), normalised
+  // with the same row scale: thread t encodes gathered elements 8t .. 8t+7 (r <= 8 kTpr)
+  bool unsure_g = false;
+  const int gj0 = t * 8;
+  if (gather.idx) {
+    const bool okg = row_ok && gj0 < gather.r;
+    float y[8];
+    float amax = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int col = okg ? gather.idx[gj0 + i] : 0;
+      y[i] = okg ? In<T>::f(xr[col]) * r32 * gain32[col] : 0.f;
+      amax = fmaxf(amax, fabsf(y[i]));
+    }
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffff, amax, 1));
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffff, amax, 2));
+    const uint32_t mant = __float_as_uint(amax) & 0x7FFFFFu;
+    bool unsure = amax != 0.f &&
+                  (mant < kMantEdge || mant > 0x7FFFFFu - kMantEdge || amax < 0x1p-100f || !(amax < 0x1p+100f));
+    const int e = mx_block_exp_f32(amax);
+    const float inv = __uint_as_float(uint32_t(127 - e) << 23);
+    const float inv_lo = inv * (1.f - kRel), inv_hi = inv * (1.f + kRel);
+    uint32_t packed = 0, packed_hi = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      packed |= cvt_e2m1x2_raw(y[2 * i] * inv_lo, y[2 * i + 1] * inv_lo) << (8 * i);
+      packed_hi |= cvt_e2m1x2_raw(y[2 * i] * inv_hi, y[2 * i + 1] * inv_hi) << (8 * i);
+    }
+    unsure |= packed != packed_hi;
+    unsure = __shfl_xor_sync(0xffffffff, int(unsure), 1) | unsure;
+    unsure = __shfl_xor_sync(0xffffffff, int(unsure), 2) | unsure;
+    if (unsure) {
+      unsure_g = okg;
+    } else if (okg) {
+      *reinterpret_cast<uint32_t*>(gather.xs_codes + row * (gather.r / 2) + gj0 / 2) = canon_neg_zero(packed);
+      if ((t & 3) == 0) gather.xs_sf[sf_offset(row, gj0 / 32, gather.kc_pad_r)] = uint8_t(e + 127);
+    }
+  }
   // ---- pass 3 (rare): rows holding an undecided block redo them with the reference's f64
   // operations: the mean of squares at f64 accuracy, IEEE division, exact E2M1 rounding
-  if (unsure_mask) s_unsure[rl] = 1;
-  if (!__syncthreads_or(unsure_mask != 0)) return;
+  if (unsure_mask || unsure_g) s_unsure[rl] = 1;
+  if (!__syncthreads_or(unsure_mask != 0 || unsure_g)) return;
   const bool redo = s_unsure[rl] != 0;
   double ss64 = 0.0;
   if (redo) {
@@ -587,6 +625,28 @@ __global__ void __launch_bounds__(256) rmsnorm_mx_encode_kernel(const T* __restr
     if (ok && ((unsure_mask >> it) & 1u)) {
       *reinterpret_cast<uint32_t*>(codes + row * (K / 2) + c / 2) = packed;
       if ((t & 3) == 0) sf[sf_offset(row, c / 32, kc_pad)] = uint8_t(e + 127);
+    }
+  }
+  if (gather.idx && __any_sync(0xffffffff, unsure_g)) {
+    const bool okg = row_ok && gj0 < gather.r;
+    double yd[8];
+    double amaxd = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int col = okg ? gather.idx[gj0 + i] : 0;
+      yd[i] = okg ? __ddiv_rn(double(In<T>::f(xr[col])), rms) * gain[col] : 0.0;
+      amaxd = fmax(amaxd, fabs(yd[i]));
+    }
+    amaxd = fmax(amaxd, __shfl_xor_sync(0xffffffff, amaxd, 1));
+    amaxd = fmax(amaxd, __shfl_xor_sync(0xffffffff, amaxd, 2));
+    const int e = mx_block_exp_f64(amaxd);
+    const double invd = ldexp(1.0, -e);
+    uint32_t packed = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) packed |= e2m1_code_f64(yd[i] * invd) << (4 * i);
+    if (unsure_g) {
+      *reinterpret_cast<uint32_t*>(gather.xs_codes + row * (gather.r / 2) + gj0 / 2) = packed;
+      if ((t & 3) == 0) gather.xs_sf[sf_offset(row, gj0 / 32, gather.kc_pad_r)] = uint8_t(e + 127);
     }
   }
 }

@@ -103,11 +103,14 @@ def quantize_mx(x: torch.Tensor, gather_idx: torch.Tensor | None = None, out: Mx
 
 
 def rmsnorm_quantize_mx(x: torch.Tensor, gain: torch.Tensor, eps: float = 1e-6,
-                        out: MxActivation | None = None) -> MxActivation:
+                        out: MxActivation | None = None, gather_idx: torch.Tensor | None = None,
+                        r: int = 0) -> MxActivation:
     """Producer fusion: mx_encode(rmsnorm(x, gain, eps)) in ONE kernel
     (saliency.py:194-196 then mxfmt.py:97-108).  x: bf16/f32 [M, K] residual
     stream on the GPU; gain: float64 [K] (the RMSNorm weight with the smoothing
-    scales folded in and the salient permutation applied)."""
+    scales folded in).  ``gather_idx`` (int32 [r]): also encode the normalised
+    salient slice rmsnorm(x)[:, idx] (compensate.py:335) into out.xs_codes /
+    out.xs_sf -- the gather fallback of q/k/v and gate/up."""
     _require_cuda(x, "x")
     if x.dim() != 2 or x.stride(1) != 1:
         raise ValidationError("x must be a row-major 2-D tensor")
@@ -118,10 +121,16 @@ def rmsnorm_quantize_mx(x: torch.Tensor, gain: torch.Tensor, eps: float = 1e-6,
         cb, sb = mx_sizes(M, K)
         out = MxActivation(torch.empty(cb, dtype=torch.uint8, device=x.device),
                            torch.empty(sb, dtype=torch.uint8, device=x.device), M, K)
+    if gather_idx is not None and out.xs_codes is None:
+        cbr, sbr = mx_sizes(M, r)
+        out.xs_codes = torch.empty(cbr, dtype=torch.uint8, device=x.device)
+        out.xs_sf = torch.empty(sbr, dtype=torch.uint8, device=x.device)
     gain = gain.contiguous()
     g32 = gain.float()
-    _lib.call("serq_rmsnorm_quant_mx", x.data_ptr(), _dtype_id(x), M, K, x.stride(0), gain.data_ptr(), g32.data_ptr(),
-              float(eps), out.codes.data_ptr(), out.sf.data_ptr(), _stream())
+    _lib.call("serq_rmsnorm_quant_mx_gather", x.data_ptr(), _dtype_id(x), M, K, x.stride(0), gain.data_ptr(),
+              g32.data_ptr(), float(eps), _ptr(gather_idx), int(r) if gather_idx is not None else 0,
+              out.codes.data_ptr(), out.sf.data_ptr(), _ptr(out.xs_codes if gather_idx is not None else None),
+              _ptr(out.xs_sf if gather_idx is not None else None), _stream())
     return out
 
 
@@ -254,11 +263,9 @@ class MxLinear:
 
     def forward_rmsnorm(self, x: torch.Tensor, gain: torch.Tensor, eps: float = 1e-6,
                         act: MxActivation | None = None, y: torch.Tensor | None = None) -> torch.Tensor:
-        """linear(rmsnorm(x, gain)) with the normalisation fused into the quantizer
-        (the permuted / contiguous salient layout: the salient slice is K-tile 0)."""
-        if not self.contiguous:
-            raise ValidationError("the fused RMSNorm quantizer needs the permuted (contiguous) salient layout")
-        act = rmsnorm_quantize_mx(x, gain, eps, act)
+        """linear(rmsnorm(x, gain)) with the normalisation fused into the quantizer; for a
+        non-contiguous salient set the same kernel also encodes the normalised slice x[:, idx]."""
+        act = rmsnorm_quantize_mx(x, gain, eps, act, None if self.contiguous else self.gather_idx, self.r)
         return self.gemm(act, y)
 
     def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor) -> None:

@@ -467,6 +467,40 @@ def test_rmsnorm_fused_linear_parity(D):
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
 
 
+@pytest.mark.parametrize("M,K,r", [(300, 4096, 64), (17, 1024, 128), (130, 8192, 32)])
+def test_rmsnorm_quant_mx_gather(D, M, K, r):
+    # the gather fallback inside the producer fusion: rmsnorm(x)[:, idx] encoded by the same kernel
+    # (compensate.py:335 re-encodes the salient columns of the normalised row)
+    rng = np.random.default_rng(M + r)
+    x = O.bf16_round(_bf16_outlier_x(M, K, seed=r) * 2.0)
+    gain = np.abs(rng.standard_normal(K)) + 0.5
+    idx = rng.permutation(K)[:r]
+    act = D.rmsnorm_quantize_mx(_cuda(x, torch.bfloat16), torch.from_numpy(gain).to("cuda"), 1e-6,
+                                gather_idx=torch.from_numpy(idx.astype(np.int32)).to("cuda"), r=r)
+    yref = O.rmsnorm(x, gain, 1e-6)
+    for codes, sf, cols, ref_y in ((act.codes, act.sf, K, yref), (act.xs_codes, act.xs_sf, r, yref[:, idx])):
+        c, e = D.unpack_mx(codes, sf, M, cols)
+        ref = O.mx_encode(np.ascontiguousarray(ref_y), 32)
+        eb = np.repeat(e.cpu().numpy() != ref.block_scale_exponents, 32, axis=1)
+        diff = (c.cpu().numpy() != ref.element_codes) | eb
+        assert not (diff & ~_near_midpoint(np.ascontiguousarray(ref_y))).any()
+
+
+def test_rmsnorm_fused_linear_gather_parity(D):
+    M, K, N, r = 400, 2048, 512, 64
+    x = O.bf16_round(_bf16_outlier_x(M, K, seed=51))
+    w = np.random.default_rng(52).standard_normal((K, N)) * 0.02
+    idx = np.random.default_rng(53).permutation(K)[:r]
+    main_t, comp = O.build_serq_rtn_mx(w, idx, 32)
+    gain = np.abs(np.random.default_rng(54).standard_normal(K)) + 0.5
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                     comp.r_q.block_scale_exponents, idx)
+    assert not lin.contiguous
+    y = lin.forward_rmsnorm(_cuda(x, torch.bfloat16), torch.from_numpy(gain).to("cuda")).float().cpu().numpy()
+    mx, mean = O.parity_errors(y, O.forward_mx(O.rmsnorm(x, gain), main_t, comp))
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
 def test_rmsnorm_quant_mx_exact_fallback_blocks(D):
     # rows built so many blocks sit exactly on E2M1 decision points / power-of-two maxima after
     # normalisation: the kernel must send them through its exact f64 path
