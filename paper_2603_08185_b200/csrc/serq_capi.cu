@@ -159,6 +159,7 @@ struct serq_linear {
   void* w4 = nullptr;                                // INT: packed int4 weights, tiled [N/128][K/128][128][64 B]
   CUtensorMap map_w4, map_r_pair;                    // INT pair kernel maps (R with 128-row boxes)
   CUtensorMap map_w8;                                // INT pair kernel, direct int8 weights: 128 B x 128-row boxes
+  CUtensorMap map_w8_64, map_r_pair64;               // the same with 64-row boxes (128-column tiles)
   bool has_w4 = false;
   // INT, group-wise weight scales along K (serq_pack_int_grouped)
   int groups = 1, gsteps = 0;
@@ -541,6 +542,7 @@ int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t
   if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_int launch failed"));
   int rc = make_map(&h->map_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, kBN);
   if (!rc) rc = make_map(&h->map_w8, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, 128);
+  if (!rc) rc = make_map(&h->map_w8_64, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, 64);
   if (rc) return bail(rc);
   if (w_bits <= 4) {
     // packed INT4 copy for the CTA-pair kernel (widened to INT8 in shared memory)
@@ -563,6 +565,7 @@ int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t
     if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "dense_r launch failed"));
     rc = make_map(&h->map_r, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h->rbuf, r, N, r * 2, 64, kBN);
     if (!rc) rc = make_map(&h->map_r_pair, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h->rbuf, r, N, r * 2, 64, 128);
+    if (!rc) rc = make_map(&h->map_r_pair64, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h->rbuf, r, N, r * 2, 64, 64);
     if (rc) return bail(rc);
   } else if (r_mode == SERQ_R_INT) {
     if (cudaMalloc(&h->rbuf, N * r) != cudaSuccess || cudaMalloc(&h->sr, N * 4) != cudaSuccess ||
@@ -575,6 +578,7 @@ int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t
     if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack R launch failed"));
     rc = make_map(&h->map_r, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r, N, r, 128, kBN);
     if (!rc) rc = make_map(&h->map_r_pair, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r, N, r, 128, 128);
+    if (!rc) rc = make_map(&h->map_r_pair64, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rbuf, r, N, r, 128, 64);
     if (rc) return bail(rc);
   }
   *out = h;
@@ -1011,6 +1015,8 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
                               I8Cfg<false>::kSmem));
       CK(cudaFuncSetAttribute(serq_i8_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               I8Cfg<true>::kSmem));
+      CK(cudaFuncSetAttribute(serq_i8_pair_kernel<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              I8Cfg<true>::kSmem));
       attri = true;
     }
     I8Maps im;
@@ -1021,8 +1027,10 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
       rc = make_map(&im.xs, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xs, h->r, M, h->r * 2, 64, 128);
     if (rc) return rc;
     if (h->r_mode != SERQ_R_DENSE) im.xs = im.a;
-    im.bp = widen ? h->map_w4 : h->map_w8;
-    im.r = h->r_mode != SERQ_R_NONE ? h->map_r_pair : im.bp;
+    // few 256x256 tiles (C1: 2 x 16 on 74 pairs): 128-column tiles put twice as many pairs to work
+    const bool narrow = !widen && cdiv(M, 256) * cdiv(h->N, 256) * 2 <= sm_count() / 2 && !(g_debug_flags & (1 << 27));
+    im.bp = widen ? h->map_w4 : (narrow ? h->map_w8_64 : h->map_w8);
+    im.r = h->r_mode != SERQ_R_NONE ? (narrow ? h->map_r_pair64 : h->map_r_pair) : im.bp;
     GemmParams p{};
     p.dbg = g_debug_flags;
     p.M = int(M);
@@ -1042,7 +1050,7 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     p.addend = addend;
     p.accr_dump = accr_dump;
     p.dbg_ts = g_debug_ts;
-    const int64_t tiles = cdiv(M, 256) * cdiv(h->N, kBN);
+    const int64_t tiles = cdiv(M, 256) * cdiv(h->N, narrow ? 128 : kBN);
     const int64_t max_pairs = sm_count() / 2;
     const dim3 grid(unsigned(2 * (tiles < max_pairs ? tiles : max_pairs)));
     // launched with programmatic dependent launch: the prologue and the first weight stages
@@ -1050,6 +1058,9 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     if (widen)
       CK(launch_pdl(serq_i8_pair_kernel<false>, grid, dim3(I8Cfg<false>::kThreads), I8Cfg<false>::kSmem, S(stream), im,
                     p));
+    else if (narrow)
+      CK(launch_pdl(serq_i8_pair_kernel<true, 128>, grid, dim3(I8Cfg<true>::kThreads), I8Cfg<true>::kSmem, S(stream),
+                    im, p));
     else
       CK(launch_pdl(serq_i8_pair_kernel<true>, grid, dim3(I8Cfg<true>::kThreads), I8Cfg<true>::kSmem, S(stream), im, p));
     LAUNCH_CHECK("serq_i8_pair_kernel");

@@ -109,9 +109,15 @@ __device__ __forceinline__ uint2 widen_int4x8(uint32_t w) {
   return make_uint2(__byte_perm(lo, hi, 0x5140), __byte_perm(lo, hi, 0x7362));
 }
 
-template <bool kDirect>
+// kN: output columns per CTA-pair tile (256, or 128 for small problems so twice as many
+// pairs get a tile; each CTA then stages 64 weight rows)
+template <bool kDirect, int kN = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThreads, 1)
     serq_i8_pair_kernel(const __grid_constant__ I8Maps maps, const GemmParams p) {
+  static_assert(kN == 256 || (kN == 128 && kDirect), "128-column tiles need the direct int8 weight feed");
+  constexpr int kBHalf = kN / 2;  // weight rows per CTA
+  constexpr uint32_t kBBytes = kBHalf * 128;  // one 128-K step of this CTA's weight rows (int8)
+  constexpr uint32_t kRBytes = kBHalf * 128;  // this CTA's R rows (int8 r <= 128 or bf16 r <= 64: 128 B each)
   constexpr int kI8Stages = I8Cfg<kDirect>::kStages;
   constexpr int kI8Stage = I8Cfg<kDirect>::kStage;
   constexpr int kBp = I8Cfg<kDirect>::kBp;
@@ -137,7 +143,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
   const int cluster_id = blockIdx.x >> 1;
   const int n_clusters = gridDim.x >> 1;
   const int tiles_m = (p.M + 255) / 256;
-  const int tiles_n = (p.N + kBN - 1) / kBN;
+  const int tiles_n = (p.N + kN - 1) / kN;
   const int n_tiles = tiles_m * tiles_n;
   const int my_tiles = cluster_id < n_tiles ? (n_tiles - 1 - cluster_id) / n_clusters + 1 : 0;
   const bool has_r = p.r_mode != kRNone;
@@ -180,11 +186,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
       // previous kernel (the activation quantizer) -- stream them before griddepcontrol.wait
       const int pre = kDirect && my_tiles > 0 ? (ks < kI8Stages ? ks : kI8Stages) : 0;
       if (my_tiles > 0) {
-        const int n_half0 = (cluster_id / tiles_m) * kBN + int(rank) * 128;
+        const int n_half0 = (cluster_id / tiles_m) * kN + int(rank) * kBHalf;
         for (int kk = 0; kk < pre; ++kk) {
           const bool with_side = has_r && kk == 0;
           if (leader)
-            mbar_expect_tx(&full[kk], 2u * (kI8A + kI8B + (with_side ? (dense ? 2 * 16384 : 16384) : 0)));
+            mbar_expect_tx(&full[kk], 2u * (kI8A + kBBytes + (with_side ? (dense ? 16384 + kRBytes : kRBytes) : 0)));
           tma_load_2d_pair(sb + kk * kI8Stage + kI8A, &maps.bp, map_rank(smem_u32(&full[kk]), 0), kk * 128, n_half0,
                            kEvictNormal);
         }
@@ -195,7 +201,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
         const int tile = cluster_id + i * n_clusters;
         const int mt = tile % tiles_m, nt = tile / tiles_m;
         const int m_own = mt * 256 + int(rank) * 128;
-        const int n_half = nt * kBN + int(rank) * 128;
+        const int n_half = nt * kN + int(rank) * kBHalf;
         for (int kk = 0; kk < ks; ++kk, ++g) {
           const int s = g % kI8Stages;
           const bool preloaded = i == 0 && kk < pre;
@@ -205,7 +211,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
           const uint32_t fbar = map_rank(smem_u32(&full[s]), 0);
           const uint32_t st = sb + s * kI8Stage;
           if (leader && !preloaded)
-            mbar_expect_tx(&full[s], 2u * (kI8A + (kDirect ? kI8B : 0) + (with_side ? (dense ? 2 * 16384 : 16384) : 0)));
+            mbar_expect_tx(&full[s], 2u * (kI8A + (kDirect ? kBBytes : 0) + (with_side ? (dense ? 16384 + kRBytes : kRBytes) : 0)));
           if constexpr (kDirect) {
             if (!preloaded)
               tma_load_2d_pair(st + kI8A, &maps.bp, fbar, kk * 128, n_half, kEvictNormal);  // int8 [N, K] rows
@@ -226,8 +232,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
     // ------------------------------------------------------------ MMA issuer (leader)
     if (leader) {
       const uint32_t sb = smem_u32(smem), sside = smem_u32(side);
-      const uint32_t id_main = idesc_i8(256, kBN, p.a_signed != 0, true);
-      const uint32_t id_r = dense ? idesc_bf16(256, kBN) : id_main;
+      const uint32_t id_main = idesc_i8(256, kN, p.a_signed != 0, true);
+      const uint32_t id_r = dense ? idesc_bf16(256, kN) : id_main;
       const uint32_t total = uint32_t(my_tiles) * ks;
       if (total > 0) {
         mbar_wait_cluster(kDirect ? &full[0] : &bready[0], 0);
@@ -364,10 +370,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
       const int tile = cluster_id + i * n_clusters;
       const int mt = tile % tiles_m, nt = tile / tiles_m;
       const int m_own = mt * 256 + int(rank) * 128;
-      const int n0 = nt * kBN;
+      const int n0 = nt * kN;
       // per-column constants of this tile
       named_bar_sync(1, 128);  // previous tile's readers are done with the constants
-      for (int c = threadIdx.x - 128; c < kBN; c += 128) {
+      for (int c = threadIdx.x - 128; c < kN; c += 128) {
         const int n = n0 + c;
         const bool ok = n < p.N;
         cst_f[c] = ok ? p.sw[n] : 0.f;
@@ -392,7 +398,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
       if (p.dbg_ts && leader && q == 0 && lane_id() == 0 && i < 8) p.dbg_ts[512 + cluster_id * 64 + i * 8 + 4] = globaltimer();
 #endif
 #pragma unroll 1
-      for (int c = 0; c < kBN / 32; ++c) {
+      for (int c = 0; c < kN / 32; ++c) {
         // exact in wrapping int32: |acc - zp*colsum| <= 255 * 8 * K < 2^31 for K < 2^20
         uint32_t packed[16];
 #pragma unroll
@@ -408,7 +414,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
 #ifdef SERQ_DIAG_TS
           if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == 1) p.dbg_ts[5300 + c * 8 + 4 + h] = globaltimer();
 #endif
-          if (c == kBN / 32 - 1 && h == 1) {
+          if (c == kN / 32 - 1 && h == 1) {
             tc_fence_before();
             __syncwarp();
             if (lane_id() == 0) mbar_arrive_cluster_relaxed(tmem_empty_leader);
