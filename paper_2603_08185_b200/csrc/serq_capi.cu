@@ -265,8 +265,7 @@ static int act_quant_mx_impl(const void* x, int dtype, int64_t M, int64_t K, int
       // 4096^2 8.1 / 8.8 / 10.8 us); debug flag 1<<30: the 8-elements-per-thread kernel (9.9 us)
       const int kR = (g_debug_flags & (1 << 21)) ? 4 : (g_debug_flags & (1 << 22)) ? 2 : 1;  // diagnostics
       const int64_t main_blocks = cdiv(cdiv(m_rows, kR) * int64_t(kc) * 4, 256);
-      const dim3 gb(unsigned(main_blocks > cdiv(g_threads, 256) ? main_blocks : cdiv(g_threads, 256)), 1u,
-                    gather_idx ? 2u : 1u);
+      const dim3 gb(unsigned(main_blocks + cdiv(g_threads, 256)));  // gather CTAs appended
       const auto* xb = static_cast<const __nv_bfloat16*>(x);
       if (kR == 4)
         CK(launch_pdl(mx_encode_blk_kernel<4>, gb, dim3(256), 0, st, xb, int(M), int(K), ldx, codes, sf, kc, mg));
@@ -803,18 +802,31 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
   p.dbg_ts = g_debug_ts;
   if (M <= kDecN && (h->r == 0 || h->has_r32) && !(g_debug_flags & 2048))
     return launch_decode_cl(h, a_codes, a_sf, nullptr, 0, nullptr, nullptr, M, y, ldy, S(stream), xs_codes, xs_sf);
-  if (M > 128 && (h->r == 0 || (h->has_r32 && h->contiguous)) && !(g_debug_flags & (16 | 512))) {
+  // pair3 for the permuted layout, and for the gather fallback with r == 64 (debug flag 1<<24: the
+  // gather cases take the older pair kernel)
+  const bool g3 = h->r > 0 && h->has_r32 && !h->contiguous && xs_codes && xs_sf && !(g_debug_flags & (1 << 24));
+  if (M > 128 && (h->r == 0 || (h->has_r32 && h->contiguous) || g3) && !(g_debug_flags & (16 | 512))) {
     static bool attr3 = false;
     if (!attr3) {
-      CK(cudaFuncSetAttribute(serq_mx_pair3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k3SmemBytes));
+      CK(cudaFuncSetAttribute(serq_mx_pair3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3SmemBytes));
+      CK(cudaFuncSetAttribute(serq_mx_pair3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3SmemBytesG));
       attr3 = true;
     }
     Pair3Maps pm;
     rc = make_map(&pm.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, 128);
     if (!rc) rc = make_sf_map(&pm.sfa, a_sf, M, h->K);
-    if (!rc)
+    if (!rc && !g3)
       rc = make_map(&pm.y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, h->N, M, ldy * 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (!rc && g3)  // 32 rows x 16 columns per epilogue box
+      rc = make_map(&pm.y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, h->N, M, ldy * 2, 16, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (!rc && g3)
+      rc = make_map(&pm.xs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_codes, h->r / 2, M, h->r / 2, 32, 128,
+                    CU_TENSOR_MAP_SWIZZLE_32B);
+    if (!rc && g3)
+      rc = make_map(&pm.sfxs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_sf, 128, uint64_t(sf_bytes_of(M, h->r) / 128), 128, 128,
+                    4, CU_TENSOR_MAP_SWIZZLE_NONE);
     if (rc) return rc;
+    if (!g3) pm.xs = pm.sfxs = pm.a;  // unused
     pm.b = h->map_b128;
     pm.sfb = h->map_sfw;
     pm.r = h->has_r32 ? h->map_r32 : h->map_b128;
@@ -830,7 +842,7 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
     p.y = static_cast<__nv_bfloat16*>(y);
     p.ldy = ldy;
     // opt-in (debug flag 8192): measured slower than 4 full rounds for 4096^3 (partner flag + partial traffic)
-    if (left > 0 && 2 * left <= clusters && p.k_steps >= 4 && (g_debug_flags & 8192)) {
+    if (left > 0 && 2 * left <= clusters && p.k_steps >= 4 && (g_debug_flags & 8192) && !g3) {
       serq_linear* hm = const_cast<serq_linear*>(h);
       const int64_t need = left * 2 * 2 * 128 * kBN;
       if (need > hm->sk_ws_floats) {
@@ -857,14 +869,17 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(2 * clusters));
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = k3SmemBytes;
+    cfg.dynamicSmemBytes = g3 ? k3SmemBytesG : k3SmemBytes;
     cfg.stream = S(stream);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap with the quantizer's tail
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, serq_mx_pair3_kernel, pm, p));
+    if (g3)
+      CK(cudaLaunchKernelEx(&cfg, serq_mx_pair3_kernel<true>, pm, p));
+    else
+      CK(cudaLaunchKernelEx(&cfg, serq_mx_pair3_kernel<false>, pm, p));
     LAUNCH_CHECK("serq_mx_pair3_kernel");
     return SERQ_OK;
   }

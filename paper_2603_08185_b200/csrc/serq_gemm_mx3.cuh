@@ -22,10 +22,18 @@ constexpr int k3RB = 128 * 32;                // R B tile (r <= 64: 32 B per row
 constexpr int k3RSF = 1024;                   // R SFB: one chunk, both 128-row blocks
 constexpr int k3SmemBytes = 1024 + k3Slots * k3SlotBytes + k3RB + k3RSF + 4 * k2EpiStage + 512;
 static_assert(k3SmemBytes <= 232448, "exceeds the 227 KB dynamic shared memory limit");
+// gather fallback (salient set not the permuted front): the salient term's A operand is the
+// quantizer's x[:, idx] slice (128 rows x 32 B + one SF atom per CTA); the room comes from
+// halving the epilogue staging boxes (32 rows x 16 columns, no swizzle)
+constexpr int k3Xs = 128 * 32 + 512;
+constexpr int k3EpiG = 32 * 32;
+constexpr int k3SmemBytesG = 1024 + k3Slots * k3SlotBytes + k3RB + k3RSF + k3Xs + 4 * k3EpiG + 512;
+static_assert(k3SmemBytesG <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 static_assert(131072 + 32768 <= k3Slots * k3SlotBytes, "split-tile exchange regions must fit in the drained pipeline");
 
 struct Pair3Maps {
   CUtensorMap a, b, r, y, sfa, sfb, sfr;
+  CUtensorMap xs, sfxs;  // gather: the quantizer's x[:, idx] codes (32-B rows, 32B swizzle) and scale factors
   CUtensorMap ws;  // split-wave fp32 partials [slabs x 128 rows][256], box 32 x 32, 128B swizzle
 };
 
@@ -34,13 +42,16 @@ __device__ __forceinline__ void tma_load_2d_pair_nohint(uint32_t dst, const CUte
   tma_load_2d_pair(dst, m, bar, c0, c1, kEvictNormal);
 }
 
+template <bool kGather = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     serq_mx_pair3_kernel(const __grid_constant__ Pair3Maps maps, const GemmParams p) {
+  constexpr int kEpiBox = kGather ? k3EpiG : k2EpiStage;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* rbuf = smem + k3Slots * k3SlotBytes;  // R B tile (1 KB aligned) then R SFB
-  uint8_t* epi_smem = rbuf + k3RB + k3RSF;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + 4 * k2EpiStage);
+  uint8_t* xsbuf = rbuf + k3RB + k3RSF;          // gather: x[:, idx] A tile then its SF atom
+  uint8_t* epi_smem = xsbuf + (kGather ? k3Xs : 0);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + 4 * kEpiBox);
   uint64_t* full = bars;                        // [k3Slots] leader's used
   uint64_t* empty = bars + k3Slots;             // [k3Slots] both
   uint64_t* tmem_full = bars + 2 * k3Slots;     // [2] both
@@ -113,6 +124,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (has_r) {
       tma_prefetch(&maps.r);
       tma_prefetch(&maps.sfr);
+      if (kGather) {
+        tma_prefetch(&maps.xs);
+        tma_prefetch(&maps.sfxs);
+      }
     }
     for (int s = 0; s < k3Slots; ++s) {
       mbar_init(&full[s], 1);
@@ -163,7 +178,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t fbar = map_rank(smem_u32(&full[slot]), 0);
           const bool no_sf = p.dbg & 32768;  // diagnostics: skip scale-factor loads (request-count test)
           if (leader)
-            mbar_expect_tx(&full[slot], 2u * (len * (k3StepBytes - (no_sf ? 3072 : 0)) + (with_r ? k3RB + k3RSF : 0)));
+            mbar_expect_tx(&full[slot], 2u * (len * (k3StepBytes - (no_sf ? 3072 : 0)) +
+                                              (with_r ? k3RB + k3RSF + (kGather ? k3Xs : 0) : 0)));
           const uint32_t st = smem_base + slot * k3SlotBytes;
           // weights (B, SFB) never depend on the previous kernel: load them first
           for (int h = 0; h < len; ++h) {
@@ -189,6 +205,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // R SFB chunk 0 for both 128-row blocks: 512 B each = 4 rows of 128 B of the SF map
             tma_load_2d_pair_nohint(rb + k3RB, &maps.sfr, fbar, 0, ((n0 / 128) * p.kc_pad_r) * 4);
             tma_load_2d_pair_nohint(rb + k3RB + 512, &maps.sfr, fbar, 0, ((n0 / 128 + 1) * p.kc_pad_r) * 4);
+            if (kGather) {  // after griddepcontrol.wait (u > 0 or the A loads above): quantizer output
+              const uint32_t xb = smem_u32(xsbuf);
+              tma_load_2d_pair_nohint(xb, &maps.xs, fbar, 0, m_own);                    // [128 rows x 32 B]
+              tma_load_2d_pair_nohint(xb + 4096, &maps.sfxs, fbar, 0, (mblk * p.kc_pad_r) * 4);  // SF atom
+            }
           }
         }
       }
@@ -259,7 +280,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               // salient term: A = K-tile 0 of X (same smem, same SFA slot), B = R (32-B rows, 32B swizzle)
               tmem_cp_pair(kSfR, make_sdesc(rb + k3RB, 128, 128, 0));
               tmem_cp_pair(kSfR + 4, make_sdesc(rb + k3RB + 512, 128, 128, 0));
-              mma_mxf4_pair(acc, a0, make_sdesc(rb, 16, 256, 6), id0, fa0, kSfR, 1u);  // r == 64: one K=64 slice
+              if constexpr (kGather) {
+                // gather: A = the quantizer's x[:, idx] slice and its scale factors (TMEM 504..507)
+                constexpr uint32_t kSfXs = kSfR + 8;
+                const uint32_t xb = smem_u32(xsbuf);
+                tmem_cp_pair(kSfXs, make_sdesc(xb + 4096, 128, 128, 0));
+                mma_mxf4_pair(acc, make_sdesc(xb, 16, 256, 6), make_sdesc(rb, 16, 256, 6), id0, kSfXs, kSfR, 1u);
+              } else {
+                mma_mxf4_pair(acc, a0, make_sdesc(rb, 16, 256, 6), id0, fa0, kSfR, 1u);  // r == 64: one K=64 slice
+              }
               tc_commit_pair(r_empty);
             }
             if (len == 2) {
@@ -307,7 +336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ epilogue (both CTAs)
     const uint32_t q = warp & 3;
     const uint32_t lane_base = (q * 32u) << 16;
-    uint8_t* stage_out = epi_smem + q * k2EpiStage;
+    uint8_t* stage_out = epi_smem + q * kEpiBox;
     const uint32_t rbase = smem_u32(stage_out) + lane_id() * 64;
     const uint32_t sw = (lane_id() >> 1) & 3;
     const uint32_t tmem_empty_leader = map_rank(smem_u32(tmem_empty), 0);
@@ -489,22 +518,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t* src = h ? w : v;
-          uint8_t* box = final_tile ? smem + q * 16384 + (cc * 2 + h) * 2048 : stage_out;
-          const uint32_t bbase = final_tile ? smem_u32(box) + lane_id() * 64 : rbase;
-          if (!final_tile && lane_id() == 0) bulk_wait_read_all();
-          __syncwarp();
+          if constexpr (kGather) {
+            // 32 rows x 16 columns per box (1 KB, no swizzle): lane = row, 32 B each
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            st_shared_v4(bbase + ((uint32_t(j) ^ sw) * 16),
-                         pack_bf16x2(__uint_as_float(src[8 * j]), __uint_as_float(src[8 * j + 1])),
-                         pack_bf16x2(__uint_as_float(src[8 * j + 2]), __uint_as_float(src[8 * j + 3])),
-                         pack_bf16x2(__uint_as_float(src[8 * j + 4]), __uint_as_float(src[8 * j + 5])),
-                         pack_bf16x2(__uint_as_float(src[8 * j + 6]), __uint_as_float(src[8 * j + 7])));
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane_id() == 0 && m_own < p.M) {
-            tma_store_2d(&maps.y, box, n0 + c * 64 + h * 32, m_own + q * 32);
-            bulk_commit();
+            for (int sb = 0; sb < 2; ++sb) {
+              uint8_t* box = final_tile ? smem + q * 16384 + ((cc * 2 + h) * 2 + sb) * 1024 : stage_out;
+              const uint32_t bbase = smem_u32(box) + lane_id() * 32;
+              if (!final_tile && lane_id() == 0) bulk_wait_read_all();
+              __syncwarp();
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                st_shared_v4(bbase + j * 16,
+                             pack_bf16x2(__uint_as_float(src[16 * sb + 8 * j]), __uint_as_float(src[16 * sb + 8 * j + 1])),
+                             pack_bf16x2(__uint_as_float(src[16 * sb + 8 * j + 2]), __uint_as_float(src[16 * sb + 8 * j + 3])),
+                             pack_bf16x2(__uint_as_float(src[16 * sb + 8 * j + 4]), __uint_as_float(src[16 * sb + 8 * j + 5])),
+                             pack_bf16x2(__uint_as_float(src[16 * sb + 8 * j + 6]), __uint_as_float(src[16 * sb + 8 * j + 7])));
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane_id() == 0 && m_own < p.M) {
+                tma_store_2d(&maps.y, box, n0 + c * 64 + h * 32 + sb * 16, m_own + q * 32);
+                bulk_commit();
+              }
+            }
+          } else {
+            uint8_t* box = final_tile ? smem + q * 16384 + (cc * 2 + h) * 2048 : stage_out;
+            const uint32_t bbase = final_tile ? smem_u32(box) + lane_id() * 64 : rbase;
+            if (!final_tile && lane_id() == 0) bulk_wait_read_all();
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              st_shared_v4(bbase + ((uint32_t(j) ^ sw) * 16),
+                           pack_bf16x2(__uint_as_float(src[8 * j]), __uint_as_float(src[8 * j + 1])),
+                           pack_bf16x2(__uint_as_float(src[8 * j + 2]), __uint_as_float(src[8 * j + 3])),
+                           pack_bf16x2(__uint_as_float(src[8 * j + 4]), __uint_as_float(src[8 * j + 5])),
+                           pack_bf16x2(__uint_as_float(src[8 * j + 6]), __uint_as_float(src[8 * j + 7])));
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane_id() == 0 && m_own < p.M) {
+              tma_store_2d(&maps.y, box, n0 + c * 64 + h * 32, m_own + q * 32);
+              bulk_commit();
+            }
           }
         }
       }
