@@ -452,6 +452,21 @@ def forward_reconstructed(x, main, comp, act_cfg, probe: OpProbe | None = None) 
     return y.float().cpu().numpy().astype(np.float64)
 
 
+def layer_forward(art, x, probe: OpProbe | None = None) -> np.ndarray:
+    """Drop-in for pipeline.layer_forward (pipeline.py:126-131): divide the activation
+    columns by the SAF smoothing scales (flatten.py:62-67, host float64 exactly as the
+    reference) and run forward_reconstructed on the device.  ``art`` is the reference's
+    LayerArtifacts (main, comp, act_cfg, smoothing) or any object with those fields."""
+    x = _as_matrix(x)
+    smoothing = getattr(art, "smoothing", None)
+    if smoothing is not None:
+        s = np.asarray(smoothing.s, dtype=np.float64)
+        if s.shape[0] != x.shape[1]:
+            raise ValidationError("plan length does not match activation columns")
+        x = x / s[None, :]
+    return forward_reconstructed(x, art.main, art.comp, art.act_cfg, probe)
+
+
 def forward_symmetric_act(x, main, comp, act_cfg: IntQuantConfig) -> np.ndarray:
     """BASELINE config 1: symmetric per-token activations.  The reference
     forward rejects symmetric act_cfg (compensate.py:298-299); this is the

@@ -47,6 +47,7 @@ from serq.quantcore import (  # noqa: E402
     quantize_symmetric,
 )
 from serq.saliency import build_plan, score_rows  # noqa: E402
+from serq.pipeline import layer_forward, quantize_layer  # noqa: E402
 from serq.gptq import GptqConfig, HessianState, accumulate_hessian  # noqa: E402
 from serq.tensorio import SyntheticSpec, gen_synthetic_activations  # noqa: E402
 from serq.flatten import compute_smoothing_scales  # noqa: E402
@@ -229,6 +230,26 @@ def main():
     for bits in (4, 8):
         g[f"fgptq_y_a{bits}"] = forward_reconstructed(xg, mq, cq, per_token_config(bits))
     g["fgrp_x"], g["fgrp_w"] = xg, wg
+
+    # -- pipeline.quantize_layer / layer_forward (SAF smoothing + salient plan built by the
+    #    reference; the layer's salient set is NOT the permuted front: the gather fallback)
+    calib_l = gen_synthetic_activations(SyntheticSpec(rows=64 + 12, cols=256, n_outlier_channels=3,
+                                                      outlier_magnitude=50.0, seed=5))
+    w_l = np.random.default_rng(6).standard_normal((256, 128)) * 0.02
+    x_l = bf16(calib_l[64:])
+    for fmt, rank in (("mxfp4", 64), ("int", 128)):
+        art = quantize_layer(w_l, calib_l[:64], rank=rank, fmt=fmt, weight_group=128 if fmt == "int" else "per-row")
+        tag = f"flayer_{fmt}"
+        g[f"{tag}_s"] = art.smoothing.s
+        g[f"{tag}_idx"] = art.comp.salient_idx
+        if fmt == "mxfp4":
+            g[f"{tag}_codes"], g[f"{tag}_exps"] = art.main.element_codes, art.main.block_scale_exponents
+            g[f"{tag}_r_codes"], g[f"{tag}_r_exps"] = art.comp.r_q.element_codes, art.comp.r_q.block_scale_exponents
+        else:
+            g[f"{tag}_codes"], g[f"{tag}_scales"] = art.main.codes, art.main.scales
+            g[f"{tag}_r_codes"], g[f"{tag}_r_scales"] = art.comp.r_q.codes, art.comp.r_q.scales
+        g[f"{tag}_y"] = layer_forward(art, x_l)
+    g["flayer_x"] = x_l
 
     # -- a small bundle written by the reference's own save_bundle (bundleio.py:73-126), for the
     #    device bundle loader: MX main + MX R, INT main + INT R, INT main + SVD factors

@@ -275,3 +275,34 @@ def test_forward_reconstructed_grouped_and_gptq_golden(gpu, golden):
         y = api.forward_reconstructed(xg, main, comp, api.per_token_config(bits))
         mx, mean = O.parity_errors(y, golden[f"fgptq_y_a{bits}"])
         assert mx <= TOL_MAX and mean <= TOL_MEAN, (bits, mx, mean)
+
+
+@pytest.mark.gpu
+def test_layer_forward_golden(gpu, golden):
+    # pipeline.quantize_layer artefacts built by the reference (SAF smoothing, a salient plan that
+    # is not the permuted front: the gather fallback) through the layer_forward drop-in
+    from types import SimpleNamespace
+
+    x = golden["flayer_x"]
+    k = x.shape[1]
+    for fmt in ("mxfp4", "int"):
+        t = f"flayer_{fmt}"
+        idx = golden[f"{t}_idx"]
+        r = idx.size
+        if fmt == "mxfp4":
+            n = golden[f"{t}_codes"].shape[0]
+            main = api.MxBlockTensor(golden[f"{t}_codes"], golden[f"{t}_exps"], 32, (n, k))
+            rq = api.MxBlockTensor(golden[f"{t}_r_codes"], golden[f"{t}_r_exps"], 32, (n, r))
+            act_cfg = None
+        else:
+            n = golden[f"{t}_codes"].shape[1]
+            main = api.QuantizedTensor(golden[f"{t}_codes"], golden[f"{t}_scales"], None,
+                                       api.IntQuantConfig(4, True, 128, "row"), (k, n))
+            rq = api.QuantizedTensor(golden[f"{t}_r_codes"], golden[f"{t}_r_scales"], None,
+                                     api.IntQuantConfig(4, True, n, "col"), (r, n))
+            act_cfg = api.per_token_config(8)
+        art = SimpleNamespace(main=main, comp=api.Compensator(api.RTN_RESIDUAL, r, idx, r_q=rq), act_cfg=act_cfg,
+                              smoothing=SimpleNamespace(s=golden[f"{t}_s"]))
+        y = api.layer_forward(art, x)
+        mx, mean = O.parity_errors(y, golden[f"{t}_y"])
+        assert mx <= TOL_MAX and mean <= TOL_MEAN, (fmt, mx, mean)
