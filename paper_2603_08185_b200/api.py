@@ -467,6 +467,18 @@ def layer_forward(art, x, probe: OpProbe | None = None) -> np.ndarray:
     return forward_reconstructed(x, art.main, art.comp, art.act_cfg, probe)
 
 
+def predict(estimator, X, probe: OpProbe | None = None) -> np.ndarray:
+    """SerqQuantizer.predict (estimators.py:89-97) on the device, for an estimator fitted by
+    the reference (its ``artifacts_`` are the LayerArtifacts of quantize_layer): the same
+    not-fitted / feature-count ValidationErrors, then layer_forward."""
+    if not hasattr(estimator, "artifacts_"):
+        raise ValidationError("estimator is not fitted")
+    X = _as_matrix(X, "X")
+    if X.shape[1] != estimator.n_features_in_:
+        raise ValidationError(f"X has {X.shape[1]} features, expected {estimator.n_features_in_}")
+    return layer_forward(estimator.artifacts_, X, probe)
+
+
 def forward_symmetric_act(x, main, comp, act_cfg: IntQuantConfig) -> np.ndarray:
     """BASELINE config 1: symmetric per-token activations.  The reference
     forward rejects symmetric act_cfg (compensate.py:298-299); this is the

@@ -306,3 +306,14 @@ def test_layer_forward_golden(gpu, golden):
         y = api.layer_forward(art, x)
         mx, mean = O.parity_errors(y, golden[f"{t}_y"])
         assert mx <= TOL_MAX and mean <= TOL_MEAN, (fmt, mx, mean)
+
+
+def test_predict_validation_mirrors_estimator():
+    # estimators.py:86-97: not fitted / wrong feature count raise before any device work
+    from types import SimpleNamespace
+
+    with pytest.raises(ValidationError, match="not fitted"):
+        api.predict(SimpleNamespace(), np.ones((2, 8)))
+    est = SimpleNamespace(artifacts_=None, n_features_in_=8)
+    with pytest.raises(ValidationError, match="features"):
+        api.predict(est, np.ones((2, 7)))
