@@ -317,3 +317,10 @@ def test_predict_validation_mirrors_estimator():
     est = SimpleNamespace(artifacts_=None, n_features_in_=8)
     with pytest.raises(ValidationError, match="features"):
         api.predict(est, np.ones((2, 7)))
+
+
+def test_empty_input_rejected_like_reference():
+    # _validation.as_matrix (reference): "x must be non-empty" before any device work
+    main = api.MxBlockTensor(np.zeros((32, 64), np.uint8), np.zeros((32, 2), np.int32), 32, (32, 64))
+    with pytest.raises(ValidationError, match="non-empty"):
+        api.forward_reconstructed(np.zeros((0, 64)), main, None, None)
