@@ -180,6 +180,10 @@ int serq_linear_int_addend(const serq_linear_t* h, const int8_t* a_codes, const 
  * in, quantize, GEMM, copy Y (bf16 [M, N]) out; synchronises `stream`.
  * Device scratch lives in the handle and grows on demand. */
 int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* y_host, serq_stream_t stream);
+/* serq_forward_mx_host for a non-contiguous salient set: gather_idx (device int32 [r]) as in
+ * serq_forward_mx; the salient slice is re-encoded per chunk on the device. */
+int serq_forward_mx_host_gather(serq_linear_t* h, const void* x_host, int64_t M, const int32_t* gather_idx,
+                                void* y_host, serq_stream_t stream);
 
 /* Number of kernels the last forward on this thread launched (evidence for bench). */
 int serq_last_launch_count(void);

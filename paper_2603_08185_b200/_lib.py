@@ -46,6 +46,7 @@ SIGNATURES = {
     "serq_linear_int": (_I, [_P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P]),
     "serq_linear_int_addend": (_I, [_P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P]),
     "serq_forward_mx": (_I, [_P, _P, _I, _I64, _I64, _P, _P, _P, _P, _P, _P, _I64, _P]),
+    "serq_forward_mx_host_gather": (_I, [_P, _P, _I64, _P, _P, _P]),
     "serq_forward_mx_host": (_I, [_P, _P, _I64, _P, _P]),
     "serq_last_launch_count": (_I, []),
     "serq_set_debug_flags": (_I, [_I]),

@@ -178,6 +178,8 @@ struct serq_linear {
   uint8_t* ws_codes = nullptr;
   uint8_t* ws_sf = nullptr;
   void* ws_y = nullptr;
+  uint8_t* ws_xs = nullptr;   // gather layers: x[:, idx] codes and scale factors per chunk
+  uint8_t* ws_xsf = nullptr;
   // end-to-end pipeline: H2D and D2H copy streams + per-chunk events (created lazily)
   cudaStream_t e2e_in = nullptr, e2e_out = nullptr;
   std::mutex e2e_mu;  // the end-to-end scratch and streams are per handle: one host call at a time
@@ -188,7 +190,7 @@ namespace {
 void free_handle(serq_linear* h) {
   void* ptrs[] = {h->w, h->sfw, h->rbuf, h->sfr, h->sw, h->colsum, h->sr, h->colsum_r,
                   h->ws_x, h->ws_codes, h->ws_sf, h->ws_y, h->sk_ws, h->sk_cnt, h->w4,
-                  h->sw_g, h->colsum_g, h->cterm};
+                  h->sw_g, h->colsum_g, h->cterm, h->ws_xs, h->ws_xsf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : h->e2e_ev)
@@ -1135,24 +1137,35 @@ int serq_linear_int_addend(const serq_linear_t* h, const int8_t* a_codes, const 
 }
 
 int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* y_host, serq_stream_t stream) {
+  return serq_forward_mx_host_gather(h, x_host, M, nullptr, y_host, stream);
+}
+
+int serq_forward_mx_host_gather(serq_linear_t* h, const void* x_host, int64_t M, const int32_t* gather_idx,
+                                void* y_host, serq_stream_t stream) {
   if (!h || h->mode != kModeMX) return fail(SERQ_EINVAL, "handle is not an MX linear");
   std::lock_guard<std::mutex> lock(h->e2e_mu);
-  if (h->r > 0 && !h->contiguous)
-    return fail(SERQ_EINVAL, "serq_forward_mx_host supports the permuted (contiguous) salient layout only");
+  const bool gather = h->r > 0 && !h->contiguous;
+  if (gather && !gather_idx)
+    return fail(SERQ_EINVAL, "a non-contiguous salient set needs gather_idx (serq_forward_mx_host_gather)");
   if (M <= 0) return fail(SERQ_EINVAL, "x must be non-empty");
   cudaStream_t st = S(stream);
-  if (M > h->ws_m) {
-    for (void* p : {h->ws_x, (void*)h->ws_codes, (void*)h->ws_sf, h->ws_y})
+  if (M > h->ws_m || (gather && !h->ws_xs)) {
+    for (void* p : {h->ws_x, (void*)h->ws_codes, (void*)h->ws_sf, h->ws_y, (void*)h->ws_xs, (void*)h->ws_xsf})
       if (p) cudaFree(p);
     h->ws_x = h->ws_y = nullptr;
-    h->ws_codes = h->ws_sf = nullptr;
-    const int64_t mm = cdiv(M, 128) * 128;
+    h->ws_codes = h->ws_sf = h->ws_xs = h->ws_xsf = nullptr;
+    const int64_t mm = cdiv(M > h->ws_m ? M : h->ws_m, 128) * 128;
     CK(cudaMalloc(&h->ws_x, mm * h->K * 2));
     CK(cudaMalloc(&h->ws_codes, mm * h->K / 2));
     CK(cudaMalloc(&h->ws_sf, sf_bytes_of(mm, h->K)));
     CK(cudaMalloc(&h->ws_y, mm * h->N * 2));
+    if (gather) {
+      CK(cudaMalloc(&h->ws_xs, mm * h->r / 2));
+      CK(cudaMalloc(&h->ws_xsf, sf_bytes_of(mm, h->r)));
+    }
     h->ws_m = mm;
   }
+  const int64_t kc_pad_r = gather ? kc_pad_of(h->r) : 0;
   // Chunked over token rows (multiples of 256) so that the H2D copy of chunk
   // i+1, the quantize + fused linear of chunk i and the D2H copy of chunk i-1
   // run concurrently on the two copy engines and the SMs.
@@ -1233,14 +1246,16 @@ int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* 
     const int64_t r0 = start[c], mc = plan[c];
     uint8_t* codes = h->ws_codes + r0 * h->K / 2;
     uint8_t* sf = h->ws_sf + (r0 / 128) * kc_pad * 512;
+    // chunks start on 256-row boundaries, so their scale-factor tiles start on row-block boundaries
+    uint8_t* xs = gather ? h->ws_xs + r0 * h->r / 2 : nullptr;
+    uint8_t* xsf = gather ? h->ws_xsf + (r0 / 128) * kc_pad_r * 512 : nullptr;
     CK(cudaStreamWaitEvent(st, ev_in[c], 0));
     if (timing) CK(cudaEventRecord(tev[kE2eMaxChunks + c], st));
     int rc = serq_act_quant_mx(static_cast<uint8_t*>(h->ws_x) + r0 * h->K * 2, SERQ_BF16, mc, h->K, h->K, codes, sf,
-                               nullptr, 0, nullptr, nullptr, stream);
+                               gather ? gather_idx : nullptr, gather ? h->r : 0, xs, xsf, stream);
     if (rc) return rc;
     launches += g_launches;
-    rc = serq_linear_mx(h, codes, sf, mc, nullptr, nullptr, static_cast<uint8_t*>(h->ws_y) + r0 * h->N * 2, h->N,
-                        stream);
+    rc = serq_linear_mx(h, codes, sf, mc, xs, xsf, static_cast<uint8_t*>(h->ws_y) + r0 * h->N * 2, h->N, stream);
     if (rc) return rc;
     launches += g_launches;
     CK(cudaEventRecord(ev_done[c], st));

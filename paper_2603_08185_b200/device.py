@@ -272,8 +272,8 @@ class MxLinear:
         """End to end from (pinned) host bf16 memory through the C-ABI."""
         if x_host.is_cuda or y_host.is_cuda:
             raise ValidationError("forward_host takes host tensors")
-        _lib.call("serq_forward_mx_host", self._h.ptr, x_host.data_ptr(), x_host.shape[0], y_host.data_ptr(),
-                  _stream())
+        _lib.call("serq_forward_mx_host_gather", self._h.ptr, x_host.data_ptr(), x_host.shape[0],
+                  _ptr(self.gather_idx), y_host.data_ptr(), _stream())
 
 
 class IntLinear:

@@ -403,6 +403,25 @@ def test_mx_forward_host_chunked(D, M):
         assert torch.equal(yd, yh)
 
 
+@pytest.mark.parametrize("M", [1000, 2600])
+def test_mx_forward_host_chunked_gather(D, M):
+    # the host pipeline on a non-contiguous salient set: the salient slice is
+    # re-encoded per chunk and every chunk reaches the gather variant of the linear
+    K, N, r = 1024, 512, 64
+    x = _bf16_outlier_x(M, K, seed=M + 9)
+    w = np.random.default_rng(M).standard_normal((K, N)) * 0.02
+    idx = np.random.default_rng(M + 1).permutation(K)[:r]
+    main_t, comp = O.build_serq_rtn_mx(w, idx, 32)
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                     comp.r_q.block_scale_exponents, idx)
+    assert not lin.contiguous
+    xh = torch.from_numpy(x).to(torch.bfloat16).pin_memory()
+    yh = torch.empty((M, N), dtype=torch.bfloat16).pin_memory()
+    lin.forward_host(xh, yh)
+    mx, mean = O.parity_errors(yh.float().numpy(), O.forward_mx(x, main_t, comp))
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
 @pytest.mark.parametrize("M,K,N", [(4096, 1024, 1024), (1000, 2048, 768), (2600, 512, 4096)])
 def test_mx_forward_fused_equals_two_launches(D, M, K, N):
     # serq_forward_mx (one C-ABI call, PDL between the two kernels) must equal
