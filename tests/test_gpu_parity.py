@@ -228,6 +228,25 @@ def test_int_linear_parity(D, bits, symmetric, r_mode):
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
 
 
+@pytest.mark.parametrize("M,N,r_mode", [(300, 520, "int"), (257, 1000, "dense"), (129, 136, "int")])
+def test_int_linear_ragged_narrow_tiles(D, M, N, r_mode):
+    # few tiles -> the 128-column CTA-pair tiles; ragged M and N (partial last tiles)
+    K, r = 1024, 64
+    x = _bf16_outlier_x(M, K, seed=M + N)
+    w = np.random.default_rng(N).standard_normal((K, N)) * 0.02
+    main, comp = O.build_per_channel_int(w, np.arange(r), r_mode=r_mode)
+    kw = dict(r_dense=comp.r_dense) if r_mode == "dense" else dict(r_codes=comp.r_q.codes, r_scales=comp.r_q.scales)
+    lin = D.IntLinear(main.codes, main.scales, 4, salient_idx=np.arange(r), **kw)
+    act = lin.quantize(_cuda(x, torch.bfloat16), 8, False)
+    acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    y = lin.gemm(act, acc_dump=acc).float().cpu().numpy()
+    y_ref, xq = O.forward_int(x, main, comp, O.IntCfg(8, False, "per-row"))
+    _, parts = O.int_gemm(xq, main, return_partials=True)
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), parts[0][1])
+    mx, mean = O.parity_errors(y, y_ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
 def test_int_linear_golden(D, golden):
     x, w = golden["fint_x"], golden["fint_w"]
     main, comp = O.build_per_channel_int(w, np.arange(32), r_mode="int")
