@@ -154,6 +154,7 @@ struct serq_linear {
   int32_t* colsum_r = nullptr;
   CUtensorMap map_b, map_r;
   CUtensorMap map_b128, map_r128, map_sfw, map_sfr;  // CTA-pair kernel: 128-row B boxes, scale-factor maps
+  CUtensorMap map_b64;                                // pair3 narrow (256 x 128) last-round tiles: 64-row B boxes
   CUtensorMap map_r32, map_sfr4;                     // pair3 kernel: R as 32-B swizzled rows, 512-B SF boxes
   bool has_r32 = false;
   void* w4 = nullptr;                                // INT: packed int4 weights, tiled [N/128][K/128][128][64 B]
@@ -392,6 +393,7 @@ int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K
                                                                   kc_pad_of(K), h->w_ksteps);
   if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_mx launch failed"));
   int rc = make_map(&h->map_b128, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, 128, uint64_t(w_bytes / 128), 128, 128, 128);
+  if (!rc) rc = make_map(&h->map_b64, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, 128, uint64_t(w_bytes / 128), 128, 128, 64);
   h->map_b = h->map_b128;
   if (!rc) rc = make_sf_map(&h->map_sfw, h->sfw, N, K);
   if (rc) return bail(rc);
@@ -830,6 +832,7 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
     if (rc) return rc;
     if (!g3) pm.xs = pm.sfxs = pm.a;  // unused
     pm.b = h->map_b128;
+    pm.b64 = h->map_b64;
     pm.sfb = h->map_sfw;
     pm.r = h->has_r32 ? h->map_r32 : h->map_b128;
     pm.sfr = h->has_r32 ? h->map_sfr4 : h->map_sfw;
@@ -839,6 +842,7 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
     // split the last partial wave into K-halves when they fit in one round
     const int64_t rounds = pairs / clusters, left = pairs - rounds * clusters;
     p.split_from = int(pairs);
+    p.narrow_from = int(pairs);
     // tile order: N-fastest measured +2.4% at 8192^3, equal at 4096^3 (tools/sweep_mx.py)
     p.group_m = (g_debug_flags & 262144) ? 0 : 1;
     p.y = static_cast<__nv_bfloat16*>(y);
@@ -867,6 +871,11 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
       p.sk_ws = hm->sk_ws;
       p.sk_cnt = hm->sk_cnt;
     }
+    // the last partial round as 256 x 128 tiles (two per leftover tile, no K split, no exchange):
+    // each takes ~3/4 of a full tile's time (the A operand is fed twice) instead of half the
+    // clusters idling through a full tile; debug flag 1<<19 disables
+    if (p.split_from >= int(pairs) && left > 0 && 2 * left <= clusters && rounds >= 1 && !(g_debug_flags & (1 << 19)))
+      p.narrow_from = int(rounds * clusters);
     if (p.split_from >= int(pairs)) pm.ws = pm.y;  // unused
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(2 * clusters));

@@ -33,6 +33,7 @@ static_assert(131072 + 32768 <= k3Slots * k3SlotBytes, "split-tile exchange regi
 
 struct Pair3Maps {
   CUtensorMap a, b, r, y, sfa, sfb, sfr;
+  CUtensorMap b64;       // narrow tiles: 64-row B boxes (each CTA's half of a 128-wide N tile)
   CUtensorMap xs, sfxs;  // gather: the quantizer's x[:, idx] codes (32-B rows, 32B swizzle) and scale factors
   CUtensorMap ws;  // split-wave fp32 partials [slabs x 128 rows][256], box 32 x 32, 128B swizzle
 };
@@ -79,10 +80,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int units = (p.k_steps + 1) >> 1;       // slots per tile (last one may hold a single step)
   // work items: tiles [0, split_from) whole, then every remaining tile as two K-halves
   const int split_from = min(p.split_from, n_tiles);
-  const int n_items = split_from + 2 * (n_tiles - split_from);
+  // or: tiles [0, narrow_from) whole, then every remaining tile as two 256 x 128 tiles
+  const int narrow_from = split_from < n_tiles ? 0x7fffffff : min(p.narrow_from, n_tiles);
+  const int n_items = split_from < n_tiles ? split_from + 2 * (n_tiles - split_from)
+                                           : narrow_from + 2 * (n_tiles - narrow_from);
   const int half_units = units >> 1;
   struct Item {
     int tile, half, lo, hi;  // half: -1 = whole tile; [lo, hi) = k-unit range
+    int nsub;                // -1: 256 columns; 0 / 1: the first / second 128 columns only
   };
   // tile -> (M tile, N tile): M fastest, or grouped (group_m M-tiles x all N-tiles per group)
   auto tile_mn = [&](int tile, int& mt, int& nt) {
@@ -100,7 +105,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   };
   auto item_of = [&](int w) {
     Item it;
-    if (w < split_from) {
+    it.nsub = -1;
+    if (w >= narrow_from) {
+      const int j = w - narrow_from;
+      it.tile = narrow_from + (j >> 1);
+      it.nsub = j & 1;
+      it.half = -1;
+      it.lo = 0;
+      it.hi = units;
+    } else if (w < split_from) {
       it.tile = w;
       it.half = -1;
       it.lo = 0;
@@ -164,8 +177,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int mt, nt;
         tile_mn(tile, mt, nt);
         const int m_own = mt * 256 + int(rank) * 128;
-        const int n0 = nt * kBN;
-        const int n_half = n0 + int(rank) * 128;
+        const bool narrow = itm.nsub >= 0 && !(p.dbg & 96);  // diagnostics 32 / 64: full-tile loads
+        const int n0 = nt * kBN + (narrow ? itm.nsub * 128 : 0);
+        const int n_half = n0 + int(rank) * (narrow ? 64 : 128);
         const int mblk = m_own / 128;
         for (int uu = itm.lo; uu < itm.hi; ++uu, ++u) {
           const int slot = u % k3Slots;
@@ -178,19 +192,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t fbar = map_rank(smem_u32(&full[slot]), 0);
           const bool no_sf = p.dbg & 32768;  // diagnostics: skip scale-factor loads (request-count test)
           if (leader)
-            mbar_expect_tx(&full[slot], 2u * (len * (k3StepBytes - (no_sf ? 3072 : 0)) +
+            mbar_expect_tx(&full[slot], 2u * (len * (k3StepBytes - (no_sf ? 3072 : 0) - (narrow ? 8192 + 1024 : 0)) +
                                               (with_r ? k3RB + k3RSF + (kGather ? k3Xs : 0) : 0)));
           const uint32_t st = smem_base + slot * k3SlotBytes;
           // weights (B, SFB) never depend on the previous kernel: load them first
           for (int h = 0; h < len; ++h) {
             const uint32_t ss = st + h * k3StepBytes;
             const int kk = k0 + h;
-            tma_load_2d_pair_nohint(ss + k2SmemA, &maps.b, fbar, 0, ((n_half >> 7) * p.w_ksteps + kk) * 128);
+            if (narrow)  // 64 rows: this CTA's half of the 128-row pre-tiled block
+              tma_load_2d_pair_nohint(ss + k2SmemA, &maps.b64, fbar, 0,
+                                      ((n_half >> 7) * p.w_ksteps + kk) * 128 + (n_half & 127));
+            else
+              tma_load_2d_pair_nohint(ss + k2SmemA, &maps.b, fbar, 0, ((n_half >> 7) * p.w_ksteps + kk) * 128);
             if (no_sf) continue;
             tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB + k2SmemSFA, &maps.sfb, fbar, 0,
                                     ((n0 / 128) * p.kc_pad + 2 * kk) * 4);
-            tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB + k2SmemSFA + 1024, &maps.sfb, fbar, 0,
-                                    ((n0 / 128 + 1) * p.kc_pad + 2 * kk) * 4);
+            if (!narrow)
+              tma_load_2d_pair_nohint(ss + k2SmemA + k2SmemB + k2SmemSFA + 1024, &maps.sfb, fbar, 0,
+                                      ((n0 / 128 + 1) * p.kc_pad + 2 * kk) * 4);
           }
           if (u == 0) pdl_wait();  // activations come from the quantizer launched just before
           for (int h = 0; h < len; ++h) {
@@ -219,7 +238,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (leader) {
       const uint32_t smem_base = smem_u32(smem);
       const uint32_t rb = smem_u32(rbuf);
-      constexpr uint32_t id0 = idesc_mxf4(256, kBN), id1 = id0 | (2u << 4) | (2u << 29);
+      constexpr uint32_t id0w = idesc_mxf4(256, kBN), id1w = id0w | (2u << 4) | (2u << 29);
+      constexpr uint32_t id0n = idesc_mxf4(256, 128), id1n = id0n | (2u << 4) | (2u << 29);
       constexpr uint32_t kSfR = kSfBase + 2 * kSfCols;  // R's SFB slot: 8 columns at 496
       uint32_t total = 0;
       for (int i = 0; i < my_tiles; ++i) {
@@ -236,6 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tmem_cp_pair(fb + 12, make_sdesc(sb + 1536, 128, 128, 0));
       };
       // 4 MMAs (K = 256) of one step
+      uint32_t id0 = id0w, id1 = id1w;
       auto step4 = [&](uint32_t acc, uint64_t a, uint64_t b, uint32_t fa, uint32_t fb, uint32_t first, int n) {
         mma_mxf4_pair(acc, a, b, id0, fa, fb, first);
         mma_mxf4_pair(acc, a + 2, b + 2, id1, fa | (2u << 30), fb | (2u << 30), 1u);
@@ -259,6 +280,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_after();
         }
         const Item itm = item_of(cluster_id + i * n_clusters);
+        id0 = itm.nsub >= 0 && !(p.dbg & 64) ? id0n : id0w;  // diagnostics 64: 256-wide MMAs
+        id1 = itm.nsub >= 0 && !(p.dbg & 64) ? id1n : id1w;
         for (int uu = itm.lo; uu < itm.hi; ++uu, ++u) {
           const int slot = u % k3Slots;
           const int len = (2 * uu + 1 < p.k_steps) ? 2 : 1;
@@ -348,7 +371,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int mt, nt;
       tile_mn(tile, mt, nt);
       const int m_own = mt * 256 + int(rank) * 128;
-      const int n0 = nt * kBN;
+      const int n0 = nt * kBN + (itm.nsub >= 0 ? itm.nsub * 128 : 0);
+      const int n_chunks = itm.nsub >= 0 ? 2 : 4;
       const uint32_t b = i & 1;
 #ifdef SERQ_DIAG_TS
       // per CTA, per work item (< 6): [before tmem_full, after tmem_full, item epilogue done, half]
@@ -501,8 +525,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         continue;
       }
 #pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        const int c = b ? cc : (cc + 3) & 3;
+      for (int cc = 0; cc < n_chunks; ++cc) {
+        const int c = (b || n_chunks == 2) ? cc : (cc + 3) & 3;
         uint32_t v[32], w[32];
         tmem_ld_32x32b_x32(acc + c * 64, v);
         tmem_ld_32x32b_x32(acc + c * 64 + 32, w);

@@ -402,6 +402,30 @@ def test_mx_linear_split_last_wave(D):
         _lib.load().serq_set_debug_flags(0)
 
 
+@pytest.mark.parametrize("M,K,N", [(2560, 1024, 2048), (2600, 512, 4096), (4096, 1024, 4096)])
+def test_mx_linear_narrow_last_round(D, M, K, N):
+    # the leftover tiles of the last partial round run as 256 x 128 tiles (two per tile):
+    # parity with the oracle and bit-equality with the all-256-wide schedule (debug flag 1<<19)
+    r = 64
+    x, main_t, comp = _mx_case(M, K, N, r, seed=M + N)
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                     comp.r_q.block_scale_exponents, np.arange(r))
+    xt = _cuda(x, torch.bfloat16)
+    y = lin(xt).float().cpu().numpy()
+    from paper_2603_08185_b200 import _lib
+
+    _lib.load().serq_set_debug_flags(1 << 19)
+    try:
+        y_wide = lin(xt).float().cpu().numpy()
+    finally:
+        _lib.load().serq_set_debug_flags(0)
+    assert np.array_equal(y, y_wide)
+    rows = np.r_[0:64, M - 300:M]  # oracle on the first rows and on the last (narrow-tile) rows
+    ref = O.forward_mx(x[rows], main_t, comp)
+    mx, mean = O.parity_errors(y[rows], ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
 @pytest.mark.parametrize("M", [1000, 300, 4096])
 def test_mx_forward_host_chunked(D, M):
     # serq_forward_mx_host pipelines H2D / quantize+linear / D2H over 256-row
