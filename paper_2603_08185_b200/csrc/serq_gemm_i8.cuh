@@ -39,7 +39,7 @@ struct I8Cfg {
   static constexpr int kStages = kDirect ? 5 : 4;
   static constexpr int kBp = kDirect ? 0 : kI8Bp;
   static constexpr int kStage = kI8A + kBp + kI8B;
-  static constexpr int kSmem = 1024 + kStages * kStage + kI8Side + kI8Const + 4 * 2048 + 512;
+  static constexpr int kSmem = 1024 + kStages * kStage + kI8Side + kI8Const + 4 * 4096 + 512;
   static constexpr int kThreads = kDirect ? 256 : kI8Threads;
   static_assert(kSmem <= 232448, "smem budget");
 };
@@ -126,8 +126,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
   uint8_t* side = smem + kI8Stages * kI8Stage;       // [A' 16K][B_R 16K]
   float* cst_f = reinterpret_cast<float*>(side + kI8Side);  // sw[256] | sr[256]
   int32_t* cst_i = reinterpret_cast<int32_t*>(cst_f + 512); // colsum[256] | colsum_r[256]
-  uint8_t* epi = reinterpret_cast<uint8_t*>(cst_i + 512);   // 4 x 2 KB staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + 4 * 2048);
+  uint8_t* epi = reinterpret_cast<uint8_t*>(cst_i + 512);   // 4 warps x 2 x 2 KB staging (ping-pong)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + 4 * 4096);
   uint64_t* full = bars;                       // [S] leader: A (+ side) landed, both CTAs
   uint64_t* bpk = bars + kI8Stages;            // [S] local: packed B landed
   uint64_t* bready = bars + 2 * kI8Stages;     // [S] leader: both CTAs widened B (+ A landed), 16 warps
@@ -362,8 +362,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
     pdl_launch_dependents();
     const uint32_t q = warp & 3;
     const uint32_t lane_base = (q * 32u) << 16;
-    uint8_t* stage_out = epi + q * 2048;
-    const uint32_t rbase = smem_u32(stage_out) + lane_id() * 64;
+    uint8_t* stage_out = epi + q * 4096;
     const uint32_t swz = (lane_id() >> 1) & 3;
     const uint32_t tmem_empty_leader = map_rank(smem_u32(tmem_empty), 0);
     for (int i = 0; i < my_tiles; ++i) {
@@ -403,7 +402,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
         uint32_t packed[16];
 #pragma unroll
 #ifdef SERQ_DIAG_TS
-        if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == 1) p.dbg_ts[5300 + c * 8 + 0] = globaltimer();
+        if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == (my_tiles > 1 ? 1 : 0)) p.dbg_ts[5300 + c * 8 + 0] = globaltimer();
 #endif
         for (int h = 0; h < 2; ++h) {
           uint32_t v[16], w[16];
@@ -412,7 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
           if (has_r) tmem_ld_32x32b_x16(lane_base + 256 + col0, w);
           tmem_ld_wait();
 #ifdef SERQ_DIAG_TS
-          if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == 1) p.dbg_ts[5300 + c * 8 + 4 + h] = globaltimer();
+          if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == (my_tiles > 1 ? 1 : 0)) p.dbg_ts[5300 + c * 8 + 4 + h] = globaltimer();
 #endif
           if (c == kN / 32 - 1 && h == 1) {
             tc_fence_before();
@@ -468,12 +467,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
           for (int j = 0; j < 8; ++j) packed[h * 8 + j] = pack_bf16x2(f[2 * j], f[2 * j + 1]);
         }
 #ifdef SERQ_DIAG_TS
-        if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == 1) p.dbg_ts[5300 + c * 8 + 1] = globaltimer();
+        if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == (my_tiles > 1 ? 1 : 0)) p.dbg_ts[5300 + c * 8 + 1] = globaltimer();
 #endif
-        if (lane_id() == 0) bulk_wait_read_all();
+        // the CTA's final tile: the pipeline is drained (its last MMAs completed before tmem_full), so
+        // every chunk gets its own 2 KB box there and no store waits on another; otherwise two
+        // boxes per warp alternate and a box is rewritten once the store from two chunks ago read it
+        const bool final_tile = i == my_tiles - 1 && !(p.dbg & (1 << 26));
+        uint8_t* box = final_tile ? smem + (int(q) * (kN / 32) + c) * 2048 : stage_out + (c & 1) * 2048;
+        const uint32_t rbase = smem_u32(box) + lane_id() * 64;
+        if (!final_tile && lane_id() == 0) bulk_wait_read_1();
         __syncwarp();
 #ifdef SERQ_DIAG_TS
-        if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == 1) p.dbg_ts[5300 + c * 8 + 2] = globaltimer();
+        if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == (my_tiles > 1 ? 1 : 0)) p.dbg_ts[5300 + c * 8 + 2] = globaltimer();
 #endif
 #pragma unroll
         for (int j = 0; j < 4; ++j)
@@ -482,11 +487,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
         fence_proxy_async_smem();
         __syncwarp();
         if (lane_id() == 0 && m_own < p.M) {
-          tma_store_2d(&maps.y, stage_out, n0 + c * 32, m_own + int(q) * 32);
+          tma_store_2d(&maps.y, box, n0 + c * 32, m_own + int(q) * 32);
           bulk_commit();
         }
 #ifdef SERQ_DIAG_TS
-        if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == 1) p.dbg_ts[5300 + c * 8 + 3] = globaltimer();
+        if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == (my_tiles > 1 ? 1 : 0)) p.dbg_ts[5300 + c * 8 + 3] = globaltimer();
 #endif
       }
 #ifdef SERQ_DIAG_TS

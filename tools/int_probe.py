@@ -4,7 +4,7 @@ import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_08185_b200 import _lib, benchmarks as B
 
-for f in (0, 1 << 28):
+for f in [int(v) for v in os.environ.get("FLAGS", "0,268435456").split(",")]:
     _lib.load().serq_set_debug_flags(f)
     c1 = B.int_linear_point(512, 4096, 4096, 64, "dense", 4, True)
     c3 = B.int_linear_point(2048, 4096, 11008, 128, "int", 8, False)
