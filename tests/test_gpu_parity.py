@@ -402,14 +402,19 @@ def test_mx_linear_split_last_wave(D):
         _lib.load().serq_set_debug_flags(0)
 
 
-@pytest.mark.parametrize("M,K,N", [(2560, 1024, 2048), (2600, 512, 4096), (4096, 1024, 4096)])
-def test_mx_linear_narrow_last_round(D, M, K, N):
+@pytest.mark.parametrize("M,K,N,gather", [(2560, 1024, 2048, False), (2600, 512, 4096, False),
+                                          (4096, 1024, 4096, False), (2600, 512, 4096, True)])
+def test_mx_linear_narrow_last_round(D, M, K, N, gather):
     # the leftover tiles of the last partial round run as 256 x 128 tiles (two per tile):
-    # parity with the oracle and bit-equality with the all-256-wide schedule (debug flag 1<<19)
+    # parity with the oracle and bit-equality with the all-256-wide schedule (debug flag 1<<19);
+    # gather: an arbitrary salient set (the salient MMA's A operand from the quantizer's slice)
     r = 64
-    x, main_t, comp = _mx_case(M, K, N, r, seed=M + N)
+    idx = np.sort(np.random.default_rng(7).choice(K, r, replace=False)) if gather else np.arange(r)
+    x = _bf16_outlier_x(M, K, seed=M + N)
+    w = np.random.default_rng(M + N + 1).standard_normal((K, N)) * 0.02
+    main_t, comp = O.build_serq_rtn_mx(w, idx, 32)
     lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
-                     comp.r_q.block_scale_exponents, np.arange(r))
+                     comp.r_q.block_scale_exponents, idx)
     xt = _cuda(x, torch.bfloat16)
     y = lin(xt).float().cpu().numpy()
     from paper_2603_08185_b200 import _lib
