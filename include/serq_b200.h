@@ -136,8 +136,8 @@ int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t
 /* Group-wise integer weights (int_gemm_reference row-grouped
  * branch, mxfmt.py:177-195; GPTQ group_size, gptq.py:98-146; _weight_config,
  * pipeline.py:134-137): scales float64 [K/group_size, N] (main.scales of a
- * row-grouped QuantizedTensor), group_size a multiple of 128 and <= 1024 that
- * divides K; group_size == K is serq_pack_int.  R as in serq_pack_int.
+ * row-grouped QuantizedTensor), group_size a multiple of 128 and <= 8192 that
+ * divides K (one integer partial per group stays exact in fp32); group_size == K is serq_pack_int.  R as in serq_pack_int.
  * serq_linear_int on such a handle promotes one integer partial per group. */
 int serq_pack_int_grouped(const int32_t* codes, const double* scales, int64_t group_size, int64_t K, int64_t N,
                           int w_bits, int r_mode, const void* r_data, const double* r_scales, int r,
@@ -187,13 +187,16 @@ int serq_forward_mx_host_gather(serq_linear_t* h, const void* x_host, int64_t M,
 
 /* Number of kernels the last forward on this thread launched (evidence for bench). */
 int serq_last_launch_count(void);
+/* Name of the last kernel launched on this thread, e.g. "serq_i8_pair_kernel<256>"
+ * (tests assert which kernel a configuration takes). */
+const char* serq_last_kernel(void);
 
-/* Diagnostics for roofline work (results are WRONG while set): bit0 = the MX
- * linear skips its operand loads (pure MMA ceiling), bit1 = skips the output
- * stores.  0 restores normal operation. */
+/* Diagnostics, SERQ_DIAG builds only (tools/): kernel-selection and feed/MMA
+ * isolation switches (results are WRONG while set).  The product library has no
+ * such state: it returns SERQ_EINVAL for any nonzero value. */
 int serq_set_debug_flags(int flags);
-/* Diagnostics: device buffer (>= 512 int64) receiving clock64 stamps around the
- * MX linear's per-stage waits in CTA 0, or NULL to disable. */
+/* Diagnostics (SERQ_DIAG_TS builds only): device buffer receiving clock / globaltimer
+ * stamps of the linears' pipelines, or NULL.  SERQ_EINVAL for non-NULL otherwise. */
 int serq_set_debug_timestamps(long long* dev_buf);
 
 #ifdef __cplusplus

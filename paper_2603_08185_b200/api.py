@@ -24,6 +24,9 @@ by duck typing.  Layouts that integer tensor cores cannot evaluate exactly
 
 from __future__ import annotations
 
+import threading
+import weakref
+from collections import OrderedDict
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -400,20 +403,51 @@ class SerqLinear:
         return self.impl(x, self.act_bits, self.act_symmetric, y)
 
 
-_CACHE: dict = {}
+# Packed device linears per artefact object.  The cache holds the artefacts WEAKLY (an
+# entry, and with it the device weights, is dropped when its main or comp artefact is
+# garbage collected) and at most CACHE_MAX entries (least recently used evicted); artefacts
+# that cannot be weakly referenced are held strongly, under the same bound.
+CACHE_MAX = 64
+_CACHE: OrderedDict = OrderedDict()
+_CACHE_LOCK = threading.Lock()
 
 
 def clear_cache() -> None:
-    _CACHE.clear()
+    with _CACHE_LOCK:
+        _CACHE.clear()
+
+
+def _ref(obj, key, entry_box):
+    if obj is None:
+        return lambda: None
+
+    def drop(_):
+        with _CACHE_LOCK:
+            if _CACHE.get(key) is entry_box[0]:
+                del _CACHE[key]
+
+    try:
+        return weakref.ref(obj, drop)
+    except TypeError:
+        return lambda: obj
 
 
 def _linear_for(main, comp, act_cfg, allow_symmetric_act=False) -> SerqLinear:
     key = (id(main), id(comp), act_cfg, allow_symmetric_act)
-    hit = _CACHE.get(key)
-    if hit is not None and hit[0] is main and hit[1] is comp:
-        return hit[2]
+    with _CACHE_LOCK:
+        hit = _CACHE.get(key)
+        if hit is not None and hit[0]() is main and hit[1]() is comp:
+            _CACHE.move_to_end(key)
+            return hit[2]
     lin = SerqLinear(main, comp, act_cfg, allow_symmetric_act)
-    _CACHE[key] = (main, comp, lin)  # keep the artefacts alive so ids stay unique
+    box = [None]
+    entry = (_ref(main, key, box), _ref(comp, key, box), lin)
+    box[0] = entry
+    with _CACHE_LOCK:
+        _CACHE[key] = entry
+        _CACHE.move_to_end(key)
+        while len(_CACHE) > CACHE_MAX:
+            _CACHE.popitem(last=False)
     return lin
 
 

@@ -4,8 +4,11 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
+#include <set>
 #include <string>
+#include <tuple>
 
 #include "../../include/serq_b200.h"
 #include "serq_gemm.cuh"
@@ -23,8 +26,15 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_launches = 0;
-int g_debug_flags = 0;  // serq_set_debug_flags (diagnostic benchmarking only)
+thread_local const char* g_last_kernel = "";  // name of the last kernel launched on this thread (tests)
+#ifdef SERQ_DIAG
+// diagnostics build only (tools/): kernel-selection / feed-isolation switches and timestamps
+int g_debug_flags = 0;
 long long* g_debug_ts = nullptr;
+#else
+constexpr int g_debug_flags = 0;
+constexpr long long* g_debug_ts = nullptr;
+#endif
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -47,6 +57,7 @@ int fail(int code, const char* fmt, ...) {
     cudaError_t e_ = cudaGetLastError();                                                          \
     if (e_ != cudaSuccess) return fail(SERQ_ECUDA, "%s launch: %s", what, cudaGetErrorString(e_)); \
     ++g_launches;                                                                                 \
+    g_last_kernel = what;                                                                         \
   } while (0)
 
 inline cudaStream_t S(serq_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -108,15 +119,36 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// Per-device state: SM count and which kernels have their dynamic shared-memory
+// limit raised (a process may drive several GPUs; both are per device).
+constexpr int kMaxDevices = 64;
 int sm_count() {
-  static int n = 0;
+  static std::atomic<int> cache[kMaxDevices];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
+}
+
+template <typename... KArgs>
+cudaError_t set_smem_attr(void (*kernel)(KArgs...), int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_tuple(dev, reinterpret_cast<const void*>(kernel), bytes);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
 }
 
 // scale factors as rows of 128 B (one 1-KB box = 2 SF chunks of a 128-row block)
@@ -125,13 +157,9 @@ int make_sf_map(CUtensorMap* m, const uint8_t* sf, int64_t rows, int64_t cols) {
                   CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
-bool g_attr_set[2] = {false, false};
 template <int kMode>
 int ensure_attr() {
-  if (!g_attr_set[kMode]) {
-    CK(cudaFuncSetAttribute(serq_linear_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    g_attr_set[kMode] = true;
-  }
+  CK(set_smem_attr(serq_linear_kernel<kMode>, kSmemBytes));
   return SERQ_OK;
 }
 
@@ -157,22 +185,15 @@ struct serq_linear {
   CUtensorMap map_b64;                                // pair3 narrow (256 x 128) last-round tiles: 64-row B boxes
   CUtensorMap map_r32, map_sfr4;                     // pair3 kernel: R as 32-B swizzled rows, 512-B SF boxes
   bool has_r32 = false;
-  void* w4 = nullptr;                                // INT: packed int4 weights, tiled [N/128][K/128][128][64 B]
-  CUtensorMap map_w4, map_r_pair;                    // INT pair kernel maps (R with 128-row boxes)
+  CUtensorMap map_r_pair;                            // INT pair kernel maps (R with 128-row boxes)
   CUtensorMap map_w8;                                // INT pair kernel, direct int8 weights: 128 B x 128-row boxes
   CUtensorMap map_w8_64, map_r_pair64;               // the same with 64-row boxes (128-column tiles)
-  bool has_w4 = false;
   // INT, group-wise weight scales along K (serq_pack_int_grouped)
   int groups = 1, gsteps = 0;
   bool use_i8g = false;        // served by serq_i8g_pair_kernel
   float* sw_g = nullptr;       // [G][N]
   int32_t* colsum_g = nullptr; // [G][N]
   float* cterm = nullptr;      // [N]
-  // CTA-pair split last wave: fp32 partials + per-(tile, rank) counters
-  float* sk_ws = nullptr;
-  int64_t sk_ws_floats = 0;
-  int* sk_cnt = nullptr;
-  int64_t sk_cnt_n = 0;
   // end-to-end scratch
   int64_t ws_m = 0;
   void* ws_x = nullptr;
@@ -190,7 +211,7 @@ struct serq_linear {
 namespace {
 void free_handle(serq_linear* h) {
   void* ptrs[] = {h->w, h->sfw, h->rbuf, h->sfr, h->sw, h->colsum, h->sr, h->colsum_r,
-                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y, h->sk_ws, h->sk_cnt, h->w4,
+                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y,
                   h->sw_g, h->colsum_g, h->cterm, h->ws_xs, h->ws_xsf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -207,13 +228,22 @@ extern "C" {
 const char* serq_last_error(void) { return g_err.c_str(); }
 const char* serq_version(void) { return "serq_b200 0.1 (sm_100a tcgen05)"; }
 int serq_last_launch_count(void) { return g_launches; }
+const char* serq_last_kernel(void) { return g_last_kernel; }
 int serq_set_debug_flags(int flags) {
+#ifdef SERQ_DIAG
   g_debug_flags = flags;
   return SERQ_OK;
+#else
+  return flags ? fail(SERQ_EINVAL, "debug flags need a SERQ_DIAG build of the library (tools/ only)") : SERQ_OK;
+#endif
 }
 int serq_set_debug_timestamps(long long* dev_buf) {
+#ifdef SERQ_DIAG
   g_debug_ts = dev_buf;
   return SERQ_OK;
+#else
+  return dev_buf ? fail(SERQ_EINVAL, "timestamps need a SERQ_DIAG build of the library (tools/ only)") : SERQ_OK;
+#endif
 }
 
 int serq_device_info(int* sm_count, int* cc_major, int* cc_minor) {
@@ -263,10 +293,10 @@ static int act_quant_mx_impl(const void* x, int dtype, int64_t M, int64_t K, int
     dim3 grid(unsigned(cdiv(int64_t(kc) * 16, 256)), unsigned(cdiv(m_rows, kMxRows)), gather_idx ? 2u : 1u);
     while (gather_idx && int64_t(grid.x) * grid.y * 256 < g_threads) ++grid.y;  // the z = 1 plane must cover it
     const MxGather mg{gather_idx, r, xs_codes, xs_sf, krc};
-    if (dtype == SERQ_BF16 && !(g_debug_flags & (1 << 30))) {
+    if (dtype == SERQ_BF16 && !SERQ_DBG(g_debug_flags, 1 << 30)) {
       // one thread per 32-block (measured best against 2 and 4 rows per thread, tools/quant_probe.py:
       // 4096^2 8.1 / 8.8 / 10.8 us); debug flag 1<<30: the 8-elements-per-thread kernel (9.9 us)
-      const int kR = (g_debug_flags & (1 << 21)) ? 4 : (g_debug_flags & (1 << 22)) ? 2 : 1;  // diagnostics
+      const int kR = SERQ_DBG(g_debug_flags, (1 << 21)) ? 4 : SERQ_DBG(g_debug_flags, (1 << 22)) ? 2 : 1;  // diagnostics
       const int64_t main_blocks = cdiv(cdiv(m_rows, kR) * int64_t(kc) * 4, 256);
       const dim3 gb(unsigned(main_blocks + cdiv(g_threads, 256)));  // gather CTAs appended
       const auto* xb = static_cast<const __nv_bfloat16*>(x);
@@ -318,7 +348,7 @@ int serq_act_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t l
     // (tools/int_quant_probe.py, C3 2048 x 4096: 12.3 us with 256 threads per row, 5.2 with 64)
     const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
     const dim3 gq{unsigned(M)};
-    const bool warp_rows = (g_debug_flags & (1 << 21)) != 0;  // diagnostics: one warp per row
+    const bool warp_rows = SERQ_DBG(g_debug_flags, (1 << 21)) != 0;  // diagnostics: one warp per row
     const int tpr = warp_rows ? 32 : 64;
     const int cpt = int(cdiv(K / 8, tpr));
 #define SERQ_INTQ(P, C)                                                                                         \
@@ -547,20 +577,6 @@ int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t
   if (!rc) rc = make_map(&h->map_w8, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, 128);
   if (!rc) rc = make_map(&h->map_w8_64, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, 64);
   if (rc) return bail(rc);
-  if (w_bits <= 4) {
-    // packed INT4 copy for the CTA-pair kernel (widened to INT8 in shared memory)
-    const int ksteps = int(cdiv(K, 128));
-    const int64_t bytes = cdiv(N, 128) * ksteps * 128 * 64;
-    if (cudaMalloc(&h->w4, bytes) != cudaSuccess) return bail(fail(SERQ_ECUDA, "cudaMalloc failed for INT4 weights"));
-    if (cudaMemsetAsync(h->w4, 0, bytes, st) != cudaSuccess) return bail(fail(SERQ_ECUDA, "memset"));
-    pack_int4_tiled_kernel<<<dim3(unsigned(cdiv(N, 256)), unsigned(cdiv(K, 2))), 256, 0, st>>>(
-        codes, K, N, ksteps, static_cast<uint8_t*>(h->w4));
-    if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_int4 launch failed"));
-    rc = make_map(&h->map_w4, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w4, 64, uint64_t(bytes / 64), 64, 64, 128,
-                  CU_TENSOR_MAP_SWIZZLE_NONE);
-    if (rc) return bail(rc);
-    h->has_w4 = true;
-  }
   if (r_mode == SERQ_R_DENSE) {
     if (cudaMalloc(&h->rbuf, N * r * 2) != cudaSuccess) return bail(fail(SERQ_ECUDA, "cudaMalloc R"));
     dense_r_kernel<<<unsigned(cdiv(N * r, 256)), 256, 0, st>>>(static_cast<const double*>(r_data), r, N,
@@ -672,23 +688,18 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
                             const __nv_bfloat16* x, int64_t ldx, uint8_t* codes_out, uint8_t* sf_out, int64_t M,
                             void* y, int64_t ldy, cudaStream_t st, const uint8_t* xs_codes = nullptr,
                             const uint8_t* xs_sf = nullptr) {
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            ClCfg<false>::kSmem));
-    CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            ClCfg<true>::kSmem));
-    CK(cudaFuncSetAttribute(serq_mx_decode_cl_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            ClCfg<true>::kSmem));
-    attr = true;
-  }
+  CK(set_smem_attr(serq_mx_decode_cl_kernel<false>, ClCfg<false>::kSmem));
+  CK(set_smem_attr(serq_mx_decode_cl_kernel<true, 1>, ClCfg<true>::kSmem));
+  CK(set_smem_attr(serq_mx_decode_cl_kernel<true, 2>, ClCfg<true>::kSmem));
   const bool fuse = x != nullptr;
   const int tiles = int(cdiv(h->N, 128));
   const int ks = int(cdiv(h->K / 2, kStepBytes));
   // CTAs per tile, ~3/4 CTA per SM in total (Llama-2-7B: up_proj 86 tiles -> 1, down_proj 32 -> 3);
   // measured best among 1..8 for both shapes (tools/decode_probe.py)
   int S = (3 * sm_count()) / (4 * tiles);
-  if (const char* e = getenv("SERQ_DEC_S")) S = atoi(e);  // diagnostics
+#ifdef SERQ_DIAG
+  if (const char* e = getenv("SERQ_DEC_S")) S = atoi(e);
+#endif
   S = S < 1 ? 1 : (S > 8 ? 8 : S);
   if (S > ks) S = ks;
   ClParams cp{};
@@ -716,7 +727,7 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
   const bool gather = h->r > 0 && !h->contiguous;
   if (gather && (fuse || !xs_codes || !xs_sf)) return fail(SERQ_EINVAL, "gather decode needs the xs slice");
   cp.gather = gather ? 1 : 0;
-  cp.red_narrow = (S - 1) * ((M + 3) / 4) * 128 * 16 <= kClRed && !(g_debug_flags & (1 << 29)) ? 1 : 0;
+  cp.red_narrow = (S - 1) * ((M + 3) / 4) * 128 * 16 <= kClRed && !SERQ_DBG(g_debug_flags, 1 << 29) ? 1 : 0;
   dm.xs = dm.sfxs = h->map_b128;  // unused unless gather
   if (gather) {
     int rc = make_map(&dm.xs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_codes, h->r / 2, M, h->r / 2, 32, kDecN,
@@ -769,11 +780,7 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
   if (ldy < h->N || ldy % 8) return fail(SERQ_EINVAL, "ldy must be >= N and a multiple of 8");
   const bool need_xs = h->r > 0 && !h->contiguous;
   if (need_xs && (!xs_codes || !xs_sf)) return fail(SERQ_EINVAL, "non-contiguous salient set needs the xs slice");
-  static bool attr_done = false;
-  if (!attr_done) {
-    CK(cudaFuncSetAttribute(serq_mx_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmemBytes));
-    attr_done = true;
-  }
+  CK(set_smem_attr(serq_mx_persistent_kernel, kPSmemBytes));
   int rc = SERQ_OK;
   CUtensorMap ma, mxs, my;
   rc = make_map(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, kBM);
@@ -804,18 +811,14 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
   p.w_ksteps = h->w_ksteps;
   p.dbg = g_debug_flags;
   p.dbg_ts = g_debug_ts;
-  if (M <= kDecN && (h->r == 0 || h->has_r32) && !(g_debug_flags & 2048))
+  if (M <= kDecN && (h->r == 0 || h->has_r32) && !SERQ_DBG(g_debug_flags, 2048))
     return launch_decode_cl(h, a_codes, a_sf, nullptr, 0, nullptr, nullptr, M, y, ldy, S(stream), xs_codes, xs_sf);
   // pair3 for the permuted layout, and for the gather fallback with r == 64 (debug flag 1<<24: the
   // gather cases take the older pair kernel)
-  const bool g3 = h->r > 0 && h->has_r32 && !h->contiguous && xs_codes && xs_sf && !(g_debug_flags & (1 << 24));
-  if (M > 128 && (h->r == 0 || (h->has_r32 && h->contiguous) || g3) && !(g_debug_flags & (16 | 512))) {
-    static bool attr3 = false;
-    if (!attr3) {
-      CK(cudaFuncSetAttribute(serq_mx_pair3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3SmemBytes));
-      CK(cudaFuncSetAttribute(serq_mx_pair3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3SmemBytesG));
-      attr3 = true;
-    }
+  const bool g3 = h->r > 0 && h->has_r32 && !h->contiguous && xs_codes && xs_sf && !SERQ_DBG(g_debug_flags, 1 << 24);
+  if (M > 128 && (h->r == 0 || (h->has_r32 && h->contiguous) || g3) && !SERQ_DBG(g_debug_flags, 16 | 512)) {
+    CK(set_smem_attr(serq_mx_pair3_kernel<false>, k3SmemBytes));
+    CK(set_smem_attr(serq_mx_pair3_kernel<true>, k3SmemBytesG));
     Pair3Maps pm;
     rc = make_map(&pm.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, 128);
     if (!rc) rc = make_sf_map(&pm.sfa, a_sf, M, h->K);
@@ -841,42 +844,14 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
     const int64_t clusters = pairs < max_pairs ? pairs : max_pairs;
     // split the last partial wave into K-halves when they fit in one round
     const int64_t rounds = pairs / clusters, left = pairs - rounds * clusters;
-    p.split_from = int(pairs);
     p.narrow_from = int(pairs);
     // tile order: N-fastest measured +2.4% at 8192^3, equal at 4096^3 (tools/sweep_mx.py)
-    p.group_m = (g_debug_flags & 262144) ? 0 : 1;
-    p.y = static_cast<__nv_bfloat16*>(y);
-    p.ldy = ldy;
-    // opt-in (debug flag 8192): measured slower than 4 full rounds for 4096^3 (partner flag + partial traffic)
-    if (left > 0 && 2 * left <= clusters && p.k_steps >= 4 && (g_debug_flags & 8192) && !g3) {
-      serq_linear* hm = const_cast<serq_linear*>(h);
-      const int64_t need = left * 2 * 2 * 128 * kBN;
-      if (need > hm->sk_ws_floats) {
-        if (hm->sk_ws) cudaFree(hm->sk_ws);
-        hm->sk_ws = nullptr;
-        CK(cudaMalloc(&hm->sk_ws, need * 4));
-        hm->sk_ws_floats = need;
-      }
-      if (left * 4 > hm->sk_cnt_n) {  // ready flags [left][2 halves][2 ranks] (self-resetting)
-        if (hm->sk_cnt) cudaFree(hm->sk_cnt);
-        hm->sk_cnt = nullptr;
-        CK(cudaMalloc(&hm->sk_cnt, left * 4 * 4));
-        CK(cudaMemsetAsync(hm->sk_cnt, 0, left * 4 * 4, S(stream)));
-        hm->sk_cnt_n = left * 4;
-      }
-      rc = make_map(&pm.ws, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, hm->sk_ws, kBN, uint64_t(left * 4 * 128), kBN * 4, 32, 32,
-                    CU_TENSOR_MAP_SWIZZLE_128B);
-      if (rc) return rc;
-      p.split_from = int(rounds * clusters);
-      p.sk_ws = hm->sk_ws;
-      p.sk_cnt = hm->sk_cnt;
-    }
-    // the last partial round as 256 x 128 tiles (two per leftover tile, no K split, no exchange):
-    // each takes ~3/4 of a full tile's time (the A operand is fed twice) instead of half the
-    // clusters idling through a full tile; debug flag 1<<19 disables
-    if (p.split_from >= int(pairs) && left > 0 && 2 * left <= clusters && rounds >= 1 && !(g_debug_flags & (1 << 19)))
+    p.group_m = SERQ_DBG(g_debug_flags, 262144) ? 0 : 1;
+    // the last partial round as 256 x 128 tiles (two per leftover tile): each takes ~3/4 of a full
+    // tile's time (the A operand is fed twice) instead of half the clusters idling through a full
+    // tile (measured faster than splitting the leftover tiles into K-halves, K2)
+    if (left > 0 && 2 * left <= clusters && rounds >= 1 && !SERQ_DBG(g_debug_flags, 1 << 19))
       p.narrow_from = int(rounds * clusters);
-    if (p.split_from >= int(pairs)) pm.ws = pm.y;  // unused
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(2 * clusters));
     cfg.blockDim = dim3(kThreads);
@@ -887,19 +862,17 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (g3)
+    if (g3) {
       CK(cudaLaunchKernelEx(&cfg, serq_mx_pair3_kernel<true>, pm, p));
-    else
+      LAUNCH_CHECK("serq_mx_pair3_kernel<gather>");
+    } else {
       CK(cudaLaunchKernelEx(&cfg, serq_mx_pair3_kernel<false>, pm, p));
-    LAUNCH_CHECK("serq_mx_pair3_kernel");
+      LAUNCH_CHECK("serq_mx_pair3_kernel");
+    }
     return SERQ_OK;
   }
-  if (M > 128 && !(g_debug_flags & 16)) {
-    static bool attr2 = false;
-    if (!attr2) {
-      CK(cudaFuncSetAttribute(serq_mx_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k2SmemBytes));
-      attr2 = true;
-    }
+  if (M > 128 && !SERQ_DBG(g_debug_flags, 16)) {
+    CK(set_smem_attr(serq_mx_pair_kernel, k2SmemBytes));
     Pair2Maps pm;
     rc = make_map(&pm.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, 128);
     if (rc) return rc;
@@ -947,8 +920,8 @@ int serq_forward_mx(serq_linear_t* h, const void* x, int dtype, int64_t M, int64
   if (gather && (!gather_idx || !xs_codes || !xs_sf))
     return fail(SERQ_EINVAL, "non-contiguous salient set needs gather_idx and the xs buffers");
   if (M <= kClFuseM && (h->r == 0 || h->has_r32) && dtype == SERQ_BF16 && !gather &&
-      !(reinterpret_cast<uintptr_t>(x) & 15) && ldx % 8 == 0 && ldx >= h->K && !(g_debug_flags & (1 << 23)) &&
-      !(g_debug_flags & 2048)) {
+      !(reinterpret_cast<uintptr_t>(x) & 15) && ldx % 8 == 0 && ldx >= h->K && !SERQ_DBG(g_debug_flags, 1 << 23) &&
+      !SERQ_DBG(g_debug_flags, 2048)) {
     // decode (M <= 8) with the quantizer inside the linear: one kernel per layer instead of
     // quantizer + PDL-chained linear (Llama-2-7B M=1: up_proj 7.8 vs 8.2 us/layer, down_proj
     // 8.1 vs 9.1; tools/decode_probe.py); debug flag 1<<23 selects the two-kernel path
@@ -981,13 +954,11 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   if (need_xs && !xs) return fail(SERQ_EINVAL, "this R mode needs the quantizer's xs slice");
   if (h->use_i8g) {
     // group-wise weight scales: one promoted integer partial per group (serq_gemm_i8g.cuh), any M
-    static bool attrg = false;
-    if (!attrg) {
+    {
       int mx = 0;
       for (int m = 0; m <= kRDenseSplit; ++m) mx = i8g_smem(m) > mx ? i8g_smem(m) : mx;
-      CK(cudaFuncSetAttribute(serq_i8g_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-      CK(cudaFuncSetAttribute(serq_i8g_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-      attrg = true;
+      CK(set_smem_attr(serq_i8g_pair_kernel<false>, mx));
+      CK(set_smem_attr(serq_i8g_pair_kernel<true>, mx));
     }
     I8Maps im;
     int rc = make_map(&im.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K, M, h->K, 128, 128);
@@ -1029,22 +1000,12 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     LAUNCH_CHECK("serq_i8g_pair_kernel");
     return SERQ_OK;
   }
-  // CTA-pair kernel: int8 weights TMA'd directly (default; measured faster than widening packed
-  // INT4 in shared memory, which remains under debug flag 1<<28)
-  const bool widen = (g_debug_flags & (1 << 28)) && h->has_w4;
+  // CTA-pair kernel: int8 weights TMA'd straight into the operand
   const bool pair_ok = M > 128 && (h->r_mode != SERQ_R_INT || h->contiguous) && h->r <= 128 &&
-                       (h->r_mode != SERQ_R_DENSE || h->r <= 64) && !(g_debug_flags & 65536);
+                       (h->r_mode != SERQ_R_DENSE || h->r <= 64) && !SERQ_DBG(g_debug_flags, 65536);
   if (pair_ok) {
-    static bool attri = false;
-    if (!attri) {
-      CK(cudaFuncSetAttribute(serq_i8_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              I8Cfg<false>::kSmem));
-      CK(cudaFuncSetAttribute(serq_i8_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              I8Cfg<true>::kSmem));
-      CK(cudaFuncSetAttribute(serq_i8_pair_kernel<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              I8Cfg<true>::kSmem));
-      attri = true;
-    }
+    CK(set_smem_attr(serq_i8_pair_kernel<256>, I8Cfg::kSmem));
+    CK(set_smem_attr(serq_i8_pair_kernel<128>, I8Cfg::kSmem));
     I8Maps im;
     int rc = make_map(&im.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K, M, h->K, 128, 128);
     if (!rc)
@@ -1054,8 +1015,8 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     if (rc) return rc;
     if (h->r_mode != SERQ_R_DENSE) im.xs = im.a;
     // few 256x256 tiles (C1: 2 x 16 on 74 pairs): 128-column tiles put twice as many pairs to work
-    const bool narrow = !widen && cdiv(M, 256) * cdiv(h->N, 256) * 2 <= sm_count() / 2 && !(g_debug_flags & (1 << 27));
-    im.bp = widen ? h->map_w4 : (narrow ? h->map_w8_64 : h->map_w8);
+    const bool narrow = cdiv(M, 256) * cdiv(h->N, 256) * 2 <= sm_count() / 2 && !SERQ_DBG(g_debug_flags, 1 << 27);
+    im.bp = narrow ? h->map_w8_64 : h->map_w8;
     im.r = h->r_mode != SERQ_R_NONE ? (narrow ? h->map_r_pair64 : h->map_r_pair) : im.bp;
     GemmParams p{};
     p.dbg = g_debug_flags;
@@ -1081,15 +1042,13 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     const dim3 grid(unsigned(2 * (tiles < max_pairs ? tiles : max_pairs)));
     // launched with programmatic dependent launch: the prologue and the first weight stages
     // overlap the activation quantizer's tail
-    if (widen)
-      CK(launch_pdl(serq_i8_pair_kernel<false>, grid, dim3(I8Cfg<false>::kThreads), I8Cfg<false>::kSmem, S(stream), im,
-                    p));
-    else if (narrow)
-      CK(launch_pdl(serq_i8_pair_kernel<true, 128>, grid, dim3(I8Cfg<true>::kThreads), I8Cfg<true>::kSmem, S(stream),
-                    im, p));
-    else
-      CK(launch_pdl(serq_i8_pair_kernel<true>, grid, dim3(I8Cfg<true>::kThreads), I8Cfg<true>::kSmem, S(stream), im, p));
-    LAUNCH_CHECK("serq_i8_pair_kernel");
+    if (narrow) {
+      CK(launch_pdl(serq_i8_pair_kernel<128>, grid, dim3(I8Cfg::kThreads), I8Cfg::kSmem, S(stream), im, p));
+      LAUNCH_CHECK("serq_i8_pair_kernel<128>");
+    } else {
+      CK(launch_pdl(serq_i8_pair_kernel<256>, grid, dim3(I8Cfg::kThreads), I8Cfg::kSmem, S(stream), im, p));
+      LAUNCH_CHECK("serq_i8_pair_kernel<256>");
+    }
     return SERQ_OK;
   }
   int rc = ensure_attr<kModeI8>();
@@ -1196,7 +1155,9 @@ int serq_forward_mx_host_gather(serq_linear_t* h, const void* x_host, int64_t M,
     int64_t mid = body - ends;
     const int64_t slots = kE2eMaxChunks - (ramp ? 4 : 0);
     int64_t step = 1024;
-    if (const char* e = getenv("SERQ_E2E_ROWS")) step = cdiv(atoll(e), 256) * 256;  // diagnostics
+#ifdef SERQ_DIAG
+    if (const char* e = getenv("SERQ_E2E_ROWS")) step = cdiv(atoll(e), 256) * 256;
+#endif
     if (cdiv(mid, step) > slots) step = cdiv(cdiv(mid, slots), 256) * 256;
     if (ramp) {
       plan[chunks++] = 256;
@@ -1213,7 +1174,8 @@ int serq_forward_mx_host_gather(serq_linear_t* h, const void* x_host, int64_t M,
     }
     if (chunks == 0) plan[chunks++] = 0;
     plan[chunks - 1] += rem;
-    if (const char* e = getenv("SERQ_E2E_PLAN")) {  // diagnostics: explicit chunk rows, last absorbs the rest
+#ifdef SERQ_DIAG
+    if (const char* e = getenv("SERQ_E2E_PLAN")) {  // explicit chunk rows, last absorbs the rest
       int64_t n = 0, used = 0;
       for (const char* q = e; *q && n < kE2eMaxChunks - 1;) {
         const int64_t v = atoll(q);
@@ -1226,9 +1188,14 @@ int serq_forward_mx_host_gather(serq_linear_t* h, const void* x_host, int64_t M,
       plan[n++] = M - used;
       chunks = n;
     }
+#endif
   }
   // diagnostics (SERQ_E2E_TIMING set): per-chunk timeline of the copies and kernels on stderr
+#ifdef SERQ_DIAG
   static const bool timing = getenv("SERQ_E2E_TIMING") != nullptr;
+#else
+  constexpr bool timing = false;
+#endif
   cudaEvent_t tev[4 * kE2eMaxChunks + 1];
   if (timing)
     for (cudaEvent_t& e : tev) CK(cudaEventCreate(&e));

@@ -71,15 +71,9 @@ struct GemmParams {
   int32_t* acc_dump;     // debug: exact main accumulators (acc - zp*colsum), [M,N]
   int32_t* accr_dump;    // debug: exact R accumulators
   long long* dbg_ts;     // diagnostics: per-iteration clock64 stamps of the MMA warp (CTA 0), or nullptr
-  // split last wave (CTA-pair MX kernel): tiles >= split_from run as two K-halves
-  int split_from;        // >= n_tiles: no split
   int narrow_from;       // pair3: tiles >= narrow_from run as two 256 x 128 tiles (>= n_tiles: none)
-  float* sk_ws;          // [split tiles][2 halves][2 ranks][128 x 256] fp32 partials
-  int* sk_cnt;           // [split tiles][2 ranks] self-resetting arrival counters
-  __nv_bfloat16* y;      // output (direct stores of split tiles)
-  int64_t ldy;
   int group_m;           // tile order: 0 = M fastest over all tiles; g > 0 = groups of g M-tiles
-  int dbg;               // diagnostics: bit0 = producer skips all loads (MMA ceiling), bit1 = no output stores
+  int dbg;               // SERQ_DIAG builds only (diagnostic switches); always 0 in the product
 };
 
 template <int kMode>

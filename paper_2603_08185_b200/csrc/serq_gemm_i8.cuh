@@ -1,16 +1,14 @@
-// serq_gemm_i8.cuh -- integer SERQ linear on CTA pairs with INT4 weights
-// widened to INT8 in shared memory (BASELINE configs 1 and 3).
+// serq_gemm_i8.cuh -- integer SERQ linear on CTA pairs (BASELINE configs 1 and 3).
 //
 // Y = sx[m] * ( sw[n] * (acc - zp[m]*colsum[n]) + R-term ),  acc = sum_k c[m,k] w[k,n]
 // (int_gemm_reference, mxfmt.py:177-195; forward_reconstructed, compensate.py:300-316).
 //
 // * tcgen05.mma.cta_group::2.kind::i8, 256 x 256 x 32 per instruction: u8
 //   (asymmetric) or s8 (symmetric) activation codes x s8 weights, s32 in TMEM.
-// * Weights stay PACKED INT4 in HBM, tiled [N/128][K/128][128 rows x 64 B];
-//   TMA brings 8 KB per 128-K step per CTA into a staging buffer and four
-//   transform warps widen nibbles to int8 straight into the 128B-swizzled
-//   K-major operand layout (PRMT/VSUB4, 8 codes per word).  Blackwell has no
-//   INT4 MMA; widening in SMEM halves the per-SM operand ingress for B.
+// * Weights: int8 [N, K] TMA'd straight into the 128B-swizzled K-major operand
+//   (Blackwell has no INT4 MMA).  A variant that kept packed INT4 in HBM and
+//   widened it in shared memory with transform warps was measured slower (the
+//   widening traffic made the SM shared-memory bound; K3) and removed.
 // * The salient term accumulates into a second TMEM accumulator (columns
 //   [256,512)): integer R (kind::i8, A = K-tile 0 of X, B = R codes) or dense
 //   bf16 R (kind::f16, A = bf16 (codes - zp) slice, B = L^T), both staged with
@@ -24,26 +22,16 @@
 namespace serq {
 
 constexpr int kI8A = 128 * 128;    // own 128 activation rows x 128 int8
-constexpr int kI8Bp = 128 * 64;    // packed int4 staging, own 128 weight rows
-constexpr int kI8B = 128 * 128;    // widened int8 operand
+constexpr int kI8B = 128 * 128;    // own 128 weight rows x 128 int8
 constexpr int kI8Side = 2 * 16384;             // R operands: [A' (dense only)] + B_R
 constexpr int kI8Const = 4 * 256 * 4;
-constexpr int kI8Threads = 512;
-constexpr int kI8TrWarps = 8;  // warps 8..15
-// Two weight feeds:
-//  kDirect = false: packed INT4 in HBM, widened in SMEM by the transform warps (4 x 40 KB stages)
-//  kDirect = true : int8 in HBM, TMA'd straight into the 128B-swizzled operand (5 x 32 KB stages,
-//                   no transform warps): twice the weight bytes, but no SMEM widening traffic
-template <bool kDirect>
 struct I8Cfg {
-  static constexpr int kStages = kDirect ? 5 : 4;
-  static constexpr int kBp = kDirect ? 0 : kI8Bp;
-  static constexpr int kStage = kI8A + kBp + kI8B;
+  static constexpr int kStages = 5;
+  static constexpr int kStage = kI8A + kI8B;
   static constexpr int kSmem = 1024 + kStages * kStage + kI8Side + kI8Const + 4 * 4096 + 512;
-  static constexpr int kThreads = kDirect ? 256 : kI8Threads;
+  static constexpr int kThreads = 256;
   static_assert(kSmem <= 232448, "smem budget");
 };
-constexpr int kI8Smem = I8Cfg<false>::kSmem;
 
 struct I8Maps {
   CUtensorMap a, bp, r, xs, y;
@@ -102,25 +90,17 @@ __device__ __forceinline__ void mbar_wait_bo(uint64_t* bar, uint32_t parity, boo
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
-// 8 packed two's-complement nibbles -> 8 int8 (element 2i in the low nibble)
-__device__ __forceinline__ uint2 widen_int4x8(uint32_t w) {
-  const uint32_t lo = __vsub4((w & 0x0F0F0F0Fu) ^ 0x08080808u, 0x08080808u);
-  const uint32_t hi = __vsub4(((w >> 4) & 0x0F0F0F0Fu) ^ 0x08080808u, 0x08080808u);
-  return make_uint2(__byte_perm(lo, hi, 0x5140), __byte_perm(lo, hi, 0x7362));
-}
-
 // kN: output columns per CTA-pair tile (256, or 128 for small problems so twice as many
 // pairs get a tile; each CTA then stages 64 weight rows)
-template <bool kDirect, int kN = 256>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThreads, 1)
+template <int kN = 256>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg::kThreads, 1)
     serq_i8_pair_kernel(const __grid_constant__ I8Maps maps, const GemmParams p) {
-  static_assert(kN == 256 || (kN == 128 && kDirect), "128-column tiles need the direct int8 weight feed");
+  static_assert(kN == 256 || kN == 128, "256- or 128-column tiles");
   constexpr int kBHalf = kN / 2;  // weight rows per CTA
   constexpr uint32_t kBBytes = kBHalf * 128;  // one 128-K step of this CTA's weight rows (int8)
   constexpr uint32_t kRBytes = kBHalf * 128;  // this CTA's R rows (int8 r <= 128 or bf16 r <= 64: 128 B each)
-  constexpr int kI8Stages = I8Cfg<kDirect>::kStages;
-  constexpr int kI8Stage = I8Cfg<kDirect>::kStage;
-  constexpr int kBp = I8Cfg<kDirect>::kBp;
+  constexpr int kI8Stages = I8Cfg::kStages;
+  constexpr int kI8Stage = I8Cfg::kStage;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* side = smem + kI8Stages * kI8Stage;       // [A' 16K][B_R 16K]
@@ -128,11 +108,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
   int32_t* cst_i = reinterpret_cast<int32_t*>(cst_f + 512); // colsum[256] | colsum_r[256]
   uint8_t* epi = reinterpret_cast<uint8_t*>(cst_i + 512);   // 4 warps x 2 x 2 KB staging (ping-pong)
   uint64_t* bars = reinterpret_cast<uint64_t*>(epi + 4 * 4096);
-  uint64_t* full = bars;                       // [S] leader: A (+ side) landed, both CTAs
-  uint64_t* bpk = bars + kI8Stages;            // [S] local: packed B landed
-  uint64_t* bready = bars + 2 * kI8Stages;     // [S] leader: both CTAs widened B (+ A landed), 16 warps
-  uint64_t* empty = bars + 3 * kI8Stages;      // [S] both: MMAs of the stage done
-  uint64_t* side_empty = bars + 4 * kI8Stages; // both: R MMAs done
+  uint64_t* full = bars;                       // [S] leader: A, B (+ side) landed, both CTAs
+  uint64_t* empty = bars + kI8Stages;          // [S] both: MMAs of the stage done
+  uint64_t* side_empty = bars + 2 * kI8Stages; // both: R MMAs done
   uint64_t* tmem_full = side_empty + 1;        // both
   uint64_t* tmem_empty = side_empty + 2;       // leader: 8 epilogue warps drained TMEM
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(side_empty + 3);
@@ -160,8 +138,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
     }
     for (int s = 0; s < kI8Stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&bpk[s], 1);
-      mbar_init(&bready[s], 2 * kI8TrWarps);
       mbar_init(&empty[s], 1);
     }
     mbar_init(side_empty, 1);
@@ -184,7 +160,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
       const uint32_t sb = smem_u32(smem), sside = smem_u32(side);
       // programmatic dependent launch: the first tile's weight stages do not depend on the
       // previous kernel (the activation quantizer) -- stream them before griddepcontrol.wait
-      const int pre = kDirect && my_tiles > 0 ? (ks < kI8Stages ? ks : kI8Stages) : 0;
+      const int pre = my_tiles > 0 ? (ks < kI8Stages ? ks : kI8Stages) : 0;
       if (my_tiles > 0) {
         const int n_half0 = (cluster_id / tiles_m) * kN + int(rank) * kBHalf;
         for (int kk = 0; kk < pre; ++kk) {
@@ -205,21 +181,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
         for (int kk = 0; kk < ks; ++kk, ++g) {
           const int s = g % kI8Stages;
           const bool preloaded = i == 0 && kk < pre;
-          if (!preloaded) mbar_wait_bo(&empty[s], ((g / kI8Stages) & 1) ^ 1, p.dbg & (1 << 20));
+          if (!preloaded) mbar_wait_bo(&empty[s], ((g / kI8Stages) & 1) ^ 1, SERQ_DBG(p.dbg, (1 << 20)));
           const bool with_side = has_r && kk == 0;
           if (with_side && i > 0) mbar_wait(side_empty, (i - 1) & 1);
           const uint32_t fbar = map_rank(smem_u32(&full[s]), 0);
           const uint32_t st = sb + s * kI8Stage;
           if (leader && !preloaded)
-            mbar_expect_tx(&full[s], 2u * (kI8A + (kDirect ? kBBytes : 0) + (with_side ? (dense ? 16384 + kRBytes : kRBytes) : 0)));
-          if constexpr (kDirect) {
-            if (!preloaded)
-              tma_load_2d_pair(st + kI8A, &maps.bp, fbar, kk * 128, n_half, kEvictNormal);  // int8 [N, K] rows
-          } else {
-            mbar_expect_tx(&bpk[s], kI8Bp);
-            tma_load_2d(smem + s * kI8Stage + kI8A, &maps.bp, &bpk[s], 0, ((n_half >> 7) * ks + kk) * 128,
-                        kEvictNormal);
-          }
+            mbar_expect_tx(&full[s], 2u * (kI8A + kBBytes + (with_side ? (dense ? 16384 + kRBytes : kRBytes) : 0)));
+          if (!preloaded)
+            tma_load_2d_pair(st + kI8A, &maps.bp, fbar, kk * 128, n_half, kEvictNormal);  // int8 [N, K] rows
           tma_load_2d_pair(st, &maps.a, fbar, kk * 128, m_own, kEvictNormal);
           if (with_side) {
             tma_load_2d_pair(sside + 16384, &maps.r, fbar, 0, n_half, kEvictNormal);
@@ -236,7 +206,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
       const uint32_t id_r = dense ? idesc_bf16(256, kN) : id_main;
       const uint32_t total = uint32_t(my_tiles) * ks;
       if (total > 0) {
-        mbar_wait_cluster(kDirect ? &full[0] : &bready[0], 0);
+        mbar_wait_cluster(&full[0], 0);
         tc_fence_after();
       }
       uint32_t g = 0;
@@ -245,7 +215,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
         if (p.dbg_ts && lane_id() == 0 && i < 8) p.dbg_ts[512 + (blockIdx.x >> 1) * 64 + i * 8] = globaltimer();
 #endif
         if (i > 0) {
-          mbar_wait_bo(tmem_empty, (i - 1) & 1, p.dbg & (1 << 20));
+          mbar_wait_bo(tmem_empty, (i - 1) & 1, SERQ_DBG(p.dbg, (1 << 20)));
           tc_fence_after();
         }
 #ifdef SERQ_DIAG_TS
@@ -254,9 +224,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
         for (int kk = 0; kk < ks; ++kk, ++g) {
           const int s = g % kI8Stages;
           const uint32_t st = sb + s * kI8Stage;
-          const uint64_t a = make_sdesc(st, 16, 1024, 2), b = make_sdesc(st + kI8A + kBp, 16, 1024, 2);
+          const uint64_t a = make_sdesc(st, 16, 1024, 2), b = make_sdesc(st + kI8A, 16, 1024, 2);
           const uint32_t first = kk > 0 ? 1u : 0u;
-          const bool no_mma = p.dbg & (1 << 18);
+          const bool no_mma = SERQ_DBG(p.dbg, (1 << 18));
           if (elect_one() && !no_mma) {
             mma_i8_pair(0, a, b, id_main, first);
             mma_i8_pair(0, a + 2, b + 2, id_main, 1u);
@@ -276,7 +246,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
 #endif
           if (g + 1 < total) {
             const uint32_t gn = g + 1;
-            mbar_wait_cluster(kDirect ? &full[gn % kI8Stages] : &bready[gn % kI8Stages], (gn / kI8Stages) & 1);
+            mbar_wait_cluster(&full[gn % kI8Stages], (gn / kI8Stages) & 1);
             tc_fence_after();
           }
 #ifdef SERQ_DIAG_TS
@@ -291,68 +261,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
         }
 #ifdef SERQ_DIAG_TS
         if (p.dbg_ts && lane_id() == 0 && i < 8) p.dbg_ts[512 + (blockIdx.x >> 1) * 64 + i * 8 + 2] = globaltimer();
-#endif
-      }
-    }
-  } else if (warp >= 8) {
-    // ------------------------------------------------------------ INT4 -> INT8 transform (both CTAs)
-    if constexpr (kDirect) return;  // (no such warps are launched in direct mode)
-    const int tw = int(warp) - 8;  // 0..7
-    const uint32_t bready_leader = map_rank(smem_u32(&bready[0]), 0);
-    uint32_t g = 0;
-    for (int i = 0; i < my_tiles; ++i) {
-      for (int kk = 0; kk < ks; ++kk, ++g) {
-        const int s = g % kI8Stages;
-        const uint32_t ph = (g / kI8Stages) & 1;
-#ifdef SERQ_DIAG_TS
-        const bool stamp = p.dbg_ts && blockIdx.x == 0 && tw == 0 && lane_id() == 0 && g < 32;
-        if (stamp) p.dbg_ts[8 * g] = clock64();
-#endif
-        mbar_wait_bo(&bpk[s], ph, p.dbg & (1 << 20));
-#ifdef SERQ_DIAG_TS
-        if (stamp) p.dbg_ts[8 * g + 1] = clock64();
-#endif
-        const uint8_t* pk = smem + s * kI8Stage + kI8A;
-        const uint32_t bdst = smem_u32(smem + s * kI8Stage + kI8A + kBp);
-        // 1024 tasks (128 rows x 8 output chunks of 16 B); a warp covers 4 rows per pass.
-        // All loads first: the st.shared asm below is a compiler barrier.
-        constexpr int kIt = 1024 / (32 * kI8TrWarps);
-        uint2 wv[kIt];
-        if (!(p.dbg & (1 << 17)))
-#pragma unroll
-        for (int it = 0; it < kIt; ++it) {
-          const int task = (it * kI8TrWarps + tw) * 32 + int(lane_id());
-          wv[it] = ld_shared_v2(pk + (task >> 3) * 64 + (task & 7) * 8);
-        }
-        if (!(p.dbg & (1 << 17)))
-#pragma unroll
-        for (int it = 0; it < kIt; ++it) {
-          const int task = (it * kI8TrWarps + tw) * 32 + int(lane_id());
-          const int row = task >> 3, chunk = task & 7;
-          const uint2 lo = widen_int4x8(wv[it].x), hi = widen_int4x8(wv[it].y);
-          st_shared_v4(bdst + row * 128 + ((uint32_t(chunk) ^ uint32_t(row & 7)) * 16), lo.x, lo.y, hi.x, hi.y);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-#ifdef SERQ_DIAG_TS
-        if (stamp) p.dbg_ts[8 * g + 2] = clock64();
-#endif
-        if (leader) {
-          // the MMA waits on this barrier only: also make it imply "A landed"
-          mbar_wait(&full[s], ph);
-        }
-        __syncwarp();
-#ifdef SERQ_DIAG_TS
-        if (stamp) p.dbg_ts[8 * g + 3] = clock64();
-#endif
-        if (lane_id() == 0) {
-          if (p.dbg & 4096)
-            mbar_arrive_cluster(bready_leader + uint32_t(s) * 8u);
-          else
-            mbar_arrive_remote(bready_leader + uint32_t(s) * 8u);
-        }
-#ifdef SERQ_DIAG_TS
-        if (stamp) p.dbg_ts[8 * g + 4] = clock64();
 #endif
       }
     }
@@ -472,7 +380,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kDirect>::kThr
         // the CTA's final tile: the pipeline is drained (its last MMAs completed before tmem_full), so
         // every chunk gets its own 2 KB box there and no store waits on another; otherwise two
         // boxes per warp alternate and a box is rewritten once the store from two chunks ago read it
-        const bool final_tile = i == my_tiles - 1 && !(p.dbg & (1 << 26));
+        const bool final_tile = i == my_tiles - 1 && !(SERQ_DBG(p.dbg, (1 << 26)));
         uint8_t* box = final_tile ? smem + (int(q) * (kN / 32) + c) * 2048 : stage_out + (c & 1) * 2048;
         const uint32_t rbase = smem_u32(box) + lane_id() * 64;
         if (!final_tile && lane_id() == 0) bulk_wait_read_1();

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* st = smem + s * kStageBytes;
           const bool rstep = it >= p.k_steps;
           const int kk = rstep ? it - p.k_steps : it;
-          if (p.dbg & 1) {
+          if (SERQ_DBG(p.dbg, 1)) {
             mbar_arrive(&full[s]);
             continue;
           }
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (my_tiles > 0) wait_unit(0, 0);
     for (int i = 0; i < my_tiles; ++i) {
       const uint32_t acc = (i & 1) ? kAccB1 : 0u;
-      if (i > 0 && !(p.dbg & 8)) {
+      if (i > 0 && !(SERQ_DBG(p.dbg, 8))) {
         mbar_wait(tmem_empty, (i - 1) & 1);  // epilogue i-1 drained the overlapping columns
         tc_fence_after();
       }
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t fa0 = kSfBase + (g & 1) * kSfCols, fb0 = fa0 + 8;
         const uint32_t fa1 = kSfBase + ((g + 1) & 1) * kSfCols, fb1 = fa1 + 8;
         const uint32_t first = uu > 0 ? 1u : 0u;
-        const bool do_cp = !(p.dbg & 4);
+        const bool do_cp = !(SERQ_DBG(p.dbg, 4));
         if (elect_one()) {
           if (do_cp) {
             const uint32_t sa = st0 + kSmemA + kSmemB, sb = sa + kSmemSFA;
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane_id() == 0 && !(p.dbg & 2)) {
+        if (lane_id() == 0 && !(SERQ_DBG(p.dbg, 2))) {
           tma_store_2d(&map_y, stage_out, n0 + c * 64, m0 + q * 32);
           bulk_commit();
         }

@@ -123,7 +123,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     mbar_init(&tmem_full[0], 1);
     mbar_init(&tmem_full[1], 1);
-    mbar_init(tmem_empty, (p.dbg & 256) ? 4 : 8);  // dbg 256: timing only, leader epilogue alone
+    mbar_init(tmem_empty, (SERQ_DBG(p.dbg, 256)) ? 4 : 8);  // dbg 256: timing only, leader epilogue alone
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -158,7 +158,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], ((g / k2Stages) & 1) ^ 1);
           const uint32_t st = smem_base + s * k2StageBytes;
           const uint32_t fbar = map_rank(smem_u32(&full[s]), 0);
-          if (p.dbg & 1) {
+          if (SERQ_DBG(p.dbg, 1)) {
             if (leader) mbar_arrive(&full[s]);
             continue;
           }
@@ -223,7 +223,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (my_tiles > 0) wait_unit(0, 0);
       for (int i = 0; i < my_tiles; ++i) {
         const uint32_t acc = (i & 1) ? kAccB1 : 0u;
-        if (i > 0 && !(p.dbg & 8)) {
+        if (i > 0 && !(SERQ_DBG(p.dbg, 8))) {
           mbar_wait(tmem_empty, (i - 1) & 1);  // both epilogues drained the overlapping columns
           tc_fence_after();
         }
@@ -247,7 +247,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t fa0 = kSfBase + (g & 1) * kSfCols, fb0 = fa0 + 8;
           const uint32_t fa1 = kSfBase + ((g + 1) & 1) * kSfCols, fb1 = fa1 + 8;
           const uint32_t first = uu > 0 ? 1u : 0u;
-          const bool do_cp = !(p.dbg & 4);
+          const bool do_cp = !(SERQ_DBG(p.dbg, 4));
 #ifdef SERQ_DIAG_TS
           const bool stamp = p.dbg_ts && blockIdx.x == 0 && ustamp < 100 && lane_id() == 0;
           if (stamp) p.dbg_ts[4 * ustamp] = clock64();
@@ -374,7 +374,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
           tc_fence_before();
           __syncwarp();
-          if (lane_id() == 0 && (leader || !(p.dbg & 256))) mbar_arrive_cluster_relaxed(tmem_empty_leader);
+          if (lane_id() == 0 && (leader || !(SERQ_DBG(p.dbg, 256)))) mbar_arrive_cluster_relaxed(tmem_empty_leader);
 #ifdef SERQ_DIAG_TS
           if (est) p.dbg_ts[423 + 4 * i] = clock64();
 #endif
@@ -393,7 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                          pack_bf16x2(__uint_as_float(src[8 * j + 6]), __uint_as_float(src[8 * j + 7])));
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane_id() == 0 && !(p.dbg & 2) && m_own < p.M) {
+          if (lane_id() == 0 && !(SERQ_DBG(p.dbg, 2)) && m_own < p.M) {
             tma_store_2d(&maps.y, stage_out, n0 + c * 64 + h * 32, m_own + q * 32);
             bulk_commit();
           }

@@ -29,13 +29,11 @@ constexpr int k3Xs = 128 * 32 + 512;
 constexpr int k3EpiG = 32 * 32;
 constexpr int k3SmemBytesG = 1024 + k3Slots * k3SlotBytes + k3RB + k3RSF + k3Xs + 4 * k3EpiG + 512;
 static_assert(k3SmemBytesG <= 232448, "exceeds the 227 KB dynamic shared memory limit");
-static_assert(131072 + 32768 <= k3Slots * k3SlotBytes, "split-tile exchange regions must fit in the drained pipeline");
 
 struct Pair3Maps {
   CUtensorMap a, b, r, y, sfa, sfb, sfr;
   CUtensorMap b64;       // narrow tiles: 64-row B boxes (each CTA's half of a 128-wide N tile)
   CUtensorMap xs, sfxs;  // gather: the quantizer's x[:, idx] codes (32-B rows, 32B swizzle) and scale factors
-  CUtensorMap ws;  // split-wave fp32 partials [slabs x 128 rows][256], box 32 x 32, 128B swizzle
 };
 
 __device__ __forceinline__ void tma_load_2d_pair_nohint(uint32_t dst, const CUtensorMap* m, uint32_t bar, int32_t c0,
@@ -58,8 +56,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tmem_full = bars + 2 * k3Slots;     // [2] both
   uint64_t* tmem_empty = bars + 2 * k3Slots + 2;
   uint64_t* r_empty = bars + 2 * k3Slots + 3;   // R side buffer consumed (both)
-  uint64_t* ws_bar = bars + 2 * k3Slots + 4;    // [4] per epilogue warp: partner partial landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * k3Slots + 8);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * k3Slots + 4);
 
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t rank = cluster_rank();
@@ -78,16 +75,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int n_tiles = tiles_m * tiles_n;
   const bool has_r = p.r > 0;
   const int units = (p.k_steps + 1) >> 1;       // slots per tile (last one may hold a single step)
-  // work items: tiles [0, split_from) whole, then every remaining tile as two K-halves
-  const int split_from = min(p.split_from, n_tiles);
-  // or: tiles [0, narrow_from) whole, then every remaining tile as two 256 x 128 tiles
-  const int narrow_from = split_from < n_tiles ? 0x7fffffff : min(p.narrow_from, n_tiles);
-  const int n_items = split_from < n_tiles ? split_from + 2 * (n_tiles - split_from)
-                                           : narrow_from + 2 * (n_tiles - narrow_from);
-  const int half_units = units >> 1;
+  // work items: tiles [0, narrow_from) whole, then every remaining tile as two 256 x 128 tiles
+  const int narrow_from = min(p.narrow_from, n_tiles);
+  const int n_items = narrow_from + 2 * (n_tiles - narrow_from);
   struct Item {
-    int tile, half, lo, hi;  // half: -1 = whole tile; [lo, hi) = k-unit range
-    int nsub;                // -1: 256 columns; 0 / 1: the first / second 128 columns only
+    int tile, lo, hi;  // [lo, hi) = k-unit range
+    int nsub;          // -1: 256 columns; 0 / 1: the first / second 128 columns only
   };
   // tile -> (M tile, N tile): M fastest, or grouped (group_m M-tiles x all N-tiles per group)
   auto tile_mn = [&](int tile, int& mt, int& nt) {
@@ -106,24 +99,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   auto item_of = [&](int w) {
     Item it;
     it.nsub = -1;
+    it.tile = w;
+    it.lo = 0;
+    it.hi = units;
     if (w >= narrow_from) {
       const int j = w - narrow_from;
       it.tile = narrow_from + (j >> 1);
       it.nsub = j & 1;
-      it.half = -1;
-      it.lo = 0;
-      it.hi = units;
-    } else if (w < split_from) {
-      it.tile = w;
-      it.half = -1;
-      it.lo = 0;
-      it.hi = units;
-    } else {
-      const int j = w - split_from;
-      it.tile = split_from + (j >> 1);
-      it.half = j & 1;
-      it.lo = it.half ? half_units : 0;
-      it.hi = it.half ? units : half_units;
     }
     return it;
   };
@@ -150,7 +132,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     mbar_init(&tmem_full[1], 1);
     mbar_init(tmem_empty, 8);
     mbar_init(r_empty, 1);
-    for (int w = 0; w < 4; ++w) mbar_init(&ws_bar[w], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -173,11 +154,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int r_uses = 0;
       for (int i = 0; i < my_tiles; ++i) {
         const Item itm = item_of(cluster_id + i * n_clusters);
-        const int tile = (p.dbg & 16384) ? 0 : itm.tile;  // diagnostics: every cluster streams tile 0
+        const int tile = (SERQ_DBG(p.dbg, 16384)) ? 0 : itm.tile;  // diagnostics: every cluster streams tile 0
         int mt, nt;
         tile_mn(tile, mt, nt);
         const int m_own = mt * 256 + int(rank) * 128;
-        const bool narrow = itm.nsub >= 0 && !(p.dbg & 96);  // diagnostics 32 / 64: full-tile loads
+        const bool narrow = itm.nsub >= 0 && !(SERQ_DBG(p.dbg, 96));  // diagnostics 32 / 64: full-tile loads
         const int n0 = nt * kBN + (narrow ? itm.nsub * 128 : 0);
         const int n_half = n0 + int(rank) * (narrow ? 64 : 128);
         const int mblk = m_own / 128;
@@ -190,7 +171,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (with_r && r_uses > 0) mbar_wait(r_empty, (r_uses - 1) & 1);  // previous R MMAs are done
           if (with_r) ++r_uses;
           const uint32_t fbar = map_rank(smem_u32(&full[slot]), 0);
-          const bool no_sf = p.dbg & 32768;  // diagnostics: skip scale-factor loads (request-count test)
+          const bool no_sf = SERQ_DBG(p.dbg, 32768);  // diagnostics: skip scale-factor loads (request-count test)
           if (leader)
             mbar_expect_tx(&full[slot], 2u * (len * (k3StepBytes - (no_sf ? 3072 : 0) - (narrow ? 8192 + 1024 : 0)) +
                                               (with_r ? k3RB + k3RSF + (kGather ? k3Xs : 0) : 0)));
@@ -280,8 +261,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_after();
         }
         const Item itm = item_of(cluster_id + i * n_clusters);
-        id0 = itm.nsub >= 0 && !(p.dbg & 64) ? id0n : id0w;  // diagnostics 64: 256-wide MMAs
-        id1 = itm.nsub >= 0 && !(p.dbg & 64) ? id1n : id1w;
+        id0 = itm.nsub >= 0 && !(SERQ_DBG(p.dbg, 64)) ? id0n : id0w;  // diagnostics 64: 256-wide MMAs
+        id1 = itm.nsub >= 0 && !(SERQ_DBG(p.dbg, 64)) ? id1n : id1w;
         for (int uu = itm.lo; uu < itm.hi; ++uu, ++u) {
           const int slot = u % k3Slots;
           const int len = (2 * uu + 1 < p.k_steps) ? 2 : 1;
@@ -295,7 +276,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const bool stamp = p.dbg_ts && blockIdx.x == 0 && u < 100 && lane_id() == 0;
           if (stamp) p.dbg_ts[4 * u] = clock64();
 #endif
-          const bool no_mma = p.dbg & 1024;  // diagnostics: feed rate alone
+          const bool no_mma = SERQ_DBG(p.dbg, 1024);  // diagnostics: feed rate alone
           if (elect_one() && !no_mma) {
             cps(st0, fa0, fb0);
             step4(acc, a0, b0, fa0, fb0, first, 4);
@@ -383,147 +364,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&tmem_full[b], (i >> 1) & 1);
       tc_fence_after();
 #ifdef SERQ_DIAG_TS
-      if (est) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); ep[1] = (long long)g; ep[3] = itm.half; }
+      if (est) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); ep[1] = (long long)g; ep[3] = -1; }
 #endif
       const uint32_t acc = (b ? kAccB1 : 0u) + lane_base;
-      if (itm.half >= 0) {
-        // ---- split tile (always in the last round: the pipeline smem is drained).
-        // Symmetric exchange: half h finalises output chunks {2h, 2h+1} (64 columns
-        // each) and publishes its fp32 partial of the OTHER two chunks to its slab,
-        // then raises its flag; it waits for the partner's flag, TMA-loads the
-        // partner's partial of its own chunks, adds its accumulator (main K-half +
-        // partner K-half, a + b == b + a in fp32: order-independent) and stores bf16.
-        // Every box has its own slot of drained pipeline memory:
-        //   [0, 64 KB): 4 warps x 2 published chunks x 2 fp32 boxes (32 x 32, 128B swizzle)
-        //   [64, 128 KB): 4 warps x 2 partner chunks x 2 fp32 boxes
-        //   [128, 160 KB): 4 warps x 2 own chunks x 2 bf16 output boxes
-        const int st_idx = tile - split_from;
-        const int hf = itm.half;
-        const uint32_t swz = lane_id() & 7;
-        const int slab_row = ((st_idx * 2) * 2 + int(rank)) * 128 + q * 32;  // + half * 256 rows
-        int* flags = p.sk_cnt + st_idx * 4;                                    // [half][rank]
-        // 1) publish the partner's chunks
-#pragma unroll 1
-        for (int k = 0; k < 2; ++k) {
-          const int c = 2 * (hf ^ 1) + k;
-          uint32_t v[32], w[32];
-          tmem_ld_32x32b_x32(acc + c * 64, v);
-          tmem_ld_32x32b_x32(acc + c * 64 + 32, w);
-          tmem_ld_wait();
-          uint8_t* wb8 = smem + q * 16384 + k * 8192;
-          const uint32_t rowb = smem_u32(wb8) + lane_id() * 128;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t* src = h ? w : v;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              st_shared_v4(rowb + h * 4096 + ((uint32_t(j) ^ swz) * 16), src[4 * j], src[4 * j + 1], src[4 * j + 2],
-                           src[4 * j + 3]);
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane_id() == 0) {
-            tma_store_2d(&maps.ws, wb8, c * 64, slab_row + hf * 256);
-            tma_store_2d(&maps.ws, wb8 + 4096, c * 64 + 32, slab_row + hf * 256);
-            bulk_commit();
-          }
-        }
-
-#ifdef SERQ_DIAG_TS
-        if (p.dbg_ts && q == 0 && lane_id() == 0) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p.dbg_ts[1024 + 148 * 24 + 296 + blockIdx.x * 8 + 0] = (long long)g; }
-#endif
-        if (lane_id() == 0) bulk_wait_all();
-        fence_proxy_async_global();
-#ifdef SERQ_DIAG_TS
-        if (p.dbg_ts && q == 0 && lane_id() == 0) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p.dbg_ts[1024 + 148 * 24 + 296 + blockIdx.x * 8 + 1] = (long long)g; }
-#endif
-        named_bar_sync(1, 128);
-        if (q == 0 && lane_id() == 0) {
-          __threadfence();
-          st_release_gpu(flags + hf * 2 + int(rank), 1);
-        }
-#ifdef SERQ_DIAG_TS
-        if (p.dbg_ts && q == 0 && lane_id() == 0) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p.dbg_ts[1024 + 148 * 24 + 296 + blockIdx.x * 8 + 2] = (long long)g; }
-#endif
-
-        // 2) the partner's partial of our chunks
-        if (lane_id() == 0) {
-          int* pf = flags + (hf ^ 1) * 2 + int(rank);
-          while (ld_acquire_gpu(pf) == 0) {
-          }
-#ifdef SERQ_DIAG_TS
-        if (p.dbg_ts && q == 0) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p.dbg_ts[1024 + 148 * 24 + 296 + blockIdx.x * 8 + 3] = (long long)g; }
-#endif
-          fence_proxy_async_global();
-          mbar_expect_tx(&ws_bar[q], 16384);
-          for (int k = 0; k < 2; ++k) {
-            const int c = 2 * hf + k;
-            uint8_t* pb = smem + 65536 + q * 16384 + k * 8192;
-            tma_load_2d(pb, &maps.ws, &ws_bar[q], c * 64, slab_row + (hf ^ 1) * 256, kEvictFirst);
-            tma_load_2d(pb + 4096, &maps.ws, &ws_bar[q], c * 64 + 32, slab_row + (hf ^ 1) * 256, kEvictFirst);
-          }
-        }
-        __syncwarp();
-        mbar_wait(&ws_bar[q], 0);
-#ifdef SERQ_DIAG_TS
-        if (p.dbg_ts && q == 0 && lane_id() == 0) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p.dbg_ts[1024 + 148 * 24 + 296 + blockIdx.x * 8 + 4] = (long long)g; }
-#endif
-
-        // 3) own chunks: accumulator + partner partial -> bf16 -> TMA store
-#pragma unroll 1
-        for (int k = 0; k < 2; ++k) {
-          const int c = 2 * hf + k;
-          uint32_t v[32], w[32];
-          tmem_ld_32x32b_x32(acc + c * 64, v);
-          tmem_ld_32x32b_x32(acc + c * 64 + 32, w);
-          tmem_ld_wait();
-          const uint8_t* pb = smem + 65536 + q * 16384 + k * 8192;
-          float f[64];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 o = *reinterpret_cast<const float4*>(pb + h * 4096 + lane_id() * 128 + ((j ^ swz) * 16));
-              const uint32_t* src = h ? w : v;
-              f[h * 32 + 4 * j] = __uint_as_float(src[4 * j]) + o.x;
-              f[h * 32 + 4 * j + 1] = __uint_as_float(src[4 * j + 1]) + o.y;
-              f[h * 32 + 4 * j + 2] = __uint_as_float(src[4 * j + 2]) + o.z;
-              f[h * 32 + 4 * j + 3] = __uint_as_float(src[4 * j + 3]) + o.w;
-            }
-          }
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint8_t* ybox = smem + 131072 + q * 8192 + (k * 2 + h) * 2048;
-            const uint32_t ybase = smem_u32(ybox) + lane_id() * 64;
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              st_shared_v4(ybase + ((uint32_t(j) ^ sw) * 16), pack_bf16x2(f[h * 32 + 8 * j], f[h * 32 + 8 * j + 1]),
-                           pack_bf16x2(f[h * 32 + 8 * j + 2], f[h * 32 + 8 * j + 3]),
-                           pack_bf16x2(f[h * 32 + 8 * j + 4], f[h * 32 + 8 * j + 5]),
-                           pack_bf16x2(f[h * 32 + 8 * j + 6], f[h * 32 + 8 * j + 7]));
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane_id() == 0 && m_own < p.M) {
-              tma_store_2d(&maps.y, ybox, n0 + c * 64 + h * 32, m_own + q * 32);
-              bulk_commit();
-            }
-          }
-        }
-        // every accumulator column has been read (no later tile reuses it: last round)
-        tc_fence_before();
-        __syncwarp();
-        if (lane_id() == 0) mbar_arrive_cluster_relaxed(tmem_empty_leader);
-        named_bar_sync(1, 128);
-        if (q == 0 && lane_id() == 0) flags[(hf ^ 1) * 2 + int(rank)] = 0;  // consumed: ready for the next launch
-#ifdef SERQ_DIAG_TS
-        if (p.dbg_ts && q == 0 && lane_id() == 0) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p.dbg_ts[1024 + 148 * 24 + 296 + blockIdx.x * 8 + 5] = (long long)g; }
-#endif
-
-#ifdef SERQ_DIAG_TS
-        if (est) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); ep[2] = (long long)g; }
-#endif
-        continue;
-      }
 #pragma unroll 1
       for (int cc = 0; cc < n_chunks; ++cc) {
         const int c = (b || n_chunks == 2) ? cc : (cc + 3) & 3;
@@ -538,7 +381,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         // the CTA's final tile: the pipeline is drained, so each (chunk, half) box gets its
         // own 2 KB of slot memory and the TMA stores go out without waiting on each other
-        const bool final_tile = i == my_tiles - 1 && !(p.dbg & (1 << 26));
+        const bool final_tile = i == my_tiles - 1 && !(SERQ_DBG(p.dbg, (1 << 26)));
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t* src = h ? w : v;

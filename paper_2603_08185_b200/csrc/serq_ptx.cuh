@@ -6,6 +6,17 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+// Diagnostics (timestamps, feed/MMA isolation switches) exist only in a SERQ_DIAG
+// build (tools/); the product library compiles every diagnostic branch away.
+#if defined(SERQ_DIAG_TS) && !defined(SERQ_DIAG)
+#define SERQ_DIAG 1
+#endif
+#ifdef SERQ_DIAG
+#define SERQ_DBG(flags, bit) ((flags) & (bit))
+#else
+#define SERQ_DBG(flags, bit) 0
+#endif
+
 namespace serq {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -1043,20 +1043,6 @@ __global__ void transpose_codes_kernel(const int32_t* __restrict__ src, int64_t 
   }
 }
 
-// reference INT codes int32 [K, N] (|code| <= 8) -> packed two's-complement nibbles,
-// tiled [N/128][K/128][128 rows][64 B] (k even -> low nibble); the CTA-pair INT
-// kernel TMA-loads one contiguous 8-KB tile per 128-K step and widens in SMEM.
-__global__ void pack_int4_tiled_kernel(const int32_t* __restrict__ src, int64_t K, int64_t N, int ksteps,
-                                       uint8_t* __restrict__ dst) {
-  const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t k = int64_t(blockIdx.y) * 2;
-  if (n >= N || k >= K) return;
-  const int32_t lo = src[k * N + n];
-  const int32_t hi = k + 1 < K ? src[(k + 1) * N + n] : 0;
-  const size_t off = ((size_t(n >> 7) * ksteps + size_t(k >> 7)) * 128 + size_t(n & 127)) * 64 + size_t((k & 127) >> 1);
-  dst[off] = uint8_t((lo & 0xF) | ((hi & 0xF) << 4));
-}
-
 // colsum[n] = sum_k codes[k, n]; scale f64 -> f32 copy
 __global__ void colsum_kernel(const int32_t* __restrict__ src, int64_t K, int64_t N, const double* __restrict__ s64,
                               int32_t* __restrict__ colsum, float* __restrict__ s32) {

@@ -45,6 +45,27 @@ def _require_cuda(t: torch.Tensor, name: str) -> None:
         raise ValidationError(f"{name} must be a CUDA tensor")
 
 
+def _check_salient_idx(salient_idx, r: int, K: int) -> np.ndarray | None:
+    """The reference indexes x[:, idx] (compensate.py:311, 335) and raises on a bad index; the
+    kernels read x[row, idx[j]] for j < r straight from device memory, so a short, out-of-range or
+    repeated index must be rejected here, before it can fault the context or read garbage."""
+    if salient_idx is None:
+        return None
+    idx = np.asarray(salient_idx.cpu() if isinstance(salient_idx, torch.Tensor) else salient_idx)
+    if idx.ndim != 1:
+        raise ValidationError(f"salient_idx must be 1-D, got shape {idx.shape}")
+    if idx.size and not np.issubdtype(idx.dtype, np.integer):
+        raise ValidationError(f"salient_idx must be integers, got {idx.dtype}")
+    idx = idx.astype(np.int64)
+    if idx.size != r:
+        raise ValidationError(f"salient_idx has {idx.size} entries, the compensator rank is {r}")
+    if idx.size and (idx.min() < 0 or idx.max() >= K):
+        raise ValidationError(f"salient_idx out of range [0, {K})")
+    if np.unique(idx).size != idx.size:
+        raise ValidationError("salient_idx repeats a channel")
+    return idx
+
+
 def mx_sizes(rows: int, cols: int) -> tuple[int, int]:
     cb, sb = ctypes.c_int64(), ctypes.c_int64()
     _lib.call("serq_mx_sizes", rows, cols, ctypes.byref(cb), ctypes.byref(sb))
@@ -197,12 +218,37 @@ class _Handle:
             pass
 
 
+def _check_host_io(x_host: torch.Tensor, y_host: torch.Tensor, K: int, N: int) -> None:
+    """The *_host entry points copy M*K*2 bytes in and M*N*2 bytes out with raw cudaMemcpyAsync:
+    the host tensors must be exactly bf16 [M, K] / [M, N], contiguous, on the host."""
+    for t, name in ((x_host, "x_host"), (y_host, "y_host")):
+        if not isinstance(t, torch.Tensor) or t.is_cuda:
+            raise ValidationError(f"{name} must be a host tensor")
+        if t.dtype != torch.bfloat16:
+            raise ValidationError(f"{name} must be bfloat16, got {t.dtype}")
+        if t.dim() != 2 or not t.is_contiguous():
+            raise ValidationError(f"{name} must be a contiguous 2-D tensor")
+    M = x_host.shape[0]
+    if M <= 0:
+        raise ValidationError("x must be non-empty")
+    if tuple(x_host.shape) != (M, K):
+        raise ValidationError(f"x_host must be [M, {K}], got {tuple(x_host.shape)}")
+    if tuple(y_host.shape) != (M, N):
+        raise ValidationError(f"y_host must be [{M}, {N}], got {tuple(y_host.shape)}")
+
+
 class MxLinear:
     """Packed MXFP4 SERQ linear (main_t + comp.r_q of build_serq_rtn_mx,
     compensate.py:343-357) resident on one GPU."""
 
     def __init__(self, codes, exps, r_codes=None, r_exps=None, salient_idx=None, device="cuda"):
         device = torch.device(device)
+        if device.type != "cuda":
+            raise ValidationError("MxLinear lives on a CUDA device")
+        with torch.cuda.device(device):
+            self._init(codes, exps, r_codes, r_exps, salient_idx, device)
+
+    def _init(self, codes, exps, r_codes, r_exps, salient_idx, device):
         codes = _dev(codes, torch.uint8, device)
         exps = _dev(exps, torch.int32, device)
         self.N, self.K = codes.shape
@@ -212,7 +258,11 @@ class MxLinear:
             re = _dev(r_exps, torch.int32, device)
         else:
             rc = re = None
-        idx = None if salient_idx is None else np.asarray(salient_idx, dtype=np.int64)
+        if exps.shape != (self.N, self.K // 32):
+            raise ValidationError(f"exps must be [N, K/32] = {(self.N, self.K // 32)}, got {tuple(exps.shape)}")
+        if self.r and (r_codes.shape[0] != self.N or tuple(r_exps.shape) != (self.N, self.r // 32)):
+            raise ValidationError("r_codes / r_exps must be [N, r] / [N, r/32]")
+        idx = _check_salient_idx(salient_idx, self.r, self.K) if self.r else None
         self.contiguous = idx is None or np.array_equal(idx, np.arange(self.r))
         self.gather_idx = None if self.contiguous else torch.from_numpy(idx.astype(np.int32)).to(device)
         h = ctypes.c_void_p()
@@ -270,10 +320,10 @@ class MxLinear:
 
     def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor) -> None:
         """End to end from (pinned) host bf16 memory through the C-ABI."""
-        if x_host.is_cuda or y_host.is_cuda:
-            raise ValidationError("forward_host takes host tensors")
-        _lib.call("serq_forward_mx_host_gather", self._h.ptr, x_host.data_ptr(), x_host.shape[0],
-                  _ptr(self.gather_idx), y_host.data_ptr(), _stream())
+        _check_host_io(x_host, y_host, self.K, self.N)
+        with torch.cuda.device(self.device):
+            _lib.call("serq_forward_mx_host_gather", self._h.ptr, x_host.data_ptr(), x_host.shape[0],
+                      _ptr(self.gather_idx), y_host.data_ptr(), _stream())
 
 
 class IntLinear:
@@ -290,6 +340,12 @@ class IntLinear:
         of one bf16 plane -- for R matrices that carry a large share of the output (a GPTQ-swapped
         R holds the salient rows themselves); served by the group-wise kernel (K <= 8192)."""
         device = torch.device(device)
+        if device.type != "cuda":
+            raise ValidationError("IntLinear lives on a CUDA device")
+        with torch.cuda.device(device):
+            self._init(codes, scales, bits, r_dense, r_codes, r_scales, salient_idx, device, group_size, r_split)
+
+    def _init(self, codes, scales, bits, r_dense, r_codes, r_scales, salient_idx, device, group_size, r_split):
         codes = _dev(codes, torch.int32, device)
         self.K, self.N = codes.shape
         scales = _dev(np.asarray(scales, dtype=np.float64) if not isinstance(scales, torch.Tensor) else scales,
@@ -315,7 +371,9 @@ class IntLinear:
                 raise ValidationError("integer R needs one scale per output column (row groups of size r)")
         else:
             self.r_mode, self.r, rdata, rs = _lib.SERQ_R_NONE, 0, None, None
-        idx = None if salient_idx is None else np.asarray(salient_idx, dtype=np.int64)
+        if self.r and rdata.shape[1] != self.N:
+            raise ValidationError(f"R must be [r, N] with N = {self.N}")
+        idx = _check_salient_idx(salient_idx, self.r, self.K) if self.r else None
         self.contiguous = idx is None or np.array_equal(idx, np.arange(self.r))
         self.salient_idx = None if idx is None or self.contiguous else torch.from_numpy(idx.astype(np.int32)).to(device)
         h = ctypes.c_void_p()
@@ -372,3 +430,9 @@ def device_info() -> dict:
 
 def last_launch_count() -> int:
     return int(_lib.load().serq_last_launch_count())
+
+
+def last_kernel() -> str:
+    """Name of the last kernel the C-ABI launched on this thread (which instantiation a
+    configuration takes, e.g. ``serq_i8_pair_kernel<256>``)."""
+    return _lib.load().serq_last_kernel().decode()

@@ -1,0 +1,230 @@
+"""GPU parity at the EXACT configurations bench.py reports (BASELINE C1, C2, C3, C5).
+
+Each test builds the config the way the bench does (workload.make_linear / the
+reference builders), runs the production launch through the C-ABI, asserts
+which kernel instantiation ran, and compares with the oracle:
+  * integer accumulators bit-exact over the FULL output (C1, C3);
+  * bf16 Y within max 1e-2 / mean 1e-3 (TOL_MAX / TOL_MEAN) of bf16(oracle) on
+    row x column slices -- exact restrictions of the full problem, because an
+    output element depends only on its activation row and its weight column, and
+    MX blocks / per-token / per-output-channel scales are local to those
+    (SURVEY 7 hard-part 7).  Slices cover the first, a middle and the last tile.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import serq_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL_MAX, TOL_MEAN = 1e-2, 1e-3
+
+
+@pytest.fixture(scope="module")
+def D():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2603_08185_b200 import device
+
+    return device
+
+
+def _cuda(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)
+
+
+def _mx_rows(t, rows):
+    codes = np.ascontiguousarray(t.element_codes[rows])
+    return O.MxT(codes, np.ascontiguousarray(t.block_scale_exponents[rows]), t.block_size,
+                 (codes.shape[0], codes.shape[1]))
+
+
+def _check_mx_slices(x, y, main_t, comp, row_slices, col_slices):
+    """Y[rows, cols] against the oracle forward on the restricted problem."""
+    for rs in row_slices:
+        for cs in col_slices:
+            mt = _mx_rows(main_t, cs)
+            c = None
+            if comp is not None and comp.rank:
+                c = O.Comp(comp.rank, np.asarray(comp.salient_idx), r_q=_mx_rows(comp.r_q, cs))
+            ref = O.forward_mx(x[rs], mt, c)
+            mx, mean = O.parity_errors(y[rs, cs], ref)
+            assert mx <= TOL_MAX and mean <= TOL_MEAN, (rs, cs, mx, mean)
+
+
+# ---------------------------------------------------------------- C2 (the headline)
+
+
+@pytest.mark.parametrize("r", [64, 0])
+def test_c2_mxfp4_4096_cubed(D, r):
+    """BASELINE C2: MXFP4 M = K = N = 4096, r = 64 -- bench.py's workload and builder
+    (workload.make_linear + api.build_serq_rtn_mx), serq_forward_mx (K1-MX + pair3),
+    K = 4096 (all 64 K-steps + the salient MMA), 256 tiles on 74 pairs incl. the narrow
+    last round.  r = 0: the pair3 kernel without a salient term."""
+    from paper_2603_08185_b200 import api, workload as WL
+
+    M = K = N = 4096
+    wl = WL.make_linear(K, N, M, 64, 0.01, 50.0, "mx")
+    main_t, comp = api.build_serq_rtn_mx(wl.w, np.arange(r))
+    # the device builder equals the reference builder (column slice: artefacts are column-local)
+    cols = np.r_[0:256, 3840:4096]
+    o_main, o_comp = O.build_serq_rtn_mx(np.ascontiguousarray(wl.w[:, cols]), np.arange(r), 32)
+    assert np.array_equal(main_t.element_codes[cols], o_main.element_codes)
+    assert np.array_equal(main_t.block_scale_exponents[cols], o_main.block_scale_exponents)
+    if r:
+        assert np.array_equal(comp.r_q.element_codes[cols], o_comp.r_q.element_codes)
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents,
+                     comp.r_q.element_codes if r else None, comp.r_q.block_scale_exponents if r else None,
+                     np.arange(r) if r else None)
+    x = _cuda(wl.x, torch.bfloat16)
+    act = D.MxActivation(torch.empty(D.mx_sizes(M, K)[0], dtype=torch.uint8, device="cuda"),
+                         torch.empty(D.mx_sizes(M, K)[1], dtype=torch.uint8, device="cuda"), M, K)
+    y = lin.forward(x, act).float().cpu().numpy()
+    assert D.last_kernel() == "serq_mx_pair3_kernel"
+    # the activation codes the step produced (all of them)
+    c, e = D.unpack_mx(act.codes, act.sf, M, K)
+    rows = np.r_[0:256, 2048:2304, 3840:4096]
+    enc = O.mx_encode(wl.x[rows], 32)
+    assert np.array_equal(c.cpu().numpy()[rows], enc.element_codes)
+    assert np.array_equal(e.cpu().numpy()[rows], enc.block_scale_exponents)
+    _check_mx_slices(wl.x, y, main_t, comp if r else None,
+                     [slice(0, 256), slice(2048, 2304), slice(3840, 4096)],
+                     [slice(0, 4096)])
+
+
+# ---------------------------------------------------------------- C1 / C3 (integer)
+
+
+def _int_case(cfg_name, group=None):
+    from paper_2603_08185_b200 import workload as WL
+
+    wl, meta = WL.make_config(cfg_name)
+    r = wl.r
+    if group is None:
+        main, comp = O.build_per_channel_int(wl.w, np.arange(r), 4, r_mode=meta["r_mode"])
+    else:
+        main, comp = O.build_grouped_int(wl.w, np.arange(r), group, 4, r_mode=meta["r_mode"])
+    return wl, meta, main, comp
+
+
+def _int_lin(D, main, comp, r, r_mode, group=None):
+    kw = dict(r_dense=comp.r_dense) if r_mode == "dense" else dict(r_codes=comp.r_q.codes, r_scales=comp.r_q.scales)
+    return D.IntLinear(main.codes, main.scales, 4, salient_idx=np.arange(r), group_size=group, **kw)
+
+
+def test_c1_int4_sym_full_accumulators(D):
+    """BASELINE C1: INT4 symmetric per-token activations, per-output-channel INT4 weights,
+    M = 512, K = N = 4096, r = 64, L in bf16: 64 tiles of 256 x 128 (the narrow CTA-pair
+    instantiation); the FULL accumulator matrix bit-exact, full Y within tolerance."""
+    wl, meta, main, comp = _int_case("c1")
+    M, K = wl.x.shape
+    N = wl.w.shape[1]
+    lin = _int_lin(D, main, comp, wl.r, "dense")
+    act = lin.quantize(_cuda(wl.x, torch.bfloat16), meta["bits"], meta["symmetric"])
+    acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    y = lin.gemm(act, acc_dump=acc).float().cpu().numpy()
+    assert D.last_kernel() == "serq_i8_pair_kernel<128>"
+    cfg = O.IntCfg(meta["bits"], True, "per-row")
+    xq = O.quantize_symmetric(wl.x, cfg)
+    assert np.array_equal(act.codes.cpu().numpy().astype(np.int32), xq.codes)
+    assert np.array_equal(act.scale64.cpu().numpy(), xq.scales[:, 0])
+    y_main, parts = O.int_gemm(xq, main, return_partials=True)
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), parts[0][1])
+    y_ref = y_main + O.dequantize(O.gather_columns(xq, np.arange(wl.r))) @ comp.r_dense
+    mx, mean = O.parity_errors(y, y_ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+def test_c3_w4a8_per_channel_full_accumulators(D):
+    """BASELINE C3: W4A8 (INT8 asymmetric per-token activations, INT4 per-channel weights),
+    M = 2048, K = 4096, N = 11008, integer R at r = 128: 344 tiles on 74 CTA pairs -> the
+    256-column instantiation with up to 5 tiles per cluster (accumulator reuse, tmem_empty /
+    side_empty phases, ping-pong epilogue staging, final tile in the drained pipeline).
+    FULL main and R accumulators bit-exact; Y within tolerance on all rows."""
+    wl, meta, main, comp = _int_case("c3")
+    M, K = wl.x.shape
+    N = wl.w.shape[1]
+    r = wl.r
+    lin = _int_lin(D, main, comp, r, "int")
+    act = lin.quantize(_cuda(wl.x, torch.bfloat16), meta["bits"], meta["symmetric"])
+    acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    accr = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    for _ in range(2):  # twice: a second launch must not depend on the first (no stale state)
+        y = lin.gemm(act, acc_dump=acc, accr_dump=accr).float().cpu().numpy()
+        assert D.last_kernel() == "serq_i8_pair_kernel<256>"
+    xq = O.quantize_asymmetric(wl.x, O.IntCfg(meta["bits"], False, "per-row"))
+    assert np.array_equal(act.codes.cpu().numpy().view(np.uint8).astype(np.int32), xq.codes)
+    assert np.array_equal(act.zp.cpu().numpy(), xq.zero_points[:, 0])
+    y_main, parts = O.int_gemm(xq, main, return_partials=True)
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), parts[0][1])
+    y_r, rparts = O.int_gemm(O.gather_columns(xq, np.arange(r)), comp.r_q, return_partials=True)
+    assert np.array_equal(accr.cpu().numpy().astype(np.int64), rparts[0][1])
+    mx, mean = O.parity_errors(y, y_main + y_r)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+def test_c3_w4a8_group128(D):
+    """C3's shape with the paper's group-wise weights (row groups of 128, scales [32, N]):
+    every group's exact integer partial on 512 rows (86 tiles on 74 pairs: multi-tile
+    clusters), and Y of the full M = 2048 launch on row slices."""
+    wl, meta, main, comp = _int_case("c3", group=128)
+    M, K = wl.x.shape
+    N = wl.w.shape[1]
+    r = wl.r
+    lin = _int_lin(D, main, comp, r, "int", group=128)
+    cfg = O.IntCfg(meta["bits"], False, "per-row")
+    # full launch: Y on row slices (per-token scales make rows independent)
+    y = lin.gemm(lin.quantize(_cuda(wl.x, torch.bfloat16), meta["bits"], False)).float().cpu().numpy()
+    assert D.last_kernel() == "serq_i8g_pair_kernel"
+    for rs in (slice(0, 256), slice(1024, 1280), slice(M - 256, M)):
+        y_ref, _ = O.forward_int(wl.x[rs], main, comp, cfg)
+        mx, mean = O.parity_errors(y[rs], y_ref)
+        assert mx <= TOL_MAX and mean <= TOL_MEAN, (rs, mx, mean)
+    # 512 rows: every group partial bit-exact
+    m2 = 512
+    x2 = np.ascontiguousarray(wl.x[:m2])
+    act = lin.quantize(_cuda(x2, torch.bfloat16), meta["bits"], False)
+    G = K // 128
+    acc = torch.zeros((G, m2, N), dtype=torch.int32, device="cuda")
+    accr = torch.zeros((m2, N), dtype=torch.int32, device="cuda")
+    lin.gemm(act, acc_dump=acc, accr_dump=accr)
+    xq = O.quantize_asymmetric(x2, cfg)
+    xc = xq.codes.astype(np.int64) - xq.zero_points.astype(np.int64)
+    for gi in range(G):
+        part = O.exact_int_matmul(xc[:, gi * 128:(gi + 1) * 128], main.codes[gi * 128:(gi + 1) * 128])
+        assert np.array_equal(acc[gi].cpu().numpy().astype(np.int64), part), gi
+    _, rparts = O.int_gemm(O.gather_columns(xq, np.arange(r)), comp.r_q, return_partials=True)
+    assert np.array_equal(accr.cpu().numpy().astype(np.int64), rparts[0][1])
+
+
+# ---------------------------------------------------------------- C5 (Llama-3-70B-shaped linears)
+
+
+@pytest.mark.parametrize("K,N,r", [(8192, 10240, 128),   # qkv_proj at tp = 1 (the C5 block's r = 128)
+                                   (3584, 8192, 32)])    # down_proj row shard at tp = 8 (32 salient / rank)
+def test_c5_linears_m8192(D, K, N, r):
+    """C5 per-linear shapes at M = 8192 tokens through the production launch (the CTA-pair
+    kernel for r != 64): the device-built artefacts (api.build_serq_rtn_mx, as the bench)
+    equal the oracle builder on column slices, and Y on row x column slices."""
+    from paper_2603_08185_b200 import api
+
+    M = 8192
+    rng = np.random.default_rng(K + N)
+    w = rng.standard_normal((K, N)) * 0.02
+    w[:r] *= 8
+    main_t, comp = api.build_serq_rtn_mx(w, np.arange(r))
+    cols = np.r_[0:256, N - 256:N]
+    o_main, o_comp = O.build_serq_rtn_mx(np.ascontiguousarray(w[:, cols]), np.arange(r), 32)
+    assert np.array_equal(main_t.element_codes[cols], o_main.element_codes)
+    assert np.array_equal(comp.r_q.element_codes[cols], o_comp.r_q.element_codes)
+    assert np.array_equal(comp.r_q.block_scale_exponents[cols], o_comp.r_q.block_scale_exponents)
+    del w
+    x = O.bf16_round(O.synthetic_activations(M, K, K // 100, 50.0, seed=K))
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                     comp.r_q.block_scale_exponents, np.arange(r))
+    y = lin(_cuda(x, torch.bfloat16)).float().cpu().numpy()
+    assert D.last_kernel() == "serq_mx_pair_kernel"
+    _check_mx_slices(x, y, main_t, comp, [slice(0, 128), slice(4096, 4224), slice(M - 128, M)],
+                     [slice(0, 512), slice(N - 512, N)])

@@ -352,27 +352,23 @@ def test_int_grouped_rejects_unsupported_groups(D):
                                      (5, 8192, 200, 32), (1, 4096, 11008, 64), (16, 11008, 4096, 64),
                                      (1, 32768, 128, 64)])  # one tile over many CTAs (slot cap 32)
 def test_mx_decode_parity(D, M, K, N, r):
-    from paper_2603_08185_b200 import _lib
-
     x, main_t, comp = _mx_case(M, K, N, r, seed=K + M)
     lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents,
                      comp.r_q.element_codes if r else None, comp.r_q.block_scale_exponents if r else None,
                      np.arange(r) if r else None)
     xt = _cuda(x, torch.bfloat16)
     ref = O.forward_mx(x, main_t, comp)
-    # debug flag 1<<29: partials of the split-K reduction in full width through the drained stages
-    for flags in (0, 1 << 29, 0):
+    # the split-K partials meet through the narrow DSMEM buffer or, when they do not fit it
+    # (e.g. M = 16 with many CTAs per tile), through the drained pipeline stages
+    for _ in range(2):
         # serq_forward_mx: for M <= 8 the quantizer runs inside the decode kernel; Y and
         # the activation codes it reports
         act = D.MxActivation(torch.empty(D.mx_sizes(M, K)[0], dtype=torch.uint8, device="cuda"),
                              torch.empty(D.mx_sizes(M, K)[1], dtype=torch.uint8, device="cuda"), M, K)
-        _lib.load().serq_set_debug_flags(flags)
-        try:
-            y = lin.forward(xt, act).float().cpu().numpy()
-            # two-kernel path (quantizer, then the linear on codes)
-            y2 = lin.gemm(lin.quantize(xt)).float().cpu().numpy()
-        finally:
-            _lib.load().serq_set_debug_flags(0)
+        y = lin.forward(xt, act).float().cpu().numpy()
+        assert D.last_kernel().startswith("serq_mx_decode_cl_kernel" if r in (0, 64) else "serq_mx_persistent")
+        # two-kernel path (quantizer, then the linear on codes)
+        y2 = lin.gemm(lin.quantize(xt)).float().cpu().numpy()
         mx, mean = O.parity_errors(y, ref)
         assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
         c, e = D.unpack_mx(act.codes, act.sf, M, K)
@@ -382,31 +378,10 @@ def test_mx_decode_parity(D, M, K, N, r):
         assert np.array_equal(y2, y)
 
 
-def test_mx_linear_split_last_wave(D):
-    # 10 x 8 = 80 CTA-pair tiles on 74 pairs: the 6 leftover tiles run as K-halves
-    M, K, N, r = 2560, 1024, 2048, 64
-    x, main_t, comp = _mx_case(M, K, N, r, seed=99)
-    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
-                     comp.r_q.block_scale_exponents, np.arange(r))
-    ref = O.forward_mx(x, main_t, comp)
-    xt = _cuda(x, torch.bfloat16)
-    from paper_2603_08185_b200 import _lib
-
-    _lib.load().serq_set_debug_flags(8192)  # the split last wave is opt-in
-    try:
-        for _ in range(2):
-            y = lin(xt).float().cpu().numpy()
-            mx, mean = O.parity_errors(y, ref)
-            assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
-    finally:
-        _lib.load().serq_set_debug_flags(0)
-
-
 @pytest.mark.parametrize("M,K,N,gather", [(2560, 1024, 2048, False), (2600, 512, 4096, False),
                                           (4096, 1024, 4096, False), (2600, 512, 4096, True)])
 def test_mx_linear_narrow_last_round(D, M, K, N, gather):
-    # the leftover tiles of the last partial round run as 256 x 128 tiles (two per tile):
-    # parity with the oracle and bit-equality with the all-256-wide schedule (debug flag 1<<19);
+    # the leftover tiles of the last partial round run as 256 x 128 tiles (two per tile);
     # gather: an arbitrary salient set (the salient MMA's A operand from the quantizer's slice)
     r = 64
     idx = np.sort(np.random.default_rng(7).choice(K, r, replace=False)) if gather else np.arange(r)
@@ -417,14 +392,8 @@ def test_mx_linear_narrow_last_round(D, M, K, N, gather):
                      comp.r_q.block_scale_exponents, idx)
     xt = _cuda(x, torch.bfloat16)
     y = lin(xt).float().cpu().numpy()
-    from paper_2603_08185_b200 import _lib
-
-    _lib.load().serq_set_debug_flags(1 << 19)
-    try:
-        y_wide = lin(xt).float().cpu().numpy()
-    finally:
-        _lib.load().serq_set_debug_flags(0)
-    assert np.array_equal(y, y_wide)
+    assert D.last_kernel() == ("serq_mx_pair3_kernel<gather>" if gather else "serq_mx_pair3_kernel")
+    assert np.array_equal(lin(xt).float().cpu().numpy(), y)  # deterministic
     rows = np.r_[0:64, M - 300:M]  # oracle on the first rows and on the last (narrow-tile) rows
     ref = O.forward_mx(x[rows], main_t, comp)
     mx, mean = O.parity_errors(y[rows], ref)
