@@ -942,6 +942,11 @@ int serq_forward_mx(serq_linear_t* h, const void* x, int dtype, int64_t M, int64
   return rc;
 }
 
+#ifndef SERQ_I8_EPI
+#define SERQ_I8_EPI 2
+#endif
+constexpr int kI8Epi = SERQ_I8_EPI;  // epilogue column groups of the INT CTA-pair kernel (4 * kI8Epi warps)
+
 static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const float* sx, const int32_t* zp,
                            int64_t M, const void* xs, void* y, int64_t ldy, const float* addend, int32_t* acc_dump,
                            int32_t* accr_dump, serq_stream_t stream) {
@@ -1004,8 +1009,8 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   const bool pair_ok = M > 128 && (h->r_mode != SERQ_R_INT || h->contiguous) && h->r <= 128 &&
                        (h->r_mode != SERQ_R_DENSE || h->r <= 64) && !SERQ_DBG(g_debug_flags, 65536);
   if (pair_ok) {
-    CK(set_smem_attr(serq_i8_pair_kernel<256>, I8Cfg::kSmem));
-    CK(set_smem_attr(serq_i8_pair_kernel<128>, I8Cfg::kSmem));
+    CK(set_smem_attr(serq_i8_pair_kernel<256, kI8Epi>, I8Cfg<kI8Epi>::kSmem));
+    CK(set_smem_attr(serq_i8_pair_kernel<128, kI8Epi>, I8Cfg<kI8Epi>::kSmem));
     I8Maps im;
     int rc = make_map(&im.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K, M, h->K, 128, 128);
     if (!rc)
@@ -1042,11 +1047,12 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     const dim3 grid(unsigned(2 * (tiles < max_pairs ? tiles : max_pairs)));
     // launched with programmatic dependent launch: the prologue and the first weight stages
     // overlap the activation quantizer's tail
+    using Cfg = I8Cfg<kI8Epi>;
     if (narrow) {
-      CK(launch_pdl(serq_i8_pair_kernel<128>, grid, dim3(I8Cfg::kThreads), I8Cfg::kSmem, S(stream), im, p));
+      CK(launch_pdl(serq_i8_pair_kernel<128, kI8Epi>, grid, dim3(Cfg::kThreads), Cfg::kSmem, S(stream), im, p));
       LAUNCH_CHECK("serq_i8_pair_kernel<128>");
     } else {
-      CK(launch_pdl(serq_i8_pair_kernel<256>, grid, dim3(I8Cfg::kThreads), I8Cfg::kSmem, S(stream), im, p));
+      CK(launch_pdl(serq_i8_pair_kernel<256, kI8Epi>, grid, dim3(Cfg::kThreads), Cfg::kSmem, S(stream), im, p));
       LAUNCH_CHECK("serq_i8_pair_kernel<256>");
     }
     return SERQ_OK;

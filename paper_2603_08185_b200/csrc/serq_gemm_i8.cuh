@@ -25,11 +25,16 @@ constexpr int kI8A = 128 * 128;    // own 128 activation rows x 128 int8
 constexpr int kI8B = 128 * 128;    // own 128 weight rows x 128 int8
 constexpr int kI8Side = 2 * 16384;             // R operands: [A' (dense only)] + B_R
 constexpr int kI8Const = 4 * 256 * 4;
+// kE: epilogue column groups -- 4 * kE epilogue warps (warp w drains TMEM lane quadrant w % 4,
+// columns chunks e, e + kE, ...), each with one 2 KB output staging box
+template <int kE>
 struct I8Cfg {
-  static constexpr int kStages = 5;
+  static constexpr int kEpiWarps = 4 * kE;
+  static constexpr int kEpiBytes = kEpiWarps * 2048;
+  static constexpr int kStages = kE >= 4 ? 4 : 5;
   static constexpr int kStage = kI8A + kI8B;
-  static constexpr int kSmem = 1024 + kStages * kStage + kI8Side + kI8Const + 4 * 4096 + 512;
-  static constexpr int kThreads = 256;
+  static constexpr int kSmem = 1024 + kStages * kStage + kI8Side + kI8Const + kEpiBytes + 512;
+  static constexpr int kThreads = 128 + 32 * kEpiWarps;
   static_assert(kSmem <= 232448, "smem budget");
 };
 
@@ -92,22 +97,25 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
 }
 // kN: output columns per CTA-pair tile (256, or 128 for small problems so twice as many
 // pairs get a tile; each CTA then stages 64 weight rows)
-template <int kN = 256>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg::kThreads, 1)
+template <int kN = 256, int kE = 2>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE>::kThreads, 1)
     serq_i8_pair_kernel(const __grid_constant__ I8Maps maps, const GemmParams p) {
   static_assert(kN == 256 || kN == 128, "256- or 128-column tiles");
+  static_assert((kN / 32) % kE == 0, "column chunks split evenly over the epilogue groups");
+  using Cfg = I8Cfg<kE>;
+  constexpr int kEpiThreads = 32 * Cfg::kEpiWarps;
   constexpr int kBHalf = kN / 2;  // weight rows per CTA
   constexpr uint32_t kBBytes = kBHalf * 128;  // one 128-K step of this CTA's weight rows (int8)
   constexpr uint32_t kRBytes = kBHalf * 128;  // this CTA's R rows (int8 r <= 128 or bf16 r <= 64: 128 B each)
-  constexpr int kI8Stages = I8Cfg::kStages;
-  constexpr int kI8Stage = I8Cfg::kStage;
+  constexpr int kI8Stages = Cfg::kStages;
+  constexpr int kI8Stage = Cfg::kStage;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* side = smem + kI8Stages * kI8Stage;       // [A' 16K][B_R 16K]
   float* cst_f = reinterpret_cast<float*>(side + kI8Side);  // sw[256] | sr[256]
   int32_t* cst_i = reinterpret_cast<int32_t*>(cst_f + 512); // colsum[256] | colsum_r[256]
-  uint8_t* epi = reinterpret_cast<uint8_t*>(cst_i + 512);   // 4 warps x 2 x 2 KB staging (ping-pong)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + 4 * 4096);
+  uint8_t* epi = reinterpret_cast<uint8_t*>(cst_i + 512);   // one 2 KB staging box per epilogue warp
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + Cfg::kEpiBytes);
   uint64_t* full = bars;                       // [S] leader: A, B (+ side) landed, both CTAs
   uint64_t* empty = bars + kI8Stages;          // [S] both: MMAs of the stage done
   uint64_t* side_empty = bars + 2 * kI8Stages; // both: R MMAs done
@@ -142,7 +150,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg::kThreads, 1)
     }
     mbar_init(side_empty, 1);
     mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, 8);
+    mbar_init(tmem_empty, 2 * Cfg::kEpiWarps);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -268,9 +276,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg::kThreads, 1)
     // ------------------------------------------------------------ epilogue (both CTAs)
     pdl_wait();  // sx / zp / xs come from the quantizer; y may still be read by a predecessor
     pdl_launch_dependents();
-    const uint32_t q = warp & 3;
+    const uint32_t q = warp & 3;  // TMEM lane quadrant of this warp (warp id % 4)
+    const int eg = int(warp - 4) >> 2;  // column group: chunks eg, eg + kE, ...
     const uint32_t lane_base = (q * 32u) << 16;
-    uint8_t* stage_out = epi + q * 4096;
+    uint8_t* stage_out = epi + (warp - 4) * 2048;
     const uint32_t swz = (lane_id() >> 1) & 3;
     const uint32_t tmem_empty_leader = map_rank(smem_u32(tmem_empty), 0);
     for (int i = 0; i < my_tiles; ++i) {
@@ -279,8 +288,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg::kThreads, 1)
       const int m_own = mt * 256 + int(rank) * 128;
       const int n0 = nt * kN;
       // per-column constants of this tile
-      named_bar_sync(1, 128);  // previous tile's readers are done with the constants
-      for (int c = threadIdx.x - 128; c < kN; c += 128) {
+      named_bar_sync(1, kEpiThreads);  // previous tile's readers are done with the constants
+      for (int c = threadIdx.x - 128; c < kN; c += kEpiThreads) {
         const int n = n0 + c;
         const bool ok = n < p.N;
         cst_f[c] = ok ? p.sw[n] : 0.f;
@@ -288,7 +297,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg::kThreads, 1)
         cst_f[256 + c] = (ok && p.r_mode == kRInt) ? p.sr[n] : 0.f;
         cst_i[256 + c] = (ok && p.zp && p.r_mode == kRInt) ? -p.colsum_r[n] : 0;
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(1, kEpiThreads);
       const int row = m_own + int(q) * 32 + int(lane_id());
       float sx = 0.f;
       uint32_t zp = 0;
@@ -305,27 +314,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg::kThreads, 1)
       if (p.dbg_ts && leader && q == 0 && lane_id() == 0 && i < 8) p.dbg_ts[512 + cluster_id * 64 + i * 8 + 4] = globaltimer();
 #endif
 #pragma unroll 1
-      for (int c = 0; c < kN / 32; ++c) {
+      for (int cc = 0; cc < kN / 32 / kE; ++cc) {
+        const int c = cc * kE + eg;
         // exact in wrapping int32: |acc - zp*colsum| <= 255 * 8 * K < 2^31 for K < 2^20
         uint32_t packed[16];
-#pragma unroll
 #ifdef SERQ_DIAG_TS
         if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == (my_tiles > 1 ? 1 : 0)) p.dbg_ts[5300 + c * 8 + 0] = globaltimer();
 #endif
+        uint32_t vv[32], ww[32];
+        tmem_ld_32x32b_x32(lane_base + uint32_t(c * 32), vv);
+        if (has_r) tmem_ld_32x32b_x32(lane_base + 256 + uint32_t(c * 32), ww);
+        tmem_ld_wait();
+        if (cc == kN / 32 / kE - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive_cluster_relaxed(tmem_empty_leader);
+        }
+#pragma unroll
         for (int h = 0; h < 2; ++h) {
-          uint32_t v[16], w[16];
+          const uint32_t* v = vv + 16 * h;
+          const uint32_t* w = ww + 16 * h;
           const uint32_t col0 = uint32_t(c * 32 + h * 16);
-          tmem_ld_32x32b_x16(lane_base + col0, v);
-          if (has_r) tmem_ld_32x32b_x16(lane_base + 256 + col0, w);
-          tmem_ld_wait();
 #ifdef SERQ_DIAG_TS
           if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == (my_tiles > 1 ? 1 : 0)) p.dbg_ts[5300 + c * 8 + 4 + h] = globaltimer();
 #endif
-          if (c == kN / 32 - 1 && h == 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane_id() == 0) mbar_arrive_cluster_relaxed(tmem_empty_leader);
-          }
           // this half-chunk's column constants: broadcast vector loads, once
           const uint32_t cf = smem_u32(cst_f) + col0 * 4, ci = smem_u32(cst_i) + col0 * 4;
           float f[16];
@@ -381,9 +393,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg::kThreads, 1)
         // every chunk gets its own 2 KB box there and no store waits on another; otherwise two
         // boxes per warp alternate and a box is rewritten once the store from two chunks ago read it
         const bool final_tile = i == my_tiles - 1 && !(SERQ_DBG(p.dbg, (1 << 26)));
-        uint8_t* box = final_tile ? smem + (int(q) * (kN / 32) + c) * 2048 : stage_out + (c & 1) * 2048;
+        uint8_t* box = final_tile ? smem + (int(q) * (kN / 32) + c) * 2048 : stage_out;
         const uint32_t rbase = smem_u32(box) + lane_id() * 64;
-        if (!final_tile && lane_id() == 0) bulk_wait_read_1();
+        if (!final_tile && lane_id() == 0) bulk_wait_read_all();  // this warp's previous store read its box
         __syncwarp();
 #ifdef SERQ_DIAG_TS
         if (p.dbg_ts && leader && cluster_id == 0 && q == 0 && lane_id() == 0 && i == (my_tiles > 1 ? 1 : 0)) p.dbg_ts[5300 + c * 8 + 2] = globaltimer();
