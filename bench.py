@@ -10,9 +10,14 @@ One step = quantize X (K1-MX) + the fused SERQ linear (K2: main GEMM + the
 salient term + epilogue) on device-resident bf16 X.  An L2 flush (256 MiB
 write, > 126 MB L2) separates timed steps and is excluded from them.
 
-Multi-GPU (torchrun, one process per GPU): every rank runs the same linear
-on its own token batch (tokens are independent, no data-path collective),
-scaling "weak"; timing is the max over ranks.
+Multi-GPU (--gpus N > 1; re-executed under torch.distributed.run when
+WORLD_SIZE is unset, one process per GPU, NCCL): BASELINE config 5 -- the
+Llama-3-70B-shaped block linears, M = 8192 tokens, column/row tensor parallel
+with one all-reduce after o_proj and after down_proj, pipelined over token
+chunks under the GEMMs and captured with the kernels in one CUDA graph
+("strong" scaling, value = whole-job TFLOPS, max over ranks).  The line also
+carries the same block measured on one GPU by rank 0 (tp = 1) and the
+resulting efficiency.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
 oracle port of serq.compensate._forward_mx, compensate.py:319-340) on the
@@ -139,6 +144,9 @@ def run_reference(args) -> None:
     ws, rank, _ = dist_env()
     if rank != 0:
         return
+    if ws > 1:
+        run_reference_c5(args, ws)
+        return
     from paper_2603_08185_b200 import workload as WL
 
     wl = WL.make_linear(K, N, M, R, 0.01, 50.0, "mx")
@@ -166,6 +174,45 @@ def run_reference(args) -> None:
         "e2e": {"value": val, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def run_reference_c5(args, ws: int) -> None:
+    """Reference arm for the multi-GPU workload (C5 block linears): the oracle port of
+    _forward_mx (compensate.py:319-340) on the host cores over a bounded sample of the
+    block -- 16 token rows x 1024 output columns of each of the four linears at their full
+    K (output elements are independent, so the sample is exact work per element)."""
+    from oracle import serq_oracle as O
+
+    rows, cols, r = 16, 1024, 128
+    shapes = [("qkv_proj", 8192, 10240), ("o_proj", 8192, 8192), ("gate_up_proj", 8192, 57344),
+              ("down_proj", 28672, 8192)]
+    cases = []
+    for i, (_, k, _n) in enumerate(shapes):
+        rng = np.random.default_rng(40 + i)
+        w = rng.standard_normal((k, cols)) * 0.02
+        main_t, comp = O.build_serq_rtn_mx(w, np.arange(r), 32)
+        x = O.bf16_round(O.synthetic_activations(rows, k, k // 100, 50.0, seed=50 + i))
+        cases.append((x, main_t, comp, 2.0 * rows * cols * (k + r)))
+    flops = sum(c[3] for c in cases)
+    for _ in range(max(1, args.warmup)):
+        for x, mt, comp, _f in cases:
+            O.forward_mx(x, mt, comp)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for x, mt, comp, _f in cases:
+            O.forward_mx(x, mt, comp)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = flops / dt / 1e12
+    sample = (f"{rows} token rows x {cols} output columns of each C5 linear (full K, r={r}) per step, oracle port of "
+              f"_forward_mx, NumPy/OpenBLAS {os.cpu_count()} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOPS", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c5: Llama-3-70B-shaped block linears, SERQ MXFP4 r=128 -- CPU sample", "sample": sample},
+        "cpu_baseline": {"value": val, "unit": "TFLOPS", "cores": os.cpu_count(), "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
 
 
 def run_serq(args) -> None:
@@ -287,7 +334,7 @@ def run_serq(args) -> None:
                        "activations": "N(0,1), 1% channels x50, SAF a=0.5, salient-permuted, bf16",
                        "l2": "inputs larger than L2: steps cycle 4 weight sets x 8 activation/output sets (~620 MB > 126 MB L2), no flush",
                        "timing": "K steps back to back in one CUDA graph between two CUDA event-record nodes (device time, max over ranks)",
-                       "parallelism": f"replicas x{ws} (tokens independent, no collective)"},
+                       "parallelism": "single GPU (BASELINE C2; --gpus N > 1 runs the C5 tensor-parallel block)"},
             "tokens_per_s": ws * M / (ms_per_step / 1e3),
             "tflops_pct_of_fp4_peak": 100.0 * value / FP4_PEAK_TFLOPS,
             "breakdown_ms": {"quantize": q_ms, "linear": g_ms},
@@ -308,13 +355,37 @@ def run_serq(args) -> None:
             "gpu_launches": launches,
             "clocks": clocks,
         }
+        line["parity"] = parity_check(wl, main_t, comp, ys[0])
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_leg(wl.x, wl.w)
         if ws == 1 and not args.no_extra:
             line["other_configs"] = other_configs(hbm)
         print(json.dumps(line), flush=True)
+        if not line["parity"]["ok"]:
+            print("bench.py: the benchmarked output does not match the oracle", file=sys.stderr)
+            sys.exit(3)
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def parity_check(wl, main_t, comp, y, rows: int = 256) -> dict:
+    """CHECKER (test infrastructure, not measured): the first `rows` token rows of the
+    benchmarked output Y (weight set 0 on activation set 0, i.e. the C2 workload itself)
+    against the oracle's _forward_mx restatement (compensate.py:319-340) on the same
+    artefacts, at the north_star tolerance (max 1e-2 / mean 1e-3 vs bf16(oracle))."""
+    from oracle import serq_oracle as O
+
+    mt = O.MxT(np.asarray(main_t.element_codes), np.asarray(main_t.block_scale_exponents), 32,
+               tuple(np.asarray(main_t.element_codes).shape))
+    rq = comp.r_q
+    c = O.Comp(int(comp.rank), np.asarray(comp.salient_idx),
+               r_q=O.MxT(np.asarray(rq.element_codes), np.asarray(rq.block_scale_exponents), 32,
+                         tuple(np.asarray(rq.element_codes).shape)))
+    ref = O.forward_mx(wl.x[:rows], mt, c)
+    mx, mean = O.parity_errors(y[:rows].float().cpu().numpy(), ref)
+    return {"rows_checked": rows, "of": "C2 output (weight set 0, activation set 0)", "max_rel": mx, "mean_rel": mean,
+            "tol_max": 1e-2, "tol_mean": 1e-3, "ok": bool(mx <= 1e-2 and mean <= 1e-3),
+            "oracle": "oracle/serq_oracle.py forward_mx (checker only)"}
 
 
 def _round(d):
@@ -351,35 +422,88 @@ def other_configs(hbm_gbs: float) -> dict:
 
 
 def run_c5(args) -> None:
-    """--workload c5: Llama-3-70B-shaped block linears, tensor parallel over
-    the launched ranks (NCCL all-reduce after o_proj and down_proj)."""
+    """BASELINE C5 (the multi-GPU workload): Llama-3-70B-shaped block linears, M = 8192
+    tokens, tensor parallel over the launched ranks (NCCL all-reduce after o_proj and
+    down_proj, pipelined over token chunks, one CUDA graph per step)."""
     import torch
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
-    group = None
     if ws > 1:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2603_08185_b200 import benchmarks as B
 
-    p = B.c5_block_point(ws, rank, M=8192, steps=max(args.steps, 3), group=group)
-    t = torch.tensor([p["block_ms"]], device="cuda")
+    M = 8192
+    ref1 = None
+    if ws > 1 and rank == 0 and not args.no_extra:
+        # the same block on ONE GPU (tp = 1) for the efficiency figure; the other ranks wait
+        ref1 = B.c5_tp_point(1, 0, M=M, steps=max(args.steps // 2, 3), warm=args.warmup, with_e2e=False)
     if ws > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms = float(t.item())
+        torch.distributed.barrier()
+    with ClockSampler(local) as clk:
+        p = B.c5_tp_point(ws, rank, M=M, steps=args.steps, warm=max(args.warmup, 3))
+    clocks = clk.summary()
+
+    def max_over_ranks(v):
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        if ws > 1:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = max_over_ranks(p["step_ms"])
+    serial = max_over_ranks(p["serial_ms"])
+    ar = max_over_ranks(p["allreduce_ms"])
+    e2e_ms = max_over_ranks(p["e2e_ms"])
     if rank == 0:
-        print(json.dumps({"metric": "SERQ W4A4 Llama-3-70B-shaped block linears tokens/s", "value": 8192 / (ms * 1e-3),
-                          "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": 2, "ms_per_step": ms,
-                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                          "dtype": "fp4(e2m1)+e8m0 -> f32 -> bf16", "data": "synthetic",
-                          "config": {"workload": "c5 block linears tp", "parallelism": f"tp{ws}", **_round(p)}}))
+        value = p["flops_per_step"] / (ms * 1e-3) / 1e12
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": ws, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "fp4(e2m1)+e8m0 -> f32 accumulate -> bf16", "data": "synthetic",
+            "config": {"workload": "c5: Llama-3-70B-shaped block linears (qkv 8192x10240, o 8192x8192, gate_up "
+                                   "8192x57344, down 28672x8192), SERQ MXFP4 r=128, M=8192 tokens",
+                       "parallelism": f"tp{ws}", "chunks": p["chunks"], "graph": p["graph"],
+                       "l2": "inputs larger than L2 (weights + activations of the block per rank exceed 126 MB at tp<=4)",
+                       "timing": "steps back to back, CUDA events on the launching stream, max over ranks",
+                       "per_rank_linears": p["linears"]},
+            "tokens_per_s": M / (ms * 1e-3),
+            "serial_ms_per_step": serial, "allreduce_ms_per_step": ar,
+            "e2e": {"value": p["flops_per_step"] / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOPS",
+                    "h2d_bytes_per_step": p["h2d_bytes_per_step"], "d2h_bytes_per_step": p["d2h_bytes_per_step"],
+                    "ms_per_step": e2e_ms, "path": "tp.PipelinedTPBlock.forward with pinned H2D of x and D2H of the output"},
+            "gpu_launches": p["gpu_launches_per_step"] * args.steps,
+            "clocks": clocks,
+        }
+        if ref1 is not None:
+            line["tp1_reference"] = {"ms_per_step": ref1["step_ms"], "tokens_per_s": ref1["tokens_per_s"],
+                                     "tflops": ref1["block_tflops"]}
+            line["efficiency_vs_tp1"] = ref1["step_ms"] / (ws * ms)
+        print(json.dumps(_round(line)), flush=True)
     if ws > 1:
+        torch.distributed.barrier()
         torch.distributed.destroy_process_group()
 
 
+def relaunch(args) -> int:
+    """--gpus N > 1 outside torchrun: re-execute this command under torch.distributed.run
+    (one process per GPU on this node, rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
+    # communicator / NVLS lines for the driver's logs (stderr: stdout carries the JSON line)
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -389,9 +513,16 @@ def main():
     ap.add_argument("--no-extra", action="store_true", help="skip the other-config measurements")
     ap.add_argument("--workload", default="c2", choices=["c2", "c5"])
     args = ap.parse_args()
+    ws = int(os.environ.get("WORLD_SIZE", "0"))
+    if ws == 0 and args.gpus > 1:
+        sys.exit(relaunch(args))
+    ws = ws or 1
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
-    elif args.workload == "c5":
+    elif args.workload == "c5" or ws > 1:
         run_c5(args)
     else:
         run_serq(args)

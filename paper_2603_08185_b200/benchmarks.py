@@ -393,3 +393,99 @@ def c5_block_point(world: int = 1, rank: int = 0, M: int = 8192, r: int = 128, g
     return {"M": M, "tp": world, "r": r, "block_ms": t, "tokens_per_s": M / (t * 1e-3),
             "rank_tflops": flops / (t * 1e-3) / 1e12, "graph": use_graph,
             "linears": {s.name: [lins[s.name].K, lins[s.name].N, lins[s.name].r] for s in specs}}
+
+
+def c5_tp_point(world: int = 1, rank: int = 0, M: int = 8192, r: int = 128, group=None, steps: int = 10,
+                chunks: int = 4, warm: int = 3, with_e2e: bool = True) -> dict:
+    """BASELINE C5 tensor parallel: this rank's shard of the Llama-3-70B-shaped block linears
+    (qkv / gate_up column-parallel, o / down row-parallel with salient_per_rank(r) channels
+    per rank), token-chunk pipelined all-reduces (tp.PipelinedTPBlock on tp.DeviceBackend),
+    the whole step -- quantizers, fused GEMMs, NCCL all-reduces -- in ONE CUDA graph.
+
+    Times (device, CUDA events, the caller takes the max over ranks):
+      step_ms        one block step, ``steps`` graph replays back to back
+      serial_ms      the same with one chunk (no communication / compute overlap)
+      allreduce_ms   the two all-reduces of [M, hidden] bf16 alone
+      e2e_ms         pinned H2D of x + the step + D2H of the block output (public API)"""
+    import torch.distributed as dist
+
+    from . import tp
+
+    specs = tp.block_specs(8192, 28672, 1024)
+    lins, feeds = {}, {}
+    for spec in specs:
+        if spec.kind == "column":
+            n0, n1 = tp.column_shard(spec.n, world, rank)
+            lins[spec.name] = device_mx_linear(spec.k, n1 - n0, r, seed=101 + len(lins))
+        else:
+            k0, k1 = tp.row_shard(spec.k, world, rank)
+            lins[spec.name] = device_mx_linear(k1 - k0, spec.n, tp.salient_per_rank(r, world), seed=101 + len(lins))
+            feeds[spec.name] = outlier_x(M, k1 - k0, seed=7 + len(feeds))
+    x = outlier_x(M, 8192, seed=3)
+
+    def timed_graph(fn, n):
+        fn()
+        torch.cuda.synchronize()
+        graph = True
+        try:
+            g = graph_of(fn)
+        except Exception:  # a collective that cannot be captured: eager replay
+            g, graph = None, False
+        run = g.replay if g is not None else fn
+        for _ in range(warm):
+            run()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(group=group)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(n):
+            run()
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b) / n, graph
+
+    be = tp.DeviceBackend(lins, group)
+    blk = tp.PipelinedTPBlock(specs, be, chunks=chunks)
+    step_ms, graph = timed_graph(lambda: blk.forward(x, feeds), steps)
+    launches = be.launches_per_forward
+    be1 = tp.DeviceBackend(lins, group)
+    blk1 = tp.PipelinedTPBlock(specs, be1, chunks=1)
+    serial_ms, _ = timed_graph(lambda: blk1.forward(x, feeds), max(3, steps // 2))
+    outs = blk.forward(x, feeds)
+    ar_ms, _ = timed_graph(lambda: (tp.allreduce_sum_(outs["o_proj"], group), tp.allreduce_sum_(outs["down_proj"], group)),
+                           max(3, steps // 2))
+    flops = sum(2.0 * M * s.n * (s.k + r) for s in specs)  # the full block (padding of per-rank salient sets not counted)
+    out = {"M": M, "tp": world, "r": r, "chunks": len(tp.chunk_bounds(M, chunks)), "graph": graph,
+           "step_ms": step_ms, "serial_ms": serial_ms, "allreduce_ms": ar_ms, "block_tflops": flops / (step_ms * 1e-3) / 1e12,
+           "tokens_per_s": M / (step_ms * 1e-3), "flops_per_step": flops, "gpu_launches_per_step": launches,
+           "linears": {s.name: [lins[s.name].K, lins[s.name].N, lins[s.name].r] for s in specs}}
+    if with_e2e:
+        xh = x.cpu().pin_memory()
+        yh = torch.empty((M, lins["down_proj"].N), dtype=torch.bfloat16).pin_memory()
+        xd = torch.empty_like(x)
+
+        def e2e():
+            xd.copy_(xh, non_blocking=True)
+            o = blk.forward(xd, feeds)
+            yh.copy_(o["down_proj"], non_blocking=True)
+
+        ts = []
+        for i in range(warm + max(3, steps // 2)):
+            if world > 1:
+                dist.barrier(group=group)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            e2e()
+            b.record()
+            b.synchronize()
+            if i >= warm:
+                ts.append(a.elapsed_time(b))
+        out["e2e_ms"] = statistics.median(ts)
+        out["h2d_bytes_per_step"] = xh.numel() * 2
+        out["d2h_bytes_per_step"] = yh.numel() * 2
+    del lins, feeds
+    torch.cuda.empty_cache()
+    return out

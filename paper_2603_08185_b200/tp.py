@@ -94,11 +94,12 @@ def row_parallel_salient_layout(scores: np.ndarray, world: int, r_rank: int) -> 
 # ------------------------------------------------------------------ collectives
 
 
-def allreduce_sum_(t, group=None):
-    """In-place sum across ranks (bf16 on NCCL / any dtype on gloo)."""
+def allreduce_sum_(t, group=None, force: bool = False):
+    """In-place sum across ranks (bf16 on NCCL / any dtype on gloo).  ``force``: issue the
+    collective even for a single rank (exercises the NCCL / graph-capture path on one GPU)."""
     import torch.distributed as dist
 
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if dist.is_available() and dist.is_initialized() and (force or dist.get_world_size(group) > 1):
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t
 
@@ -163,3 +164,177 @@ class TPBlockLinears:
                 h = y
             out[spec.name] = y
         return out
+
+
+# ------------------------------------------------------------------ pipelined device driver
+
+
+def pipeline_schedule(n_chunks: int) -> list[tuple[str, int]]:
+    """Issue order of the token-chunk pipeline (SURVEY 7 hard-part 5).
+
+    ``("A", c)``: q/k/v and o_proj of chunk c, then o_proj's all-reduce of chunk c on the
+    communication stream.  ``("B", c)``: gate/up (on the reduced o output of chunk c) and
+    down_proj, then down_proj's all-reduce.  A(c + 1) is issued before B(c), so the o_proj
+    all-reduce of chunk c runs under chunk c + 1's q/k/v and o_proj GEMMs, and the
+    down_proj all-reduce of chunk c under B(c + 1).  Every chunk appears once in each
+    phase and B(c) always follows A(c)."""
+    if n_chunks < 1:
+        raise ValidationError("need at least one token chunk")
+    order = [("A", 0)]
+    for c in range(n_chunks):
+        if c + 1 < n_chunks:
+            order.append(("A", c + 1))
+        order.append(("B", c))
+    return order
+
+
+def chunk_bounds(m: int, n_chunks: int, align: int = 256) -> list[tuple[int, int]]:
+    """Row ranges of the token chunks: ``align``-row multiples (whole CTA-pair tiles), the
+    last chunk absorbing the remainder."""
+    n = max(1, min(n_chunks, m // align if m >= align else 1))
+    step = -(-m // n)
+    step = -(-step // align) * align
+    out, r0 = [], 0
+    while r0 < m:
+        out.append((r0, min(m, r0 + step)))
+        r0 += step
+    return out
+
+
+class PipelinedTPBlock:
+    """The C5 block linears of one rank with the two all-reduces pipelined under the GEMMs
+    (``pipeline_schedule`` over ``chunk_bounds`` token chunks).
+
+    The schedule is backend-independent; ``backend`` provides
+      ``out(name, m, n)``                   the [m, n] output buffer of a linear (allocated once),
+      ``linear(name, c, x_rows, y_rows)``   linear ``name`` on token chunk c,
+      ``reduce(name, c, y_rows)``           start the all-reduce (sum) of chunk c's output,
+      ``wait(name, c)``                     make later work wait for that all-reduce,
+      ``join()``                            wait for every outstanding all-reduce.
+    ``DeviceBackend`` issues the kernels on the current CUDA stream and the NCCL
+    collectives on a dedicated stream (events in between), so one ``forward`` -- quantizers,
+    fused SERQ GEMMs and collectives -- captures into ONE CUDA graph; the CPU tests drive the
+    same schedule over gloo."""
+
+    def __init__(self, specs: list[TPLinearSpec], backend, chunks: int = 4):
+        self.specs = {s.name: s for s in specs}
+        col = [s.name for s in specs if s.kind == "column"]
+        row = [s.name for s in specs if s.kind == "row"]
+        if len(col) != 2 or len(row) != 2:
+            raise ValidationError("the pipelined block expects qkv, o, gate_up, down")
+        (self.qkv, self.gate_up), (self.o_proj, self.down) = col, row
+        self.backend = backend
+        self.chunks = chunks
+
+    def forward(self, x, feeds: dict) -> dict:
+        """x [M, hidden] (replicated); feeds: this rank's K-slices of the o_proj input
+        (attention output) and of the down_proj input (SiLU(gate) * up).  gate/up consumes
+        the all-reduced o_proj output (the residual stream in the real block)."""
+        be = self.backend
+        m = x.shape[0]
+        bounds = chunk_bounds(m, self.chunks)
+        outs = {n: be.out(n, m, self.specs[n].n) for n in self.specs}
+
+        def rows(t, c):
+            r0, r1 = bounds[c]
+            return t[r0:r1]
+
+        for phase, c in pipeline_schedule(len(bounds)):
+            if phase == "A":
+                be.linear(self.qkv, c, rows(x, c), rows(outs[self.qkv], c))
+                be.linear(self.o_proj, c, rows(feeds[self.o_proj], c), rows(outs[self.o_proj], c))
+                be.reduce(self.o_proj, c, rows(outs[self.o_proj], c))
+            else:
+                be.wait(self.o_proj, c)
+                be.linear(self.gate_up, c, rows(outs[self.o_proj], c), rows(outs[self.gate_up], c))
+                be.linear(self.down, c, rows(feeds[self.down], c), rows(outs[self.down], c))
+                be.reduce(self.down, c, rows(outs[self.down], c))
+        be.join()
+        return outs
+
+
+class DeviceBackend:
+    """CUDA backend of ``PipelinedTPBlock``: per-shard device linears (``MxLinear``; their
+    N is this rank's shard), per-(linear, chunk) activation buffers, NCCL all-reduces on a
+    communication stream ordered by events."""
+
+    def __init__(self, lins: dict, group=None, force_collective: bool = False):
+        import torch
+
+        self.lins = lins
+        self.group = group
+        self.force = force_collective
+        self.comm = torch.cuda.Stream()
+        self._outs = {}
+        self._acts = {}
+        self._ev = {}
+        self._started = False
+        self.launches_per_forward = 0  # kernels of ours one forward issues (not counting NCCL's)
+        self._launches = 0
+
+    def out(self, name, m, n):
+        import torch
+
+        lin = self.lins[name]
+        key = (name, m)
+        if key not in self._outs:
+            self._outs[key] = torch.empty((m, lin.N), dtype=torch.bfloat16, device="cuda")
+        return self._outs[key]
+
+    def _act(self, name, c, m):
+        import torch
+
+        from . import device as D
+
+        key = (name, c, m)
+        if key not in self._acts:
+            lin = self.lins[name]
+            cb, sb = D.mx_sizes(m, lin.K)
+            a = D.MxActivation(torch.empty(cb, dtype=torch.uint8, device="cuda"),
+                               torch.empty(sb, dtype=torch.uint8, device="cuda"), m, lin.K)
+            if not lin.contiguous:
+                cbr, sbr = D.mx_sizes(m, lin.r)
+                a.xs_codes = torch.empty(cbr, dtype=torch.uint8, device="cuda")
+                a.xs_sf = torch.empty(sbr, dtype=torch.uint8, device="cuda")
+            self._acts[key] = a
+        return self._acts[key]
+
+    def _event(self, *key):
+        import torch
+
+        if key not in self._ev:
+            self._ev[key] = torch.cuda.Event()
+        return self._ev[key]
+
+    def linear(self, name, c, x_rows, y_rows):
+        import torch
+
+        if not self._started:  # the comm stream must follow earlier work on the caller's stream
+            self.comm.wait_stream(torch.cuda.current_stream())
+            self._started = True
+        from . import device as D
+
+        self.lins[name].forward(x_rows, self._act(name, c, x_rows.shape[0]), y_rows)
+        self._launches += D.last_launch_count()
+
+    def reduce(self, name, c, y_rows):
+        import torch
+
+        ready, done = self._event(name, c, "ready"), self._event(name, c, "done")
+        ready.record(torch.cuda.current_stream())
+        self.comm.wait_event(ready)
+        with torch.cuda.stream(self.comm):
+            allreduce_sum_(y_rows, self.group, self.force)
+            done.record(self.comm)
+
+    def wait(self, name, c):
+        import torch
+
+        torch.cuda.current_stream().wait_event(self._event(name, c, "done"))
+
+    def join(self):
+        import torch
+
+        torch.cuda.current_stream().wait_stream(self.comm)
+        self._started = False
+        self.launches_per_forward, self._launches = self._launches, 0

@@ -158,3 +158,84 @@ def _block_worker(rank, hidden, ffn, kv, m):
 
 def test_block_driver_reduces_after_o_and_down_only():
     _spawn(_block_worker, 64, 128, 16, 4)
+
+
+# ------------------------------------------------------------------ pipelined block (token chunks)
+
+
+def test_pipeline_schedule_overlaps_and_orders():
+    for n in (1, 2, 4, 7):
+        order = tp.pipeline_schedule(n)
+        assert sorted(order) == sorted([("A", c) for c in range(n)] + [("B", c) for c in range(n)])
+        pos = {op: i for i, op in enumerate(order)}
+        for c in range(n):
+            assert pos[("A", c)] < pos[("B", c)]  # gate/up needs the reduced o_proj output
+            if c + 1 < n:  # the o_proj all-reduce of chunk c has chunk c + 1's GEMMs to hide under
+                assert pos[("A", c + 1)] < pos[("B", c)]
+    for m, n in [(8192, 4), (300, 4), (1000, 4), (4096, 3)]:
+        b = tp.chunk_bounds(m, n)
+        assert b[0][0] == 0 and b[-1][1] == m and all(x[1] == y[0] for x, y in zip(b, b[1:]))
+        assert all(r0 % 256 == 0 for r0, _ in b)
+
+
+class _CpuBackend:
+    """Synchronous gloo backend: records the issue order of linears and all-reduces."""
+
+    def __init__(self, fns):
+        self.fns, self.log, self._outs = fns, [], {}
+
+    def out(self, name, m, n):
+        return self._outs.setdefault(name, torch.zeros((m, self.fns[name][1]), dtype=torch.float64))
+
+    def linear(self, name, c, x_rows, y_rows):
+        self.log.append(("lin", name, c))
+        y_rows.copy_(self.fns[name][0](x_rows))
+
+    def reduce(self, name, c, y_rows):
+        self.log.append(("ar", name, c))
+        tp.allreduce_sum_(y_rows)
+
+    def wait(self, name, c):
+        assert ("ar", name, c) in self.log
+
+    def join(self):
+        pass
+
+
+def _pipelined_worker(rank, hidden, ffn, kv, m, chunks):
+    specs = tp.block_specs(hidden, ffn, kv)
+    rng = np.random.default_rng(21)
+    weights = {s.name: rng.standard_normal((s.k, s.n)) for s in specs}
+    fns = {}
+    for s in specs:
+        w = weights[s.name]
+        if s.kind == "column":
+            n0, n1 = tp.column_shard(s.n, WORLD, rank)
+            fns[s.name] = ((lambda w=w, n0=n0, n1=n1: lambda x: x @ torch.from_numpy(w[:, n0:n1]))(), n1 - n0)
+        else:
+            k0, k1 = tp.row_shard(s.k, WORLD, rank)
+            fns[s.name] = ((lambda w=w, k0=k0, k1=k1: lambda x: x @ torch.from_numpy(w[k0:k1]))(), s.n)
+    be = _CpuBackend(fns)
+    blk = tp.PipelinedTPBlock(specs, be, chunks=chunks)
+    x = torch.from_numpy(np.random.default_rng(22).standard_normal((m, hidden)))
+    attn = np.random.default_rng(23).standard_normal((m, hidden))
+    act = np.random.default_rng(24).standard_normal((m, ffn))
+    k0, k1 = tp.row_shard(hidden, WORLD, rank)
+    f0, f1 = tp.row_shard(ffn, WORLD, rank)
+    out = blk.forward(x, {"o_proj": torch.from_numpy(attn[:, k0:k1]), "down_proj": torch.from_numpy(act[:, f0:f1])})
+    # exactly one all-reduce per chunk, after o_proj and down_proj only
+    ars = [e for e in be.log if e[0] == "ar"]
+    n_chunks = len(tp.chunk_bounds(m, chunks))
+    assert sorted(ars) == sorted([("ar", "o_proj", c) for c in range(n_chunks)] +
+                                 [("ar", "down_proj", c) for c in range(n_chunks)])
+    o_full = attn @ weights["o_proj"]
+    np.testing.assert_allclose(out["o_proj"].numpy(), o_full, rtol=1e-10, atol=1e-9)
+    n0, n1 = tp.column_shard(specs[2].n, WORLD, rank)
+    np.testing.assert_allclose(out["gate_up_proj"].numpy(), o_full @ weights["gate_up_proj"][:, n0:n1],
+                               rtol=1e-9, atol=1e-8)
+    np.testing.assert_allclose(out["down_proj"].numpy(), act @ weights["down_proj"], rtol=1e-10, atol=1e-9)
+
+
+@pytest.mark.parametrize("m,chunks", [(1024, 4), (600, 4), (256, 2)])
+def test_pipelined_block_matches_unchunked(m, chunks):
+    _spawn(_pipelined_worker, 64, 128, 16, m, chunks)
