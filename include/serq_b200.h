@@ -32,6 +32,10 @@
  *                          (+ re-encode of x[:, idx]) then the fused GEMM      compensate.py:319-340
  *   serq_forward_mx_host   forward_reconstructed(x, main_t, comp, None) end to end from host memory
  *                                                                         compensate.py:272-295
+ *   serq_forward_int       forward_reconstructed(x, main, comp, act_cfg) on device: quantize_asymmetric
+ *                          (or _symmetric) per token + gather_columns + the fused integer GEMM
+ *                                                                         compensate.py:296-316
+ *   serq_forward_int_host  the same end to end from host memory            compensate.py:272-316
  */
 #ifndef SERQ_B200_H
 #define SERQ_B200_H
@@ -184,6 +188,23 @@ int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* 
  * serq_forward_mx; the salient slice is re-encoded per chunk on the device. */
 int serq_forward_mx_host_gather(serq_linear_t* h, const void* x_host, int64_t M, const int32_t* gather_idx,
                                 void* y_host, serq_stream_t stream);
+
+/* Integer quantize + linear in one call (compensate.py:296-316, the int branch of
+ * forward_reconstructed): x (bf16 / f32 / f64 [M, K], row pitch ldx) -> per-token codes /
+ * scales / zero points (serq_act_quant_int layout, caller-allocated; zp unused and may be
+ * NULL when symmetric) -> y bf16 [M, N] (pitch ldy).  xs: the salient slice buffer the
+ * handle's R needs (bf16 [M, r] for a dense R, int8 [M, r] for an integer R on a
+ * non-contiguous salient set, else NULL); salient_idx (device int32 [r]) only for a
+ * non-contiguous salient set.  The linear is PDL-chained to the quantizer. */
+int serq_forward_int(serq_linear_t* h, const void* x, int dtype, int64_t M, int64_t ldx, int bits, int symmetric,
+                     const int32_t* salient_idx, int8_t* codes, double* scale64, float* scale32, int32_t* zp,
+                     void* xs, void* y, int64_t ldy, serq_stream_t stream);
+
+/* serq_forward_int end to end from HOST memory: X bf16 [M, K] in, Y bf16 [M, N] out (pinned
+ * for full PCIe rate), pipelined over token chunks on two copy streams; device scratch in the
+ * handle; synchronises `stream`. */
+int serq_forward_int_host(serq_linear_t* h, const void* x_host, int64_t M, int bits, int symmetric,
+                          const int32_t* salient_idx, void* y_host, serq_stream_t stream);
 
 /* Number of kernels the last forward on this thread launched (evidence for bench). */
 int serq_last_launch_count(void);

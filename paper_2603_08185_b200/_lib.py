@@ -48,6 +48,8 @@ SIGNATURES = {
     "serq_forward_mx": (_I, [_P, _P, _I, _I64, _I64, _P, _P, _P, _P, _P, _P, _I64, _P]),
     "serq_forward_mx_host_gather": (_I, [_P, _P, _I64, _P, _P, _P]),
     "serq_forward_mx_host": (_I, [_P, _P, _I64, _P, _P]),
+    "serq_forward_int": (_I, [_P, _P, _I, _I64, _I64, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I64, _P]),
+    "serq_forward_int_host": (_I, [_P, _P, _I64, _I, _I, _P, _P, _P]),
     "serq_last_launch_count": (_I, []),
     "serq_last_kernel": (ctypes.c_char_p, []),
     "serq_set_debug_flags": (_I, [_I]),

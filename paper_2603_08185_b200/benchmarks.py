@@ -234,12 +234,34 @@ def int_linear_point(M, K, N, r, r_mode, bits, symmetric, flush: Flusher | None 
     def lin_only(i):
         lins[i % 8].gemm(acts[i % 8], ys[i % 8])
 
+    def fwd(i):  # the public single call (serq_forward_int): quantizer + PDL-chained linear
+        lins[i % 8].forward(xs[i % 8], bits, symmetric, acts[i % 8], ys[i % 8])
+
     t_step = time_steps(step, n_steps)
+    t_fwd = time_steps(fwd, n_steps)
     t_lin = time_steps(lin_only, n_steps)
     flops = 2.0 * M * N * (K + r)
-    return {"M": M, "K": K, "N": N, "r": r, "r_mode": r_mode, "act_bits": bits, "act_symmetric": symmetric,
-            "weight_group": group or K, "step_us": t_step * 1e3, "linear_us": t_lin * 1e3, "linear_tops": flops / (t_lin * 1e-3) / 1e12,
-            "step_tops": flops / (t_step * 1e-3) / 1e12, "tokens_per_s": M / (t_step * 1e-3)}
+    out = {"M": M, "K": K, "N": N, "r": r, "r_mode": r_mode, "act_bits": bits, "act_symmetric": symmetric,
+           "weight_group": group or K, "step_us": t_fwd * 1e3, "two_call_step_us": t_step * 1e3,
+           "linear_us": t_lin * 1e3, "linear_tops": flops / (t_lin * 1e-3) / 1e12,
+           "step_tops": flops / (t_fwd * 1e-3) / 1e12, "tokens_per_s": M / (t_fwd * 1e-3)}
+    # end to end through the C-ABI from pinned host memory (serq_forward_int_host)
+    xh = xs[0].cpu().pin_memory()
+    yh = torch.empty((M, N), dtype=torch.bfloat16).pin_memory()
+    for _ in range(2):
+        lins[0].forward_host(xh, yh, bits, symmetric)
+    ts = []
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        lins[0].forward_host(xh, yh, bits, symmetric)
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    e2e = statistics.median(ts)
+    out["e2e"] = {"us": e2e * 1e3, "tops": flops / (e2e * 1e-3) / 1e12, "h2d_bytes": M * K * 2, "d2h_bytes": M * N * 2,
+                  "path": "serq_forward_int_host (C-ABI): pinned H2D, quantize, fused linear, D2H"}
+    return out
 
 
 def svd_baseline_point(M, K, N, r, bits=8, n_steps: int = 16) -> dict:

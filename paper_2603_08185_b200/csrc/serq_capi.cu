@@ -200,8 +200,11 @@ struct serq_linear {
   uint8_t* ws_codes = nullptr;
   uint8_t* ws_sf = nullptr;
   void* ws_y = nullptr;
-  uint8_t* ws_xs = nullptr;   // gather layers: x[:, idx] codes and scale factors per chunk
+  uint8_t* ws_xs = nullptr;   // gather layers: x[:, idx] codes and scale factors per chunk (INT: xs slice)
   uint8_t* ws_xsf = nullptr;
+  double* ws_s64 = nullptr;   // INT end to end: per-token scales and zero points
+  float* ws_s32 = nullptr;
+  int32_t* ws_zp = nullptr;
   // end-to-end pipeline: H2D and D2H copy streams + per-chunk events (created lazily)
   cudaStream_t e2e_in = nullptr, e2e_out = nullptr;
   std::mutex e2e_mu;  // the end-to-end scratch and streams are per handle: one host call at a time
@@ -212,7 +215,7 @@ namespace {
 void free_handle(serq_linear* h) {
   void* ptrs[] = {h->w, h->sfw, h->rbuf, h->sfr, h->sw, h->colsum, h->sr, h->colsum_r,
                   h->ws_x, h->ws_codes, h->ws_sf, h->ws_y,
-                  h->sw_g, h->colsum_g, h->cterm, h->ws_xs, h->ws_xsf};
+                  h->sw_g, h->colsum_g, h->cterm, h->ws_xs, h->ws_xsf, h->ws_s64, h->ws_s32, h->ws_zp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : h->e2e_ev)
@@ -1110,6 +1113,111 @@ int serq_linear_int_addend(const serq_linear_t* h, const int8_t* a_codes, const 
   return linear_int_impl(h, a_codes, sx, zp, M, xs, y, ldy, addend, nullptr, nullptr, stream);
 }
 
+// ---------------------------------------------------------------- end to end from host memory
+}  // extern "C"
+
+namespace {
+
+// Chunk plan over token rows: every chunk starts on a 256-row boundary (whole MX scale-factor
+// tiles), small chunks at both ends (the first H2D and the last D2H overlap nothing), 1024-row
+// chunks in the middle (per-chunk launch / copy setup ~25 us, measured with uniform 256-row
+// chunks); the last chunk absorbs M % 256.
+int64_t e2e_plan(int64_t M, int64_t* plan) {
+  int64_t chunks = 0;
+  const int64_t body = (M / 256) * 256, rem = M - body;
+  const bool ramp = body >= 2560;  // 256 + 512 + [>= 1024] + 512 + 256
+  int64_t mid = body - (ramp ? 1536 : 0);
+  const int64_t slots = kE2eMaxChunks - (ramp ? 4 : 0);
+  int64_t step = 1024;
+#ifdef SERQ_DIAG
+  if (const char* e = getenv("SERQ_E2E_ROWS")) step = cdiv(atoll(e), 256) * 256;
+#endif
+  if (cdiv(mid, step) > slots) step = cdiv(cdiv(mid, slots), 256) * 256;
+  if (ramp) {
+    plan[chunks++] = 256;
+    plan[chunks++] = 512;
+  }
+  while (mid > 0) {
+    const int64_t c = mid < step ? mid : step;
+    plan[chunks++] = c;
+    mid -= c;
+  }
+  if (ramp) {
+    plan[chunks++] = 512;
+    plan[chunks++] = 256;
+  }
+  if (chunks == 0) plan[chunks++] = 0;
+  plan[chunks - 1] += rem;
+  return chunks;
+}
+
+// H2D of chunk i+1, the device work of chunk i and the D2H of chunk i-1 run concurrently on
+// the two copy engines and the SMs.  `compute(r0, rows)` enqueues on `st` the work turning
+// ws_x rows [r0, r0 + rows) into ws_y rows and returns a status.  Synchronises `st`.
+template <typename F>
+int host_pipeline(serq_linear* h, const void* x_host, int64_t M, void* y_host, cudaStream_t st, F compute) {
+  if (!h->e2e_in) {
+    CK(cudaStreamCreateWithFlags(&h->e2e_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->e2e_out, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : h->e2e_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  int64_t plan[kE2eMaxChunks];
+  const int64_t chunks = e2e_plan(M, plan);
+  cudaEvent_t* ev_in = h->e2e_ev;                       // [chunks] x chunk landed
+  cudaEvent_t* ev_done = h->e2e_ev + kE2eMaxChunks;     // [chunks] y chunk computed
+  cudaEvent_t* ev_out = h->e2e_ev + 2 * kE2eMaxChunks;  // [chunks] y chunk copied out
+  cudaEvent_t ev_start = h->e2e_ev[3 * kE2eMaxChunks];
+  CK(cudaEventRecord(ev_start, st));  // the copies must follow earlier work on the caller's stream
+  CK(cudaStreamWaitEvent(h->e2e_in, ev_start, 0));
+  int64_t start[kE2eMaxChunks];
+  for (int64_t c = 0, r0 = 0; c < chunks; r0 += plan[c], ++c) start[c] = r0;
+  for (int64_t c = 0; c < chunks; ++c) {
+    CK(cudaMemcpyAsync(static_cast<uint8_t*>(h->ws_x) + start[c] * h->K * 2,
+                       static_cast<const uint8_t*>(x_host) + start[c] * h->K * 2, plan[c] * h->K * 2,
+                       cudaMemcpyHostToDevice, h->e2e_in));
+    CK(cudaEventRecord(ev_in[c], h->e2e_in));
+  }
+  int launches = 0;
+  for (int64_t c = 0; c < chunks; ++c) {
+    const int64_t r0 = start[c], mc = plan[c];
+    CK(cudaStreamWaitEvent(st, ev_in[c], 0));
+    const int rc = compute(r0, mc);
+    if (rc) return rc;
+    launches += g_launches;
+    CK(cudaEventRecord(ev_done[c], st));
+    CK(cudaStreamWaitEvent(h->e2e_out, ev_done[c], 0));
+    CK(cudaMemcpyAsync(static_cast<uint8_t*>(y_host) + r0 * h->N * 2, static_cast<uint8_t*>(h->ws_y) + r0 * h->N * 2,
+                       mc * h->N * 2, cudaMemcpyDeviceToHost, h->e2e_out));
+    CK(cudaEventRecord(ev_out[c], h->e2e_out));
+  }
+  g_launches = launches;
+  CK(cudaStreamWaitEvent(st, ev_out[chunks - 1], 0));
+  CK(cudaStreamSynchronize(st));
+  return SERQ_OK;
+}
+
+void free_ws(serq_linear* h) {
+  for (void* p : {h->ws_x, (void*)h->ws_codes, (void*)h->ws_sf, h->ws_y, (void*)h->ws_xs, (void*)h->ws_xsf,
+                  (void*)h->ws_s64, (void*)h->ws_s32, (void*)h->ws_zp})
+    if (p) cudaFree(p);
+  h->ws_x = h->ws_y = nullptr;
+  h->ws_codes = h->ws_sf = h->ws_xs = h->ws_xsf = nullptr;
+  h->ws_s64 = nullptr;
+  h->ws_s32 = nullptr;
+  h->ws_zp = nullptr;
+  h->ws_m = 0;
+}
+
+int xs_kind_of(const serq_linear* h) {
+  if (h->r_mode == SERQ_R_DENSE || h->r_mode == SERQ_R_DENSE_SPLIT) return 1;
+  if (h->r_mode == SERQ_R_INT && !h->contiguous) return 2;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
 int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* y_host, serq_stream_t stream) {
   return serq_forward_mx_host_gather(h, x_host, M, nullptr, y_host, stream);
 }
@@ -1117,18 +1225,15 @@ int serq_forward_mx_host(serq_linear_t* h, const void* x_host, int64_t M, void* 
 int serq_forward_mx_host_gather(serq_linear_t* h, const void* x_host, int64_t M, const int32_t* gather_idx,
                                 void* y_host, serq_stream_t stream) {
   if (!h || h->mode != kModeMX) return fail(SERQ_EINVAL, "handle is not an MX linear");
+  if (!x_host || !y_host) return fail(SERQ_EINVAL, "null host buffer");
   std::lock_guard<std::mutex> lock(h->e2e_mu);
   const bool gather = h->r > 0 && !h->contiguous;
   if (gather && !gather_idx)
     return fail(SERQ_EINVAL, "a non-contiguous salient set needs gather_idx (serq_forward_mx_host_gather)");
   if (M <= 0) return fail(SERQ_EINVAL, "x must be non-empty");
-  cudaStream_t st = S(stream);
   if (M > h->ws_m || (gather && !h->ws_xs)) {
-    for (void* p : {h->ws_x, (void*)h->ws_codes, (void*)h->ws_sf, h->ws_y, (void*)h->ws_xs, (void*)h->ws_xsf})
-      if (p) cudaFree(p);
-    h->ws_x = h->ws_y = nullptr;
-    h->ws_codes = h->ws_sf = h->ws_xs = h->ws_xsf = nullptr;
     const int64_t mm = cdiv(M > h->ws_m ? M : h->ws_m, 128) * 128;
+    free_ws(h);
     CK(cudaMalloc(&h->ws_x, mm * h->K * 2));
     CK(cudaMalloc(&h->ws_codes, mm * h->K / 2));
     CK(cudaMalloc(&h->ws_sf, sf_bytes_of(mm, h->K)));
@@ -1139,129 +1244,67 @@ int serq_forward_mx_host_gather(serq_linear_t* h, const void* x_host, int64_t M,
     }
     h->ws_m = mm;
   }
-  const int64_t kc_pad_r = gather ? kc_pad_of(h->r) : 0;
-  // Chunked over token rows (multiples of 256) so that the H2D copy of chunk
-  // i+1, the quantize + fused linear of chunk i and the D2H copy of chunk i-1
-  // run concurrently on the two copy engines and the SMs.
-  if (!h->e2e_in) {
-    CK(cudaStreamCreateWithFlags(&h->e2e_in, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&h->e2e_out, cudaStreamNonBlocking));
-    for (cudaEvent_t& e : h->e2e_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-  // Chunk plan: small chunks at both ends (the first H2D and the last D2H are not
-  // overlapped with anything), 1024-row chunks in the middle (per-chunk launch /
-  // copy setup costs ~25 us, measured with uniform 256-row chunks).
-  int64_t plan[kE2eMaxChunks];
-  int64_t chunks = 0;
-  {
-    // every chunk starts on a 256-row boundary; the last one absorbs M % 256
-    const int64_t body = (M / 256) * 256, rem = M - body;
-    const bool ramp = body >= 2560;  // 256 + 512 + [>= 1024] + 512 + 256
-    const int64_t ends = ramp ? 1536 : 0;
-    int64_t mid = body - ends;
-    const int64_t slots = kE2eMaxChunks - (ramp ? 4 : 0);
-    int64_t step = 1024;
-#ifdef SERQ_DIAG
-    if (const char* e = getenv("SERQ_E2E_ROWS")) step = cdiv(atoll(e), 256) * 256;
-#endif
-    if (cdiv(mid, step) > slots) step = cdiv(cdiv(mid, slots), 256) * 256;
-    if (ramp) {
-      plan[chunks++] = 256;
-      plan[chunks++] = 512;
-    }
-    while (mid > 0) {
-      const int64_t c = mid < step ? mid : step;
-      plan[chunks++] = c;
-      mid -= c;
-    }
-    if (ramp) {
-      plan[chunks++] = 512;
-      plan[chunks++] = 256;
-    }
-    if (chunks == 0) plan[chunks++] = 0;
-    plan[chunks - 1] += rem;
-#ifdef SERQ_DIAG
-    if (const char* e = getenv("SERQ_E2E_PLAN")) {  // explicit chunk rows, last absorbs the rest
-      int64_t n = 0, used = 0;
-      for (const char* q = e; *q && n < kE2eMaxChunks - 1;) {
-        const int64_t v = atoll(q);
-        if (v <= 0 || used + v >= M) break;
-        plan[n++] = v;
-        used += v;
-        while (*q && *q != ',') ++q;
-        if (*q == ',') ++q;
-      }
-      plan[n++] = M - used;
-      chunks = n;
-    }
-#endif
-  }
-  // diagnostics (SERQ_E2E_TIMING set): per-chunk timeline of the copies and kernels on stderr
-#ifdef SERQ_DIAG
-  static const bool timing = getenv("SERQ_E2E_TIMING") != nullptr;
-#else
-  constexpr bool timing = false;
-#endif
-  cudaEvent_t tev[4 * kE2eMaxChunks + 1];
-  if (timing)
-    for (cudaEvent_t& e : tev) CK(cudaEventCreate(&e));
-  cudaEvent_t* ev_in = h->e2e_ev;                       // [chunks] x chunk landed
-  cudaEvent_t* ev_done = h->e2e_ev + kE2eMaxChunks;     // [chunks] y chunk computed
-  cudaEvent_t* ev_out = h->e2e_ev + 2 * kE2eMaxChunks;  // [chunks] y chunk copied out
-  cudaEvent_t ev_start = h->e2e_ev[3 * kE2eMaxChunks];
-  CK(cudaEventRecord(ev_start, st));  // the copies must follow earlier work on the caller's stream
-  CK(cudaStreamWaitEvent(h->e2e_in, ev_start, 0));
-  const int64_t kc_pad = kc_pad_of(h->K);
-  int64_t start[kE2eMaxChunks];
-  for (int64_t c = 0, r0 = 0; c < chunks; r0 += plan[c], ++c) start[c] = r0;
-  if (timing) CK(cudaEventRecord(tev[4 * kE2eMaxChunks], h->e2e_in));
-  for (int64_t c = 0; c < chunks; ++c) {
-    const int64_t r0 = start[c], mc = plan[c];
-    CK(cudaMemcpyAsync(static_cast<uint8_t*>(h->ws_x) + r0 * h->K * 2, static_cast<const uint8_t*>(x_host) + r0 * h->K * 2,
-                       mc * h->K * 2, cudaMemcpyHostToDevice, h->e2e_in));
-    CK(cudaEventRecord(ev_in[c], h->e2e_in));
-    if (timing) CK(cudaEventRecord(tev[c], h->e2e_in));
-  }
-  const int n0 = g_launches;
-  int launches = 0;
-  for (int64_t c = 0; c < chunks; ++c) {
-    const int64_t r0 = start[c], mc = plan[c];
+  const int64_t kc_pad = kc_pad_of(h->K), kc_pad_r = gather ? kc_pad_of(h->r) : 0;
+  return host_pipeline(h, x_host, M, y_host, S(stream), [&](int64_t r0, int64_t mc) {
+    // chunks start on 256-row boundaries, so their scale-factor tiles start on row-block boundaries
     uint8_t* codes = h->ws_codes + r0 * h->K / 2;
     uint8_t* sf = h->ws_sf + (r0 / 128) * kc_pad * 512;
-    // chunks start on 256-row boundaries, so their scale-factor tiles start on row-block boundaries
     uint8_t* xs = gather ? h->ws_xs + r0 * h->r / 2 : nullptr;
     uint8_t* xsf = gather ? h->ws_xsf + (r0 / 128) * kc_pad_r * 512 : nullptr;
-    CK(cudaStreamWaitEvent(st, ev_in[c], 0));
-    if (timing) CK(cudaEventRecord(tev[kE2eMaxChunks + c], st));
     int rc = serq_act_quant_mx(static_cast<uint8_t*>(h->ws_x) + r0 * h->K * 2, SERQ_BF16, mc, h->K, h->K, codes, sf,
                                gather ? gather_idx : nullptr, gather ? h->r : 0, xs, xsf, stream);
     if (rc) return rc;
-    launches += g_launches;
+    const int n1 = g_launches;
     rc = serq_linear_mx(h, codes, sf, mc, xs, xsf, static_cast<uint8_t*>(h->ws_y) + r0 * h->N * 2, h->N, stream);
-    if (rc) return rc;
-    launches += g_launches;
-    CK(cudaEventRecord(ev_done[c], st));
-    if (timing) CK(cudaEventRecord(tev[2 * kE2eMaxChunks + c], st));
-    CK(cudaStreamWaitEvent(h->e2e_out, ev_done[c], 0));
-    CK(cudaMemcpyAsync(static_cast<uint8_t*>(y_host) + r0 * h->N * 2, static_cast<uint8_t*>(h->ws_y) + r0 * h->N * 2,
-                       mc * h->N * 2, cudaMemcpyDeviceToHost, h->e2e_out));
-    CK(cudaEventRecord(ev_out[c], h->e2e_out));
-    if (timing) CK(cudaEventRecord(tev[3 * kE2eMaxChunks + c], h->e2e_out));
+    g_launches += n1;
+    return rc;
+  });
+}
+
+int serq_forward_int(serq_linear_t* h, const void* x, int dtype, int64_t M, int64_t ldx, int bits, int symmetric,
+                     const int32_t* salient_idx, int8_t* codes, double* scale64, float* scale32, int32_t* zp,
+                     void* xs, void* y, int64_t ldy, serq_stream_t stream) {
+  if (!h || h->mode != kModeI8) return fail(SERQ_EINVAL, "handle is not an INT linear");
+  const int xk = xs_kind_of(h);
+  if (xk && !xs) return fail(SERQ_EINVAL, "this R mode needs the xs buffer (serq_act_quant_int xs_out)");
+  if (xk == 2 && !salient_idx) return fail(SERQ_EINVAL, "a non-contiguous salient set needs salient_idx");
+  if (!symmetric && !zp) return fail(SERQ_EINVAL, "asymmetric quantization needs a zero-point buffer");
+  int rc = serq_act_quant_int(x, dtype, M, h->K, ldx, bits, symmetric, codes, scale64, scale32, symmetric ? nullptr : zp,
+                              xk ? (h->contiguous ? nullptr : salient_idx) : nullptr, xk ? h->r : 0, xs, xk, stream);
+  if (rc) return rc;
+  const int n1 = g_launches;
+  rc = linear_int_impl(h, codes, scale32, symmetric ? nullptr : zp, M, xs, y, ldy, nullptr, nullptr, nullptr, stream);
+  g_launches += n1;
+  return rc;
+}
+
+int serq_forward_int_host(serq_linear_t* h, const void* x_host, int64_t M, int bits, int symmetric,
+                          const int32_t* salient_idx, void* y_host, serq_stream_t stream) {
+  if (!h || h->mode != kModeI8) return fail(SERQ_EINVAL, "handle is not an INT linear");
+  if (!x_host || !y_host) return fail(SERQ_EINVAL, "null host buffer");
+  if (M <= 0) return fail(SERQ_EINVAL, "x must be non-empty");
+  const int xk = xs_kind_of(h);
+  if (xk == 2 && !salient_idx) return fail(SERQ_EINVAL, "a non-contiguous salient set needs salient_idx");
+  std::lock_guard<std::mutex> lock(h->e2e_mu);
+  const int64_t xs_row = xk == 1 ? 2 * int64_t(h->r) : (xk == 2 ? int64_t(h->r) : 0);  // bytes per row
+  if (M > h->ws_m || !h->ws_s64) {
+    const int64_t mm = cdiv(M > h->ws_m ? M : h->ws_m, 128) * 128;
+    free_ws(h);
+    CK(cudaMalloc(&h->ws_x, mm * h->K * 2));
+    CK(cudaMalloc(&h->ws_codes, mm * h->K));
+    CK(cudaMalloc(&h->ws_s64, mm * 8));
+    CK(cudaMalloc(&h->ws_s32, mm * 4));
+    CK(cudaMalloc(&h->ws_zp, mm * 4));
+    CK(cudaMalloc(&h->ws_y, mm * h->N * 2));
+    if (xs_row) CK(cudaMalloc(&h->ws_xs, mm * xs_row));
+    h->ws_m = mm;
   }
-  (void)n0;
-  g_launches = launches;
-  CK(cudaStreamWaitEvent(st, ev_out[chunks - 1], 0));
-  CK(cudaStreamSynchronize(st));
-  if (timing) {
-    for (int64_t c = 0; c < chunks; ++c) {
-      float t[4];
-      for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&t[k], tev[4 * kE2eMaxChunks], tev[k * kE2eMaxChunks + c]);
-      fprintf(stderr, "e2e chunk %lld rows %lld: h2d_end %.1f compute %.1f..%.1f d2h_end %.1f us\n", (long long)c,
-              (long long)plan[c], t[0] * 1e3, t[1] * 1e3, t[2] * 1e3, t[3] * 1e3);
-    }
-    for (cudaEvent_t& e : tev) cudaEventDestroy(e);
-  }
-  return SERQ_OK;
+  return host_pipeline(h, x_host, M, y_host, S(stream), [&](int64_t r0, int64_t mc) {
+    return serq_forward_int(h, static_cast<uint8_t*>(h->ws_x) + r0 * h->K * 2, SERQ_BF16, mc, h->K, bits, symmetric,
+                            salient_idx, reinterpret_cast<int8_t*>(h->ws_codes) + r0 * h->K, h->ws_s64 + r0,
+                            h->ws_s32 + r0, h->ws_zp + r0, xs_row ? h->ws_xs + r0 * xs_row : nullptr,
+                            static_cast<uint8_t*>(h->ws_y) + r0 * h->N * 2, h->N, stream);
+  });
 }
 
 }  // extern "C"

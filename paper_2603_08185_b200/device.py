@@ -163,6 +163,17 @@ def unpack_mx(codes: torch.Tensor, sf: torch.Tensor, rows: int, cols: int) -> tu
     return c, e
 
 
+def _int_activation(M: int, K: int, bits: int, symmetric: bool, xs_kind: int, r: int, dev) -> IntActivation:
+    xs = None
+    if xs_kind == 1:
+        xs = torch.empty((M, r), dtype=torch.bfloat16, device=dev)
+    elif xs_kind == 2:
+        xs = torch.empty((M, r), dtype=torch.int8, device=dev)
+    return IntActivation(torch.empty((M, K), dtype=torch.int8, device=dev), torch.empty(M, dtype=torch.float64, device=dev),
+                         torch.empty(M, dtype=torch.float32, device=dev),
+                         None if symmetric else torch.empty(M, dtype=torch.int32, device=dev), bits, symmetric, xs)
+
+
 def quantize_int(x: torch.Tensor, bits: int, symmetric: bool, salient_idx: torch.Tensor | None = None, r: int = 0,
                  xs_kind: int = 0) -> IntActivation:
     """K1-INT per-token quantizer (quantcore.py:108-137), bit-exact codes/scales/zps.
@@ -418,8 +429,35 @@ class IntLinear:
             c = c - act.zp.float()[:, None]
         return c * act.scale32[:, None]
 
+    def forward(self, x: torch.Tensor, bits: int, symmetric: bool, act: IntActivation | None = None,
+                y: torch.Tensor | None = None) -> torch.Tensor:
+        """Quantize + linear in ONE C-ABI call (serq_forward_int, the int branch of
+        forward_reconstructed, compensate.py:296-316); ``act`` (optional) receives the codes,
+        scales and zero points."""
+        _require_cuda(x, "x")
+        if x.dim() != 2 or x.stride(1) != 1:
+            raise ValidationError("x must be a row-major 2-D tensor")
+        M, K = x.shape
+        if K != self.K:
+            raise ValidationError("x columns must equal main rows")
+        if act is None:
+            act = _int_activation(M, K, bits, symmetric, self.xs_kind(), self.r, x.device)
+        if y is None:
+            y = torch.empty((M, self.N), dtype=torch.bfloat16, device=self.device)
+        _lib.call("serq_forward_int", self._h.ptr, x.data_ptr(), _dtype_id(x), M, x.stride(0), bits, int(symmetric),
+                  _ptr(self.salient_idx), act.codes.data_ptr(), act.scale64.data_ptr(), act.scale32.data_ptr(),
+                  _ptr(act.zp), _ptr(act.xs), y.data_ptr(), y.stride(0), _stream())
+        return y
+
+    def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor, bits: int, symmetric: bool) -> None:
+        """End to end from (pinned) host bf16 memory through the C-ABI (serq_forward_int_host)."""
+        _check_host_io(x_host, y_host, self.K, self.N)
+        with torch.cuda.device(self.device):
+            _lib.call("serq_forward_int_host", self._h.ptr, x_host.data_ptr(), x_host.shape[0], bits, int(symmetric),
+                      _ptr(self.salient_idx), y_host.data_ptr(), _stream())
+
     def __call__(self, x: torch.Tensor, bits: int, symmetric: bool, y=None) -> torch.Tensor:
-        return self.gemm(self.quantize(x, bits, symmetric), y)
+        return self.forward(x, bits, symmetric, None, y)
 
 
 def device_info() -> dict:

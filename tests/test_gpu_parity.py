@@ -613,3 +613,40 @@ def test_mx_decode_gather_parity(D, M, K, N):
         y = lin(_cuda(x, torch.bfloat16)).float().cpu().numpy()
         mx, mean = O.parity_errors(y, O.forward_mx(x, main_t, comp))
         assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+# ---------------------------------------------------------------- INT single-call and host entry points
+
+
+@pytest.mark.parametrize("M,K,N,r,r_mode,bits,sym,gather,group", [
+    (2048, 4096, 1024, 128, "int", 8, False, False, None),   # C3-like, per-channel, integer R
+    (512, 1024, 768, 64, "dense", 4, True, False, None),     # C1-like, symmetric A4, bf16 L
+    (300, 1024, 512, 32, "int", 8, False, True, None),       # non-contiguous salient set, integer R
+    (1000, 1024, 512, 64, "int", 8, False, False, 128),      # group-wise weights
+    (5, 512, 256, 32, "dense", 8, False, True, None),        # small M (1-CTA kernel), gathered dense R
+])
+def test_int_forward_single_call_and_host(D, M, K, N, r, r_mode, bits, sym, gather, group):
+    # serq_forward_int (quantize + linear in one call) == quantize then gemm, bit for bit;
+    # serq_forward_int_host (pinned host in / out, chunked) == the device forward
+    x = _bf16_outlier_x(M, K, seed=M + K)
+    w = np.random.default_rng(N).standard_normal((K, N)) * 0.02
+    idx = np.sort(np.random.default_rng(K).choice(K, r, replace=False)) if gather else np.arange(r)
+    if group:
+        main, comp = O.build_grouped_int(w, idx, group, 4, r_mode=r_mode)
+    else:
+        main, comp = O.build_per_channel_int(w, idx, 4, r_mode=r_mode)
+    kw = dict(r_dense=comp.r_dense) if r_mode == "dense" else dict(r_codes=comp.r_q.codes, r_scales=comp.r_q.scales)
+    lin = D.IntLinear(main.codes, main.scales, 4, salient_idx=idx, group_size=group, **kw)
+    xt = _cuda(x, torch.bfloat16)
+    y1 = lin.forward(xt, bits, sym)
+    assert D.last_launch_count() == 2
+    y2 = lin.gemm(lin.quantize(xt, bits, sym))
+    assert torch.equal(y1, y2)
+    xh = xt.cpu().pin_memory()
+    yh = torch.empty((M, N), dtype=torch.bfloat16).pin_memory()
+    lin.forward_host(xh, yh, bits, sym)
+    assert torch.equal(yh, y1.cpu())
+    cfg = O.IntCfg(bits, sym, "per-row")
+    y_ref, _ = O.forward_int(x, main, comp, cfg, symmetric_act=sym)
+    mx, mean = O.parity_errors(y1.float().cpu().numpy(), y_ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
