@@ -89,6 +89,18 @@ int serq_act_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t l
                        int8_t* codes, double* scale64, float* scale32, int32_t* zp, const int32_t* salient_idx, int r,
                        void* xs_out, int xs_kind, serq_stream_t stream);
 
+/* K-sharded integer activations (row-parallel INT layers): the per-token scale
+ * spans the FULL row (quantcore.py:127-129), so each rank first writes its K-slice's row
+ * range -- range float [2, M]: range[m] = min, range[M + m] = max (exact: bf16 values) --
+ * the ranks all-reduce MIN over range[0:M] and MAX over range[M:2M], and then quantize their
+ * slice with serq_act_quant_int_ext on the global range: codes, scales and zero points equal
+ * serq_act_quant_int of the unsharded row.  bf16 input, K % 8 == 0, K <= 8192. */
+int serq_act_quant_int_range(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, float* range,
+                             serq_stream_t stream);
+int serq_act_quant_int_ext(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, int bits, int symmetric,
+                           const float* range, int8_t* codes, double* scale64, float* scale32, int32_t* zp,
+                           const int32_t* salient_idx, int r, void* xs_out, int xs_kind, serq_stream_t stream);
+
 /* Pack MX artefacts held in DEVICE memory, reference layouts:
  * codes uint8 [N, K] (values 0..15), exps int32 [N, K/32] (main_t of
  * build_serq_rtn_mx, stored transposed), r_codes uint8 [N, r], r_exps int32

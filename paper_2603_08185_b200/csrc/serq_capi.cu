@@ -333,14 +333,40 @@ int serq_act_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ld
   return act_quant_mx_impl(x, dtype, M, K, ldx, codes, sf, gather_idx, r, xs_codes, xs_sf, stream);
 }
 
+static int act_quant_int_impl(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, int bits, int symmetric,
+                              int8_t* codes, double* scale64, float* scale32, int32_t* zp, const int32_t* salient_idx,
+                              int r, void* xs_out, int xs_kind, float* range, int range_mode, serq_stream_t stream);
+
 int serq_act_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, int bits, int symmetric,
                        int8_t* codes, double* scale64, float* scale32, int32_t* zp, const int32_t* salient_idx, int r,
                        void* xs_out, int xs_kind, serq_stream_t stream) {
+  return act_quant_int_impl(x, dtype, M, K, ldx, bits, symmetric, codes, scale64, scale32, zp, salient_idx, r, xs_out,
+                            xs_kind, nullptr, 0, stream);
+}
+
+int serq_act_quant_int_range(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, float* range,
+                             serq_stream_t stream) {
+  if (!range) return fail(SERQ_EINVAL, "range is NULL");
+  return act_quant_int_impl(x, dtype, M, K, ldx, 8, 0, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0,
+                            range, 1, stream);
+}
+
+int serq_act_quant_int_ext(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, int bits, int symmetric,
+                           const float* range, int8_t* codes, double* scale64, float* scale32, int32_t* zp,
+                           const int32_t* salient_idx, int r, void* xs_out, int xs_kind, serq_stream_t stream) {
+  if (!range) return fail(SERQ_EINVAL, "range is NULL");
+  return act_quant_int_impl(x, dtype, M, K, ldx, bits, symmetric, codes, scale64, scale32, zp, salient_idx, r, xs_out,
+                            xs_kind, const_cast<float*>(range), 2, stream);
+}
+
+static int act_quant_int_impl(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, int bits, int symmetric,
+                              int8_t* codes, double* scale64, float* scale32, int32_t* zp, const int32_t* salient_idx,
+                              int r, void* xs_out, int xs_kind, float* range, int range_mode, serq_stream_t stream) {
   g_launches = 0;
   if (M <= 0 || K <= 0) return fail(SERQ_EINVAL, "x must be non-empty");
   if (bits < 2 || bits > 8) return fail(SERQ_EINVAL, "bits must be in [2, 8], got %d", bits);
   if (ldx < K) return fail(SERQ_EINVAL, "ldx < K");
-  if (!symmetric && !zp) return fail(SERQ_EINVAL, "asymmetric quantization needs a zero-point buffer");
+  if (!symmetric && !zp && range_mode != 1) return fail(SERQ_EINVAL, "asymmetric quantization needs a zero-point buffer");
   if (xs_kind && (r <= 0 || r > K || !xs_out)) return fail(SERQ_EINVAL, "salient slice needs 0 < r <= K and xs_out");
   cudaStream_t st = S(stream);
   const dim3 grid(static_cast<unsigned>(M));
@@ -356,7 +382,7 @@ int serq_act_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t l
     const int cpt = int(cdiv(K / 8, tpr));
 #define SERQ_INTQ(P, C)                                                                                         \
   CK(launch_pdl(int_quant_bf16_kernel<P, C, P>, gq, dim3(P), 0, st, xb, int(M), int(K), ldx, bits, symmetric, codes, \
-                scale64, scale32, zp, salient_idx, r, xs_out, xs_kind))
+                scale64, scale32, zp, salient_idx, r, xs_out, xs_kind, range, range_mode))
     if (warp_rows) {
       if (cpt <= 4) SERQ_INTQ(32, 4);
       else if (cpt <= 8) SERQ_INTQ(32, 8);
@@ -372,6 +398,8 @@ int serq_act_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t l
     LAUNCH_CHECK("int_quant_bf16");
     return SERQ_OK;
   }
+  if (range_mode)
+    return fail(SERQ_EINVAL, "K-sharded per-token ranges need bf16 rows (16-B aligned, K %% 8 == 0, K <= 8192)");
   switch (dtype) {
     case SERQ_BF16:
       int_quant_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), M, K, ldx, bits,

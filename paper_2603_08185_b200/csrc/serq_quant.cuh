@@ -854,7 +854,11 @@ __global__ void __launch_bounds__(kBlock) int_quant_bf16_kernel(const __nv_bfloa
                                                              int8_t* __restrict__ codes, double* __restrict__ scale64,
                                                              float* __restrict__ scale32, int32_t* __restrict__ zp_out,
                                                              const int32_t* __restrict__ sidx, int r,
-                                                             void* __restrict__ xs_out, int xs_kind) {
+                                                             void* __restrict__ xs_out, int xs_kind,
+                                                             float* __restrict__ range, int range_mode) {
+  // range_mode 1: write this row's (min, max) to range[row], range[M + row] and stop (a K-shard's
+  // local range); 2: quantize with the row range read from there (the all-reduced MIN / MAX over
+  // the K-shards: the reference's per-token scale spans the full row, quantcore.py:127-129)
   constexpr int kRows = kBlock / kTpr, kWarps = kTpr / 32;
   __shared__ float red_lo[kRows][kWarps], red_hi[kRows][kWarps];
   __shared__ double s_scale[kRows];
@@ -900,6 +904,10 @@ __global__ void __launch_bounds__(kBlock) int_quant_bf16_kernel(const __nv_bfloa
       lo = fminf(lo, red_lo[rl][w]);
       hi = fmaxf(hi, red_hi[rl][w]);
     }
+    if (range_mode == 2) {
+      lo = range[row];
+      hi = range[M + row];
+    }
     const double dlo = lo, dhi = hi;  // exact (bf16 values)
     double sc;
     int zp = 0;
@@ -914,12 +922,17 @@ __global__ void __launch_bounds__(kBlock) int_quant_bf16_kernel(const __nv_bfloa
     s_scale[rl] = sc;
     s_inv32[rl] = float(1.0 / sc);
     s_zp[rl] = zp;
-    scale64[row] = sc;
-    scale32[row] = float(sc);
-    if (zp_out) zp_out[row] = zp;
+    if (range_mode == 1) {
+      range[row] = lo;
+      range[M + row] = hi;
+    } else {
+      scale64[row] = sc;
+      scale32[row] = float(sc);
+      if (zp_out) zp_out[row] = zp;
+    }
   }
   __syncthreads();
-  if (!row_ok) return;
+  if (!row_ok || range_mode == 1) return;
   const double sc = s_scale[rl];
   const int zp = s_zp[rl];
   const float inv32 = s_inv32[rl];

@@ -200,6 +200,36 @@ def quantize_int(x: torch.Tensor, bits: int, symmetric: bool, salient_idx: torch
     return IntActivation(codes, s64, s32, zp, bits, symmetric, xs)
 
 
+def int_token_ranges(x: torch.Tensor) -> torch.Tensor:
+    """Per-token (min, max) of a K-slice of the activations: float32 [2, M] (row 0 min, row 1
+    max; exact for bf16 input) -- the local half of a K-sharded INT quantization."""
+    _require_cuda(x, "x")
+    if x.dim() != 2 or x.stride(1) != 1 or x.dtype != torch.bfloat16:
+        raise ValidationError("x must be a row-major bf16 2-D tensor")
+    M, K = x.shape
+    rng = torch.empty((2, M), dtype=torch.float32, device=x.device)
+    _lib.call("serq_act_quant_int_range", x.data_ptr(), _lib.SERQ_BF16, M, K, x.stride(0), rng.data_ptr(), _stream())
+    return rng
+
+
+def quantize_int_with_range(x: torch.Tensor, rng: torch.Tensor, bits: int, symmetric: bool,
+                            salient_idx: torch.Tensor | None = None, r: int = 0, xs_kind: int = 0) -> IntActivation:
+    """K1-INT on a K-slice with the GLOBAL per-token range ``rng`` ([2, M], all-reduced MIN /
+    MAX over the slices, tp.int_token_range_allreduce): codes / scales / zero points of the
+    unsharded row (quantcore.py:121-137)."""
+    _require_cuda(x, "x")
+    if x.dim() != 2 or x.stride(1) != 1 or x.dtype != torch.bfloat16:
+        raise ValidationError("x must be a row-major bf16 2-D tensor")
+    M, K = x.shape
+    if rng.dtype != torch.float32 or tuple(rng.shape) != (2, M) or not rng.is_contiguous():
+        raise ValidationError("range must be a contiguous float32 [2, M] tensor")
+    act = _int_activation(M, K, bits, symmetric, xs_kind, r, x.device)
+    _lib.call("serq_act_quant_int_ext", x.data_ptr(), _lib.SERQ_BF16, M, K, x.stride(0), bits, int(symmetric),
+              rng.data_ptr(), act.codes.data_ptr(), act.scale64.data_ptr(), act.scale32.data_ptr(), _ptr(act.zp),
+              _ptr(salient_idx), r, _ptr(act.xs), xs_kind, _stream())
+    return act
+
+
 # ---------------------------------------------------------------- weights
 
 

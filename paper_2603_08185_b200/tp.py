@@ -115,6 +115,20 @@ def int_token_range_allreduce(lo, hi, group=None):
     return lo, hi
 
 
+def quantize_int_k_sharded(x_shard, bits: int, symmetric: bool, group=None, salient_idx=None, r: int = 0,
+                           xs_kind: int = 0):
+    """K1-INT for a row-parallel INT layer: this rank's K-slice of the activations quantized
+    with the per-token range of the WHOLE row -- local (min, max) on the device
+    (serq_act_quant_int_range), one [2, M] MIN / MAX all-reduce, then the quantizer on the
+    global range (serq_act_quant_int_ext).  Codes, scales and zero points equal the
+    unsharded quantizer's, so the sharded integer accumulators sum exactly."""
+    from . import device as D
+
+    rng = D.int_token_ranges(x_shard)
+    int_token_range_allreduce(rng[0], rng[1], group)
+    return D.quantize_int_with_range(x_shard, rng, bits, symmetric, salient_idx, r, xs_kind)
+
+
 # ------------------------------------------------------------------ block driver
 
 

@@ -650,3 +650,37 @@ def test_int_forward_single_call_and_host(D, M, K, N, r, r_mode, bits, sym, gath
     y_ref, _ = O.forward_int(x, main, comp, cfg, symmetric_act=sym)
     mx, mean = O.parity_errors(y1.float().cpu().numpy(), y_ref)
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+@pytest.mark.parametrize("bits,sym,world", [(8, False, 2), (4, True, 4), (8, False, 8)])
+def test_int_k_sharded_quantizer_and_accumulators(D, bits, sym, world):
+    # row-parallel INT layer, ranks emulated on one GPU: per-slice ranges, the MIN / MAX
+    # reduction (what tp.int_token_range_allreduce does over NCCL), per-slice quantization on
+    # the global range -> the unsharded codes / scales / zero points, and per-slice integer
+    # accumulators that sum EXACTLY to the single-device ones (int_gemm_reference, mxfmt.py:177-195)
+    M, K, N = 300, 4096, 512
+    x = _bf16_outlier_x(M, K, seed=world + bits)
+    w = np.random.default_rng(world).standard_normal((K, N)) * 0.02
+    main = O.quantize_symmetric(w, O.IntCfg(4, True, K, "row"))
+    xt = _cuda(x, torch.bfloat16)
+    full = D.quantize_int(xt, bits, sym)
+    ks = K // world
+    rngs = [D.int_token_ranges(xt[:, i * ks:(i + 1) * ks].contiguous()) for i in range(world)]
+    g = torch.stack(rngs)
+    glob = torch.stack([g[:, 0].amin(0), g[:, 1].amax(0)]).contiguous()
+    acc_sum = torch.zeros((M, N), dtype=torch.int64, device="cuda")
+    for i in range(world):
+        xs_i = xt[:, i * ks:(i + 1) * ks].contiguous()
+        a = D.quantize_int_with_range(xs_i, glob, bits, sym)
+        assert torch.equal(a.codes, full.codes[:, i * ks:(i + 1) * ks])
+        assert torch.equal(a.scale64, full.scale64)
+        if not sym:
+            assert torch.equal(a.zp, full.zp)
+        lin = D.IntLinear(main.codes[i * ks:(i + 1) * ks], main.scales, 4)
+        acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+        lin.gemm(a, acc_dump=acc)
+        acc_sum += acc.long()
+    cfg = O.IntCfg(bits, sym, "per-row")
+    xq = O.quantize_symmetric(x, cfg) if sym else O.quantize_asymmetric(x, cfg)
+    _, parts = O.int_gemm(xq, main, return_partials=True)
+    assert np.array_equal(acc_sum.cpu().numpy(), parts[0][1])
