@@ -149,6 +149,15 @@ int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t
                   const void* r_data, const double* r_scales, int r, int salient_contiguous, serq_linear_t** out,
                   serq_stream_t stream);
 
+/* serq_pack_int with the weights held as PACKED INT4 in HBM (0.5 B / weight; w_bits <= 4):
+ * the CTA-pair kernel's loader warps widen the nibbles to int8 in shared memory (Blackwell has
+ * no INT4 MMA).  Needs a layout that kernel serves: R permuted-integer (r <= 128), dense
+ * (r <= 64) or none.  Bit-identical results to serq_pack_int's int8 weights; serq_pack_int
+ * remains the default because its TMA feed is faster today (K3). */
+int serq_pack_int4(const int32_t* codes, const double* scales, int64_t K, int64_t N, int w_bits, int r_mode,
+                   const void* r_data, const double* r_scales, int r, int salient_contiguous, serq_linear_t** out,
+                   serq_stream_t stream);
+
 /* Group-wise integer weights (int_gemm_reference row-grouped
  * branch, mxfmt.py:177-195; GPTQ group_size, gptq.py:98-146; _weight_config,
  * pipeline.py:134-137): scales float64 [K/group_size, N] (main.scales of a
@@ -161,6 +170,10 @@ int serq_pack_int_grouped(const int32_t* codes, const double* scales, int64_t gr
 
 int serq_linear_destroy(serq_linear_t* h);
 int serq_linear_info(const serq_linear_t* h, int64_t* N, int64_t* K, int* r, int* mode, int* r_mode);
+/* Bytes of the resident main weights (padding included) and whether they are held as packed
+ * 4-bit codes (MXFP4 always; INT when the handle is served by the CTA-pair kernel, which
+ * widens packed INT4 in the SM -- 8-bit codes and the other INT layouts keep int8). */
+int serq_linear_weight_bytes(const serq_linear_t* h, int64_t* main_bytes, int* packed_int4);
 
 /* K2: Y[M, N] (bf16, row stride ldy) = Xq.Wq + Xs,q.R in one kernel.  a_codes /
  * a_sf from serq_act_quant_mx; xs_codes / xs_sf only for a non-contiguous

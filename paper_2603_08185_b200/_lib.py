@@ -41,9 +41,11 @@ SIGNATURES = {
     "serq_rmsnorm_quant_mx_gather": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, ctypes.c_double, _P, _I, _P, _P, _P, _P,
                                           _P]),
     "serq_pack_int": (_I, [_P, _P, _I64, _I64, _I, _I, _P, _P, _I, _I, _P, _P]),
+    "serq_pack_int4": (_I, [_P, _P, _I64, _I64, _I, _I, _P, _P, _I, _I, _P, _P]),
     "serq_pack_int_grouped": (_I, [_P, _P, _I64, _I64, _I64, _I, _I, _P, _P, _I, _I, _P, _P]),
     "serq_linear_destroy": (_I, [_P]),
     "serq_linear_info": (_I, [_P, _P, _P, _P, _P, _P]),
+    "serq_linear_weight_bytes": (_I, [_P, _P, _P]),
     "serq_linear_mx": (_I, [_P, _P, _P, _I64, _P, _P, _P, _I64, _P]),
     "serq_linear_int": (_I, [_P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P]),
     "serq_linear_int_addend": (_I, [_P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P]),

@@ -186,6 +186,8 @@ struct serq_linear {
   CUtensorMap map_r32, map_sfr4;                     // pair3 kernel: R as 32-B swizzled rows, 512-B SF boxes
   bool has_r32 = false;
   CUtensorMap map_r_pair;                            // INT pair kernel maps (R with 128-row boxes)
+  bool has_w4 = false;                               // INT: weights packed INT4, tiled [N/128][K/128][128][64 B]
+  int64_t w_bytes = 0;                               // bytes of the resident main weights
   CUtensorMap map_w8;                                // INT pair kernel, direct int8 weights: 128 B x 128-row boxes
   CUtensorMap map_w8_64, map_r_pair64;               // the same with 64-row boxes (128-column tiles)
   // INT, group-wise weight scales along K (serq_pack_int_grouped)
@@ -569,9 +571,32 @@ int serq_mx_container_decode(const uint8_t* body, int64_t rows, int64_t cols, ui
   return SERQ_OK;
 }
 
+static int pack_int_impl(const int32_t* codes, const double* scales, int64_t K, int64_t N, int w_bits, int r_mode,
+                         const void* r_data, const double* r_scales, int r, int salient_contiguous, bool allow_w4,
+                         serq_linear_t** out, serq_stream_t stream);
+
 int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t N, int w_bits, int r_mode,
                   const void* r_data, const double* r_scales, int r, int salient_contiguous, serq_linear_t** out,
                   serq_stream_t stream) {
+  return pack_int_impl(codes, scales, K, N, w_bits, r_mode, r_data, r_scales, r, salient_contiguous, false, out,
+                       stream);
+}
+
+int serq_pack_int4(const int32_t* codes, const double* scales, int64_t K, int64_t N, int w_bits, int r_mode,
+                   const void* r_data, const double* r_scales, int r, int salient_contiguous, serq_linear_t** out,
+                   serq_stream_t stream) {
+  if (w_bits > 4) return fail(SERQ_EINVAL, "packed INT4 weights need w_bits <= 4 (got %d)", w_bits);
+  const int rr = r_mode == SERQ_R_NONE ? 0 : r;
+  if ((r_mode == SERQ_R_INT && !salient_contiguous) || rr > 128 || (r_mode == SERQ_R_DENSE && rr > 64))
+    return fail(SERQ_EINVAL,
+                "packed INT4 weights are served by the CTA-pair kernel: R permuted-integer (r <= 128), dense "
+                "(r <= 64) or none");
+  return pack_int_impl(codes, scales, K, N, w_bits, r_mode, r_data, r_scales, r, salient_contiguous, true, out, stream);
+}
+
+static int pack_int_impl(const int32_t* codes, const double* scales, int64_t K, int64_t N, int w_bits, int r_mode,
+                         const void* r_data, const double* r_scales, int r, int salient_contiguous, bool allow_w4,
+                         serq_linear_t** out, serq_stream_t stream) {
   g_launches = 0;
   if (!out) return fail(SERQ_EINVAL, "out is NULL");
   *out = nullptr;
@@ -597,17 +622,36 @@ int serq_pack_int(const int32_t* codes, const double* scales, int64_t K, int64_t
     free_handle(h);
     return code;
   };
-  if (cudaMalloc(&h->w, N * K) != cudaSuccess || cudaMalloc(&h->sw, N * 4) != cudaSuccess ||
-      cudaMalloc(&h->colsum, N * 4) != cudaSuccess)
-    return bail(fail(SERQ_ECUDA, "cudaMalloc failed for INT weights"));
-  transpose_codes_kernel<<<dim3(unsigned(cdiv(N, 32)), unsigned(cdiv(K, 32))), dim3(32, 8), 0, st>>>(
-      codes, K, N, static_cast<int8_t*>(h->w));
+  if (cudaMalloc(&h->sw, N * 4) != cudaSuccess || cudaMalloc(&h->colsum, N * 4) != cudaSuccess)
+    return bail(fail(SERQ_ECUDA, "cudaMalloc failed for INT weight scales"));
   colsum_kernel<<<unsigned(cdiv(N, 256)), 256, 0, st>>>(codes, K, N, scales, h->colsum, h->sw);
-  if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_int launch failed"));
-  int rc = make_map(&h->map_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, kBN);
-  if (!rc) rc = make_map(&h->map_w8, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, 128);
-  if (!rc) rc = make_map(&h->map_w8_64, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, 64);
-  if (rc) return bail(rc);
+  // weights in HBM: packed INT4 (0.5 B / weight, serq_pack_int4: the CTA-pair kernel widens them
+  // in the SM) or int8 [N, K] (serq_pack_int, the faster feed today: TMA straight into the
+  // operand).  Never both copies.
+  const bool pair_cfg = (r_mode != SERQ_R_INT || salient_contiguous) && h->r <= 128 &&
+                        (r_mode != SERQ_R_DENSE || h->r <= 64);
+  h->has_w4 = allow_w4 && w_bits <= 4 && pair_cfg;
+  int rc = SERQ_OK;
+  if (h->has_w4) {
+    const int ksteps = int(cdiv(K, 128));
+    const int64_t bytes = cdiv(N, 128) * ksteps * 128 * 64;
+    if (cudaMalloc(&h->w, bytes) != cudaSuccess) return bail(fail(SERQ_ECUDA, "cudaMalloc failed for INT4 weights"));
+    if (cudaMemsetAsync(h->w, 0, bytes, st) != cudaSuccess) return bail(fail(SERQ_ECUDA, "memset"));
+    pack_int4_tiled_kernel<<<dim3(unsigned(cdiv(N, 256)), unsigned(ksteps * 64)), 256, 0, st>>>(
+        codes, K, N, ksteps, static_cast<uint8_t*>(h->w));
+    if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_int4 launch failed"));
+    h->w_bytes = bytes;
+  } else {
+    if (cudaMalloc(&h->w, N * K) != cudaSuccess) return bail(fail(SERQ_ECUDA, "cudaMalloc failed for INT weights"));
+    transpose_codes_kernel<<<dim3(unsigned(cdiv(N, 32)), unsigned(cdiv(K, 32))), dim3(32, 8), 0, st>>>(
+        codes, K, N, static_cast<int8_t*>(h->w));
+    if (cudaGetLastError() != cudaSuccess) return bail(fail(SERQ_ECUDA, "pack_int launch failed"));
+    rc = make_map(&h->map_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, kBN);
+    if (!rc) rc = make_map(&h->map_w8, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, 128);
+    if (!rc) rc = make_map(&h->map_w8_64, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->w, K, N, K, 128, 64);
+    if (rc) return bail(rc);
+    h->w_bytes = N * K;
+  }
   if (r_mode == SERQ_R_DENSE) {
     if (cudaMalloc(&h->rbuf, N * r * 2) != cudaSuccess) return bail(fail(SERQ_ECUDA, "cudaMalloc R"));
     dense_r_kernel<<<unsigned(cdiv(N * r, 256)), 256, 0, st>>>(static_cast<const double*>(r_data), r, N,
@@ -655,8 +699,8 @@ int serq_pack_int_grouped(const int32_t* codes, const double* scales, int64_t gr
   // scales go unused
   serq_linear_t* h = nullptr;
   const bool split = r_mode == SERQ_R_DENSE_SPLIT;
-  int rc = serq_pack_int(codes, scales, K, N, w_bits, split ? SERQ_R_NONE : r_mode, split ? nullptr : r_data,
-                         r_scales, split ? 0 : r, salient_contiguous, &h, stream);
+  int rc = pack_int_impl(codes, scales, K, N, w_bits, split ? SERQ_R_NONE : r_mode, split ? nullptr : r_data,
+                         r_scales, split ? 0 : r, salient_contiguous, false, &h, stream);
   if (rc) return rc;
   h->use_i8g = true;
   if (split) {
@@ -698,6 +742,13 @@ int serq_pack_int_grouped(const int32_t* codes, const double* scales, int64_t gr
 
 int serq_linear_destroy(serq_linear_t* h) {
   if (h) free_handle(h);
+  return SERQ_OK;
+}
+
+int serq_linear_weight_bytes(const serq_linear_t* h, int64_t* main_bytes, int* packed_int4) {
+  if (!h) return fail(SERQ_EINVAL, "NULL handle");
+  if (main_bytes) *main_bytes = h->mode == kModeI8 ? h->w_bytes : cdiv(h->N, 128) * h->w_ksteps * 128 * 128;
+  if (packed_int4) *packed_int4 = h->mode == kModeI8 ? (h->has_w4 ? 1 : 0) : 1;
   return SERQ_OK;
 }
 
@@ -1037,11 +1088,15 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     return SERQ_OK;
   }
   // CTA-pair kernel: int8 weights TMA'd straight into the operand
-  const bool pair_ok = M > 128 && (h->r_mode != SERQ_R_INT || h->contiguous) && h->r <= 128 &&
-                       (h->r_mode != SERQ_R_DENSE || h->r <= 64) && !SERQ_DBG(g_debug_flags, 65536);
+  // W4 handles always take the CTA-pair kernel (it is the one that widens packed INT4); int8
+  // handles above 128 rows when their R layout allows it
+  const bool pair_ok = h->has_w4 || (M > 128 && (h->r_mode != SERQ_R_INT || h->contiguous) && h->r <= 128 &&
+                                     (h->r_mode != SERQ_R_DENSE || h->r <= 64) && !SERQ_DBG(g_debug_flags, 65536));
   if (pair_ok) {
-    CK(set_smem_attr(serq_i8_pair_kernel<256, kI8Epi>, I8Cfg<kI8Epi>::kSmem));
-    CK(set_smem_attr(serq_i8_pair_kernel<128, kI8Epi>, I8Cfg<kI8Epi>::kSmem));
+    CK(set_smem_attr(serq_i8_pair_kernel<256, kI8Epi, false>, I8Cfg<kI8Epi>::kSmem));
+    CK(set_smem_attr(serq_i8_pair_kernel<128, kI8Epi, false>, I8Cfg<kI8Epi>::kSmem));
+    CK(set_smem_attr(serq_i8_pair_kernel<256, kI8Epi, true>, I8Cfg<kI8Epi>::kSmem));
+    CK(set_smem_attr(serq_i8_pair_kernel<128, kI8Epi, true>, I8Cfg<kI8Epi>::kSmem));
     I8Maps im;
     int rc = make_map(&im.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K, M, h->K, 128, 128);
     if (!rc)
@@ -1052,7 +1107,7 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     if (h->r_mode != SERQ_R_DENSE) im.xs = im.a;
     // few 256x256 tiles (C1: 2 x 16 on 74 pairs): 128-column tiles put twice as many pairs to work
     const bool narrow = cdiv(M, 256) * cdiv(h->N, 256) * 2 <= sm_count() / 2 && !SERQ_DBG(g_debug_flags, 1 << 27);
-    im.bp = narrow ? h->map_w8_64 : h->map_w8;
+    im.bp = h->has_w4 ? im.a : (narrow ? h->map_w8_64 : h->map_w8);  // (W4: no weight tensor map)
     im.r = h->r_mode != SERQ_R_NONE ? (narrow ? h->map_r_pair64 : h->map_r_pair) : im.bp;
     GemmParams p{};
     p.dbg = g_debug_flags;
@@ -1073,17 +1128,25 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     p.addend = addend;
     p.accr_dump = accr_dump;
     p.dbg_ts = g_debug_ts;
+    p.w4 = h->has_w4 ? static_cast<const uint8_t*>(h->w) : nullptr;
     const int64_t tiles = cdiv(M, 256) * cdiv(h->N, narrow ? 128 : kBN);
     const int64_t max_pairs = sm_count() / 2;
     const dim3 grid(unsigned(2 * (tiles < max_pairs ? tiles : max_pairs)));
     // launched with programmatic dependent launch: the prologue and the first weight stages
     // overlap the activation quantizer's tail
     using Cfg = I8Cfg<kI8Epi>;
-    if (narrow) {
-      CK(launch_pdl(serq_i8_pair_kernel<128, kI8Epi>, grid, dim3(Cfg::kThreads), Cfg::kSmem, S(stream), im, p));
+    const dim3 blk(Cfg::kThreads);
+    if (h->has_w4 && narrow) {
+      CK(launch_pdl(serq_i8_pair_kernel<128, kI8Epi, true>, grid, blk, Cfg::kSmem, S(stream), im, p));
+      LAUNCH_CHECK("serq_i8_pair_kernel<128,w4>");
+    } else if (h->has_w4) {
+      CK(launch_pdl(serq_i8_pair_kernel<256, kI8Epi, true>, grid, blk, Cfg::kSmem, S(stream), im, p));
+      LAUNCH_CHECK("serq_i8_pair_kernel<256,w4>");
+    } else if (narrow) {
+      CK(launch_pdl(serq_i8_pair_kernel<128, kI8Epi, false>, grid, blk, Cfg::kSmem, S(stream), im, p));
       LAUNCH_CHECK("serq_i8_pair_kernel<128>");
     } else {
-      CK(launch_pdl(serq_i8_pair_kernel<256, kI8Epi>, grid, dim3(Cfg::kThreads), Cfg::kSmem, S(stream), im, p));
+      CK(launch_pdl(serq_i8_pair_kernel<256, kI8Epi, false>, grid, blk, Cfg::kSmem, S(stream), im, p));
       LAUNCH_CHECK("serq_i8_pair_kernel<256>");
     }
     return SERQ_OK;

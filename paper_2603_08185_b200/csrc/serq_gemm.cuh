@@ -72,6 +72,7 @@ struct GemmParams {
   int32_t* accr_dump;    // debug: exact R accumulators
   long long* dbg_ts;     // diagnostics: per-iteration clock64 stamps of the MMA warp (CTA 0), or nullptr
   int narrow_from;       // pair3: tiles >= narrow_from run as two 256 x 128 tiles (>= n_tiles: none)
+  const uint8_t* w4;     // INT CTA-pair kernel, W4 weights: packed int4 tiled [N/128][K/128][128][64 B]
   int group_m;           // tile order: 0 = M fastest over all tiles; g > 0 = groups of g M-tiles
   int dbg;               // SERQ_DIAG builds only (diagnostic switches); always 0 in the product
 };

@@ -95,9 +95,25 @@ __device__ __forceinline__ void mbar_wait_bo(uint64_t* bar, uint32_t parity, boo
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
+// 8 packed two's-complement nibbles -> 8 int8.  Pack-time order (pack_int4_tiled_kernel): byte j
+// of the word holds elements j (low nibble) and j + 4 (high nibble), so the low nibbles widen to
+// elements 0..3 and the high nibbles to 4..7 with no byte shuffle.  Per byte, with b = n ^ 8
+// (the nibble biased to [0, 15]): ((b + 0x78) ^ 0x80) = the sign-extended nibble, and b + 0x78
+// <= 0x87 never carries into the next byte: 3 integer ops per 4 codes.
+__device__ __forceinline__ uint2 widen_int4x8(uint32_t w) {
+  const uint32_t lo = (((w & 0x0F0F0F0Fu) ^ 0x08080808u) + 0x78787878u) ^ 0x80808080u;
+  const uint32_t hi = ((((w >> 4) & 0x0F0F0F0Fu) ^ 0x08080808u) + 0x78787878u) ^ 0x80808080u;
+  return make_uint2(lo, hi);
+}
+constexpr int kI8LoadWarps = 2;  // W4 weights: warps 2..3 widen packed INT4 into the operand
 // kN: output columns per CTA-pair tile (256, or 128 for small problems so twice as many
 // pairs get a tile; each CTA then stages 64 weight rows)
-template <int kN = 256, int kE = 2>
+// kW4: the weights stay PACKED INT4 in HBM (0.5 B / weight, pre-tiled [N/128][K/128][128 rows x
+// 64 B]); two loader warps per CTA read them with plain 8-byte global loads (three K-steps ahead
+// in registers), widen 8 codes per word (LOP3 / VSUB4 / PRMT) and store the int8 operand straight
+// into the 128B-swizzled stage -- the same shared-memory traffic as the TMA'd int8 feed (the
+// staging copy of an earlier variant made the SM shared-memory bound).  Blackwell has no INT4 MMA.
+template <int kN = 256, int kE = 2, bool kW4 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE>::kThreads, 1)
     serq_i8_pair_kernel(const __grid_constant__ I8Maps maps, const GemmParams p) {
   static_assert(kN == 256 || kN == 128, "256- or 128-column tiles");
@@ -145,7 +161,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE>::kThreads,
       tma_prefetch(&maps.xs);
     }
     for (int s = 0; s < kI8Stages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kW4 ? 1 + 2 * kI8LoadWarps : 1);  // W4: + the loader warps of both CTAs
       mbar_init(&empty[s], 1);
     }
     mbar_init(side_empty, 1);
@@ -168,7 +184,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE>::kThreads,
       const uint32_t sb = smem_u32(smem), sside = smem_u32(side);
       // programmatic dependent launch: the first tile's weight stages do not depend on the
       // previous kernel (the activation quantizer) -- stream them before griddepcontrol.wait
-      const int pre = my_tiles > 0 ? (ks < kI8Stages ? ks : kI8Stages) : 0;
+      const int pre = (!kW4 && my_tiles > 0) ? (ks < kI8Stages ? ks : kI8Stages) : 0;
+      constexpr uint32_t kBTma = kW4 ? 0u : kBBytes;  // W4: B is written by the loader warps
       if (my_tiles > 0) {
         const int n_half0 = (cluster_id / tiles_m) * kN + int(rank) * kBHalf;
         for (int kk = 0; kk < pre; ++kk) {
@@ -195,8 +212,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE>::kThreads,
           const uint32_t fbar = map_rank(smem_u32(&full[s]), 0);
           const uint32_t st = sb + s * kI8Stage;
           if (leader && !preloaded)
-            mbar_expect_tx(&full[s], 2u * (kI8A + kBBytes + (with_side ? (dense ? 16384 + kRBytes : kRBytes) : 0)));
-          if (!preloaded)
+            mbar_expect_tx(&full[s], 2u * (kI8A + kBTma + (with_side ? (dense ? 16384 + kRBytes : kRBytes) : 0)));
+          if (!preloaded && !kW4)
             tma_load_2d_pair(st + kI8A, &maps.bp, fbar, kk * 128, n_half, kEvictNormal);  // int8 [N, K] rows
           tma_load_2d_pair(st, &maps.a, fbar, kk * 128, m_own, kEvictNormal);
           if (with_side) {
@@ -270,6 +287,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE>::kThreads,
 #ifdef SERQ_DIAG_TS
         if (p.dbg_ts && lane_id() == 0 && i < 8) p.dbg_ts[512 + (blockIdx.x >> 1) * 64 + i * 8 + 2] = globaltimer();
 #endif
+      }
+    }
+  } else if (kW4 && warp < 2 + kI8LoadWarps) {
+    // ------------------------------------------------------------ W4 loaders (both CTAs)
+    // thread lt covers chunk c = lt % 8 (16 int8 = 8 packed bytes) of rows lt / 8 + 8 j: a warp
+    // reads 4 rows x 64 B per load (coalesced) and stores 4 rows x 128 B (conflict-free)
+    constexpr int kJ = kBHalf / 8;
+    const int lt = int(threadIdx.x) - 64;
+    const int c = lt & 7, r0 = lt >> 3;
+    const uint32_t full_leader = map_rank(smem_u32(&full[0]), 0);
+    const uint8_t* w4 = p.w4;
+    const int total = my_tiles * ks;
+    auto block_of = [&](int g) {  // this CTA's contiguous kBHalf x 64 B block of K-step g
+      const int i = g / ks, kk = g - i * ks;
+      const int tile = cluster_id + i * n_clusters;
+      const int n_half = (tile / tiles_m) * kN + int(rank) * kBHalf;
+      return w4 + (size_t((n_half >> 7) * ks + kk) * 128 + (n_half & 127)) * 64;
+    };
+    auto src_of = [&](int g) { return block_of(g) + r0 * 64 + c * 8; };
+    // the register loads run 2 K-steps ahead; an L2 prefetch of the whole block kPf steps ahead
+    // keeps them L2 hits (HBM latency is far longer than the ~0.4 us per step)
+    constexpr int kPf = 8;
+    if (lt == 0)
+      for (int g = 0; g < kPf && g < total; ++g)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(block_of(g)), "r"(uint32_t(kBHalf * 64)) : "memory");
+    auto load = [&](uint2 (&b)[kJ], int g) {
+      if (g < total) {
+        const uint8_t* src = src_of(g);
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) b[j] = __ldg(reinterpret_cast<const uint2*>(src + j * 8 * 64));
+      }
+    };
+    uint2 b0[kJ], b1[kJ], b2[kJ], b3[kJ];
+    load(b0, 0);
+    load(b1, 1);
+    load(b2, 2);
+    for (int g = 0; g < total; ++g) {
+      if (lt == 0 && g + kPf < total)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(block_of(g + kPf)), "r"(uint32_t(kBHalf * 64))
+                     : "memory");
+      load(b3, g + 3);  // four K-steps in flight per thread
+      const int s = g % kI8Stages;
+      mbar_wait(&empty[s], ((g / kI8Stages) & 1) ^ 1);
+      const uint32_t dst = smem_u32(smem + s * kI8Stage + kI8A);
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const int row = r0 + 8 * j;
+        const uint2 e0 = widen_int4x8(b0[j].x), e1 = widen_int4x8(b0[j].y);  // elements 0..7, 8..15
+        st_shared_v4(dst + row * 128 + ((uint32_t(c) ^ uint32_t(row & 7)) * 16), e0.x, e0.y, e1.x, e1.y);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive_remote(full_leader + uint32_t(s) * 8u);
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        b0[j] = b1[j];
+        b1[j] = b2[j];
+        b2[j] = b3[j];
       }
     }
   } else if (warp >= 4) {

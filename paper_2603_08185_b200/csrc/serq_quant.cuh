@@ -1056,6 +1056,26 @@ __global__ void transpose_codes_kernel(const int32_t* __restrict__ src, int64_t 
   }
 }
 
+// reference INT codes int32 [K, N] (two's complement, |code| <= 8) -> packed nibbles tiled
+// [N/128][K/128][128 rows][64 B]: the W4 CTA-pair kernel's loader warps read one contiguous block
+// per 128-K step.  Within a row's 64 B, 8 bytes hold one 16-element chunk; byte j of each 4-byte
+// word holds elements j (low nibble) and j + 4 (high nibble) of that word's 8 elements, the order
+// widen_int4x8 expands without byte shuffles.  One thread per output byte.
+__global__ void pack_int4_tiled_kernel(const int32_t* __restrict__ src, int64_t K, int64_t N, int ksteps,
+                                       uint8_t* __restrict__ dst) {
+  const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t bidx = blockIdx.y;  // byte of the row's packed K: step = bidx / 64, b = bidx % 64
+  if (n >= N) return;
+  const int64_t step = bidx >> 6;
+  const int b = int(bidx & 63);
+  const int e_lo = (b >> 3) * 16 + ((b >> 2) & 1) * 8 + (b & 3);
+  const int64_t k_lo = step * 128 + e_lo, k_hi = k_lo + 4;
+  const int32_t lo = k_lo < K ? src[k_lo * N + n] : 0;
+  const int32_t hi = k_hi < K ? src[k_hi * N + n] : 0;
+  const size_t off = ((size_t(n >> 7) * ksteps + size_t(step)) * 128 + size_t(n & 127)) * 64 + size_t(b);
+  dst[off] = uint8_t((lo & 0xF) | ((hi & 0xF) << 4));
+}
+
 // colsum[n] = sum_k codes[k, n]; scale f64 -> f32 copy
 __global__ void colsum_kernel(const int32_t* __restrict__ src, int64_t K, int64_t N, const double* __restrict__ s64,
                               int32_t* __restrict__ colsum, float* __restrict__ s32) {

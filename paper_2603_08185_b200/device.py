@@ -376,10 +376,15 @@ class IntLinear:
     output column (r_q, row groups of size r)."""
 
     def __init__(self, codes, scales, bits=4, r_dense=None, r_codes=None, r_scales=None, salient_idx=None,
-                 device="cuda", group_size=None, r_split=False):
+                 device="cuda", group_size=None, r_split=False, weight_format="int8"):
         """``r_split``: consume the dense R as bf16 hi + lo planes (relative error 2^-17) instead
         of one bf16 plane -- for R matrices that carry a large share of the output (a GPTQ-swapped
-        R holds the salient rows themselves); served by the group-wise kernel (K <= 8192)."""
+        R holds the salient rows themselves); served by the group-wise kernel (K <= 8192).
+        ``weight_format``: "int8" (weights int8 in HBM, TMA'd into the operand; the default) or
+        "int4" (packed INT4 in HBM, 0.5 B / weight, widened in the SM; serq_pack_int4)."""
+        if weight_format not in ("int8", "int4"):
+            raise ValidationError(f"weight_format must be 'int8' or 'int4', got {weight_format!r}")
+        self.weight_format = weight_format
         device = torch.device(device)
         if device.type != "cuda":
             raise ValidationError("IntLinear lives on a CUDA device")
@@ -418,11 +423,24 @@ class IntLinear:
         self.contiguous = idx is None or np.array_equal(idx, np.arange(self.r))
         self.salient_idx = None if idx is None or self.contiguous else torch.from_numpy(idx.astype(np.int32)).to(device)
         h = ctypes.c_void_p()
-        _lib.call("serq_pack_int_grouped", codes.data_ptr(), scales.data_ptr(), self.group_size, self.K, self.N, bits,
-                  self.r_mode, _ptr(rdata), _ptr(rs), self.r, int(self.contiguous), ctypes.byref(h), _stream())
+        if self.weight_format == "int4":
+            if self.group_size != self.K or self.r_mode == _lib.SERQ_R_DENSE_SPLIT:
+                raise ValidationError("packed INT4 weights need per-output-channel scales and a plain R")
+            _lib.call("serq_pack_int4", codes.data_ptr(), scales.data_ptr(), self.K, self.N, bits, self.r_mode,
+                      _ptr(rdata), _ptr(rs), self.r, int(self.contiguous), ctypes.byref(h), _stream())
+        else:
+            _lib.call("serq_pack_int_grouped", codes.data_ptr(), scales.data_ptr(), self.group_size, self.K, self.N,
+                      bits, self.r_mode, _ptr(rdata), _ptr(rs), self.r, int(self.contiguous), ctypes.byref(h),
+                      _stream())
         torch.cuda.current_stream().synchronize()
         self._h = _Handle(h)
         self.device = device
+
+    def weight_bytes(self) -> tuple[int, bool]:
+        """(bytes of the resident main weights, held as packed INT4?)"""
+        b, w4 = ctypes.c_int64(), ctypes.c_int()
+        _lib.call("serq_linear_weight_bytes", self._h.ptr, ctypes.byref(b), ctypes.byref(w4))
+        return b.value, bool(w4.value)
 
     def xs_kind(self) -> int:
         if self.r_mode in (_lib.SERQ_R_DENSE, _lib.SERQ_R_DENSE_SPLIT):

@@ -109,9 +109,10 @@ def _int_case(cfg_name, group=None):
     return wl, meta, main, comp
 
 
-def _int_lin(D, main, comp, r, r_mode, group=None):
+def _int_lin(D, main, comp, r, r_mode, group=None, weight_format="int8"):
     kw = dict(r_dense=comp.r_dense) if r_mode == "dense" else dict(r_codes=comp.r_q.codes, r_scales=comp.r_q.scales)
-    return D.IntLinear(main.codes, main.scales, 4, salient_idx=np.arange(r), group_size=group, **kw)
+    return D.IntLinear(main.codes, main.scales, 4, salient_idx=np.arange(r), group_size=group,
+                       weight_format=weight_format, **kw)
 
 
 def test_c1_int4_sym_full_accumulators(D):
@@ -137,7 +138,8 @@ def test_c1_int4_sym_full_accumulators(D):
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
 
 
-def test_c3_w4a8_per_channel_full_accumulators(D):
+@pytest.mark.parametrize("weight_format", ["int8", "int4"])
+def test_c3_w4a8_per_channel_full_accumulators(D, weight_format):
     """BASELINE C3: W4A8 (INT8 asymmetric per-token activations, INT4 per-channel weights),
     M = 2048, K = 4096, N = 11008, integer R at r = 128: 344 tiles on 74 CTA pairs -> the
     256-column instantiation with up to 5 tiles per cluster (accumulator reuse, tmem_empty /
@@ -147,13 +149,16 @@ def test_c3_w4a8_per_channel_full_accumulators(D):
     M, K = wl.x.shape
     N = wl.w.shape[1]
     r = wl.r
-    lin = _int_lin(D, main, comp, r, "int")
+    lin = _int_lin(D, main, comp, r, "int", weight_format=weight_format)
     act = lin.quantize(_cuda(wl.x, torch.bfloat16), meta["bits"], meta["symmetric"])
     acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
     accr = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    w4 = weight_format == "int4"
     for _ in range(2):  # twice: a second launch must not depend on the first (no stale state)
         y = lin.gemm(act, acc_dump=acc, accr_dump=accr).float().cpu().numpy()
-        assert D.last_kernel() == "serq_i8_pair_kernel<256>"
+        assert D.last_kernel() == ("serq_i8_pair_kernel<256,w4>" if w4 else "serq_i8_pair_kernel<256>")
+    # resident main weights: packed INT4 (N padded to 128-row blocks) or int8
+    assert lin.weight_bytes() == ((-(-N // 128) * 128 * K // 2, True) if w4 else (N * K, False))
     xq = O.quantize_asymmetric(wl.x, O.IntCfg(meta["bits"], False, "per-row"))
     assert np.array_equal(act.codes.cpu().numpy().view(np.uint8).astype(np.int32), xq.codes)
     assert np.array_equal(act.zp.cpu().numpy(), xq.zero_points[:, 0])

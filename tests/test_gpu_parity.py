@@ -684,3 +684,40 @@ def test_int_k_sharded_quantizer_and_accumulators(D, bits, sym, world):
     xq = O.quantize_symmetric(x, cfg) if sym else O.quantize_asymmetric(x, cfg)
     _, parts = O.int_gemm(xq, main, return_partials=True)
     assert np.array_equal(acc_sum.cpu().numpy(), parts[0][1])
+
+
+@pytest.mark.parametrize("M,N,w_bits,r_mode,fmt", [(600, 1024, 8, "int", "int8"),   # 8-bit weights, int8 feed
+                                                   (64, 520, 4, "int", "int4"),    # W4 handle at small M
+                                                   (1000, 4104, 4, "dense", "int4"),  # W4, ragged N, multi-tile
+                                                   (1000, 4104, 4, "dense", "int8")])
+def test_int_weight_storage_paths(D, M, N, w_bits, r_mode, fmt):
+    # W4 (packed INT4 widened in the SM) and int8 weight feeds of the CTA-pair kernel: exact
+    # accumulators against the oracle and the resident weight bytes
+    K, r = 2048, 64
+    x = _bf16_outlier_x(M, K, seed=M + w_bits)
+    w = np.random.default_rng(N + w_bits).standard_normal((K, N)) * 0.02
+    main = O.quantize_symmetric(w, O.IntCfg(w_bits, True, K, "row"))
+    resid = w[:r] - O.dequantize(main)[:r]
+    if r_mode == "dense":
+        comp = O.Comp(r, np.arange(r), r_dense=O.bf16_round(resid))
+        kw = dict(r_dense=comp.r_dense)
+    else:
+        comp = O.Comp(r, np.arange(r), r_q=O.quantize_symmetric(resid, O.IntCfg(4, True, r, "row")))
+        kw = dict(r_codes=comp.r_q.codes, r_scales=comp.r_q.scales)
+    lin = D.IntLinear(main.codes, main.scales, w_bits, salient_idx=np.arange(r), weight_format=fmt, **kw)
+    nbytes, packed = lin.weight_bytes()
+    if fmt == "int4":
+        assert packed and nbytes == -(-N // 128) * 128 * K // 2
+    else:
+        assert not packed and nbytes == N * K
+    act = lin.quantize(_cuda(x, torch.bfloat16), 8, False)
+    acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    y = lin.gemm(act, acc_dump=acc).float().cpu().numpy()
+    if M > 128 or fmt == "int4":
+        assert D.last_kernel().startswith("serq_i8_pair_kernel") and D.last_kernel().endswith(",w4>") == (fmt == "int4")
+    xq = O.quantize_asymmetric(x, O.IntCfg(8, False, "per-row"))
+    _, parts = O.int_gemm(xq, main, return_partials=True)
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), parts[0][1])
+    y_ref, _ = O.forward_int(x, main, comp, O.IntCfg(8, False, "per-row"))
+    mx, mean = O.parity_errors(y, y_ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
