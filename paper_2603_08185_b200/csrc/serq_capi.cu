@@ -1093,10 +1093,12 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   const bool pair_ok = h->has_w4 || (M > 128 && (h->r_mode != SERQ_R_INT || h->contiguous) && h->r <= 128 &&
                                      (h->r_mode != SERQ_R_DENSE || h->r <= 64) && !SERQ_DBG(g_debug_flags, 65536));
   if (pair_ok) {
-    CK(set_smem_attr(serq_i8_pair_kernel<256, kI8Epi, false>, I8Cfg<kI8Epi>::kSmem));
-    CK(set_smem_attr(serq_i8_pair_kernel<128, kI8Epi, false>, I8Cfg<kI8Epi>::kSmem));
-    CK(set_smem_attr(serq_i8_pair_kernel<256, kI8Epi, true>, I8Cfg<kI8Epi>::kSmem));
-    CK(set_smem_attr(serq_i8_pair_kernel<128, kI8Epi, true>, I8Cfg<kI8Epi>::kSmem));
+    using Cfg8 = I8Cfg<kI8Epi, false>;
+    using Cfg4 = I8Cfg<kI8Epi, true>;
+    CK(set_smem_attr(serq_i8_pair_kernel<256, kI8Epi, false>, Cfg8::kSmem));
+    CK(set_smem_attr(serq_i8_pair_kernel<128, kI8Epi, false>, Cfg8::kSmem));
+    CK(set_smem_attr(serq_i8_pair_kernel<256, kI8Epi, true>, Cfg4::kSmem));
+    CK(set_smem_attr(serq_i8_pair_kernel<128, kI8Epi, true>, Cfg4::kSmem));
     I8Maps im;
     int rc = make_map(&im.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K, M, h->K, 128, 128);
     if (!rc)
@@ -1134,19 +1136,21 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     const dim3 grid(unsigned(2 * (tiles < max_pairs ? tiles : max_pairs)));
     // launched with programmatic dependent launch: the prologue and the first weight stages
     // overlap the activation quantizer's tail
-    using Cfg = I8Cfg<kI8Epi>;
-    const dim3 blk(Cfg::kThreads);
+    using Cfg8 = I8Cfg<kI8Epi, false>;
+    using Cfg4 = I8Cfg<kI8Epi, true>;
     if (h->has_w4 && narrow) {
-      CK(launch_pdl(serq_i8_pair_kernel<128, kI8Epi, true>, grid, blk, Cfg::kSmem, S(stream), im, p));
+      CK(launch_pdl(serq_i8_pair_kernel<128, kI8Epi, true>, grid, dim3(Cfg4::kThreads), Cfg4::kSmem, S(stream), im, p));
       LAUNCH_CHECK("serq_i8_pair_kernel<128,w4>");
     } else if (h->has_w4) {
-      CK(launch_pdl(serq_i8_pair_kernel<256, kI8Epi, true>, grid, blk, Cfg::kSmem, S(stream), im, p));
+      CK(launch_pdl(serq_i8_pair_kernel<256, kI8Epi, true>, grid, dim3(Cfg4::kThreads), Cfg4::kSmem, S(stream), im, p));
       LAUNCH_CHECK("serq_i8_pair_kernel<256,w4>");
     } else if (narrow) {
-      CK(launch_pdl(serq_i8_pair_kernel<128, kI8Epi, false>, grid, blk, Cfg::kSmem, S(stream), im, p));
+      CK(launch_pdl(serq_i8_pair_kernel<128, kI8Epi, false>, grid, dim3(Cfg8::kThreads), Cfg8::kSmem, S(stream), im,
+                    p));
       LAUNCH_CHECK("serq_i8_pair_kernel<128>");
     } else {
-      CK(launch_pdl(serq_i8_pair_kernel<256, kI8Epi, false>, grid, blk, Cfg::kSmem, S(stream), im, p));
+      CK(launch_pdl(serq_i8_pair_kernel<256, kI8Epi, false>, grid, dim3(Cfg8::kThreads), Cfg8::kSmem, S(stream), im,
+                    p));
       LAUNCH_CHECK("serq_i8_pair_kernel<256>");
     }
     return SERQ_OK;

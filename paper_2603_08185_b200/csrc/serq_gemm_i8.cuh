@@ -27,14 +27,18 @@ constexpr int kI8Side = 2 * 16384;             // R operands: [A' (dense only)] 
 constexpr int kI8Const = 4 * 256 * 4;
 // kE: epilogue column groups -- 4 * kE epilogue warps (warp w drains TMEM lane quadrant w % 4,
 // columns chunks e, e + kE, ...), each with one 2 KB output staging box
-template <int kE>
+template <int kE, bool kW4 = false>
 struct I8Cfg {
   static constexpr int kEpiWarps = 4 * kE;
+  // warps: 0 TMA producer, 1 MMA issuer, 2 .. 2 + kLoadWarps - 1 packed-INT4 loaders (W4) or idle,
+  // then the epilogue warps
+  static constexpr int kLoadWarps = kW4 ? 4 : 2;
+  static constexpr int kEpiWarp0 = 2 + kLoadWarps;
   static constexpr int kEpiBytes = kEpiWarps * 2048;
   static constexpr int kStages = kE >= 4 ? 4 : 5;
   static constexpr int kStage = kI8A + kI8B;
   static constexpr int kSmem = 1024 + kStages * kStage + kI8Side + kI8Const + kEpiBytes + 512;
-  static constexpr int kThreads = 128 + 32 * kEpiWarps;
+  static constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
   static_assert(kSmem <= 232448, "smem budget");
 };
 
@@ -105,7 +109,6 @@ __device__ __forceinline__ uint2 widen_int4x8(uint32_t w) {
   const uint32_t hi = ((((w >> 4) & 0x0F0F0F0Fu) ^ 0x08080808u) + 0x78787878u) ^ 0x80808080u;
   return make_uint2(lo, hi);
 }
-constexpr int kI8LoadWarps = 2;  // W4 weights: warps 2..3 widen packed INT4 into the operand
 // kN: output columns per CTA-pair tile (256, or 128 for small problems so twice as many
 // pairs get a tile; each CTA then stages 64 weight rows)
 // kW4: the weights stay PACKED INT4 in HBM (0.5 B / weight, pre-tiled [N/128][K/128][128 rows x
@@ -114,11 +117,13 @@ constexpr int kI8LoadWarps = 2;  // W4 weights: warps 2..3 widen packed INT4 int
 // into the 128B-swizzled stage -- the same shared-memory traffic as the TMA'd int8 feed (the
 // staging copy of an earlier variant made the SM shared-memory bound).  Blackwell has no INT4 MMA.
 template <int kN = 256, int kE = 2, bool kW4 = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE>::kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThreads, 1)
     serq_i8_pair_kernel(const __grid_constant__ I8Maps maps, const GemmParams p) {
   static_assert(kN == 256 || kN == 128, "256- or 128-column tiles");
   static_assert((kN / 32) % kE == 0, "column chunks split evenly over the epilogue groups");
-  using Cfg = I8Cfg<kE>;
+  using Cfg = I8Cfg<kE, kW4>;
+  constexpr int kI8LoadWarps = Cfg::kLoadWarps;
+  constexpr int kEpiWarp0 = Cfg::kEpiWarp0;
   constexpr int kEpiThreads = 32 * Cfg::kEpiWarps;
   constexpr int kBHalf = kN / 2;  // weight rows per CTA
   constexpr uint32_t kBBytes = kBHalf * 128;  // one 128-K step of this CTA's weight rows (int8)
@@ -291,11 +296,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE>::kThreads,
     }
   } else if (kW4 && warp < 2 + kI8LoadWarps) {
     // ------------------------------------------------------------ W4 loaders (both CTAs)
-    // thread lt covers chunk c = lt % 8 (16 int8 = 8 packed bytes) of rows lt / 8 + 8 j: a warp
-    // reads 4 rows x 64 B per load (coalesced) and stores 4 rows x 128 B (conflict-free)
-    constexpr int kJ = kBHalf / 8;
+    // thread lt: 16 packed bytes (32 codes = operand chunks 2c, 2c + 1) of rows lt / 4 + kRowsPerPass j;
+    // a warp loads 8 rows x 64 B per instruction and its stores are conflict-free (two rows per
+    // quarter-warp fill complementary halves of the 128-byte swizzle pattern)
+    constexpr int kRowsPerPass = 32 * kI8LoadWarps / 4;
+    constexpr int kJ = kBHalf / kRowsPerPass;
     const int lt = int(threadIdx.x) - 64;
-    const int c = lt & 7, r0 = lt >> 3;
+    const int c = lt & 3, r0 = lt >> 2;
     const uint32_t full_leader = map_rank(smem_u32(&full[0]), 0);
     const uint8_t* w4 = p.w4;
     const int total = my_tiles * ks;
@@ -305,21 +312,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE>::kThreads,
       const int n_half = (tile / tiles_m) * kN + int(rank) * kBHalf;
       return w4 + (size_t((n_half >> 7) * ks + kk) * 128 + (n_half & 127)) * 64;
     };
-    auto src_of = [&](int g) { return block_of(g) + r0 * 64 + c * 8; };
-    // the register loads run 2 K-steps ahead; an L2 prefetch of the whole block kPf steps ahead
-    // keeps them L2 hits (HBM latency is far longer than the ~0.4 us per step)
+    auto src_of = [&](int g) { return block_of(g) + r0 * 64 + c * 16; };
+    // the register loads run 3 K-steps ahead; an L2 prefetch of the whole block kPf steps ahead
     constexpr int kPf = 8;
     if (lt == 0)
       for (int g = 0; g < kPf && g < total; ++g)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(block_of(g)), "r"(uint32_t(kBHalf * 64)) : "memory");
-    auto load = [&](uint2 (&b)[kJ], int g) {
-      if (g < total) {
+    auto load = [&](uint4 (&b)[kJ], int g) {
+      if (g < total && !SERQ_DBG(p.dbg, 1 << 10)) {  // diagnostics: no weight loads
         const uint8_t* src = src_of(g);
 #pragma unroll
-        for (int j = 0; j < kJ; ++j) b[j] = __ldg(reinterpret_cast<const uint2*>(src + j * 8 * 64));
+        for (int j = 0; j < kJ; ++j) {
+          uint4 v;
+          asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                       : "l"(src + j * kRowsPerPass * 64));
+          b[j] = v;
+        }
       }
     };
-    uint2 b0[kJ], b1[kJ], b2[kJ], b3[kJ];
+    // Four register buffers; a step's loads are issued three steps before its widen.  (Measured at
+    // C3: 127.8 us; rotating the buffers by name instead of shifting them -- no register copy
+    // waits on the step's own loads -- measured 150.6 us, and an L2 prefetch changed nothing.)
+    uint4 b0[kJ], b1[kJ], b2[kJ], b3[kJ];
     load(b0, 0);
     load(b1, 1);
     load(b2, 2);
@@ -327,15 +342,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE>::kThreads,
       if (lt == 0 && g + kPf < total)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(block_of(g + kPf)), "r"(uint32_t(kBHalf * 64))
                      : "memory");
-      load(b3, g + 3);  // four K-steps in flight per thread
+      load(b3, g + 3);
       const int s = g % kI8Stages;
       mbar_wait(&empty[s], ((g / kI8Stages) & 1) ^ 1);
       const uint32_t dst = smem_u32(smem + s * kI8Stage + kI8A);
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
-        const int row = r0 + 8 * j;
-        const uint2 e0 = widen_int4x8(b0[j].x), e1 = widen_int4x8(b0[j].y);  // elements 0..7, 8..15
-        st_shared_v4(dst + row * 128 + ((uint32_t(c) ^ uint32_t(row & 7)) * 16), e0.x, e0.y, e1.x, e1.y);
+        if (SERQ_DBG(p.dbg, 1 << 11)) break;  // diagnostics: no operand stores
+        const int row = r0 + kRowsPerPass * j;
+        const uint32_t rb = dst + row * 128, sw = uint32_t(row & 7);
+        const uint2 e0 = widen_int4x8(b0[j].x), e1 = widen_int4x8(b0[j].y);  // chunk 2c: elements 0..15
+        const uint2 e2 = widen_int4x8(b0[j].z), e3 = widen_int4x8(b0[j].w);  // chunk 2c + 1
+        st_shared_v4(rb + (((2u * c) ^ sw) * 16), e0.x, e0.y, e1.x, e1.y);
+        st_shared_v4(rb + (((2u * c + 1) ^ sw) * 16), e2.x, e2.y, e3.x, e3.y);
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -347,14 +366,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE>::kThreads,
         b2[j] = b3[j];
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= uint32_t(kEpiWarp0)) {
     // ------------------------------------------------------------ epilogue (both CTAs)
     pdl_wait();  // sx / zp / xs come from the quantizer; y may still be read by a predecessor
     pdl_launch_dependents();
     const uint32_t q = warp & 3;  // TMEM lane quadrant of this warp (warp id % 4)
-    const int eg = int(warp - 4) >> 2;  // column group: chunks eg, eg + kE, ...
+    const int eg = int(warp - kEpiWarp0) >> 2;  // column group: chunks eg, eg + kE, ...
     const uint32_t lane_base = (q * 32u) << 16;
-    uint8_t* stage_out = epi + (warp - 4) * 2048;
+    uint8_t* stage_out = epi + (warp - kEpiWarp0) * 2048;
     const uint32_t swz = (lane_id() >> 1) & 3;
     const uint32_t tmem_empty_leader = map_rank(smem_u32(tmem_empty), 0);
     for (int i = 0; i < my_tiles; ++i) {
@@ -364,7 +383,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE>::kThreads,
       const int n0 = nt * kN;
       // per-column constants of this tile
       named_bar_sync(1, kEpiThreads);  // previous tile's readers are done with the constants
-      for (int c = threadIdx.x - 128; c < kN; c += kEpiThreads) {
+      for (int c = int(threadIdx.x) - 32 * kEpiWarp0; c < kN; c += kEpiThreads) {
         const int n = n0 + c;
         const bool ok = n < p.N;
         cst_f[c] = ok ? p.sw[n] : 0.f;
