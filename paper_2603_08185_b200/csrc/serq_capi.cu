@@ -185,6 +185,9 @@ struct serq_linear {
   CUtensorMap map_b64;                                // pair3 narrow (256 x 128) last-round tiles: 64-row B boxes
   CUtensorMap map_r32, map_sfr4;                     // pair3 kernel: R as 32-B swizzled rows, 512-B SF boxes
   bool has_r32 = false;
+  void* rdec = nullptr;                               // decode: R zero-padded to 64 / 128 columns (r != 64)
+  CUtensorMap map_rdec;                               // decode: R rows of dec_rw bytes (32- / 64-byte swizzle)
+  int dec_rw = 0;                                     // 0: the decode kernel cannot take this R (r > 128)
   CUtensorMap map_r_pair;                            // INT pair kernel maps (R with 128-row boxes)
   bool has_w4 = false;                               // INT: weights packed INT4, tiled [N/128][K/128][128][64 B]
   int64_t w_bytes = 0;                               // bytes of the resident main weights
@@ -217,7 +220,7 @@ namespace {
 void free_handle(serq_linear* h) {
   void* ptrs[] = {h->w, h->sfw, h->rbuf, h->sfr, h->sw, h->colsum, h->sr, h->colsum_r,
                   h->ws_x, h->ws_codes, h->ws_sf, h->ws_y,
-                  h->sw_g, h->colsum_g, h->cterm, h->ws_xs, h->ws_xsf, h->ws_s64, h->ws_s32, h->ws_zp};
+                  h->sw_g, h->colsum_g, h->cterm, h->ws_xs, h->ws_xsf, h->ws_s64, h->ws_s32, h->ws_zp, h->rdec};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : h->e2e_ev)
@@ -481,6 +484,23 @@ int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K
                       128, 128, 4, CU_TENSOR_MAP_SWIZZLE_NONE);
       if (rc) return bail(rc);
       h->has_r32 = true;
+      h->map_rdec = h->map_r32;
+      h->dec_rw = 32;
+    } else if (r <= 128) {
+      // decode kernel: R zero-padded to 64 (32-B rows) or 128 columns (64-B rows, two K = 64 MMAs);
+      // padded codes are 0, so the padded columns contribute nothing whatever X holds there
+      const int rp = r <= 64 ? 64 : 128;
+      if (cudaMalloc(&h->rdec, N * rp / 2) != cudaSuccess) return bail(fail(SERQ_ECUDA, "cudaMalloc R (decode)"));
+      if (cudaMemsetAsync(h->rdec, 0, N * rp / 2, st) != cudaSuccess ||
+          cudaMemcpy2DAsync(h->rdec, rp / 2, h->rbuf, r / 2, r / 2, N, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return bail(fail(SERQ_ECUDA, "R (decode) copy"));
+      rc = make_map(&h->map_rdec, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->rdec, rp / 2, N, rp / 2, rp / 2, 128,
+                    rp == 64 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B);
+      if (!rc)
+        rc = make_map(&h->map_sfr4, CU_TENSOR_MAP_DATA_TYPE_UINT8, h->sfr, 128, uint64_t(sf_bytes_of(N, r) / 128),
+                      128, 128, 4, CU_TENSOR_MAP_SWIZZLE_NONE);
+      if (rc) return bail(rc);
+      h->dec_rw = rp / 2;
     }
   }
   *out = h;
@@ -770,9 +790,13 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
                             const __nv_bfloat16* x, int64_t ldx, uint8_t* codes_out, uint8_t* sf_out, int64_t M,
                             void* y, int64_t ldy, cudaStream_t st, const uint8_t* xs_codes = nullptr,
                             const uint8_t* xs_sf = nullptr) {
-  CK(set_smem_attr(serq_mx_decode_cl_kernel<false>, ClCfg<false>::kSmem));
-  CK(set_smem_attr(serq_mx_decode_cl_kernel<true, 1>, ClCfg<true>::kSmem));
-  CK(set_smem_attr(serq_mx_decode_cl_kernel<true, 2>, ClCfg<true>::kSmem));
+  CK(set_smem_attr(serq_mx_decode_cl_kernel<false, 1, 32>, ClCfg<false, 32>::kSmem));
+  CK(set_smem_attr(serq_mx_decode_cl_kernel<true, 1, 32>, ClCfg<true, 32>::kSmem));
+  CK(set_smem_attr(serq_mx_decode_cl_kernel<true, 2, 32>, ClCfg<true, 32>::kSmem));
+  CK(set_smem_attr(serq_mx_decode_cl_kernel<false, 1, 64>, ClCfg<false, 64>::kSmem));
+  CK(set_smem_attr(serq_mx_decode_cl_kernel<true, 1, 64>, ClCfg<true, 64>::kSmem));
+  CK(set_smem_attr(serq_mx_decode_cl_kernel<true, 2, 64>, ClCfg<true, 64>::kSmem));
+  const bool rw64 = h->r > 0 && h->dec_rw == 64;
   const bool fuse = x != nullptr;
   const int tiles = int(cdiv(h->N, 128));
   const int ks = int(cdiv(h->K / 2, kStepBytes));
@@ -804,8 +828,8 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
   DecodeMaps dm;
   dm.w = h->map_b128;
   dm.sfw = h->map_sfw;
-  dm.r = h->has_r32 ? h->map_r32 : h->map_b128;
-  dm.sfr = h->has_r32 ? h->map_sfr4 : h->map_sfw;
+  dm.r = h->dec_rw ? h->map_rdec : h->map_b128;
+  dm.sfr = h->dec_rw ? h->map_sfr4 : h->map_sfw;
   const bool gather = h->r > 0 && !h->contiguous;
   if (gather && (fuse || !xs_codes || !xs_sf)) return fail(SERQ_EINVAL, "gather decode needs the xs slice");
   cp.gather = gather ? 1 : 0;
@@ -830,7 +854,8 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(tiles * S));
   cfg.blockDim = dim3(kClThreads);
-  cfg.dynamicSmemBytes = fuse ? ClCfg<true>::kSmem : ClCfg<false>::kSmem;
+  cfg.dynamicSmemBytes = rw64 ? (fuse ? ClCfg<true, 64>::kSmem : ClCfg<false, 64>::kSmem)
+                              : (fuse ? ClCfg<true, 32>::kSmem : ClCfg<false, 32>::kSmem);
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -844,11 +869,14 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
   if (fuse) {
     // converter lanes carry 1 or 2 token rows
     if (M <= 4)
-      CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<true, 1>, dm, cp));
+      CK(rw64 ? cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<true, 1, 64>, dm, cp)
+              : cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<true, 1, 32>, dm, cp));
     else
-      CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<true, 2>, dm, cp));
+      CK(rw64 ? cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<true, 2, 64>, dm, cp)
+              : cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<true, 2, 32>, dm, cp));
   } else {
-    CK(cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<false>, dm, cp));
+    CK(rw64 ? cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<false, 1, 64>, dm, cp)
+            : cudaLaunchKernelEx(&cfg, serq_mx_decode_cl_kernel<false, 1, 32>, dm, cp));
   }
   LAUNCH_CHECK("serq_mx_decode_cl_kernel");
   return SERQ_OK;
@@ -893,7 +921,9 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
   p.w_ksteps = h->w_ksteps;
   p.dbg = g_debug_flags;
   p.dbg_ts = g_debug_ts;
-  if (M <= kDecN && (h->r == 0 || h->has_r32) && !SERQ_DBG(g_debug_flags, 2048))
+  // decode kernel: any contiguous R up to r = 128; the gather fallback with r = 64 (32-B xs rows)
+  const bool dec_ok = h->r == 0 || (h->dec_rw && (h->contiguous || h->has_r32));
+  if (M <= kDecN && dec_ok && !SERQ_DBG(g_debug_flags, 2048))
     return launch_decode_cl(h, a_codes, a_sf, nullptr, 0, nullptr, nullptr, M, y, ldy, S(stream), xs_codes, xs_sf);
   // pair3 for the permuted layout, and for the gather fallback with r == 64 (debug flag 1<<24: the
   // gather cases take the older pair kernel)
@@ -1001,7 +1031,7 @@ int serq_forward_mx(serq_linear_t* h, const void* x, int dtype, int64_t M, int64
   const bool gather = h->r > 0 && !h->contiguous;
   if (gather && (!gather_idx || !xs_codes || !xs_sf))
     return fail(SERQ_EINVAL, "non-contiguous salient set needs gather_idx and the xs buffers");
-  if (M <= kClFuseM && (h->r == 0 || h->has_r32) && dtype == SERQ_BF16 && !gather &&
+  if (M <= kClFuseM && (h->r == 0 || h->dec_rw) && dtype == SERQ_BF16 && !gather &&
       !(reinterpret_cast<uintptr_t>(x) & 15) && ldx % 8 == 0 && ldx >= h->K && !SERQ_DBG(g_debug_flags, 1 << 23) &&
       !SERQ_DBG(g_debug_flags, 2048)) {
     // decode (M <= 8) with the quantizer inside the linear: one kernel per layer instead of

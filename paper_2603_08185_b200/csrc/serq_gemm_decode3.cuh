@@ -39,7 +39,8 @@ constexpr int kDecW = 128 * kStepBytes;                // 16 KB weight tile per 
 constexpr int kDecX = kDecN * kStepBytes;              // 2 KB token tile
 constexpr int kDecSF = 1024;                           // 2 SF chunks of one 128-row block
 constexpr int kDecStage = kDecW + kDecX + 2 * kDecSF;  // 20 KB (1 KB aligned)
-constexpr int kDecRB = 128 * 32;                       // R tile: 128 rows x 32 B (r <= 64)
+// R tile: 128 rows x kRW bytes -- 32 B (r <= 64, 32-byte swizzle) or 64 B (64 < r <= 128,
+// 64-byte swizzle, two K = 64 MMAs); smaller ranks are zero-padded at pack time
 static_assert(kDecStage % 1024 == 0, "stage alignment");
 
 struct DecodeMaps {
@@ -53,9 +54,10 @@ constexpr int kClRed = 6 * 1024;     // rank-0 landing buffer for narrow partial
 // fused quantizer: kP (token row, 32-block) pairs per lane, M <= 4 kP; used for M <= 8 (at
 // M = 16 the 4-pair converter was slower than the quantizer kernel + PDL: 10.5 vs 8.6 us)
 constexpr int kClFuseM = 8;
-template <bool kFuse>
+template <bool kFuse, int kRW = 32>
 struct ClCfg {
-  static constexpr int kStages = 5;
+  static constexpr int kStages = kRW == 64 ? 4 : 5;  // the 8 KB R tile costs one stage
+  static constexpr int kDecRB = 128 * kRW;
   static constexpr int kSmem = 1024 + kStages * kDecStage + kDecRB + 512 + kClXs + kClRed + 512;
   // 228 KB per SM, 1 KB reserved per CTA
   static_assert(2 * (kSmem + 1024) <= 228 * 1024, "two CTAs (this linear and the next) must fit on one SM");
@@ -102,10 +104,12 @@ __device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t bar_cluster
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
-template <bool kFuse, int kP = 1>
+template <bool kFuse, int kP = 1, int kRW = 32>
 __global__ void __launch_bounds__(kClThreads, 2) serq_mx_decode_cl_kernel(const __grid_constant__ DecodeMaps maps,
                                                                           const ClParams p) {
-  constexpr int kClStages = ClCfg<kFuse>::kStages;
+  static_assert(kRW == 32 || kRW == 64, "R rows of 32 or 64 bytes");
+  constexpr int kClStages = ClCfg<kFuse, kRW>::kStages;
+  constexpr int kDecRB = ClCfg<kFuse, kRW>::kDecRB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* rbuf = smem + kClStages * kDecStage;  // R tile (4 KB) + R scale factors (512 B)
@@ -240,8 +244,13 @@ __global__ void __launch_bounds__(kClThreads, 2) serq_mx_decode_cl_kernel(const 
             tmem_cp_32x128b_x4(sfxs, make_sdesc(smem_u32(xsbuf + 512), 128, 128, 0));
             mma_mxf4(acc, make_sdesc(smem_u32(rbuf), 16, 256, 6), make_sdesc(smem_u32(xsbuf), 16, 256, 6), id0, sfr,
                      sfxs, 1u);
-          } else {
+          } else if constexpr (kRW == 32) {
             mma_mxf4(acc, make_sdesc(smem_u32(rbuf), 16, 256, 6), b, id0, sfr, sfb, 1u);
+          } else {
+            // r in (64, 128]: R rows of 64 B (64-byte swizzle), K-tile 0 of X as two K = 64 slices
+            const uint64_t rd = make_sdesc(smem_u32(rbuf), 16, 512, 4);
+            mma_mxf4(acc, rd, b, id0, sfr, sfb, 1u);
+            mma_mxf4(acc, rd + 2, b + 2, id1, sfr | (2u << 30), sfb | (2u << 30), 1u);
           }
         }
         tc_commit(&empty[s]);

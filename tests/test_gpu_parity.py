@@ -350,7 +350,10 @@ def test_int_grouped_rejects_unsupported_groups(D):
                                      # several CTAs (few tiles, long K), ragged N, 86 tiles on 148 SMs
                                      (7, 256, 11008, 0), (2, 512, 20000, 64), (16, 11008, 256, 64),
                                      (5, 8192, 200, 32), (1, 4096, 11008, 64), (16, 11008, 4096, 64),
-                                     (1, 32768, 128, 64)])  # one tile over many CTAs (slot cap 32)
+                                     (1, 32768, 128, 64),  # one tile over many CTAs (slot cap 32)
+                                     # R zero-padded to 64 / 128 columns (two K = 64 salient MMAs)
+                                     (1, 4096, 1024, 128), (16, 2048, 768, 96), (4, 8192, 512, 128),
+                                     (8, 4096, 296, 128), (3, 1024, 384, 32)])
 def test_mx_decode_parity(D, M, K, N, r):
     x, main_t, comp = _mx_case(M, K, N, r, seed=K + M)
     lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents,
@@ -366,7 +369,7 @@ def test_mx_decode_parity(D, M, K, N, r):
         act = D.MxActivation(torch.empty(D.mx_sizes(M, K)[0], dtype=torch.uint8, device="cuda"),
                              torch.empty(D.mx_sizes(M, K)[1], dtype=torch.uint8, device="cuda"), M, K)
         y = lin.forward(xt, act).float().cpu().numpy()
-        assert D.last_kernel().startswith("serq_mx_decode_cl_kernel" if r in (0, 64) else "serq_mx_persistent")
+        assert D.last_kernel().startswith("serq_mx_decode_cl_kernel")
         # two-kernel path (quantizer, then the linear on codes)
         y2 = lin.gemm(lin.quantize(xt)).float().cpu().numpy()
         mx, mean = O.parity_errors(y, ref)

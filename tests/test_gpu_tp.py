@@ -28,6 +28,8 @@ def nccl():
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     yield dist
+    if dist.is_initialized():
+        dist.destroy_process_group()
 
 
 def _block(r=64):
