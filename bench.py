@@ -415,6 +415,8 @@ def other_configs(hbm_gbs: float) -> dict:
         # the paper's comparison at C3's shape: SVD baseline (two-factor L1 L2, r = 128) vs SERQ's fused R
         out["c3_svd_baseline_r128"] = B.svd_baseline_point(2048, 4096, 11008, 128)
         out["c4_decode"] = B.decode_points(hbm_gbs)
+        # q/k/v and gate/up each as ONE fused launch (own salient set per part, gather fallback)
+        out["c4_decode_fused"] = B.decode_fused_points(hbm_gbs)
         out["producer_rmsnorm_quant_c2"] = B.rmsnorm_quant_point(4096, 4096, hbm_gbs)
         # C4 as a whole block: Llama-2-7B-shaped decoder block (SERQ linears + f32 non-linear nodes)
         out["c4_block"] = [B.llama7b_block_point(m) for m in (1, 16, 2048)]

@@ -168,6 +168,19 @@ int serq_pack_int_grouped(const int32_t* codes, const double* scales, int64_t gr
                           int w_bits, int r_mode, const void* r_data, const double* r_scales, int r,
                           int salient_contiguous, serq_linear_t** out, serq_stream_t stream);
 
+/* Fused linears (SURVEY 7 hard-part 6; e.g. q/k/v or gate/up, which read the same activation but
+ * have their own salient sets): an MX handle packed from the row-concatenated artefacts of nseg
+ * linears (seg_rows[j] output rows each, multiples of 128, summing to N) runs them as ONE kernel.
+ * The quantizer's salient buffer then holds 128 columns per segment: gather_idx (length
+ * 128 * nseg) lists segment j's r indices at [128 j, 128 j + r), any valid index after them.
+ * One kernel covers M <= 16 (decode) and M > 128 with r = 64 and 256-row-aligned segments;
+ * other shapes return SERQ_EINVAL -- run them through per-segment views. */
+int serq_linear_set_segments(serq_linear_t* h, int nseg, const int64_t* seg_rows);
+/* A handle over output rows [row0, row0 + rows) of an MX handle (128-row aligned): no copy, the
+ * parent owns the weights and must outlive the view; salient_contiguous as for serq_pack_mx. */
+int serq_linear_view(const serq_linear_t* parent, int64_t row0, int64_t rows, int salient_contiguous,
+                     serq_linear_t** out);
+
 int serq_linear_destroy(serq_linear_t* h);
 int serq_linear_info(const serq_linear_t* h, int64_t* N, int64_t* K, int* r, int* mode, int* r_mode);
 /* Bytes of the resident main weights (padding included) and whether they are held as packed

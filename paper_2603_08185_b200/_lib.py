@@ -44,6 +44,8 @@ SIGNATURES = {
     "serq_pack_int4": (_I, [_P, _P, _I64, _I64, _I, _I, _P, _P, _I, _I, _P, _P]),
     "serq_pack_int_grouped": (_I, [_P, _P, _I64, _I64, _I64, _I, _I, _P, _P, _I, _I, _P, _P]),
     "serq_linear_destroy": (_I, [_P]),
+    "serq_linear_set_segments": (_I, [_P, _I, _P]),
+    "serq_linear_view": (_I, [_P, _I64, _I64, _I, _P]),
     "serq_linear_info": (_I, [_P, _P, _P, _P, _P, _P]),
     "serq_linear_weight_bytes": (_I, [_P, _P, _P]),
     "serq_linear_mx": (_I, [_P, _P, _P, _I64, _P, _P, _P, _I64, _P]),

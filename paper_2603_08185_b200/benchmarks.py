@@ -110,6 +110,11 @@ def device_mx_linear(K: int, N: int, r: int, seed: int = 1, salient_idx=None):
     main_t = mx_encode(W^T), R = exact residual of the first r rows (the
     salient rows after the offline permutation), encoded [N, r].  With
     ``salient_idx`` (length r) R covers those rows instead (gather fallback)."""
+    return D.MxLinear(*device_mx_parts(K, N, r, seed, salient_idx))
+
+
+def device_mx_parts(K: int, N: int, r: int, seed: int = 1, salient_idx=None):
+    """The artefacts of device_mx_linear: (codes [N, K], exps, r_codes [N, r], r_exps, salient_idx)."""
     g = torch.Generator(device="cuda").manual_seed(seed)
     wt = torch.randn((N, K), generator=g, device="cuda", dtype=torch.float32) * 0.02
     act = D.quantize_mx(wt)
@@ -126,9 +131,8 @@ def device_mx_linear(K: int, N: int, r: int, seed: int = 1, salient_idx=None):
         rc, re_ = D.unpack_mx(ra.codes, ra.sf, N, r)
     else:
         rc = re_ = None
-    lin = D.MxLinear(codes, exps, rc, re_, (np.arange(r) if salient_idx is None else np.asarray(salient_idx)) if r else None)
     del wt
-    return lin
+    return codes, exps, rc, re_, (np.arange(r) if salient_idx is None else np.asarray(salient_idx)) if r else None
 
 
 def outlier_x(M: int, K: int, seed: int = 0, frac=0.01, mag=50.0) -> torch.Tensor:
@@ -189,6 +193,51 @@ def decode_points(hbm_peak_gbs: float, layers: int = 16) -> list:
                         "linear_hbm_frac": (w_bytes + io_bytes) / (t_lin * 1e-3) / 1e9 / hbm_peak_gbs,
                         "step_tflops": flops / (t_step * 1e-3) / 1e12, "tokens_per_s": M / (t_step * 1e-3)})
         del lins
+        torch.cuda.empty_cache()
+    return out
+
+
+def decode_fused_points(hbm_peak_gbs: float, layers: int = 8) -> list:
+    """Decode through FUSED linears (device.FusedMxLinear): Llama-2-7B gate/up (2 x 11008) and
+    q/k/v (3 x 4096) as one handle each, every part with its own salient set (the gather
+    fallback these layers take in the reference's block), against the same parts as
+    separate linears.  ``layers`` distinct weight sets chained in one graph (> L2); per-layer
+    time = graph time / layers; bytes = every part's weights + R + activations + outputs."""
+    out = []
+    rng = np.random.default_rng(5)
+    r, K = 64, 4096
+    for name, ns in (("gate_up_proj", (11008, 11008)), ("qkv_proj", (4096, 4096, 4096))):
+        fused, sep = [], []
+        for i in range(layers):
+            parts = [device_mx_parts(K, n, r, seed=100 * i + j, salient_idx=np.sort(rng.permutation(K)[:r]))
+                     for j, n in enumerate(ns)]
+            fused.append(D.FusedMxLinear(parts))
+            sep.append([D.MxLinear(*p) for p in parts])
+        N = sum(ns)
+        for M in (1, 4, 16):
+            x = outlier_x(M, K)
+            ys = [torch.empty((M, N), dtype=torch.bfloat16, device="cuda") for _ in range(layers)]
+            acts = [f.fused._activation(M, x.device) for f in fused]
+            acts_s = [[lin._activation(M, x.device) for lin in ls] for ls in sep]
+
+            def run_fused():
+                for f, a, y in zip(fused, acts, ys):
+                    f.fused.forward(x, a, y)
+
+            def run_sep():
+                for ls, aa, y in zip(sep, acts_s, ys):
+                    for j, (lin, a) in enumerate(zip(ls, aa)):
+                        lin.forward(x, a, y[:, sum(ns[:j]):sum(ns[:j + 1])])
+
+            t_f = time_in_graph(run_fused, None, n=10) / layers
+            t_s = time_in_graph(run_sep, None, n=10) / layers
+            byts = N * K / 2 + N * K / 32 + N * r / 2 + N * r / 32 + M * K / 2 + M * K / 32 + 2 * M * N
+            out.append({"linear": name, "parts": list(ns), "M": M, "K": K, "r": r, "layers_in_graph": layers,
+                        "fused_step_us": t_f * 1e3, "separate_step_us": t_s * 1e3,
+                        "fused_hbm_gbs": byts / (t_f * 1e-3) / 1e9,
+                        "fused_hbm_frac": byts / (t_f * 1e-3) / 1e9 / hbm_peak_gbs,
+                        "tokens_per_s": M / (t_f * 1e-3)})
+        del fused, sep
         torch.cuda.empty_cache()
     return out
 

@@ -167,6 +167,7 @@ int ensure_attr() {
 
 // ------------------------------------------------------------------ handle
 constexpr int kE2eMaxChunks = 16;
+constexpr int kMaxSeg = 4;
 
 struct serq_linear {
   int mode = 0;  // kModeMX / kModeI8
@@ -188,6 +189,11 @@ struct serq_linear {
   void* rdec = nullptr;                               // decode: R zero-padded to 64 / 128 columns (r != 64)
   CUtensorMap map_rdec;                               // decode: R rows of dec_rw bytes (32- / 64-byte swizzle)
   int dec_rw = 0;                                     // 0: the decode kernel cannot take this R (r > 128)
+  // fused linears (serq_linear_set_segments): row segments, each with its own salient set; the
+  // quantizer's salient buffer holds 128 columns per segment (xs_cols = 128 * nseg)
+  int nseg = 1;
+  int64_t seg_row[kMaxSeg] = {0};  // start row of segments 1 .. nseg-1
+  const serq_linear* parent = nullptr;  // views (serq_linear_view): the handle owning the memory
   CUtensorMap map_r_pair;                            // INT pair kernel maps (R with 128-row boxes)
   bool has_w4 = false;                               // INT: weights packed INT4, tiled [N/128][K/128][128][64 B]
   int64_t w_bytes = 0;                               // bytes of the resident main weights
@@ -218,11 +224,17 @@ struct serq_linear {
 
 namespace {
 void free_handle(serq_linear* h) {
-  void* ptrs[] = {h->w, h->sfw, h->rbuf, h->sfr, h->sw, h->colsum, h->sr, h->colsum_r,
-                  h->ws_x, h->ws_codes, h->ws_sf, h->ws_y,
-                  h->sw_g, h->colsum_g, h->cterm, h->ws_xs, h->ws_xsf, h->ws_s64, h->ws_s32, h->ws_zp, h->rdec};
-  for (void* p : ptrs)
+  // scratch (end-to-end buffers, copy streams, events) always belongs to the handle; the packed
+  // weights only to an owning handle (a view references its parent's)
+  void* scratch[] = {h->ws_x, h->ws_codes, h->ws_sf, h->ws_y, h->ws_xs, h->ws_xsf, h->ws_s64, h->ws_s32, h->ws_zp};
+  for (void* p : scratch)
     if (p) cudaFree(p);
+  if (!h->parent) {
+    void* owned[] = {h->w, h->sfw, h->rbuf, h->sfr, h->sw, h->colsum, h->sr, h->colsum_r,
+                     h->sw_g, h->colsum_g, h->cterm, h->rdec};
+    for (void* p : owned)
+      if (p) cudaFree(p);
+  }
   for (cudaEvent_t e : h->e2e_ev)
     if (e) cudaEventDestroy(e);
   if (h->e2e_in) cudaStreamDestroy(h->e2e_in);
@@ -507,6 +519,83 @@ int serq_pack_mx(const uint8_t* codes, const int32_t* exps, int64_t N, int64_t K
   return SERQ_OK;
 }
 
+int serq_linear_set_segments(serq_linear_t* h, int nseg, const int64_t* seg_rows) {
+  if (!h || h->mode != kModeMX || h->parent) return fail(SERQ_EINVAL, "segments need an owning MX handle");
+  if (nseg < 1 || nseg > kMaxSeg || !seg_rows) return fail(SERQ_EINVAL, "1 <= nseg <= %d", kMaxSeg);
+  if (nseg > 1 && (h->r <= 0 || h->r > 128 || h->contiguous))
+    return fail(SERQ_EINVAL, "fused segments need per-segment (gathered) salient sets with 0 < r <= 128");
+  int64_t sum = 0;
+  for (int j = 0; j < nseg; ++j) {
+    if (seg_rows[j] <= 0 || seg_rows[j] % 128) return fail(SERQ_EINVAL, "segment rows must be positive multiples of 128");
+    sum += seg_rows[j];
+  }
+  if (sum != h->N) return fail(SERQ_EINVAL, "segment rows must sum to N = %lld", (long long)h->N);
+  h->nseg = nseg;
+  for (int j = 0, acc = 0; j + 1 < nseg; ++j) {
+    acc += int(seg_rows[j]);
+    h->seg_row[j] = acc;
+  }
+  return SERQ_OK;
+}
+
+int serq_linear_view(const serq_linear_t* parent, int64_t row0, int64_t rows, int salient_contiguous,
+                     serq_linear_t** out) {
+  if (!out) return fail(SERQ_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!parent || parent->mode != kModeMX) return fail(SERQ_EINVAL, "views are of MX handles");
+  const serq_linear* root = parent->parent ? parent->parent : parent;
+  if (row0 < 0 || rows <= 0 || row0 % 128 || row0 + rows > parent->N || (rows % 128 && row0 + rows != parent->N))
+    return fail(SERQ_EINVAL, "a view is a 128-row-aligned row range of the parent");
+  serq_linear* v = new serq_linear();
+  v->parent = root;
+  v->mode = kModeMX;
+  v->N = rows;
+  v->K = parent->K;
+  v->r = parent->r;
+  v->r_mode = parent->r_mode;
+  v->contiguous = salient_contiguous ? 1 : 0;
+  v->w_ksteps = parent->w_ksteps;
+  const int64_t blk = row0 / 128, r = parent->r;
+  v->w = static_cast<uint8_t*>(parent->w) + blk * parent->w_ksteps * 128 * 128;
+  v->sfw = parent->sfw + blk * kc_pad_of(parent->K) * 512;
+  const int64_t w_bytes = cdiv(rows, 128) * v->w_ksteps * 128 * 128;
+  int rc = make_map(&v->map_b128, CU_TENSOR_MAP_DATA_TYPE_UINT8, v->w, 128, uint64_t(w_bytes / 128), 128, 128, 128);
+  if (!rc) rc = make_map(&v->map_b64, CU_TENSOR_MAP_DATA_TYPE_UINT8, v->w, 128, uint64_t(w_bytes / 128), 128, 128, 64);
+  if (!rc) rc = make_sf_map(&v->map_sfw, v->sfw, rows, v->K);
+  v->map_b = v->map_b128;
+  v->map_r128 = v->map_b128;
+  v->map_sfr = v->map_sfw;
+  if (!rc && r > 0) {
+    v->rbuf = static_cast<uint8_t*>(parent->rbuf) + row0 * r / 2;
+    v->sfr = parent->sfr + blk * kc_pad_of(r) * 512;
+    rc = make_map(&v->map_r, CU_TENSOR_MAP_DATA_TYPE_UINT8, v->rbuf, r / 2, rows, r / 2, 128, kBN);
+    if (!rc) rc = make_map(&v->map_r128, CU_TENSOR_MAP_DATA_TYPE_UINT8, v->rbuf, r / 2, rows, r / 2, 128, 128);
+    if (!rc) rc = make_sf_map(&v->map_sfr, v->sfr, rows, r);
+    if (!rc && r <= 128)
+      rc = make_map(&v->map_sfr4, CU_TENSOR_MAP_DATA_TYPE_UINT8, v->sfr, 128, uint64_t(sf_bytes_of(rows, r) / 128), 128,
+                    128, 4, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (!rc && r == 64) {
+      rc = make_map(&v->map_r32, CU_TENSOR_MAP_DATA_TYPE_UINT8, v->rbuf, r / 2, rows, r / 2, 32, 128,
+                    CU_TENSOR_MAP_SWIZZLE_32B);
+      v->has_r32 = true;
+      v->map_rdec = v->map_r32;
+      v->dec_rw = 32;
+    } else if (!rc && r <= 128) {
+      const int64_t rp = r <= 64 ? 64 : 128;
+      v->rdec = static_cast<uint8_t*>(parent->rdec) + row0 * rp / 2;
+      rc = make_map(&v->map_rdec, CU_TENSOR_MAP_DATA_TYPE_UINT8, v->rdec, rp / 2, rows, rp / 2, rp / 2, 128,
+                    rp == 64 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B);
+      v->dec_rw = int(rp / 2);
+    }
+  }
+  if (rc) {
+    delete v;
+    return rc;
+  }
+  *out = v;
+  return SERQ_OK;
+}
+
 int serq_unpack_mx(const uint8_t* codes_packed, const uint8_t* sf, int64_t rows, int64_t cols, uint8_t* codes,
                    int32_t* exps, serq_stream_t stream) {
   g_launches = 0;
@@ -782,6 +871,9 @@ int serq_linear_info(const serq_linear_t* h, int64_t* N, int64_t* K, int* r, int
   return SERQ_OK;
 }
 
+// the quantizer's salient-slice buffer: r columns, or 128 per segment for fused linears
+static int64_t xs_cols_of(const serq_linear* h) { return h->nseg > 1 ? 128 * int64_t(h->nseg) : h->r; }
+
 // Decode (M <= 16): one cluster of S CTAs per 128-row weight tile, split-K,
 // DSMEM reduction (serq_gemm_decode3.cuh).  x != nullptr: the quantizer is
 // fused in (x bf16 [M, K], pitch ldx); codes_out / sf_out optionally receive
@@ -835,11 +927,14 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
   cp.gather = gather ? 1 : 0;
   cp.red_narrow = (S - 1) * ((M + 3) / 4) * 128 * 16 <= kClRed && !SERQ_DBG(g_debug_flags, 1 << 29) ? 1 : 0;
   dm.xs = dm.sfxs = h->map_b128;  // unused unless gather
+  cp.nseg = h->nseg;
+  for (int j = 0; j + 1 < h->nseg; ++j) cp.seg_row[j] = int(h->seg_row[j]);
   if (gather) {
-    int rc = make_map(&dm.xs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_codes, h->r / 2, M, h->r / 2, 32, kDecN,
+    const int64_t xc = xs_cols_of(h);  // a tile's slice: 32 B at byte column 64 * segment
+    int rc = make_map(&dm.xs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_codes, xc / 2, M, xc / 2, 32, kDecN,
                       CU_TENSOR_MAP_SWIZZLE_32B);
     if (!rc)
-      rc = make_map(&dm.sfxs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_sf, 128, uint64_t(sf_bytes_of(M, h->r) / 128), 128, 128,
+      rc = make_map(&dm.sfxs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_sf, 128, uint64_t(sf_bytes_of(M, xc) / 128), 128, 128,
                     4, CU_TENSOR_MAP_SWIZZLE_NONE);
     if (rc) return rc;
   }
@@ -890,6 +985,17 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
   if (ldy < h->N || ldy % 8) return fail(SERQ_EINVAL, "ldy must be >= N and a multiple of 8");
   const bool need_xs = h->r > 0 && !h->contiguous;
   if (need_xs && (!xs_codes || !xs_sf)) return fail(SERQ_EINVAL, "non-contiguous salient set needs the xs slice");
+  if (h->nseg > 1) {
+    // fused linears run as ONE kernel on the decode kernel (M <= 16) and the CTA-pair kernel (r = 64,
+    // segments of whole 256-column tiles); other shapes go through per-segment views (serq_linear_view)
+    bool tiles256 = true;
+    for (int j = 0; j + 1 < h->nseg; ++j) tiles256 = tiles256 && h->seg_row[j] % 256 == 0;
+    const bool dec = M <= kDecN && h->has_r32;
+    const bool pair = M > 128 && h->has_r32 && tiles256;
+    if (!dec && !pair)
+      return fail(SERQ_EINVAL, "fused segments need M <= 16, or M > 128 with r = 64 and 256-row-aligned segments "
+                               "(use per-segment views)");
+  }
   CK(set_smem_attr(serq_mx_persistent_kernel, kPSmemBytes));
   int rc = SERQ_OK;
   CUtensorMap ma, mxs, my;
@@ -938,12 +1044,16 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
       rc = make_map(&pm.y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, h->N, M, ldy * 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
     if (!rc && g3)  // 32 rows x 16 columns per epilogue box
       rc = make_map(&pm.y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, h->N, M, ldy * 2, 16, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const int64_t xc = xs_cols_of(h);  // per tile: 32 B at byte column 64 * segment
     if (!rc && g3)
-      rc = make_map(&pm.xs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_codes, h->r / 2, M, h->r / 2, 32, 128,
+      rc = make_map(&pm.xs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_codes, xc / 2, M, xc / 2, 32, 128,
                     CU_TENSOR_MAP_SWIZZLE_32B);
     if (!rc && g3)
-      rc = make_map(&pm.sfxs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_sf, 128, uint64_t(sf_bytes_of(M, h->r) / 128), 128, 128,
+      rc = make_map(&pm.sfxs, CU_TENSOR_MAP_DATA_TYPE_UINT8, xs_sf, 128, uint64_t(sf_bytes_of(M, xc) / 128), 128, 128,
                     4, CU_TENSOR_MAP_SWIZZLE_NONE);
+    p.kc_pad_xs = kc_pad_of(xc > 0 ? xc : 32);
+    p.nseg = h->nseg;
+    for (int j = 0; j + 1 < h->nseg; ++j) p.seg_row[j] = int(h->seg_row[j]);
     if (rc) return rc;
     if (!g3) pm.xs = pm.sfxs = pm.a;  // unused
     pm.b = h->map_b128;
@@ -1045,7 +1155,8 @@ int serq_forward_mx(serq_linear_t* h, const void* x, int dtype, int64_t M, int64
   // the linear is launched with programmatic dependent launch: its prologue and
   // weight stream overlap the quantizer (a per-row-tile counter hand-off was
   // measured slower: 45.1 vs 43.0 us at 4096^3, tools/fuse_probe.py)
-  int rc = act_quant_mx_impl(x, dtype, M, h->K, ldx, codes, sf, gather ? gather_idx : nullptr, gather ? h->r : 0,
+  int rc = act_quant_mx_impl(x, dtype, M, h->K, ldx, codes, sf, gather ? gather_idx : nullptr,
+                             gather ? int(xs_cols_of(h)) : 0,
                              xs_codes, xs_sf, stream);
   if (rc) return rc;
   const int n1 = g_launches;
@@ -1364,20 +1475,21 @@ int serq_forward_mx_host_gather(serq_linear_t* h, const void* x_host, int64_t M,
     CK(cudaMalloc(&h->ws_sf, sf_bytes_of(mm, h->K)));
     CK(cudaMalloc(&h->ws_y, mm * h->N * 2));
     if (gather) {
-      CK(cudaMalloc(&h->ws_xs, mm * h->r / 2));
-      CK(cudaMalloc(&h->ws_xsf, sf_bytes_of(mm, h->r)));
+      CK(cudaMalloc(&h->ws_xs, mm * xs_cols_of(h) / 2));
+      CK(cudaMalloc(&h->ws_xsf, sf_bytes_of(mm, xs_cols_of(h))));
     }
     h->ws_m = mm;
   }
-  const int64_t kc_pad = kc_pad_of(h->K), kc_pad_r = gather ? kc_pad_of(h->r) : 0;
+  const int64_t xc = xs_cols_of(h);
+  const int64_t kc_pad = kc_pad_of(h->K), kc_pad_r = gather ? kc_pad_of(xc) : 0;
   return host_pipeline(h, x_host, M, y_host, S(stream), [&](int64_t r0, int64_t mc) {
     // chunks start on 256-row boundaries, so their scale-factor tiles start on row-block boundaries
     uint8_t* codes = h->ws_codes + r0 * h->K / 2;
     uint8_t* sf = h->ws_sf + (r0 / 128) * kc_pad * 512;
-    uint8_t* xs = gather ? h->ws_xs + r0 * h->r / 2 : nullptr;
+    uint8_t* xs = gather ? h->ws_xs + r0 * xc / 2 : nullptr;
     uint8_t* xsf = gather ? h->ws_xsf + (r0 / 128) * kc_pad_r * 512 : nullptr;
     int rc = serq_act_quant_mx(static_cast<uint8_t*>(h->ws_x) + r0 * h->K * 2, SERQ_BF16, mc, h->K, h->K, codes, sf,
-                               gather ? gather_idx : nullptr, gather ? h->r : 0, xs, xsf, stream);
+                               gather ? gather_idx : nullptr, gather ? int(xc) : 0, xs, xsf, stream);
     if (rc) return rc;
     const int n1 = g_launches;
     rc = serq_linear_mx(h, codes, sf, mc, xs, xsf, static_cast<uint8_t*>(h->ws_y) + r0 * h->N * 2, h->N, stream);

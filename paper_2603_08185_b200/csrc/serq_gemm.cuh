@@ -60,6 +60,9 @@ struct GemmParams {
   int w_ksteps;          // MX weights are pre-tiled [N/128][w_ksteps][128 rows x 128 B]
   int kc_pad_r;          // SF chunks per row block for R and the salient slice
   int xs_is_x;           // salient slice = leading columns of X (no side buffer)
+  int kc_pad_xs;         // SF chunks per row block of the quantizer's salient slice buffer
+  int nseg;              // fused linears: weight-row segments with their own 128-column xs slices
+  int seg_row[3];        //   (segment j+1 starts at output row seg_row[j])
   // INT epilogue operands
   const float* sx;       // [M] per-token scale
   const int32_t* zp;     // [M] zero point (asym) or nullptr

@@ -69,6 +69,8 @@ struct ClParams {
   int k_steps, S;        // K steps per tile, CTAs per tile (cluster size)
   int kc_pad, kc_pad_r, w_ksteps;
   int gather;            // the salient term's B operand is the quantizer's x[:, idx] slice, not K-tile 0 of X
+  int nseg;              // fused linears: weight-row segments, each with its own salient slice of 128
+  int seg_row[3];        //   columns in the xs buffer (segment j+1 starts at output row seg_row[j])
   int red_narrow;        // partials carry only the M token columns and land in a dedicated buffer
   __nv_bfloat16* y;
   int64_t ldy;
@@ -192,9 +194,11 @@ __global__ void __launch_bounds__(kClThreads, 2) serq_mx_decode_cl_kernel(const 
       pdl_wait();  // activations (bf16 or codes) come from the previous kernel
       CL_STAMP(1);
       if (!kFuse && with_r && p.gather) {
+        int seg = 0;  // fused linears: this tile's segment picks its 128-column slice of xs
+        for (int j = 0; j + 1 < p.nseg; ++j) seg += n0 >= p.seg_row[j] ? 1 : 0;
         mbar_expect_tx(xsfull, kClXs);
-        tma_load_2d(xsbuf, &maps.xs, xsfull, 0, 0, kEvictLast);
-        tma_load_2d(xsbuf + 512, &maps.sfxs, xsfull, 0, 0, kEvictLast);
+        tma_load_2d(xsbuf, &maps.xs, xsfull, seg * 64, 0, kEvictLast);
+        tma_load_2d(xsbuf + 512, &maps.sfxs, xsfull, 0, seg * 4, kEvictLast);
       }
       for (int i = 0; i < nsteps; ++i) {
         const int s = i % kClStages;

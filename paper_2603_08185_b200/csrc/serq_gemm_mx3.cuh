@@ -206,9 +206,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tma_load_2d_pair_nohint(rb + k3RB, &maps.sfr, fbar, 0, ((n0 / 128) * p.kc_pad_r) * 4);
             tma_load_2d_pair_nohint(rb + k3RB + 512, &maps.sfr, fbar, 0, ((n0 / 128 + 1) * p.kc_pad_r) * 4);
             if (kGather) {  // after griddepcontrol.wait (u > 0 or the A loads above): quantizer output
+              int seg = 0;  // fused linears: the tile's segment picks its 128-column slice of xs
+              for (int j = 0; j + 1 < p.nseg; ++j) seg += n0 >= p.seg_row[j] ? 1 : 0;
               const uint32_t xb = smem_u32(xsbuf);
-              tma_load_2d_pair_nohint(xb, &maps.xs, fbar, 0, m_own);                    // [128 rows x 32 B]
-              tma_load_2d_pair_nohint(xb + 4096, &maps.sfxs, fbar, 0, (mblk * p.kc_pad_r) * 4);  // SF atom
+              tma_load_2d_pair_nohint(xb, &maps.xs, fbar, seg * 64, m_own);  // [128 rows x 32 B]
+              tma_load_2d_pair_nohint(xb + 4096, &maps.sfxs, fbar, 0, (mblk * p.kc_pad_xs + seg) * 4);  // SF atom
             }
           }
         }

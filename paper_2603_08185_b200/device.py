@@ -306,6 +306,7 @@ class MxLinear:
         idx = _check_salient_idx(salient_idx, self.r, self.K) if self.r else None
         self.contiguous = idx is None or np.array_equal(idx, np.arange(self.r))
         self.gather_idx = None if self.contiguous else torch.from_numpy(idx.astype(np.int32)).to(device)
+        self.xs_cols = self.r  # columns of the quantizer's salient slice (128 per segment when fused)
         h = ctypes.c_void_p()
         _lib.call("serq_pack_mx", codes.data_ptr(), exps.data_ptr(), self.N, self.K, _ptr(rc), _ptr(re), self.r,
                   int(self.contiguous), ctypes.byref(h), _stream())
@@ -315,6 +316,16 @@ class MxLinear:
 
     def quantize(self, x: torch.Tensor, out: MxActivation | None = None) -> MxActivation:
         return quantize_mx(x, None if self.contiguous else self.gather_idx, out)
+
+    def _activation(self, M: int, dev) -> MxActivation:
+        cb, sb = mx_sizes(M, self.K)
+        act = MxActivation(torch.empty(cb, dtype=torch.uint8, device=dev), torch.empty(sb, dtype=torch.uint8, device=dev),
+                           M, self.K)
+        if not self.contiguous:
+            cbr, sbr = mx_sizes(M, self.xs_cols)
+            act.xs_codes = torch.empty(cbr, dtype=torch.uint8, device=dev)
+            act.xs_sf = torch.empty(sbr, dtype=torch.uint8, device=dev)
+        return act
 
     def gemm(self, act: MxActivation, y: torch.Tensor | None = None) -> torch.Tensor:
         if act.K != self.K:
@@ -335,13 +346,7 @@ class MxLinear:
         if K != self.K:
             raise ValidationError("x columns must equal weight input dim")
         if act is None:
-            cb, sb = mx_sizes(M, K)
-            act = MxActivation(torch.empty(cb, dtype=torch.uint8, device=x.device),
-                               torch.empty(sb, dtype=torch.uint8, device=x.device), M, K)
-            if not self.contiguous:
-                cbr, sbr = mx_sizes(M, self.r)
-                act.xs_codes = torch.empty(cbr, dtype=torch.uint8, device=x.device)
-                act.xs_sf = torch.empty(sbr, dtype=torch.uint8, device=x.device)
+            act = self._activation(M, x.device)
         if y is None:
             y = torch.empty((M, self.N), dtype=torch.bfloat16, device=self.device)
         _lib.call("serq_forward_mx", self._h.ptr, x.data_ptr(), _dtype_id(x), M, x.stride(0), _ptr(self.gather_idx),
@@ -365,6 +370,72 @@ class MxLinear:
         with torch.cuda.device(self.device):
             _lib.call("serq_forward_mx_host_gather", self._h.ptr, x_host.data_ptr(), x_host.shape[0],
                       _ptr(self.gather_idx), y_host.data_ptr(), _stream())
+
+
+class FusedMxLinear:
+    """Several MX SERQ linears that read the same activation -- q/k/v, gate/up (SURVEY 7
+    hard-part 6) -- packed as ONE handle over their row-concatenated weights, each keeping its
+    own salient set (the reference plans them separately, toymodel.py:267-277; every one takes
+    the gather fallback).  The quantizer runs once (its salient buffer holds 128 columns per
+    part) and, with r = 64, for M <= 16 and for M > 128 with 256-row-aligned parts, ONE kernel
+    computes every part (serq_linear_set_segments); other token counts run per-part views of
+    the same weights (serq_linear_view, no copy).  ``parts``: (codes [N_j, K], exps, r_codes
+    [N_j, r], r_exps, salient_idx [r]) per linear, N_j a multiple of 128, equal K and r."""
+
+    def __init__(self, parts, device="cuda"):
+        device = torch.device(device)
+        if not 1 <= len(parts) <= 4:
+            raise ValidationError("fuse 1 to 4 linears")
+        arrs = [[np.asarray(a.cpu() if isinstance(a, torch.Tensor) else a) for a in p[:4]] for p in parts]
+        K = arrs[0][0].shape[1]
+        r = arrs[0][2].shape[1]
+        self.n_parts = [a[0].shape[0] for a in arrs]
+        if any(a[0].shape[1] != K or a[2].shape[1] != r for a in arrs):
+            raise ValidationError("fused linears need the same K and rank")
+        if any(n % 128 for n in self.n_parts) or not 0 < r <= 128:
+            raise ValidationError("fused linears need output dims that are multiples of 128 and 0 < r <= 128")
+        idxs = [_check_salient_idx(p[4], r, K) for p in parts]
+        pad = np.concatenate([np.concatenate([ix, np.full(128 - r, ix[0], np.int64)]) for ix in idxs])
+        cat = [np.ascontiguousarray(np.concatenate([a[j] for a in arrs])) for j in range(4)]
+        # any non-contiguous index set puts the packed handle in gather mode; the real list follows
+        self.fused = MxLinear(cat[0], cat[1], cat[2], cat[3], np.arange(r)[::-1].copy(), device)
+        self.fused.gather_idx = torch.from_numpy(pad.astype(np.int32)).to(device)
+        self.fused.xs_cols = 128 * len(parts)
+        rows = (ctypes.c_int64 * len(parts))(*self.n_parts)
+        _lib.call("serq_linear_set_segments", self.fused._h.ptr, len(parts), rows)
+        self.K, self.N, self.r, self.device = K, sum(self.n_parts), r, device
+        self.bounds = np.concatenate([[0], np.cumsum(self.n_parts)]).tolist()
+        self.views = []
+        for j, ix in enumerate(idxs):
+            h = ctypes.c_void_p()
+            contiguous = bool(np.array_equal(ix, np.arange(r)))
+            _lib.call("serq_linear_view", self.fused._h.ptr, self.bounds[j], self.n_parts[j], int(contiguous),
+                      ctypes.byref(h))
+            v = MxLinear.__new__(MxLinear)
+            v._h, v.N, v.K, v.r, v.device, v.contiguous, v.xs_cols = _Handle(h), self.n_parts[j], K, r, device, contiguous, r
+            v.gather_idx = None if contiguous else torch.from_numpy(ix.astype(np.int32)).to(device)
+            v._parent = self.fused  # the weights belong to the fused handle
+            self.views.append(v)
+        aligned = all(b % 256 == 0 for b in self.bounds[1:-1])
+        # one kernel: the decode kernel (M <= 16) and the CTA-pair kernel (M > 128) take the gathered
+        # salient slice as 32-byte rows, i.e. r = 64
+        self._one_kernel = lambda m: r == 64 and (m <= 16 or (m > 128 and aligned))
+
+    def forward(self, x: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
+        """Y [M, sum N_j] (bf16): part j's output in columns [bounds[j], bounds[j+1])."""
+        M = x.shape[0]
+        if y is None:
+            y = torch.empty((M, self.N), dtype=torch.bfloat16, device=self.device)
+        if self._one_kernel(M):
+            return self.fused.forward(x, None, y)
+        for j, v in enumerate(self.views):
+            v.forward(x, None, y[:, self.bounds[j]:self.bounds[j + 1]])
+        return y
+
+    __call__ = forward
+
+    def split(self, y: torch.Tensor) -> list:
+        return [y[:, self.bounds[j]:self.bounds[j + 1]] for j in range(len(self.n_parts))]
 
 
 class IntLinear:

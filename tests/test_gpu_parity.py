@@ -724,3 +724,37 @@ def test_int_weight_storage_paths(D, M, N, w_bits, r_mode, fmt):
     y_ref, _ = O.forward_int(x, main, comp, O.IntCfg(8, False, "per-row"))
     mx, mean = O.parity_errors(y, y_ref)
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+# ---------------------------------------------------------------- fused linears (q/k/v, gate/up)
+
+
+@pytest.mark.parametrize("M", [1, 5, 16, 64, 300])
+@pytest.mark.parametrize("r", [64, 128])
+def test_fused_linears_per_part_salient_sets(D, M, r):
+    # two (or three) linears reading the same activation, each with its own salient set, packed as
+    # ONE handle: one quantizer launch, one kernel (decode / CTA pair) or per-part views -- every
+    # part equals the oracle forward of that linear alone (compensate.py:319-340)
+    K = 1024
+    ns = [512, 768] if r == 64 else [256, 512, 384]
+    rng = np.random.default_rng(M + r)
+    x = _bf16_outlier_x(M, K, seed=M + 7)
+    parts, refs = [], []
+    for j, n in enumerate(ns):
+        w = rng.standard_normal((K, n)) * 0.02
+        idx = np.sort(rng.choice(K, r, replace=False))
+        w[idx] *= 8
+        main_t, comp = O.build_serq_rtn_mx(w, idx, 32)
+        parts.append((main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                      comp.r_q.block_scale_exponents, idx))
+        refs.append(O.forward_mx(x, main_t, comp))
+    fl = D.FusedMxLinear(parts)
+    y = fl(_cuda(x, torch.bfloat16))
+    assert D.last_launch_count() >= 1
+    if M <= 16 and r == 64:
+        assert D.last_kernel().startswith("serq_mx_decode_cl_kernel")
+    elif M > 128 and r == 64:
+        assert D.last_kernel() == "serq_mx_pair3_kernel<gather>"
+    for j, yj in enumerate(fl.split(y)):
+        mx, mean = O.parity_errors(yj.float().cpu().numpy(), refs[j])
+        assert mx <= TOL_MAX and mean <= TOL_MEAN, (j, mx, mean)
