@@ -420,6 +420,8 @@ def other_configs(hbm_gbs: float) -> dict:
         out["producer_rmsnorm_quant_c2"] = B.rmsnorm_quant_point(4096, 4096, hbm_gbs)
         # C4 as a whole block: Llama-2-7B-shaped decoder block (SERQ linears + f32 non-linear nodes)
         out["c4_block"] = [B.llama7b_block_point(m) for m in (1, 16, 2048)]
+        # the same block with q/k/v and up/gate fused (device.FusedMxLinear)
+        out["c4_block_fused"] = [B.llama7b_block_point(m, fused=True) for m in (1, 16, 2048)]
         out["c5_block_tp1"] = B.c5_block_point(1, 0, flush=fl)
     except Exception as e:  # secondary numbers must not hide the headline line
         out["error"] = f"{type(e).__name__}: {e}"

@@ -368,7 +368,7 @@ def rmsnorm_quant_point(M: int, K: int, hbm_peak_gbs: float, n_steps: int = 16) 
             "unfused_extra_bytes": 4 * M * K}
 
 
-def llama7b_block_point(M: int, n_blocks: int = 4, r: int = 64) -> dict:
+def llama7b_block_point(M: int, n_blocks: int = 4, r: int = 64, fused: bool = False) -> dict:
     """Whole Llama-2-7B-shaped decoder block on the device (block.DeviceBlock: SERQ MXFP4
     linears + f32 RMSNorm / attention / SiLU), ``n_blocks`` distinct blocks chained in ONE
     CUDA graph (~400 MB of weights > L2, so every block streams its weights).  q/k/v and
@@ -381,12 +381,18 @@ def llama7b_block_point(M: int, n_blocks: int = 4, r: int = 64) -> dict:
     rng = np.random.default_rng(9)
     blocks = []
     for b in range(n_blocks):
-        def lin(k, n, gather, s):
+        def parts(k, n, gather, s):
             idx = np.sort(rng.permutation(k)[:r]) if gather else None
-            return device_mx_linear(k, n, r, seed=100 * b + s, salient_idx=idx)
-        lins = {"q_proj": lin(H, H, True, 1), "k_proj": lin(H, H, True, 2), "v_proj": lin(H, H, True, 3),
-                "o_proj": lin(H, H, False, 4), "up_proj": lin(H, F, True, 5), "gate_proj": lin(H, F, True, 6),
-                "down_proj": lin(F, H, False, 7)}
+            return device_mx_parts(k, n, r, seed=100 * b + s, salient_idx=idx)
+        pq, pk, pv = parts(H, H, True, 1), parts(H, H, True, 2), parts(H, H, True, 3)
+        pu, pg = parts(H, F, True, 5), parts(H, F, True, 6)
+        lins = {"o_proj": D.MxLinear(*parts(H, H, False, 4)), "down_proj": D.MxLinear(*parts(F, H, False, 7))}
+        if fused:  # q/k/v and up/gate as one launch each (own salient set per part)
+            lins["qkv_proj"] = D.FusedMxLinear([pq, pk, pv])
+            lins["up_gate_proj"] = D.FusedMxLinear([pu, pg])
+        else:
+            lins.update({"q_proj": D.MxLinear(*pq), "k_proj": D.MxLinear(*pk), "v_proj": D.MxLinear(*pv),
+                         "up_proj": D.MxLinear(*pu), "gate_proj": D.MxLinear(*pg)})
         gains = {"ln1": np.abs(rng.standard_normal(H)) + 0.5, "ln2": np.abs(rng.standard_normal(H)) + 0.5}
         blocks.append(DeviceBlock(lins, gains, hd, fast_attention=True))
     x = outlier_x(M, H).float()
@@ -399,7 +405,8 @@ def llama7b_block_point(M: int, n_blocks: int = 4, r: int = 64) -> dict:
 
     t = time_in_graph(step, None, n=10) / n_blocks
     flops = 2.0 * M * (4 * H * (H + r) + 2 * H * (F + r) + F * (H + r))
-    return {"M": M, "hidden": H, "ffn": F, "r": r, "blocks_in_graph": n_blocks, "block_us": t * 1e3,
+    return {"M": M, "hidden": H, "ffn": F, "r": r, "fused_qkv_up_gate": fused, "blocks_in_graph": n_blocks,
+            "block_us": t * 1e3,
             "tokens_per_s": M / (t * 1e-3), "linear_tflops_equiv": flops / (t * 1e-3) / 1e12}
 
 

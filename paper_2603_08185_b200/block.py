@@ -63,10 +63,17 @@ class DeviceBlock:
 
     def __init__(self, linears: dict, gains: dict, head_dim: int, eps: float = 1e-6, device="cuda",
                  fast_attention: bool = False):
-        missing = [n for n in LINEAR_NAMES if n not in linears]
+        """``linears`` may hold "qkv_proj" (q, k, v) and / or "up_gate_proj" (up, gate) as one
+        ``device.FusedMxLinear`` (one quantizer + one kernel for the parts) instead of the parts."""
+        self.qkv = linears.get("qkv_proj")
+        self.up_gate = linears.get("up_gate_proj")
+        need = [n for n in LINEAR_NAMES
+                if not (self.qkv is not None and n in ("q_proj", "k_proj", "v_proj"))
+                and not (self.up_gate is not None and n in ("up_proj", "gate_proj"))]
+        missing = [n for n in need if n not in linears]
         if missing:
             raise ValidationError(f"block needs linears {missing}")
-        self.lin = {n: linears[n] for n in LINEAR_NAMES}
+        self.lin = {n: linears[n] for n in need}
         self.g1 = torch.as_tensor(np.asarray(gains["ln1"]), dtype=torch.float32, device=device)
         self.g2 = torch.as_tensor(np.asarray(gains["ln2"]), dtype=torch.float32, device=device)
         self.head_dim = int(head_dim)
@@ -81,14 +88,21 @@ class DeviceBlock:
         """x [M, hidden] on the GPU -> block output float32 [M, hidden]."""
         x = x.float()
         h1 = rmsnorm(x, self.g1, self.eps)
-        q = self.lin["q_proj"](h1)
-        k = self.lin["k_proj"](h1)
-        v = self.lin["v_proj"](h1)
+        if self.qkv is not None:
+            q, k, v = (t.contiguous() for t in self.qkv.split(self.qkv(h1)))
+        else:
+            q = self.lin["q_proj"](h1)
+            k = self.lin["k_proj"](h1)
+            v = self.lin["v_proj"](h1)
         attn = attention_mix(q, k, v, self.head_dim, self.fast_attention)
         res1 = x + self.lin["o_proj"](attn.contiguous())  # bf16 + f32 -> f32
         h2 = rmsnorm(res1, self.g2, self.eps)
-        up = self.lin["up_proj"](h2)
-        gate = self.lin["gate_proj"](h2).float()
+        if self.up_gate is not None:
+            up, gate = self.up_gate.split(self.up_gate(h2))
+            gate = gate.float()
+        else:
+            up = self.lin["up_proj"](h2)
+            gate = self.lin["gate_proj"](h2).float()
         mid = torch.nn.functional.silu(gate) * up
         return res1 + self.lin["down_proj"](mid)
 

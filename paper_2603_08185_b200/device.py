@@ -377,12 +377,15 @@ class FusedMxLinear:
     hard-part 6) -- packed as ONE handle over their row-concatenated weights, each keeping its
     own salient set (the reference plans them separately, toymodel.py:267-277; every one takes
     the gather fallback).  The quantizer runs once (its salient buffer holds 128 columns per
-    part) and, with r = 64, for M <= 16 and for M > 128 with 256-row-aligned parts, ONE kernel
-    computes every part (serq_linear_set_segments); other token counts run per-part views of
-    the same weights (serq_linear_view, no copy).  ``parts``: (codes [N_j, K], exps, r_codes
+    part) and, with r = 64, for M <= 16 (and optionally M > 128 with 256-row-aligned parts) ONE
+    kernel computes every part (serq_linear_set_segments); other token counts run per-part views
+    of the same weights (serq_linear_view, no copy).  ``parts``: (codes [N_j, K], exps, r_codes
     [N_j, r], r_exps, salient_idx [r]) per linear, N_j a multiple of 128, equal K and r."""
 
-    def __init__(self, parts, device="cuda"):
+    def __init__(self, parts, device="cuda", prefill_one_kernel: bool = False):
+        """``prefill_one_kernel``: also run M > 128 as ONE CTA-pair launch over all parts (r = 64,
+        256-row-aligned parts); off by default -- per-part launches measured faster in the
+        Llama-2-7B block at M = 2048 (558 vs 597 us per block)."""
         device = torch.device(device)
         if not 1 <= len(parts) <= 4:
             raise ValidationError("fuse 1 to 4 linears")
@@ -419,7 +422,7 @@ class FusedMxLinear:
         aligned = all(b % 256 == 0 for b in self.bounds[1:-1])
         # one kernel: the decode kernel (M <= 16) and the CTA-pair kernel (M > 128) take the gathered
         # salient slice as 32-byte rows, i.e. r = 64
-        self._one_kernel = lambda m: r == 64 and (m <= 16 or (m > 128 and aligned))
+        self._one_kernel = lambda m: r == 64 and (m <= 16 or (prefill_one_kernel and m > 128 and aligned))
 
     def forward(self, x: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
         """Y [M, sum N_j] (bf16): part j's output in columns [bounds[j], bounds[j+1])."""
