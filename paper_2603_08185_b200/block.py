@@ -89,7 +89,7 @@ class DeviceBlock:
         x = x.float()
         h1 = rmsnorm(x, self.g1, self.eps)
         if self.qkv is not None:
-            q, k, v = (t.contiguous() for t in self.qkv.split(self.qkv(h1)))
+            q, k, v = (t.contiguous() for t in self.qkv.forward_parts(h1))
         else:
             q = self.lin["q_proj"](h1)
             k = self.lin["k_proj"](h1)
@@ -98,7 +98,7 @@ class DeviceBlock:
         res1 = x + self.lin["o_proj"](attn.contiguous())  # bf16 + f32 -> f32
         h2 = rmsnorm(res1, self.g2, self.eps)
         if self.up_gate is not None:
-            up, gate = self.up_gate.split(self.up_gate(h2))
+            up, gate = self.up_gate.forward_parts(h2)
             gate = gate.float()
         else:
             up = self.lin["up_proj"](h2)

@@ -437,6 +437,13 @@ class FusedMxLinear:
 
     __call__ = forward
 
+    def forward_parts(self, x: torch.Tensor) -> list:
+        """Each part's output as its own tensor: column views of one buffer when one kernel ran
+        (small M), separate contiguous buffers from the per-part launches otherwise."""
+        if self._one_kernel(x.shape[0]):
+            return self.split(self.forward(x))
+        return [v.forward(x) for v in self.views]
+
     def split(self, y: torch.Tensor) -> list:
         return [y[:, self.bounds[j]:self.bounds[j + 1]] for j in range(len(self.n_parts))]
 
