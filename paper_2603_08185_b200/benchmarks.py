@@ -524,16 +524,19 @@ def c5_tp_point(world: int = 1, rank: int = 0, M: int = 8192, r: int = 128, grou
         b.synchronize()
         return a.elapsed_time(b) / n, graph
 
-    be = tp.DeviceBackend(lins, group)
+    coll = world > 1  # a tp = 1 reference inside a multi-rank job must not issue collectives
+    be = tp.DeviceBackend(lins, group, collectives=coll)
     blk = tp.PipelinedTPBlock(specs, be, chunks=chunks)
     step_ms, graph = timed_graph(lambda: blk.forward(x, feeds), steps)
     launches = be.launches_per_forward
-    be1 = tp.DeviceBackend(lins, group)
+    be1 = tp.DeviceBackend(lins, group, collectives=coll)
     blk1 = tp.PipelinedTPBlock(specs, be1, chunks=1)
     serial_ms, _ = timed_graph(lambda: blk1.forward(x, feeds), max(3, steps // 2))
     outs = blk.forward(x, feeds)
-    ar_ms, _ = timed_graph(lambda: (tp.allreduce_sum_(outs["o_proj"], group), tp.allreduce_sum_(outs["down_proj"], group)),
-                           max(3, steps // 2))
+    ar_ms = 0.0
+    if coll:
+        ar_ms, _ = timed_graph(lambda: (tp.allreduce_sum_(outs["o_proj"], group),
+                                        tp.allreduce_sum_(outs["down_proj"], group)), max(3, steps // 2))
     flops = sum(2.0 * M * s.n * (s.k + r) for s in specs)  # the full block (padding of per-rank salient sets not counted)
     out = {"M": M, "tp": world, "r": r, "chunks": len(tp.chunk_bounds(M, chunks)), "graph": graph,
            "step_ms": step_ms, "serial_ms": serial_ms, "allreduce_ms": ar_ms, "block_tflops": flops / (step_ms * 1e-3) / 1e12,

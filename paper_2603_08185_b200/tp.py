@@ -272,12 +272,15 @@ class DeviceBackend:
     N is this rank's shard), per-(linear, chunk) activation buffers, NCCL all-reduces on a
     communication stream ordered by events."""
 
-    def __init__(self, lins: dict, group=None, force_collective: bool = False):
+    def __init__(self, lins: dict, group=None, force_collective: bool = False, collectives: bool = True):
+        """``collectives=False``: a single-GPU (tp = 1) run inside a multi-rank job -- no
+        collective may be issued from one rank alone."""
         import torch
 
         self.lins = lins
         self.group = group
         self.force = force_collective
+        self.collectives = collectives
         self.comm = torch.cuda.Stream()
         self._outs = {}
         self._acts = {}
@@ -338,7 +341,8 @@ class DeviceBackend:
         ready.record(torch.cuda.current_stream())
         self.comm.wait_event(ready)
         with torch.cuda.stream(self.comm):
-            allreduce_sum_(y_rows, self.group, self.force)
+            if self.collectives:
+                allreduce_sum_(y_rows, self.group, self.force)
             done.record(self.comm)
 
     def wait(self, name, c):
