@@ -395,7 +395,12 @@ static int act_quant_int_impl(const void* x, int dtype, int64_t M, int64_t K, in
     const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
     const dim3 gq{unsigned(M)};
     const bool warp_rows = SERQ_DBG(g_debug_flags, (1 << 21)) != 0;  // diagnostics: one warp per row
-    const int tpr = warp_rows ? 32 : 64;
+    // few rows (fewer than ~4 per SM): wider rows put more warps in flight per SM
+#ifndef SERQ_INTQ_WIDE_ROWS
+#define SERQ_INTQ_WIDE_ROWS 4
+#endif
+    const bool wide = !warp_rows && M < int64_t(SERQ_INTQ_WIDE_ROWS) * sm_count() && K >= 2048;
+    const int tpr = warp_rows ? 32 : (wide ? 256 : 64);
     const int cpt = int(cdiv(K / 8, tpr));
 #define SERQ_INTQ(P, C)                                                                                         \
   CK(launch_pdl(int_quant_bf16_kernel<P, C, P>, gq, dim3(P), 0, st, xb, int(M), int(K), ldx, bits, symmetric, codes, \
@@ -405,6 +410,10 @@ static int act_quant_int_impl(const void* x, int dtype, int64_t M, int64_t K, in
       else if (cpt <= 8) SERQ_INTQ(32, 8);
       else if (cpt <= 16) SERQ_INTQ(32, 16);
       else SERQ_INTQ(32, 32);
+    } else if (wide) {
+      if (cpt <= 1) SERQ_INTQ(256, 1);
+      else if (cpt <= 2) SERQ_INTQ(256, 2);
+      else SERQ_INTQ(256, 4);
     } else {
       if (cpt <= 2) SERQ_INTQ(64, 2);
       else if (cpt <= 4) SERQ_INTQ(64, 4);
