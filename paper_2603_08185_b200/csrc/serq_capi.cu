@@ -395,12 +395,11 @@ static int act_quant_int_impl(const void* x, int dtype, int64_t M, int64_t K, in
     const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
     const dim3 gq{unsigned(M)};
     const bool warp_rows = SERQ_DBG(g_debug_flags, (1 << 21)) != 0;  // diagnostics: one warp per row
-    // few rows (fewer than ~4 per SM): wider rows put more warps in flight per SM
-#ifndef SERQ_INTQ_WIDE_ROWS
-#define SERQ_INTQ_WIDE_ROWS 4
-#endif
-    const bool wide = !warp_rows && M < int64_t(SERQ_INTQ_WIDE_ROWS) * sm_count() && K >= 2048;
-    const int tpr = warp_rows ? 32 : (wide ? 256 : 64);
+    // threads per row by rows per SM: wider rows put more warps in flight when rows are few
+    // (tools/probes/intq_grid_probe.py: 512 x 4096 5.95 / 4.84 / 4.37 us with 64 / 128 / 256
+    // threads, 2048 x 4096 10.0 / 9.1 / 10.2 us)
+    const int64_t rows_per_sm = M / sm_count();
+    const int tpr = warp_rows ? 32 : (K < 2048 ? 64 : rows_per_sm < 4 ? 256 : rows_per_sm < 16 ? 128 : 64);
     const int cpt = int(cdiv(K / 8, tpr));
 #define SERQ_INTQ(P, C)                                                                                         \
   CK(launch_pdl(int_quant_bf16_kernel<P, C, P>, gq, dim3(P), 0, st, xb, int(M), int(K), ldx, bits, symmetric, codes, \
@@ -410,10 +409,13 @@ static int act_quant_int_impl(const void* x, int dtype, int64_t M, int64_t K, in
       else if (cpt <= 8) SERQ_INTQ(32, 8);
       else if (cpt <= 16) SERQ_INTQ(32, 16);
       else SERQ_INTQ(32, 32);
-    } else if (wide) {
-      if (cpt <= 1) SERQ_INTQ(256, 1);
-      else if (cpt <= 2) SERQ_INTQ(256, 2);
+    } else if (tpr == 256) {
+      if (cpt <= 2) SERQ_INTQ(256, 2);
       else SERQ_INTQ(256, 4);
+    } else if (tpr == 128) {
+      if (cpt <= 2) SERQ_INTQ(128, 2);
+      else if (cpt <= 4) SERQ_INTQ(128, 4);
+      else SERQ_INTQ(128, 8);
     } else {
       if (cpt <= 2) SERQ_INTQ(64, 2);
       else if (cpt <= 4) SERQ_INTQ(64, 4);
