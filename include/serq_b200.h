@@ -129,6 +129,18 @@ int serq_rmsnorm_quant_mx_gather(const void* x, int dtype, int64_t M, int64_t K,
                                  const float* gain32, double eps, const int32_t* gather_idx, int r, uint8_t* codes,
                                  uint8_t* sf, uint8_t* xs_codes, uint8_t* xs_sf, serq_stream_t stream);
 
+/* Producer fusion for the integer formats: rmsnorm(x, gain) (saliency.py:194-196) quantized per
+ * token (quantcore.py:108-137) in one kernel, in float64 exactly as the reference -- including
+ * NumPy's pairwise summation order for the row mean of squares, replayed from the row length --
+ * so codes, scales and zero points equal quantize_*(rmsnorm(x)) bit for bit.  x bf16 / f32 [M, K]
+ * (K <= 8192), gain f64 [K] and its f32 rounding gain32 (16-byte aligned; the fast kernel's f32
+ * pass, exactness kept by an error bound -- NULL selects the all-f64 kernel); outputs and xs
+ * as serq_act_quant_int. */
+int serq_rmsnorm_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, const double* gain,
+                           const float* gain32, double eps, int bits, int symmetric, int8_t* codes, double* scale64,
+                           float* scale32, int32_t* zp, const int32_t* salient_idx, int r, void* xs_out, int xs_kind,
+                           serq_stream_t stream);
+
 /* The reference's packed MX file body (mxfmt.py:228-251, after the 28-byte
  * header; bundleio.py load path): rows x cols/32 records of 17 bytes (exponent
  * byte e+127, 16 nibble bytes, element 2i low) already in device memory ->

@@ -368,6 +368,30 @@ def rmsnorm_quant_point(M: int, K: int, hbm_peak_gbs: float, n_steps: int = 16) 
             "unfused_extra_bytes": 4 * M * K}
 
 
+def rmsnorm_int_quant_point(M: int, K: int, bits: int, symmetric: bool, hbm_peak_gbs: float,
+                            n_steps: int = 16) -> dict:
+    """Producer fusion for the integer formats: rmsnorm(x, gain) -> per-token INT codes with the
+    reference's f64 scales (serq_rmsnorm_quant_int) vs the plain K1-INT quantizer on the same
+    shape, and vs torch RMSNorm to bf16 + K1-INT (whose scales are not the reference's).  Bytes
+    per launch: 2MK in, MK codes + 12M (f64 + f32 scales) [+ 4M zero points] out."""
+    xs = [outlier_x(M, K, seed=i) for i in range(8)]
+    gain = (torch.rand(K, device="cuda", dtype=torch.float64) + 0.5)
+    t_f = time_steps(lambda i: D.rmsnorm_quantize_int(xs[i % 8], gain, 1e-6, bits, symmetric), n_steps)
+    t_q = time_steps(lambda i: D.quantize_int(xs[i % 8], bits, symmetric), n_steps)
+    g16 = gain.to(torch.bfloat16)
+    hs = [torch.empty_like(x) for x in xs]
+
+    def unfused(i):
+        hs[i % 8].copy_(torch.nn.functional.rms_norm(xs[i % 8], (K,), g16, 1e-6))
+        D.quantize_int(hs[i % 8], bits, symmetric)
+
+    t_u = time_steps(unfused, n_steps)
+    byts = 2 * M * K + M * K + 12 * M + (0 if symmetric else 4 * M)
+    return {"M": M, "K": K, "bits": bits, "symmetric": symmetric, "rmsnorm_quant_us": t_f * 1e3,
+            "quant_only_us": t_q * 1e3, "unfused_torch_rmsnorm_then_quant_us": t_u * 1e3,
+            "rmsnorm_quant_hbm_frac": byts / (t_f * 1e-3) / 1e9 / hbm_peak_gbs}
+
+
 def llama7b_block_point(M: int, n_blocks: int = 4, r: int = 64, fused: bool = False) -> dict:
     """Whole Llama-2-7B-shaped decoder block on the device (block.DeviceBlock: SERQ MXFP4
     linears + f32 RMSNorm / attention / SiLU), ``n_blocks`` distinct blocks chained in ONE

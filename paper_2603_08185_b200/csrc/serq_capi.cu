@@ -678,6 +678,120 @@ int serq_rmsnorm_quant_mx_gather(const void* x, int dtype, int64_t M, int64_t K,
   return SERQ_OK;
 }
 
+// NumPy's pairwise summation tree for K elements (numpy pairwise_sum: leaves of <= 128, split
+// at n/2 rounded down to a multiple of 8): leaves left to right, internal nodes ordered by height
+struct PwBuild {
+  int nleaf = 0, nnode = 0;
+  int16_t start[64], len[64];
+  int ca[64], cb[64], height[64];
+};
+
+// returns the value id of the subtree over [off, off + n): a leaf index, or 64 + node index
+static int pw_rec(int64_t off, int64_t n, PwBuild& b, int& h) {
+  if (n <= 128) {
+    if (b.nleaf >= 64) return -1;
+    b.start[b.nleaf] = int16_t(off);
+    b.len[b.nleaf] = int16_t(n);
+    h = 0;
+    return b.nleaf++;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  int hl = 0, hr = 0;
+  const int l = pw_rec(off, n2, b, hl);
+  const int r = l < 0 ? -1 : pw_rec(off + n2, n - n2, b, hr);
+  if (r < 0 || b.nnode >= 63) return -1;
+  const int j = b.nnode++;
+  b.ca[j] = l;
+  b.cb[j] = r;
+  h = std::max(hl, hr) + 1;
+  b.height[j] = h;
+  return 64 + j;
+}
+
+static bool rms_tree(int64_t K, RmsPairwise& t) {
+  PwBuild b;
+  int h = 0;
+  if (pw_rec(0, K, b, h) < 0 || h > 8) return false;
+  t = RmsPairwise{};
+  t.nleaf = b.nleaf;
+  t.nnode = b.nnode;
+  t.nlevel = h;
+  t.perfect = b.nleaf == (1 << h) && b.nleaf <= 64;  // all 2^h leaves at depth h
+  for (int i = 0; i < b.nleaf; ++i) {
+    t.start[i] = b.start[i];
+    t.len[i] = b.len[i];
+  }
+  int slot[64], n = 0;
+  for (int hh = 1; hh <= h; ++hh) {
+    for (int j = 0; j < b.nnode; ++j)
+      if (b.height[j] == hh) slot[j] = n++;
+    t.level_end[hh - 1] = uint8_t(n);
+  }
+  auto vid = [&](int id) { return uint8_t(id < 64 ? id : b.nleaf + slot[id - 64]); };
+  for (int j = 0; j < b.nnode; ++j) {
+    t.a[slot[j]] = vid(b.ca[j]);
+    t.b[slot[j]] = vid(b.cb[j]);
+  }
+  return true;
+}
+
+int serq_rmsnorm_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, const double* gain,
+                           const float* gain32, double eps, int bits, int symmetric, int8_t* codes, double* scale64,
+                           float* scale32, int32_t* zp, const int32_t* salient_idx, int r, void* xs_out, int xs_kind,
+                           serq_stream_t stream) {
+  g_launches = 0;
+  if (M <= 0 || K <= 0) return fail(SERQ_EINVAL, "x must be non-empty (M=%lld, K=%lld)", (long long)M, (long long)K);
+  if (K > 8192) return fail(SERQ_EINVAL, "fused RMSNorm quantizer supports rows up to 8192 elements");
+  if (ldx < K) return fail(SERQ_EINVAL, "ldx < K");
+  if (!gain) return fail(SERQ_EINVAL, "gain is NULL");
+  if (!(eps >= 0.0)) return fail(SERQ_EINVAL, "eps must be >= 0");
+  if (bits < 2 || bits > 8) return fail(SERQ_EINVAL, "bits must be in [2, 8], got %d", bits);
+  if (!symmetric && !zp) return fail(SERQ_EINVAL, "asymmetric quantization needs a zero-point buffer");
+  if (xs_kind && (r <= 0 || r > K || !xs_out)) return fail(SERQ_EINVAL, "salient slice needs 0 < r <= K and xs_out");
+  if (dtype != SERQ_BF16 && dtype != SERQ_F32) return fail(SERQ_EINVAL, "rmsnorm input must be bf16 or f32");
+  RmsPairwise tree{};
+  if (!rms_tree(K, tree)) return fail(SERQ_EINVAL, "pairwise tree too large");
+  cudaStream_t st = S(stream);
+  const int64_t esz = dtype == SERQ_BF16 ? 2 : 4;
+  const bool fast = gain32 && !(reinterpret_cast<uintptr_t>(gain32) & 15) && K % 8 == 0 &&
+                    !(reinterpret_cast<uintptr_t>(x) & 15) && (ldx * esz) % 16 == 0 && !(reinterpret_cast<uintptr_t>(codes) & 7);
+  if (fast) {
+    // threads per row and 8-element chunks per thread (K <= kTpr * kChunks * 8): one row per
+    // CTA above 1024 elements (small per-thread state, more CTAs resident per SM)
+    const int tpr = K <= 1024 ? 128 : 256;
+    const int chunks = K <= 2048 ? 1 : K <= 4096 ? 2 : 4;
+    const dim3 grid{unsigned(cdiv(M, 256 / tpr))}, blk{256};
+#define RMSI_LAUNCH(T, P, C)                                                                                           \
+  CK(launch_pdl(rmsnorm_int_quant_fast_kernel<T, P, C>, grid, blk, 0, st, static_cast<const T*>(x), int(M), int(K), ldx, \
+                gain, gain32, eps, tree, bits, symmetric, codes, scale64, scale32, zp, salient_idx, r, xs_out, xs_kind))
+    if (dtype == SERQ_BF16) {
+      if (tpr == 128) RMSI_LAUNCH(__nv_bfloat16, 128, 1);
+      else if (chunks == 1) RMSI_LAUNCH(__nv_bfloat16, 256, 1);
+      else if (chunks == 2) RMSI_LAUNCH(__nv_bfloat16, 256, 2);
+      else RMSI_LAUNCH(__nv_bfloat16, 256, 4);
+    } else {
+      if (tpr == 128) RMSI_LAUNCH(float, 128, 1);
+      else if (chunks == 1) RMSI_LAUNCH(float, 256, 1);
+      else if (chunks == 2) RMSI_LAUNCH(float, 256, 2);
+      else RMSI_LAUNCH(float, 256, 4);
+    }
+#undef RMSI_LAUNCH
+    LAUNCH_CHECK("rmsnorm_int_quant_fast_kernel");
+    return SERQ_OK;
+  }
+  // any other layout (K % 8 != 0, unaligned rows, no f32 gain): the all-f64 kernel
+  const dim3 grid{unsigned(M)}, blk{256};
+  if (dtype == SERQ_BF16)
+    CK(launch_pdl(rmsnorm_int_quant_kernel<__nv_bfloat16>, grid, blk, 0, st, static_cast<const __nv_bfloat16*>(x), M, K,
+                  ldx, gain, eps, tree, bits, symmetric, codes, scale64, scale32, zp, salient_idx, r, xs_out, xs_kind));
+  else
+    CK(launch_pdl(rmsnorm_int_quant_kernel<float>, grid, blk, 0, st, static_cast<const float*>(x), M, K, ldx, gain, eps,
+                  tree, bits, symmetric, codes, scale64, scale32, zp, salient_idx, r, xs_out, xs_kind));
+  LAUNCH_CHECK("rmsnorm_int_quant_kernel");
+  return SERQ_OK;
+}
+
 int serq_mx_container_decode(const uint8_t* body, int64_t rows, int64_t cols, uint8_t* codes, int32_t* exps,
                              serq_stream_t stream) {
   g_launches = 0;

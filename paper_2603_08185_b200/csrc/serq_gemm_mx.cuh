@@ -124,7 +124,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t smem_base = smem_u32(smem);
     constexpr uint32_t id0 = idesc_mxf4(kBM, kBN), id1 = id0 | (2u << 4) | (2u << 29);  // sf_id 0 / 2
     uint32_t g = 0;
-    int u_tile = 0, u = 0;  // position of the NEXT unit to wait for
     auto wait_unit = [&](uint32_t gg, int uu) {
       // stages of unit uu (within a tile) starting at global stage gg
       mbar_wait(&full[gg & (kPStages - 1)], (gg / kPStages) & 1);
@@ -216,8 +215,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         g = gn;
       }
     }
-    (void)u_tile;
-    (void)u;
   } else {
     // ------------------------------------------------------------ epilogue
     const uint32_t q = warp & 3;

@@ -436,6 +436,13 @@ struct Raw8<__nv_bfloat16> {
   __device__ __forceinline__ float f(int i) const {
     return __uint_as_float((i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16));
   }
+  __device__ __forceinline__ void store(__nv_bfloat16* p) const {
+    *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  __device__ __forceinline__ void load_shared(const __nv_bfloat16* p) {
+    const uint4 r = *reinterpret_cast<const uint4*>(p);
+    w[0] = r.x; w[1] = r.y; w[2] = r.z; w[3] = r.w;
+  }
 };
 template <>
 struct Raw8<float> {
@@ -446,6 +453,14 @@ struct Raw8<float> {
     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
   }
   __device__ __forceinline__ float f(int i) const { return v[i]; }
+  __device__ __forceinline__ void store(float* p) const {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+  __device__ __forceinline__ void load_shared(const float* p) {
+    const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
 };
 
 template <typename T, int kTpr, int kChunks>
@@ -709,6 +724,425 @@ __device__ __forceinline__ double rint_quot(T xv, double s, float inv32, double 
       if (fabsf(fr - 0.5f) > margin) return double(fr > 0.5f ? fl + 1.f : fl);
     }
     return rint(double(xf) / s);
+  }
+}
+
+// ---------------------------------------------------------------- RMSNorm -> INT producer
+// The reference's row mean of squares is NumPy's pairwise float64 sum (np.mean over the last,
+// contiguous axis: pairwise_sum with 128-element leaves, eight strided accumulators per leaf
+// combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), the leaf tail added in order, leaves combined
+// along the recursion that halves n at a multiple of 8).  The host replays that recursion for K
+// once and passes the leaves and the internal nodes ordered by height, so every row's sum has
+// the reference's exact rounding sequence and a warp can evaluate one height level at a time.
+struct RmsPairwise {
+  int nleaf, nnode, nlevel, perfect;  // perfect: 2^d leaves, all at depth d
+  int16_t start[64], len[64];
+  uint8_t a[64], b[64];  // node j (value slot nleaf + j) = val[a[j]] + val[b[j]]
+  uint8_t level_end[8];  // nodes of height h + 1: [level_end[h - 1], level_end[h])
+};
+
+// Evaluate the internal nodes over val[0 .. nleaf) (the leaf sums); one full warp.
+__device__ __forceinline__ double rms_tree_eval(const RmsPairwise& tr, double* val, int lane) {
+  int j0 = 0;
+  for (int h = 0; h < tr.nlevel; ++h) {
+    const int j1 = tr.level_end[h];
+    for (int j = j0 + lane; j < j1; j += 32) val[tr.nleaf + j] = val[tr.a[j]] + val[tr.b[j]];
+    __syncwarp();
+    j0 = j1;
+  }
+  return val[tr.nnode ? tr.nleaf + tr.nnode - 1 : 0];
+}
+
+// y = x / sqrt(mean(x^2) + eps) * gain in float64 exactly as saliency.py:194-196, then the
+// per-token quantizer on y exactly as quantize_asymmetric / quantize_symmetric
+// (quantcore.py:108-137): codes, f64 scales and zero points bit-identical to the reference's.
+// One 256-thread CTA per row, every operation in f64 -- the kernel for layouts the fast one
+// below does not serve (K % 8 != 0, unaligned rows) and its cross-check.
+template <typename T>
+__global__ void __launch_bounds__(256) rmsnorm_int_quant_kernel(const T* __restrict__ x, int64_t M, int64_t K,
+                                                                int64_t ldx, const double* __restrict__ gain,
+                                                                double eps, const RmsPairwise tree, int bits,
+                                                                int symmetric, int8_t* __restrict__ codes,
+                                                                double* __restrict__ scale64,
+                                                                float* __restrict__ scale32, int32_t* __restrict__ zp_out,
+                                                                const int32_t* __restrict__ sidx, int r,
+                                                                void* __restrict__ xs_out, int xs_kind) {
+  const int64_t row = blockIdx.x;
+  const T* xr = x + row * ldx;
+  __shared__ double val[128];
+  __shared__ double red_lo[8], red_hi[8];
+  __shared__ double s_rms, s_scale;
+  __shared__ int s_zp;
+  pdl_launch_dependents();
+  pdl_wait();
+  // pass 1: the leaves, an 8-thread group per leaf (thread j: accumulator r_j)
+  const int grp = int(threadIdx.x) >> 3, j = int(threadIdx.x) & 7;
+  for (int lf = grp; lf < tree.nleaf; lf += int(blockDim.x) >> 3) {
+    const int st = tree.start[lf], n = tree.len[lf];
+    double acc = 0.0;
+    if (n >= 8) {
+      const int body = n - (n % 8);
+      for (int i = j; i < body; i += 8) {
+        const double v = load_as_f64(xr + st + i);
+        acc = fma(v, v, acc);  // x*x is exact in f64 for bf16 / f32 x: rounds as acc + x*x
+      }
+      const unsigned gmask = 0xFFu << (threadIdx.x & 24);  // this leaf's 8 lanes only
+      acc += __shfl_xor_sync(gmask, acc, 1);  // (r0 + r1), (r2 + r3), ...
+      acc += __shfl_xor_sync(gmask, acc, 2);
+      acc += __shfl_xor_sync(gmask, acc, 4);
+      if (j == 0)
+        for (int i = body; i < n; ++i) {
+          const double v = load_as_f64(xr + st + i);
+          acc = fma(v, v, acc);
+        }
+    } else if (j == 0) {
+      for (int i = 0; i < n; ++i) {
+        const double v = load_as_f64(xr + st + i);
+        acc = fma(v, v, acc);
+      }
+    }
+    if (j == 0) val[lf] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const double sum = rms_tree_eval(tree, val, threadIdx.x);
+    if (threadIdx.x == 0) s_rms = sqrt(sum / double(K) + eps);
+  }
+  __syncthreads();
+  const double rms = s_rms;
+  // pass 2: y = x / rms * gain (f64, two roundings as the reference), row min / max
+  double lo = INFINITY, hi = -INFINITY;
+  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+    const double y = load_as_f64(xr + k) / rms * gain[k];
+    lo = fmin(lo, y);
+    hi = fmax(hi, y);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffff, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffff, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red_lo[threadIdx.x >> 5] = lo;
+    red_hi[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+      lo = fmin(lo, red_lo[w]);
+      hi = fmax(hi, red_hi[w]);
+    }
+    double sc;
+    int zp = 0;
+    if (symmetric) {
+      sc = fmax(fabs(lo), fabs(hi)) / double((1 << (bits - 1)) - 1);
+      if (sc == 0.0) sc = 1.0;
+    } else {
+      sc = (hi - lo) / double((1 << bits) - 1);
+      if (sc == 0.0) sc = 1.0;
+      zp = int(rint(-lo / sc));
+    }
+    s_scale = sc;
+    s_zp = zp;
+    scale64[row] = sc;
+    scale32[row] = float(sc);
+    if (zp_out) zp_out[row] = zp;
+  }
+  __syncthreads();
+  const double sc = s_scale;
+  const int zp = s_zp;
+  const int qmax = symmetric ? (1 << (bits - 1)) - 1 : (1 << bits) - 1;
+  const int qmin = symmetric ? -qmax : 0;
+  // pass 3: codes of y (recomputed: the same f64 operations give the same value)
+  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+    const double y = load_as_f64(xr + k) / rms * gain[k];
+    double q = rint(y / sc) + double(zp);
+    q = fmin(fmax(q, double(qmin)), double(qmax));
+    codes[row * K + k] = int8_t(int(q));
+  }
+  if (xs_kind != 0) {
+    __syncthreads();
+    for (int jj = threadIdx.x; jj < r; jj += blockDim.x) {
+      const int col = sidx ? sidx[jj] : jj;
+      const int c = symmetric ? int(codes[row * K + col]) : int(uint8_t(codes[row * K + col]));
+      if (xs_kind == 1)
+        reinterpret_cast<__nv_bfloat16*>(xs_out)[row * r + jj] = __int2bfloat16_rn(c - zp);
+      else
+        reinterpret_cast<int8_t*>(xs_out)[row * r + jj] = int8_t(c);
+    }
+  }
+}
+
+// The same producer at HBM speed for 16-B aligned rows with K % 8 == 0 (every pairwise leaf is
+// then a whole number of 8-element vectors).  kRows = 256 / kTpr rows per CTA, each row's
+// elements in its threads' registers (read once) and staged in shared memory for the leaf sums:
+// one thread per leaf holds the eight accumulators r_0..r_7 of pairwise_sum and walks the leaf
+// in 16-B vectors (the staging pads 8 elements per 128 so the leaves a warp reads sit in
+// different banks).  Only the row sum is float64 per element.  Everything else runs on
+// z = x * g32 in f32 -- y = z / rms up to rounding, so the extremes of y are those of z and no
+// pass waits for the row sum -- with a proven error bound, and the reference's f64 operations
+// are evaluated only where the bound cannot decide:
+//  * the row's min / max (max |y|): z32 is within 2 * 2^-24 relative (g, x * g roundings) plus
+//    2^-149 absolute of x * g, so the reference's extreme element is among those within 2^-20
+//    relative + 2^-100 of the f32 extreme; those few (listed in shared memory) take the
+//    reference's (x / rms) * g and the f64 extreme of them is the reference's;
+//  * codes: t = z32 * f32(1 / (rms s)) is within 4 * 2^-24 relative + 2^-69 absolute of the
+//    reference's y / s; rint(t) (round-half-even by the 1.5 * 2^23 add, the zero point folded
+//    in) is decided in f32 unless t lies within |t| 2^-20 + 2^-25 of a .5 tie, where the element
+//    takes rint((x / rms) * g / s) in f64;
+//  * rows outside those premises (|x| > 2^20, |z| > 2^100, more than kMaxCand candidates,
+//    1 / (rms s) outside [2^-120, 2^80]) run every element in the f64 reference operations.
+template <typename T, int kTpr, int kChunks>
+__global__ void __launch_bounds__(256) rmsnorm_int_quant_fast_kernel(
+    const T* __restrict__ x, int M, int K, int64_t ldx, const double* __restrict__ gain,
+    const float* __restrict__ gain32, double eps, const RmsPairwise tree, int bits, int symmetric,
+    int8_t* __restrict__ codes, double* __restrict__ scale64, float* __restrict__ scale32, int32_t* __restrict__ zp_out,
+    const int32_t* __restrict__ sidx, int r, void* __restrict__ xs_out, int xs_kind) {
+  constexpr int kRows = 256 / kTpr, kWarps = kTpr / 32, kRowElems = kTpr * kChunks * 8;
+  constexpr int kRowSmem = kRowElems + kRowElems / 16;  // + 8 elements per 128
+  constexpr int kMaxCand = 64;
+  static_assert(kChunks * 8 <= 32, "one mask bit per element");
+  __shared__ alignas(16) T srow[kRows][kRowSmem];
+  __shared__ double val[kRows][128];
+  __shared__ float red_f[kRows][kWarps][3];
+  __shared__ double red_d[kRows][kWarps][2];
+  __shared__ int16_t cand_idx[kRows][kMaxCand];
+  __shared__ int n_cand[kRows];
+  __shared__ double s_rms[kRows], s_scale[kRows];
+  __shared__ float s_c32[kRows];
+  __shared__ int s_zp[kRows];
+  pdl_launch_dependents();
+  pdl_wait();
+  const int rl = threadIdx.x / kTpr, t = threadIdx.x % kTpr, wr = t >> 5, lane = threadIdx.x & 31;
+  const int64_t row = int64_t(blockIdx.x) * kRows + rl;
+  const bool row_ok = row < M;
+  const T* xr = x + (row_ok ? row : 0) * ldx;
+  T* sr = srow[rl];
+  auto spos = [](int c) { return c + ((c >> 7) << 3); };
+  auto elem = [&](int k) { return (k >> 3) * (kTpr * 8) + t * 8 + (k & 7); };  // mask bit -> column
+  Raw8<T> v[kChunks];
+#pragma unroll
+  for (int it = 0; it < kChunks; ++it) {
+    const int c = it * (kTpr * 8) + t * 8;
+    v[it].load(xr + c, row_ok && c < K);
+    v[it].store(sr + spos(c));
+  }
+  if (t == 0) n_cand[rl] = 0;
+  // ---- z = x * g32 and the row's f32 extremes (independent of the row sum)
+  float z[kChunks][8];
+  float hi = -INFINITY, lo = INFINITY, xmax = 0.f;
+#pragma unroll
+  for (int it = 0; it < kChunks; ++it) {
+    const int c = it * (kTpr * 8) + t * 8;
+    // elements outside the matrix read x = 0, g = NaN: z = NaN, which fmaxf / fminf ignore
+    float4 g0 = make_float4(NAN, NAN, NAN, NAN), g1 = g0;
+    if (row_ok && c < K) {
+      g0 = __ldg(reinterpret_cast<const float4*>(gain32 + c));
+      g1 = __ldg(reinterpret_cast<const float4*>(gain32 + c) + 1);
+    }
+    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float xf = v[it].f(i);
+      z[it][i] = xf * g[i];
+      hi = fmaxf(hi, z[it][i]);
+      lo = fminf(lo, z[it][i]);
+      xmax = fmaxf(xmax, fabsf(xf));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffff, hi, o));
+    lo = fminf(lo, __shfl_xor_sync(0xffffffff, lo, o));
+    xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffff, xmax, o));
+  }
+  if (lane == 0) {
+    red_f[rl][wr][0] = hi;
+    red_f[rl][wr][1] = lo;
+    red_f[rl][wr][2] = xmax;
+  }
+  __syncthreads();
+  // ---- the reference's pairwise float64 sum of squares: four threads per leaf, thread q
+  // holding accumulators r_2q, r_2q+1 (spreads the f32 -> f64 conversions over every warp)
+  if (t < 4 * tree.nleaf) {
+    const int lf = t >> 2, q = t & 3;
+    const int st = tree.start[lf], n = tree.len[lf];
+    double a0 = 0.0, a1 = 0.0;
+    auto step = [&](const T* p) {
+      double d0, d1;
+      if constexpr (In<T>::kId == 0) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(p);
+        d0 = __uint_as_float(w << 16);
+        d1 = __uint_as_float(w & 0xFFFF0000u);
+      } else {
+        const float2 f = *reinterpret_cast<const float2*>(p);
+        d0 = f.x;
+        d1 = f.y;
+      }
+      a0 = fma(d0, d0, a0);  // x*x exact in f64: rounds as acc + x*x
+      a1 = fma(d1, d1, a1);
+    };
+    // a leaf (<= 128 elements, starting at a multiple of 8) crosses at most one padded boundary
+    const int first = min(n, 128 - (st & 127));
+    const T* p = sr + spos(st) + 2 * q;
+    int i = 0;
+    for (; i < first; i += 8, p += 8) step(p);
+    p += 8;
+    for (; i < n; i += 8, p += 8) step(p);
+    double pr = a0 + a1;  // (r0 + r1), (r2 + r3), ...
+    const unsigned gmask = 0xFu << (lane & 28);
+    pr += __shfl_xor_sync(gmask, pr, 1);  // ((r0 + r1) + (r2 + r3)), ((r4 + r5) + (r6 + r7))
+    pr += __shfl_xor_sync(gmask, pr, 2);
+    if (q == 0) val[rl][lf] = pr;
+  }
+  // ---- candidates for the extremes (while the leaf threads sum)
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    hi = fmaxf(hi, red_f[rl][w][0]);
+    lo = fminf(lo, red_f[rl][w][1]);
+    xmax = fmaxf(xmax, red_f[rl][w][2]);
+  }
+  bool slow = !(xmax <= 0x1p20f) || !(fmaxf(fabsf(hi), fabsf(lo)) <= 0x1p100f);  // also NaN
+  if (!slow && row_ok) {
+    const float amax32 = fmaxf(fabsf(hi), fabsf(lo));
+    const float cut_hi = symmetric ? amax32 - (amax32 * 0x1p-20f + 0x1p-100f) : hi - (fabsf(hi) * 0x1p-20f + 0x1p-100f);
+    const float cut_lo = lo + (fabsf(lo) * 0x1p-20f + 0x1p-100f);
+#pragma unroll
+    for (int it = 0; it < kChunks; ++it) {
+      if (it * (kTpr * 8) + t * 8 >= K) break;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float zv = z[it][i];
+        if (symmetric ? fabsf(zv) >= cut_hi : (zv >= cut_hi || zv <= cut_lo)) {
+          const int j = atomicAdd(&n_cand[rl], 1);
+          if (j < kMaxCand) cand_idx[rl][j] = int16_t(it * (kTpr * 8) + t * 8 + i);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (wr == 0) {
+    double sum;
+    if (tree.perfect) {  // a perfect binary tree over 2^d leaves: the warp butterfly pairs alike
+      sum = lane < tree.nleaf ? val[rl][lane] : 0.0;
+      for (int o = 1; o < min(tree.nleaf, 32); o <<= 1) sum += __shfl_xor_sync(0xffffffff, sum, o);
+      if (tree.nleaf == 64) {  // root = (leaves 0..31) + (leaves 32..63)
+        double u = val[rl][32 + lane];
+        for (int o = 1; o < 32; o <<= 1) u += __shfl_xor_sync(0xffffffff, u, o);
+        sum += u;
+      }
+    } else {
+      sum = rms_tree_eval(tree, val[rl], lane);
+    }
+    if (lane == 0) s_rms[rl] = sqrt(sum / double(K) + eps);
+  }
+  slow = __syncthreads_or(slow || n_cand[rl] > kMaxCand);  // CTA-uniform from here on
+  const double rms = s_rms[rl];
+  double hi64 = -INFINITY, lo64 = INFINITY;
+  if (!slow && wr != 0) goto codes_pass;  // the few candidates: one warp per row
+  if (!slow) {
+    for (int j = lane; j < n_cand[rl]; j += 32) {
+        const int c = cand_idx[rl][j];
+        const float xf = In<T>::f(sr[spos(c)]);
+        const double y64 = xf == 0.f ? 0.0 : double(xf) / rms * gain[c];
+        hi64 = fmax(hi64, symmetric ? fabs(y64) : y64);
+        lo64 = fmin(lo64, y64);
+    }
+  } else {
+    // every element (rare rows): the reference's y for the whole row
+#pragma unroll
+    for (int it = 0; it < kChunks; ++it) {
+      const int c = it * (kTpr * 8) + t * 8;
+      if (!row_ok || c >= K) break;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xf = In<T>::f(sr[spos(c + i)]);
+        const double y64 = xf == 0.f ? 0.0 : double(xf) / rms * gain[c + i];
+        hi64 = fmax(hi64, symmetric ? fabs(y64) : y64);
+        lo64 = fmin(lo64, y64);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    hi64 = fmax(hi64, __shfl_xor_sync(0xffffffff, hi64, o));
+    lo64 = fmin(lo64, __shfl_xor_sync(0xffffffff, lo64, o));
+  }
+  if (slow) {
+    if (lane == 0) {
+      red_d[rl][wr][0] = hi64;
+      red_d[rl][wr][1] = lo64;
+    }
+    __syncthreads();  // CTA-uniform branch
+    if (t == 0)
+      for (int w = 1; w < kWarps; ++w) {
+        hi64 = fmax(hi64, red_d[rl][w][0]);
+        lo64 = fmin(lo64, red_d[rl][w][1]);
+      }
+  }
+  if (t == 0 && row_ok) {
+    double sc = symmetric ? hi64 / double((1 << (bits - 1)) - 1) : (hi64 - lo64) / double((1 << bits) - 1);
+    if (sc == 0.0) sc = 1.0;
+    const int zp = symmetric ? 0 : int(rint(-lo64 / sc));
+    const double c64 = 1.0 / (rms * sc);
+    s_scale[rl] = sc;
+    s_c32[rl] = (!slow && c64 >= 0x1p-120 && c64 <= 0x1p80) ? float(c64) : NAN;
+    s_zp[rl] = zp;
+    scale64[row] = sc;
+    scale32[row] = float(sc);
+    if (zp_out) zp_out[row] = zp;
+  }
+codes_pass:
+  __syncthreads();
+  // ---- codes
+  const int zp = s_zp[rl];
+  if (row_ok) {
+    const double sc = s_scale[rl];
+    const float c32 = s_c32[rl];
+    const int qmax = symmetric ? (1 << (bits - 1)) - 1 : (1 << bits) - 1;
+    const int qmin = symmetric ? -qmax : 0;
+    // q + (1.5 * 2^23 + zp) rounds q + zp half-to-even (|q + zp| < 2^22); rint(q) + zp differs
+    // from that only at an exact .5 tie of q with zp odd, which the margin sends to the f64 path
+    const float magic = 12582912.f + float(zp);
+    const uint32_t magic_bits = __float_as_uint(magic);
+    uint32_t redo = c32 != c32 ? 0xFFFFFFFFu : 0u;
+#pragma unroll
+    for (int it = 0; it < kChunks; ++it) {
+      const int c = it * (kTpr * 8) + t * 8;
+      if (c >= K) break;
+      int cq[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float q = z[it][i] * c32;
+        const float mq = q + magic;
+        const float d = q - (mq - magic);  // q - (rint(q + zp) - zp), exact
+        if (fabsf(d) >= fmaf(fabsf(q), -0x1p-20f, 0.5f - 0x1p-25f)) redo |= 1u << (it * 8 + i);
+        cq[i] = min(max(int(__float_as_uint(mq) - magic_bits) + zp, qmin), qmax);
+      }
+      const uint32_t w0 = __byte_perm(__byte_perm(cq[0], cq[1], 0x0040), __byte_perm(cq[2], cq[3], 0x0040), 0x5410);
+      const uint32_t w1 = __byte_perm(__byte_perm(cq[4], cq[5], 0x0040), __byte_perm(cq[6], cq[7], 0x0040), 0x5410);
+      *reinterpret_cast<uint2*>(codes + row * K + c) = make_uint2(w0, w1);
+    }
+    for (uint32_t m = redo; m; m &= m - 1) {
+      const int c = elem(__ffs(m) - 1);
+      if (c >= K) break;  // chunks are in order: the rest lies past K too
+      const float xf = In<T>::f(sr[spos(c)]);
+      const double y64 = xf == 0.f ? 0.0 : double(xf) / rms * gain[c];
+      codes[row * K + c] = int8_t(min(max(int(rint(y64 / sc)) + zp, qmin), qmax));
+    }
+  }
+  if (xs_kind != 0) {
+    __syncthreads();
+    if (row_ok) {
+      for (int jj = t; jj < r; jj += kTpr) {
+        const int col = sidx ? sidx[jj] : jj;
+        const int c = symmetric ? int(codes[row * K + col]) : int(uint8_t(codes[row * K + col]));
+        if (xs_kind == 1)
+          reinterpret_cast<__nv_bfloat16*>(xs_out)[row * r + jj] = __int2bfloat16_rn(c - zp);
+        else
+          reinterpret_cast<int8_t*>(xs_out)[row * r + jj] = int8_t(c);
+      }
+    }
   }
 }
 

@@ -13,6 +13,8 @@ Layouts (DESIGN.md "Data layout in HBM"):
 from __future__ import annotations
 
 import ctypes
+import threading
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -147,12 +149,55 @@ def rmsnorm_quantize_mx(x: torch.Tensor, gain: torch.Tensor, eps: float = 1e-6,
         out.xs_codes = torch.empty(cbr, dtype=torch.uint8, device=x.device)
         out.xs_sf = torch.empty(sbr, dtype=torch.uint8, device=x.device)
     gain = gain.contiguous()
-    g32 = gain.float()
+    g32 = _gain32(gain)
     _lib.call("serq_rmsnorm_quant_mx_gather", x.data_ptr(), _dtype_id(x), M, K, x.stride(0), gain.data_ptr(),
               g32.data_ptr(), float(eps), _ptr(gather_idx), int(r) if gather_idx is not None else 0,
               out.codes.data_ptr(), out.sf.data_ptr(), _ptr(out.xs_codes if gather_idx is not None else None),
               _ptr(out.xs_sf if gather_idx is not None else None), _stream())
     return out
+
+
+_G32: dict = {}
+_G32_LOCK = threading.Lock()
+
+
+def _gain32(gain: torch.Tensor) -> torch.Tensor:
+    """The f32 rounding of an RMSNorm gain (a layer weight), converted once per tensor version."""
+    key = id(gain)
+    with _G32_LOCK:
+        hit = _G32.get(key)
+        if hit is not None and hit[0]() is gain and hit[1] == gain._version:
+            return hit[2]
+    g32 = gain.float()
+    if torch.cuda.is_current_stream_capturing():
+        return g32  # a captured conversion: its result only exists once the graph replays
+    with _G32_LOCK:
+        if len(_G32) >= 64:
+            _G32.clear()
+        _G32[key] = (weakref.ref(gain), gain._version, g32)
+    return g32
+
+
+def rmsnorm_quantize_int(x: torch.Tensor, gain: torch.Tensor, eps: float, bits: int, symmetric: bool,
+                         salient_idx: torch.Tensor | None = None, r: int = 0, xs_kind: int = 0,
+                         exact_f64: bool = False) -> IntActivation:
+    """Producer fusion for the integer formats: quantize_*(rmsnorm(x, gain, eps)) per token in ONE
+    kernel, bit-identical to the reference's float64 (saliency.py:194-196, quantcore.py:108-137;
+    NumPy's pairwise row sum replayed): codes / scales / zero points.  ``exact_f64`` forces the
+    all-f64 kernel (otherwise used only for rows it alone serves: K % 8 != 0, unaligned rows)."""
+    _require_cuda(x, "x")
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ValidationError("x must be a row-major 2-D tensor")
+    M, K = x.shape
+    if gain.dtype != torch.float64 or gain.numel() != K or not gain.is_cuda:
+        raise ValidationError("gain must be a float64 CUDA vector of length K")
+    act = _int_activation(M, K, bits, symmetric, xs_kind, r, x.device)
+    gain = gain.contiguous()
+    g32 = _gain32(gain) if exact_f64 is False else None
+    _lib.call("serq_rmsnorm_quant_int", x.data_ptr(), _dtype_id(x), M, K, x.stride(0), gain.data_ptr(), _ptr(g32),
+              float(eps), bits, int(symmetric), act.codes.data_ptr(), act.scale64.data_ptr(), act.scale32.data_ptr(),
+              _ptr(act.zp), _ptr(salient_idx), r, _ptr(act.xs), xs_kind, _stream())
+    return act
 
 
 def unpack_mx(codes: torch.Tensor, sf: torch.Tensor, rows: int, cols: int) -> tuple[torch.Tensor, torch.Tensor]:
@@ -516,6 +561,12 @@ class IntLinear:
         torch.cuda.current_stream().synchronize()
         self._h = _Handle(h)
         self.device = device
+
+    def forward_rmsnorm(self, x: torch.Tensor, gain: torch.Tensor, eps: float, bits: int, symmetric: bool,
+                        y: torch.Tensor | None = None) -> torch.Tensor:
+        """linear(rmsnorm(x, gain)) with the normalisation fused into the per-token quantizer."""
+        return self.gemm(rmsnorm_quantize_int(x, gain, eps, bits, symmetric, self.salient_idx, self.r,
+                                              self.xs_kind()), y)
 
     def weight_bytes(self) -> tuple[int, bool]:
         """(bytes of the resident main weights, held as packed INT4?)"""

@@ -555,6 +555,118 @@ def test_rmsnorm_quant_mx_exact_fallback_blocks(D):
     assert np.array_equal(c.cpu().numpy(), ref.element_codes)
 
 
+# ---------------------------------------------------------------- RMSNorm -> INT producer
+
+
+def _check_rms_int(D, x, tdt, gain, eps, bits, symmetric, exact_f64=False):
+    act = D.rmsnorm_quantize_int(_cuda(x, tdt), torch.from_numpy(gain).to("cuda"), eps, bits, symmetric,
+                                 exact_f64=exact_f64)
+    cfg = O.IntCfg(bits, symmetric, "per-row")
+    y = O.rmsnorm(x, gain, eps)
+    ref = O.quantize_symmetric(y, cfg) if symmetric else O.quantize_asymmetric(y, cfg)
+    codes = act.codes.cpu().numpy()
+    codes = codes.astype(np.int32) if symmetric else codes.view(np.uint8).astype(np.int32)
+    assert np.array_equal(act.scale64.cpu().numpy(), ref.scales[:, 0])
+    if not symmetric:
+        assert np.array_equal(act.zp.cpu().numpy(), ref.zero_points[:, 0])
+    assert np.array_equal(codes, ref.codes), int((codes != ref.codes).sum())
+
+
+# K % 8 != 0 (100, 4100) runs the all-f64 kernel, the rest the f32-bounded fast kernel
+@pytest.mark.parametrize("dtype,K", [("bf16", 100), ("bf16", 1000), ("bf16", 1024), ("f32", 2560), ("bf16", 3008),
+                                     ("bf16", 4096), ("f32", 4100), ("bf16", 6144), ("f32", 8192), ("bf16", 8192)])
+@pytest.mark.parametrize("bits,symmetric", [(8, False), (4, True), (4, False)])
+def test_rmsnorm_quant_int_bitexact(D, dtype, K, bits, symmetric):
+    # codes, f64 scales and zero points of quantize_*(rmsnorm(x, gain)) bit for bit: the kernel
+    # replays NumPy's pairwise row sum, so even the f64 rms equals the reference's
+    M = 67
+    rng = np.random.default_rng(K + bits)
+    x = O.bf16_round(_bf16_outlier_x(M, K, seed=K) * 3.0)
+    if dtype == "f32":
+        x = (x + rng.standard_normal(x.shape) * 1e-3).astype(np.float32).astype(np.float64)
+    gain = (np.abs(rng.standard_normal(K)) + 0.5) / np.exp2(rng.uniform(-2, 2, K))
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    _check_rms_int(D, x, tdt, gain, 1e-6, bits, symmetric)
+    if K in (1024, 3008):
+        _check_rms_int(D, x, tdt, gain, 1e-6, bits, symmetric, exact_f64=True)
+
+
+@pytest.mark.parametrize("symmetric", [True, False])
+@pytest.mark.parametrize("K", [1024, 4096])
+def test_rmsnorm_quant_int_fast_kernel_ties_and_slow_rows(D, symmetric, K):
+    # rows built to stress the fast kernel's bounds: (a) exact .5 ties of y / s (|x| = 2 with
+    # eps = 0: rms = 2, y = +-1, s = 2/255 -> y / s = +-127.5), (b) values so small that the f32
+    # pass would go denormal (whole row in f64), (c) huge values, (d) an f32-denormal gain entry
+    # and zero rows (eps > 0)
+    rng = np.random.default_rng(5)
+    x = O.bf16_round(rng.standard_normal((5, K)))
+    x[0] = np.where(rng.random(K) < 0.5, -2.0, 2.0)
+    x[1] = O.bf16_round(rng.standard_normal(K) * 1e-33)
+    x[2] = O.bf16_round(rng.standard_normal(K) * 1e30)
+    x[3, ::3] = 0.0
+    gain = np.ones(K)
+    _check_rms_int(D, x, torch.bfloat16, gain, 0.0, 8, symmetric)
+    x2 = x.copy()
+    x2[4] = 0.0
+    gain2 = np.abs(rng.standard_normal(K)) + 0.5
+    gain2[7] = 1e-40
+    gain2[9] = 0.0
+    _check_rms_int(D, x2, torch.bfloat16, gain2, 1e-6, 8, symmetric)
+
+
+@pytest.mark.parametrize("dtype,K", [("bf16", 4096), ("f32", 2048)])
+def test_rmsnorm_quant_int_fast_matches_f64_kernel(D, dtype, K):
+    # the two kernels agree on a larger sample (the fast one's exactness argument, checked)
+    M = 1024
+    x = _bf16_outlier_x(M, K, seed=21) * 1.7
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    xt = _cuda(x, tdt)
+    g = torch.from_numpy(np.random.default_rng(2).uniform(0.3, 3.0, K)).to("cuda")
+    for bits, sym in ((8, False), (4, True), (2, False)):
+        a = D.rmsnorm_quantize_int(xt, g, 1e-6, bits, sym)
+        b = D.rmsnorm_quantize_int(xt, g, 1e-6, bits, sym, exact_f64=True)
+        assert torch.equal(a.codes, b.codes) and torch.equal(a.scale64, b.scale64)
+        if not sym:
+            assert torch.equal(a.zp, b.zp)
+
+
+@pytest.mark.parametrize("r_mode,contiguous", [("int", True), ("dense", True), ("int", False)])
+def test_rmsnorm_fused_int_linear_matches_two_step(D, r_mode, contiguous):
+    # linear(rmsnorm(x)) with the norm fused into K1-INT == the linear on the reference's rmsnorm
+    # output quantized by the plain K1-INT (same codes -> identical bf16 Y), incl. the xs slices
+    M, K, N, r = 300, 2048, 512, 64
+    rng = np.random.default_rng(3)
+    x = O.bf16_round(_bf16_outlier_x(M, K, seed=9) * 2.0)
+    gain = np.abs(rng.standard_normal(K)) + 0.5
+    w = rng.standard_normal((K, N)) * 0.02
+    idx = np.arange(r) if contiguous else np.sort(rng.choice(K, r, replace=False))
+    main, comp = O.build_per_channel_int(w, idx, r_mode=r_mode)
+    kw = dict(r_dense=comp.r_dense) if r_mode == "dense" else dict(r_codes=comp.r_q.codes, r_scales=comp.r_q.scales)
+    lin = D.IntLinear(main.codes, main.scales, 4, salient_idx=idx, **kw)
+    y1 = lin.forward_rmsnorm(_cuda(x, torch.bfloat16), torch.from_numpy(gain).to("cuda"), 1e-6, 8, False)
+    y2 = lin.gemm(lin.quantize(_cuda(O.rmsnorm(x, gain, 1e-6), torch.float64), 8, False))
+    assert torch.equal(y1, y2)
+
+
+def test_rmsnorm_quant_int_constant_and_zero_rows(D):
+    # all-zero rows (rms = sqrt(eps), scale 0 -> 1) and constant rows (hi == lo)
+    K = 1024
+    x = np.zeros((4, K))
+    x[1] = 3.0
+    x[2, ::2] = -1.5
+    x[3] = _bf16_outlier_x(1, K, seed=4)[0]
+    gain = np.ones(K)
+    for sym in (True, False):
+        act = D.rmsnorm_quantize_int(_cuda(x, torch.bfloat16), torch.from_numpy(gain).to("cuda"), 1e-6, 8, sym)
+        cfg = O.IntCfg(8, sym, "per-row")
+        y = O.rmsnorm(x, gain, 1e-6)
+        ref = O.quantize_symmetric(y, cfg) if sym else O.quantize_asymmetric(y, cfg)
+        codes = act.codes.cpu().numpy()
+        codes = codes.astype(np.int32) if sym else codes.view(np.uint8).astype(np.int32)
+        assert np.array_equal(act.scale64.cpu().numpy(), ref.scales[:, 0])
+        assert np.array_equal(codes, ref.codes)
+
+
 @pytest.mark.parametrize("world", [2, 4])
 def test_tp_shards_on_device_match_single_device(D, world):
     # SURVEY 8(e) with the real kernels: the per-rank shards of a column-parallel and a
