@@ -1147,8 +1147,9 @@ codes_pass:
 }
 
 // rint(x / s) as an int for 16-bit / 32-bit inputs: the f32 fast path decides with the proven
-// margin and everything stays on the FP32 / integer pipes (this GPU's FP64 pipe runs ~64x
-// slower); only values within the margin of a .5 tie take the correctly rounded f64 division.
+// margin and everything stays on the FP32 / integer pipes (an f64 division is a ~10-DFMA
+// dependent sequence; tools/probes/fp64_rate.cu measures DFMA at 0.42x the FFMA rate); only
+// values within the margin of a .5 tie take the correctly rounded f64 division.
 // Returns clip(rint(x / s) + zp, qmin, qmax).  |x/s| < 2^21 implies |zp| < 2^21 + 2^bits
 // (x lies in [lo, hi], zp = rint(-lo/s)), so the int sum is exact; larger quotients take
 // the reference's f64 expression.
@@ -1258,8 +1259,8 @@ __global__ void __launch_bounds__(256) int_quant_kernel(const T* __restrict__ x,
 // the exact residual r = RN(x - h*s) (one DFMA; x, h exact): r == 0 means x / s == h and
 // rint picks the even neighbour; |r| > 2 * (ulp(h)/2) * s means the f64 quotient cannot
 // round onto h, so the sign decides.  Only the razor-thin rest (and |x/s| >= 2^21) pays
-// the correctly rounded f64 division.  This GPU's FP64 pipe is slow: one DFMA instead
-// of a DDIV keeps a flagged row off the kernel's critical path.
+// the correctly rounded f64 division.  One DFMA instead of a DDIV (a ~10-DFMA dependent
+// sequence) keeps a flagged row off the kernel's critical path.
 __device__ __forceinline__ int int_code_tie(float xf, double s, float inv32, int zp, int qmin, int qmax) {
   const float q = xf * inv32;  // only steers toward the nearby half-integer
   double k;
