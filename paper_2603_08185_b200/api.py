@@ -321,16 +321,16 @@ class SerqLinear:
         has_r = comp is not None and getattr(comp, "rank", 0)
         self.svd = None
         if has_r and getattr(comp, "mode", RTN_RESIDUAL) == SVD_BASELINE:
-            # SVD baseline (compensate.py:209-224, 304-310): INT main through the fused kernel with no
-            # salient term; the two-factor correction (x_hat @ L1) @ L2 spans all K columns, so it runs as
-            # two plain fp32 cuBLAS GEMMs whose result is added in the kernel epilogue before the bf16 store
+            # SVD baseline (compensate.py:209-224, 304-310): the two-factor correction (x_hat @ L1) @ L2
+            # spans all K columns: U = (codes - zp) @ L1 as one bf16 GEMM, then U @ L2 as the fused INT
+            # kernel's dense side term (device.SvdIntLinear)
             if _is_mx(main):
                 raise ValidationError("the SVD baseline compensates integer mains only")
             l1 = np.asarray(comp.l1, dtype=np.float64)
             l2 = np.asarray(comp.l2, dtype=np.float64)
             if l1.shape != (main.shape[0], comp.rank) or l2.shape != (comp.rank, main.shape[1]):
                 raise ValidationError("SVD factors must be L1 [K, r] and L2 [r, N]")
-            self.svd = (torch.from_numpy(l1).to(device, torch.float32), torch.from_numpy(l2).to(device, torch.float32))
+            self.svd = (l1, l2)
             comp, has_r = None, 0
         idx = None if not has_r else np.asarray(comp.salient_idx, dtype=np.intp)
         if self.fmt == "mx":
@@ -378,8 +378,12 @@ class SerqLinear:
                         raise ValidationError(
                             "integer R must be symmetric with one scale per output column (row groups of size r) or "
                             "column-grouped (default_r_config)")
-            self.impl = D.IntLinear(main.codes, main.scales, main.config.bits, salient_idx=idx, device=device,
-                                    group_size=gs, **kw)
+            if self.svd is not None:
+                self.impl = D.SvdIntLinear(main.codes, main.scales, main.config.bits, *self.svd, device=device,
+                                           group_size=gs)
+            else:
+                self.impl = D.IntLinear(main.codes, main.scales, main.config.bits, salient_idx=idx, device=device,
+                                        group_size=gs, **kw)
             self.act_bits, self.act_symmetric = act_cfg.bits, act_cfg.symmetric
             self.K, self.N = main.shape
         self.rank = int(comp.rank) if has_r else 0
@@ -391,15 +395,7 @@ class SerqLinear:
         if self.fmt == "mx":
             return self.impl(x, y)
         if self.svd is not None:
-            act = self.impl.quantize(x, self.act_bits, self.act_symmetric)
-            l1, l2 = self.svd
-            prev = torch.backends.cuda.matmul.allow_tf32
-            torch.backends.cuda.matmul.allow_tf32 = False  # fp32 products, like the reference's f64 within tolerance
-            try:
-                corr = (D.IntLinear.dequantize(act) @ l1) @ l2
-            finally:
-                torch.backends.cuda.matmul.allow_tf32 = prev
-            return self.impl.gemm(act, y, addend=corr.contiguous())
+            return self.impl.forward(x, self.act_bits, self.act_symmetric, y)
         return self.impl(x, self.act_bits, self.act_symmetric, y)
 
 

@@ -315,32 +315,40 @@ def int_linear_point(M, K, N, r, r_mode, bits, symmetric, flush: Flusher | None 
 
 def svd_baseline_point(M, K, N, r, bits=8, n_steps: int = 16) -> dict:
     """The paper's L2QER-style comparison (SVD baseline, compensate.py:209-224,
-    304-310) at an INT shape: the same fused INT kernel without a salient term,
-    plus the two-factor correction (x_hat @ L1) @ L2 as two fp32 cuBLAS GEMMs
-    added in the epilogue.  Factors are random with the right shapes (only the
-    cost is measured here; parity is a test)."""
-    lins = [device_int_linear(K, N, 0, "dense", seed=1 + i) for i in range(8)]
-    g = torch.Generator(device="cuda").manual_seed(5)
-    l1 = torch.randn((K, r), generator=g, device="cuda") * 0.01
-    l2 = torch.randn((r, N), generator=g, device="cuda") * 0.01
+    304-310) at an INT shape, two ways: (a) device.SvdIntLinear -- the quantizer's
+    exact bf16 (codes - zp), one bf16 GEMM U = (codes - zp) L1, and U L2 as the fused
+    INT kernel's dense side term (our kernel); (b) the correction as two fp32 cuBLAS
+    GEMMs added in the INT kernel's epilogue from an [M, N] fp32 buffer.  Factors are
+    random with the right shapes (only the cost is measured here; parity is a test)."""
+    rng = np.random.default_rng(5)
+    mains = []
+    for i in range(8):
+        w = np.random.default_rng(1 + i).integers(-7, 8, (K, N))
+        mains.append((w, np.random.default_rng(2 + i).uniform(0.01, 0.02, N)))
+    l1 = rng.standard_normal((K, r)) * 0.01
+    l2 = rng.standard_normal((r, N)) * 0.01
+    svds = [D.SvdIntLinear(w, s, 4, l1, l2) for w, s in mains]
     xs = [outlier_x(M, K, seed=i, frac=0.005, mag=100.0) for i in range(8)]
     ys = [torch.empty((M, N), dtype=torch.bfloat16, device="cuda") for _ in xs]
+    t_fused = time_steps(lambda i: svds[i % 8].forward(xs[i % 8], bits, False, ys[i % 8]), n_steps)
+    lins = [device_int_linear(K, N, 0, "dense", seed=1 + i) for i in range(8)]
+    l1t = torch.from_numpy(l1).to("cuda", torch.float32)
+    l2t = torch.from_numpy(l2).to("cuda", torch.float32)
     prev = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = False
 
-    def step(i):
+    def two_gemm(i):
         lin = lins[i % 8]
         act = lin.quantize(xs[i % 8], bits, False)
-        corr = (D.IntLinear.dequantize(act) @ l1) @ l2
+        corr = (D.IntLinear.dequantize(act) @ l1t) @ l2t
         lin.gemm(act, ys[i % 8], addend=corr)
 
     try:
-        t = time_steps(step, n_steps)
+        t_lib = time_steps(two_gemm, n_steps)
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev
-    return {"M": M, "K": K, "N": N, "r": r, "act_bits": bits, "step_us": t * 1e3, "aux_matmuls": 2,
-            "tokens_per_s": M / (t * 1e-3)}
-
+    return {"M": M, "K": K, "N": N, "r": r, "act_bits": bits, "step_us": t_fused * 1e3, "aux_matmuls": 2,
+            "tokens_per_s": M / (t_fused * 1e-3), "cublas_two_gemm_addend_step_us": t_lib * 1e3}
 
 def rmsnorm_quant_point(M: int, K: int, hbm_peak_gbs: float, n_steps: int = 16) -> dict:
     """Producer fusion: rmsnorm(x, gain) -> MX codes in one

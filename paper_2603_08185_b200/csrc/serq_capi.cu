@@ -821,10 +821,10 @@ int serq_pack_int4(const int32_t* codes, const double* scales, int64_t K, int64_
                    serq_stream_t stream) {
   if (w_bits > 4) return fail(SERQ_EINVAL, "packed INT4 weights need w_bits <= 4 (got %d)", w_bits);
   const int rr = r_mode == SERQ_R_NONE ? 0 : r;
-  if ((r_mode == SERQ_R_INT && !salient_contiguous) || rr > 128 || (r_mode == SERQ_R_DENSE && rr > 64))
+  if ((r_mode == SERQ_R_INT && !salient_contiguous) || rr > 128 || (r_mode == SERQ_R_DENSE && cdiv(K, 128) < cdiv(rr, 64)))
     return fail(SERQ_EINVAL,
                 "packed INT4 weights are served by the CTA-pair kernel: R permuted-integer (r <= 128), dense "
-                "(r <= 64) or none");
+                "(r <= 128, K >= 128 ceil(r / 64)) or none");
   return pack_int_impl(codes, scales, K, N, w_bits, r_mode, r_data, r_scales, r, salient_contiguous, true, out, stream);
 }
 
@@ -862,8 +862,9 @@ static int pack_int_impl(const int32_t* codes, const double* scales, int64_t K, 
   // weights in HBM: packed INT4 (0.5 B / weight, serq_pack_int4: the CTA-pair kernel widens them
   // in the SM) or int8 [N, K] (serq_pack_int, the faster feed today: TMA straight into the
   // operand).  Never both copies.
+  // dense R of r > 64 takes ceil(r / 64) side tiles, staged with distinct K-steps (needs K >= 128 nr)
   const bool pair_cfg = (r_mode != SERQ_R_INT || salient_contiguous) && h->r <= 128 &&
-                        (r_mode != SERQ_R_DENSE || h->r <= 64);
+                        (r_mode != SERQ_R_DENSE || cdiv(K, 128) >= cdiv(h->r, 64));
   h->has_w4 = allow_w4 && w_bits <= 4 && pair_cfg;
   int rc = SERQ_OK;
   if (h->has_w4) {
@@ -1357,7 +1358,8 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   // W4 handles always take the CTA-pair kernel (it is the one that widens packed INT4); int8
   // handles above 128 rows when their R layout allows it
   const bool pair_ok = h->has_w4 || (M > 128 && (h->r_mode != SERQ_R_INT || h->contiguous) && h->r <= 128 &&
-                                     (h->r_mode != SERQ_R_DENSE || h->r <= 64) && !SERQ_DBG(g_debug_flags, 65536));
+                                     (h->r_mode != SERQ_R_DENSE || cdiv(h->K, 128) >= cdiv(h->r, 64)) &&
+                                     !SERQ_DBG(g_debug_flags, 65536));
   if (pair_ok) {
     using Cfg8 = I8Cfg<kI8Epi, false>;
     using Cfg4 = I8Cfg<kI8Epi, true>;

@@ -127,7 +127,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
   constexpr int kEpiThreads = 32 * Cfg::kEpiWarps;
   constexpr int kBHalf = kN / 2;  // weight rows per CTA
   constexpr uint32_t kBBytes = kBHalf * 128;  // one 128-K step of this CTA's weight rows (int8)
-  constexpr uint32_t kRBytes = kBHalf * 128;  // this CTA's R rows (int8 r <= 128 or bf16 r <= 64: 128 B each)
+  constexpr uint32_t kRBytes = kBHalf * 128;  // this CTA's R rows per side tile (int8 r <= 128 or 64 bf16: 128 B each)
   constexpr int kI8Stages = Cfg::kStages;
   constexpr int kI8Stage = Cfg::kStage;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -156,6 +156,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
   const bool has_r = p.r_mode != kRNone;
   const bool dense = p.r_mode == kRDense;
   const int ks = p.k_steps;  // 128-K steps
+  // the salient term in side tiles of 64 bf16 (dense) / 128 int8 (integer R) columns: tile j is
+  // staged with main K-step j * sstep (spread out, so reloading the one side buffer stays off
+  // the MMA's critical path; the host guarantees ks >= nr)
+  const int nr = has_r ? (dense ? (p.r + 63) / 64 : 1) : 0;
+  const int sstep = nr > 0 ? ks / nr : 1;
+  auto side_tile = [&](int kk) { return (nr > 0 && kk % sstep == 0 && kk / sstep < nr) ? kk / sstep : -1; };
 
   if (warp == 0 && elect_one()) {
     tma_prefetch(&maps.a);
@@ -194,7 +200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
       if (my_tiles > 0) {
         const int n_half0 = (cluster_id / tiles_m) * kN + int(rank) * kBHalf;
         for (int kk = 0; kk < pre; ++kk) {
-          const bool with_side = has_r && kk == 0;
+          const bool with_side = side_tile(kk) >= 0;
           if (leader)
             mbar_expect_tx(&full[kk], 2u * (kI8A + kBBytes + (with_side ? (dense ? 16384 + kRBytes : kRBytes) : 0)));
           tma_load_2d_pair(sb + kk * kI8Stage + kI8A, &maps.bp, map_rank(smem_u32(&full[kk]), 0), kk * 128, n_half0,
@@ -212,8 +218,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
           const int s = g % kI8Stages;
           const bool preloaded = i == 0 && kk < pre;
           if (!preloaded) mbar_wait_bo(&empty[s], ((g / kI8Stages) & 1) ^ 1, SERQ_DBG(p.dbg, (1 << 20)));
-          const bool with_side = has_r && kk == 0;
-          if (with_side && i > 0) mbar_wait(side_empty, (i - 1) & 1);
+          const int sj = side_tile(kk);
+          const bool with_side = sj >= 0;
+          const int su = i * nr + sj;  // side-buffer use count
+          if (with_side && su > 0) mbar_wait(side_empty, (su - 1) & 1);
           const uint32_t fbar = map_rank(smem_u32(&full[s]), 0);
           const uint32_t st = sb + s * kI8Stage;
           if (leader && !preloaded)
@@ -222,8 +230,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
             tma_load_2d_pair(st + kI8A, &maps.bp, fbar, kk * 128, n_half, kEvictNormal);  // int8 [N, K] rows
           tma_load_2d_pair(st, &maps.a, fbar, kk * 128, m_own, kEvictNormal);
           if (with_side) {
-            tma_load_2d_pair(sside + 16384, &maps.r, fbar, 0, n_half, kEvictNormal);
-            if (dense) tma_load_2d_pair(sside, &maps.xs, fbar, 0, m_own, kEvictNormal);
+            tma_load_2d_pair(sside + 16384, &maps.r, fbar, 64 * sj, n_half, kEvictNormal);
+            if (dense) tma_load_2d_pair(sside, &maps.xs, fbar, 64 * sj, m_own, kEvictNormal);
           }
         }
       }
@@ -261,12 +269,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
             mma_i8_pair(0, a, b, id_main, first);
             mma_i8_pair(0, a + 2, b + 2, id_main, 1u);
             mma_i8_pair(0, a + 4, b + 4, id_main, 1u);
-            if (has_r && kk == 0) {
-              // salient term into the second accumulator (columns [256, 512))
+            const int sj = side_tile(kk);
+            if (sj >= 0) {
+              // salient term (side tile sj) into the second accumulator (columns [256, 512))
               const uint64_t ar = dense ? make_sdesc(sside, 16, 1024, 2) : a;
               const uint64_t br = make_sdesc(sside + 16384, 16, 1024, 2);
-              const int nk = dense ? (2 * p.r + 31) / 32 : (p.r + 31) / 32;
-              for (int j = 0; j < nk; ++j) mma_i8_or_bf16(dense, 256, ar + 2 * j, br + 2 * j, id_r, j > 0 ? 1u : 0u);
+              const int rr = dense ? min(64, p.r - 64 * sj) : p.r;
+              const int nk = dense ? (2 * rr + 31) / 32 : (rr + 31) / 32;
+              for (int j = 0; j < nk; ++j)
+                mma_i8_or_bf16(dense, 256, ar + 2 * j, br + 2 * j, id_r, (sj > 0 || j > 0) ? 1u : 0u);
               tc_commit_pair(side_empty);
             }
           }

@@ -640,6 +640,51 @@ class IntLinear:
         return self.forward(x, bits, symmetric, None, y)
 
 
+
+class SvdIntLinear:
+    """The SVD baseline (build_svd_baseline, compensate.py:209-224; forward_reconstructed,
+    compensate.py:304-310): Y = x_hat W + (x_hat L1) L2 with x_hat = s (codes - zp).
+
+    B200 path: the quantizer also emits the exact bf16 (codes - zp) of every column, one plain
+    bf16 GEMM (cuBLAS, fp32 accumulation) forms U = (codes - zp) L1 [M, r], and the fused INT
+    kernel runs U L2 as its dense side term -- tcgen05 kind::f16 into the second TMEM
+    accumulator, scaled by s in the epilogue -- so the second factor product and the add never
+    leave the SM (no [M, N] fp32 correction in HBM).  L1 / L2 / U are bf16 (2^-9 relative on the
+    correction term)."""
+
+    def __init__(self, codes, scales, bits, l1, l2, device="cuda", group_size=None):
+        l1 = np.asarray(l1, dtype=np.float64)
+        l2 = np.asarray(l2, dtype=np.float64)
+        K, r = l1.shape
+        if l2.shape[0] != r:
+            raise ValidationError("SVD factors must be L1 [K, r] and L2 [r, N]")
+        rp = -(-r // 8) * 8  # dense R rows in multiples of 8 (zero factors add nothing)
+        l1p = np.zeros((K, rp))
+        l1p[:, :r] = l1
+        l2p = np.zeros((rp, l2.shape[1]))
+        l2p[:r] = l2
+        self.K, self.r = K, rp
+        self.lin = IntLinear(codes, scales, bits, r_dense=l2p, salient_idx=np.arange(rp), device=device,
+                             group_size=group_size)
+        self.N = self.lin.N
+        self.l1 = torch.from_numpy(l1p).to(self.lin.device, torch.bfloat16)
+
+    def quantize(self, x: torch.Tensor, bits: int, symmetric: bool) -> IntActivation:
+        """Codes / scales / zero points and U = (codes - zp) L1 as the activation's side slice."""
+        act = quantize_int(x, bits, symmetric, None, self.K, 1)  # xs: bf16 (codes - zp) of all K columns
+        prev = torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction
+        torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
+        try:
+            act.xs = (act.xs @ self.l1).contiguous()
+        finally:
+            torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = prev
+        return act
+
+    def forward(self, x: torch.Tensor, bits: int, symmetric: bool, y: torch.Tensor | None = None) -> torch.Tensor:
+        return self.lin.gemm(self.quantize(x, bits, symmetric), y)
+
+    __call__ = forward
+
 def device_info() -> dict:
     sm, ma, mi = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     _lib.call("serq_device_info", ctypes.byref(sm), ctypes.byref(ma), ctypes.byref(mi))

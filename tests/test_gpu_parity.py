@@ -228,6 +228,43 @@ def test_int_linear_parity(D, bits, symmetric, r_mode):
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
 
 
+@pytest.mark.parametrize("M,K,N,r", [(300, 1024, 512, 128), (1024, 2048, 1536, 96), (260, 512, 264, 72)])
+def test_int_linear_dense_r_above_64_pair_kernel(D, M, K, N, r):
+    # dense R with r > 64 on the CTA-pair kernel: ceil(r / 64) side tiles staged with spread
+    # K-steps into one TMEM accumulator; partial last side tile (72, 96), many tiles per pair
+    x = _bf16_outlier_x(M, K, seed=r)
+    w = np.random.default_rng(r).standard_normal((K, N)) * 0.02
+    main, comp = O.build_per_channel_int(w, np.arange(r), r_mode="dense")
+    lin = D.IntLinear(main.codes, main.scales, 4, r_dense=comp.r_dense, salient_idx=np.arange(r))
+    act = lin.quantize(_cuda(x, torch.bfloat16), 8, False)
+    acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    y = lin.gemm(act, acc_dump=acc).float().cpu().numpy()
+    assert D.last_kernel().startswith("serq_i8_pair_kernel"), D.last_kernel()
+    y_ref, xq = O.forward_int(x, main, comp, O.IntCfg(8, False, "per-row"))
+    _, parts = O.int_gemm(xq, main, return_partials=True)
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), parts[0][1])
+    mx, mean = O.parity_errors(y, y_ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+@pytest.mark.parametrize("M,K,N,r", [(300, 1024, 512, 128), (2048, 4096, 1024, 128), (40, 512, 256, 8)])
+def test_svd_baseline_fused_matches_oracle(D, M, K, N, r):
+    # SVD baseline (compensate.py:304-310): U = (codes - zp) L1 by one bf16 GEMM, U L2 as the
+    # fused kernel's dense side term; vs the oracle's f64 (x_hat L1) L2 at the north_star tolerance
+    rng = np.random.default_rng(M + r)
+    x = _bf16_outlier_x(M, K, seed=7)
+    w = rng.standard_normal((K, N)) * 0.02
+    main = O.quantize_symmetric(w, O.IntCfg(4, True, K, "row"))
+    err = w - O.dequantize(main)
+    u, sv, vt = np.linalg.svd(err, full_matrices=False)
+    l1, l2 = u[:, :r] * sv[:r], vt[:r]
+    lin = D.SvdIntLinear(main.codes, main.scales, 4, l1, l2)
+    y = lin.forward(_cuda(x, torch.bfloat16), 8, False).float().cpu().numpy()
+    y_ref, _ = O.forward_int(x, main, O.Comp(r, l1=l1, l2=l2), O.IntCfg(8, False, "per-row"))
+    mx, mean = O.parity_errors(y, y_ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
 @pytest.mark.parametrize("M,N,r_mode", [(300, 520, "int"), (257, 1000, "dense"), (129, 136, "int")])
 def test_int_linear_ragged_narrow_tiles(D, M, N, r_mode):
     # few tiles -> the 128-column CTA-pair tiles; ragged M and N (partial last tiles)
