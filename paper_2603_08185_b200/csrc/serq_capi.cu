@@ -18,6 +18,7 @@
 #include "serq_gemm_decode3.cuh"
 #include "serq_gemm_i8.cuh"
 #include "serq_gemm_i8g.cuh"
+#include "serq_gemv_i8.cuh"
 #include "serq_quant.cuh"
 
 using namespace serq;
@@ -1306,6 +1307,58 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   const bool need_xs = h->r_mode == SERQ_R_DENSE || h->r_mode == SERQ_R_DENSE_SPLIT ||
                        (h->r_mode == SERQ_R_INT && !h->contiguous);
   if (need_xs && !xs) return fail(SERQ_EINVAL, "this R mode needs the quantizer's xs slice");
+  if (M <= 16 && !h->use_i8g && !h->has_w4 && h->r <= 128 && !SERQ_DBG(g_debug_flags, 1 << 29)) {
+    // decode sizes: the weight stream with warp-level MMAs (serq_gemv_i8.cuh)
+    GemvI8Params gp{};
+    gp.w = static_cast<const int8_t*>(h->w);
+    gp.K = int(h->K);
+    gp.N = int(h->N);
+    gp.M = int(M);
+    gp.a = reinterpret_cast<const uint8_t*>(a_codes);
+    gp.sx = sx;
+    gp.zp = zp;
+    gp.sw = h->sw;
+    gp.colsum = h->colsum;
+    gp.r = h->r;
+    gp.rw = h->rbuf;
+    gp.sr = h->sr;
+    gp.colsum_r = h->colsum_r;
+    gp.xs = (h->r_mode == SERQ_R_INT && h->contiguous) ? nullptr : xs;
+    gp.y = static_cast<__nv_bfloat16*>(y);
+    gp.ldy = ldy;
+    gp.addend = addend;
+    gp.acc_dump = acc_dump;
+    gp.accr_dump = accr_dump;
+    const bool sgn = zp == nullptr;
+    // 16 weight rows per CTA; 8 warps split K when the row groups alone leave SMs idle (a wave
+    // holds ~2 such CTAs per SM), 4 otherwise (all CTAs in one wave)
+    const int64_t groups = cdiv(h->N, 16);
+    const bool wide = groups <= 2 * int64_t(sm_count());
+    const dim3 grid{unsigned(groups)}, blk{wide ? 256u : 128u};
+    cudaError_t e = cudaSuccess;
+#define GEMV_W(NT, SG, KR)                                                                                          \
+  e = wide ? launch_pdl(serq_i8_gemv_kernel<NT, SG, KR, 8>, grid, blk, 0, S(stream), gp)                           \
+           : launch_pdl(serq_i8_gemv_kernel<NT, SG, KR, 4>, grid, blk, 0, S(stream), gp)
+#define GEMV_R(NT, KR)                                                                                              \
+  do {                                                                                                             \
+    if (sgn) GEMV_W(NT, true, KR);                                                                                 \
+    else GEMV_W(NT, false, KR);                                                                                    \
+  } while (0)
+#define GEMV_M(NT)                                                                                                 \
+  do {                                                                                                             \
+    if (h->r_mode == SERQ_R_INT) GEMV_R(NT, kRInt);                                                                \
+    else if (h->r_mode == SERQ_R_DENSE) GEMV_R(NT, kRDense);                                                       \
+    else GEMV_R(NT, 0);                                                                                            \
+  } while (0)
+    if (M <= 8) GEMV_M(1);
+    else GEMV_M(2);
+#undef GEMV_M
+#undef GEMV_R
+#undef GEMV_W
+    CK(e);
+    LAUNCH_CHECK("serq_i8_gemv_kernel");
+    return SERQ_OK;
+  }
   if (h->use_i8g) {
     // group-wise weight scales: one promoted integer partial per group (serq_gemm_i8g.cuh), any M
     {

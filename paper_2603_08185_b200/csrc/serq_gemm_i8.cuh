@@ -161,7 +161,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
   // the MMA's critical path; the host guarantees ks >= nr)
   const int nr = has_r ? (dense ? (p.r + 63) / 64 : 1) : 0;
   const int sstep = nr > 0 ? ks / nr : 1;
-  auto side_tile = [&](int kk) { return (nr > 0 && kk % sstep == 0 && kk / sstep < nr) ? kk / sstep : -1; };
+  // side-tile cursor over a tile's K-steps (no runtime division in the issue loops: an integer
+  // divide is a ~40-instruction dependent chain that slowed every K-step of the MMA warp)
+  struct SideCursor {
+    int next, cnt, nr, sstep;
+    __device__ int step(int kk) {  // side tile staged / consumed at K-step kk, or -1
+      if (kk != next) return -1;
+      const int j = cnt++;
+      next = cnt < nr ? next + sstep : 0x7fffffff;
+      return j;
+    }
+  };
+  auto side_cursor = [&]() { return SideCursor{nr > 0 ? 0 : 0x7fffffff, 0, nr, sstep}; };
 
   if (warp == 0 && elect_one()) {
     tma_prefetch(&maps.a);
@@ -199,8 +210,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
       constexpr uint32_t kBTma = kW4 ? 0u : kBBytes;  // W4: B is written by the loader warps
       if (my_tiles > 0) {
         const int n_half0 = (cluster_id / tiles_m) * kN + int(rank) * kBHalf;
+        SideCursor sc0 = side_cursor();
         for (int kk = 0; kk < pre; ++kk) {
-          const bool with_side = side_tile(kk) >= 0;
+          const bool with_side = sc0.step(kk) >= 0;
           if (leader)
             mbar_expect_tx(&full[kk], 2u * (kI8A + kBBytes + (with_side ? (dense ? 16384 + kRBytes : kRBytes) : 0)));
           tma_load_2d_pair(sb + kk * kI8Stage + kI8A, &maps.bp, map_rank(smem_u32(&full[kk]), 0), kk * 128, n_half0,
@@ -214,11 +226,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
         const int mt = tile % tiles_m, nt = tile / tiles_m;
         const int m_own = mt * 256 + int(rank) * 128;
         const int n_half = nt * kN + int(rank) * kBHalf;
+        SideCursor sc = side_cursor();
         for (int kk = 0; kk < ks; ++kk, ++g) {
           const int s = g % kI8Stages;
           const bool preloaded = i == 0 && kk < pre;
           if (!preloaded) mbar_wait_bo(&empty[s], ((g / kI8Stages) & 1) ^ 1, SERQ_DBG(p.dbg, (1 << 20)));
-          const int sj = side_tile(kk);
+          const int sj = sc.step(kk);
           const bool with_side = sj >= 0;
           const int su = i * nr + sj;  // side-buffer use count
           if (with_side && su > 0) mbar_wait(side_empty, (su - 1) & 1);
@@ -259,9 +272,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
 #ifdef SERQ_DIAG_TS
         if (p.dbg_ts && lane_id() == 0 && i < 8) p.dbg_ts[512 + (blockIdx.x >> 1) * 64 + i * 8 + 1] = globaltimer();
 #endif
+        SideCursor sc = side_cursor();
         for (int kk = 0; kk < ks; ++kk, ++g) {
           const int s = g % kI8Stages;
           const uint32_t st = sb + s * kI8Stage;
+          const int sj = sc.step(kk);  // every lane: the cursor advances whether or not this lane issues
           const uint64_t a = make_sdesc(st, 16, 1024, 2), b = make_sdesc(st + kI8A, 16, 1024, 2);
           const uint32_t first = kk > 0 ? 1u : 0u;
           const bool no_mma = SERQ_DBG(p.dbg, (1 << 18));
@@ -269,7 +284,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
             mma_i8_pair(0, a, b, id_main, first);
             mma_i8_pair(0, a + 2, b + 2, id_main, 1u);
             mma_i8_pair(0, a + 4, b + 4, id_main, 1u);
-            const int sj = side_tile(kk);
             if (sj >= 0) {
               // salient term (side tile sj) into the second accumulator (columns [256, 512))
               const uint64_t ar = dense ? make_sdesc(sside, 16, 1024, 2) : a;

@@ -1,0 +1,241 @@
+// serq_gemv_i8.cuh -- integer SERQ linear at decode sizes (M <= 16 tokens).
+//
+// Y[t, n] = sx[t] * ( sw[n] * (acc[t, n] - zp[t] * colsum[n]) + R-term ),
+// acc[t, n] = sum_k c[t, k] w[n, k]        (int_gemm_reference, mxfmt.py:177-195;
+//                                           forward_reconstructed, compensate.py:300-316)
+//
+// At M <= 16 the layer is a weight stream (K x N int8 bytes), so the kernel is sized for HBM,
+// not for the tensor pipe: a CTA owns 16 weight rows and its 4 or 8 warps split K; each lane streams
+// 16-byte pieces of two weight rows with non-allocating loads, several 64-byte K chunks in
+// flight, and the products run as warp-level tensor-core MMAs (mma.sync m16n8k32, s8 weights x
+// u8 / s8 codes, s32 exact; the <= 16 tokens are the n8 side), far below the stream's time.
+// K-permutation: a lane holds bytes [16q, 16q + 16) of a 64-byte chunk of its row; the MMA pair
+// of that chunk reads them as logical k {4q..4q+3, 16+4q..} (bytes 0-7) and the same for bytes
+// 8-15 -- the activation fragments are loaded with the identical permutation, and a sum over k
+// does not depend on its order.  The warps' accumulator fragments meet in shared memory; the
+// zero-point correction is exact in wrapping int32 as in the CTA-pair kernel.  The salient term:
+// integer R (int8 [N, r] x the permuted slice = the first r codes, or the quantizer's gathered
+// codes; own scale and zero-point correction) or dense R (bf16 [N, r] x the quantizer's bf16
+// (codes - zp) slice, mma.sync m16n8k16 in fp32).
+#pragma once
+#include "serq_ptx.cuh"
+
+namespace serq {
+
+struct GemvI8Params {
+  const int8_t* w;          // [N, K] int8, K-major rows
+  int K, N, M;
+  const uint8_t* a;         // [M, K] activation codes (u8 asymmetric / s8 symmetric)
+  const float* sx;          // [M]
+  const int32_t* zp;        // [M] or nullptr (symmetric)
+  const float* sw;          // [N]
+  const int32_t* colsum;    // [N]
+  int r;                    // salient rank
+  const void* rw;           // int8 [N, r] (integer R) / bf16 [N, r] (dense R)
+  const float* sr;          // [N] integer-R scale
+  const int32_t* colsum_r;  // [N]
+  const void* xs;           // integer R: gathered codes [M, r] (nullptr: the first r codes of a);
+                            // dense R: bf16 (codes - zp) [M, r]
+  __nv_bfloat16* y;         // [M, ldy]
+  int64_t ldy;
+  const float* addend;      // optional fp32 [M, N] added after scaling (the SVD-baseline path)
+  int32_t* acc_dump;        // tests: exact accumulators acc - zp * colsum, [M, N]
+  int32_t* accr_dump;       // tests: exact integer-R accumulators
+};
+
+template <bool kSigned>
+__device__ __forceinline__ void mma_s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                       uint32_t b1) {
+  if constexpr (kSigned)
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  else
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint4 ld_stream16(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// one 64-byte K chunk: A = weight rows g / g + 8 (16 B each, bytes 16q..), B = token rows
+// f * 8 + g (16 B each); two m16n8k32 per token fragment
+template <int kNT, bool kSigned>
+__device__ __forceinline__ void gemv_mma_chunk(const uint4& wlo, const uint4& whi, const uint4 (&b)[kNT],
+                                               int (&acc)[kNT][4]) {
+#pragma unroll
+  for (int f = 0; f < kNT; ++f) {
+    mma_s8<kSigned>(acc[f], wlo.x, whi.x, wlo.y, whi.y, b[f].x, b[f].y);
+    mma_s8<kSigned>(acc[f], wlo.z, whi.z, wlo.w, whi.w, b[f].z, b[f].w);
+  }
+}
+
+// kNT: token fragments of 8 (1: M <= 8, 2: M <= 16); kR: 0 no salient term, kRInt, kRDense;
+// kWarps: warps splitting K (8 when there are few row groups, 4 otherwise: one wave of CTAs)
+template <int kNT, bool kSigned, int kR, int kWarps>
+__global__ void __launch_bounds__(32 * kWarps) serq_i8_gemv_kernel(const GemvI8Params p) {
+  __shared__ int red_i[kWarps][kNT][2][32][4];  // [warp][fragment][main | R][lane][c]
+  __shared__ float red_f[kWarps][kNT][32][4];   // dense R
+  pdl_launch_dependents();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int row0 = blockIdx.x * 16;
+  const int rlo = row0 + g, rhi = row0 + g + 8;
+  const bool ok_lo = rlo < p.N, ok_hi = rhi < p.N;
+  // this warp's K chunks (64 B each): a contiguous 1 / kWarps
+  const int nch = (p.K + 63) >> 6;
+  const int per = (nch + kWarps - 1) / kWarps;
+  const int c0 = warp * per, c1 = min(nch, c0 + per);
+  const int8_t* wlo_p = p.w + size_t(ok_lo ? rlo : 0) * p.K + 16 * q;
+  const int8_t* whi_p = p.w + size_t(ok_hi ? rhi : 0) * p.K + 16 * q;
+  auto wload = [&](const int8_t* base, bool ok, int c) {
+    return (ok && c < c1 && c * 64 + 16 * q < p.K) ? ld_stream16(base + size_t(c) * 64) : make_uint4(0, 0, 0, 0);
+  };
+  // the first weight chunks do not depend on the previous kernel: in flight before the wait
+  constexpr int kAhead = kWarps == 8 ? 6 : 4;  // 64-B chunks per row in flight per lane
+  uint4 wl[kAhead], wh[kAhead];
+#pragma unroll
+  for (int u = 0; u < kAhead; ++u) {
+    wl[u] = wload(wlo_p, ok_lo, c0 + u);
+    wh[u] = wload(whi_p, ok_hi, c0 + u);
+  }
+  pdl_wait();  // activation codes / scales come from the quantizer
+  int acc[kNT][4];
+#pragma unroll
+  for (int f = 0; f < kNT; ++f)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[f][i] = 0;
+  for (int c = c0; c < c1; c += kAhead) {
+#pragma unroll
+    for (int u = 0; u < kAhead; ++u) {
+      const uint4 lo = wl[u], hi = wh[u];
+      wl[u] = wload(wlo_p, ok_lo, c + u + kAhead);
+      wh[u] = wload(whi_p, ok_hi, c + u + kAhead);
+      if (c + u < c1) {
+        uint4 b[kNT];
+#pragma unroll
+        for (int f = 0; f < kNT; ++f) {
+          const int t = f * 8 + g;
+          b[f] = (t < p.M && (c + u) * 64 + 16 * q < p.K)
+                     ? __ldg(reinterpret_cast<const uint4*>(p.a + size_t(t) * p.K + size_t(c + u) * 64 + 16 * q))
+                     : make_uint4(0, 0, 0, 0);
+        }
+        gemv_mma_chunk<kNT, kSigned>(lo, hi, b, acc);
+      }
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < kNT; ++f)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) red_i[warp][f][0][lane][i] = acc[f][i];
+  // the salient term (r <= 128: at most two 64-byte chunks / eight 16-element bf16 chunks), warp 1
+  if constexpr (kR == kRInt) {
+    int accr[kNT][4];
+#pragma unroll
+    for (int f = 0; f < kNT; ++f)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) accr[f][i] = 0;
+    if (warp == 1) {
+      const uint8_t* ar = p.xs ? static_cast<const uint8_t*>(p.xs) : p.a;
+      const int lda = p.xs ? p.r : p.K;
+      const int8_t* rw = static_cast<const int8_t*>(p.rw);
+      for (int c = 0; c * 64 < p.r; ++c) {
+        const bool in = c * 64 + 16 * q < p.r;
+        const uint4 lo = (ok_lo && in) ? __ldg(reinterpret_cast<const uint4*>(rw + size_t(rlo) * p.r + c * 64 + 16 * q))
+                                       : make_uint4(0, 0, 0, 0);
+        const uint4 hi = (ok_hi && in) ? __ldg(reinterpret_cast<const uint4*>(rw + size_t(rhi) * p.r + c * 64 + 16 * q))
+                                       : make_uint4(0, 0, 0, 0);
+        uint4 b[kNT];
+#pragma unroll
+        for (int f = 0; f < kNT; ++f) {
+          const int t = f * 8 + g;
+          b[f] = (t < p.M && in) ? __ldg(reinterpret_cast<const uint4*>(ar + size_t(t) * lda + c * 64 + 16 * q))
+                                 : make_uint4(0, 0, 0, 0);
+        }
+        gemv_mma_chunk<kNT, kSigned>(lo, hi, b, accr);
+      }
+#pragma unroll
+      for (int f = 0; f < kNT; ++f)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) red_i[0][f][1][lane][i] = accr[f][i];
+    }
+  } else if constexpr (kR == kRDense) {
+    if (warp == 1) {
+      float accd[kNT][4];
+#pragma unroll
+      for (int f = 0; f < kNT; ++f)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) accd[f][i] = 0.f;
+      const __nv_bfloat16* rw = static_cast<const __nv_bfloat16*>(p.rw);
+      const __nv_bfloat16* xs = static_cast<const __nv_bfloat16*>(p.xs);
+      // 16-element chunks: a lane holds elements [4q, 4q + 4) (logical k {2q, 2q+1, 2q+8, 2q+9})
+      for (int c = 0; c * 16 < p.r; ++c) {
+        const bool in = c * 16 + 4 * q < p.r;
+        const uint2 lo = (ok_lo && in) ? *reinterpret_cast<const uint2*>(rw + size_t(rlo) * p.r + c * 16 + 4 * q)
+                                       : make_uint2(0, 0);
+        const uint2 hi = (ok_hi && in) ? *reinterpret_cast<const uint2*>(rw + size_t(rhi) * p.r + c * 16 + 4 * q)
+                                       : make_uint2(0, 0);
+#pragma unroll
+        for (int f = 0; f < kNT; ++f) {
+          const int t = f * 8 + g;
+          const uint2 b = (t < p.M && in) ? *reinterpret_cast<const uint2*>(xs + size_t(t) * p.r + c * 16 + 4 * q)
+                                          : make_uint2(0, 0);
+          mma_bf16(accd[f], lo.x, hi.x, lo.y, hi.y, b.x, b.y);
+        }
+      }
+#pragma unroll
+      for (int f = 0; f < kNT; ++f)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) red_f[0][f][lane][i] = accd[f][i];
+    }
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  // lane (g, q) of fragment f holds rows g / g + 8, tokens f * 8 + 2q / 2q + 1
+#pragma unroll
+  for (int f = 0; f < kNT; ++f)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int s = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) s += red_i[w][f][0][lane][i];  // exact
+      const int n = row0 + g + (i >= 2 ? 8 : 0);
+      const int t = f * 8 + 2 * q + (i & 1);
+      if (n >= p.N || t >= p.M) continue;
+      const uint32_t zp = p.zp ? uint32_t(p.zp[t]) : 0u;
+      const int32_t a_ref = int32_t(uint32_t(s) - zp * uint32_t(p.colsum[n]));  // wrapping int32, exact
+      float yv = float(a_ref) * p.sw[n];
+      if constexpr (kR == kRInt) {
+        const int32_t ar_ref = int32_t(uint32_t(red_i[0][f][1][lane][i]) - zp * uint32_t(p.colsum_r[n]));
+        yv += float(ar_ref) * p.sr[n];
+        if (p.accr_dump) p.accr_dump[size_t(t) * p.N + n] = ar_ref;
+      } else if constexpr (kR == kRDense) {
+        yv += red_f[0][f][lane][i];
+      }
+      if (p.acc_dump) p.acc_dump[size_t(t) * p.N + n] = a_ref;
+      float out = yv * p.sx[t];
+      if (p.addend) out += p.addend[size_t(t) * p.N + n];
+      p.y[size_t(t) * p.ldy + n] = __float2bfloat16_rn(out);
+    }
+}
+
+}  // namespace serq
