@@ -171,16 +171,18 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
                          (cluster_id / tiles_m) * 256 + int(rank) * 128, kEvictNormal);
       }
       pdl_wait();
-      uint32_t g = 0;
+      // stage slot and phase tracked incrementally (S is a runtime value: g % S, g / S would be
+      // integer divides in the issue loop)
+      int s = 0;
+      uint32_t ph = 0;
       for (int i = 0; i < my_tiles; ++i) {
         const int tile = cluster_id + i * n_clusters;
         const int mt = tile % tiles_m, nt = tile / tiles_m;
         const int m_own = mt * 256 + int(rank) * 128;
         const int n_half = nt * 256 + int(rank) * 128;
-        for (int kk = 0; kk < ks; ++kk, ++g) {
-          const int s = g % S;
+        for (int kk = 0; kk < ks; ++kk, s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0) ? 1u : 0u) {
           const bool preloaded = i == 0 && kk < pre;
-          if (!preloaded) mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
+          if (!preloaded) mbar_wait(&empty[s], ph ^ 1);
           const bool with_side = has_r && kk == 0;
           if (with_side && i > 0) mbar_wait(side_empty, (i - 1) & 1);
           const uint32_t fbar = map_rank(smem_u32(&full[s]), 0);
@@ -218,10 +220,12 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
         }
         return (unit & 1) * 256u;
       };
+      int s = 0, kg = 0;  // stage slot / phase and the K-step within the scale group, tracked incrementally
+      uint32_t ph = 0;
       for (int i = 0; i < my_tiles; ++i) {
-        for (int kk = 0; kk < ks; ++kk, ++g) {
-          const int s = g % S;
-          mbar_wait_cluster(&full[s], (g / S) & 1);
+        for (int kk = 0; kk < ks; ++kk, s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0) ? 1u : 0u,
+                 kg = (kg + 1 == p.gsteps) ? 0 : kg + 1) {
+          mbar_wait_cluster(&full[s], ph);
           tc_fence_after();
           const uint32_t st = sb + s * kI8gStage;
           const uint64_t a = make_sdesc(st, 16, 1024, 2), b = make_sdesc(st + kI8A, 16, 1024, 2);
@@ -244,7 +248,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
             tc_commit_pair(&acc_full[u & 1]);
             ++u;
           }
-          const int kg = kk % p.gsteps;
           const uint32_t d = kg == 0 ? claim(u) : (u & 1) * 256u;
           for (int j = 0; j < 4; ++j) mma_i8_pair(d, a + 2 * j, b + 2 * j, id_main, (kg > 0 || j > 0) ? 1u : 0u);
           tc_commit_pair(&empty[s]);
