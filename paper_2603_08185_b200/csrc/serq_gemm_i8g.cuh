@@ -212,7 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(96)
       const uint32_t sb = smem_u32(smem), sside = smem_u32(side);
       const uint32_t id_main = idesc_i8(256, 256, p.a_signed != 0, true);
       const uint32_t id_r = dense ? idesc_bf16(256, 256) : id_main;
-      uint32_t g = 0, u = 0;
+      uint32_t u = 0;
       auto claim = [&](uint32_t unit) {  // accumulator (unit & 1) free again?
         if (unit >= 2) {
           mbar_wait(&acc_empty[unit & 1], ((unit >> 1) & 1) ^ 1);
