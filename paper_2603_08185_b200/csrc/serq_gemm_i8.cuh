@@ -331,21 +331,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
     const uint32_t full_leader = map_rank(smem_u32(&full[0]), 0);
     const uint8_t* w4 = p.w4;
     const int total = my_tiles * ks;
-    auto block_of = [&](int g) {  // this CTA's contiguous kBHalf x 64 B block of K-step g
-      const int i = g / ks, kk = g - i * ks;
+    // this CTA's contiguous kBHalf x 64 B block of each K-step, walked by cursors (a division per
+    // tile, none per step: the loads run ahead at g + 3, the L2 prefetch at g + kPf)
+    auto tile_base = [&](int i) {
       const int tile = cluster_id + i * n_clusters;
       const int n_half = (tile / tiles_m) * kN + int(rank) * kBHalf;
-      return w4 + (size_t((n_half >> 7) * ks + kk) * 128 + (n_half & 127)) * 64;
+      return w4 + (size_t(n_half >> 7) * ks * 128 + (n_half & 127)) * 64;
     };
-    auto src_of = [&](int g) { return block_of(g) + r0 * 64 + c * 16; };
+    struct WCursor {
+      int i, kk;
+      const uint8_t* base;
+    };
+    auto next_block = [&](WCursor& cu) {
+      const uint8_t* b = cu.base + size_t(cu.kk) * 128 * 64;
+      if (++cu.kk == ks) {
+        cu.kk = 0;
+        if (++cu.i < my_tiles) cu.base = tile_base(cu.i);
+      }
+      return b;
+    };
+    WCursor load_cur{0, 0, my_tiles > 0 ? tile_base(0) : w4}, pf_cur = load_cur;
     // the register loads run 3 K-steps ahead; an L2 prefetch of the whole block kPf steps ahead
     constexpr int kPf = 8;
     if (lt == 0)
       for (int g = 0; g < kPf && g < total; ++g)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(block_of(g)), "r"(uint32_t(kBHalf * 64)) : "memory");
-    auto load = [&](uint4 (&b)[kJ], int g) {
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(next_block(pf_cur)), "r"(uint32_t(kBHalf * 64))
+                     : "memory");
+    auto load = [&](uint4 (&b)[kJ], int g) {  // called for g = 0, 1, 2, ... in order
       if (g < total && !SERQ_DBG(p.dbg, 1 << 10)) {  // diagnostics: no weight loads
-        const uint8_t* src = src_of(g);
+        const uint8_t* src = next_block(load_cur) + r0 * 64 + c * 16;
 #pragma unroll
         for (int j = 0; j < kJ; ++j) {
           uint4 v;
@@ -357,7 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
       }
     };
     // Four register buffers; a step's loads are issued three steps before its widen.  (Measured at
-    // C3: 127.8 us; rotating the buffers by name instead of shifting them -- no register copy
+    // C3: 127.8 us at the time; rotating the buffers by name instead of shifting them -- no register copy
     // waits on the step's own loads -- measured 150.6 us, and an L2 prefetch changed nothing.)
     uint4 b0[kJ], b1[kJ], b2[kJ], b3[kJ];
     load(b0, 0);
@@ -365,7 +379,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8Cfg<kE, kW4>::kThr
     load(b2, 2);
     for (int g = 0; g < total; ++g) {
       if (lt == 0 && g + kPf < total)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(block_of(g + kPf)), "r"(uint32_t(kBHalf * 64))
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(next_block(pf_cur)), "r"(uint32_t(kBHalf * 64))
                      : "memory");
       load(b3, g + 3);
       const int s = g % kI8Stages;
