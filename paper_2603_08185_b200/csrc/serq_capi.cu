@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <set>
 #include <string>
@@ -150,6 +151,23 @@ cudaError_t set_smem_attr(void (*kernel)(KArgs...), int bytes) {
   e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) done.insert(key);
   return e;
+}
+
+// resident CTAs per SM of a kernel at (threads, dynamic smem), cached per device
+template <typename... KArgs>
+int occupancy_of(void (*kernel)(KArgs...), int threads, int smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, reinterpret_cast<const void*>(kernel), threads, smem);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, size_t(smem)) != cudaSuccess || n < 1) n = 1;
+  cache[key] = n;
+  return n;
 }
 
 // scale factors as rows of 128 B (one 1-KB box = 2 SF chunks of a 128-row block)
@@ -394,7 +412,6 @@ static int act_quant_int_impl(const void* x, int dtype, int64_t M, int64_t K, in
     // codes) is latency-bound, so many resident rows per SM matter more than wide rows
     // (tools/int_quant_probe.py, C3 2048 x 4096: 12.3 us with 256 threads per row, 5.2 with 64)
     const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
-    const dim3 gq{unsigned(M)};
     const bool warp_rows = SERQ_DBG(g_debug_flags, (1 << 21)) != 0;  // diagnostics: one warp per row
     // threads per row by rows per SM: wider rows put more warps in flight when rows are few
     // (tools/probes/intq_grid_probe.py: 512 x 4096 5.95 / 4.84 / 4.37 us with 64 / 128 / 256
@@ -402,9 +419,14 @@ static int act_quant_int_impl(const void* x, int dtype, int64_t M, int64_t K, in
     const int64_t rows_per_sm = M / sm_count();
     const int tpr = warp_rows ? 32 : (K < 2048 ? 64 : rows_per_sm < 4 ? 256 : rows_per_sm < 16 ? 128 : 64);
     const int cpt = int(cdiv(K / 8, tpr));
-#define SERQ_INTQ(P, C)                                                                                         \
-  CK(launch_pdl(int_quant_bf16_kernel<P, C, P>, gq, dim3(P), 0, st, xb, int(M), int(K), ldx, bits, symmetric, codes, \
-                scale64, scale32, zp, salient_idx, r, xs_out, xs_kind, range, range_mode))
+    // persistent: at most the resident CTAs, each walking rows with the next row prefetched
+#define SERQ_INTQ(P, C)                                                                                              \
+  do {                                                                                                               \
+    auto kern = int_quant_bf16_kernel<P, C, P>;                                                                      \
+    const dim3 gp{unsigned(std::min<int64_t>(M, int64_t(sm_count()) * occupancy_of(kern, P, 0)))};                  \
+    CK(launch_pdl(kern, gp, dim3(P), 0, st, xb, int(M), int(K), ldx, bits, symmetric, codes, scale64, scale32, zp,    \
+                  salient_idx, r, xs_out, xs_kind, range, range_mode));                                               \
+  } while (0)
     if (warp_rows) {
       if (cpt <= 4) SERQ_INTQ(32, 4);
       else if (cpt <= 8) SERQ_INTQ(32, 8);

@@ -1302,17 +1302,30 @@ __global__ void __launch_bounds__(kBlock) int_quant_bf16_kernel(const __nv_bfloa
   pdl_launch_dependents();
   pdl_wait();
   const int rl = threadIdx.x / kTpr, t = threadIdx.x % kTpr;
-  const int64_t row = int64_t(blockIdx.x) * kRows + rl;
-  const bool row_ok = row < M;
-  const uint4* xr = reinterpret_cast<const uint4*>(x + (row_ok ? row : 0) * ldx);
   const int n8 = K >> 3;
+  // persistent over row groups (grid sized to the resident CTAs): the next group's rows are
+  // loaded into registers before this group's reduction -> scale -> codes chain runs
+  const int64_t rstride = int64_t(gridDim.x) * kRows;
+  auto load_row = [&](int64_t rw, uint4 (&dst)[kCpt]) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + (rw < M ? rw : 0) * ldx);
+#pragma unroll
+    for (int j = 0; j < kCpt; ++j) {
+      const int c8 = t + j * kTpr;
+      dst[j] = (rw < M && c8 < n8) ? __ldg(xr + c8) : make_uint4(0, 0, 0, 0);
+    }
+  };
   uint4 raw[kCpt];
+  load_row(int64_t(blockIdx.x) * kRows + rl, raw);
+  for (int64_t base = int64_t(blockIdx.x) * kRows; base < M; base += rstride) {
+  const int64_t row = base + rl;
+  const bool row_ok = row < M;
+  uint4 nxt[kCpt];
+  load_row(row + rstride, nxt);
   float lo = INFINITY, hi = -INFINITY;
 #pragma unroll
   for (int j = 0; j < kCpt; ++j) {
     const int c8 = t + j * kTpr;
     const bool ok = row_ok && c8 < n8;
-    raw[j] = ok ? __ldg(xr + c8) : make_uint4(0, 0, 0, 0);
     if (ok) {
       const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
 #pragma unroll
@@ -1367,7 +1380,7 @@ __global__ void __launch_bounds__(kBlock) int_quant_bf16_kernel(const __nv_bfloa
     }
   }
   __syncthreads();
-  if (!row_ok || range_mode == 1) return;
+  if (row_ok && range_mode != 1) {
   const double sc = s_scale[rl];
   const int zp = s_zp[rl];
   const float inv32 = s_inv32[rl];
@@ -1436,6 +1449,10 @@ __global__ void __launch_bounds__(kBlock) int_quant_bf16_kernel(const __nv_bfloa
         reinterpret_cast<int8_t*>(xs_out)[row * r + j] = int8_t(c);
     }
   }
+  }  // row_ok
+#pragma unroll
+  for (int j = 0; j < kCpt; ++j) raw[j] = nxt[j];
+  }  // row groups
 }
 
 // ------------------------------------------------------------------ packers
