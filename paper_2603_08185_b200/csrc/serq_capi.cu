@@ -1631,6 +1631,48 @@ int host_pipeline(serq_linear* h, const void* x_host, int64_t M, void* y_host, c
   g_launches = launches;
   CK(cudaStreamWaitEvent(st, ev_out[chunks - 1], 0));
   CK(cudaStreamSynchronize(st));
+#ifdef SERQ_DIAG
+  if (getenv("SERQ_E2E_TRACE")) {  // diagnostics: rerun with timing events, print the spans (us)
+    cudaEvent_t t0, th[kE2eMaxChunks], tc0[kE2eMaxChunks], tc[kE2eMaxChunks], to[kE2eMaxChunks];
+    cudaEventCreate(&t0);
+    for (int64_t c = 0; c < chunks; ++c) {
+      cudaEventCreate(&th[c]);
+      cudaEventCreate(&tc0[c]);
+      cudaEventCreate(&tc[c]);
+      cudaEventCreate(&to[c]);
+    }
+    cudaEventRecord(t0, st);
+    cudaStreamWaitEvent(h->e2e_in, t0, 0);
+    for (int64_t c = 0; c < chunks; ++c) {
+      cudaMemcpyAsync(static_cast<uint8_t*>(h->ws_x) + start[c] * h->K * 2,
+                      static_cast<const uint8_t*>(x_host) + start[c] * h->K * 2, plan[c] * h->K * 2,
+                      cudaMemcpyHostToDevice, h->e2e_in);
+      cudaEventRecord(th[c], h->e2e_in);
+    }
+    for (int64_t c = 0; c < chunks; ++c) {
+      cudaStreamWaitEvent(st, th[c], 0);
+      cudaEventRecord(tc0[c], st);
+      compute(start[c], plan[c]);
+      cudaEventRecord(tc[c], st);
+      cudaStreamWaitEvent(h->e2e_out, tc[c], 0);
+      cudaMemcpyAsync(static_cast<uint8_t*>(y_host) + start[c] * h->N * 2,
+                      static_cast<uint8_t*>(h->ws_y) + start[c] * h->N * 2, plan[c] * h->N * 2, cudaMemcpyDeviceToHost,
+                      h->e2e_out);
+      cudaEventRecord(to[c], h->e2e_out);
+    }
+    cudaStreamWaitEvent(st, to[chunks - 1], 0);
+    cudaStreamSynchronize(st);
+    for (int64_t c = 0; c < chunks; ++c) {
+      float a, b, d, e;
+      cudaEventElapsedTime(&a, t0, th[c]);
+      cudaEventElapsedTime(&b, t0, tc0[c]);
+      cudaEventElapsedTime(&d, t0, tc[c]);
+      cudaEventElapsedTime(&e, t0, to[c]);
+      fprintf(stderr, "e2e chunk %lld rows %lld: h2d_end %.1f compute %.1f..%.1f d2h_end %.1f\n", (long long)c,
+              (long long)plan[c], a * 1e3, b * 1e3, d * 1e3, e * 1e3);
+    }
+  }
+#endif
   return SERQ_OK;
 }
 
