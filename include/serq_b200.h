@@ -94,7 +94,7 @@ int serq_act_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64_t l
  * range -- range float [2, M]: range[m] = min, range[M + m] = max (exact: bf16 values) --
  * the ranks all-reduce MIN over range[0:M] and MAX over range[M:2M], and then quantize their
  * slice with serq_act_quant_int_ext on the global range: codes, scales and zero points equal
- * serq_act_quant_int of the unsharded row.  bf16 input, K % 8 == 0, K <= 8192. */
+ * serq_act_quant_int of the unsharded row.  bf16 input, K % 8 == 0, K <= 16384. */
 int serq_act_quant_int_range(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, float* range,
                              serq_stream_t stream);
 int serq_act_quant_int_ext(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, int bits, int symmetric,

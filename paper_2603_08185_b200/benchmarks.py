@@ -197,6 +197,27 @@ def decode_points(hbm_peak_gbs: float, layers: int = 16) -> list:
     return out
 
 
+def int_decode_points(hbm_peak_gbs: float, layers: int = 8) -> list:
+    """INT decode (serq_i8_gemv_kernel): Llama-2-7B up_proj / down_proj with int8 weights and an
+    integer R (r = 128), A8 asymmetric tokens, M = 1 / 4 / 16; ``layers`` distinct weight sets per
+    graph (> L2).  Bytes = int8 weights + R + scales / colsums + activations + outputs."""
+    out = []
+    for K, N in ((4096, 11008), (11008, 4096)):
+        lins = [device_int_linear(K, N, 128, "int", seed=1 + i) for i in range(layers)]
+        for M in (1, 4, 16):
+            xs = [outlier_x(M, K, seed=i) for i in range(layers)]
+            acts = [lins[0].quantize(x, 8, False) for x in xs]
+            ys = [torch.empty((M, N), dtype=torch.bfloat16, device="cuda") for _ in xs]
+            t_lin = time_steps(lambda i: lins[i % layers].gemm(acts[i % layers], ys[i % layers]), 2 * layers)
+            t_step = time_steps(lambda i: lins[i % layers].forward(xs[i % layers], 8, False, acts[i % layers],
+                                                                  ys[i % layers]), 2 * layers)
+            byts = K * N + 128 * N + 16 * N + M * K + 8 * M + 2 * M * N
+            out.append({"M": M, "K": K, "N": N, "r": 128, "kernel": D.last_kernel(), "step_us": t_step * 1e3,
+                        "linear_us": t_lin * 1e3, "linear_hbm_gbs": byts / (t_lin * 1e-3) / 1e9,
+                        "linear_hbm_frac": byts / (t_lin * 1e-3) / 1e9 / hbm_peak_gbs})
+    return out
+
+
 def decode_fused_points(hbm_peak_gbs: float, layers: int = 8) -> list:
     """Decode through FUSED linears (device.FusedMxLinear): Llama-2-7B gate/up (2 x 11008) and
     q/k/v (3 x 4096) as one handle each, every part with its own salient set (the gather

@@ -406,7 +406,7 @@ static int act_quant_int_impl(const void* x, int dtype, int64_t M, int64_t K, in
   if (xs_kind && (r <= 0 || r > K || !xs_out)) return fail(SERQ_EINVAL, "salient slice needs 0 < r <= K and xs_out");
   cudaStream_t st = S(stream);
   const dim3 grid(static_cast<unsigned>(M));
-  if (dtype == SERQ_BF16 && K % 8 == 0 && K <= 8192 && ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+  if (dtype == SERQ_BF16 && K % 8 == 0 && K <= 16384 && ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(codes) & 7) == 0) {
     // one token row per SMALL CTA: the per-row chain (load, min/max reduction, f64 scale,
     // codes) is latency-bound, so many resident rows per SM matter more than wide rows
@@ -417,7 +417,9 @@ static int act_quant_int_impl(const void* x, int dtype, int64_t M, int64_t K, in
     // (tools/probes/intq_grid_probe.py: 512 x 4096 5.95 / 4.84 / 4.37 us with 64 / 128 / 256
     // threads, 2048 x 4096 10.0 / 9.1 / 10.2 us)
     const int64_t rows_per_sm = M / sm_count();
-    const int tpr = warp_rows ? 32 : (K < 2048 ? 64 : rows_per_sm < 4 ? 256 : rows_per_sm < 16 ? 128 : 64);
+    // (rows above 8192 elements: 256 threads, up to 8 chunks of 8 per thread)
+    const int tpr = warp_rows ? 32
+                              : (K > 8192 ? 256 : K < 2048 ? 64 : rows_per_sm < 4 ? 256 : rows_per_sm < 16 ? 128 : 64);
     const int cpt = int(cdiv(K / 8, tpr));
     // persistent: at most the resident CTAs, each walking rows with the next row prefetched
 #define SERQ_INTQ(P, C)                                                                                              \
@@ -434,7 +436,8 @@ static int act_quant_int_impl(const void* x, int dtype, int64_t M, int64_t K, in
       else SERQ_INTQ(32, 32);
     } else if (tpr == 256) {
       if (cpt <= 2) SERQ_INTQ(256, 2);
-      else SERQ_INTQ(256, 4);
+      else if (cpt <= 4) SERQ_INTQ(256, 4);
+      else SERQ_INTQ(256, 8);
     } else if (tpr == 128) {
       if (cpt <= 2) SERQ_INTQ(128, 2);
       else if (cpt <= 4) SERQ_INTQ(128, 4);
@@ -450,7 +453,7 @@ static int act_quant_int_impl(const void* x, int dtype, int64_t M, int64_t K, in
     return SERQ_OK;
   }
   if (range_mode)
-    return fail(SERQ_EINVAL, "K-sharded per-token ranges need bf16 rows (16-B aligned, K %% 8 == 0, K <= 8192)");
+    return fail(SERQ_EINVAL, "K-sharded per-token ranges need bf16 rows (16-B aligned, K %% 8 == 0, K <= 16384)");
   switch (dtype) {
     case SERQ_BF16:
       int_quant_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), M, K, ldx, bits,

@@ -88,6 +88,20 @@ def test_mx_encode_acceptance_grid(D):
 # ---------------------------------------------------------------- K1-INT
 
 
+@pytest.mark.parametrize("M,K", [(1, 11008), (3, 16384), (200, 9216)])
+def test_int_quant_long_rows_bitexact(D, M, K):
+    # rows above 8192 elements (down_proj's 11008): the 256-thread kernel with 8 chunks per thread
+    x = _bf16_outlier_x(M, K, seed=K)
+    for bits, sym in ((8, False), (4, True)):
+        act = D.quantize_int(_cuda(x, torch.bfloat16), bits, sym)
+        cfg = O.IntCfg(bits, sym, "per-row")
+        ref = O.quantize_symmetric(x, cfg) if sym else O.quantize_asymmetric(x, cfg)
+        codes = act.codes.cpu().numpy()
+        codes = codes.astype(np.int32) if sym else codes.view(np.uint8).astype(np.int32)
+        assert np.array_equal(act.scale64.cpu().numpy(), ref.scales[:, 0])
+        assert np.array_equal(codes, ref.codes)
+
+
 @pytest.mark.parametrize("bits", [2, 4, 8])
 @pytest.mark.parametrize("symmetric", [True, False])
 @pytest.mark.parametrize("dtype", ["bf16", "f64"])
@@ -107,7 +121,7 @@ def test_int_quant_bitexact(D, bits, symmetric, dtype):
     assert np.array_equal(codes, ref.codes)
 
 
-@pytest.mark.parametrize("K", [1024, 4096, 8192])
+@pytest.mark.parametrize("K", [1024, 4096, 8192, 11008, 16384])
 def test_int_quant_exact_ties(D, K):
     # rows built so that x / s lands EXACTLY on k + 1/2 for many elements (s a power of two),
     # plus values a few ulps off the ties: the fast path must hand every one of them to the
