@@ -151,11 +151,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(st, &map_a, &full[s], kk * kStepBytes, m0, kEvictNormal);
           tma_load_2d(st + kSmemA, &map_b, &full[s], kk * kStepBytes, n0, kEvictNormal);
         } else {
+          // tensor-map coordinates are in elements: a 128-byte step is 64 bf16 (dense R)
+          const int rc = (kMode != kModeMX && p.r_mode == kRDense) ? kk * (kStepBytes / 2) : kk * kStepBytes;
           if (p.xs_is_x)
-            tma_load_2d(st, &map_a, &full[s], kk * kStepBytes, m0, kEvictNormal);
+            tma_load_2d(st, &map_a, &full[s], rc, m0, kEvictNormal);
           else
-            tma_load_2d(st, &map_xs, &full[s], kk * kStepBytes, m0, kEvictNormal);
-          tma_load_2d(st + kSmemA, &map_r, &full[s], kk * kStepBytes, n0, kEvictNormal);
+            tma_load_2d(st, &map_xs, &full[s], rc, m0, kEvictNormal);
+          tma_load_2d(st + kSmemA, &map_r, &full[s], rc, n0, kEvictNormal);
         }
         if (kMode == kModeMX) {
           const uint8_t* sa = rstep ? p.sfa_r : p.sfa;
