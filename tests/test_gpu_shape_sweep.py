@@ -129,3 +129,38 @@ def test_int_grouped_shape_sweep(D, M, K, N, g, r_mode, single_call):
     y_ref, _ = O.forward_int(x, main, comp, O.IntCfg(8, False, "per-row"))
     mx, mean = O.parity_errors(y, y_ref)
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (D.last_kernel(), mx, mean)
+
+
+def _odd_k_cases(n=24):
+    # K not a multiple of the 128-byte / 256-element steps (partial last K-step, padded SF chunks)
+    rng = np.random.default_rng(2029)
+    return [(int(rng.choice(MS)), int(rng.choice([96, 544, 2080])), int(rng.choice([16, 272, 1040])),
+             int(rng.choice([128, 520]))) for _ in range(n)]
+
+
+@pytest.mark.parametrize("M,Kmx,Kint,N", _odd_k_cases())
+def test_odd_k_sweep(D, M, Kmx, Kint, N):
+    rng = np.random.default_rng(M + Kmx + Kint + N)
+    # MX (K % 32 == 0): r = 32 salient columns
+    x = _x(M, Kmx, seed=M + 11)
+    w = rng.standard_normal((Kmx, N)) * 0.02
+    main_t, comp = O.build_serq_rtn_mx(w, np.arange(32), 32)
+    lin = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                     comp.r_q.block_scale_exponents, np.arange(32))
+    y = lin(_cuda(x, torch.bfloat16)).float().cpu().numpy()
+    mx, mean = O.parity_errors(y, O.forward_mx(x, main_t, comp))
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, ("mx", D.last_kernel(), mx, mean)
+    # INT (K % 16 == 0): integer R at r = 16
+    x = _x(M, Kint, seed=M + 12)
+    w = rng.standard_normal((Kint, N)) * 0.02
+    main, comp = O.build_per_channel_int(w, np.arange(16), r_mode="int")
+    lin = D.IntLinear(main.codes, main.scales, 4, r_codes=comp.r_q.codes, r_scales=comp.r_q.scales,
+                      salient_idx=np.arange(16))
+    act = lin.quantize(_cuda(x, torch.bfloat16), 8, False)
+    acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    y = lin.gemm(act, acc_dump=acc).float().cpu().numpy()
+    y_ref, xq = O.forward_int(x, main, comp, O.IntCfg(8, False, "per-row"))
+    _, parts = O.int_gemm(xq, main, return_partials=True)
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), parts[0][1]), ("int", D.last_kernel())
+    mx, mean = O.parity_errors(y, y_ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, ("int", D.last_kernel(), mx, mean)
