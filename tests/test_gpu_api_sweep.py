@@ -120,3 +120,39 @@ def test_quantizers_on_f32_f64_input(D, dtype, M, K):
         codes = codes.astype(np.int32) if sym else codes.view(np.uint8).astype(np.int32)
         assert np.array_equal(a.scale64.cpu().numpy(), q.scales[:, 0])
         assert np.array_equal(codes, q.codes)
+
+
+def test_threads_and_streams_share_a_layer(D):
+    # SPEC: pure functions, results independent of the thread count -- four host threads drive
+    # one MX and one INT layer on their own streams; every result equals the sequential one
+    import threading
+
+    K, N, r = 1024, 512, 64
+    rng = np.random.default_rng(77)
+    w = rng.standard_normal((K, N)) * 0.02
+    main_t, comp = O.build_serq_rtn_mx(w, np.arange(r), 32)
+    mxl = D.MxLinear(main_t.element_codes, main_t.block_scale_exponents, comp.r_q.element_codes,
+                     comp.r_q.block_scale_exponents, np.arange(r))
+    main, icomp = O.build_per_channel_int(w, np.arange(r), r_mode="int")
+    il = D.IntLinear(main.codes, main.scales, 4, r_codes=icomp.r_q.codes, r_scales=icomp.r_q.scales,
+                     salient_idx=np.arange(r))
+    xs = [_cuda(_x(m, K, seed=m), torch.bfloat16) for m in (1, 16, 200, 513)]
+    seq = [(mxl.forward(x).clone(), il.forward(x, 8, False).clone()) for x in xs]
+    torch.cuda.synchronize()
+    out = [None] * len(xs)
+
+    def work(i):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for _ in range(5):
+                out[i] = (mxl.forward(xs[i]), il.forward(xs[i], 8, False))
+        s.synchronize()
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(xs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    torch.cuda.synchronize()
+    for (a, b), (c, d) in zip(out, seq):
+        assert torch.equal(a, c) and torch.equal(b, d)
