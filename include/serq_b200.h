@@ -141,7 +141,20 @@ int serq_rmsnorm_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64
                            float* scale32, int32_t* zp, const int32_t* salient_idx, int r, void* xs_out, int xs_kind,
                            serq_stream_t stream);
 
-/* The reference's packed MX file body (mxfmt.py:228-251, after the 28-byte
+/* Decoder-block glue for decode-sized token counts (toy_block_graph, toymodel.py:88-124; the
+ * non-SERQ nodes, f32): res = x (+ o, bf16 [M, ldo], may be NULL), h = rmsnorm(res) * gain
+ * (saliency.py:194-196; res may be NULL); mid = silu(gate) * up (saliency.py:199-200; bf16 in,
+ * f32 out); and the token-batch attention (attention_mix, saliency.py:203-216) over M <= 16
+ * tokens, head_dim 128, reading q / k / v rows in place (e.g. column views of the fused q/k/v
+ * output).  All float32 row-major [M, H] unless a pitch is given. */
+int serq_block_add_rmsnorm(const float* x, const void* o, int64_t ldo, int64_t M, int64_t H, const float* gain,
+                           float eps, float* res, float* h, serq_stream_t stream);
+int serq_block_silu_mul(const void* gate, int64_t ldg, const void* up, int64_t ldu, int64_t M, int64_t F, float* mid,
+                        serq_stream_t stream);
+int serq_block_attention(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, int64_t M,
+                         int64_t heads, int64_t head_dim, float scale, float* out, int64_t ldo, serq_stream_t stream);
+
+/* The reference's packed MX file body/* The reference's packed MX file body (mxfmt.py:228-251, after the 28-byte
  * header; bundleio.py load path): rows x cols/32 records of 17 bytes (exponent
  * byte e+127, 16 nibble bytes, element 2i low) already in device memory ->
  * element codes uint8 [rows, cols] (16-B aligned) and exponents int32

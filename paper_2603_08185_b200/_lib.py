@@ -36,6 +36,9 @@ SIGNATURES = {
     "serq_act_quant_int_ext": (_I, [_P, _I, _I64, _I64, _I64, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _I, _P]),
     "serq_pack_mx": (_I, [_P, _P, _I64, _I64, _P, _P, _I, _I, _P, _P]),
     "serq_unpack_mx": (_I, [_P, _P, _I64, _I64, _P, _P, _P]),
+    "serq_block_add_rmsnorm": (_I, [_P, _P, _I64, _I64, _I64, _P, ctypes.c_float, _P, _P, _P]),
+    "serq_block_silu_mul": (_I, [_P, _I64, _P, _I64, _I64, _I64, _P, _P]),
+    "serq_block_attention": (_I, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, ctypes.c_float, _P, _I64, _P]),
     "serq_rmsnorm_quant_int": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, ctypes.c_double, _I, _I, _P, _P, _P, _P, _P, _I,
                                     _P, _I, _P]),
     "serq_mx_container_decode": (_I, [_P, _I64, _I64, _P, _P, _P]),

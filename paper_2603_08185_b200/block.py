@@ -62,7 +62,7 @@ class DeviceBlock:
     (the folded RMSNorm gains of the quantized bundle, toymodel.py:203-217)."""
 
     def __init__(self, linears: dict, gains: dict, head_dim: int, eps: float = 1e-6, device="cuda",
-                 fast_attention: bool = False):
+                 fast_attention: bool = False, glue_kernels: bool = True):
         """``linears`` may hold "qkv_proj" (q, k, v) and / or "up_gate_proj" (up, gate) as one
         ``device.FusedMxLinear`` (one quantizer + one kernel for the parts) instead of the parts."""
         self.qkv = linears.get("qkv_proj")
@@ -79,14 +79,20 @@ class DeviceBlock:
         self.head_dim = int(head_dim)
         self.eps = eps
         self.fast_attention = fast_attention
+        self.glue_kernels = glue_kernels  # M <= 16: the fused f32 glue kernels (csrc/serq_block.cuh)
 
     @classmethod
     def from_bundle(cls, bundle, head_dim: int, **kw) -> "DeviceBlock":
         return cls({n: bundle.linears[n].linear for n in LINEAR_NAMES}, bundle.nl_weights, head_dim, **kw)
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
-        """x [M, hidden] on the GPU -> block output float32 [M, hidden]."""
-        x = x.float()
+        """x [M, hidden] on the GPU -> block output float32 [M, hidden].  At M <= 16 (decode) the
+        non-SERQ glue runs as 4 fused f32 kernels (csrc/serq_block.cuh) instead of ~9 PyTorch
+        micro-kernels; larger batches use the PyTorch ops."""
+        x = x.float().contiguous()
+        m, hidden = x.shape
+        if self.glue_kernels and m <= 16 and self.head_dim == 128:
+            return self._forward_small(x)
         h1 = rmsnorm(x, self.g1, self.eps)
         if self.qkv is not None:
             q, k, v = (t.contiguous() for t in self.qkv.forward_parts(h1))
@@ -104,6 +110,37 @@ class DeviceBlock:
             up = self.lin["up_proj"](h2)
             gate = self.lin["gate_proj"](h2).float()
         mid = torch.nn.functional.silu(gate) * up
+        return res1 + self.lin["down_proj"](mid)
+
+    def _forward_small(self, x: torch.Tensor) -> torch.Tensor:
+        from . import _lib
+        from .device import _stream
+
+        m, hidden = x.shape
+        st = _stream()
+        h1 = torch.empty_like(x)
+        _lib.call("serq_block_add_rmsnorm", x.data_ptr(), None, 0, m, hidden, self.g1.data_ptr(), self.eps, None,
+                  h1.data_ptr(), st)
+        if self.qkv is not None:
+            q, k, v = self.qkv.forward_parts(h1)  # column views of one buffer (read in place)
+        else:
+            q, k, v = (self.lin[n](h1) for n in ("q_proj", "k_proj", "v_proj"))
+        attn = torch.empty_like(x)
+        _lib.call("serq_block_attention", q.data_ptr(), q.stride(0), k.data_ptr(), k.stride(0), v.data_ptr(),
+                  v.stride(0), m, hidden // self.head_dim, self.head_dim, 1.0 / math.sqrt(self.head_dim),
+                  attn.data_ptr(), hidden, st)
+        o = self.lin["o_proj"](attn)
+        res1, h2 = torch.empty_like(x), torch.empty_like(x)
+        _lib.call("serq_block_add_rmsnorm", x.data_ptr(), o.data_ptr(), o.stride(0), m, hidden, self.g2.data_ptr(),
+                  self.eps, res1.data_ptr(), h2.data_ptr(), st)
+        if self.up_gate is not None:
+            up, gate = self.up_gate.forward_parts(h2)
+        else:
+            up, gate = self.lin["up_proj"](h2), self.lin["gate_proj"](h2)
+        ffn = up.shape[1]
+        mid = torch.empty((m, ffn), dtype=torch.float32, device=x.device)
+        _lib.call("serq_block_silu_mul", gate.data_ptr(), gate.stride(0), up.data_ptr(), up.stride(0), m, ffn,
+                  mid.data_ptr(), st)
         return res1 + self.lin["down_proj"](mid)
 
     __call__ = forward

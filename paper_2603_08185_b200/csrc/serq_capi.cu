@@ -20,6 +20,7 @@
 #include "serq_gemm_i8.cuh"
 #include "serq_gemm_i8g.cuh"
 #include "serq_gemv_i8.cuh"
+#include "serq_block.cuh"
 #include "serq_quant.cuh"
 
 using namespace serq;
@@ -815,6 +816,42 @@ int serq_rmsnorm_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64
     CK(launch_pdl(rmsnorm_int_quant_kernel<float>, grid, blk, 0, st, static_cast<const float*>(x), M, K, ldx, gain, eps,
                   tree, bits, symmetric, codes, scale64, scale32, zp, salient_idx, r, xs_out, xs_kind));
   LAUNCH_CHECK("rmsnorm_int_quant_kernel");
+  return SERQ_OK;
+}
+
+// ---------------------------------------------------------------- block glue (M <= 16)
+int serq_block_add_rmsnorm(const float* x, const void* o, int64_t ldo, int64_t M, int64_t H, const float* gain,
+                           float eps, float* res, float* h, serq_stream_t stream) {
+  g_launches = 0;
+  if (M <= 0 || H <= 0 || !x || !gain || !h) return fail(SERQ_EINVAL, "add_rmsnorm needs x, gain, h and M, H > 0");
+  if (o && ldo < H) return fail(SERQ_EINVAL, "ldo < H");
+  CK(launch_pdl(block_add_rmsnorm_kernel, dim3(unsigned(M)), dim3(256), 0, S(stream), x,
+                static_cast<const __nv_bfloat16*>(o), ldo, int(M), int(H), gain, eps, res, h));
+  LAUNCH_CHECK("block_add_rmsnorm_kernel");
+  return SERQ_OK;
+}
+
+int serq_block_silu_mul(const void* gate, int64_t ldg, const void* up, int64_t ldu, int64_t M, int64_t F, float* mid,
+                        serq_stream_t stream) {
+  g_launches = 0;
+  if (M <= 0 || F <= 0 || !gate || !up || !mid || ldg < F || ldu < F) return fail(SERQ_EINVAL, "silu_mul arguments");
+  CK(launch_pdl(block_silu_mul_kernel, dim3(unsigned(cdiv(M * F, 256))), dim3(256), 0, S(stream),
+                static_cast<const __nv_bfloat16*>(gate), ldg, static_cast<const __nv_bfloat16*>(up), ldu, int(M),
+                int(F), mid));
+  LAUNCH_CHECK("block_silu_mul_kernel");
+  return SERQ_OK;
+}
+
+int serq_block_attention(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, int64_t M,
+                         int64_t heads, int64_t head_dim, float scale, float* out, int64_t ldo, serq_stream_t stream) {
+  g_launches = 0;
+  if (M <= 0 || M > 16) return fail(SERQ_EINVAL, "the small-batch attention takes 1..16 tokens, got %lld", (long long)M);
+  if (head_dim != 128 || heads <= 0) return fail(SERQ_EINVAL, "the small-batch attention needs head_dim 128");
+  if (!q || !k || !v || !out) return fail(SERQ_EINVAL, "attention pointers");
+  CK(launch_pdl(block_attention_small_kernel<16>, dim3(unsigned(heads), unsigned(M)), dim3(128), 0, S(stream),
+                static_cast<const __nv_bfloat16*>(q), ldq, static_cast<const __nv_bfloat16*>(k), ldk,
+                static_cast<const __nv_bfloat16*>(v), ldv, int(M), int(head_dim), scale, out, ldo));
+  LAUNCH_CHECK("block_attention_small_kernel");
   return SERQ_OK;
 }
 

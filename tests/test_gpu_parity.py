@@ -992,3 +992,65 @@ def test_device_block_fused_linears_match_separate(D, M):
     a, b = sep(x).cpu().numpy(), fus(x).cpu().numpy()
     mx, mean = O.parity_errors(b, a)
     assert mx <= TOL_MAX and mean <= 4e-3, (mx, mean)
+
+
+@pytest.mark.parametrize("M", [1, 5, 16])
+def test_block_glue_kernels_match_torch_ops(D, M):
+    # the decode-size glue (csrc/serq_block.cuh) against the PyTorch ops it replaces, f32
+    from paper_2603_08185_b200 import _lib
+    from paper_2603_08185_b200.block import attention_mix, rmsnorm
+
+    H, F, hd = 1024, 2048, 128
+    g = torch.Generator(device="cuda").manual_seed(M)
+    x = torch.randn((M, H), device="cuda", generator=g) * 3
+    o = (torch.randn((M, H), device="cuda", generator=g)).to(torch.bfloat16)
+    gain = torch.rand(H, device="cuda", generator=g) + 0.5
+    res, h = torch.empty_like(x), torch.empty_like(x)
+    _lib.call("serq_block_add_rmsnorm", x.data_ptr(), o.data_ptr(), H, M, H, gain.data_ptr(), 1e-6, res.data_ptr(),
+              h.data_ptr(), 0)
+    torch.cuda.synchronize()
+    r_ref = x + o
+    assert torch.equal(res, r_ref)
+    torch.testing.assert_close(h, rmsnorm(r_ref, gain, 1e-6), rtol=2e-6, atol=1e-6)
+    qkv = (torch.randn((M, 3 * H), device="cuda", generator=g) * 2).to(torch.bfloat16)
+    q, k, v = qkv[:, :H], qkv[:, H:2 * H], qkv[:, 2 * H:]
+    att = torch.empty((M, H), device="cuda")
+    _lib.call("serq_block_attention", q.data_ptr(), q.stride(0), k.data_ptr(), k.stride(0), v.data_ptr(), v.stride(0),
+              M, H // hd, hd, 1.0 / hd ** 0.5, att.data_ptr(), H, 0)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(att, attention_mix(q.contiguous(), k.contiguous(), v.contiguous(), hd), rtol=1e-4,
+                               atol=1e-5)
+    gate = torch.randn((M, 2 * F), device="cuda", generator=g).to(torch.bfloat16)
+    up, gt = gate[:, :F], gate[:, F:]
+    mid = torch.empty((M, F), device="cuda")
+    _lib.call("serq_block_silu_mul", gt.data_ptr(), gt.stride(0), up.data_ptr(), up.stride(0), M, F, mid.data_ptr(), 0)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(mid, torch.nn.functional.silu(gt.float()) * up, rtol=2e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("M", [1, 4, 16])
+def test_device_block_glue_path_matches_torch_path(D, M):
+    # the whole block at decode size: glue kernels vs the PyTorch glue, same SERQ linears
+    from paper_2603_08185_b200 import benchmarks as B
+    from paper_2603_08185_b200.block import DeviceBlock
+
+    H, F, r = 512, 1024, 64
+    rng = np.random.default_rng(M + 100)
+
+    def parts(k, n, s):
+        return B.device_mx_parts(k, n, r, seed=s, salient_idx=np.sort(rng.permutation(k)[:r]))
+
+    lins = {"qkv_proj": D.FusedMxLinear([parts(H, H, 1), parts(H, H, 2), parts(H, H, 3)]),
+            "up_gate_proj": D.FusedMxLinear([parts(H, F, 5), parts(H, F, 6)]),
+            "o_proj": D.MxLinear(*B.device_mx_parts(H, H, r, seed=4)),
+            "down_proj": D.MxLinear(*B.device_mx_parts(F, H, r, seed=7))}
+    gains = {"ln1": np.abs(rng.standard_normal(H)) + 0.5, "ln2": np.abs(rng.standard_normal(H)) + 0.5}
+    glue = DeviceBlock(lins, gains, 128)
+    ref = DeviceBlock(lins, gains, 128, glue_kernels=False)
+    x = B.outlier_x(M, H, mag=1.0).float()
+    a, b = glue(x).cpu().numpy(), ref(x).cpu().numpy()
+    # the two f32 RMSNorms sum in different orders; a last-ulp difference of an activation moves
+    # an MX code at an E2M1 decision point now and then and one bf16 output ulp propagates through
+    # five linears (as between the fused and separate blocks above): 1e-2 max / 4e-3 mean
+    mx, mean = O.parity_errors(a, b)
+    assert mx <= TOL_MAX and mean <= 4e-3, (mx, mean)

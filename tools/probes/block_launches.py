@@ -16,7 +16,11 @@ lins = {"qkv_proj": D.FusedMxLinear([pq, pk, pv]), "up_gate_proj": D.FusedMxLine
         "o_proj": D.MxLinear(*parts(H, H, False, 4)), "down_proj": D.MxLinear(*parts(F, H, False, 7))}
 blk = DeviceBlock(lins, {"ln1": np.ones(H), "ln2": np.ones(H)}, hd, fast_attention=True)
 x = B.outlier_x(M, H).float()
-for _ in range(3):
+for _ in range(2):
     blk(x)
 torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStart()  # ncu --profile-from-start off: one forward only
+blk(x)
+torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStop()
 print("ok")
