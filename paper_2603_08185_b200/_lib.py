@@ -14,7 +14,8 @@ import os
 from .errors import ValidationError
 
 LIB_NAME = "libserq_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# SERQ_B200_LIB: load another build of the same library (A/B timing of compile-time variants)
+LIB_PATH = os.environ.get("SERQ_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 SERQ_OK, SERQ_EINVAL, SERQ_ECUDA = 0, 1, 2
 SERQ_BF16, SERQ_F32, SERQ_F64 = 0, 1, 2

@@ -197,13 +197,15 @@ def decode_points(hbm_peak_gbs: float, layers: int = 16) -> list:
     return out
 
 
-def int_decode_points(hbm_peak_gbs: float, layers: int = 8) -> list:
-    """INT decode (serq_i8_gemv_kernel): Llama-2-7B up_proj / down_proj with int8 weights and an
-    integer R (r = 128), A8 asymmetric tokens, M = 1 / 4 / 16; ``layers`` distinct weight sets per
-    graph (> L2).  Bytes = int8 weights + R + scales / colsums + activations + outputs."""
+def int_decode_points(hbm_peak_gbs: float, layers: int = 8, weight_format: str = "int8") -> list:
+    """INT decode (serq_i8_gemv_kernel): Llama-2-7B up_proj / down_proj with int8 or packed INT4
+    (``weight_format``) weights and an integer R (r = 128), A8 asymmetric tokens, M = 1 / 4 / 16;
+    ``layers`` distinct weight sets per graph (> L2).  Bytes = resident weights + R + scales /
+    colsums + activations + outputs."""
     out = []
     for K, N in ((4096, 11008), (11008, 4096)):
-        lins = [device_int_linear(K, N, 128, "int", seed=1 + i) for i in range(layers)]
+        lins = [device_int_linear(K, N, 128, "int", seed=1 + i, weight_format=weight_format) for i in range(layers)]
+        wbytes = lins[0].weight_bytes()[0]
         for M in (1, 4, 16):
             xs = [outlier_x(M, K, seed=i) for i in range(layers)]
             acts = [lins[0].quantize(x, 8, False) for x in xs]
@@ -211,9 +213,10 @@ def int_decode_points(hbm_peak_gbs: float, layers: int = 8) -> list:
             t_lin = time_steps(lambda i: lins[i % layers].gemm(acts[i % layers], ys[i % layers]), 2 * layers)
             t_step = time_steps(lambda i: lins[i % layers].forward(xs[i % layers], 8, False, acts[i % layers],
                                                                   ys[i % layers]), 2 * layers)
-            byts = K * N + 128 * N + 16 * N + M * K + 8 * M + 2 * M * N
-            out.append({"M": M, "K": K, "N": N, "r": 128, "kernel": D.last_kernel(), "step_us": t_step * 1e3,
-                        "linear_us": t_lin * 1e3, "linear_hbm_gbs": byts / (t_lin * 1e-3) / 1e9,
+            byts = wbytes + 128 * N + 16 * N + M * K + 8 * M + 2 * M * N
+            out.append({"M": M, "K": K, "N": N, "r": 128, "weights": weight_format, "kernel": D.last_kernel(),
+                        "step_us": t_step * 1e3, "linear_us": t_lin * 1e3,
+                        "linear_hbm_gbs": byts / (t_lin * 1e-3) / 1e9,
                         "linear_hbm_frac": byts / (t_lin * 1e-3) / 1e9 / hbm_peak_gbs})
     return out
 
@@ -263,7 +266,8 @@ def decode_fused_points(hbm_peak_gbs: float, layers: int = 8) -> list:
     return out
 
 
-def device_int_linear(K: int, N: int, r: int, r_mode: str, seed: int = 1, group: int | None = None):
+def device_int_linear(K: int, N: int, r: int, r_mode: str, seed: int = 1, group: int | None = None,
+                      weight_format: str = "int8"):
     """Synthetic SERQ INT4 linear (SURVEY F4 composition): W ~ N(0, 0.02) [K, N];
     main = symmetric INT4 with one scale per output column (``group`` None) or
     per (row group of ``group`` input rows, column); R = residual
@@ -286,7 +290,8 @@ def device_int_linear(K: int, N: int, r: int, r_mode: str, seed: int = 1, group:
             sr = torch.where(sr == 0, torch.ones_like(sr), sr)
             kw = dict(r_codes=torch.clamp(torch.round(resid / sr), -7, 7).to(torch.int32), r_scales=sr,
                       salient_idx=np.arange(r))
-    return D.IntLinear(codes, s if group is not None else s.reshape(-1), 4, group_size=gs, **kw)
+    return D.IntLinear(codes, s if group is not None else s.reshape(-1), 4, group_size=gs,
+                       weight_format=weight_format, **kw)
 
 
 def int_linear_point(M, K, N, r, r_mode, bits, symmetric, flush: Flusher | None = None, n_steps: int = 16,

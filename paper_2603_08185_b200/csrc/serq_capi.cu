@@ -1369,8 +1369,8 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   const bool need_xs = h->r_mode == SERQ_R_DENSE || h->r_mode == SERQ_R_DENSE_SPLIT ||
                        (h->r_mode == SERQ_R_INT && !h->contiguous);
   if (need_xs && !xs) return fail(SERQ_EINVAL, "this R mode needs the quantizer's xs slice");
-  if (M <= 16 && !h->use_i8g && !h->has_w4 && h->r <= 128 && !SERQ_DBG(g_debug_flags, 1 << 29)) {
-    // decode sizes: the weight stream with warp-level MMAs (serq_gemv_i8.cuh)
+  if (M <= 16 && !h->use_i8g && h->r <= 128 && !SERQ_DBG(g_debug_flags, 1 << 29)) {
+    // decode sizes: the weight stream with warp-level MMAs (serq_gemv_i8.cuh), int8 or packed INT4
     GemvI8Params gp{};
     gp.w = static_cast<const int8_t*>(h->w);
     gp.K = int(h->K);
@@ -1392,15 +1392,21 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     gp.acc_dump = acc_dump;
     gp.accr_dump = accr_dump;
     const bool sgn = zp == nullptr;
-    // 16 weight rows per CTA; 8 warps split K when the row groups alone leave SMs idle (a wave
-    // holds ~2 such CTAs per SM), 4 otherwise (all CTAs in one wave)
+    // 16 weight rows per CTA; 8 (M <= 8) / 7 warps split K when the row groups alone leave SMs
+    // idle (a wave holds 2 such CTAs per SM), 4 otherwise (all CTAs in one wave); plus one warp
+    // for the salient term and the epilogue (tools/probes/int_decode_probe.py for the A/B)
     const int64_t groups = cdiv(h->N, 16);
     const bool wide = groups <= 2 * int64_t(sm_count());
-    const dim3 grid{unsigned(groups)}, blk{wide ? 256u : 128u};
+    const dim3 grid{unsigned(groups)}, blk{!wide ? 160u : M <= 8 ? 288u : 256u};  // + the side / epilogue warp
     cudaError_t e = cudaSuccess;
+#define GEMV_W4(NT, SG, KR, W4)                                                                                     \
+  e = wide ? launch_pdl(serq_i8_gemv_kernel<NT, SG, KR, NT == 1 ? 8 : 7, W4>, grid, blk, 0, S(stream), gp)        \
+           : launch_pdl(serq_i8_gemv_kernel<NT, SG, KR, 4, W4>, grid, blk, 0, S(stream), gp)
 #define GEMV_W(NT, SG, KR)                                                                                          \
-  e = wide ? launch_pdl(serq_i8_gemv_kernel<NT, SG, KR, 8>, grid, blk, 0, S(stream), gp)                           \
-           : launch_pdl(serq_i8_gemv_kernel<NT, SG, KR, 4>, grid, blk, 0, S(stream), gp)
+  do {                                                                                                             \
+    if (h->has_w4) GEMV_W4(NT, SG, KR, true);                                                                      \
+    else GEMV_W4(NT, SG, KR, false);                                                                               \
+  } while (0)
 #define GEMV_R(NT, KR)                                                                                              \
   do {                                                                                                             \
     if (sgn) GEMV_W(NT, true, KR);                                                                                 \
@@ -1417,6 +1423,7 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
 #undef GEMV_M
 #undef GEMV_R
 #undef GEMV_W
+#undef GEMV_W4
     CK(e);
     LAUNCH_CHECK("serq_i8_gemv_kernel");
     return SERQ_OK;

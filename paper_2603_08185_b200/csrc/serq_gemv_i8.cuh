@@ -19,11 +19,21 @@
 // (codes - zp) slice, mma.sync m16n8k16 in fp32).
 #pragma once
 #include "serq_ptx.cuh"
+#include "serq_gemm_i8.cuh"  // widen_int4x8
+
+// minimum resident CTAs: 5 of the 4 + 1-warp CTAs (<= 80 registers: the whole grid of a
+// 11008-row layer in one wave), 2 of the wider ones (<= 112)
+#ifndef SERQ_GEMV_MINB4
+#define SERQ_GEMV_MINB4 5
+#endif
+#ifndef SERQ_GEMV_MINB8
+#define SERQ_GEMV_MINB8 2
+#endif
 
 namespace serq {
 
 struct GemvI8Params {
-  const int8_t* w;          // [N, K] int8, K-major rows
+  const int8_t* w;          // [N, K] int8, K-major rows; kW4: packed INT4 tiled [N/128][K/128][128 rows][64 B]
   int K, N, M;
   const uint8_t* a;         // [M, K] activation codes (u8 asymmetric / s8 symmetric)
   const float* sx;          // [M]
@@ -90,126 +100,191 @@ __device__ __forceinline__ void gemv_mma_chunk(const uint4& wlo, const uint4& wh
 }
 
 // kNT: token fragments of 8 (1: M <= 8, 2: M <= 16); kR: 0 no salient term, kRInt, kRDense;
-// kWarps: warps splitting K (8 when there are few row groups, 4 otherwise: one wave of CTAs)
-template <int kNT, bool kSigned, int kR, int kWarps>
-__global__ void __launch_bounds__(32 * kWarps) serq_i8_gemv_kernel(const GemvI8Params p) {
-  __shared__ int red_i[kWarps][kNT][2][32][4];  // [warp][fragment][main | R][lane][c]
-  __shared__ float red_f[kWarps][kNT][32][4];   // dense R
+// kWarps: warps splitting K (8 when there are few row groups, 4 otherwise: one wave of CTAs);
+// kW4: the weights are the CTA-pair kernel's packed INT4 layout (pack_int4_tiled_kernel: per
+// 128-row tile and 128-K step, 64 B per row, so a CTA's 16 rows are one contiguous 1 KB); a K
+// "chunk" is then 128 elements, a lane's 16 B are its rows' elements [32q, 32q + 32) of it, widened
+// in registers (widen_int4x8, natural order) to the two 16-B pieces the int8 path would have loaded
+template <int kNT, bool kSigned, int kR, int kWarps, bool kW4 = false>
+__global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MINB4 : SERQ_GEMV_MINB8) serq_i8_gemv_kernel(const GemvI8Params p) {
+  __shared__ int red_i[kWarps][kNT][32][4];  // [main warp][fragment][lane][c]
   pdl_launch_dependents();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int row0 = blockIdx.x * 16;
   const int rlo = row0 + g, rhi = row0 + g + 8;
   const bool ok_lo = rlo < p.N, ok_hi = rhi < p.N;
-  // this warp's K chunks (64 B each): a contiguous 1 / kWarps
-  const int nch = (p.K + 63) >> 6;
-  const int per = (nch + kWarps - 1) / kWarps;
-  const int c0 = warp * per, c1 = min(nch, c0 + per);
-  const int8_t* wlo_p = p.w + size_t(ok_lo ? rlo : 0) * p.K + 16 * q;
-  const int8_t* whi_p = p.w + size_t(ok_hi ? rhi : 0) * p.K + 16 * q;
-  auto wload = [&](const int8_t* base, bool ok, int c) {
-    return (ok && c < c1 && c * 64 + 16 * q < p.K) ? ld_stream16(base + size_t(c) * 64) : make_uint4(0, 0, 0, 0);
-  };
-  // the first weight chunks do not depend on the previous kernel: in flight before the wait
-  constexpr int kAhead = kWarps == 8 ? 6 : 4;  // 64-B chunks per row in flight per lane
-  uint4 wl[kAhead], wh[kAhead];
-#pragma unroll
-  for (int u = 0; u < kAhead; ++u) {
-    wl[u] = wload(wlo_p, ok_lo, c0 + u);
-    wh[u] = wload(whi_p, ok_hi, c0 + u);
-  }
-  pdl_wait();  // activation codes / scales come from the quantizer
-  int acc[kNT][4];
-#pragma unroll
-  for (int f = 0; f < kNT; ++f)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) acc[f][i] = 0;
-  for (int c = c0; c < c1; c += kAhead) {
+  if (warp < kWarps) {
+    // ---- main warps: this warp's K chunks (64 elements each; 128 packed INT4), a contiguous 1 / kWarps
+    constexpr int kChunk = kW4 ? 128 : 64;
+    const int nch = (p.K + kChunk - 1) / kChunk;
+    const int per = (nch + kWarps - 1) / kWarps;
+    const int c0 = warp * per, c1 = min(nch, c0 + per);
+    const int8_t* wlo_p;
+    const int8_t* whi_p;
+    size_t cstride;  // bytes from one chunk of a row to the next
+    if constexpr (kW4) {
+      const int rl = ok_lo ? rlo : 0, rh = ok_hi ? rhi : 0;
+      wlo_p = p.w + (size_t(rl >> 7) * nch * 128 + (rl & 127)) * 64 + 16 * q;
+      whi_p = p.w + (size_t(rh >> 7) * nch * 128 + (rh & 127)) * 64 + 16 * q;
+      cstride = 128 * 64;
+    } else {
+      wlo_p = p.w + size_t(ok_lo ? rlo : 0) * p.K + 16 * q;
+      whi_p = p.w + size_t(ok_hi ? rhi : 0) * p.K + 16 * q;
+      cstride = 64;
+    }
+    auto wload = [&](const int8_t* base, bool ok, int c) {
+      // (W4: the packed tail beyond K is zero nibbles, written at pack time)
+      return (ok && c < c1 && (kW4 || c * 64 + 16 * q < p.K)) ? ld_stream16(base + size_t(c) * cstride)
+                                                               : make_uint4(0, 0, 0, 0);
+    };
+    // the first weight chunks do not depend on the previous kernel: in flight before the wait
+    constexpr int kAhead = kWarps > 4 ? 6 : 4;  // chunks per row in flight per lane
+    uint4 wl[kAhead], wh[kAhead];
 #pragma unroll
     for (int u = 0; u < kAhead; ++u) {
-      const uint4 lo = wl[u], hi = wh[u];
-      wl[u] = wload(wlo_p, ok_lo, c + u + kAhead);
-      wh[u] = wload(whi_p, ok_hi, c + u + kAhead);
-      if (c + u < c1) {
-        uint4 b[kNT];
-#pragma unroll
-        for (int f = 0; f < kNT; ++f) {
-          const int t = f * 8 + g;
-          b[f] = (t < p.M && (c + u) * 64 + 16 * q < p.K)
-                     ? __ldg(reinterpret_cast<const uint4*>(p.a + size_t(t) * p.K + size_t(c + u) * 64 + 16 * q))
-                     : make_uint4(0, 0, 0, 0);
-        }
-        gemv_mma_chunk<kNT, kSigned>(lo, hi, b, acc);
-      }
+      wl[u] = wload(wlo_p, ok_lo, c0 + u);
+      wh[u] = wload(whi_p, ok_hi, c0 + u);
     }
-  }
-#pragma unroll
-  for (int f = 0; f < kNT; ++f)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) red_i[warp][f][0][lane][i] = acc[f][i];
-  // the salient term (r <= 128: at most two 64-byte chunks / eight 16-element bf16 chunks), warp 1
-  if constexpr (kR == kRInt) {
-    int accr[kNT][4];
+    pdl_wait();  // activation codes come from the quantizer
+    int acc[kNT][4];
 #pragma unroll
     for (int f = 0; f < kNT; ++f)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) accr[f][i] = 0;
-    if (warp == 1) {
-      const uint8_t* ar = p.xs ? static_cast<const uint8_t*>(p.xs) : p.a;
-      const int lda = p.xs ? p.r : p.K;
-      const int8_t* rw = static_cast<const int8_t*>(p.rw);
-      for (int c = 0; c * 64 < p.r; ++c) {
-        const bool in = c * 64 + 16 * q < p.r;
-        const uint4 lo = (ok_lo && in) ? __ldg(reinterpret_cast<const uint4*>(rw + size_t(rlo) * p.r + c * 64 + 16 * q))
-                                       : make_uint4(0, 0, 0, 0);
-        const uint4 hi = (ok_hi && in) ? __ldg(reinterpret_cast<const uint4*>(rw + size_t(rhi) * p.r + c * 64 + 16 * q))
-                                       : make_uint4(0, 0, 0, 0);
-        uint4 b[kNT];
+      for (int i = 0; i < 4; ++i) acc[f][i] = 0;
+    // the token fragments of the 16 activation bytes at element k of each token row
+    auto act = [&](int k, uint4 (&b)[kNT]) {
 #pragma unroll
-        for (int f = 0; f < kNT; ++f) {
-          const int t = f * 8 + g;
-          b[f] = (t < p.M && in) ? __ldg(reinterpret_cast<const uint4*>(ar + size_t(t) * lda + c * 64 + 16 * q))
-                                 : make_uint4(0, 0, 0, 0);
-        }
-        gemv_mma_chunk<kNT, kSigned>(lo, hi, b, accr);
+      for (int f = 0; f < kNT; ++f) {
+        const int t = f * 8 + g;
+        b[f] = (t < p.M && k < p.K) ? __ldg(reinterpret_cast<const uint4*>(p.a + size_t(t) * p.K + k))
+                                    : make_uint4(0, 0, 0, 0);
       }
+    };
+    for (int c = c0; c < c1; c += kAhead) {
 #pragma unroll
-      for (int f = 0; f < kNT; ++f)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) red_i[0][f][1][lane][i] = accr[f][i];
+      for (int u = 0; u < kAhead; ++u) {
+        const uint4 lo = wl[u], hi = wh[u];
+        wl[u] = wload(wlo_p, ok_lo, c + u + kAhead);
+        wh[u] = wload(whi_p, ok_hi, c + u + kAhead);
+        if (c + u < c1) {
+          uint4 b[kNT];
+          if constexpr (kW4) {
+            const uint2 l0 = widen_int4x8(lo.x), l1 = widen_int4x8(lo.y), l2 = widen_int4x8(lo.z),
+                        l3 = widen_int4x8(lo.w);
+            const uint2 h0 = widen_int4x8(hi.x), h1 = widen_int4x8(hi.y), h2 = widen_int4x8(hi.z),
+                        h3 = widen_int4x8(hi.w);
+            const int k = (c + u) * 128 + 32 * q;
+            act(k, b);
+            gemv_mma_chunk<kNT, kSigned>(make_uint4(l0.x, l0.y, l1.x, l1.y), make_uint4(h0.x, h0.y, h1.x, h1.y), b,
+                                         acc);
+            act(k + 16, b);
+            gemv_mma_chunk<kNT, kSigned>(make_uint4(l2.x, l2.y, l3.x, l3.y), make_uint4(h2.x, h2.y, h3.x, h3.y), b,
+                                         acc);
+          } else {
+            act((c + u) * 64 + 16 * q, b);
+            gemv_mma_chunk<kNT, kSigned>(lo, hi, b, acc);
+          }
+        }
+      }
     }
-  } else if constexpr (kR == kRDense) {
-    if (warp == 1) {
-      float accd[kNT][4];
 #pragma unroll
-      for (int f = 0; f < kNT; ++f)
+    for (int f = 0; f < kNT; ++f)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) accd[f][i] = 0.f;
-      const __nv_bfloat16* rw = static_cast<const __nv_bfloat16*>(p.rw);
-      const __nv_bfloat16* xs = static_cast<const __nv_bfloat16*>(p.xs);
-      // 16-element chunks: a lane holds elements [4q, 4q + 4) (logical k {2q, 2q+1, 2q+8, 2q+9})
-      for (int c = 0; c * 16 < p.r; ++c) {
-        const bool in = c * 16 + 4 * q < p.r;
-        const uint2 lo = (ok_lo && in) ? *reinterpret_cast<const uint2*>(rw + size_t(rlo) * p.r + c * 16 + 4 * q)
-                                       : make_uint2(0, 0);
-        const uint2 hi = (ok_hi && in) ? *reinterpret_cast<const uint2*>(rw + size_t(rhi) * p.r + c * 16 + 4 * q)
-                                       : make_uint2(0, 0);
+      for (int i = 0; i < 4; ++i) red_i[warp][f][lane][i] = acc[f][i];
+    __syncthreads();
+    return;
+  }
+  // ---- the side warp: the salient term and the epilogue.  Its weights (R rows, r <= 128) and
+  // the per-column constants do not depend on the previous kernel either: loaded before the
+  // wait, so after it only the activation reads and the main warps' results remain.
+  int32_t cs[2] = {0, 0}, csr[2] = {0, 0};
+  float swv[2] = {0.f, 0.f}, srv[2] = {0.f, 0.f};
 #pragma unroll
-        for (int f = 0; f < kNT; ++f) {
-          const int t = f * 8 + g;
-          const uint2 b = (t < p.M && in) ? *reinterpret_cast<const uint2*>(xs + size_t(t) * p.r + c * 16 + 4 * q)
-                                          : make_uint2(0, 0);
-          mma_bf16(accd[f], lo.x, hi.x, lo.y, hi.y, b.x, b.y);
-        }
+  for (int h = 0; h < 2; ++h) {
+    const int n = h ? rhi : rlo;
+    if (n < p.N) {
+      cs[h] = __ldg(p.colsum + n);
+      swv[h] = __ldg(p.sw + n);
+      if constexpr (kR == kRInt) {
+        csr[h] = __ldg(p.colsum_r + n);
+        srv[h] = __ldg(p.sr + n);
       }
-#pragma unroll
-      for (int f = 0; f < kNT; ++f)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) red_f[0][f][lane][i] = accd[f][i];
     }
   }
+  int accr[kNT][4];   // integer R: exact s32
+  float accd[kNT][4]; // dense R: fp32
+#pragma unroll
+  for (int f = 0; f < kNT; ++f)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      accr[f][i] = 0;
+      accd[f][i] = 0.f;
+    }
+  if constexpr (kR == kRInt) {
+    const int8_t* rw = static_cast<const int8_t*>(p.rw);
+    uint4 rwl[2], rwh[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const bool in = c * 64 + 16 * q < p.r;
+      rwl[c] = (ok_lo && in) ? __ldg(reinterpret_cast<const uint4*>(rw + size_t(rlo) * p.r + c * 64 + 16 * q))
+                             : make_uint4(0, 0, 0, 0);
+      rwh[c] = (ok_hi && in) ? __ldg(reinterpret_cast<const uint4*>(rw + size_t(rhi) * p.r + c * 64 + 16 * q))
+                             : make_uint4(0, 0, 0, 0);
+    }
+    pdl_wait();
+    const uint8_t* ar = p.xs ? static_cast<const uint8_t*>(p.xs) : p.a;
+    const int lda = p.xs ? p.r : p.K;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const bool in = c * 64 + 16 * q < p.r;
+      uint4 b[kNT];
+#pragma unroll
+      for (int f = 0; f < kNT; ++f) {
+        const int t = f * 8 + g;
+        b[f] = (t < p.M && in) ? __ldg(reinterpret_cast<const uint4*>(ar + size_t(t) * lda + c * 64 + 16 * q))
+                               : make_uint4(0, 0, 0, 0);
+      }
+      gemv_mma_chunk<kNT, kSigned>(rwl[c], rwh[c], b, accr);
+    }
+  } else if constexpr (kR == kRDense) {
+    const __nv_bfloat16* rw = static_cast<const __nv_bfloat16*>(p.rw);
+    const __nv_bfloat16* xs = static_cast<const __nv_bfloat16*>(p.xs);
+    // 16-element chunks (r <= 128: eight): a lane holds elements [4q, 4q + 4) (logical k {2q, 2q+1, 2q+8, 2q+9})
+    uint2 rl[8], rh[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const bool in = c * 16 + 4 * q < p.r;
+      rl[c] = (ok_lo && in) ? *reinterpret_cast<const uint2*>(rw + size_t(rlo) * p.r + c * 16 + 4 * q) : make_uint2(0, 0);
+      rh[c] = (ok_hi && in) ? *reinterpret_cast<const uint2*>(rw + size_t(rhi) * p.r + c * 16 + 4 * q) : make_uint2(0, 0);
+    }
+    pdl_wait();
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const bool in = c * 16 + 4 * q < p.r;
+#pragma unroll
+      for (int f = 0; f < kNT; ++f) {
+        const int t = f * 8 + g;
+        const uint2 b = (t < p.M && in) ? *reinterpret_cast<const uint2*>(xs + size_t(t) * p.r + c * 16 + 4 * q)
+                                        : make_uint2(0, 0);
+        mma_bf16(accd[f], rl[c].x, rh[c].x, rl[c].y, rh[c].y, b.x, b.y);
+      }
+    }
+  } else {
+    pdl_wait();
+  }
+  // per-token scale / zero point (written by the quantizer): after the wait
+  float sxv[kNT][2];
+  uint32_t zpv[kNT][2];
+#pragma unroll
+  for (int f = 0; f < kNT; ++f)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int t = f * 8 + 2 * q + j;
+      sxv[f][j] = t < p.M ? __ldg(p.sx + t) : 0.f;
+      zpv[f][j] = (p.zp && t < p.M) ? uint32_t(__ldg(p.zp + t)) : 0u;
+    }
   __syncthreads();
-  if (warp != 0) return;
   // lane (g, q) of fragment f holds rows g / g + 8, tokens f * 8 + 2q / 2q + 1
 #pragma unroll
   for (int f = 0; f < kNT; ++f)
@@ -217,22 +292,23 @@ __global__ void __launch_bounds__(32 * kWarps) serq_i8_gemv_kernel(const GemvI8P
     for (int i = 0; i < 4; ++i) {
       int s = 0;
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) s += red_i[w][f][0][lane][i];  // exact
-      const int n = row0 + g + (i >= 2 ? 8 : 0);
+      for (int w = 0; w < kWarps; ++w) s += red_i[w][f][lane][i];  // exact
+      const int h = i >> 1;
+      const int n = h ? rhi : rlo;
       const int t = f * 8 + 2 * q + (i & 1);
       if (n >= p.N || t >= p.M) continue;
-      const uint32_t zp = p.zp ? uint32_t(p.zp[t]) : 0u;
-      const int32_t a_ref = int32_t(uint32_t(s) - zp * uint32_t(p.colsum[n]));  // wrapping int32, exact
-      float yv = float(a_ref) * p.sw[n];
+      const uint32_t zp = zpv[f][i & 1];
+      const int32_t a_ref = int32_t(uint32_t(s) - zp * uint32_t(cs[h]));  // wrapping int32, exact
+      float yv = float(a_ref) * swv[h];
       if constexpr (kR == kRInt) {
-        const int32_t ar_ref = int32_t(uint32_t(red_i[0][f][1][lane][i]) - zp * uint32_t(p.colsum_r[n]));
-        yv += float(ar_ref) * p.sr[n];
+        const int32_t ar_ref = int32_t(uint32_t(accr[f][i]) - zp * uint32_t(csr[h]));
+        yv += float(ar_ref) * srv[h];
         if (p.accr_dump) p.accr_dump[size_t(t) * p.N + n] = ar_ref;
       } else if constexpr (kR == kRDense) {
-        yv += red_f[0][f][lane][i];
+        yv += accd[f][i];
       }
       if (p.acc_dump) p.acc_dump[size_t(t) * p.N + n] = a_ref;
-      float out = yv * p.sx[t];
+      float out = yv * sxv[f][i & 1];
       if (p.addend) out += p.addend[size_t(t) * p.N + n];
       p.y[size_t(t) * p.ldy + n] = __float2bfloat16_rn(out);
     }

@@ -298,6 +298,46 @@ def test_int_decode_gemv_parity(D, M, r_mode, contiguous, bits, sym):
     assert np.array_equal(y1, y)
 
 
+@pytest.mark.parametrize("M", [1, 5, 16])
+@pytest.mark.parametrize("K,N", [(1536, 1000), (1552, 264), (11008, 520)])
+@pytest.mark.parametrize("r_mode,bits,sym", [("int", 8, False), ("dense", 4, True), ("none", 8, True)])
+def test_int_decode_gemv_w4_parity(D, M, K, N, r_mode, bits, sym):
+    # packed INT4 weights (0.5 B / weight) at decode sizes: the gemv widens the CTA-pair kernel's
+    # tiled nibbles in registers; ragged K (1552 = 12 * 128 + 16) reads the zero-padded tail
+    r = 64
+    rng = np.random.default_rng(M + K + N)
+    x = _bf16_outlier_x(M, K, seed=M + 1)
+    w = rng.standard_normal((K, N)) * 0.02
+    idx = np.arange(r)
+    if r_mode == "none":
+        main = O.quantize_symmetric(w, O.IntCfg(4, True, K, "row"))
+        comp, kw = None, {}
+    else:
+        main, comp = O.build_per_channel_int(w, idx, r_mode=r_mode)
+        kw = (dict(r_dense=comp.r_dense) if r_mode == "dense" else dict(r_codes=comp.r_q.codes, r_scales=comp.r_q.scales))
+        kw["salient_idx"] = idx
+    lin = D.IntLinear(main.codes, main.scales, 4, weight_format="int4", **kw)
+    nbytes, packed = lin.weight_bytes()
+    assert packed and nbytes == -(-N // 128) * -(-K // 128) * 128 * 64
+    act = lin.quantize(_cuda(x, torch.bfloat16), bits, sym)
+    acc = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    accr = torch.zeros((M, N), dtype=torch.int32, device="cuda")
+    y = lin.gemm(act, acc_dump=acc, accr_dump=accr).float().cpu().numpy()
+    assert D.last_kernel() == "serq_i8_gemv_kernel"
+    cfg = O.IntCfg(bits, sym, "per-row")
+    y_ref, xq = O.forward_int(x, main, comp, cfg, symmetric_act=sym)
+    _, parts = O.int_gemm(xq, main, return_partials=True)
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), parts[0][1])
+    if r_mode == "int":
+        _, rp = O.int_gemm(O.gather_columns(xq, idx), comp.r_q, return_partials=True)
+        assert np.array_equal(accr.cpu().numpy().astype(np.int64), rp[0][1])
+    mx, mean = O.parity_errors(y, y_ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+    # same Y as the int8-resident copy of the same weights
+    lin8 = D.IntLinear(main.codes, main.scales, 4, **kw)
+    assert np.array_equal(lin8.gemm(act).float().cpu().numpy(), y)
+
+
 @pytest.mark.parametrize("M,K,N,r", [(300, 1024, 512, 128), (2048, 4096, 1024, 128), (40, 512, 256, 8)])
 def test_svd_baseline_fused_matches_oracle(D, M, K, N, r):
     # SVD baseline (compensate.py:304-310): U = (codes - zp) L1 by one bf16 GEMM, U L2 as the
