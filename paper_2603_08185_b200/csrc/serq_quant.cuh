@@ -1321,7 +1321,9 @@ __global__ void __launch_bounds__(kBlock) int_quant_bf16_kernel(const __nv_bfloa
   const bool row_ok = row < M;
   uint4 nxt[kCpt];
   load_row(row + rstride, nxt);
-  float lo = INFINITY, hi = -INFINITY;
+  // min / max on packed bf16 pairs (one HMNMX2 per two elements; exact: bf16 -> f32 is exact)
+  __nv_bfloat162 lo2 = __halves2bfloat162(__ushort_as_bfloat16(0x7F80), __ushort_as_bfloat16(0x7F80));
+  __nv_bfloat162 hi2 = __halves2bfloat162(__ushort_as_bfloat16(0xFF80), __ushort_as_bfloat16(0xFF80));
 #pragma unroll
   for (int j = 0; j < kCpt; ++j) {
     const int c8 = t + j * kTpr;
@@ -1330,12 +1332,13 @@ __global__ void __launch_bounds__(kBlock) int_quant_bf16_kernel(const __nv_bfloa
       const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const float a = __uint_as_float(w[i] << 16), b = __uint_as_float(w[i] & 0xFFFF0000u);
-        lo = fminf(lo, fminf(a, b));
-        hi = fmaxf(hi, fmaxf(a, b));
+        const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+        lo2 = __hmin2(lo2, v);
+        hi2 = __hmax2(hi2, v);
       }
     }
   }
+  float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     lo = fminf(lo, __shfl_xor_sync(0xffffffff, lo, o));
@@ -1396,7 +1399,11 @@ __global__ void __launch_bounds__(kBlock) int_quant_bf16_kernel(const __nv_bfloa
   // n = rint(q) by the 1.5*2^23 magic add (|q| < 2^21), the code byte from the low
   // mantissa bits of (clamp(n + zp) + 1.5*2^23).
   constexpr float kMagic = 12582912.f;
-  const float zpf = float(zp), qminf = float(qmin), qmaxf = float(qmax);
+  // m = q + (1.5 2^23 + zp) rounds q + zp to an integer whose f32 bits are 0x4B400000 + rint(q) + zp
+  // (|q + zp| < 2^22; at exact .5 ties the rounding may differ from rint(q) + zp, but those are
+  // flagged below); the clamp runs on those bits (integer min / max), whose low byte is the code
+  const float mz = kMagic + float(zp);
+  const int bmin = 0x4B400000 + qmin, bmax = 0x4B400000 + qmax;
   constexpr int kBadWords = (8 * kCpt + 63) / 64;
   uint64_t bad[kBadWords];  // bit 8j+i: element i of group j takes the exact path
 #pragma unroll
@@ -1408,15 +1415,14 @@ __global__ void __launch_bounds__(kBlock) int_quant_bf16_kernel(const __nv_bfloa
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const float xf = __uint_as_float((i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16));
-      const float q = xf * inv32;             // |q - x/s| <= |q| * 2^-22.9
-      const float n = (q + kMagic) - kMagic;  // rint(q), exact for |q| < 2^22
-      const float d = q - n;                  // exact, |d| <= 1/2
+      const float q = xf * inv32;  // |q - x/s| <= |q| * 2^-22.9
+      const float m = q + mz;      // 1.5 2^23 + zp + rint(q)
+      const float d = q - (m - mz);  // exact, |d| <= 1/2
       // not within the margin of a .5 tie: |d| + |q| 2^-21 < 1/2 (also excludes |q| >= 2^21,
       // where the bound analysis stops)
       const bool ok = fmaf(fabsf(q), 0x1p-21f, fabsf(d)) < 0.5f;
       bad[(8 * j + i) >> 6] |= uint64_t(!ok) << ((8 * j + i) & 63);
-      const float c = fminf(fmaxf(n + zpf, qminf), qmaxf);
-      cb[i] = __float_as_uint(c + kMagic);  // low byte = two's-complement code
+      cb[i] = uint32_t(min(max(__float_as_int(m), bmin), bmax));  // low byte = two's-complement code
     }
     const uint2 v = make_uint2(__byte_perm(__byte_perm(cb[0], cb[1], 0x0040), __byte_perm(cb[2], cb[3], 0x0040), 0x5410),
                                __byte_perm(__byte_perm(cb[4], cb[5], 0x0040), __byte_perm(cb[6], cb[7], 0x0040), 0x5410));
