@@ -414,6 +414,8 @@ def other_configs(hbm_gbs: float) -> dict:
         out["c3_w4a8_group128_int_R"] = B.int_linear_point(2048, 4096, 11008, 128, "int", 8, False, fl, group=128)
         # the paper's comparison at C3's shape: SVD baseline (two-factor L1 L2, r = 128) vs SERQ's fused R
         out["c3_svd_baseline_r128"] = B.svd_baseline_point(2048, 4096, 11008, 128)
+        # the same comparison over an MX main at C2 (compensate.py:326-331)
+        out["c2_mx_svd_baseline_r64"] = B.mx_svd_baseline_point(4096, 4096, 4096, 64)
         out["c4_decode"] = B.decode_points(hbm_gbs)
         # q/k/v and gate/up each as ONE fused launch (own salient set per part, gather fallback)
         out["c4_decode_fused"] = B.decode_fused_points(hbm_gbs)

@@ -28,6 +28,9 @@
  *                                                                         compensate.py:300-316, mxfmt.py:135-195
  *   serq_linear_int_addend forward_reconstructed int branch, SVD baseline: int_gemm + (x_hat L1) L2
  *                                                                         compensate.py:300-310
+ *   serq_mx_decode_bf16    mx_decode of a device MX activation -> bf16 (exact) mxfmt.py:111-113
+ *   serq_linear_mx_addend  _forward_mx, SVD baseline: mx_gemm_reference(x, main) + (x_hat L1) L2
+ *                                                                         compensate.py:319-331
  *   serq_forward_mx        forward_reconstructed(x, main_t, comp, None) on device: mx_encode(x)
  *                          (+ re-encode of x[:, idx]) then the fused GEMM      compensate.py:319-340
  *   serq_forward_mx_host   forward_reconstructed(x, main_t, comp, None) end to end from host memory
@@ -165,6 +168,11 @@ int serq_mx_container_decode(const uint8_t* body, int64_t rows, int64_t cols, ui
 int serq_unpack_mx(const uint8_t* codes_packed, const uint8_t* sf, int64_t rows, int64_t cols, uint8_t* codes,
                    int32_t* exps, serq_stream_t stream);
 
+/* mx_decode (mxfmt.py:111-113) of a device MX tensor: bf16 [rows, cols] (16-B aligned) of
+ * e2m1(code) * 2^e, exact in bf16.  The SVD baseline's x_hat (compensate.py:327). */
+int serq_mx_decode_bf16(const uint8_t* codes_packed, const uint8_t* sf, int64_t rows, int64_t cols, void* out,
+                        serq_stream_t stream);
+
 /* Pack INT artefacts held in DEVICE memory, reference layouts: codes int32
  * [K, N] (main.codes), scales float64 [N] (main.scales, one group: group_size
  * == K, axis 'row').  r_mode SERQ_R_DENSE: r_data = float64 [r, N] (r_dense);
@@ -242,6 +250,13 @@ int serq_forward_mx(serq_linear_t* h, const void* x, int dtype, int64_t M, int64
 int serq_linear_int_addend(const serq_linear_t* h, const int8_t* a_codes, const float* sx, const int32_t* zp,
                            int64_t M, const void* xs, const float* addend, void* y, int64_t ldy,
                            serq_stream_t stream);
+
+/* K2 with an fp32 addend C [M, N] (row pitch N, 16-B aligned) summed into the fp32 accumulator before the
+ * bf16 store: y = bf16(mx_gemm(x, main) + C).  The MX SVD baseline (compensate.py:326-331);
+ * the handle must carry no salient term (r = 0).  M > 128: the CTA-pair kernel; smaller M
+ * the one-CTA persistent kernel. */
+int serq_linear_mx_addend(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t* a_sf, int64_t M,
+                          const float* addend, void* y, int64_t ldy, serq_stream_t stream);
 
 /* End to end from HOST memory (pinned for full PCIe rate): copy X (bf16 [M, K])
  * in, quantize, GEMM, copy Y (bf16 [M, N]) out; synchronises `stream`.

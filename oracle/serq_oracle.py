@@ -343,13 +343,17 @@ def forward_int(x, main: IntQ, comp: Comp | None, act_cfg: IntCfg, symmetric_act
 
 def forward_mx(x, main_t: MxT, comp: Comp | None):
     """compensate.py:319-340: encode X, main MX GEMM, re-encode the gathered
-    salient columns, R GEMM."""
+    salient columns, R GEMM (or the SVD baseline's two factors, :326-331)."""
     x = np.ascontiguousarray(x, dtype=np.float64)
     bs = main_t.block_size
     xm = mx_encode(x, bs)
     y = mx_gemm(xm, main_t)
     if comp is None or comp.rank == 0:
         return y
+    if comp.l1 is not None:
+        # SVD baseline over an MX main (compensate.py:326-331): the decoded activation times the
+        # two factors, in sequence, no rank restriction
+        return y + (mx_decode(xm) @ comp.l1) @ comp.l2
     if comp.rank % bs:
         raise OracleError("MX residual path needs rank divisible by block size")
     xs = mx_encode(np.ascontiguousarray(x[:, comp.salient_idx]), bs)

@@ -37,6 +37,8 @@ SIGNATURES = {
     "serq_act_quant_int_ext": (_I, [_P, _I, _I64, _I64, _I64, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _I, _P]),
     "serq_pack_mx": (_I, [_P, _P, _I64, _I64, _P, _P, _I, _I, _P, _P]),
     "serq_unpack_mx": (_I, [_P, _P, _I64, _I64, _P, _P, _P]),
+    "serq_mx_decode_bf16": (_I, [_P, _P, _I64, _I64, _P, _P]),
+    "serq_linear_mx_addend": (_I, [_P, _P, _P, _I64, _P, _P, _I64, _P]),
     "serq_block_add_rmsnorm": (_I, [_P, _P, _I64, _I64, _I64, _P, ctypes.c_float, _P, _P, _P]),
     "serq_block_silu_mul": (_I, [_P, _I64, _P, _I64, _I64, _I64, _P, _P]),
     "serq_block_attention": (_I, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, ctypes.c_float, _P, _I64, _P]),

@@ -321,14 +321,15 @@ class SerqLinear:
         has_r = comp is not None and getattr(comp, "rank", 0)
         self.svd = None
         if has_r and getattr(comp, "mode", RTN_RESIDUAL) == SVD_BASELINE:
-            # SVD baseline (compensate.py:209-224, 304-310): the two-factor correction (x_hat @ L1) @ L2
-            # spans all K columns: U = (codes - zp) @ L1 as one bf16 GEMM, then U @ L2 as the fused INT
-            # kernel's dense side term (device.SvdIntLinear)
-            if _is_mx(main):
-                raise ValidationError("the SVD baseline compensates integer mains only")
+            # SVD baseline (compensate.py:209-224, 304-310, MX 326-331): the two-factor correction
+            # (x_hat @ L1) @ L2 spans all K columns.  INT: U = (codes - zp) @ L1 as one bf16 GEMM, then
+            # U @ L2 as the fused INT kernel's dense side term (device.SvdIntLinear); MX: x_hat =
+            # mx_decode(x_mx) on the device, the correction as an fp32 addend of the MX kernel
+            # (device.SvdMxLinear)
             l1 = np.asarray(comp.l1, dtype=np.float64)
             l2 = np.asarray(comp.l2, dtype=np.float64)
-            if l1.shape != (main.shape[0], comp.rank) or l2.shape != (comp.rank, main.shape[1]):
+            k_in, n_out = (main.shape[1], main.shape[0]) if _is_mx(main) else main.shape
+            if l1.shape != (k_in, comp.rank) or l2.shape != (comp.rank, n_out):
                 raise ValidationError("SVD factors must be L1 [K, r] and L2 [r, N]")
             self.svd = (l1, l2)
             comp, has_r = None, 0
@@ -341,9 +342,12 @@ class SerqLinear:
             if has_r and comp.rank % 32:
                 raise ValidationError("MX residual path needs rank divisible by block size")
             rq = comp.r_q if has_r else None
-            self.impl = D.MxLinear(main.element_codes, main.block_scale_exponents,
-                                   None if rq is None else rq.element_codes,
-                                   None if rq is None else rq.block_scale_exponents, idx, device)
+            if self.svd is not None:
+                self.impl = D.SvdMxLinear(main.element_codes, main.block_scale_exponents, *self.svd, device=device)
+            else:
+                self.impl = D.MxLinear(main.element_codes, main.block_scale_exponents,
+                                       None if rq is None else rq.element_codes,
+                                       None if rq is None else rq.block_scale_exponents, idx, device)
             self.K, self.N = main.shape[1], main.shape[0]
         else:
             if act_cfg is None or (act_cfg.symmetric and not allow_symmetric_act):
@@ -477,7 +481,7 @@ def forward_reconstructed(x, main, comp, act_cfg, probe: OpProbe | None = None) 
     y = lin(_to_gpu(x))
     if probe is not None and lin.aux_matmuls:
         probe.aux_matmuls += lin.aux_matmuls
-        if lin.svd is not None:
+        if lin.svd is not None and lin.fmt == "int":  # (the MX branch adds no note, compensate.py:328-329)
             probe.notes.append("sequential two-factor path")
     return y.float().cpu().numpy().astype(np.float64)
 

@@ -376,6 +376,28 @@ def svd_baseline_point(M, K, N, r, bits=8, n_steps: int = 16) -> dict:
     return {"M": M, "K": K, "N": N, "r": r, "act_bits": bits, "step_us": t_fused * 1e3, "aux_matmuls": 2,
             "tokens_per_s": M / (t_fused * 1e-3), "cublas_two_gemm_addend_step_us": t_lib * 1e3}
 
+def mx_svd_baseline_point(M, K, N, r, n_steps: int = 16) -> dict:
+    """The SVD baseline over an MX main (compensate.py:326-331, device.SvdMxLinear: K1-MX,
+    exact bf16 mx_decode, two cuBLAS GEMMs for the correction, the MX kernel with the fp32
+    addend) against SERQ's MX linear with its fused salient term (device.MxLinear.forward) at
+    the same shape and rank; 8 weight / activation sets (cold).  Factors are random with the
+    right shapes (cost only; parity is a test)."""
+    rng = np.random.default_rng(6)
+    l1 = rng.standard_normal((K, r)) * 0.01
+    l2 = rng.standard_normal((r, N)) * 0.01
+    svds, serq = [], []
+    for i in range(8):
+        codes, exps, rc, re_, idx = device_mx_parts(K, N, r, seed=1 + i)
+        svds.append(D.SvdMxLinear(codes, exps, l1, l2))
+        serq.append(D.MxLinear(codes, exps, rc, re_, idx))
+    xs = [outlier_x(M, K, seed=i) for i in range(8)]
+    ys = [torch.empty((M, N), dtype=torch.bfloat16, device="cuda") for _ in xs]
+    t_svd = time_steps(lambda i: svds[i % 8].forward(xs[i % 8], ys[i % 8]), n_steps)
+    t_serq = time_steps(lambda i: serq[i % 8].forward(xs[i % 8], None, ys[i % 8]), n_steps)
+    return {"M": M, "K": K, "N": N, "r": r, "svd_step_us": t_svd * 1e3, "serq_step_us": t_serq * 1e3,
+            "svd_aux_matmuls": 2, "serq_aux_matmuls": 1}
+
+
 def rmsnorm_quant_point(M: int, K: int, hbm_peak_gbs: float, n_steps: int = 16) -> dict:
     """Producer fusion: rmsnorm(x, gain) -> MX codes in one
     kernel vs the plain MX quantizer on an already-normalised bf16 X, same shape,

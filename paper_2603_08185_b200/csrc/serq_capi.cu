@@ -644,6 +644,19 @@ int serq_unpack_mx(const uint8_t* codes_packed, const uint8_t* sf, int64_t rows,
   return SERQ_OK;
 }
 
+int serq_mx_decode_bf16(const uint8_t* codes_packed, const uint8_t* sf, int64_t rows, int64_t cols, void* out,
+                        serq_stream_t stream) {
+  g_launches = 0;
+  if (rows <= 0 || cols <= 0 || cols % 32) return fail(SERQ_EINVAL, "MX layout needs cols %% 32 == 0");
+  if (!codes_packed || !sf || !out) return fail(SERQ_EINVAL, "NULL buffer");
+  if (reinterpret_cast<uintptr_t>(out) & 15) return fail(SERQ_EINVAL, "out must be 16-byte aligned");
+  if (rows > 65535) return fail(SERQ_EINVAL, "at most 65535 rows per call");
+  mx_decode_bf16_kernel<<<dim3(unsigned(cdiv(cols / 8, 256)), unsigned(rows)), 256, 0, S(stream)>>>(
+      codes_packed, sf, rows, cols, kc_pad_of(cols), static_cast<__nv_bfloat16*>(out));
+  LAUNCH_CHECK("mx_decode_bf16");
+  return SERQ_OK;
+}
+
 int serq_rmsnorm_quant_mx(const void* x, int dtype, int64_t M, int64_t K, int64_t ldx, const double* gain,
                           const float* gain32, double eps, uint8_t* codes, uint8_t* sf, serq_stream_t stream) {
   return serq_rmsnorm_quant_mx_gather(x, dtype, M, K, ldx, gain, gain32, eps, nullptr, 0, codes, sf, nullptr, nullptr,
@@ -1167,9 +1180,12 @@ static int launch_decode_cl(const serq_linear* h, const uint8_t* a_codes, const 
 }
 
 static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t* a_sf, int64_t M,
-                          const uint8_t* xs_codes, const uint8_t* xs_sf, void* y, int64_t ldy, serq_stream_t stream) {
+                          const uint8_t* xs_codes, const uint8_t* xs_sf, void* y, int64_t ldy, serq_stream_t stream,
+                          const float* addend = nullptr) {
   g_launches = 0;
   if (!h || h->mode != kModeMX) return fail(SERQ_EINVAL, "handle is not an MX linear");
+  if (addend && (h->r != 0 || h->nseg > 1))
+    return fail(SERQ_EINVAL, "an fp32 addend needs an MX linear without salient term or segments");
   if (M <= 0) return fail(SERQ_EINVAL, "x must be non-empty");
   if (ldy < h->N || ldy % 8) return fail(SERQ_EINVAL, "ldy must be >= N and a multiple of 8");
   const bool need_xs = h->r > 0 && !h->contiguous;
@@ -1216,8 +1232,9 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
   p.w_ksteps = h->w_ksteps;
   p.dbg = g_debug_flags;
   p.dbg_ts = g_debug_ts;
+  p.addend = addend;  // (the SVD baseline: the CTA-pair kernel for M > 128, else the one-CTA kernel)
   // decode kernel: any contiguous R up to r = 128; the gather fallback with r = 64 (32-B xs rows)
-  const bool dec_ok = h->r == 0 || (h->dec_rw && (h->contiguous || h->has_r32));
+  const bool dec_ok = !addend && (h->r == 0 || (h->dec_rw && (h->contiguous || h->has_r32)));
   if (M <= kDecN && dec_ok && !SERQ_DBG(g_debug_flags, 2048))
     return launch_decode_cl(h, a_codes, a_sf, nullptr, 0, nullptr, nullptr, M, y, ldy, S(stream), xs_codes, xs_sf);
   // pair3 for the permuted layout, and for the gather fallback with r == 64 (debug flag 1<<24: the
@@ -1282,7 +1299,7 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
     }
     return SERQ_OK;
   }
-  if (M > 128 && !SERQ_DBG(g_debug_flags, 16)) {
+  if (M > 128 && !addend && !SERQ_DBG(g_debug_flags, 16)) {
     CK(set_smem_attr(serq_mx_pair_kernel, k2SmemBytes));
     Pair2Maps pm;
     rc = make_map(&pm.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, 128);
@@ -1316,6 +1333,14 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
                                                                         my, p);
   LAUNCH_CHECK("serq_mx_persistent_kernel");
   return SERQ_OK;
+}
+
+int serq_linear_mx_addend(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t* a_sf, int64_t M,
+                          const float* addend, void* y, int64_t ldy, serq_stream_t stream) {
+  if (!addend) return fail(SERQ_EINVAL, "addend is NULL");
+  // (rows of N % 8 == 0 floats: 16-B aligned when the base is; the kernels read 16 B at a time)
+  if (reinterpret_cast<uintptr_t>(addend) & 15) return fail(SERQ_EINVAL, "addend must be 16-byte aligned");
+  return linear_mx_impl(h, a_codes, a_sf, M, nullptr, nullptr, y, ldy, stream, addend);
 }
 
 int serq_linear_mx(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t* a_sf, int64_t M,

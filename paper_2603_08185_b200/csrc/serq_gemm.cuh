@@ -70,7 +70,8 @@ struct GemmParams {
   const int32_t* colsum; // [N] sum_k W[k,n] (for the zero-point correction)
   const float* sr;       // [N] R scale (int R)
   const int32_t* colsum_r;
-  const float* addend;   // INT: optional fp32 [M, N] (pitch N) added after scaling (SVD-baseline correction)
+  const float* addend;   // optional fp32 [M, N] (pitch N) added after scaling (SVD-baseline correction;
+                         // MX: the CTA-pair pair3 and one-CTA persistent kernels)
   int32_t* acc_dump;     // debug: exact main accumulators (acc - zp*colsum), [M,N]
   int32_t* accr_dump;    // debug: exact R accumulators
   long long* dbg_ts;     // diagnostics: per-iteration clock64 stamps of the MMA warp (CTA 0), or nullptr

@@ -242,6 +242,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane_id() == 0) mbar_arrive(tmem_empty);
         }
+        const int row = m0 + int(q) * 32 + int(lane_id());
+        if (p.addend && row < p.M) {  // the SVD baseline's fp32 correction (compensate.py:326-331)
+          const float* ad = p.addend + size_t(row) * p.N + n0 + c * 64;
+          // 16-B loads (N % 4 == 0, 16-B aligned rows: checked at the boundary); each lane reads
+          // its row's 256 contiguous bytes
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            if (n0 + c * 64 + j < p.N) {
+              const float4 a = __ldg(reinterpret_cast<const float4*>(ad + j));
+              v[j] = __float_as_uint(__uint_as_float(v[j]) + a.x);
+              v[j + 1] = __float_as_uint(__uint_as_float(v[j + 1]) + a.y);
+              v[j + 2] = __float_as_uint(__uint_as_float(v[j + 2]) + a.z);
+              v[j + 3] = __float_as_uint(__uint_as_float(v[j + 3]) + a.w);
+            }
+            if (n0 + c * 64 + 32 + j < p.N) {
+              const float4 a = __ldg(reinterpret_cast<const float4*>(ad + 32 + j));
+              w[j] = __float_as_uint(__uint_as_float(w[j]) + a.x);
+              w[j + 1] = __float_as_uint(__uint_as_float(w[j + 1]) + a.y);
+              w[j + 2] = __float_as_uint(__uint_as_float(w[j + 2]) + a.z);
+              w[j + 3] = __float_as_uint(__uint_as_float(w[j + 3]) + a.w);
+            }
+          }
+        }
         // the previous TMA store must have finished reading the staging box
         if (lane_id() == 0) bulk_wait_read_all();
         __syncwarp();

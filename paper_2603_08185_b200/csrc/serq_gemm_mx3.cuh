@@ -363,6 +363,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       long long* ep = p.dbg_ts + 1024 + blockIdx.x * 24 + i * 4;
       if (est) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); ep[0] = (long long)g; }
 #endif
+      if (p.addend) {  // pull this tile's addend rows into L2 while its MMAs run
+        const int row = m_own + int(q) * 32 + int(lane_id());
+        if (row < p.M)
+          for (int cb = 0; cb < n_chunks * 64; cb += 32)
+            if (n0 + cb < p.N)
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(p.addend + size_t(row) * p.N + n0 + cb));
+      }
       mbar_wait(&tmem_full[b], (i >> 1) & 1);
       tc_fence_after();
 #ifdef SERQ_DIAG_TS
@@ -380,6 +387,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane_id() == 0) mbar_arrive_cluster_relaxed(tmem_empty_leader);
+        }
+        if (p.addend) {  // the SVD baseline's fp32 correction (compensate.py:326-331; r = 0 handles only)
+          const int row = m_own + int(q) * 32 + int(lane_id());
+          if (row < p.M) {
+            const float* ad = p.addend + size_t(row) * p.N + n0 + c * 64;
+            // 16-B loads (N % 4 == 0, 16-B aligned rows: checked at the boundary); each lane reads
+            // its row's 256 contiguous bytes
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              if (n0 + c * 64 + j < p.N) {
+                const float4 a = __ldg(reinterpret_cast<const float4*>(ad + j));
+                v[j] = __float_as_uint(__uint_as_float(v[j]) + a.x);
+                v[j + 1] = __float_as_uint(__uint_as_float(v[j + 1]) + a.y);
+                v[j + 2] = __float_as_uint(__uint_as_float(v[j + 2]) + a.z);
+                v[j + 3] = __float_as_uint(__uint_as_float(v[j + 3]) + a.w);
+              }
+              if (n0 + c * 64 + 32 + j < p.N) {
+                const float4 a = __ldg(reinterpret_cast<const float4*>(ad + 32 + j));
+                w[j] = __float_as_uint(__uint_as_float(w[j]) + a.x);
+                w[j + 1] = __float_as_uint(__uint_as_float(w[j + 1]) + a.y);
+                w[j + 2] = __float_as_uint(__uint_as_float(w[j + 2]) + a.z);
+                w[j + 3] = __float_as_uint(__uint_as_float(w[j + 3]) + a.w);
+              }
+            }
+          }
         }
         // the CTA's final tile: the pipeline is drained, so each (chunk, half) box gets its
         // own 2 KB of slot memory and the TMA stores go out without waiting on each other

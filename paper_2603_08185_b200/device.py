@@ -685,6 +685,61 @@ class SvdIntLinear:
 
     __call__ = forward
 
+class SvdMxLinear:
+    """The SVD baseline over an MX main (_forward_mx, compensate.py:326-331):
+    Y = mx_gemm_reference(x_mx, main_t) + (mx_decode(x_mx) L1) L2, any rank.
+
+    B200 path: K1-MX encodes X; ``serq_mx_decode_bf16`` writes x_hat = mx_decode(x_mx) (exact in
+    bf16); U = x_hat L1 and C = U L2 are two plain cuBLAS GEMMs (bf16 operands, fp32
+    accumulation, U rounded to bf16 between them -- 2^-9 relative on the correction term, as in
+    SvdIntLinear -- and C kept in fp32); the MX kernel adds C to its fp32 accumulator before the
+    one bf16 rounding of Y (``serq_linear_mx_addend``: the CTA-pair kernel for M > 128).  A
+    comparison baseline, not the SERQ hot path: the salient-term fusion of MxLinear does not
+    apply, because the correction spans all K columns."""
+
+    def __init__(self, codes, exps, l1, l2, device="cuda"):
+        l1 = np.asarray(l1, dtype=np.float64)
+        l2 = np.asarray(l2, dtype=np.float64)
+        self.lin = MxLinear(codes, exps, device=device)
+        self.K, self.N, self.device = self.lin.K, self.lin.N, self.lin.device
+        if l1.ndim != 2 or l2.ndim != 2 or l1.shape[0] != self.K or l2.shape != (l1.shape[1], self.N):
+            raise ValidationError("SVD factors must be L1 [K, r] and L2 [r, N]")
+        self.r = l1.shape[1]
+        self.l1 = torch.from_numpy(l1).to(self.device, torch.bfloat16)
+        self.l2 = torch.from_numpy(l2).to(self.device, torch.bfloat16)
+
+    def forward(self, x: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
+        _require_cuda(x, "x")
+        if x.dim() != 2 or x.stride(1) != 1 or x.shape[1] != self.K:
+            raise ValidationError("x must be a row-major [M, K] tensor")
+        M = x.shape[0]
+        act = self.lin.quantize(x)
+        xhat = torch.empty((M, self.K), dtype=torch.bfloat16, device=self.device)
+        _lib.call("serq_mx_decode_bf16", act.codes.data_ptr(), act.sf.data_ptr(), M, self.K, xhat.data_ptr(),
+                  _stream())
+        prev = torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction
+        torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
+        try:
+            u = xhat @ self.l1
+            c = torch.mm(u, self.l2, out_dtype=torch.float32)
+        finally:
+            torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = prev
+        if y is None:
+            y = torch.empty((M, self.N), dtype=torch.bfloat16, device=self.device)
+        _lib.call("serq_linear_mx_addend", self.lin._h.ptr, act.codes.data_ptr(), act.sf.data_ptr(), M, c.data_ptr(),
+                  y.data_ptr(), y.stride(0), _stream())
+        return y
+
+    __call__ = forward
+
+
+def mx_decode_bf16(act: MxActivation) -> torch.Tensor:
+    """mx_decode (mxfmt.py:111-113) of a device MX activation, bf16 [M, K] (exact)."""
+    out = torch.empty((act.M, act.K), dtype=torch.bfloat16, device=act.codes.device)
+    _lib.call("serq_mx_decode_bf16", act.codes.data_ptr(), act.sf.data_ptr(), act.M, act.K, out.data_ptr(), _stream())
+    return out
+
+
 def device_info() -> dict:
     sm, ma, mi = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     _lib.call("serq_device_info", ctypes.byref(sm), ctypes.byref(ma), ctypes.byref(mi))

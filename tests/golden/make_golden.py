@@ -33,6 +33,7 @@ from serq.compensate import (  # noqa: E402
 )
 from serq.mxfmt import (  # noqa: E402
     e2m1_nearest,
+    mx_decode,
     int_gemm_reference,
     mx_encode,
     mx_gemm_reference,
@@ -169,6 +170,15 @@ def main():
     comp_g = Compensator("rtn_residual", 64, idx, r_q=comp.r_q)
     g["fmx_gidx"] = idx
     g["fmx_y_gather"] = forward_reconstructed(xp, main_t, comp_g, None)
+    # SVD baseline over an MX main (compensate.py:326-331): (mx_decode(x_mx) L1) L2, two aux products
+    err = wp - mx_decode(main_t).T
+    u, sv, vt = np.linalg.svd(err, full_matrices=False)
+    root = np.sqrt(sv[:48])
+    comp_svd = Compensator("svd_baseline", 48, l1=u[:, :48] * root[None, :], l2=root[:, None] * vt[:48])
+    probe = OpProbe()
+    g["fmxsvd_y"] = forward_reconstructed(xp, main_t, comp_svd, None, probe)
+    g["fmxsvd_aux"] = np.array(probe.aux_matmuls)
+    g["fmxsvd_l1"], g["fmxsvd_l2"] = comp_svd.l1, comp_svd.l2
 
     # -- full decomposed forward, INT (asym A8, per-output-channel W, int R) ---
     k, n, r = 256, 96, 32

@@ -115,6 +115,19 @@ def test_forward_reconstructed_mx_golden(gpu, golden):
 
 
 @pytest.mark.gpu
+def test_forward_reconstructed_mx_svd_baseline_golden(gpu, golden):
+    # SVD baseline over an MX main (compensate.py:326-331), reference-built golden: two aux
+    # products and no probe note (unlike the integer branch)
+    main = api.MxBlockTensor(golden["fmx_main_codes"], golden["fmx_main_exps"], 32, golden["fmx_main_codes"].shape)
+    comp = api.Compensator(api.SVD_BASELINE, 48, l1=golden["fmxsvd_l1"], l2=golden["fmxsvd_l2"])
+    probe = api.OpProbe()
+    y = api.forward_reconstructed(golden["fmx_x"], main, comp, None, probe)
+    assert probe.aux_matmuls == int(golden["fmxsvd_aux"]) == 2 and probe.notes == []
+    mx, mean = O.parity_errors(y, golden["fmxsvd_y"])
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+@pytest.mark.gpu
 def test_forward_reconstructed_int_golden(gpu, golden):
     x, w = golden["fint_x"], golden["fint_w"]
     main, comp = api.build_per_channel_int(w, np.arange(32), r_mode="int")

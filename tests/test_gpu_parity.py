@@ -338,6 +338,27 @@ def test_int_decode_gemv_w4_parity(D, M, K, N, r_mode, bits, sym):
     assert np.array_equal(lin8.gemm(act).float().cpu().numpy(), y)
 
 
+@pytest.mark.parametrize("M,K,N,r", [(5, 512, 264, 48), (300, 1024, 520, 128), (2048, 4096, 1024, 64)])
+def test_mx_svd_baseline_matches_oracle(D, M, K, N, r):
+    # SVD baseline over an MX main (compensate.py:326-331): x_hat = mx_decode(x_mx) exact in bf16,
+    # (x_hat L1) L2 as the MX kernel's fp32 addend; Y vs the oracle at the north_star tolerance
+    rng = np.random.default_rng(M + N)
+    x = _bf16_outlier_x(M, K, seed=M)
+    w = rng.standard_normal((K, N)) * 0.02
+    main_t = O.mx_encode(w.T, 32)
+    u, sv, vt = np.linalg.svd(w - O.mx_decode(main_t).T, full_matrices=False)
+    l1, l2 = u[:, :r] * np.sqrt(sv[:r]), np.sqrt(sv[:r])[:, None] * vt[:r]
+    lin = D.SvdMxLinear(main_t.element_codes, main_t.block_scale_exponents, l1, l2)
+    xt = _cuda(x, torch.bfloat16)
+    # the decoded activation is exactly the oracle's mx_decode(mx_encode(x))
+    xhat = D.mx_decode_bf16(lin.lin.quantize(xt)).double().cpu().numpy()
+    assert np.array_equal(xhat, O.mx_decode(O.mx_encode(x, 32)))
+    y = lin(xt).float().cpu().numpy()
+    y_ref = O.forward_mx(x, main_t, O.Comp(r, l1=l1, l2=l2))
+    mx, mean = O.parity_errors(y, y_ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
 @pytest.mark.parametrize("M,K,N,r", [(300, 1024, 512, 128), (2048, 4096, 1024, 128), (40, 512, 256, 8)])
 def test_svd_baseline_fused_matches_oracle(D, M, K, N, r):
     # SVD baseline (compensate.py:304-310): U = (codes - zp) L1 by one bf16 GEMM, U L2 as the

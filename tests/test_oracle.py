@@ -80,6 +80,14 @@ def test_mx_forward_matches_reference_golden(golden):
     assert np.array_equal(O.forward_mx(golden["fmx_x"], main_t, comp_g), golden["fmx_y_gather"])
 
 
+def test_mx_svd_baseline_forward_matches_reference_golden(golden):
+    # SVD baseline over an MX main (compensate.py:326-331): y + (mx_decode(x_mx) L1) L2
+    main_t, _ = O.build_serq_rtn_mx(golden["fmx_w"], golden["fmx_idx"], 32)
+    comp = O.Comp(48, l1=golden["fmxsvd_l1"], l2=golden["fmxsvd_l2"])
+    assert np.array_equal(O.forward_mx(golden["fmx_x"], main_t, comp), golden["fmxsvd_y"])
+    assert int(golden["fmxsvd_aux"]) == 2
+
+
 def test_int_forward_matches_reference_golden(golden):
     xi, wi = golden["fint_x"], golden["fint_w"]
     main, comp = O.build_per_channel_int(wi, np.arange(32), r_mode="int")
