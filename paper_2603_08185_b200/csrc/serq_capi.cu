@@ -1243,6 +1243,7 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
   if (M > 128 && (h->r == 0 || (h->has_r32 && h->contiguous) || g3) && !SERQ_DBG(g_debug_flags, 16 | 512)) {
     CK(set_smem_attr(serq_mx_pair3_kernel<false>, k3SmemBytes));
     CK(set_smem_attr(serq_mx_pair3_kernel<true>, k3SmemBytesG));
+    CK(set_smem_attr(serq_mx_pair3_kernel<false, true>, k3SmemBytes));
     Pair3Maps pm;
     rc = make_map(&pm.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, 128);
     if (!rc) rc = make_sf_map(&pm.sfa, a_sf, M, h->K);
@@ -1293,6 +1294,9 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
     if (g3) {
       CK(cudaLaunchKernelEx(&cfg, serq_mx_pair3_kernel<true>, pm, p));
       LAUNCH_CHECK("serq_mx_pair3_kernel<gather>");
+    } else if (addend) {
+      CK(cudaLaunchKernelEx(&cfg, serq_mx_pair3_kernel<false, true>, pm, p));
+      LAUNCH_CHECK("serq_mx_pair3_kernel<addend>");
     } else {
       CK(cudaLaunchKernelEx(&cfg, serq_mx_pair3_kernel<false>, pm, p));
       LAUNCH_CHECK("serq_mx_pair3_kernel");

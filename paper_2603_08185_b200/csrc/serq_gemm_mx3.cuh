@@ -41,7 +41,9 @@ __device__ __forceinline__ void tma_load_2d_pair_nohint(uint32_t dst, const CUte
   tma_load_2d_pair(dst, m, bar, c0, c1, kEvictNormal);
 }
 
-template <bool kGather = false>
+// kAddend: the SVD baseline's fp32 addend in the epilogue (compensate.py:326-331; r = 0 handles),
+// a separate instantiation so the SERQ kernels carry none of it
+template <bool kGather = false, bool kAddend = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     serq_mx_pair3_kernel(const __grid_constant__ Pair3Maps maps, const GemmParams p) {
   constexpr int kEpiBox = kGather ? k3EpiG : k2EpiStage;
@@ -363,7 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       long long* ep = p.dbg_ts + 1024 + blockIdx.x * 24 + i * 4;
       if (est) { uint64_t g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); ep[0] = (long long)g; }
 #endif
-      if (p.addend) {  // pull this tile's addend rows into L2 while its MMAs run
+      if (kAddend) {  // pull this tile's addend rows into L2 while its MMAs run
         const int row = m_own + int(q) * 32 + int(lane_id());
         if (row < p.M)
           for (int cb = 0; cb < n_chunks * 64; cb += 32)
@@ -388,7 +390,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane_id() == 0) mbar_arrive_cluster_relaxed(tmem_empty_leader);
         }
-        if (p.addend) {  // the SVD baseline's fp32 correction (compensate.py:326-331; r = 0 handles only)
+        if (kAddend) {  // the SVD baseline's fp32 correction (compensate.py:326-331; r = 0 handles only)
           const int row = m_own + int(q) * 32 + int(lane_id());
           if (row < p.M) {
             const float* ad = p.addend + size_t(row) * p.N + n0 + c * 64;
