@@ -337,12 +337,15 @@ class SerqLinear:
         if self.fmt == "mx":
             if getattr(main, "block_size", 32) != 32:
                 raise ValidationError("the device MX format uses 32-element blocks")
-            if has_r and comp.r_dense is not None:
-                raise ValidationError("MX layers need an MX-encoded compensator (comp.r_q)")
             if has_r and comp.rank % 32:
                 raise ValidationError("MX residual path needs rank divisible by block size")
             rq = comp.r_q if has_r else None
-            if self.svd is not None:
+            if has_r and comp.r_dense is not None:
+                # unquantized R (compensate.py:338-339): the decoded salient slice times R, added in
+                # the MX kernel's epilogue (device.MxDenseRLinear)
+                self.impl = D.MxDenseRLinear(main.element_codes, main.block_scale_exponents, comp.r_dense, idx,
+                                             device=device)
+            elif self.svd is not None:
                 self.impl = D.SvdMxLinear(main.element_codes, main.block_scale_exponents, *self.svd, device=device)
             else:
                 self.impl = D.MxLinear(main.element_codes, main.block_scale_exponents,

@@ -733,6 +733,54 @@ class SvdMxLinear:
     __call__ = forward
 
 
+class MxDenseRLinear:
+    """An MX main with an UNQUANTIZED salient R (the reference's "test mode" r_dense,
+    compensate.py:54, :338-339): Y = mx_gemm_reference(x_mx, main_t) + mx_decode(mx_encode(x[:, idx])) @ R.
+
+    K1-MX encodes X and the gathered slice x[:, idx] in one launch; ``serq_mx_decode_bf16`` turns
+    the slice's codes into its exact bf16 values; one cuBLAS GEMM forms C = x_s_hat @ R with R as
+    bf16 hi + lo planes (relative 2^-17; the rows of R may carry a large share of Y) and fp32
+    accumulation / output; the MX kernel adds C before Y's one bf16 rounding
+    (``serq_linear_mx_addend``)."""
+
+    def __init__(self, codes, exps, r_dense, salient_idx, device="cuda"):
+        r_dense = np.asarray(r_dense, dtype=np.float64)
+        self.lin = MxLinear(codes, exps, device=device)
+        self.K, self.N, self.device = self.lin.K, self.lin.N, self.lin.device
+        self.r = r_dense.shape[0]
+        if r_dense.ndim != 2 or r_dense.shape[1] != self.N:
+            raise ValidationError(f"r_dense must be [r, N] with N = {self.N}")
+        if self.r % 32:
+            raise ValidationError("MX residual path needs rank divisible by block size")
+        idx = _check_salient_idx(salient_idx, self.r, self.K)
+        self.gather_idx = torch.from_numpy(idx.astype(np.int32)).to(self.device)
+        rt = torch.from_numpy(r_dense).to(self.device)
+        hi = rt.to(torch.bfloat16)
+        lo = (rt - hi.double()).to(torch.bfloat16)
+        self.r_hilo = torch.cat([hi, lo], 0).contiguous()  # [2r, N]
+
+    def forward(self, x: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
+        _require_cuda(x, "x")
+        if x.dim() != 2 or x.stride(1) != 1 or x.shape[1] != self.K:
+            raise ValidationError("x must be a row-major [M, K] tensor")
+        M = x.shape[0]
+        act = quantize_mx(x, self.gather_idx)
+        xs = mx_decode_bf16(MxActivation(act.xs_codes, act.xs_sf, M, self.r))
+        prev = torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction
+        torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
+        try:
+            c = torch.mm(torch.cat([xs, xs], 1), self.r_hilo, out_dtype=torch.float32)
+        finally:
+            torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = prev
+        if y is None:
+            y = torch.empty((M, self.N), dtype=torch.bfloat16, device=self.device)
+        _lib.call("serq_linear_mx_addend", self.lin._h.ptr, act.codes.data_ptr(), act.sf.data_ptr(), M, c.data_ptr(),
+                  y.data_ptr(), y.stride(0), _stream())
+        return y
+
+    __call__ = forward
+
+
 def mx_decode_bf16(act: MxActivation) -> torch.Tensor:
     """mx_decode (mxfmt.py:111-113) of a device MX activation, bf16 [M, K] (exact)."""
     out = torch.empty((act.M, act.K), dtype=torch.bfloat16, device=act.codes.device)

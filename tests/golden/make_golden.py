@@ -170,8 +170,13 @@ def main():
     comp_g = Compensator("rtn_residual", 64, idx, r_q=comp.r_q)
     g["fmx_gidx"] = idx
     g["fmx_y_gather"] = forward_reconstructed(xp, main_t, comp_g, None)
-    # SVD baseline over an MX main (compensate.py:326-331): (mx_decode(x_mx) L1) L2, two aux products
+    # MX main with a dense (unquantized, "test mode") R: y + mx_decode(mx_encode(x[:, idx])) @ r_dense
+    # (compensate.py:338-339)
     err = wp - mx_decode(main_t).T
+    comp_dr = Compensator("rtn_residual", 64, plan_p.salient_idx.copy(), r_dense=err[plan_p.salient_idx])
+    g["fmx_y_dense"] = forward_reconstructed(xp, main_t, comp_dr, None)
+    g["fmx_r_dense"] = comp_dr.r_dense
+    # SVD baseline over an MX main (compensate.py:326-331): (mx_decode(x_mx) L1) L2, two aux products
     u, sv, vt = np.linalg.svd(err, full_matrices=False)
     root = np.sqrt(sv[:48])
     comp_svd = Compensator("svd_baseline", 48, l1=u[:, :48] * root[None, :], l2=root[:, None] * vt[:48])

@@ -115,6 +115,18 @@ def test_forward_reconstructed_mx_golden(gpu, golden):
 
 
 @pytest.mark.gpu
+def test_forward_reconstructed_mx_dense_r_golden(gpu, golden):
+    # MX main + unquantized R ("test mode", compensate.py:338-339), reference-built golden
+    main = api.MxBlockTensor(golden["fmx_main_codes"], golden["fmx_main_exps"], 32, golden["fmx_main_codes"].shape)
+    comp = api.Compensator(api.RTN_RESIDUAL, 64, np.asarray(golden["fmx_idx"]), r_dense=golden["fmx_r_dense"])
+    probe = api.OpProbe()
+    y = api.forward_reconstructed(golden["fmx_x"], main, comp, None, probe)
+    assert probe.aux_matmuls == 1
+    mx, mean = O.parity_errors(y, golden["fmx_y_dense"])
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
+@pytest.mark.gpu
 def test_forward_reconstructed_mx_svd_baseline_golden(gpu, golden):
     # SVD baseline over an MX main (compensate.py:326-331), reference-built golden: two aux
     # products and no probe note (unlike the integer branch)

@@ -359,6 +359,22 @@ def test_mx_svd_baseline_matches_oracle(D, M, K, N, r):
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
 
 
+@pytest.mark.parametrize("M,K,N,r", [(3, 512, 264, 32), (300, 1024, 520, 64), (1024, 2048, 1024, 128)])
+def test_mx_dense_r_matches_oracle(D, M, K, N, r):
+    # MX main + unquantized R at an arbitrary salient set (compensate.py:335-339)
+    rng = np.random.default_rng(M + r)
+    x = _bf16_outlier_x(M, K, seed=M + 2)
+    w = rng.standard_normal((K, N)) * 0.02
+    main_t = O.mx_encode(w.T, 32)
+    idx = np.sort(rng.choice(K, r, replace=False))
+    r_dense = (w - O.mx_decode(main_t).T)[idx]
+    lin = D.MxDenseRLinear(main_t.element_codes, main_t.block_scale_exponents, r_dense, idx)
+    y = lin(_cuda(x, torch.bfloat16)).float().cpu().numpy()
+    y_ref = O.forward_mx(x, main_t, O.Comp(r, idx, r_dense=r_dense))
+    mx, mean = O.parity_errors(y, y_ref)
+    assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+
+
 @pytest.mark.parametrize("M,K,N,r", [(300, 1024, 512, 128), (2048, 4096, 1024, 128), (40, 512, 256, 8)])
 def test_svd_baseline_fused_matches_oracle(D, M, K, N, r):
     # SVD baseline (compensate.py:304-310): U = (codes - zp) L1 by one bf16 GEMM, U L2 as the

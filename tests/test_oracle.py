@@ -80,6 +80,13 @@ def test_mx_forward_matches_reference_golden(golden):
     assert np.array_equal(O.forward_mx(golden["fmx_x"], main_t, comp_g), golden["fmx_y_gather"])
 
 
+def test_mx_dense_r_forward_matches_reference_golden(golden):
+    # MX main with an unquantized R (compensate.py:338-339): mx_decode(mx_encode(x[:, idx])) @ r_dense
+    main_t, _ = O.build_serq_rtn_mx(golden["fmx_w"], golden["fmx_idx"], 32)
+    comp = O.Comp(64, golden["fmx_idx"], r_dense=golden["fmx_r_dense"])
+    assert np.array_equal(O.forward_mx(golden["fmx_x"], main_t, comp), golden["fmx_y_dense"])
+
+
 def test_mx_svd_baseline_forward_matches_reference_golden(golden):
     # SVD baseline over an MX main (compensate.py:326-331): y + (mx_decode(x_mx) L1) L2
     main_t, _ = O.build_serq_rtn_mx(golden["fmx_w"], golden["fmx_idx"], 32)
