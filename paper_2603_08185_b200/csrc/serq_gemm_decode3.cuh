@@ -54,13 +54,18 @@ constexpr int kClRed = 6 * 1024;     // rank-0 landing buffer for narrow partial
 // fused quantizer: kP (token row, 32-block) pairs per lane, M <= 4 kP; used for M <= 8 (at
 // M = 16 the 4-pair converter was slower than the quantizer kernel + PDL: 10.5 vs 8.6 us)
 constexpr int kClFuseM = 8;
+#ifndef SERQ_DEC_STAGES
+#define SERQ_DEC_STAGES 5  // weight stages per CTA (diagnostic builds may raise it: one CTA per SM)
+#endif
 template <bool kFuse, int kRW = 32>
 struct ClCfg {
-  static constexpr int kStages = kRW == 64 ? 4 : 5;  // the 8 KB R tile costs one stage
+  static constexpr int kStages = kRW == 64 ? SERQ_DEC_STAGES - 1 : SERQ_DEC_STAGES;  // the 8 KB R tile costs one stage
   static constexpr int kDecRB = 128 * kRW;
   static constexpr int kSmem = 1024 + kStages * kDecStage + kDecRB + 512 + kClXs + kClRed + 512;
   // 228 KB per SM, 1 KB reserved per CTA
-  static_assert(2 * (kSmem + 1024) <= 228 * 1024, "two CTAs (this linear and the next) must fit on one SM");
+  static_assert(SERQ_DEC_STAGES > 5 || 2 * (kSmem + 1024) <= 228 * 1024,
+                "two CTAs (this linear and the next) must fit on one SM");
+  static_assert(kSmem + 1024 <= 228 * 1024, "one CTA must fit");
   static_assert(7 * 128 * kDecN * 4 <= kStages * kDecStage, "rank-0 reduction buffer reuses the stages");
 };
 

@@ -10,7 +10,8 @@ from paper_2603_08185_b200 import benchmarks as B, _lib
 
 layers = 16
 variants = os.environ.get("VARIANTS", "auto,1,2,3,4,6,8").split(",")
-for K, N in ((4096, 11008), (11008, 4096)):
+SHAPES = [tuple(int(v) for v in kn.split(":")) for kn in os.environ.get("SHAPES", "4096:11008,11008:4096").split(",")]
+for K, N in SHAPES:
     lins = [B.device_mx_linear(K, N, 64, seed=1 + i) for i in range(layers)]
     for M in [int(v) for v in os.environ.get("MS", "1,16").split(",")]:
         x = B.outlier_x(M, K)
