@@ -650,8 +650,8 @@ int serq_mx_decode_bf16(const uint8_t* codes_packed, const uint8_t* sf, int64_t 
   if (rows <= 0 || cols <= 0 || cols % 32) return fail(SERQ_EINVAL, "MX layout needs cols %% 32 == 0");
   if (!codes_packed || !sf || !out) return fail(SERQ_EINVAL, "NULL buffer");
   if (reinterpret_cast<uintptr_t>(out) & 15) return fail(SERQ_EINVAL, "out must be 16-byte aligned");
-  if (rows > 65535) return fail(SERQ_EINVAL, "at most 65535 rows per call");
-  mx_decode_bf16_kernel<<<dim3(unsigned(cdiv(cols / 8, 256)), unsigned(rows)), 256, 0, S(stream)>>>(
+  mx_decode_bf16_kernel<<<dim3(unsigned(cdiv(cols / 8, 256)), unsigned(rows < 65535 ? rows : 65535)), 256, 0,
+                          S(stream)>>>(
       codes_packed, sf, rows, cols, kc_pad_of(cols), static_cast<__nv_bfloat16*>(out));
   LAUNCH_CHECK("mx_decode_bf16");
   return SERQ_OK;

@@ -1506,44 +1506,46 @@ __global__ void unpack_mx_kernel(const uint8_t* __restrict__ packed, const uint8
 // 4-B code load, one 16-B store.
 __global__ void mx_decode_bf16_kernel(const uint8_t* __restrict__ packed, const uint8_t* __restrict__ sf,
                                       int64_t rows, int64_t cols, int kc_pad, __nv_bfloat16* __restrict__ out) {
-  const int64_t row = blockIdx.y;
   const int64_t c0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
   if (c0 >= cols) return;
-  const uint32_t p = *reinterpret_cast<const uint32_t*>(packed + row * (cols / 2) + c0 / 2);
-  const int e = int(sf[sf_offset(row, int(c0 / 32), kc_pad)]) - 127;
-  // |value| = (1 + (m & 1) / 2) 2^((m >> 1) - 1 + e) for m >= 2, 2^(e - 1) for m = 1: the bf16
-  // bits directly (biased exponent, one mantissa bit); a block whose smallest non-zero value
-  // would be subnormal (e <= -125) takes ldexpf
-  uint32_t w[4];
-  if (e > -125) {
+  for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+    const uint32_t p = *reinterpret_cast<const uint32_t*>(packed + row * (cols / 2) + c0 / 2);
+    const int e = int(sf[sf_offset(row, int(c0 / 32), kc_pad)]) - 127;
+    // |value| = (1 + (m & 1) / 2) 2^((m >> 1) - 1 + e) for m >= 2, 2^(e - 1) for m = 1: the bf16
+    // bits directly (biased exponent, one mantissa bit); a block whose smallest non-zero value
+    // would be subnormal (e <= -125), or whose largest would overflow (e >= 126, not reachable
+    // from finite bf16 / f32 input), takes ldexpf
+    uint32_t w[4];
+    if (e > -125 && e < 126) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      uint32_t hv[2];
+      for (int i = 0; i < 4; ++i) {
+        uint32_t hv[2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t c = (p >> (8 * i + 4 * h)) & 0xFu;
-        const uint32_t m = c & 7u;
-        const int ex = (m >= 2 ? int(m >> 1) - 1 : -1) + e + 127;
-        const uint32_t mag = m == 0 ? 0u : (uint32_t(ex) << 7) | ((m >= 2 ? (m & 1u) : 0u) << 6);
-        hv[h] = mag | ((c & 8u) << 12);
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t c = (p >> (8 * i + 4 * h)) & 0xFu;
+          const uint32_t m = c & 7u;
+          const int ex = (m >= 2 ? int(m >> 1) - 1 : -1) + e + 127;
+          const uint32_t mag = m == 0 ? 0u : (uint32_t(ex) << 7) | ((m >= 2 ? (m & 1u) : 0u) << 6);
+          hv[h] = mag | ((c & 8u) << 12);
+        }
+        w[i] = hv[0] | (hv[1] << 16);
       }
-      w[i] = hv[0] | (hv[1] << 16);
-    }
-  } else {
+    } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float v[2];
+      for (int i = 0; i < 4; ++i) {
+        float v[2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t c = (p >> (8 * i + 4 * h)) & 0xFu;
-        const uint32_t m = c & 7u;  // 0, .5, 1, 1.5, 2, 3, 4, 6
-        const float mag = m < 4 ? 0.5f * float(m) : float(1u << ((m >> 1) - 1)) * (m & 1 ? 1.5f : 1.f);
-        v[h] = ldexpf(c & 8u ? -mag : mag, e);
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t c = (p >> (8 * i + 4 * h)) & 0xFu;
+          const uint32_t m = c & 7u;  // 0, .5, 1, 1.5, 2, 3, 4, 6
+          const float mag = m < 4 ? 0.5f * float(m) : float(1u << ((m >> 1) - 1)) * (m & 1 ? 1.5f : 1.f);
+          v[h] = ldexpf(c & 8u ? -mag : mag, e);
+        }
+        w[i] = pack_bf16x2(v[0], v[1]);
       }
-      w[i] = pack_bf16x2(v[0], v[1]);
     }
+    *reinterpret_cast<uint4*>(out + row * cols + c0) = make_uint4(w[0], w[1], w[2], w[3]);
   }
-  *reinterpret_cast<uint4*>(out + row * cols + c0) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // reference INT codes int32 [K, N] (in, out) -> int8 [N, K] K-major, 32x32 smem transpose
