@@ -146,7 +146,7 @@ int serq_rmsnorm_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64
 
 /* Decoder-block glue for decode-sized token counts (toy_block_graph, toymodel.py:88-124; the
  * non-SERQ nodes, f32): res = x (+ o, bf16 [M, ldo], may be NULL), h = rmsnorm(res) * gain
- * (saliency.py:194-196; res may be NULL); mid = silu(gate) * up (saliency.py:199-200; bf16 in,
+ * (saliency.py:194-196; res may be NULL; h NULL: the residual add alone into res); mid = silu(gate) * up (saliency.py:199-200; bf16 in,
  * f32 out); and the token-batch attention (attention_mix, saliency.py:203-216) over M <= 16
  * tokens, head_dim 128, reading q / k / v rows in place (e.g. column views of the fused q/k/v
  * output).  All float32 row-major [M, H] unless a pitch is given. */

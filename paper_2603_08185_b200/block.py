@@ -141,7 +141,11 @@ class DeviceBlock:
         mid = torch.empty((m, ffn), dtype=torch.float32, device=x.device)
         _lib.call("serq_block_silu_mul", gate.data_ptr(), gate.stride(0), up.data_ptr(), up.stride(0), m, ffn,
                   mid.data_ptr(), st)
-        return res1 + self.lin["down_proj"](mid)
+        down = self.lin["down_proj"](mid)
+        out = torch.empty_like(x)  # res1 + down, PDL-chained like the rest of the glue
+        _lib.call("serq_block_add_rmsnorm", res1.data_ptr(), down.data_ptr(), down.stride(0), m, hidden, None,
+                  self.eps, out.data_ptr(), None, st)
+        return out
 
     __call__ = forward
 

@@ -15,7 +15,8 @@
 
 namespace serq {
 
-// res = x (+ float(o)); h = res * rsqrt(mean(res^2) + eps) * g.  One 256-thread CTA per row.
+// res = x (+ float(o)); h = res * rsqrt(mean(res^2) + eps) * g (h == nullptr: the add alone).  One
+// 256-thread CTA per row.
 __global__ void __launch_bounds__(256) block_add_rmsnorm_kernel(const float* __restrict__ x,
                                                                 const __nv_bfloat16* __restrict__ o, int64_t ldo,
                                                                 int M, int H, const float* __restrict__ g, float eps,
@@ -33,6 +34,7 @@ __global__ void __launch_bounds__(256) block_add_rmsnorm_kernel(const float* __r
     if (res) res[int64_t(row) * H + c] = v;
     ss = fmaf(v, v, ss);
   }
+  if (!h) return;  // the residual add alone (the block's output)
 #pragma unroll
   for (int s = 16; s > 0; s >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, s);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
@@ -45,6 +47,76 @@ __global__ void __launch_bounds__(256) block_add_rmsnorm_kernel(const float* __r
     float v = xr[c];
     if (o) v += __bfloat162float(o[int64_t(row) * ldo + c]);
     h[int64_t(row) * H + c] = v * rs * g[c];
+  }
+}
+
+// The same with the row held in registers: 1024 threads per row, kC 16-B chunks per thread (H <=
+// 4096 kC, H % 4 == 0, 16-B aligned rows, o rows 8-B aligned).  Every load of the row is issued
+// before the first use (the loop above waits out one global round trip per 256 elements -- at
+// M = 1 the whole block's latency chain), and res / h are written from the registers.
+template <int kC>
+__global__ void __launch_bounds__(1024) block_add_rmsnorm_reg_kernel(const float* __restrict__ x,
+                                                                    const __nv_bfloat16* __restrict__ o, int64_t ldo,
+                                                                    int M, int H, const float* __restrict__ g,
+                                                                    float eps, float* __restrict__ res,
+                                                                    float* __restrict__ h) {
+  __shared__ float red[32];
+  pdl_launch_dependents();
+  const int row = blockIdx.x, t = threadIdx.x;
+  float4 gv[kC];
+#pragma unroll
+  for (int j = 0; j < kC; ++j) {  // the gain does not depend on the previous kernel
+    const int c = 4 * (t + 1024 * j);
+    gv[j] = (h && c < H) ? __ldg(reinterpret_cast<const float4*>(g + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  pdl_wait();
+  if (row >= M) return;
+  float4 v[kC];
+#pragma unroll
+  for (int j = 0; j < kC; ++j) {
+    const int c = 4 * (t + 1024 * j);
+    v[j] = c < H ? *reinterpret_cast<const float4*>(x + int64_t(row) * H + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (o) {
+    uint2 ov[kC];
+#pragma unroll
+    for (int j = 0; j < kC; ++j) {
+      const int c = 4 * (t + 1024 * j);
+      ov[j] = c < H ? *reinterpret_cast<const uint2*>(o + int64_t(row) * ldo + c) : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int j = 0; j < kC; ++j) {
+      v[j].x += __uint_as_float(ov[j].x << 16);
+      v[j].y += __uint_as_float(ov[j].x & 0xFFFF0000u);
+      v[j].z += __uint_as_float(ov[j].y << 16);
+      v[j].w += __uint_as_float(ov[j].y & 0xFFFF0000u);
+    }
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < kC; ++j) {
+    ss = fmaf(v[j].x, v[j].x, ss);
+    ss = fmaf(v[j].y, v[j].y, ss);
+    ss = fmaf(v[j].z, v[j].z, ss);
+    ss = fmaf(v[j].w, v[j].w, ss);
+    const int c = 4 * (t + 1024 * j);
+    if (res && c < H) *reinterpret_cast<float4*>(res + int64_t(row) * H + c) = v[j];
+  }
+  if (!h) return;  // the residual add alone (the block's output)
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, s);
+  if ((t & 31) == 0) red[t >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < 32; ++w) tot += red[w];
+  const float rs = rsqrtf(tot / float(H) + eps);
+#pragma unroll
+  for (int j = 0; j < kC; ++j) {
+    const int c = 4 * (t + 1024 * j);
+    if (c < H)
+      *reinterpret_cast<float4*>(h + int64_t(row) * H + c) =
+          make_float4(v[j].x * rs * gv[j].x, v[j].y * rs * gv[j].y, v[j].z * rs * gv[j].z, v[j].w * rs * gv[j].w);
   }
 }
 

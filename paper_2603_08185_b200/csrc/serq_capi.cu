@@ -836,11 +836,26 @@ int serq_rmsnorm_quant_int(const void* x, int dtype, int64_t M, int64_t K, int64
 int serq_block_add_rmsnorm(const float* x, const void* o, int64_t ldo, int64_t M, int64_t H, const float* gain,
                            float eps, float* res, float* h, serq_stream_t stream) {
   g_launches = 0;
-  if (M <= 0 || H <= 0 || !x || !gain || !h) return fail(SERQ_EINVAL, "add_rmsnorm needs x, gain, h and M, H > 0");
+  if (M <= 0 || H <= 0 || !x) return fail(SERQ_EINVAL, "add_rmsnorm needs x and M, H > 0");
+  if (h ? !gain : !res) return fail(SERQ_EINVAL, "add_rmsnorm needs gain with h, or res without h");
   if (o && ldo < H) return fail(SERQ_EINVAL, "ldo < H");
-  CK(launch_pdl(block_add_rmsnorm_kernel, dim3(unsigned(M)), dim3(256), 0, S(stream), x,
-                static_cast<const __nv_bfloat16*>(o), ldo, int(M), int(H), gain, eps, res, h));
-  LAUNCH_CHECK("block_add_rmsnorm_kernel");
+  const auto al = [](const void* ptr, int a) { return (reinterpret_cast<uintptr_t>(ptr) & (a - 1)) == 0; };
+  const bool regs = H % 4 == 0 && H <= 8192 && al(x, 16) && (!h || (al(gain, 16) && al(h, 16))) && (!res || al(res, 16)) &&
+                    (!o || (al(o, 8) && ldo % 4 == 0));
+  const __nv_bfloat16* ob = static_cast<const __nv_bfloat16*>(o);
+  if (regs && H <= 4096) {
+    CK(launch_pdl(block_add_rmsnorm_reg_kernel<1>, dim3(unsigned(M)), dim3(1024), 0, S(stream), x, ob, ldo, int(M),
+                  int(H), gain, eps, res, h));
+    LAUNCH_CHECK("block_add_rmsnorm_reg_kernel");
+  } else if (regs) {
+    CK(launch_pdl(block_add_rmsnorm_reg_kernel<2>, dim3(unsigned(M)), dim3(1024), 0, S(stream), x, ob, ldo, int(M),
+                  int(H), gain, eps, res, h));
+    LAUNCH_CHECK("block_add_rmsnorm_reg_kernel");
+  } else {
+    CK(launch_pdl(block_add_rmsnorm_kernel, dim3(unsigned(M)), dim3(256), 0, S(stream), x, ob, ldo, int(M), int(H),
+                  gain, eps, res, h));
+    LAUNCH_CHECK("block_add_rmsnorm_kernel");
+  }
   return SERQ_OK;
 }
 

@@ -1105,6 +1105,33 @@ def test_block_glue_kernels_match_torch_ops(D, M):
     torch.testing.assert_close(mid, torch.nn.functional.silu(gt.float()) * up, rtol=2e-6, atol=1e-6)
 
 
+@pytest.mark.parametrize("M", [1, 3, 16])
+@pytest.mark.parametrize("H", [4096, 6144, 8192, 1002])
+def test_block_add_rmsnorm_shapes(D, M, H):
+    # register-resident residual add + RMSNorm (one or two float4 chunks per thread) and the
+    # looped fallback (H = 1002: rows not 16-B aligned), with and without the bf16 addend / res
+    from paper_2603_08185_b200 import _lib
+    from paper_2603_08185_b200.block import rmsnorm
+
+    g = torch.Generator(device="cuda").manual_seed(M + H)
+    x = torch.randn((M, H), device="cuda", generator=g) * 3
+    o = (torch.randn((M, H), device="cuda", generator=g)).to(torch.bfloat16)
+    gain = torch.rand(H, device="cuda", generator=g) + 0.5
+    for with_o in (True, False):
+        res, h = torch.empty_like(x), torch.empty_like(x)
+        _lib.call("serq_block_add_rmsnorm", x.data_ptr(), o.data_ptr() if with_o else None, H, M, H, gain.data_ptr(),
+                  1e-6, res.data_ptr(), h.data_ptr(), 0)
+        torch.cuda.synchronize()
+        r_ref = x + o if with_o else x
+        assert torch.equal(res, r_ref)
+        torch.testing.assert_close(h, rmsnorm(r_ref, gain, 1e-6), rtol=2e-6, atol=1e-6)
+    # the residual add alone (h NULL): the block's output
+    out = torch.empty_like(x)
+    _lib.call("serq_block_add_rmsnorm", x.data_ptr(), o.data_ptr(), H, M, H, None, 1e-6, out.data_ptr(), None, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(out, x + o)
+
+
 @pytest.mark.parametrize("M", [1, 4, 16])
 def test_device_block_glue_path_matches_torch_path(D, M):
     # the whole block at decode size: glue kernels vs the PyTorch glue, same SERQ linears
