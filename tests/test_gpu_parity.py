@@ -359,6 +359,20 @@ def test_mx_svd_baseline_matches_oracle(D, M, K, N, r):
     assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
 
 
+def test_mx_decode_bf16_many_rows_and_extremes(D):
+    # serq_mx_decode_bf16 past the 65535-row grid limit (grid-stride rows) and at the exponent
+    # extremes (subnormal-range blocks take the ldexpf path): exact vs the oracle's mx_decode
+    rng = np.random.default_rng(17)
+    x = rng.standard_normal((70000, 64)).astype(np.float32)
+    x[:8] *= np.float32(2.0 ** -120)  # blocks whose smallest values are bf16 subnormals
+    x[8:16] *= np.float32(2.0 ** 100)
+    xt = torch.from_numpy(x).cuda()
+    act = D.quantize_mx(xt)
+    got = D.mx_decode_bf16(act).double().cpu().numpy()
+    ref = O.mx_decode(O.mx_encode(x.astype(np.float64), 32))
+    assert np.array_equal(got, ref)
+
+
 @pytest.mark.parametrize("M,K,N,r", [(3, 512, 264, 32), (300, 1024, 520, 64), (1024, 2048, 1024, 128)])
 def test_mx_dense_r_matches_oracle(D, M, K, N, r):
     # MX main + unquantized R at an arbitrary salient set (compensate.py:335-339)
