@@ -1522,8 +1522,10 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   }
   // CTA-pair kernel: int8 weights TMA'd straight into the operand
   // W4 handles always take the CTA-pair kernel (it is the one that widens packed INT4); int8
-  // handles above 128 rows when their R layout allows it
-  const bool pair_ok = h->has_w4 || (M > 128 && (h->r_mode != SERQ_R_INT || h->contiguous) && h->r <= 128 &&
+  // handles too when their R layout allows it -- also between the gemv's 16 rows and one 256-row
+  // tile (rows past M are TMA zero-filled and never stored): up_proj at M = 17..128 took 41 us
+  // on the one-CTA kernel below
+  const bool pair_ok = h->has_w4 || ((h->r_mode != SERQ_R_INT || h->contiguous) && h->r <= 128 &&
                                      (h->r_mode != SERQ_R_DENSE || cdiv(h->K, 128) >= cdiv(h->r, 64)) &&
                                      !SERQ_DBG(g_debug_flags, 65536));
   if (pair_ok) {
