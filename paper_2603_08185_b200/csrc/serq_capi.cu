@@ -1255,7 +1255,10 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
   // pair3 for the permuted layout, and for the gather fallback with r == 64 (debug flag 1<<24: the
   // gather cases take the older pair kernel)
   const bool g3 = h->r > 0 && h->has_r32 && !h->contiguous && xs_codes && xs_sf && !SERQ_DBG(g_debug_flags, 1 << 24);
-  if (M > 128 && (h->r == 0 || (h->has_r32 && h->contiguous) || g3) && !SERQ_DBG(g_debug_flags, 16 | 512)) {
+  // (M > 16: between the decode kernel and one 256-row tile the pair kernels also beat the one-CTA
+  // kernel -- rows past M are TMA zero-filled and never stored; Llama-2-7B up_proj at M = 17..128:
+  // 14.3-15.8 us one-CTA vs 11.6 us pair3, tools/probes/mx_midm_probe.py)
+  if (M > kDecN && (h->r == 0 || (h->has_r32 && h->contiguous) || g3) && !SERQ_DBG(g_debug_flags, 16 | 512)) {
     CK(set_smem_attr(serq_mx_pair3_kernel<false>, k3SmemBytes));
     CK(set_smem_attr(serq_mx_pair3_kernel<true>, k3SmemBytesG));
     CK(set_smem_attr(serq_mx_pair3_kernel<false, true>, k3SmemBytes));
@@ -1318,7 +1321,7 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
     }
     return SERQ_OK;
   }
-  if (M > 128 && !addend && !SERQ_DBG(g_debug_flags, 16)) {
+  if (M > kDecN && !addend && !SERQ_DBG(g_debug_flags, 16)) {
     CK(set_smem_attr(serq_mx_pair_kernel, k2SmemBytes));
     Pair2Maps pm;
     rc = make_map(&pm.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, a_codes, h->K / 2, M, h->K / 2, 128, 128);
