@@ -253,7 +253,7 @@ int serq_linear_int_addend(const serq_linear_t* h, const int8_t* a_codes, const 
 
 /* K2 with an fp32 addend C [M, N] (row pitch N, 16-B aligned) summed into the fp32 accumulator before the
  * bf16 store: y = bf16(mx_gemm(x, main) + C).  The MX SVD baseline (compensate.py:326-331);
- * the handle must carry no salient term (r = 0).  M > 128: the CTA-pair kernel; smaller M
+ * the handle must carry no salient term (r = 0).  M > 16: the CTA-pair kernel; smaller M
  * the one-CTA persistent kernel. */
 int serq_linear_mx_addend(const serq_linear_t* h, const uint8_t* a_codes, const uint8_t* a_sf, int64_t M,
                           const float* addend, void* y, int64_t ldy, serq_stream_t stream);

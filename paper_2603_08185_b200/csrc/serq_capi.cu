@@ -1247,7 +1247,7 @@ static int linear_mx_impl(const serq_linear_t* h, const uint8_t* a_codes, const 
   p.w_ksteps = h->w_ksteps;
   p.dbg = g_debug_flags;
   p.dbg_ts = g_debug_ts;
-  p.addend = addend;  // (the SVD baseline: the CTA-pair kernel for M > 128, else the one-CTA kernel)
+  p.addend = addend;  // (the SVD baseline: the CTA-pair kernel for M > 16, else the one-CTA kernel)
   // decode kernel: any contiguous R up to r = 128; the gather fallback with r = 64 (32-B xs rows)
   const bool dec_ok = !addend && (h->r == 0 || (h->dec_rw && (h->contiguous || h->has_r32)));
   if (M <= kDecN && dec_ok && !SERQ_DBG(g_debug_flags, 2048))

@@ -382,8 +382,9 @@ class MxLinear:
         return y
 
     def forward(self, x: torch.Tensor, act: MxActivation | None = None, y: torch.Tensor | None = None) -> torch.Tensor:
-        """Quantize + linear in ONE C-ABI call (serq_forward_mx): for M > 128 the
-        quantizer hands finished 256-row tiles to the running linear."""
+        """Quantize + linear in ONE C-ABI call (serq_forward_mx): the linear is launched with
+        programmatic dependent launch behind the quantizer (M <= 8: the quantizer runs inside
+        the decode kernel)."""
         _require_cuda(x, "x")
         if x.dim() != 2 or x.stride(1) != 1:
             raise ValidationError("x must be a row-major 2-D tensor")
@@ -693,7 +694,7 @@ class SvdMxLinear:
     bf16); U = x_hat L1 and C = U L2 are two plain cuBLAS GEMMs (bf16 operands, fp32
     accumulation, U rounded to bf16 between them -- 2^-9 relative on the correction term, as in
     SvdIntLinear -- and C kept in fp32); the MX kernel adds C to its fp32 accumulator before the
-    one bf16 rounding of Y (``serq_linear_mx_addend``: the CTA-pair kernel for M > 128).  A
+    one bf16 rounding of Y (``serq_linear_mx_addend``: the CTA-pair kernel for M > 16).  A
     comparison baseline, not the SERQ hot path: the salient-term fusion of MxLinear does not
     apply, because the correction spans all K columns."""
 
