@@ -1416,7 +1416,9 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   const bool need_xs = h->r_mode == SERQ_R_DENSE || h->r_mode == SERQ_R_DENSE_SPLIT ||
                        (h->r_mode == SERQ_R_INT && !h->contiguous);
   if (need_xs && !xs) return fail(SERQ_EINVAL, "this R mode needs the quantizer's xs slice");
-  if (M <= 16 && !h->use_i8g && h->r <= 128 && !SERQ_DBG(g_debug_flags, 1 << 29)) {
+  // (group-wise handles too: each main warp owns whole groups, at most kGemvMaxGpw of them)
+  const bool gemv_fmt_ok = !h->use_i8g || h->groups <= kGemvMaxGpw * 4;
+  if (M <= 16 && gemv_fmt_ok && h->r <= 128 && !SERQ_DBG(g_debug_flags, 1 << 29)) {
     // decode sizes: the weight stream with warp-level MMAs (serq_gemv_i8.cuh), int8 or packed INT4
     GemvI8Params gp{};
     gp.w = static_cast<const int8_t*>(h->w);
@@ -1438,6 +1440,12 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     gp.addend = addend;
     gp.acc_dump = acc_dump;
     gp.accr_dump = accr_dump;
+    gp.sw_g = h->sw_g;
+    gp.cterm = h->cterm;
+    gp.colsum_g = h->colsum_g;
+    gp.groups = h->groups;
+    gp.gchunks = 2 * h->gsteps;  // 64-K chunks per group
+    const int fmt = h->use_i8g ? 2 : h->has_w4 ? 1 : 0;
     const bool sgn = zp == nullptr;
     // 16 weight rows per CTA; 8 (M <= 8) / 7 warps split K when the row groups alone leave SMs
     // idle (a wave holds 2 such CTAs per SM), 4 otherwise (all CTAs in one wave); plus one warp
@@ -1451,8 +1459,9 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
            : launch_pdl(serq_i8_gemv_kernel<NT, SG, KR, 4, W4>, grid, blk, 0, S(stream), gp)
 #define GEMV_W(NT, SG, KR)                                                                                          \
   do {                                                                                                             \
-    if (h->has_w4) GEMV_W4(NT, SG, KR, true);                                                                      \
-    else GEMV_W4(NT, SG, KR, false);                                                                               \
+    if (fmt == 2) GEMV_W4(NT, SG, KR, 2);                                                                          \
+    else if (fmt == 1) GEMV_W4(NT, SG, KR, 1);                                                                     \
+    else GEMV_W4(NT, SG, KR, 0);                                                                                   \
   } while (0)
 #define GEMV_R(NT, KR)                                                                                              \
   do {                                                                                                             \
@@ -1463,6 +1472,7 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   do {                                                                                                             \
     if (h->r_mode == SERQ_R_INT) GEMV_R(NT, kRInt);                                                                \
     else if (h->r_mode == SERQ_R_DENSE) GEMV_R(NT, kRDense);                                                       \
+    else if (h->r_mode == SERQ_R_DENSE_SPLIT) GEMV_R(NT, kRDenseSplit);                                            \
     else GEMV_R(NT, 0);                                                                                            \
   } while (0)
     if (M <= 8) GEMV_M(1);

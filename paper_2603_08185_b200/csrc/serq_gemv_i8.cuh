@@ -49,8 +49,14 @@ struct GemvI8Params {
   __nv_bfloat16* y;         // [M, ldy]
   int64_t ldy;
   const float* addend;      // optional fp32 [M, N] added after scaling (the SVD-baseline path)
-  int32_t* acc_dump;        // tests: exact accumulators acc - zp * colsum, [M, N]
+  int32_t* acc_dump;        // tests: exact accumulators acc - zp * colsum, [M, N] (group-wise: [G][M][N])
   int32_t* accr_dump;       // tests: exact integer-R accumulators
+  // group-wise weights (row groups of gchunks 64-K chunks, serq_pack_int_grouped; the i8g kernel's
+  // promotion): Y = sx * (sum_g sw_g[g, n] A_g + R term - zp * cterm[n])
+  const float* sw_g;        // [G][N]
+  const float* cterm;       // [N] sum_g sw_g * colsum_g (+ sr * colsum_r)
+  const int32_t* colsum_g;  // [G][N] (dumps only)
+  int groups, gchunks;
 };
 
 template <bool kSigned>
@@ -105,9 +111,16 @@ __device__ __forceinline__ void gemv_mma_chunk(const uint4& wlo, const uint4& wh
 // 128-row tile and 128-K step, 64 B per row, so a CTA's 16 rows are one contiguous 1 KB); a K
 // "chunk" is then 128 elements, a lane's 16 B are its rows' elements [32q, 32q + 32) of it, widened
 // in registers (widen_int4x8, natural order) to the two 16-B pieces the int8 path would have loaded
-template <int kNT, bool kSigned, int kR, int kWarps, bool kW4 = false>
+// kFmt: 0 int8 weights, one scale per output column; 1 packed INT4 (kW4 below); 2 group-wise int8
+// weights (kG): every main warp owns whole groups, promotes each group's exact s32 partial with its
+// scale in fp32 (scales staged in shared memory before the wait) and the side warp applies the
+// folded zero-point term, as serq_i8g_pair_kernel does
+constexpr int kGemvMaxGpw = 32;  // groups per main warp (group-wise: G <= 32 * warps)
+template <int kNT, bool kSigned, int kR, int kWarps, int kFmt = 0>
 __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MINB4 : SERQ_GEMV_MINB8) serq_i8_gemv_kernel(const GemvI8Params p) {
-  __shared__ int red_i[kWarps][kNT][32][4];  // [main warp][fragment][lane][c]
+  constexpr bool kW4 = kFmt == 1, kG = kFmt == 2;
+  __shared__ int red_i[kWarps][kNT][32][4];  // [main warp][fragment][lane][c] (group-wise: fp32 bits)
+  __shared__ float sgr[kG ? kWarps * kGemvMaxGpw * 16 : 1];  // group-wise: [warp][group][row] scales
   pdl_launch_dependents();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
@@ -118,8 +131,17 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
     // ---- main warps: this warp's K chunks (64 elements each; 128 packed INT4), a contiguous 1 / kWarps
     constexpr int kChunk = kW4 ? 128 : 64;
     const int nch = (p.K + kChunk - 1) / kChunk;
-    const int per = (nch + kWarps - 1) / kWarps;
+    const int gpw = kG ? (p.groups + kWarps - 1) / kWarps : 0;
+    const int per = kG ? gpw * p.gchunks : (nch + kWarps - 1) / kWarps;
     const int c0 = warp * per, c1 = min(nch, c0 + per);
+    if constexpr (kG) {  // this warp's group scales for its 16 rows (weights: before the wait)
+      for (int j = lane; j < gpw * 16; j += 32) {
+        const int gi = warp * gpw + (j >> 4), n = row0 + (j & 15);
+        sgr[(warp * kGemvMaxGpw + (j >> 4)) * 16 + (j & 15)] =
+            (gi < p.groups && n < p.N) ? __ldg(p.sw_g + size_t(gi) * p.N + n) : 0.f;
+      }
+      __syncwarp();
+    }
     const int8_t* wlo_p;
     const int8_t* whi_p;
     size_t cstride;  // bytes from one chunk of a row to the next
@@ -148,10 +170,37 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
     }
     pdl_wait();  // activation codes come from the quantizer
     int acc[kNT][4];
+    float facc[kNT][4];  // group-wise: the promoted partials
 #pragma unroll
     for (int f = 0; f < kNT; ++f)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc[f][i] = 0;
+      for (int i = 0; i < 4; ++i) {
+        acc[f][i] = 0;
+        facc[f][i] = 0.f;
+      }
+    int gc = 0, gl = 0;  // group-wise: chunks into the current group, group index within the warp
+    // group-wise: fold the finished group's exact partial (and dump it for the tests)
+    auto fold = [&]() {
+      const float s_lo = sgr[(warp * kGemvMaxGpw + gl) * 16 + g], s_hi = sgr[(warp * kGemvMaxGpw + gl) * 16 + g + 8];
+      const int gi = warp * gpw + gl;
+#pragma unroll
+      for (int f = 0; f < kNT; ++f)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (p.acc_dump) {
+            const int n = i >= 2 ? rhi : rlo, t = f * 8 + 2 * q + (i & 1);
+            if (n < p.N && t < p.M) {
+              const uint32_t zp = p.zp ? uint32_t(p.zp[t]) : 0u;
+              p.acc_dump[(size_t(gi) * p.M + t) * p.N + n] =
+                  int32_t(uint32_t(acc[f][i]) - zp * uint32_t(p.colsum_g[size_t(gi) * p.N + n]));
+            }
+          }
+          facc[f][i] = fmaf(float(acc[f][i]), i >= 2 ? s_hi : s_lo, facc[f][i]);
+          acc[f][i] = 0;
+        }
+      gc = 0;
+      ++gl;
+    };
     // the token fragments of the 16 activation bytes at element k of each token row
     auto act = [&](int k, uint4 (&b)[kNT]) {
 #pragma unroll
@@ -185,13 +234,16 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
             act((c + u) * 64 + 16 * q, b);
             gemv_mma_chunk<kNT, kSigned>(lo, hi, b, acc);
           }
+          if constexpr (kG) {
+            if (++gc == p.gchunks || c + u + 1 == c1) fold();
+          }
         }
       }
     }
 #pragma unroll
     for (int f = 0; f < kNT; ++f)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) red_i[warp][f][lane][i] = acc[f][i];
+      for (int i = 0; i < 4; ++i) red_i[warp][f][lane][i] = kG ? __float_as_int(facc[f][i]) : acc[f][i];
     __syncthreads();
     return;
   }
@@ -204,8 +256,12 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
   for (int h = 0; h < 2; ++h) {
     const int n = h ? rhi : rlo;
     if (n < p.N) {
-      cs[h] = __ldg(p.colsum + n);
-      swv[h] = __ldg(p.sw + n);
+      if constexpr (kG) {
+        swv[h] = __ldg(p.cterm + n);  // (group-wise: the folded zero-point term)
+      } else {
+        cs[h] = __ldg(p.colsum + n);
+        swv[h] = __ldg(p.sw + n);
+      }
       if constexpr (kR == kRInt) {
         csr[h] = __ldg(p.colsum_r + n);
         srv[h] = __ldg(p.sr + n);
@@ -247,27 +303,31 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
       }
       gemv_mma_chunk<kNT, kSigned>(rwl[c], rwh[c], b, accr);
     }
-  } else if constexpr (kR == kRDense) {
-    const __nv_bfloat16* rw = static_cast<const __nv_bfloat16*>(p.rw);
+  } else if constexpr (kR == kRDense || kR == kRDenseSplit) {
     const __nv_bfloat16* xs = static_cast<const __nv_bfloat16*>(p.xs);
-    // 16-element chunks (r <= 128: eight): a lane holds elements [4q, 4q + 4) (logical k {2q, 2q+1, 2q+8, 2q+9})
-    uint2 rl[8], rh[8];
+    // 16-element chunks (r <= 128: eight): a lane holds elements [4q, 4q + 4) (logical k {2q, 2q+1, 2q+8, 2q+9});
+    // split R: the bf16 hi plane (rows [0, N)) then the lo plane (rows [N, 2N)) into the same fp32 sum
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const bool in = c * 16 + 4 * q < p.r;
-      rl[c] = (ok_lo && in) ? *reinterpret_cast<const uint2*>(rw + size_t(rlo) * p.r + c * 16 + 4 * q) : make_uint2(0, 0);
-      rh[c] = (ok_hi && in) ? *reinterpret_cast<const uint2*>(rw + size_t(rhi) * p.r + c * 16 + 4 * q) : make_uint2(0, 0);
-    }
-    pdl_wait();
+    for (int plane = 0; plane < (kR == kRDenseSplit ? 2 : 1); ++plane) {
+      const __nv_bfloat16* rw = static_cast<const __nv_bfloat16*>(p.rw) + size_t(plane) * p.N * p.r;
+      uint2 rl[8], rh[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const bool in = c * 16 + 4 * q < p.r;
+      for (int c = 0; c < 8; ++c) {
+        const bool in = c * 16 + 4 * q < p.r;
+        rl[c] = (ok_lo && in) ? *reinterpret_cast<const uint2*>(rw + size_t(rlo) * p.r + c * 16 + 4 * q) : make_uint2(0, 0);
+        rh[c] = (ok_hi && in) ? *reinterpret_cast<const uint2*>(rw + size_t(rhi) * p.r + c * 16 + 4 * q) : make_uint2(0, 0);
+      }
+      if (plane == 0) pdl_wait();
 #pragma unroll
-      for (int f = 0; f < kNT; ++f) {
-        const int t = f * 8 + g;
-        const uint2 b = (t < p.M && in) ? *reinterpret_cast<const uint2*>(xs + size_t(t) * p.r + c * 16 + 4 * q)
-                                        : make_uint2(0, 0);
-        mma_bf16(accd[f], rl[c].x, rh[c].x, rl[c].y, rh[c].y, b.x, b.y);
+      for (int c = 0; c < 8; ++c) {
+        const bool in = c * 16 + 4 * q < p.r;
+#pragma unroll
+        for (int f = 0; f < kNT; ++f) {
+          const int t = f * 8 + g;
+          const uint2 b = (t < p.M && in) ? *reinterpret_cast<const uint2*>(xs + size_t(t) * p.r + c * 16 + 4 * q)
+                                          : make_uint2(0, 0);
+          mma_bf16(accd[f], rl[c].x, rh[c].x, rl[c].y, rh[c].y, b.x, b.y);
+        }
       }
     }
   } else {
@@ -290,24 +350,39 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
   for (int f = 0; f < kNT; ++f)
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      int s = 0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) s += red_i[w][f][lane][i];  // exact
       const int h = i >> 1;
       const int n = h ? rhi : rlo;
       const int t = f * 8 + 2 * q + (i & 1);
       if (n >= p.N || t >= p.M) continue;
       const uint32_t zp = zpv[f][i & 1];
-      const int32_t a_ref = int32_t(uint32_t(s) - zp * uint32_t(cs[h]));  // wrapping int32, exact
-      float yv = float(a_ref) * swv[h];
-      if constexpr (kR == kRInt) {
-        const int32_t ar_ref = int32_t(uint32_t(accr[f][i]) - zp * uint32_t(csr[h]));
-        yv += float(ar_ref) * srv[h];
-        if (p.accr_dump) p.accr_dump[size_t(t) * p.N + n] = ar_ref;
-      } else if constexpr (kR == kRDense) {
-        yv += accd[f][i];
+      float yv;
+      if constexpr (kG) {
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) s += __int_as_float(red_i[w][f][lane][i]);
+        yv = s;
+        if constexpr (kR == kRInt) {
+          yv = fmaf(float(accr[f][i]), srv[h], yv);  // raw: sr * colsum_r is in cterm
+          if (p.accr_dump) p.accr_dump[size_t(t) * p.N + n] = int32_t(uint32_t(accr[f][i]) - zp * uint32_t(csr[h]));
+        } else if constexpr (kR == kRDense || kR == kRDenseSplit) {
+          yv += accd[f][i];
+        }
+        yv -= float(zp) * swv[h];
+      } else {
+        int s = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) s += red_i[w][f][lane][i];  // exact
+        const int32_t a_ref = int32_t(uint32_t(s) - zp * uint32_t(cs[h]));  // wrapping int32, exact
+        yv = float(a_ref) * swv[h];
+        if constexpr (kR == kRInt) {
+          const int32_t ar_ref = int32_t(uint32_t(accr[f][i]) - zp * uint32_t(csr[h]));
+          yv += float(ar_ref) * srv[h];
+          if (p.accr_dump) p.accr_dump[size_t(t) * p.N + n] = ar_ref;
+        } else if constexpr (kR == kRDense || kR == kRDenseSplit) {
+          yv += accd[f][i];
+        }
+        if (p.acc_dump) p.acc_dump[size_t(t) * p.N + n] = a_ref;
       }
-      if (p.acc_dump) p.acc_dump[size_t(t) * p.N + n] = a_ref;
       float out = yv * sxv[f][i & 1];
       if (p.addend) out += p.addend[size_t(t) * p.N + n];
       p.y[size_t(t) * p.ldy + n] = __float2bfloat16_rn(out);

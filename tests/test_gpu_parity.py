@@ -471,6 +471,11 @@ def test_int_linear_gather_int_r(D):
     (130, 1024, 776, 256, 96, 4, False, "dense"),
     (300, 1024, 512, 128, 128, 8, False, "split"),  # dequantize(col-grouped R) as bf16 hi + lo
     (64, 2048, 256, 2048, 64, 8, False, "split"),   # one group spanning K: the split R on a per-channel main
+    # decode sizes (M <= 16): the group-wise gemv (whole groups per warp, fp32 promotion)
+    (1, 1024, 520, 128, 128, 8, False, "int"),
+    (5, 2048, 264, 256, 64, 4, True, "dense"),
+    (16, 1024, 512, 128, 128, 8, False, "split"),
+    (3, 4096, 1000, 128, 64, 8, False, "none"),
 ])
 def test_int_grouped_linear_parity(D, M, K, N, g, r, bits, symmetric, r_mode):
     # int_gemm_reference row-grouped branch: one exact integer partial per group
@@ -507,6 +512,7 @@ def test_int_grouped_linear_parity(D, M, K, N, g, r, bits, symmetric, r_mode):
             assert np.array_equal(accr.cpu().numpy().astype(np.int64), rp[0][1])
         mx, mean = O.parity_errors(y, y_ref)
         assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
+    assert D.last_kernel() == ("serq_i8_gemv_kernel" if M <= 16 else "serq_i8g_pair_kernel")
 
 
 def test_int_grouped_rejects_unsupported_groups(D):
