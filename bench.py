@@ -421,6 +421,7 @@ def other_configs(hbm_gbs: float) -> dict:
         out["c4_decode_fused"] = B.decode_fused_points(hbm_gbs)
         out["int_decode_7b"] = B.int_decode_points(hbm_gbs)
         out["int_decode_7b_w4"] = B.int_decode_points(hbm_gbs, weight_format="int4")
+        out["int_decode_7b_g128"] = B.int_decode_points(hbm_gbs, group=128)
         out["producer_rmsnorm_quant_c2"] = B.rmsnorm_quant_point(4096, 4096, hbm_gbs)
         out["producer_rmsnorm_quant_int_c3"] = B.rmsnorm_int_quant_point(2048, 4096, 8, False, hbm_gbs)
         # C4 as a whole block: Llama-2-7B-shaped decoder block (SERQ linears + f32 non-linear nodes)

@@ -197,15 +197,17 @@ def decode_points(hbm_peak_gbs: float, layers: int = 16) -> list:
     return out
 
 
-def int_decode_points(hbm_peak_gbs: float, layers: int = 8, weight_format: str = "int8") -> list:
+def int_decode_points(hbm_peak_gbs: float, layers: int = 8, weight_format: str = "int8",
+                      group: int | None = None) -> list:
     """INT decode (serq_i8_gemv_kernel): Llama-2-7B up_proj / down_proj with int8 or packed INT4
-    (``weight_format``) weights and an integer R (r = 128), A8 asymmetric tokens, M = 1 / 4 / 16;
-    ``layers`` distinct weight sets per graph (> L2).  Bytes = resident weights + R + scales /
-    colsums + activations + outputs."""
+    (``weight_format``) weights -- per output channel, or in row groups of ``group`` (int8) -- and
+    an integer R (r = 128), A8 asymmetric tokens, M = 1 / 4 / 16; ``layers`` distinct weight sets
+    per graph (> L2).  Bytes = resident weights + R + scales / colsums + activations + outputs."""
     out = []
     for K, N in ((4096, 11008), (11008, 4096)):
-        lins = [device_int_linear(K, N, 128, "int", seed=1 + i, weight_format=weight_format) for i in range(layers)]
-        wbytes = lins[0].weight_bytes()[0]
+        lins = [device_int_linear(K, N, 128, "int", seed=1 + i, weight_format=weight_format, group=group)
+                for i in range(layers)]
+        wbytes = lins[0].weight_bytes()[0] + (4 * N * (K // group) if group else 0)  # + fp32 group scales
         for M in (1, 4, 16):
             xs = [outlier_x(M, K, seed=i) for i in range(layers)]
             acts = [lins[0].quantize(x, 8, False) for x in xs]
@@ -214,7 +216,8 @@ def int_decode_points(hbm_peak_gbs: float, layers: int = 8, weight_format: str =
             t_step = time_steps(lambda i: lins[i % layers].forward(xs[i % layers], 8, False, acts[i % layers],
                                                                   ys[i % layers]), 2 * layers)
             byts = wbytes + 128 * N + 16 * N + M * K + 8 * M + 2 * M * N
-            out.append({"M": M, "K": K, "N": N, "r": 128, "weights": weight_format, "kernel": D.last_kernel(),
+            out.append({"M": M, "K": K, "N": N, "r": 128, "weights": weight_format, "group": group or K,
+                        "kernel": D.last_kernel(),
                         "step_us": t_step * 1e3, "linear_us": t_lin * 1e3,
                         "linear_hbm_gbs": byts / (t_lin * 1e-3) / 1e9,
                         "linear_hbm_frac": byts / (t_lin * 1e-3) / 1e9 / hbm_peak_gbs})
