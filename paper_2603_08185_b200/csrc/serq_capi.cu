@@ -23,6 +23,10 @@
 #include "serq_block.cuh"
 #include "serq_quant.cuh"
 
+#ifndef SERQ_GEMV_I8G_MAX_M
+#define SERQ_GEMV_I8G_MAX_M 32  // group-wise INT handles with few tiles: the token-grouped gemv up to this many rows
+#endif
+
 using namespace serq;
 
 namespace {
@@ -1418,7 +1422,13 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   if (need_xs && !xs) return fail(SERQ_EINVAL, "this R mode needs the quantizer's xs slice");
   // (group-wise handles too: each main warp owns whole groups, at most kGemvMaxGpw of them)
   const bool gemv_fmt_ok = !h->use_i8g || h->groups <= kGemvMaxGpw * 4;
-  if (M <= 16 && gemv_fmt_ok && h->r <= 128 && !SERQ_DBG(g_debug_flags, 1 << 29)) {
+  // group-wise handles with few 256-column tiles (the i8g pair kernel would leave most CTA pairs
+  // idle) take the gemv up to M = 32, one 16-token group per grid row; each group re-streams the
+  // weights, so this pays only there (tools/probes/i8g_smallm_probe.py: Llama-2-7B down_proj, 16
+  // tiles, M = 32: 36 vs 79 us; up_proj, 43 tiles: 39 vs 34 us, not taken)
+  const int64_t gemv_max_m =
+      h->use_i8g && 3 * cdiv(h->N, 256) <= int64_t(sm_count()) / 2 ? SERQ_GEMV_I8G_MAX_M : 16;
+  if (M <= gemv_max_m && gemv_fmt_ok && h->r <= 128 && !SERQ_DBG(g_debug_flags, 1 << 29)) {
     // decode sizes: the weight stream with warp-level MMAs (serq_gemv_i8.cuh), int8 or packed INT4
     GemvI8Params gp{};
     gp.w = static_cast<const int8_t*>(h->w);
@@ -1452,7 +1462,7 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
     // for the salient term and the epilogue (tools/probes/int_decode_probe.py for the A/B)
     const int64_t groups = cdiv(h->N, 16);
     const bool wide = groups <= 2 * int64_t(sm_count());
-    const dim3 grid{unsigned(groups)}, blk{!wide ? 160u : M <= 8 ? 288u : 256u};  // + the side / epilogue warp
+    const dim3 grid{unsigned(groups), unsigned(cdiv(M, 16))}, blk{!wide ? 160u : M <= 8 ? 288u : 256u};  // + side warp
     cudaError_t e = cudaSuccess;
 #define GEMV_W4(NT, SG, KR, W4)                                                                                     \
   e = wide ? launch_pdl(serq_i8_gemv_kernel<NT, SG, KR, NT == 1 ? 8 : 7, W4>, grid, blk, 0, S(stream), gp)        \

@@ -125,6 +125,9 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int row0 = blockIdx.x * 16;
+  // tokens: blockIdx.y selects 16 of them (M > 16: each token group re-streams the weights, mostly
+  // from L2); t below is the token within the group
+  const int t0 = blockIdx.y * 16, mloc = min(16, p.M - t0);
   const int rlo = row0 + g, rhi = row0 + g + 8;
   const bool ok_lo = rlo < p.N, ok_hi = rhi < p.N;
   if (warp < kWarps) {
@@ -189,9 +192,9 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
         for (int i = 0; i < 4; ++i) {
           if (p.acc_dump) {
             const int n = i >= 2 ? rhi : rlo, t = f * 8 + 2 * q + (i & 1);
-            if (n < p.N && t < p.M) {
-              const uint32_t zp = p.zp ? uint32_t(p.zp[t]) : 0u;
-              p.acc_dump[(size_t(gi) * p.M + t) * p.N + n] =
+            if (n < p.N && t < mloc) {
+              const uint32_t zp = p.zp ? uint32_t(p.zp[t0 + t]) : 0u;
+              p.acc_dump[(size_t(gi) * p.M + t0 + t) * p.N + n] =
                   int32_t(uint32_t(acc[f][i]) - zp * uint32_t(p.colsum_g[size_t(gi) * p.N + n]));
             }
           }
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
 #pragma unroll
       for (int f = 0; f < kNT; ++f) {
         const int t = f * 8 + g;
-        b[f] = (t < p.M && k < p.K) ? __ldg(reinterpret_cast<const uint4*>(p.a + size_t(t) * p.K + k))
+        b[f] = (t < mloc && k < p.K) ? __ldg(reinterpret_cast<const uint4*>(p.a + size_t(t0 + t) * p.K + k))
                                     : make_uint4(0, 0, 0, 0);
       }
     };
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
 #pragma unroll
       for (int f = 0; f < kNT; ++f) {
         const int t = f * 8 + g;
-        b[f] = (t < p.M && in) ? __ldg(reinterpret_cast<const uint4*>(ar + size_t(t) * lda + c * 64 + 16 * q))
+        b[f] = (t < mloc && in) ? __ldg(reinterpret_cast<const uint4*>(ar + size_t(t0 + t) * lda + c * 64 + 16 * q))
                                : make_uint4(0, 0, 0, 0);
       }
       gemv_mma_chunk<kNT, kSigned>(rwl[c], rwh[c], b, accr);
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
 #pragma unroll
         for (int f = 0; f < kNT; ++f) {
           const int t = f * 8 + g;
-          const uint2 b = (t < p.M && in) ? *reinterpret_cast<const uint2*>(xs + size_t(t) * p.r + c * 16 + 4 * q)
+          const uint2 b = (t < mloc && in) ? *reinterpret_cast<const uint2*>(xs + size_t(t0 + t) * p.r + c * 16 + 4 * q)
                                           : make_uint2(0, 0);
           mma_bf16(accd[f], rl[c].x, rh[c].x, rl[c].y, rh[c].y, b.x, b.y);
         }
@@ -341,8 +344,8 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int t = f * 8 + 2 * q + j;
-      sxv[f][j] = t < p.M ? __ldg(p.sx + t) : 0.f;
-      zpv[f][j] = (p.zp && t < p.M) ? uint32_t(__ldg(p.zp + t)) : 0u;
+      sxv[f][j] = t < mloc ? __ldg(p.sx + t0 + t) : 0.f;
+      zpv[f][j] = (p.zp && t < mloc) ? uint32_t(__ldg(p.zp + t0 + t)) : 0u;
     }
   __syncthreads();
   // lane (g, q) of fragment f holds rows g / g + 8, tokens f * 8 + 2q / 2q + 1
@@ -353,7 +356,7 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
       const int h = i >> 1;
       const int n = h ? rhi : rlo;
       const int t = f * 8 + 2 * q + (i & 1);
-      if (n >= p.N || t >= p.M) continue;
+      if (n >= p.N || t >= mloc) continue;
       const uint32_t zp = zpv[f][i & 1];
       float yv;
       if constexpr (kG) {
@@ -363,7 +366,7 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
         yv = s;
         if constexpr (kR == kRInt) {
           yv = fmaf(float(accr[f][i]), srv[h], yv);  // raw: sr * colsum_r is in cterm
-          if (p.accr_dump) p.accr_dump[size_t(t) * p.N + n] = int32_t(uint32_t(accr[f][i]) - zp * uint32_t(csr[h]));
+          if (p.accr_dump) p.accr_dump[size_t(t0 + t) * p.N + n] = int32_t(uint32_t(accr[f][i]) - zp * uint32_t(csr[h]));
         } else if constexpr (kR == kRDense || kR == kRDenseSplit) {
           yv += accd[f][i];
         }
@@ -377,15 +380,15 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kWarps == 4 ? SERQ_GEMV_MIN
         if constexpr (kR == kRInt) {
           const int32_t ar_ref = int32_t(uint32_t(accr[f][i]) - zp * uint32_t(csr[h]));
           yv += float(ar_ref) * srv[h];
-          if (p.accr_dump) p.accr_dump[size_t(t) * p.N + n] = ar_ref;
+          if (p.accr_dump) p.accr_dump[size_t(t0 + t) * p.N + n] = ar_ref;
         } else if constexpr (kR == kRDense || kR == kRDenseSplit) {
           yv += accd[f][i];
         }
-        if (p.acc_dump) p.acc_dump[size_t(t) * p.N + n] = a_ref;
+        if (p.acc_dump) p.acc_dump[size_t(t0 + t) * p.N + n] = a_ref;
       }
       float out = yv * sxv[f][i & 1];
-      if (p.addend) out += p.addend[size_t(t) * p.N + n];
-      p.y[size_t(t) * p.ldy + n] = __float2bfloat16_rn(out);
+      if (p.addend) out += p.addend[size_t(t0 + t) * p.N + n];
+      p.y[size_t(t0 + t) * p.ldy + n] = __float2bfloat16_rn(out);
     }
 }
 

@@ -476,6 +476,10 @@ def test_int_linear_gather_int_r(D):
     (5, 2048, 264, 256, 64, 4, True, "dense"),
     (16, 1024, 512, 128, 128, 8, False, "split"),
     (3, 4096, 1000, 128, 64, 8, False, "none"),
+    # 16 < M <= 64: the same gemv over 16-token groups (grid rows)
+    (24, 1024, 520, 128, 128, 8, False, "int"),
+    (32, 2048, 264, 256, 64, 4, True, "dense"),
+    (64, 2048, 264, 256, 64, 4, True, "dense"),  # past the token-grouped gemv: the i8g pair kernel
 ])
 def test_int_grouped_linear_parity(D, M, K, N, g, r, bits, symmetric, r_mode):
     # int_gemm_reference row-grouped branch: one exact integer partial per group
@@ -512,7 +516,7 @@ def test_int_grouped_linear_parity(D, M, K, N, g, r, bits, symmetric, r_mode):
             assert np.array_equal(accr.cpu().numpy().astype(np.int64), rp[0][1])
         mx, mean = O.parity_errors(y, y_ref)
         assert mx <= TOL_MAX and mean <= TOL_MEAN, (mx, mean)
-    assert D.last_kernel() == ("serq_i8_gemv_kernel" if M <= 16 else "serq_i8g_pair_kernel")
+    assert D.last_kernel() == ("serq_i8_gemv_kernel" if M <= 32 else "serq_i8g_pair_kernel")
 
 
 def test_int_grouped_rejects_unsupported_groups(D):
