@@ -1422,12 +1422,14 @@ static int linear_int_impl(const serq_linear_t* h, const int8_t* a_codes, const 
   if (need_xs && !xs) return fail(SERQ_EINVAL, "this R mode needs the quantizer's xs slice");
   // (group-wise handles too: each main warp owns whole groups, at most kGemvMaxGpw of them)
   const bool gemv_fmt_ok = !h->use_i8g || h->groups <= kGemvMaxGpw * 4;
-  // group-wise handles with few 256-column tiles (the i8g pair kernel would leave most CTA pairs
-  // idle) take the gemv up to M = 32, one 16-token group per grid row; each group re-streams the
-  // weights, so this pays only there (tools/probes/i8g_smallm_probe.py: Llama-2-7B down_proj, 16
-  // tiles, M = 32: 36 vs 79 us; up_proj, 43 tiles: 39 vs 34 us, not taken)
-  const int64_t gemv_max_m =
-      h->use_i8g && 3 * cdiv(h->N, 256) <= int64_t(sm_count()) / 2 ? SERQ_GEMV_I8G_MAX_M : 16;
+  // group-wise and packed-INT4 handles with few 256-column tiles (their pair kernels would leave
+  // most CTA pairs idle) take the gemv up to M = 32, one 16-token group per grid row; each group
+  // re-streams the weights, so this pays only there (Llama-2-7B down_proj, 16 tiles, M = 32:
+  // group-wise 36 vs 79 us, tools/probes/i8g_smallm_probe.py; INT4 vs 38.6 us; up_proj, 43 tiles:
+  // not taken)
+  const int64_t gemv_max_m = (h->use_i8g || h->has_w4) && 3 * cdiv(h->N, 256) <= int64_t(sm_count()) / 2
+                                 ? SERQ_GEMV_I8G_MAX_M
+                                 : 16;
   if (M <= gemv_max_m && gemv_fmt_ok && h->r <= 128 && !SERQ_DBG(g_debug_flags, 1 << 29)) {
     // decode sizes: the weight stream with warp-level MMAs (serq_gemv_i8.cuh), int8 or packed INT4
     GemvI8Params gp{};

@@ -298,7 +298,7 @@ def test_int_decode_gemv_parity(D, M, r_mode, contiguous, bits, sym):
     assert np.array_equal(y1, y)
 
 
-@pytest.mark.parametrize("M", [1, 5, 16])
+@pytest.mark.parametrize("M", [1, 5, 16, 24])  # 24: two 16-token groups (few tiles: the gemv up to 32)
 @pytest.mark.parametrize("K,N", [(1536, 1000), (1552, 264), (11008, 520)])
 @pytest.mark.parametrize("r_mode,bits,sym", [("int", 8, False), ("dense", 4, True), ("none", 8, True)])
 def test_int_decode_gemv_w4_parity(D, M, K, N, r_mode, bits, sym):
